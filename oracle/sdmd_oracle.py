@@ -1,0 +1,327 @@
+"""ORACLE — test infrastructure, NOT part of the product.
+
+Plain, slow, obviously-correct fp64 CPU implementation of the streaming method-of-snapshots
+SVD / DMD / background-subtraction path of arXiv 1612.07875 (reference: /root/reference/
+PAPER.md, cited as P:<line>).  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this module.  It shares
+no code with the CUDA path (``paper_1612_07875_b200/``) and never imports it.
+
+Each function follows the paper's algorithm in the paper's order and notation; library
+primitives serve as single steps exactly where the paper itself calls a library routine
+(``X.T * X`` → numpy matmul/dot, ``eig`` → LAPACK via numpy.linalg, ``lstsq``).  Readings
+where the paper is ambiguous or garbled are the ones listed in DESIGN.md §"Readings"
+(SURVEY.md §8(c) Q1–Q24); each is cited as Qk where used.
+
+Pins (tests/test_oracle_*.py, ``-m "not gpu"``): closed-form planted spectra, worked examples
+from SPEC.md (cited), exact-rational brute force on tiny inputs, streamed == batch, Gram
+slice identities, invariance under orthonormal transforms, Eckart–Young, eigenvalue
+equivalence with the full operator X' pinv(X), LAPACK SVD of X on tiny inputs.
+
+Parity unpinned: eigenvalues of Ã for noisy video windows with r ≈ m have no closed form;
+they are checked only GPU-vs-oracle within κ(λ)·‖ΔÃ‖ (DESIGN.md §"Parity").
+"""
+from __future__ import annotations
+
+import numpy as np
+
+# ----------------------------------------------------------------------------------------
+# status codes (mirror of include/sdmd.h values, redefined here: no shared code)
+# ----------------------------------------------------------------------------------------
+OK, E_INVALID, E_NONFINITE, E_WINDOW_NOT_FULL, E_ZERO_MATRIX = 0, 1, 2, 3, 4
+E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE = 5, 6, 7
+
+
+class OracleError(Exception):
+    def __init__(self, code: int, msg: str = ""):
+        super().__init__(f"status {code}: {msg}")
+        self.code = code
+
+
+# ----------------------------------------------------------------------------------------
+# O1  Gram matrix  (Alg 1 first branch "xtx = X.T * X"; §3.1)
+# ----------------------------------------------------------------------------------------
+
+def gram(Z) -> np.ndarray:
+    """G = Zᵀ Z of the full window Z = [z_0 .. z_m] (n x (m+1)), fp64.
+
+    Alg 1 P:291 ("xtx = X.T * X") applied to the full window (reading Q2: the full-window
+    Gram holds both XᵀX = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1]).  fp32 inputs are promoted
+    exactly to fp64 before the products (Q9)."""
+    Zd = np.asarray(Z, dtype=np.float64)
+    return Zd.T @ Zd
+
+
+def gram_column(cols, x_new) -> np.ndarray:
+    """g_k = <z_k, x_new> for each window column z_k (x_new itself last gives the self-dot).
+
+    Alg 1 else-branch P:294 ("xtx[:, -1] = X.T * X[:, -1]"); §3.1 P:236 ("only the last row
+    or column will need to be recalculated").  One library dot per column."""
+    x = np.asarray(x_new, dtype=np.float64)
+    return np.array([float(np.dot(np.asarray(c, dtype=np.float64), x)) for c in cols])
+
+
+def sparse_gram_column(slots, x_new, n: int) -> np.ndarray:
+    """Sparse variant (§3.5): each snapshot is (idx, val) in an orthonormal
+    coefficient basis; g_k is the dot of the *scattered* dense vectors (definition)."""
+    def dense(sv):
+        idx, val = sv
+        d = np.zeros(n, dtype=np.float64)
+        d[np.asarray(idx, dtype=np.int64)] = np.asarray(val, dtype=np.float64)
+        return d
+    xd = dense(x_new)
+    return np.array([float(np.dot(dense(s), xd)) for s in slots])
+
+
+class StreamingGram:
+    """Sliding-window Gram state (Alg 1 else-branch P:293-295, on the full window, Q2).
+
+    Warm-up: while fewer than m+1 columns are held, push appends a column and extends G
+    (Q14).  Full: push drops the oldest column, keeps G[1:,1:] (copied,
+    not recomputed) and computes the new last row/column.  A frame whose
+    self-dot is not finite is rejected and the state is left unchanged."""
+
+    def __init__(self, m: int):
+        self.m = m
+        self.cols: list[np.ndarray] = []
+        self.G = np.zeros((0, 0))
+        self.fresh_dots = 0          # instrumentation: fresh length-n inner products
+
+    @property
+    def full(self) -> bool:
+        return len(self.cols) == self.m + 1
+
+    def push(self, x) -> None:
+        x = np.asarray(x, dtype=np.float64).copy()
+        if self.full:
+            keep = self.cols[1:]
+            Gk = self.G[1:, 1:]                       # "xtx[:-1, :-1] = xtx[1:, 1:]"
+        else:
+            keep = self.cols
+            Gk = self.G
+        g = gram_column(keep + [x], x)                 # "xtx[:, -1] = X.T * X[:, -1]"
+        if not np.isfinite(g[-1]) or not np.all(np.isfinite(g)):
+            raise OracleError(E_NONFINITE, "non-finite frame rejected; state unchanged")
+        self.fresh_dots += len(g)
+        k = len(keep)
+        G = np.zeros((k + 1, k + 1))
+        G[:k, :k] = Gk
+        G[:, k] = g
+        G[k, :] = g                                    # "xtx[-1, :] = xtx[:, -1].T"
+        self.cols = keep + [x]
+        self.G = G
+
+
+# ----------------------------------------------------------------------------------------
+# O3–O4  Method-of-snapshots SVD from the Gram  (§2.1; Alg 1)
+# ----------------------------------------------------------------------------------------
+
+def _sign_normalize_real(V: np.ndarray) -> np.ndarray:
+    """Q6: make each column's largest-|.| entry positive (first such entry on ties)."""
+    V = V.copy()
+    for j in range(V.shape[1]):
+        i = int(np.argmax(np.abs(V[:, j])))
+        if V[i, j] < 0:
+            V[:, j] = -V[:, j]
+    return V
+
+
+def svd_from_gram(S, rank_tol: float = 1e-7, r_max: int | None = None):
+    """σ, V, r of X from S = XᵀX.
+
+    "s, v = eig(xtx)" (Alg 1; eig of the symmetric Gram, LAPACK via numpy),
+    "sigma = sort(sqrt(abs(s)), 'desc')" with V permuted alike (Q6),
+    r = min(r_max, #{σ_i > rank_tol·σ_1}) (Q7).  Raises E_ZERO_MATRIX if σ_1 == 0."""
+    S = np.asarray(S, dtype=np.float64)
+    S = 0.5 * (S + S.T)
+    mu, V = np.linalg.eigh(S)
+    sigma = np.sqrt(np.abs(mu))
+    order = np.argsort(-sigma, kind="stable")
+    sigma = sigma[order]
+    V = _sign_normalize_real(V[:, order])
+    if sigma.size == 0 or sigma[0] == 0.0:
+        raise OracleError(E_ZERO_MATRIX, "sigma_1 == 0")
+    r = int(np.count_nonzero(sigma > rank_tol * sigma[0]))
+    if r_max is not None:
+        r = min(r, int(r_max))
+    return sigma, V, r
+
+
+def left_singular(X, sigma, V, r: int) -> np.ndarray:
+    """U = X V Σ⁻¹ (§2.1 Eq. P:95).  Tests only: the paper never forms U."""
+    return np.asarray(X, dtype=np.float64) @ (V[:, :r] / sigma[:r])
+
+
+# ----------------------------------------------------------------------------------------
+# O5–O6  Projected operator and its eigendecomposition  (Eq. Atilde; Alg 2)
+# ----------------------------------------------------------------------------------------
+
+def order_eigs(lam: np.ndarray) -> np.ndarray:
+    """Q12: |λ| descending, then Re descending, then Im descending (stable)."""
+    keys = [(-abs(l), -l.real, -l.imag, i) for i, l in enumerate(lam)]
+    return np.array([k[3] for k in sorted(keys)], dtype=np.int64)
+
+
+def normalize_eigvecs(W: np.ndarray) -> np.ndarray:
+    """Q12: unit 2-norm columns, largest-|.| entry made real positive."""
+    W = np.asarray(W, dtype=np.complex128).copy()
+    for j in range(W.shape[1]):
+        w = W[:, j]
+        w = w / np.linalg.norm(w)
+        i = int(np.argmax(np.abs(w)))
+        w = w * (np.conj(w[i]) / abs(w[i]))
+        W[:, j] = w
+    return W
+
+
+def dmd_from_gram(G, rank_tol: float = 1e-7, r_max: int | None = None) -> dict:
+    """Streaming DMD from the full-window Gram (Alg 2 P:308-316 with reading Q2).
+
+    sigma, v from SSVD of X = window[:, :-1] ("SSVD(X[:, :-1])") → S = G[0:m,0:m];
+    xty = XᵀX' = G[0:m,1:m+1] ("xty[:, :-1] = xtx[:, 1:]; xty[:, -1] = X[:, :-1].T*X[:, -1]",
+    P:310-311); vsi = v Σ⁻¹; atilde = vsiᵀ xty vsi; lambda, w = eig(atilde)
+    (P:314)."""
+    G = np.asarray(G, dtype=np.float64)
+    m = G.shape[0] - 1
+    S = G[:m, :m]
+    xty = G[:m, 1:m + 1]
+    sigma, V, r = svd_from_gram(S, rank_tol, r_max)
+    vsi = V[:, :r] / sigma[:r]
+    atilde = vsi.T @ xty @ vsi
+    lam, W = np.linalg.eig(atilde)
+    o = order_eigs(lam)
+    lam = lam[o]
+    W = normalize_eigvecs(W[:, o])
+    return dict(m=m, r=r, sigma=sigma, V=V, vsi=vsi, atilde=atilde, lam=lam, W=W, S=S,
+                xty=xty)
+
+
+# ----------------------------------------------------------------------------------------
+# O8–O10  Amplitudes and background mode  (§3.3; Alg 3)
+# ----------------------------------------------------------------------------------------
+
+def amplitudes(d: dict) -> tuple[np.ndarray, int]:
+    """b = (WΛ)⁻¹ α₁ with α₁ = POD coefficients of x₁ = σ ⊙ V[0, :r] (Q3).
+
+    "alpha1 = sigma * v[:, 0].T; wl = w * lambda; b = lstsq(wl, alpha1)" (Alg 3),
+    §3.3 P:268.  Returns (b, status): W_SINGULAR when WΛ is numerically singular, in which
+    case modes with |λ| < rank_tol·max|λ| get b = 0 and the rest are solved (Q15)."""
+    r = d["r"]
+    alpha1 = d["sigma"][:r] * d["V"][0, :r]
+    lam, W = d["lam"], d["W"]
+    wl = W * lam[None, :]
+    s = np.linalg.svd(wl, compute_uv=False)
+    if s[-1] > 1e-13 * s[0]:
+        return np.linalg.solve(wl, alpha1.astype(np.complex128)), OK
+    keep = np.abs(lam) >= 1e-7 * max(np.abs(lam).max(), 1e-300)
+    b = np.zeros(len(lam), dtype=np.complex128)
+    if keep.any():
+        b[keep] = np.linalg.lstsq(wl[:, keep], alpha1.astype(np.complex128), rcond=None)[0]
+    return b, W_SINGULAR
+
+
+def background_index(lam) -> int:
+    """idx = argmin_i |log λ_i| (Alg 3), principal branch, λ = 0 excluded (Q5).
+
+    Ties (conjugate pairs tie exactly): smaller |Im log λ|, then Im(λ) >= 0, then the lowest
+    index.  Raises E_NO_VIABLE_MODE when every λ is zero."""
+    best, bkey = -1, None
+    for i, l in enumerate(np.asarray(lam, dtype=np.complex128)):
+        if l == 0:
+            continue
+        lg = np.log(l)
+        key = (abs(lg), abs(lg.imag), 0 if l.imag >= 0 else 1, i)
+        if bkey is None or key < bkey:
+            best, bkey = i, key
+    if best < 0:
+        raise OracleError(E_NO_VIABLE_MODE, "all eigenvalues zero")
+    return best
+
+
+# ----------------------------------------------------------------------------------------
+# O7, O11–O12  Modes and background/foreground  (Eq. Phi; Alg 3)
+# ----------------------------------------------------------------------------------------
+
+def modes(Xp_cols, d: dict, which=None) -> np.ndarray:
+    """Φ = X' V Σ⁻¹ W = X' (vsi w)  ("vsiw = vsi * w; phi = X[:, 1:] * vsiw").
+
+    ``Xp_cols``: the m columns of X' (list of n-vectors); ``which``: mode indices (default
+    all).  Explicit accumulation over the m columns."""
+    vsiw = d["vsi"] @ d["W"]
+    cols = range(vsiw.shape[1]) if which is None else list(which)
+    n = len(Xp_cols[0])
+    Phi = np.zeros((n, len(cols)), dtype=np.complex128)
+    for k, xk in enumerate(Xp_cols):
+        xk = np.asarray(xk, dtype=np.float64)
+        Phi += np.outer(xk, vsiw[k, cols])
+    return Phi
+
+
+def background_newest(Xp_cols, x_newest, d: dict, b, idx: int, threshold: float = 0.2):
+    """Streaming branch of Alg 3 for the newest column:
+    l = b[idx] φ_idx λ_idx^e with e = m (Q4; b is fitted to the oldest column, λ⁰),
+    s = x − |l| (Q8: complex modulus), mask = s > threshold (strict)."""
+    m = d["m"]
+    phi = modes(Xp_cols, d, [idx])[:, 0]
+    l = b[idx] * phi * d["lam"][idx] ** m
+    low = np.abs(l)
+    s = np.asarray(x_newest, dtype=np.float64) - low
+    return low, s, s > threshold
+
+
+def background_first_window(Z_cols, d: dict, b, idx: int, threshold: float = 0.2):
+    """First-window branch of Alg 3: exponents 0..m over all m+1 window columns
+    (Q24).  Returns (|L|, S, mask) as (n, m+1) arrays."""
+    m = d["m"]
+    phi = modes(Z_cols[1:], d, [idx])[:, 0]
+    pw = d["lam"][idx] ** np.arange(m + 1)
+    L = np.abs(b[idx] * np.outer(phi, pw))
+    Z = np.stack([np.asarray(c, dtype=np.float64) for c in Z_cols], axis=1)
+    S = Z - L
+    return L, S, S > threshold
+
+
+# ----------------------------------------------------------------------------------------
+# Streaming engine (Fig. 3, §3.2): one push = a2..a11 of SURVEY §8(a)
+# ----------------------------------------------------------------------------------------
+
+class StreamingDMD:
+    """Oracle counterpart of the C-ABI ``sdmd_push_*`` + getters (one writer).
+
+    Each push slides the Gram (Alg 1), and once the window is full runs SDMD (Alg 2) and the
+    streaming branch of SBackSub (Alg 3) for the newest column."""
+
+    def __init__(self, m: int, rank_tol: float = 1e-7, r_max: int | None = None,
+                 threshold: float = 0.2, background: bool = True):
+        self.m, self.rank_tol, self.r_max = m, rank_tol, r_max
+        self.threshold, self.background = threshold, background
+        self.gram = StreamingGram(m)
+        self.frames = 0
+        self.last = None
+
+    def push(self, x) -> dict | None:
+        self.gram.push(x)
+        self.frames += 1
+        if not self.gram.full:
+            self.last = None
+            return None
+        G = self.gram.G
+        d = dmd_from_gram(G, self.rank_tol, self.r_max)
+        b, st = amplitudes(d)
+        idx = background_index(d["lam"])
+        out = dict(d, b=b, amp_status=st, idx=idx, G=G.copy(), frame=self.frames - 1)
+        if self.background:
+            cols = self.gram.cols
+            low, s, mask = background_newest(cols[1:], cols[-1], d, b, idx, self.threshold)
+            out.update(lowrank=low, sparse=s, mask=mask)
+        self.last = out
+        return out
+
+
+def dmd_window(Z, rank_tol: float = 1e-7, r_max: int | None = None) -> dict:
+    """Batch counterpart: everything from one window Z (n x (m+1)) recomputed from scratch
+    (the paper's non-streaming CPU/GPU variants)."""
+    G = gram(Z)
+    d = dmd_from_gram(G, rank_tol, r_max)
+    b, st = amplitudes(d)
+    idx = background_index(d["lam"])
+    return dict(d, b=b, amp_status=st, idx=idx, G=G)

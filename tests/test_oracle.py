@@ -1,0 +1,375 @@
+"""Pins of the oracle (oracle/sdmd_oracle.py) against things other than itself:
+closed forms, SPEC worked examples (tests/golden), exact rational arithmetic, invariants and
+independent library routines (LAPACK SVD of X, pinv) on tiny inputs.  CPU only."""
+import json
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle.sdmd_oracle as O
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                   "spec_worked_examples.json")))
+
+
+def normwise(Ga, Gb):
+    """Q17: max_ij |ΔG_ij| / sqrt(G_ii G_jj) (computed against Gb's diagonal)."""
+    d = np.sqrt(np.abs(np.diag(Gb)))
+    den = np.outer(d, d)
+    den[den == 0] = 1.0
+    return float(np.max(np.abs(Ga - Gb) / den))
+
+
+def match_eigs(a, b):
+    """Max |a_i - b_π(i)| under the optimal assignment (Hungarian; scipy)."""
+    from scipy.optimize import linear_sum_assignment
+    C = np.abs(np.asarray(a)[:, None] - np.asarray(b)[None, :])
+    r, c = linear_sum_assignment(C)
+    return float(C[r, c].max())
+
+
+# ---------------------------------------------------------------- Gram (O1) ----------
+
+@pytest.mark.parametrize("ex", GOLD["gram"], ids=lambda e: e["cite"][:20])
+def test_gram_worked_examples(ex):
+    Z = np.array(ex["Z_cols"], dtype=np.float64).T
+    assert np.array_equal(O.gram(Z), np.array(ex["G"], dtype=np.float64))
+
+
+@pytest.mark.parametrize("ex", GOLD["slide"], ids=lambda e: e["cite"][:20])
+def test_slide_worked_examples(ex):
+    sg = O.StreamingGram(ex["m"])
+    for x in ex["push"]:
+        sg.push(np.array(x, dtype=np.float64))
+    assert np.array_equal(sg.G, np.array(ex["G_final"], dtype=np.float64))
+
+
+def test_gram_exact_rational():
+    """fp64 Gram vs exact rational arithmetic on a small random window (brute force)."""
+    rng = np.random.default_rng(3)
+    Z = rng.standard_normal((40, 6))
+    G = O.gram(Z)
+    F = [[sum(Fraction(Z[k, i]) * Fraction(Z[k, j]) for k in range(Z.shape[0]))
+          for j in range(6)] for i in range(6)]
+    E = np.array([[float(v) for v in row] for row in F])
+    assert normwise(G, E) < 1e-15
+
+
+def test_gram_fp32_promotion_exact():
+    """fp32 inputs: products are exact in fp64 (Q9) — compare with exact rationals."""
+    rng = np.random.default_rng(4)
+    Z = rng.random((30, 4)).astype(np.float32)
+    G = O.gram(Z)
+    E = np.array([[float(sum(Fraction(float(Z[k, i])) * Fraction(float(Z[k, j]))
+                             for k in range(30))) for j in range(4)] for i in range(4)])
+    assert normwise(G, E) < 1e-15
+
+
+def test_streamed_equals_batch_c1():
+    """§3.1 reuse claim: streamed G == batch G of the final window, every slide;
+    and exactly m+1 fresh dots per slide."""
+    pm = synth.planted_c1()
+    m = 16
+    X = pm.frames(0, 81)
+    sg = O.StreamingGram(m)
+    for t in range(81):
+        before = sg.fresh_dots
+        sg.push(X[:, t])
+        if t >= m:
+            assert sg.fresh_dots - before == m + 1
+            Gb = O.gram(X[:, t - m:t + 1])
+            assert normwise(sg.G, Gb) < 1e-13
+
+
+def test_gram_slices_psd_symmetry():
+    rng = np.random.default_rng(5)
+    Z = rng.standard_normal((300, 9))
+    G = O.gram(Z)
+    m = 8
+    X, Xp = Z[:, :m], Z[:, 1:]
+    # slice identities (BJ north_star): G[0:m,0:m] = XᵀX, G[0:m,1:m+1] = XᵀX'
+    Sxx = np.array([[math.fsum(X[:, i] * X[:, j]) for j in range(m)] for i in range(m)])
+    Sxy = np.array([[math.fsum(X[:, i] * Xp[:, j]) for j in range(m)] for i in range(m)])
+    assert normwise(G[:m, :m], Sxx) < 1e-14
+    assert np.max(np.abs(G[:m, 1:] - Sxy)) < 1e-12 * np.max(np.abs(Sxy))
+    assert np.array_equal(G, G.T)
+    assert np.linalg.eigvalsh(G).min() > -1e-13 * np.trace(G)
+
+
+def test_nonfinite_rejected_state_unchanged():
+    sg = O.StreamingGram(3)
+    rng = np.random.default_rng(6)
+    for _ in range(5):
+        sg.push(rng.standard_normal(20))
+    G0, cols0 = sg.G.copy(), [c.copy() for c in sg.cols]
+    bad = rng.standard_normal(20)
+    bad[7] = np.nan
+    with pytest.raises(O.OracleError) as e:
+        sg.push(bad)
+    assert e.value.code == O.E_NONFINITE
+    assert np.array_equal(sg.G, G0) and all(np.array_equal(a, b) for a, b in zip(sg.cols, cols0))
+
+
+def test_sparse_gram_matches_dense():
+    st = synth.SparseDCTStream(N=64, k_low=8.0, n_shell=30, seed=11)
+    frames = [st.frame(t) for t in range(5)]
+    g = O.sparse_gram_column(frames, frames[-1], st.n)
+    D = np.stack([st.dense(t) for t in range(5)], axis=1)
+    ref = np.array([math.fsum(D[:, k] * D[:, 4]) for k in range(5)])
+    assert np.max(np.abs(g - ref)) <= 1e-15 * np.max(np.abs(ref))
+
+
+def test_gram_invariant_under_orthonormal_dct():
+    """Unitary invariance: Gram of orthonormal DCT-II coefficients == Gram of
+    the fields."""
+    from scipy.fft import dctn
+    rng = np.random.default_rng(8)
+    fields = rng.standard_normal((6, 16, 16))
+    Z = np.stack([f.ravel() for f in fields], axis=1)
+    C = np.stack([dctn(f, norm="ortho").ravel() for f in fields], axis=1)
+    assert normwise(O.gram(C), O.gram(Z)) < 1e-13
+
+
+# ------------------------------------------------------------- SVD (O3-O4) -----------
+
+@pytest.mark.parametrize("ex", GOLD["sym_eig"], ids=lambda e: e["cite"][:20])
+def test_svd_from_gram_worked(ex):
+    S = np.array(ex["S"], dtype=np.float64)
+    sigma, V, r = O.svd_from_gram(S)
+    assert np.allclose(sigma ** 2, ex["evals"], atol=1e-13)
+    if "r" in ex:
+        assert r == ex["r"]
+    if "evecs_abs" in ex:
+        assert np.allclose(np.abs(V), ex["evecs_abs"], atol=1e-14)
+
+
+def test_mos_sigma_vs_lapack_svd():
+    """MoS σ (eig of XᵀX) vs LAPACK SVD of X itself (acceptance 1): 20 random
+    1000x50 matrices."""
+    rng = np.random.default_rng(9)
+    for _ in range(20):
+        X = rng.standard_normal((1000, 50))
+        sigma, V, r = O.svd_from_gram(O.gram(X))
+        ref = np.linalg.svd(X, compute_uv=False)
+        assert r == 50
+        assert np.max(np.abs(sigma - ref) / ref) < 1e-12
+
+
+def test_constant_stream_sigma():
+    """the same column repeated m times -> sigma_1 = sqrt(m)·‖x‖, r = 1."""
+    rng = np.random.default_rng(10)
+    x = rng.random(500)
+    m = 12
+    sigma, V, r = O.svd_from_gram(O.gram(np.tile(x[:, None], (1, m))))
+    assert r == 1
+    assert abs(sigma[0] - math.sqrt(m) * np.linalg.norm(x)) < 1e-12 * sigma[0]
+
+
+def test_left_singular_and_eckart_young():
+    rng = np.random.default_rng(12)
+    X = rng.standard_normal((400, 10)) @ np.diag(np.logspace(0, -3, 10))
+    sigma, V, r = O.svd_from_gram(O.gram(X))
+    U = O.left_singular(X, sigma, V, r)
+    assert np.max(np.abs(U.T @ U - np.eye(r))) < 1e-8
+    assert np.linalg.norm(X - U * sigma[:r] @ V[:, :r].T) < 1e-10 * np.linalg.norm(X)
+    for k in (1, 4, 7):
+        err = np.linalg.norm(X - (U[:, :k] * sigma[:k]) @ V[:, :k].T)
+        assert abs(err - math.sqrt(np.sum(sigma[k:] ** 2))) < 1e-8 * np.linalg.norm(X)
+
+
+def test_zero_window():
+    with pytest.raises(O.OracleError) as e:
+        O.svd_from_gram(np.zeros((4, 4)))
+    assert e.value.code == O.E_ZERO_MATRIX
+
+
+# ---------------------------------------------------------- DMD (O5-O9) --------------
+
+@pytest.mark.parametrize("ex", GOLD["eig"], ids=lambda e: e["cite"][:20])
+def test_eig_worked(ex):
+    A = np.array(ex["A"])
+    lam = np.linalg.eig(A)[0]
+    assert match_eigs(lam, np.array(ex["lam_re"]) + 1j * np.array(ex["lam_im"])) < 1e-14
+
+
+def test_c1_closed_form_lambda_every_window():
+    """BJ north_star: planted x_t = Σ b_j φ_j λ_j^t must recover λ_j to 1e-10 — all 64
+    streamed windows of C1 (plus the b_j φ_j products and Φb = x_1)."""
+    pm = synth.planted_c1()
+    m = 16
+    X = pm.frames(0, 81)
+    eng = O.StreamingDMD(m, background=False)
+    nwin = 0
+    for t in range(81):
+        out = eng.push(X[:, t])
+        if out is None:
+            continue
+        nwin += 1
+        assert out["r"] == 4
+        assert match_eigs(out["lam"], pm.lambdas) < 1e-10
+        # amplitudes: Φ b reproduces the oldest column x_{t-m}
+        cols = eng.gram.cols
+        Phi = O.modes(cols[1:], out)
+        x1 = cols[0]
+        assert np.linalg.norm(Phi @ out["b"] - x1) < 1e-10 * np.linalg.norm(x1)
+        # scale-free products b_j φ_j == planted b_j λ_j^{t0} φ_j
+        planted = pm.mode_products(t - m)
+        for j, lam in enumerate(out["lam"]):
+            key = min(planted, key=lambda k: abs(k - lam))
+            ref = planted[key]
+            assert np.linalg.norm(out["b"][j] * Phi[:, j] - ref) < 1e-9 * np.linalg.norm(ref)
+    assert nwin == 65          # initial window + 64 streamed frames
+
+
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_spec_planted_spectra(which):
+    """SPEC acceptance 3: {0.9,0.5}, {e^{±iπ/8}}, {1, 0.7e^{±0.3i}} at n=64, w=12."""
+    pm = synth.planted_spec(which)
+    Z = pm.frames(0, 12)
+    out = O.dmd_window(Z)
+    assert out["r"] == pm.rank
+    assert match_eigs(out["lam"], pm.lambdas) < 1e-8
+
+
+def test_eigs_equal_full_operator():
+    """§2.2: Ã has the same (nonzero) eigenvalues as A = X' pinv(X)."""
+    rng = np.random.default_rng(13)
+    for _ in range(10):
+        n, w, k = 25, 9, 5
+        Z = rng.standard_normal((n, k)) @ rng.standard_normal((k, w))
+        out = O.dmd_window(Z)
+        X, Xp = Z[:, :-1], Z[:, 1:]
+        A = Xp @ np.linalg.pinv(X)
+        ev = np.linalg.eigvals(A)
+        ev = ev[np.argsort(-np.abs(ev))][:out["r"]]
+        assert match_eigs(out["lam"], ev) < 1e-8
+
+
+def test_amplitudes_equal_least_squares():
+    """§3.3: b = (WΛ)⁻¹α₁ equals the high-dimensional b = Φ†x₁ when x₁ is in the
+    POD span (exact low-rank data)."""
+    pm = synth.planted_spec(2, n=200)
+    Z = pm.frames(0, 12)
+    out = O.dmd_window(Z)
+    Phi = O.modes([Z[:, k] for k in range(1, 12)], out)
+    b_ls = np.linalg.pinv(Phi) @ Z[:, 0]
+    assert np.linalg.norm(out["b"] - b_ls) < 1e-8 * np.linalg.norm(b_ls)
+
+
+def test_modes_are_eigvecs_of_A():
+    """A Φ_i = λ_i Φ_i with A v = X'(pinv(X) v) on exactly low-rank data."""
+    pm = synth.planted_spec(1, n=100)
+    Z = pm.frames(0, 12)
+    out = O.dmd_window(Z)
+    X, Xp = Z[:, :-1], Z[:, 1:]
+    Phi = O.modes([Z[:, k] for k in range(1, 12)], out)
+    AP = Xp @ (np.linalg.pinv(X) @ Phi)
+    assert np.linalg.norm(AP - Phi * out["lam"][None, :]) < 1e-8 * np.linalg.norm(Phi)
+
+
+def test_alpha1_first_row_reading_Q3():
+    """Q3: α₁ = σ ⊙ V[0,:] reproduces x₁ (residual ~1e-15); the column reading does not."""
+    pm = synth.planted_c1()
+    Z = pm.frames(0, 17)
+    out = O.dmd_window(Z)
+    Phi = O.modes([Z[:, k] for k in range(1, 17)], out)
+    assert np.linalg.norm(Phi @ out["b"] - Z[:, 0]) < 1e-12 * np.linalg.norm(Z[:, 0])
+    r = out["r"]
+    alt = out["sigma"][:r] * out["V"][:r, 0]
+    wl = out["W"] * out["lam"][None, :]
+    b_alt = np.linalg.solve(wl, alt.astype(complex))
+    assert np.linalg.norm(Phi @ b_alt - Z[:, 0]) > 1e-3 * np.linalg.norm(Z[:, 0])
+
+
+# --------------------------------------------------- background (O10-O12) ------------
+
+@pytest.mark.parametrize("ex", GOLD["background_index"], ids=lambda e: e["cite"][:20])
+def test_background_index_worked(ex):
+    lam = np.array(ex["lam_re"]) + 1j * np.array(ex["lam_im"])
+    assert O.background_index(lam) == ex["idx"]
+
+
+def test_background_index_conjugate_tie_and_none():
+    lam = np.array([0.5, 0.99 * np.exp(-0.01j), 0.99 * np.exp(0.01j)])
+    assert O.background_index(lam) == 2          # tie -> Im >= 0
+    with pytest.raises(O.OracleError):
+        O.background_index(np.zeros(3, dtype=complex))
+
+
+def test_exponent_reading_Q4_newest_column():
+    """Q4: with b fitted to the oldest column, λ^m reproduces the newest column x_t
+    (planted C1b with a λ=1 mode); λ^{m+1} does not."""
+    pm = synth.planted_c1(with_unit_mode=True)
+    m = 16
+    Z = pm.frames(0, m + 1)
+    out = O.dmd_window(Z)
+    Phi = O.modes([Z[:, k] for k in range(1, m + 1)], out)
+    rec_m = Phi @ (out["b"] * out["lam"] ** m)
+    rec_m1 = Phi @ (out["b"] * out["lam"] ** (m + 1))
+    nz = np.linalg.norm(Z[:, m])
+    assert np.linalg.norm(rec_m - Z[:, m]) < 1e-10 * nz
+    assert np.linalg.norm(rec_m1 - Z[:, m]) > 1e-2 * nz
+    assert abs(out["lam"][out["idx"]] - 1.0) < 1e-10
+
+
+def test_constant_video_fixed_point():
+    """constant stream → λ_idx = 1, |L| = c, s ≈ 0."""
+    vs = synth.VideoStream(24, 32, 1, seed=3, n_squares=0, noise_sigma=0.0)
+    c = vs.frame(0).numpy().astype(np.float64)
+    m = 10
+    eng = O.StreamingDMD(m)
+    for _ in range(m + 3):
+        out = eng.push(c)
+    assert abs(out["lam"][out["idx"]] - 1.0) < 1e-9
+    assert np.max(np.abs(out["sparse"])) < 1e-6
+    assert np.max(np.abs(out["lowrank"] - c)) < 1e-8 * np.max(c)
+
+
+def test_background_additivity_and_monotone_threshold():
+    vs = synth.VideoStream(36, 48, 1, seed=5, side=8)
+    m = 12
+    eng = O.StreamingDMD(m)
+    for t in range(m + 4):
+        out = eng.push(vs.frame(t).numpy())
+    x = eng.gram.cols[-1]
+    assert np.max(np.abs(out["lowrank"] + out["sparse"] - x)) <= 4e-16 * 4
+    d = {k: out[k] for k in ("m", "lam", "vsi", "W")}
+    masks = [O.background_newest(eng.gram.cols[1:], x, d, out["b"], out["idx"], th)[2]
+             for th in (0.1, 0.2, 0.3)]
+    assert np.all(masks[1] <= masks[0]) and np.all(masks[2] <= masks[1])
+
+
+def test_moving_blob_foreground_sanity():
+    """S:363 / SURVEY §8(c): synthetic moving squares → per-frame F-measure sanity bar
+    (not parity).  Small C3-like stream, m=20."""
+    vs = synth.VideoStream(48, 64, 1, seed=21, side=8, n_squares=2)
+    m = 20
+    eng = O.StreamingDMD(m)
+    fs = []
+    for t in range(m + 15):
+        out = eng.push(vs.frame(t).numpy())
+        if out is None:
+            continue
+        gt = vs.truth_mask(t)
+        pred = out["mask"]
+        tp = np.sum(pred & gt)
+        p = tp / max(1, pred.sum())
+        rc = tp / max(1, gt.sum())
+        fs.append(0 if tp == 0 else 2 * p * rc / (p + rc))
+    assert np.mean(fs) > 0.85
+
+
+def test_c2_wake_rank_and_lambda():
+    """C2 (BJ config 2): r = 21 and λ = {1, e^{±ikω}} (ω = 2π/30, k=1..10) to 1e-10."""
+    pm = synth.cylinder_wake()
+    m = 150
+    Z = pm.frames(0, m + 1)
+    out = O.dmd_window(Z)
+    assert out["r"] == 21
+    ref = [1.0] + [np.exp(s * 1j * k * 2 * np.pi / 30) for k in range(1, 11) for s in (1, -1)]
+    assert match_eigs(out["lam"], np.array(ref)) < 1e-10
+    assert abs(out["lam"][out["idx"]] - 1.0) < 1e-10
