@@ -1,0 +1,209 @@
+/*
+ * sdmd.h — C ABI of the B200-native streaming method-of-snapshots SVD / DMD library
+ *          (hot path of arXiv 1612.07875, "streaming DMD"; PAPER.md cited as P:<line>).
+ *
+ * One context (sdmd_ctx) owns a sliding window of tall-skinny snapshots x_t (n rows each) in an
+ * HBM ring buffer, the window's Gram matrix G = Zᵀ Z (Z = [x_{t-m} … x_t], n x (m+1)), and the
+ * small on-device eigenproblems that turn G into the DMD of the window:
+ *
+ *   push x_t  →  g_k = <x_{t-m+k}, x_t>, k = 0..m           (§3.1; Alg 1)
+ *             →  [allreduce of g over row shards]             (row sharding; no paper analogue)
+ *             →  commit: G ← slide(G) with g as last row/col  (Alg 1)
+ *             →  S = XᵀX = G[0:m,0:m]:   S V = V Λ,  Σ = sqrt|Λ| sorted desc   (§2.1; Alg 1)
+ *             →  Ã = (VΣ⁻¹)ᵀ XᵀX' (VΣ⁻¹),  XᵀX' = G[0:m,1:m+1]                 (Eq. Atilde; Alg 2)
+ *             →  Ã W = W Λ                                                     (Alg 2)
+ *             →  α₁ = Σ V[0,:]ᵀ,  b = (WΛ)⁻¹ α₁  (only b_idx per frame)          (§3.3; Alg 3)
+ *             →  idx = argmin |log λ_i|                                         (Alg 3)
+ *             →  l = b_idx φ_idx λ_idx^m,  s = x − |l|,  mask = s > threshold   (Alg 3)
+ *
+ * Everything after sdmd_create runs on the GPU (sm_100a).  There is no CPU fallback: every
+ * entry point returns SDMD_E_CUDA if the device work cannot be launched.
+ *
+ * Conventions
+ *  - Every function returns an int status (enum below); 0 = SDMD_OK.  No exceptions, no abort,
+ *    no exit cross the ABI.  Argument/shape errors are returned before anything is enqueued.
+ *  - Matrices are column-major unless stated.  Complex numbers are interleaved (re, im) doubles.
+ *  - `where` says where a caller buffer lives: SDMD_HOST (pageable or pinned host memory) or
+ *    SDMD_DEVICE (device pointer on the ctx's device).
+ *  - Stream semantics: all device work of a ctx is ordered on the ctx stream (cfg.stream, or a
+ *    stream the ctx creates) plus internal eigen-worker streams joined back to it.  DEVICE
+ *    inputs must stay valid and unmodified until the ctx stream passes the push (e.g. until
+ *    sdmd_sync).  HOST inputs are read in stream order as well (pinned memory: asynchronously;
+ *    pageable memory: copied before the call returns).  Calls that return HOST outputs
+ *    synchronise the ctx first.
+ *  - Device-detected errors (non-finite frame) are recorded in a device status word; the frame
+ *    is rejected ON THE DEVICE (state bit-identical) and every frame pushed after it is
+ *    discarded until the next sdmd_sync(), which returns the error and the rejected frame index.
+ *  - One writer per ctx.  With nranks > 1, sdmd_init_window and sdmd_push_* are collective:
+ *    every rank calls them in the same order (NCCL semantics).
+ */
+#ifndef SDMD_H
+#define SDMD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SDMD_ABI_VERSION 1
+#define SDMD_MAX_M 256   /* largest window width m supported                              */
+#define SDMD_MAX_R 224   /* largest rank r (shared-memory Hessenberg QR)    */
+
+enum sdmd_status {
+  SDMD_OK = 0,
+  SDMD_E_INVALID = 1,          /* bad argument, shape or config          */
+  SDMD_E_NONFINITE = 2,        /* a pushed frame had a non-finite self inner product  */
+  SDMD_E_WINDOW_NOT_FULL = 3,  /* fewer than m+1 frames pushed yet (warm-up, Q14)             */
+  SDMD_E_ZERO_MATRIX = 4,      /* σ₁ == 0 (all-zero window) or r == 0                 */
+  SDMD_E_NO_CONVERGENCE = 5,   /* an on-device eigensolver exceeded its sweep budget   */
+  SDMD_W_SINGULAR = 6,         /* WΛ numerically singular; amplitudes of zero modes set to 0 */
+  SDMD_E_NO_VIABLE_MODE = 7,   /* every DMD eigenvalue is zero: no background mode    */
+  SDMD_E_CUDA = 8,             /* CUDA runtime error (details in sdmd_last_error)             */
+  SDMD_E_NCCL = 9,             /* NCCL error or NCCL unavailable for nranks > 1               */
+  SDMD_E_OOM = 10,             /* device allocation failed                                    */
+  SDMD_E_STATE = 11            /* call not valid in the current state (e.g. no DMD computed)  */
+};
+
+enum sdmd_dtype { SDMD_F32 = 0, SDMD_F64 = 1 };
+enum sdmd_storage { SDMD_DENSE = 0, SDMD_SPARSE = 1 };
+enum sdmd_where { SDMD_HOST = 0, SDMD_DEVICE = 1, SDMD_HOST_ASYNC = 2 /* pinned host, stream-ordered */ };
+
+typedef struct sdmd_ctx sdmd_ctx; /* opaque; owns ALL device state (ring, G history, factors) */
+
+typedef struct sdmd_config {
+  /* rows: this rank holds rows [row_begin, row_begin + n_local) of n_global (dense), or the
+   * coefficient indices in that range (sparse).  Single GPU: row_begin = 0, n_local = n_global. */
+  int64_t n_global;
+  int64_t row_begin;
+  int64_t n_local;
+  int32_t m;          /* width of X; the window holds m+1 snapshots. 2 <= m <= SDMD_MAX_M */
+  int32_t dtype;      /* dense storage dtype SDMD_F32 | SDMD_F64 (sparse values are always f64) */
+  int32_t storage;    /* SDMD_DENSE | SDMD_SPARSE (orthonormal-DCT coefficient snapshots, §3.5) */
+  int32_t nnz_cap;    /* sparse: max nonzeros per snapshot held by this rank                   */
+  int32_t r_max;      /* rank cap; 0 → min(m, SDMD_MAX_R)                                      */
+  double rank_tol;    /* r = min(r_max, #{σ_i > rank_tol·σ₁}); 0 → 1e-7 (reading Q7)         */
+  float threshold;    /* foreground threshold on s = x − |l| (".2"), strict '>'          */
+  int32_t background; /* 1: compute the newest background column every push (fused into the Gram
+                       * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
+  int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
+  int32_t workers;    /* concurrent eigen-worker streams (0 → 4); lag = workers + 1           */
+  int32_t device;     /* CUDA device ordinal                                                   */
+  void* stream;       /* cudaStream_t to order work on, or NULL (the ctx creates one)          */
+  int32_t rank;       /* this rank, 0..nranks-1                                                 */
+  int32_t nranks;     /* row shards; > 1 needs NCCL (uid from sdmd_nccl_unique_id on rank 0)   */
+  const uint8_t* nccl_uid; /* 128 bytes, identical on all ranks; ignored when nranks == 1       */
+} sdmd_config;
+
+typedef struct sdmd_info {
+  int64_t frames;       /* frames accepted so far (exact after sdmd_sync)                        */
+  int32_t window;       /* columns currently held (<= m+1)                                       */
+  int32_t lag;          /* background of frame t is produced by the push of frame t + lag        */
+  int32_t ring_slots;   /* HBM ring slots                                                        */
+  int32_t workers;      /* eigen-worker streams                                                  */
+  int64_t ring_bytes;   /* device bytes of the ring                                              */
+  int64_t ld;           /* ring slot stride in elements                                          */
+} sdmd_info;
+
+typedef struct sdmd_stats {
+  int64_t k1_launches;  /* Gram-update (K1/K3) launches timed since the last reset               */
+  double k1_ms;         /* their summed device time (CUDA events on the ctx stream)             */
+  int64_t k4_launches;  /* per-frame eigen (K4) launches                                         */
+  double k4_ms;         /* summed device time of K4 (events on the worker streams)               */
+  int64_t gpu_launches; /* all kernels this ctx launched since the last reset                   */
+} sdmd_stats;
+
+/* Fill *cfg with defaults (rank_tol 1e-7, threshold 0.2, dmd 1, background 0, workers 4, …).
+ * n_global/n_local/m must still be set by the caller. */
+int sdmd_config_init(sdmd_config* cfg);
+
+/* Create a context: allocates the ring (ring_slots x ld elements of dtype), the Gram history, the
+ * eigen-worker workspaces and, for nranks > 1, the NCCL communicator.  *out owned by the caller,
+ * released with sdmd_destroy.  Errors: E_INVALID (shape), E_OOM, E_CUDA, E_NCCL. */
+int sdmd_create(const sdmd_config* cfg, sdmd_ctx** out);
+int sdmd_destroy(sdmd_ctx* ctx);
+
+/* First window in one call (Alg 1 first branch "xtx = X.T * X"): Z is n_local x (m+1),
+ * column-major with leading dimension ldz >= n_local, oldest column first, dtype = cfg.dtype.
+ * The batch Gram runs on the fp64 tensor pipe (DMMA, kernel K2); the DMD of the window is then
+ * computed if cfg.dmd.  Replaces any previous state.  Dense storage only. */
+int sdmd_init_window(sdmd_ctx* ctx, const void* Z, int64_t ldz, int where);
+
+/* Push one dense snapshot (n_local values of cfg.dtype).  While fewer than m+1 frames are held
+ * the column is appended (warm-up, Q14); afterwards the oldest column is dropped (§3.1).  Work is
+ * enqueued asynchronously; see the header notes for the NONFINITE contract. */
+int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
+
+/* Push one sparse snapshot in an orthonormal coefficient basis (§3.5): nnz pairs,
+ * idx strictly ascending in [row_begin, row_begin + n_local) (int32), val fp64.  nnz <= nnz_cap.
+ * The Gram column uses sparse–sparse inner products; nothing is densified in HBM. */
+int sdmd_push_sparse(sdmd_ctx* ctx, int32_t nnz, const int32_t* idx, const double* val,
+                     int where);
+
+/* Zero-copy ingest: *dev_ptr receives the device address of the slot the next dense frame will
+ * occupy (n_local values); fill it (on the ctx stream or before), then sdmd_commit_slot. */
+int sdmd_acquire_slot(sdmd_ctx* ctx, void** dev_ptr);
+int sdmd_commit_slot(sdmd_ctx* ctx);
+
+/* Order the ctx stream after every eigen-worker launch enqueued so far (device-side join; the
+ * host does not wait).  Work enqueued on the ctx stream afterwards — e.g. a CUDA event that ends a
+ * timed region — follows the DMD of every pushed frame. */
+int sdmd_join(sdmd_ctx* ctx);
+
+/* Wait for all queued work.  Returns the first deferred device error (SDMD_E_NONFINITE) since the
+ * previous sync and, if failed_frame != NULL, the index of the rejected frame (-1 if none). */
+int sdmd_sync(sdmd_ctx* ctx, int64_t* failed_frame);
+
+int sdmd_get_info(sdmd_ctx* ctx, sdmd_info* info);
+
+/* Gram of the current window in logical (oldest-first) order: k x k doubles where k = columns
+ * held (<= m+1), written to host memory G (column-major, ld k).  *k_out receives k. */
+int sdmd_get_gram(sdmd_ctx* ctx, double* G, int32_t* k_out);
+
+/* This rank's pre-allreduce Gram column of the last push (k doubles, oldest first). */
+int sdmd_get_partial_gram_column(sdmd_ctx* ctx, double* g, int32_t* k_out);
+
+/* Method-of-snapshots SVD of X = window[:, 0:m] of the newest DMD frame (Alg 1): sigma gets m
+ * values (descending, sqrt|eig|), V gets m x r (column-major, ld m) or is NULL.  *frame gets the
+ * frame index.  Returns E_WINDOW_NOT_FULL during warm-up, or the frame's own status. */
+int sdmd_get_svd(sdmd_ctx* ctx, int32_t* r, double* sigma, double* V, int64_t* frame);
+
+/* DMD spectrum of the newest DMD frame: r eigenvalues of Ã (interleaved complex, ordered by |λ|
+ * desc, Re desc, Im desc), background index idx (into that order), and, if b != NULL, all r
+ * amplitudes b = (WΛ)⁻¹α₁ (computed on demand from left/right eigenvectors).  lambda needs 2r
+ * doubles (pass SDMD_MAX_R-sized buffers). */
+int sdmd_get_spectrum(sdmd_ctx* ctx, int32_t* r, double* lambda, double* b, int32_t* idx,
+                      int64_t* frame);
+
+/* Right eigenvectors W of Ã for the newest DMD frame (r x r complex, column-major, unit-norm,
+ * largest entry real positive), host memory. */
+int sdmd_get_eigvecs(sdmd_ctx* ctx, double* W, int32_t* r);
+
+/* DMD modes of the newest DMD frame, this rank's rows: Φ[:, cols] = X' V Σ⁻¹ W[:, cols]
+ * (Eq. Phi), computed on demand on the fp64 tensor pipe (K2).  phi_dev: device buffer,
+ * n_local x ncols complex (interleaved), column-major with leading dimension ld >= n_local. */
+int sdmd_get_modes(sdmd_ctx* ctx, const int32_t* cols, int32_t ncols, double* phi_dev, int64_t ld);
+
+/* Newest background column produced (frame index in *frame, -1 if none yet): lowrank = |l|,
+ * sparse = x − |l| (cfg.dtype, n_local values each; either may be NULL) and mask (uint8, 1 where
+ * sparse > threshold; may be NULL).  where = SDMD_HOST (synchronises) or SDMD_DEVICE (copies on
+ * the ctx stream) or SDMD_HOST_ASYNC (pinned host buffers, copied in stream order without
+ * synchronising; valid once the ctx stream has passed the call, e.g. after sdmd_sync). */
+int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
+                        int where);
+
+/* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */
+int sdmd_set_timing(sdmd_ctx* ctx, int enable);
+int sdmd_get_stats(sdmd_ctx* ctx, sdmd_stats* stats, int reset);
+
+/* NCCL bootstrap: rank 0 calls this and broadcasts the 128 bytes (e.g. torch.distributed). */
+int sdmd_nccl_unique_id(uint8_t out[128]);
+
+const char* sdmd_status_string(int status);
+const char* sdmd_last_error(const sdmd_ctx* ctx);
+int sdmd_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SDMD_H */

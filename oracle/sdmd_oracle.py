@@ -298,12 +298,30 @@ class StreamingDMD:
         self.frames = 0
         self.last = None
 
+    def init_window(self, Z) -> dict | None:
+        """First step (Alg 1 first branch "xtx = X.T * X"): the whole window at once.
+        Z: n x (m+1) array (or a list of m+1 columns), oldest first."""
+        cols = [np.asarray(c, dtype=np.float64) for c in
+                (Z if isinstance(Z, (list, tuple)) else np.asarray(Z).T)]
+        if len(cols) != self.m + 1:
+            raise OracleError(E_INVALID, "init_window needs m+1 columns")
+        G = gram(np.stack(cols, axis=1))
+        if not np.all(np.isfinite(G)):
+            raise OracleError(E_NONFINITE, "non-finite window")
+        self.gram.cols = cols
+        self.gram.G = G
+        self.frames = self.m + 1
+        return self._dmd()
+
     def push(self, x) -> dict | None:
         self.gram.push(x)
         self.frames += 1
         if not self.gram.full:
             self.last = None
             return None
+        return self._dmd()
+
+    def _dmd(self) -> dict:
         G = self.gram.G
         d = dmd_from_gram(G, self.rank_tol, self.r_max)
         b, st = amplitudes(d)

@@ -1,0 +1,241 @@
+// k1_gram.cu — K1: streaming Gram column over the HBM ring (+ fused background column).
+//
+// Computes g_k = <x_{t-m+k}, x_t> for the nd newest window columns (§3.1: "only the
+// last row or column will need to be recalculated"; Alg 1) in ONE pass over the ring, with
+// fp64 accumulation of exact fp32/fp64 products (reading Q9).  When a background coefficient
+// vector c_{t'} of an earlier frame t' = t - lag is ready, the same pass also forms
+// l = X'_{t'} c_{t'} = b_idx φ_idx λ_idx^m (Alg 3, reading Q4) and s = x_{t'} - |l|,
+// mask = s > threshold: the columns of X'_{t'} are streamed anyway, so the
+// background costs no extra HBM reads beyond lag-1 columns.
+//
+// Work split: persistent grid (one 256-thread CTA per SM); a CTA walks 256-row super-tiles;
+// warp w owns union columns j ≡ w (mod 8); each lane holds 8 rows of the new frame x_t (fp64)
+// and streams 16-byte vectors of its columns (evict-first: the ring is ≫ L2).  Per-column partial
+// dots are warp-reduced per tile into shared memory (deterministic order), written per CTA, and
+// the last CTA to finish reduces the CTA partials in fixed order and commits the column into the
+// Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
+#include "sdmd_internal.cuh"
+
+namespace sdmd {
+
+constexpr int K1_THREADS = 256;
+constexpr int K1_WARPS = K1_THREADS / 32;
+constexpr int K1_MAXU = kMaxM + kMaxWorkers + 8;   // union columns: m + lag (lag <= workers+1)
+constexpr int PSTRIDE = kMaxM + 16;                // partials row stride (doubles)
+
+template <typename T> struct VecOf;
+template <> struct VecOf<float> { using type = float4; static constexpr int E = 4; };
+template <> struct VecOf<double> { using type = double2; static constexpr int E = 2; };
+
+__device__ __forceinline__ void to_double(const float4& v, double* d) {
+  d[0] = (double)v.x; d[1] = (double)v.y; d[2] = (double)v.z; d[3] = (double)v.w;
+}
+__device__ __forceinline__ void to_double(const double2& v, double* d) { d[0] = v.x; d[1] = v.y; }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T, bool BG>
+// (K1_THREADS, 2): <= 128 registers so an eigen-worker CTA (K4) can co-reside on the SM
+__global__ void __launch_bounds__(K1_THREADS, 2) k1_gram_kernel(const K1Params p) {
+  using VT = typename VecOf<T>::type;
+  constexpr int EPV = VecOf<T>::E;          // elements per 16-byte vector
+  constexpr int VPL = 8 / EPV;              // vectors per lane per column (8 rows per lane)
+  constexpr int CB = sizeof(T) == 4 ? 4 : 2;  // columns in flight per batch
+  __shared__ double acc_s[K1_MAXU];
+  __shared__ double2 c_s[BG ? kMaxM : 1];
+  __shared__ double2 red[BG ? K1_WARPS * kSuperTile : 1];
+  __shared__ int am_last;
+
+  if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long f_dot0 = p.f_new - p.nd + 1;
+  const long long f_bg0 = p.f_bg - p.m + 1;         // first column of X'_{f_bg}
+  const long long F0 = BG ? (f_dot0 < f_bg0 ? f_dot0 : f_bg0) : f_dot0;
+  const int U = (int)(p.f_new - F0 + 1);
+  for (int j = tid; j < U; j += K1_THREADS) acc_s[j] = 0.0;
+  if (BG)
+    for (int k = tid; k < p.m; k += K1_THREADS) c_s[k] = p.cbg[k];
+  __syncthreads();
+
+  const int cnt = (U > warp) ? (U - warp + K1_WARPS - 1) / K1_WARPS : 0;
+  const T* __restrict__ ring = (const T*)p.ring;
+  const long long NT = p.ld / kSuperTile;
+  const T* xslot = ring + (p.f_new % p.NS) * p.ld;
+
+  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x) {
+    const long long row0 = tile * kSuperTile;
+    double xd[8];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
+      to_double(xv, xd + v * EPV);
+    }
+    double bre[8], bim[8];
+    if (BG) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { bre[e] = 0.0; bim[e] = 0.0; }
+    }
+    for (int q0 = 0; q0 < cnt; q0 += CB) {
+      VT z[CB][VPL];
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int q = q0 + b;
+        if (q < cnt) {
+          const long long f = F0 + warp + K1_WARPS * q;
+          const VT* zp = reinterpret_cast<const VT*>(ring + (f % p.NS) * p.ld + row0);
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int q = q0 + b;
+        if (q < cnt) {
+          const int j = warp + K1_WARPS * q;
+          const long long f = F0 + j;
+          double zd[8];
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
+          if (f >= f_dot0) {
+            double s = 0.0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s = fma(xd[e], zd[e], s);
+            s = warp_sum(s);
+            if (lane == 0) acc_s[j] += s;
+          }
+          if (BG) {
+            const long long kb = f - f_bg0;
+            if (kb >= 0 && kb < p.m) {
+              const double2 c = c_s[kb];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                bre[e] = fma(c.x, zd[e], bre[e]);
+                bim[e] = fma(c.y, zd[e], bim[e]);
+              }
+            }
+          }
+        }
+      }
+    }
+    if (BG) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int rt = (e / EPV) * (32 * EPV) + lane * EPV + (e % EPV);
+        red[warp * kSuperTile + rt] = make_double2(bre[e], bim[e]);
+      }
+      __syncthreads();
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int w = 0; w < K1_WARPS; ++w) {
+        const double2 v = red[w * kSuperTile + tid];
+        s.x += v.x; s.y += v.y;
+      }
+      const long long row = row0 + tid;
+      if (row < p.n) {
+        const double l = hypot(s.x, s.y);                       // |l| (Q8)
+        const double xv = (double)ring[(p.f_bg % p.NS) * p.ld + row];
+        const double sp = xv - l;                               // s = x - |l|
+        ((T*)p.lowrank)[row] = (T)l;
+        ((T*)p.sparse)[row] = (T)sp;
+        p.mask[row] = (sp > (double)p.thr) ? 1 : 0;             // strict '>'
+      }
+      __syncthreads();
+    }
+  }
+
+  __syncthreads();
+  for (int j = tid; j < U; j += K1_THREADS) {
+    const long long f = F0 + j;
+    if (f >= f_dot0) p.partials[(long long)blockIdx.x * PSTRIDE + (f - f_dot0)] = acc_s[j];
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(&p.st->k1_done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int k = tid; k < p.nd; k += K1_THREADS) {
+    double s = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(&p.partials[(long long)b * PSTRIDE + k]);
+    p.gout[k] = s;
+  }
+  if (tid == 0) {
+    p.st->k1_done = 0;
+    if (BG) p.st->bg_frame = p.f_bg;
+  }
+  if (p.do_commit) {
+    __syncthreads();
+    commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
+  }
+}
+
+__global__ void commit_kernel(const K1Params p) {
+  if (*(volatile int*)&p.st->status != 0) return;
+  commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
+}
+
+cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
+  if (dtype == 0) {
+    if (p.bg) k1_gram_kernel<float, true><<<grid, K1_THREADS, 0, s>>>(p);
+    else k1_gram_kernel<float, false><<<grid, K1_THREADS, 0, s>>>(p);
+  } else {
+    if (p.bg) k1_gram_kernel<double, true><<<grid, K1_THREADS, 0, s>>>(p);
+    else k1_gram_kernel<double, false><<<grid, K1_THREADS, 0, s>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_commit(const K1Params& p, cudaStream_t s) {
+  commit_kernel<<<1, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// Gram-history helpers (init_window path and get_gram)
+// ---------------------------------------------------------------------------------------------
+
+// Scatter a k x k window Gram (columns = frames first_frame .. first_frame+k-1) into ghist rows.
+__global__ void ghist_from_gram_kernel(const double* G, int k, double* ghist, int NH, int m,
+                                       long long first_frame) {
+  const int j = blockIdx.x;                       // frame first_frame + j
+  const long long f = first_frame + j;
+  double* row = ghist + (f % NH) * (m + 1);
+  for (int kk = threadIdx.x; kk < m + 1; kk += blockDim.x) {
+    const int i = kk - m + j;                     // column index of x_{f-m+kk} in the window
+    row[kk] = (i >= 0 && i <= j) ? G[(long long)j * k + i] : 0.0;
+  }
+}
+
+cudaError_t launch_ghist_from_gram(const double* G, int k, double* ghist, int NH, int m,
+                                   long long first_frame, cudaStream_t s) {
+  ghist_from_gram_kernel<<<k, 128, 0, s>>>(G, k, ghist, NH, m, first_frame);
+  return cudaGetLastError();
+}
+
+// Gather the logical-order k x k Gram of the window ending at frame f_last.
+__global__ void gather_gram_kernel(const double* ghist, int NH, int m, long long f_last, int k,
+                                   double* Gout) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= k * k) return;
+  const int i = idx % k, j = idx / k;
+  const int a = i < j ? i : j, b = i < j ? j : i;
+  const long long fb = f_last - (k - 1) + b;      // frame of column b
+  const int kk = a - b + m;                       // <x_{fb-m+kk}, x_fb> with fb-m+kk = frame of a
+  Gout[idx] = ghist[(fb % NH) * (m + 1) + kk];
+}
+
+cudaError_t launch_gather_gram(const double* ghist, int NH, int m, long long f_last, int k,
+                               double* Gout, cudaStream_t s) {
+  const int n = k * k;
+  gather_gram_kernel<<<(n + 255) / 256, 256, 0, s>>>(ghist, NH, m, f_last, k, Gout);
+  return cudaGetLastError();
+}
+
+}  // namespace sdmd

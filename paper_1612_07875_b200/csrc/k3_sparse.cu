@@ -1,0 +1,92 @@
+// k3_sparse.cu — K3: Gram column over natively compressed (sparse orthonormal-DCT) snapshots.
+//
+// §3.5: SVD and DMD are invariant under unitary transforms, so the window may be kept
+// in a sparse transform basis and "many of the core steps … performed on sparse data matrices"
+// — the paper did not implement this.  Each ring slot holds (idx int32 ascending,
+// val fp64, nnz).  Per push: (1) scatter x̂_new into a dense fp64 scratch vector that stays
+// L2-resident (8 MB for 1024²), (2) for every window column, gather-multiply its nonzeros against
+// the scratch (g_k = <ẑ_k, x̂_new>), partial sums per (column, chunk) reduced in fixed order by the
+// last block, which also (3) clears the scattered positions and commits the column.
+#include "sdmd_internal.cuh"
+
+namespace sdmd {
+
+constexpr int K3_THREADS = 256;
+constexpr int K3_CHUNK = 2048;     // nonzeros per block
+
+__global__ void k3_scatter_kernel(const K3Params p) {
+  if (*(volatile int*)&p.st->status != 0) return;
+  const int slot = (int)(p.f_new % p.NS);
+  const int nnz = p.nnz[slot];
+  const int* idx = p.idx + (long long)slot * p.nnz_cap;
+  const double* val = p.val + (long long)slot * p.nnz_cap;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += gridDim.x * blockDim.x)
+    p.scratch[idx[e] - p.row_begin] = val[e];
+}
+
+__global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
+  __shared__ double red[K3_THREADS / 32];
+  __shared__ int am_last;
+  if (*(volatile int*)&p.st->status != 0) return;
+  const int kd = blockIdx.y;                          // dot column (frame f_new - nd + 1 + kd)
+  const int c = blockIdx.x;                           // chunk of its nonzeros
+  const long long f = p.f_new - p.nd + 1 + kd;
+  const int slot = (int)(f % p.NS);
+  const int nnz = p.nnz[slot];
+  const int* idx = p.idx + (long long)slot * p.nnz_cap;
+  const double* val = p.val + (long long)slot * p.nnz_cap;
+  double s = 0.0;
+  const int e0 = c * K3_CHUNK, e1 = min(nnz, e0 + K3_CHUNK);
+  for (int e = e0 + threadIdx.x; e < e1; e += K3_THREADS)
+    s = fma(val[e], __ldcg(&p.scratch[idx[e] - p.row_begin]), s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < K3_THREADS / 32; ++w) t += red[w];
+    p.partials[(long long)kd * p.chunks + c] = t;
+    __threadfence();
+    const unsigned prev = atomicAdd(&p.st->k3_done, 1u);
+    am_last = (prev == gridDim.x * gridDim.y - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int k = threadIdx.x; k < p.nd; k += K3_THREADS) {
+    double t = 0.0;
+    for (int cc = 0; cc < p.chunks; ++cc) t += __ldcg(&p.partials[(long long)k * p.chunks + cc]);
+    p.gout[k] = t;
+  }
+  // clear the scatter positions of the new frame (scratch stays all-zero between pushes)
+  const int sl = (int)(p.f_new % p.NS);
+  const int nn = p.nnz[sl];
+  const int* ix = p.idx + (long long)sl * p.nnz_cap;
+  __syncthreads();
+  for (int e = threadIdx.x; e < nn; e += K3_THREADS) p.scratch[ix[e] - p.row_begin] = 0.0;
+  if (threadIdx.x == 0) p.st->k3_done = 0;
+  if (p.do_commit) {
+    __syncthreads();
+    commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
+  }
+}
+
+cudaError_t launch_k3(const K3Params& p, cudaStream_t s) {
+  k3_scatter_kernel<<<64, 256, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.chunks, p.nd);
+  k3_dot_kernel<<<grid, K3_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// Record the nonzero count of a ring slot (stream-ordered, no host staging).
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s) {
+  set_int_kernel<<<1, 1, 0, s>>>(p, v);
+  return cudaGetLastError();
+}
+
+}  // namespace sdmd

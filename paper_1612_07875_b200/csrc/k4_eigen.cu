@@ -1,0 +1,761 @@
+// k4_eigen.cu — K4: single-CTA on-device eigen engine of one streamed frame (no CPU fallback).
+//
+// For the window ending at frame f (Z = [x_{f-m} … x_f]), entirely from the Gram history:
+//   a5  S = XᵀX = G[0:m,0:m]; one-sided (Hestenes) Jacobi on S: S J = A with orthogonal columns,
+//       so |eig(S)| = ‖a_j‖ and V = a_j/‖a_j‖ (no rotation accumulation)   (§2.1; Alg 1)
+//   a6  σ = sqrt(|μ|) sorted desc, V permuted, r = #{σ > τσ₁} (Alg 1; reading Q7),
+//       Y = V Σ⁻¹ ("vsi", Alg 2)
+//   a7  Ã = Yᵀ (XᵀX') Y with XᵀX' = G[0:m,1:m+1] — zero new n-length dots (Alg 2)
+//   a8  eig(Ã): Householder Hessenberg reduction + Francis double-shift QR (eigenvalues) in
+//       shared memory (textbook algorithms, Golub–Van Loan §7.4-7.5; the paper only says "eig",
+//       P:314); inverse iteration on the Hessenberg form for the right/left eigenvectors needed
+//   a9  α₁ = Σ V[0,:]ᵀ (reading Q3), b_idx = y_idxᴴα₁ / (λ_idx y_idxᴴ w_idx)  (§3.3 P:264-273:
+//       "only the row corresponding to the … DMD eigenvalue need be calculated")
+//   a10 idx = argmin |log λ| (Alg 3; tie rule Q5)
+//   a11 (coefficients) c = b_idx λ_idx^m Y w_idx, so that l = X' c = b_idx φ_idx λ_idx^m (Q4)
+// The result c is consumed by a later K1 pass (fused background).  Everything is deterministic
+// (fixed reduction orders, no atomics), so replicated ranks compute bit-identical factors.
+#include <cfloat>
+#include "sdmd_internal.cuh"
+
+namespace sdmd {
+
+constexpr int K4_THREADS = 256;
+constexpr int K4_WARPS = K4_THREADS / 32;
+constexpr int JACOBI_MAX_SWEEPS = 60;
+constexpr int QR_MAXITS = 60;
+
+// ------------------------------------------------------------------ small helpers ------------
+static __device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+static __device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+static __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+static __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+static __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+static __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+static __device__ __forceinline__ double cabs2(double2 a) { return hypot(a.x, a.y); }
+static __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  // Smith's algorithm
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double rr = b.y / b.x, den = b.x + b.y * rr;
+    return make_double2((a.x + a.y * rr) / den, (a.y - a.x * rr) / den);
+  }
+  const double rr = b.x / b.y, den = b.x * rr + b.y;
+  return make_double2((a.x * rr + a.y) / den, (a.y * rr - a.x) / den);
+}
+static __device__ __forceinline__ double2 wsum2(double2 v) { return make_double2(wsum(v.x), wsum(v.y)); }
+
+// G_f(i, j), 0 <= i, j <= m, for the window ending at frame f (see sdmd_internal.cuh)
+static __device__ __forceinline__ double gram_at(const double* gh, int NH, int m, long long f, int i,
+                                                  int j) {
+  const int a = i < j ? i : j, b = i < j ? j : i;
+  const long long fb = f - m + b;
+  return gh[(fb % NH) * (m + 1) + (a - b + m)];
+}
+
+static __device__ __forceinline__ int rr_player(int pos, int step, int mp) {
+  return pos == 0 ? 0 : 1 + (pos - 1 + step) % (mp - 1);
+}
+
+// Packed upper-Hessenberg storage with 3 sub-diagonals of slack for the double-shift bulge.
+struct HsAcc {
+  double* hs;
+  const int* off;
+  __device__ __forceinline__ double& operator()(int i, int j) const {
+    const int lo = i > 3 ? i - 3 : 0;
+    return hs[off[i] + j - lo];
+  }
+};
+
+__host__ __device__ inline long long hs_elems(int r) {
+  long long s = 0;
+  for (int i = 0; i < r; ++i) s += r - (i > 3 ? i - 3 : 0);
+  return s;
+}
+
+// Eigenvalues of an upper Hessenberg matrix by the Francis double-shift QR iteration with
+// deflation on negligible sub-diagonals and ad-hoc exceptional shifts every 10 iterations
+// (eigenvalues only: updates restricted to the active block).  Executed by ONE warp: every lane
+// runs the scalar recurrences redundantly on identical shared-memory data; lanes split the row
+// and column updates of each 3x3 reflector.  Returns 0, or -1 when an eigenvalue needs more than
+// QR_MAXITS iterations.
+static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* total_its) {
+  double an = 0.0;
+  for (int i = 0; i < n; ++i)
+    for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(a(i, j));
+  an = wsum(an);
+  int nn = n - 1, tot = 0;
+  double t = 0.0;
+  while (nn >= 0) {
+    int its = 0, l;
+    do {
+      for (l = nn; l >= 1; --l) {
+        double s = fabs(a(l - 1, l - 1)) + fabs(a(l, l));
+        if (s == 0.0) s = an;
+        if (fabs(a(l, l - 1)) + s == s) {
+          __syncwarp();
+          if (lane == 0) a(l, l - 1) = 0.0;
+          __syncwarp();
+          break;
+        }
+      }
+      double x = a(nn, nn);
+      if (l == nn) {                                   // one root
+        if (lane == 0) wv[nn] = make_double2(x + t, 0.0);
+        nn -= 1;
+      } else {
+        double y = a(nn - 1, nn - 1), w = a(nn, nn - 1) * a(nn - 1, nn);
+        if (l == nn - 1) {                             // two roots (2x2 block)
+          const double p = 0.5 * (y - x), q = p * p + w;
+          double z = sqrt(fabs(q));
+          x += t;
+          if (q >= 0.0) {
+            z = p + copysign(z, p);
+            const double e1 = x + z, e2 = (z != 0.0) ? x - w / z : e1;
+            if (lane == 0) { wv[nn - 1] = make_double2(e1, 0.0); wv[nn] = make_double2(e2, 0.0); }
+          } else if (lane == 0) {
+            wv[nn - 1] = make_double2(x + p, z);
+            wv[nn] = make_double2(x + p, -z);
+          }
+          nn -= 2;
+        } else {                                       // no root yet: one double-shift sweep
+          if (its == QR_MAXITS) return -1;
+          if (its > 0 && its % 10 == 0) {              // exceptional shift
+            t += x;
+            __syncwarp();
+            for (int i = lane; i <= nn; i += 32) a(i, i) -= x;
+            __syncwarp();
+            const double s = fabs(a(nn, nn - 1)) + fabs(a(nn - 1, nn - 2));
+            y = x = 0.75 * s;
+            w = -0.4375 * s * s;
+          }
+          ++its;
+          ++tot;
+          int mm;
+          double p = 0.0, q = 0.0, r = 0.0, z = 0.0;
+          for (mm = nn - 2; mm >= l; --mm) {           // two small consecutive sub-diagonals?
+            z = a(mm, mm);
+            r = x - z;
+            double s = y - z;
+            p = (r * s - w) / a(mm + 1, mm) + a(mm, mm + 1);
+            q = a(mm + 1, mm + 1) - z - r - s;
+            r = a(mm + 2, mm + 1);
+            s = fabs(p) + fabs(q) + fabs(r);
+            p /= s; q /= s; r /= s;
+            if (mm == l) break;
+            const double u = fabs(a(mm, mm - 1)) * (fabs(q) + fabs(r));
+            const double v = fabs(p) * (fabs(a(mm - 1, mm - 1)) + fabs(z) + fabs(a(mm + 1, mm + 1)));
+            if (u + v == v) break;
+          }
+          __syncwarp();
+          for (int i = mm + 2 + lane; i <= nn; i += 32) {
+            a(i, i - 2) = 0.0;
+            if (i != mm + 2) a(i, i - 3) = 0.0;
+          }
+          __syncwarp();
+          for (int k = mm; k <= nn - 1; ++k) {          // chase the bulge
+            if (k != mm) {
+              p = a(k, k - 1);
+              q = a(k + 1, k - 1);
+              r = (k != nn - 1) ? a(k + 2, k - 1) : 0.0;
+              x = fabs(p) + fabs(q) + fabs(r);
+              if (x != 0.0) { p /= x; q /= x; r /= x; }
+            }
+            const double s = copysign(sqrt(p * p + q * q + r * r), p);
+            if (s != 0.0) {
+              __syncwarp();
+              if (k == mm) {
+                if (l != mm && lane == 0) a(k, k - 1) = -a(k, k - 1);
+              } else if (lane == 0) {
+                a(k, k - 1) = -s * x;
+              }
+              p += s;
+              x = p / s; y = q / s; z = r / s;
+              q /= p; r /= p;
+              __syncwarp();
+              for (int j = k + lane; j <= nn; j += 32) {   // row modification
+                double pp = a(k, j) + q * a(k + 1, j);
+                if (k != nn - 1) { pp += r * a(k + 2, j); a(k + 2, j) -= pp * z; }
+                a(k + 1, j) -= pp * y;
+                a(k, j) -= pp * x;
+              }
+              __syncwarp();
+              const int mmin = nn < k + 3 ? nn : k + 3;
+              for (int i = l + lane; i <= mmin; i += 32) { // column modification
+                double pp = x * a(i, k) + y * a(i, k + 1);
+                if (k != nn - 1) { pp += z * a(i, k + 2); a(i, k + 2) -= pp * r; }
+                a(i, k + 1) -= pp * q;
+                a(i, k) -= pp;
+              }
+              __syncwarp();
+            }
+          }
+        }
+      }
+    } while (l < nn - 1);
+  }
+  *total_its = tot;
+  return 0;
+}
+
+// Inverse iteration on the Hessenberg form H (row-major r x r, global) for eigenvalue lam, one
+// warp.  Returns the right eigenvector w = Q z and (if yout) the left eigenvector y = Q u of the
+// ORIGINAL matrix Ã = Q H Qᵀ, both unit 2-norm; w additionally has its largest entry real > 0.
+// M: r*r complex workspace; smem: z, rhs (r complex each), lk (r complex), sw (r ints).
+static __device__ void inverse_iteration(const double* H, const double* Qv, const double* tau, int r,
+                                         double2 lam, double2* M, double2* z, double2* rhs,
+                                         double2* lk, int* sw, double2* wout, double2* yout,
+                                         int lane) {
+  double hn = 0.0;
+  for (int i = 0; i < r; ++i)
+    for (int j = (i > 0 ? i - 1 : 0) + lane; j < r; j += 32) {
+      const double h = H[(long long)i * r + j];
+      hn = fmax(hn, fabs(h));
+      double2 v = make_double2(h, 0.0);
+      if (i == j) v = csub(v, lam);
+      M[(long long)i * r + j] = v;
+    }
+  hn = wmax(hn);
+  const double small = (hn > 0.0 ? hn : 1.0) * DBL_EPSILON;
+  for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
+  __syncwarp();
+  // LU with adjacent-row partial pivoting (Hessenberg: one sub-diagonal)
+  for (int k = 0; k < r - 1; ++k) {
+    double2* Mk = M + (long long)k * r;
+    double2* Mk1 = M + (long long)(k + 1) * r;
+    const bool swp = cabs2(Mk1[k]) > cabs2(Mk[k]);
+    __syncwarp();
+    if (swp) {
+      for (int j = k + lane; j < r; j += 32) { const double2 t = Mk[j]; Mk[j] = Mk1[j]; Mk1[j] = t; }
+      if (lane == 0) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
+    }
+    __syncwarp();
+    double2 piv = Mk[k];
+    if (cabs2(piv) == 0.0) piv = make_double2(small, 0.0);
+    const double2 l = cdiv(Mk1[k], piv);
+    __syncwarp();
+    if (lane == 0) { Mk[k] = piv; lk[k] = l; sw[k] = swp ? 1 : 0; rhs[k + 1] = csub(rhs[k + 1], cmul(l, rhs[k])); }
+    for (int j = k + 1 + lane; j < r; j += 32) Mk1[j] = csub(Mk1[j], cmul(l, Mk[j]));
+    __syncwarp();
+  }
+  if (lane == 0 && cabs2(M[(long long)(r - 1) * r + r - 1]) == 0.0)
+    M[(long long)(r - 1) * r + r - 1] = make_double2(small, 0.0);
+  __syncwarp();
+
+  // ---- right vector: two solves U z = (L⁻¹P) rhs
+  for (int it = 0; it < 2; ++it) {
+    if (it == 1) {   // rhs = z normalised, transformed by the stored row operations
+      if (lane == 0) {
+        for (int k = 0; k < r - 1; ++k) {
+          if (sw[k]) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
+          rhs[k + 1] = csub(rhs[k + 1], cmul(lk[k], rhs[k]));
+        }
+      }
+      __syncwarp();
+    }
+    for (int i = r - 1; i >= 0; --i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = i + 1 + lane; j < r; j += 32) s = cadd(s, cmul(M[(long long)i * r + j], z[j]));
+      s = wsum2(s);
+      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), M[(long long)i * r + i]);
+      __syncwarp();
+    }
+    double nrm = 0.0;
+    for (int i = lane; i < r; i += 32) nrm = fmax(nrm, cabs2(z[i]));
+    nrm = wmax(nrm);
+    double ss = 0.0;
+    for (int i = lane; i < r; i += 32) { const double2 v = z[i]; ss += (v.x / nrm) * (v.x / nrm) + (v.y / nrm) * (v.y / nrm); }
+    ss = wsum(ss);
+    const double inv = 1.0 / (nrm * sqrt(ss));
+    __syncwarp();
+    for (int i = lane; i < r; i += 32) { z[i] = make_double2(z[i].x * inv, z[i].y * inv); rhs[i] = z[i]; }
+    __syncwarp();
+  }
+  // w = Q z  (Q = P_0 P_1 … P_{r-3}; apply P_{r-3} first)
+  for (int i = lane; i < r; i += 32) wout[i] = z[i];
+  __syncwarp();
+  for (int k = r - 3; k >= 0; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* v = Qv + (long long)k * r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = k + 1 + lane; i < r; i += 32) s = cadd(s, make_double2(v[i] * wout[i].x, v[i] * wout[i].y));
+    s = wsum2(s);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < r; i += 32)
+      wout[i] = csub(wout[i], make_double2(tk * s.x * v[i], tk * s.y * v[i]));
+    __syncwarp();
+  }
+  // normalise: unit norm, largest-|.| entry real positive (reading Q12)
+  {
+    double best = -1.0;
+    int bi = 0;
+    double ss = 0.0;
+    for (int i = lane; i < r; i += 32) {
+      const double a = cabs2(wout[i]);
+      ss += a * a;
+      if (a > best) { best = a; bi = i; }
+    }
+    ss = wsum(ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double2 piv = wout[bi];
+    const double ap = cabs2(piv);
+    const double2 ph = make_double2(piv.x / ap, -piv.y / ap);      // conj(piv)/|piv|
+    const double inv = 1.0 / sqrt(ss);
+    __syncwarp();
+    for (int i = lane; i < r; i += 32) {
+      const double2 v = cmul(wout[i], ph);
+      wout[i] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncwarp();
+    if (lane == 0) wout[bi] = make_double2(wout[bi].x, 0.0);
+    __syncwarp();
+  }
+  if (yout == nullptr) return;
+
+  // ---- left vector: Mᴴ u = e  →  Uᴴ a = e, then a ← S_k E_kᴴ a for k = r-2 … 0
+  for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
+  __syncwarp();
+  for (int it = 0; it < 2; ++it) {
+    for (int i = 0; i < r; ++i) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = lane; j < i; j += 32) s = cadd(s, cmul(cconj(M[(long long)j * r + i]), z[j]));
+      s = wsum2(s);
+      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), cconj(M[(long long)i * r + i]));
+      __syncwarp();
+    }
+    if (lane == 0) {
+      for (int k = r - 2; k >= 0; --k) {
+        z[k] = csub(z[k], cmul(cconj(lk[k]), z[k + 1]));
+        if (sw[k]) { const double2 t = z[k]; z[k] = z[k + 1]; z[k + 1] = t; }
+      }
+    }
+    __syncwarp();
+    double nrm = 0.0;
+    for (int i = lane; i < r; i += 32) nrm = fmax(nrm, cabs2(z[i]));
+    nrm = wmax(nrm);
+    double ss = 0.0;
+    for (int i = lane; i < r; i += 32) { const double2 v = z[i]; ss += (v.x / nrm) * (v.x / nrm) + (v.y / nrm) * (v.y / nrm); }
+    ss = wsum(ss);
+    const double inv = 1.0 / (nrm * sqrt(ss));
+    __syncwarp();
+    for (int i = lane; i < r; i += 32) { z[i] = make_double2(z[i].x * inv, z[i].y * inv); rhs[i] = z[i]; }
+    __syncwarp();
+  }
+  for (int i = lane; i < r; i += 32) yout[i] = z[i];
+  __syncwarp();
+  for (int k = r - 3; k >= 0; --k) {
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* v = Qv + (long long)k * r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = k + 1 + lane; i < r; i += 32) s = cadd(s, make_double2(v[i] * yout[i].x, v[i] * yout[i].y));
+    s = wsum2(s);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < r; i += 32)
+      yout[i] = csub(yout[i], make_double2(tk * s.x * v[i], tk * s.y * v[i]));
+    __syncwarp();
+  }
+}
+
+// ------------------------------------------------------------------ the per-frame kernel ------
+__global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params p) {
+  extern __shared__ __align__(16) unsigned char k4_smem[];
+  __shared__ double mu[kMaxM];
+  __shared__ double sig[kMaxM];
+  __shared__ int perm[kMaxM];
+  __shared__ double vbuf[kMaxR];
+  __shared__ int hoff[kMaxR + 1];
+  __shared__ int sh_r, sh_status, sh_idx, sh_its;
+  __shared__ double sh_tau;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = p.m;
+  const long long f = p.f;
+  K4Result* res = p.res;
+  {
+    volatile DevState* st = p.st;
+    if (st->status != 0 && st->failed_frame <= f) {   // frame discarded by the poison contract
+      if (tid == 0) { res->frame = f; res->status = -1; }
+      return;
+    }
+  }
+  // ---- a5: S and XᵀX' from the Gram history
+  for (int idx = tid; idx < m * m; idx += K4_THREADS) {
+    const int i = idx % m, j = idx / m;
+    p.A[idx] = gram_at(p.ghist, p.NH, m, f, i, j);
+    p.Gxy[idx] = gram_at(p.ghist, p.NH, m, f, i, j + 1);
+  }
+  __syncthreads();
+
+  // ---- a5: one-sided Jacobi, round-robin (circle) ordering of column pairs
+  const int mp = m + (m & 1);
+  const int npairs = mp / 2;
+  const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
+  int sweeps = 0;
+  bool converged = false;
+  for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
+    int rot = 0;
+    for (int s = 0; s < mp - 1; ++s) {
+      for (int k = warp; k < npairs; k += K4_WARPS) {
+        const int pp = rr_player(k, s, mp), qq = rr_player(mp - 1 - k, s, mp);
+        if (pp >= m || qq >= m) continue;
+        double* cp = p.A + (long long)pp * m;
+        double* cq = p.A + (long long)qq * m;
+        double ap[kMaxM / 32], aq[kMaxM / 32];
+        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+        for (int e = 0; e < kMaxM / 32; ++e) {
+          const int i = lane + 32 * e;
+          ap[e] = (i < m) ? cp[i] : 0.0;
+          aq[e] = (i < m) ? cq[i] : 0.0;
+          al = fma(ap[e], ap[e], al);
+          be = fma(aq[e], aq[e], be);
+          ga = fma(ap[e], aq[e], ga);
+        }
+        al = wsum(al); be = wsum(be); ga = wsum(ga);
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+#pragma unroll
+          for (int e = 0; e < kMaxM / 32; ++e) {
+            const int i = lane + 32 * e;
+            if (i < m) {
+              cp[i] = c * ap[e] - sn * aq[e];
+              cq[i] = sn * ap[e] + c * aq[e];
+            }
+          }
+          rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    ++sweeps;
+    if (!__syncthreads_or(rot)) { converged = true; break; }
+  }
+
+  // ---- a6: μ_j = ‖a_j‖ = |eig_j(S)|, sort descending, σ = sqrt(|μ|), rank, V
+  for (int j = warp; j < m; j += K4_WARPS) {
+    const double* cj = p.A + (long long)j * m;
+    double s = 0.0;
+    for (int i = lane; i < m; i += 32) s = fma(cj[i], cj[i], s);
+    s = wsum(s);
+    if (lane == 0) mu[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < m; j += K4_THREADS) {
+    int rank = 0;
+    const double mj = mu[j];
+    for (int i = 0; i < m; ++i) rank += (mu[i] > mj || (mu[i] == mj && i < j)) ? 1 : 0;
+    perm[rank] = j;
+  }
+  __syncthreads();
+  for (int i = tid; i < m; i += K4_THREADS) {
+    const double s = sqrt(mu[perm[i]]);
+    sig[i] = s;
+    p.sigma[i] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int r = 0;
+    const double thr = p.rank_tol * sig[0];
+    for (int i = 0; i < m; ++i) r += (sig[i] > thr) ? 1 : 0;
+    if (r > p.r_max) r = p.r_max;
+    sh_r = r;
+    sh_status = (sig[0] == 0.0 || r == 0) ? 4 /*SDMD_E_ZERO_MATRIX*/ : (converged ? 0 : 5);
+  }
+  __syncthreads();
+  const int r = sh_r;
+  if (sh_status == 4) {
+    for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
+    if (tid == 0) {
+      res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps;
+      res->qr_its = 0; res->sigma1 = sig[0];
+    }
+    return;
+  }
+  for (int i = warp; i < m; i += K4_WARPS) {
+    const int src = perm[i];
+    const double inv = mu[src] > 0.0 ? 1.0 / mu[src] : 0.0;
+    const double* cj = p.A + (long long)src * m;
+    double best = -1.0;
+    int bi = 0;
+    for (int k = lane; k < m; k += 32) {
+      const double a = fabs(cj[k]);
+      if (a > best) { best = a; bi = k; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double sgn = (cj[bi] < 0.0) ? -inv : inv;         // reading Q6
+    for (int k = lane; k < m; k += 32) p.V[(long long)i * m + k] = cj[k] * sgn;
+  }
+  __syncthreads();
+
+  // ---- a6/a7: Y = V Σ⁻¹, B = (XᵀX') Y, Ã = Yᵀ B  (zero n-length dots)
+  for (int idx = tid; idx < m * r; idx += K4_THREADS) {
+    const int j = idx / m;
+    p.Y[idx] = p.V[idx] / sig[j];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < m * r; idx += K4_THREADS) {
+    const int i = idx % m, j = idx / m;
+    const double* yj = p.Y + (long long)j * m;
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) s = fma(p.Gxy[(long long)k * m + i], yj[k], s);
+    p.B[idx] = s;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < r * r; idx += K4_THREADS) {
+    const int i = idx % r, j = idx / r;
+    const double* yi = p.Y + (long long)i * m;
+    const double* bj = p.B + (long long)j * m;
+    double s = 0.0;
+    for (int k = 0; k < m; ++k) s = fma(yi[k], bj[k], s);
+    p.H[(long long)i * r + j] = s;
+  }
+  for (int j = tid; j < r; j += K4_THREADS) p.alpha1[j] = sig[j] * p.V[(long long)j * m];  // Q3
+  __syncthreads();
+
+  // ---- a8: Householder reduction of Ã to upper Hessenberg form (H row-major, ld r)
+  double* H = p.H;
+  for (int k = 0; k < r - 2; ++k) {
+    const int L = r - k - 1;
+    if (warp == 0) {
+      double x[kMaxR / 32];
+      double s2 = 0.0, x0 = 0.0;
+#pragma unroll
+      for (int e = 0; e < kMaxR / 32; ++e) {
+        const int i = lane + 32 * e;
+        x[e] = (i < L) ? H[(long long)(k + 1 + i) * r + k] : 0.0;
+        if (i == 0) x0 = x[e];
+        else s2 = fma(x[e], x[e], s2);
+      }
+      s2 = wsum(s2);
+      x0 = __shfl_sync(0xffffffffu, x0, 0);
+      double tauk = 0.0, beta = x0, v0 = 1.0;
+      if (s2 != 0.0) {
+        const double mu_ = sqrt(x0 * x0 + s2);
+        v0 = (x0 <= 0.0) ? x0 - mu_ : -s2 / (x0 + mu_);
+        tauk = 2.0 * v0 * v0 / (s2 + v0 * v0);
+        beta = mu_;
+      }
+#pragma unroll
+      for (int e = 0; e < kMaxR / 32; ++e) {
+        const int i = lane + 32 * e;
+        if (i < L) {
+          const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? x[e] / v0 : 0.0);
+          vbuf[i] = v;
+          p.Qv[(long long)k * r + k + 1 + i] = v;
+          H[(long long)(k + 1 + i) * r + k] = (i == 0) ? beta : 0.0;
+        }
+      }
+      if (lane == 0) { p.tau[k] = tauk; sh_tau = tauk; }
+    }
+    __syncthreads();
+    const double tk = sh_tau;
+    if (tk != 0.0) {
+      for (int j = k + 1 + tid; j < r; j += K4_THREADS) {          // left: (I - τvvᵀ) H
+        double s = 0.0;
+        for (int i = 0; i < L; ++i) s = fma(vbuf[i], H[(long long)(k + 1 + i) * r + j], s);
+        s *= tk;
+        for (int i = 0; i < L; ++i) H[(long long)(k + 1 + i) * r + j] -= s * vbuf[i];
+      }
+      __syncthreads();
+      for (int i = warp; i < r; i += K4_WARPS) {                   // right: H (I - τvvᵀ)
+        double* hi = H + (long long)i * r + k + 1;
+        double s = 0.0;
+        for (int jj = lane; jj < L; jj += 32) s = fma(hi[jj], vbuf[jj], s);
+        s = wsum(s) * tk;
+        for (int jj = lane; jj < L; jj += 32) hi[jj] -= s * vbuf[jj];
+      }
+    }
+    __syncthreads();
+  }
+  if (r >= 2 && tid == 0) p.tau[r - 2] = 0.0;
+  if (tid == 0) { p.tau[r > 0 ? r - 1 : 0] = 0.0; }
+
+  // ---- a8: eigenvalues by Francis double-shift QR in shared memory (warp 0)
+  double* hs = reinterpret_cast<double*>(k4_smem);
+  const long long hsz = hs_elems(r);
+  double2* lam_raw = reinterpret_cast<double2*>(hs + ((hsz + 1) & ~1LL));
+  if (tid == 0) {
+    int o = 0;
+    for (int i = 0; i < r; ++i) { hoff[i] = o; o += r - (i > 3 ? i - 3 : 0); }
+    hoff[r] = o;
+  }
+  __syncthreads();
+  for (int i = warp; i < r; i += K4_WARPS) {
+    const int lo = i > 3 ? i - 3 : 0;
+    for (int j = lo + lane; j < r; j += 32)
+      hs[hoff[i] + j - lo] = (j >= i - 1) ? H[(long long)i * r + j] : 0.0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int its = 0;
+    const int rc = hessenberg_qr(HsAcc{hs, hoff}, r, lam_raw, lane, &its);
+    if (lane == 0) { sh_its = its; if (rc != 0) sh_status = 5; }
+  }
+  __syncthreads();
+
+  // ---- sort λ: |λ| desc, Re desc, Im desc (reading Q12)
+  for (int j = tid; j < r; j += K4_THREADS) {
+    const double2 lj = lam_raw[j];
+    const double aj = hypot(lj.x, lj.y);
+    int rank = 0;
+    for (int i = 0; i < r; ++i) {
+      const double2 li = lam_raw[i];
+      const double ai = hypot(li.x, li.y);
+      const bool before = (ai > aj) || (ai == aj && (li.x > lj.x || (li.x == lj.x && (li.y > lj.y ||
+                          (li.y == lj.y && i < j)))));
+      rank += before ? 1 : 0;
+    }
+    p.lam[rank] = lj;
+  }
+  __syncthreads();
+
+  // ---- a10: idx = argmin |log λ| (principal branch), λ = 0 excluded; ties (Q5)
+  if (tid == 0) {
+    int best = -1;
+    double k1 = 0, k2 = 0;
+    int k3 = 0;
+    for (int i = 0; i < r; ++i) {
+      const double2 l = p.lam[i];
+      if (l.x == 0.0 && l.y == 0.0) continue;
+      const double lr = log(hypot(l.x, l.y)), li = atan2(l.y, l.x);
+      const double a1 = hypot(lr, li), a2 = fabs(li);
+      const int a3 = (l.y >= 0.0) ? 0 : 1;
+      if (best < 0 || a1 < k1 || (a1 == k1 && (a2 < k2 || (a2 == k2 && a3 < k3)))) {
+        best = i; k1 = a1; k2 = a2; k3 = a3;
+      }
+    }
+    sh_idx = best;
+    if (best < 0 && sh_status == 0) sh_status = 7;
+  }
+  __syncthreads();
+  const int idx = sh_idx;
+
+  // ---- a8/a9: eigenvectors of the background mode, b_idx, and c (warp 0)
+  // scratch aliases the (now free) packed Hessenberg area
+  double2* z = reinterpret_cast<double2*>(k4_smem);
+  double2* rhs = z + kMaxR;
+  double2* lk = rhs + kMaxR;
+  int* swk = reinterpret_cast<int*>(lk + kMaxR);
+  if (idx >= 0 && warp == 0) {
+    const double2 lam = p.lam[idx];
+    inverse_iteration(H, p.Qv, p.tau, r, lam, p.M, z, rhs, lk, swk, p.w, p.y, lane);
+    // b_idx = yᴴα₁ / (λ yᴴw)
+    double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
+    for (int i = lane; i < r; i += 32) {
+      const double2 yc = cconj(p.y[i]);
+      ya = cadd(ya, make_double2(yc.x * p.alpha1[i], yc.y * p.alpha1[i]));
+      yw = cadd(yw, cmul(yc, p.w[i]));
+    }
+    ya = wsum2(ya);
+    yw = wsum2(yw);
+    const double2 den = cmul(lam, yw);
+    double2 b = make_double2(0.0, 0.0);
+    int st = sh_status;
+    if (cabs2(den) > 1e-300) b = cdiv(ya, den);
+    else if (st == 0) st = 6;
+    // λ^m by binary powering
+    double2 pw = make_double2(1.0, 0.0), base = lam;
+    for (int e = m; e > 0; e >>= 1) {
+      if (e & 1) pw = cmul(pw, base);
+      base = cmul(base, base);
+    }
+    const double2 coef = cmul(b, pw);
+    for (int i = lane; i < m; i += 32) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int j = 0; j < r; ++j) {
+        const double yv = p.Y[(long long)j * m + i];
+        s = cadd(s, make_double2(yv * p.w[j].x, yv * p.w[j].y));
+      }
+      p.cout[i] = cmul(coef, s);
+    }
+    if (lane == 0) {
+      res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
+      res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
+      res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sig[0];
+    }
+  } else if (idx < 0) {
+    for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
+    if (tid == 0) {
+      res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
+      res->qr_its = sh_its; res->sigma1 = sig[0];
+    }
+  }
+}
+
+size_t k4_smem_bytes(int r_max) {
+  const long long hs = hs_elems(r_max);
+  const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
+  const size_t b = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);
+  return a > b ? a : b;
+}
+
+cudaError_t launch_k4(const K4Params& p, cudaStream_t s) {
+  const size_t smem = k4_smem_bytes(p.r_max);
+  cudaError_t e = cudaFuncSetAttribute(k4_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k4_frame_kernel<<<1, K4_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- on-demand eigenvectors and b --------
+__global__ void __launch_bounds__(32) k4_vecs_kernel(const K4VecParams p) {
+  extern __shared__ __align__(16) unsigned char vs_smem[];
+  const int r = p.r;
+  double2* z = reinterpret_cast<double2*>(vs_smem);
+  double2* rhs = z + r;
+  double2* lk = rhs + r;
+  double2* wv = lk + r;
+  double2* yv = wv + r;
+  int* swk = reinterpret_cast<int*>(yv + r);
+  const int j = p.j0 + blockIdx.x;
+  if (j >= r) return;
+  const int lane = threadIdx.x;
+  const double2 lam = p.lam[j];
+  double2* M = p.Mws + (long long)blockIdx.x * r * r;
+  inverse_iteration(p.H, p.Qv, p.tau, r, lam, M, z, rhs, lk, swk, wv, yv, lane);
+  double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
+  for (int i = lane; i < r; i += 32) {
+    const double2 yc = cconj(yv[i]);
+    ya = cadd(ya, make_double2(yc.x * p.alpha1[i], yc.y * p.alpha1[i]));
+    yw = cadd(yw, cmul(yc, wv[i]));
+  }
+  ya = wsum2(ya);
+  yw = wsum2(yw);
+  for (int i = lane; i < r; i += 32) p.W[(long long)j * r + i] = wv[i];
+  if (lane == 0) {
+    const double2 den = cmul(lam, yw);
+    p.b[j] = (cabs2(den) > 1e-300) ? cdiv(ya, den) : make_double2(0.0, 0.0);
+  }
+}
+
+cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s) {
+  const size_t smem = 5 * (size_t)p.r * sizeof(double2) + (size_t)p.r * sizeof(int) + 16;
+  k4_vecs_kernel<<<count, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace sdmd

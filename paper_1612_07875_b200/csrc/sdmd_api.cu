@@ -1,0 +1,804 @@
+// sdmd_api.cu — host runtime behind include/sdmd.h: context, HBM ring, Gram history, the per-frame
+// DAG (ingest → K1/K3 → [NCCL allreduce] → commit → K4 on round-robin eigen-worker streams →
+// fused background in a later K1), event bookkeeping, getters and the NCCL bootstrap.
+//
+// Per push of frame t (all enqueued asynchronously; the host never waits):
+//   main stream : [wait done(t-lag)] → copy x_t into slot t mod NS → K1(t) (+ background of t-lag)
+//                 → [ncclAllReduce(g) → commit] → record commit(t)
+//   worker t%W  : wait commit(t) → K4(t) → record done(t)
+// K4(t) overlaps the K1 passes of frames t+1 … t+lag-1 (they touch disjoint data), so the eigen
+// work is hidden behind the bandwidth-bound Gram pass when lag·t_K1 ≥ t_K4.
+#include <dlfcn.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/sdmd.h"
+#include "nccl.h"
+#include "sdmd_internal.cuh"
+
+using namespace sdmd;
+
+namespace {
+
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  if (api.loaded) return &api;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return nullptr;
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy) return nullptr;
+  api.loaded = true;
+  return &api;
+}
+
+constexpr int kEvents = 64;
+
+struct Worker {
+  cudaStream_t s = nullptr;
+  double *A = nullptr, *Gxy = nullptr, *V = nullptr, *sigma = nullptr, *Y = nullptr, *B = nullptr;
+  double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
+  double2 *M = nullptr, *lam = nullptr, *w = nullptr, *y = nullptr;
+  K4Result* res = nullptr;
+  long long vecs_frame = -1;            // frame whose full W/b are cached in Wall/ball
+};
+
+}  // namespace
+
+struct sdmd_ctx {
+  sdmd_config cfg{};
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148;
+  long long ld = 0;
+  size_t es = 4;
+  void* ring = nullptr;
+  DevState* dst = nullptr;
+  double* ghist = nullptr;
+  double2* cbuf = nullptr;
+  double* partials = nullptr;
+  double* gout = nullptr;
+  double* gpart = nullptr;              // pre-allreduce copy
+  int last_nd = 0;
+  // sparse storage
+  int* sp_idx = nullptr;
+  double* sp_val = nullptr;
+  int* sp_nnz = nullptr;
+  double* scratch = nullptr;
+  int k3_chunks = 1;
+  // background outputs
+  void* bg_low = nullptr;
+  void* bg_sparse = nullptr;
+  unsigned char* bg_mask = nullptr;
+  // workers
+  Worker wk[kMaxWorkers];
+  cudaEvent_t ev_commit[kEvents]{};
+  cudaEvent_t ev_done[kEvents]{};
+  cudaEvent_t ev_k1[kEvents]{};         // after K1(t) on the main stream (slot-reuse fence)
+  cudaEvent_t ev_copy[kEvents]{};       // after the H2D copy of frame t on the copy stream
+  cudaStream_t copy_stream = nullptr;   // overlaps host→device ingest with the previous K1
+  // on-demand buffers
+  double2* Wall = nullptr;
+  double2* ball = nullptr;
+  double2* Mws = nullptr;
+  int mws_chunk = 16;
+  double* Tbuf = nullptr;
+  int* colbuf = nullptr;
+  double* Gtmp = nullptr;
+  double* init_work = nullptr;
+  size_t init_work_elems = 0;
+  // host mirror (valid unless a deferred error is pending)
+  long long frames = 0;
+  long long last_dmd = -1;
+  // timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev;
+  long long launches = 0;
+  // nccl
+  ncclComm_t comm = nullptr;
+  std::string err;
+};
+
+// ------------------------------------------------------------------------- helpers ------------
+static int fail_cuda(sdmd_ctx* c, cudaError_t e, const char* what) {
+  if (c) c->err = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? SDMD_E_OOM : SDMD_E_CUDA;
+}
+#define CK(call)                                            \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return fail_cuda(c, e_, #call);  \
+  } while (0)
+
+static int invalid(sdmd_ctx* c, const char* msg) {
+  if (c) c->err = msg;
+  return SDMD_E_INVALID;
+}
+
+template <typename T>
+static cudaError_t dalloc(T** p, size_t count) {
+  return cudaMalloc((void**)p, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
+}
+
+static void destroy_timing(sdmd_ctx* c) {
+  for (auto& pr : c->k1_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto& pr : c->k4_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  c->k1_ev.clear();
+  c->k4_ev.clear();
+}
+
+static std::pair<cudaEvent_t, cudaEvent_t> new_pair() {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  return {a, b};
+}
+
+static int sync_all(sdmd_ctx* c) {
+  CK(cudaStreamSynchronize(c->copy_stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int w = 0; w < c->W; ++w) CK(cudaStreamSynchronize(c->wk[w].s));
+  return SDMD_OK;
+}
+
+// ------------------------------------------------------------------------- ABI ----------------
+extern "C" {
+
+int sdmd_abi_version(void) { return SDMD_ABI_VERSION; }
+
+const char* sdmd_status_string(int s) {
+  switch (s) {
+    case SDMD_OK: return "ok";
+    case SDMD_E_INVALID: return "invalid argument";
+    case SDMD_E_NONFINITE: return "non-finite frame rejected";
+    case SDMD_E_WINDOW_NOT_FULL: return "window not full";
+    case SDMD_E_ZERO_MATRIX: return "zero matrix (sigma_1 == 0)";
+    case SDMD_E_NO_CONVERGENCE: return "eigensolver did not converge";
+    case SDMD_W_SINGULAR: return "W*Lambda singular";
+    case SDMD_E_NO_VIABLE_MODE: return "no viable background mode";
+    case SDMD_E_CUDA: return "CUDA error";
+    case SDMD_E_NCCL: return "NCCL error";
+    case SDMD_E_OOM: return "out of device memory";
+    case SDMD_E_STATE: return "invalid state";
+    default: return "unknown status";
+  }
+}
+
+const char* sdmd_last_error(const sdmd_ctx* c) { return c ? c->err.c_str() : ""; }
+
+int sdmd_config_init(sdmd_config* cfg) {
+  if (!cfg) return SDMD_E_INVALID;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->rank_tol = 1e-7;
+  cfg->threshold = 0.2f;
+  cfg->dmd = 1;
+  cfg->background = 0;
+  cfg->workers = 4;
+  cfg->nranks = 1;
+  cfg->dtype = SDMD_F32;
+  cfg->storage = SDMD_DENSE;
+  return SDMD_OK;
+}
+
+int sdmd_nccl_unique_id(uint8_t out[128]) {
+  if (!out) return SDMD_E_INVALID;
+  NcclApi* api = nccl_api();
+  if (!api) return SDMD_E_NCCL;
+  ncclUniqueId id;
+  if (api->GetUniqueId(&id) != ncclSuccess) return SDMD_E_NCCL;
+  std::memcpy(out, id.internal, 128);
+  return SDMD_OK;
+}
+
+int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
+  if (!cfg_in || !out) return SDMD_E_INVALID;
+  *out = nullptr;
+  const sdmd_config& cfg = *cfg_in;
+  if (cfg.m < 2 || cfg.m > SDMD_MAX_M || cfg.n_local < 1 || cfg.n_global < cfg.n_local ||
+      cfg.row_begin < 0 || cfg.row_begin + cfg.n_local > cfg.n_global ||
+      (cfg.dtype != SDMD_F32 && cfg.dtype != SDMD_F64) ||
+      (cfg.storage != SDMD_DENSE && cfg.storage != SDMD_SPARSE) || cfg.nranks < 1 ||
+      cfg.rank < 0 || cfg.rank >= cfg.nranks || cfg.r_max < 0 || cfg.workers < 0 ||
+      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0))
+    return SDMD_E_INVALID;
+  if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
+  if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
+
+  sdmd_ctx* c = new sdmd_ctx();
+  c->cfg = cfg;
+  if (c->cfg.rank_tol == 0.0) c->cfg.rank_tol = 1e-7;
+  int rmax = c->cfg.r_max > 0 ? c->cfg.r_max : c->cfg.m;
+  if (rmax > c->cfg.m) rmax = c->cfg.m;
+  if (rmax > SDMD_MAX_R) rmax = SDMD_MAX_R;
+  c->cfg.r_max = rmax;
+  c->W = c->cfg.workers > 0 ? c->cfg.workers : 4;
+  c->L = c->W + 1;
+  const int m = c->cfg.m;
+  c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
+  c->NH = 2 * (m + c->L + 4);
+  c->NC = c->L + 2;
+  c->es = c->cfg.dtype == SDMD_F32 ? 4 : 8;
+  c->ld = (c->cfg.n_local + kSuperTile - 1) / kSuperTile * kSuperTile;
+  c->dev = c->cfg.device;
+  auto bail = [&](int st) { sdmd_destroy(c); return st; };
+  cudaError_t e = cudaSetDevice(c->dev);
+  if (e != cudaSuccess) { c->err = cudaGetErrorString(e); delete c; return SDMD_E_CUDA; }
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->dev);
+  if (c->cfg.stream) {
+    c->stream = (cudaStream_t)c->cfg.stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+    c->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+#define AL(ptr, n)                                                   \
+  do {                                                               \
+    if (dalloc(&(ptr), (n)) != cudaSuccess) return bail(SDMD_E_OOM); \
+  } while (0)
+  if (c->cfg.storage == SDMD_DENSE) {
+    const size_t bytes = (size_t)c->NS * c->ld * c->es;
+    if (cudaMalloc(&c->ring, bytes) != cudaSuccess) return bail(SDMD_E_OOM);
+    if (cudaMemsetAsync(c->ring, 0, bytes, c->stream) != cudaSuccess) return bail(SDMD_E_CUDA);
+  } else {
+    AL(c->sp_idx, (size_t)c->NS * c->cfg.nnz_cap);
+    AL(c->sp_val, (size_t)c->NS * c->cfg.nnz_cap);
+    AL(c->sp_nnz, (size_t)c->NS);
+    AL(c->scratch, (size_t)c->cfg.n_local);
+    cudaMemsetAsync(c->scratch, 0, c->cfg.n_local * sizeof(double), c->stream);
+    cudaMemsetAsync(c->sp_nnz, 0, c->NS * sizeof(int), c->stream);
+    c->k3_chunks = (c->cfg.nnz_cap + 2047) / 2048;
+  }
+  AL(c->dst, 1);
+  cudaMemsetAsync(c->dst, 0, sizeof(DevState), c->stream);
+  AL(c->ghist, (size_t)c->NH * (m + 1));
+  cudaMemsetAsync(c->ghist, 0, (size_t)c->NH * (m + 1) * sizeof(double), c->stream);
+  AL(c->cbuf, (size_t)c->NC * m);
+  cudaMemsetAsync(c->cbuf, 0, (size_t)c->NC * m * sizeof(double2), c->stream);
+  const size_t np = (size_t)(c->nsm > 0 ? c->nsm : 148) * (kMaxM + 16);
+  const size_t np3 = (size_t)(m + 1) * c->k3_chunks;
+  AL(c->partials, np > np3 ? np : np3);
+  AL(c->gout, (size_t)(m + 1));
+  AL(c->gpart, (size_t)(m + 1));
+  AL(c->Gtmp, (size_t)(m + 1) * (m + 1));
+  if (c->cfg.background) {
+    if (cudaMalloc(&c->bg_low, c->cfg.n_local * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+    if (cudaMalloc(&c->bg_sparse, c->cfg.n_local * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+    AL(c->bg_mask, (size_t)c->cfg.n_local);
+  }
+  const int R = kMaxR;
+  for (int w = 0; w < c->W; ++w) {
+    Worker& k = c->wk[w];
+    if (cudaStreamCreateWithFlags(&k.s, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+    AL(k.A, (size_t)m * m);
+    AL(k.Gxy, (size_t)m * m);
+    AL(k.V, (size_t)m * m);
+    AL(k.sigma, (size_t)m);
+    AL(k.Y, (size_t)m * R);
+    AL(k.B, (size_t)m * R);
+    AL(k.H, (size_t)R * R);
+    AL(k.Qv, (size_t)R * R);
+    AL(k.tau, (size_t)R);
+    AL(k.alpha1, (size_t)R);
+    AL(k.M, (size_t)R * R);
+    AL(k.lam, (size_t)R);
+    AL(k.w, (size_t)R);
+    AL(k.y, (size_t)R);
+    AL(k.res, 1);
+    cudaMemsetAsync(k.res, 0, sizeof(K4Result), c->stream);
+  }
+  for (int i = 0; i < kEvents; ++i) {
+    if (cudaEventCreateWithFlags(&c->ev_commit[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_k1[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess)
+      return bail(SDMD_E_CUDA);
+  }
+  if (c->cfg.nranks > 1) {
+    NcclApi* api = nccl_api();
+    if (!api) { c->err = "libnccl.so.2 not loadable"; return bail(SDMD_E_NCCL); }
+    ncclUniqueId id;
+    std::memcpy(id.internal, c->cfg.nccl_uid, 128);
+    if (api->CommInitRank(&c->comm, c->cfg.nranks, id, c->cfg.rank) != ncclSuccess) {
+      c->err = "ncclCommInitRank failed";
+      return bail(SDMD_E_NCCL);
+    }
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(SDMD_E_CUDA);
+  *out = c;
+  return SDMD_OK;
+#undef AL
+}
+
+int sdmd_destroy(sdmd_ctx* c) {
+  if (!c) return SDMD_OK;
+  cudaSetDevice(c->dev);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (int w = 0; w < kMaxWorkers; ++w)
+    if (c->wk[w].s) cudaStreamSynchronize(c->wk[w].s);
+  if (c->comm) {
+    NcclApi* api = nccl_api();
+    if (api) api->CommDestroy(c->comm);
+  }
+  destroy_timing(c);
+  for (int i = 0; i < kEvents; ++i) {
+    if (c->ev_commit[i]) cudaEventDestroy(c->ev_commit[i]);
+    if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
+    if (c->ev_k1[i]) cudaEventDestroy(c->ev_k1[i]);
+    if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
+                  c->sp_val, c->sp_nnz, c->scratch, c->bg_low,
+                  c->bg_sparse, c->bg_mask, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
+                  c->Gtmp, c->init_work};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int w = 0; w < kMaxWorkers; ++w) {
+    Worker& k = c->wk[w];
+    void* wp[] = {k.A, k.Gxy, k.V, k.sigma, k.Y, k.B, k.H, k.Qv, k.tau, k.alpha1, k.M, k.lam, k.w,
+                  k.y, k.res};
+    for (void* p : wp)
+      if (p) cudaFree(p);
+    if (k.s) cudaStreamDestroy(k.s);
+  }
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return SDMD_OK;
+}
+
+static K4Params k4_params(sdmd_ctx* c, long long f) {
+  Worker& k = c->wk[f % c->W];
+  K4Params p{};
+  p.ghist = c->ghist; p.NH = c->NH; p.m = c->cfg.m; p.f = f; p.r_max = c->cfg.r_max;
+  p.rank_tol = c->cfg.rank_tol; p.st = c->dst;
+  p.A = k.A; p.Gxy = k.Gxy; p.V = k.V; p.sigma = k.sigma; p.Y = k.Y; p.B = k.B; p.H = k.H;
+  p.Qv = k.Qv; p.tau = k.tau; p.M = k.M; p.lam = k.lam; p.w = k.w; p.y = k.y; p.alpha1 = k.alpha1;
+  p.res = k.res;
+  p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
+  return p;
+}
+
+// Everything after the frame data sits in its slot: Gram column, reduction, DMD, events.
+static int enqueue_frame(sdmd_ctx* c, long long t) {
+  const int m = c->cfg.m;
+  const int nd = (int)(t + 1 < m + 1 ? t + 1 : m + 1);
+  const bool do_dmd = c->cfg.dmd && t >= m;
+  const bool sparse = c->cfg.storage == SDMD_SPARSE;
+  const bool bg = c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
+                  (t - c->L) <= c->last_dmd;
+  if (bg) CK(cudaStreamWaitEvent(c->stream, c->ev_done[(t - c->L) % kEvents], 0));
+  std::pair<cudaEvent_t, cudaEvent_t> tp{};
+  if (c->timing) {
+    tp = new_pair();
+    CK(cudaEventRecord(tp.first, c->stream));
+  }
+  const int do_commit = c->cfg.nranks == 1 ? 1 : 0;
+  if (!sparse) {
+    K1Params p{};
+    p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f_new = t;
+    p.nd = nd; p.bg = bg ? 1 : 0; p.f_bg = bg ? t - c->L : 0;
+    p.cbg = bg ? c->cbuf + ((t - c->L) % c->NC) * m : nullptr;
+    p.lowrank = c->bg_low; p.sparse = c->bg_sparse; p.mask = c->bg_mask; p.thr = c->cfg.threshold;
+    p.partials = c->partials; p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist;
+    p.NH = c->NH; p.st = c->dst;
+    CK(launch_k1(p, c->cfg.dtype, c->nsm, c->stream));
+    c->launches += 1;
+    if (c->timing) { CK(cudaEventRecord(tp.second, c->stream)); c->k1_ev.push_back(tp); }
+    if (c->cfg.nranks > 1) {
+      CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      NcclApi* api = nccl_api();
+      if (!api || api->AllReduce(c->gout, c->gout, nd, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
+        c->err = "ncclAllReduce failed";
+        return SDMD_E_NCCL;
+      }
+      CK(launch_commit(p, c->stream));
+      c->launches += 1;
+    }
+  } else {
+    K3Params p{};
+    p.idx = c->sp_idx; p.val = c->sp_val; p.nnz = c->sp_nnz; p.nnz_cap = c->cfg.nnz_cap;
+    p.NS = c->NS; p.m = m; p.f_new = t; p.nd = nd; p.scratch = c->scratch;
+    p.row_begin = c->cfg.row_begin; p.partials = c->partials; p.chunks = c->k3_chunks;
+    p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
+    CK(launch_k3(p, c->stream));
+    c->launches += 2;
+    if (c->timing) { CK(cudaEventRecord(tp.second, c->stream)); c->k1_ev.push_back(tp); }
+    if (c->cfg.nranks > 1) {
+      CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      NcclApi* api = nccl_api();
+      if (!api || api->AllReduce(c->gout, c->gout, nd, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
+        c->err = "ncclAllReduce failed";
+        return SDMD_E_NCCL;
+      }
+      K1Params q{};
+      q.gout = c->gout; q.nd = nd; q.m = m; q.f_new = t; q.ghist = c->ghist; q.NH = c->NH; q.st = c->dst;
+      CK(launch_commit(q, c->stream));
+      c->launches += 1;
+    }
+  }
+  c->last_nd = nd;
+  CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
+  CK(cudaEventRecord(c->ev_k1[t % kEvents], c->stream));
+  if (do_dmd) {
+    Worker& k = c->wk[t % c->W];
+    CK(cudaStreamWaitEvent(k.s, c->ev_commit[t % kEvents], 0));
+    std::pair<cudaEvent_t, cudaEvent_t> kp{};
+    if (c->timing) { kp = new_pair(); CK(cudaEventRecord(kp.first, k.s)); }
+    CK(launch_k4(k4_params(c, t), k.s));
+    c->launches += 1;
+    if (c->timing) { CK(cudaEventRecord(kp.second, k.s)); c->k4_ev.push_back(kp); }
+    CK(cudaEventRecord(c->ev_done[t % kEvents], k.s));
+    k.vecs_frame = -1;
+    c->last_dmd = t;
+  }
+  c->frames = t + 1;
+  return SDMD_OK;
+}
+
+int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
+  if (!c || !x || (where != SDMD_HOST && where != SDMD_DEVICE)) return invalid(c, "push_dense: bad argument");
+  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "push_dense on a sparse context");
+  CK(cudaSetDevice(c->dev));
+  const long long t = c->frames;
+  char* dst = (char*)c->ring + (size_t)(t % c->NS) * c->ld * c->es;
+  if (where == SDMD_HOST) {
+    // H2D on the copy stream so it overlaps K1(t-1): slot t mod NS was last read by K1(t-2)
+    if (t >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_k1[(t - 2) % kEvents], 0));
+    CK(cudaMemcpyAsync(dst, x, c->cfg.n_local * c->es, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaEventRecord(c->ev_copy[t % kEvents], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_copy[t % kEvents], 0));
+  } else {
+    CK(cudaMemcpyAsync(dst, x, c->cfg.n_local * c->es, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  return enqueue_frame(c, t);
+}
+
+int sdmd_acquire_slot(sdmd_ctx* c, void** dev_ptr) {
+  if (!c || !dev_ptr) return invalid(c, "acquire_slot: bad argument");
+  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "acquire_slot on a sparse context");
+  *dev_ptr = (char*)c->ring + (size_t)(c->frames % c->NS) * c->ld * c->es;
+  return SDMD_OK;
+}
+
+int sdmd_commit_slot(sdmd_ctx* c) {
+  if (!c) return SDMD_E_INVALID;
+  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "commit_slot on a sparse context");
+  CK(cudaSetDevice(c->dev));
+  return enqueue_frame(c, c->frames);
+}
+
+int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double* val, int where) {
+  if (!c || nnz < 0 || (nnz > 0 && (!idx || !val)) || (where != SDMD_HOST && where != SDMD_DEVICE))
+    return invalid(c, "push_sparse: bad argument");
+  if (c->cfg.storage != SDMD_SPARSE) return invalid(c, "push_sparse on a dense context");
+  if (nnz > c->cfg.nnz_cap) return invalid(c, "push_sparse: nnz > nnz_cap");
+  CK(cudaSetDevice(c->dev));
+  const long long lo = c->cfg.row_begin, hi = c->cfg.row_begin + c->cfg.n_local;
+  if (where == SDMD_HOST) {
+    for (int e = 0; e < nnz; ++e) {
+      if (idx[e] < lo || idx[e] >= hi || (e > 0 && idx[e] <= idx[e - 1]))
+        return invalid(c, "push_sparse: indices must be strictly ascending and in range");
+    }
+  }
+  const long long t = c->frames;
+  const int slot = (int)(t % c->NS);
+  int* sidx = c->sp_idx + (size_t)slot * c->cfg.nnz_cap;
+  double* sval = c->sp_val + (size_t)slot * c->cfg.nnz_cap;
+  const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), kind, c->stream));
+    CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), kind, c->stream));
+  }
+  CK(launch_set_int(c->sp_nnz + slot, nnz, c->stream));
+  c->launches += 1;
+  return enqueue_frame(c, t);
+}
+
+int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
+  if (!c || !Z || ldz < c->cfg.n_local || (where != SDMD_HOST && where != SDMD_DEVICE))
+    return invalid(c, "init_window: bad argument");
+  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "init_window needs dense storage");
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  const int m = c->cfg.m, k = m + 1;
+  // fresh state: frames 0..m occupy slots 0..m
+  CK(cudaMemsetAsync(c->dst, 0, sizeof(DevState), c->stream));
+  CK(cudaMemsetAsync(c->ghist, 0, (size_t)c->NH * (m + 1) * sizeof(double), c->stream));
+  CK(cudaMemcpy2DAsync(c->ring, c->ld * c->es, Z, (size_t)ldz * c->es, c->cfg.n_local * c->es, k,
+                       where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       c->stream));
+  const size_t need = init_gram_work_elems(c->cfg.n_local, k);
+  if (need > c->init_work_elems) {
+    if (c->init_work) cudaFree(c->init_work);
+    c->init_work = nullptr;
+    if (dalloc(&c->init_work, need) != cudaSuccess) { c->init_work_elems = 0; return SDMD_E_OOM; }
+    c->init_work_elems = need;
+  }
+  CK(launch_init_gram(c->ring, c->ld, c->cfg.dtype, c->cfg.n_local, k, c->Gtmp, c->init_work, c->stream));
+  c->launches += 2;
+  if (c->cfg.nranks > 1) {
+    NcclApi* api = nccl_api();
+    if (!api || api->AllReduce(c->Gtmp, c->Gtmp, (size_t)k * k, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
+      c->err = "ncclAllReduce (init) failed";
+      return SDMD_E_NCCL;
+    }
+  }
+  CK(launch_ghist_from_gram(c->Gtmp, k, c->ghist, c->NH, m, 0, c->stream));
+  c->launches += 1;
+  DevState hs{};
+  hs.committed = k;
+  hs.bg_frame = -1;
+  CK(cudaMemcpyAsync(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  for (int f = 0; f < k; ++f) CK(cudaEventRecord(c->ev_k1[f % kEvents], c->stream));
+  c->frames = k;
+  c->last_dmd = -1;
+  c->last_nd = k;
+  if (c->cfg.dmd) {
+    const long long t = m;
+    CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
+    Worker& w = c->wk[t % c->W];
+    CK(cudaStreamWaitEvent(w.s, c->ev_commit[t % kEvents], 0));
+    CK(launch_k4(k4_params(c, t), w.s));
+    c->launches += 1;
+    CK(cudaEventRecord(c->ev_done[t % kEvents], w.s));
+    w.vecs_frame = -1;
+    c->last_dmd = t;
+  }
+  return SDMD_OK;
+}
+
+int sdmd_join(sdmd_ctx* c) {
+  if (!c) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  if (c->last_dmd < 0) return SDMD_OK;
+  for (long long f = c->last_dmd; f > c->last_dmd - c->W && f >= c->cfg.m; --f)
+    CK(cudaStreamWaitEvent(c->stream, c->ev_done[f % kEvents], 0));
+  return SDMD_OK;
+}
+
+int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
+  if (!c) return SDMD_E_INVALID;
+  if (failed_frame) *failed_frame = -1;
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  DevState hs{};
+  CK(cudaMemcpy(&hs, c->dst, sizeof(hs), cudaMemcpyDeviceToHost));
+  if (hs.status != 0) {
+    if (failed_frame) *failed_frame = hs.failed_frame;
+    c->frames = hs.committed;
+    const int m = c->cfg.m;
+    c->last_dmd = (c->cfg.dmd && hs.committed - 1 >= m) ? hs.committed - 1 : -1;
+    hs.status = 0;
+    CK(cudaMemcpy(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    c->err = "frame " + std::to_string(hs.failed_frame) + " rejected (non-finite)";
+    return SDMD_E_NONFINITE;
+  }
+  return SDMD_OK;
+}
+
+int sdmd_get_info(sdmd_ctx* c, sdmd_info* info) {
+  if (!c || !info) return SDMD_E_INVALID;
+  info->frames = c->frames;
+  info->window = (int32_t)(c->frames < c->cfg.m + 1 ? c->frames : c->cfg.m + 1);
+  info->lag = c->L;
+  info->ring_slots = c->NS;
+  info->workers = c->W;
+  info->ring_bytes = c->cfg.storage == SDMD_DENSE ? (int64_t)c->NS * c->ld * c->es
+                                                   : (int64_t)c->NS * c->cfg.nnz_cap * 12;
+  info->ld = c->ld;
+  return SDMD_OK;
+}
+
+int sdmd_get_gram(sdmd_ctx* c, double* G, int32_t* k_out) {
+  if (!c || !G) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  const int k = (int)(c->frames < c->cfg.m + 1 ? c->frames : c->cfg.m + 1);
+  if (k_out) *k_out = k;
+  if (k == 0) return SDMD_E_STATE;
+  CK(launch_gather_gram(c->ghist, c->NH, c->cfg.m, c->frames - 1, k, c->Gtmp, c->stream));
+  c->launches += 1;
+  CK(cudaMemcpyAsync(G, c->Gtmp, (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return SDMD_OK;
+}
+
+int sdmd_get_partial_gram_column(sdmd_ctx* c, double* g, int32_t* k_out) {
+  if (!c || !g) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  if (k_out) *k_out = c->last_nd;
+  if (c->last_nd == 0) return SDMD_E_STATE;
+  CK(cudaMemcpy(g, c->cfg.nranks > 1 ? c->gpart : c->gout, c->last_nd * sizeof(double),
+                cudaMemcpyDeviceToHost));
+  return SDMD_OK;
+}
+
+static int newest_result(sdmd_ctx* c, K4Result* r) {
+  int st = sync_all(c);
+  if (st) return st;
+  if (c->last_dmd < 0) return SDMD_E_WINDOW_NOT_FULL;
+  Worker& k = c->wk[c->last_dmd % c->W];
+  CK(cudaMemcpy(r, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
+  if (r->frame != c->last_dmd) { c->err = "stale worker result"; return SDMD_E_STATE; }
+  return SDMD_OK;
+}
+
+int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* frame) {
+  if (!c) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);
+  if (st) return st;
+  Worker& k = c->wk[c->last_dmd % c->W];
+  if (r) *r = res.r;
+  if (frame) *frame = res.frame;
+  const int m = c->cfg.m;
+  if (sigma) CK(cudaMemcpy(sigma, k.sigma, m * sizeof(double), cudaMemcpyDeviceToHost));
+  if (V && res.r > 0) CK(cudaMemcpy(V, k.V, (size_t)m * res.r * sizeof(double), cudaMemcpyDeviceToHost));
+  return res.status == 6 ? SDMD_OK : (res.status > 0 ? res.status : SDMD_OK);
+}
+
+static int ensure_vecs(sdmd_ctx* c) {
+  Worker& k = c->wk[c->last_dmd % c->W];
+  if (k.vecs_frame == c->last_dmd) return SDMD_OK;
+  K4Result res{};
+  CK(cudaMemcpy(&res, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
+  const int r = res.r;
+  if (r <= 0) return SDMD_E_ZERO_MATRIX;
+  const int R = kMaxR;
+  if (!c->Wall) {
+    if (dalloc(&c->Wall, (size_t)R * R) != cudaSuccess) return SDMD_E_OOM;
+    if (dalloc(&c->ball, (size_t)R) != cudaSuccess) return SDMD_E_OOM;
+    if (dalloc(&c->Mws, (size_t)c->mws_chunk * R * R) != cudaSuccess) return SDMD_E_OOM;
+  }
+  K4VecParams p{};
+  p.r = r; p.H = k.H; p.Qv = k.Qv; p.tau = k.tau; p.lam = k.lam; p.alpha1 = k.alpha1;
+  p.Mws = c->Mws; p.W = c->Wall; p.b = c->ball;
+  for (int j0 = 0; j0 < r; j0 += c->mws_chunk) {
+    p.j0 = j0;
+    const int cnt = r - j0 < c->mws_chunk ? r - j0 : c->mws_chunk;
+    CK(launch_k4_vecs(p, cnt, c->stream));
+    c->launches += 1;
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  k.vecs_frame = c->last_dmd;
+  return SDMD_OK;
+}
+
+int sdmd_get_spectrum(sdmd_ctx* c, int32_t* r, double* lambda, double* b, int32_t* idx, int64_t* frame) {
+  if (!c) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);
+  if (st) return st;
+  Worker& k = c->wk[c->last_dmd % c->W];
+  if (r) *r = res.r;
+  if (idx) *idx = res.idx;
+  if (frame) *frame = res.frame;
+  if (lambda && res.r > 0) CK(cudaMemcpy(lambda, k.lam, res.r * sizeof(double2), cudaMemcpyDeviceToHost));
+  if (b && res.r > 0) {
+    st = ensure_vecs(c);
+    if (st) return st;
+    CK(cudaMemcpy(b, c->ball, res.r * sizeof(double2), cudaMemcpyDeviceToHost));
+  }
+  return res.status > 0 ? res.status : SDMD_OK;
+}
+
+int sdmd_get_eigvecs(sdmd_ctx* c, double* W, int32_t* r) {
+  if (!c || !W) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);
+  if (st) return st;
+  if (r) *r = res.r;
+  st = ensure_vecs(c);
+  if (st) return st;
+  CK(cudaMemcpy(W, c->Wall, (size_t)res.r * res.r * sizeof(double2), cudaMemcpyDeviceToHost));
+  return SDMD_OK;
+}
+
+int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_dev, int64_t ld) {
+  if (!c || !cols || ncols < 1 || !phi_dev || ld < c->cfg.n_local) return invalid(c, "get_modes: bad argument");
+  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "get_modes: dense storage only");
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);
+  if (st) return st;
+  for (int q = 0; q < ncols; ++q)
+    if (cols[q] < 0 || cols[q] >= res.r) return invalid(c, "get_modes: column out of range");
+  st = ensure_vecs(c);
+  if (st) return st;
+  const int m = c->cfg.m;
+  if (c->Tbuf) cudaFree(c->Tbuf);
+  if (c->colbuf) cudaFree(c->colbuf);
+  c->Tbuf = nullptr;
+  c->colbuf = nullptr;
+  if (dalloc(&c->Tbuf, (size_t)2 * m * ncols) != cudaSuccess) return SDMD_E_OOM;
+  if (dalloc(&c->colbuf, (size_t)ncols) != cudaSuccess) return SDMD_E_OOM;
+  CK(cudaMemcpy(c->colbuf, cols, ncols * sizeof(int), cudaMemcpyHostToDevice));
+  Worker& k = c->wk[c->last_dmd % c->W];
+  CK(launch_make_T(k.Y, m, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
+  // X' of the frame's window = frames last_dmd-m+1 .. last_dmd
+  CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - m + 1, m,
+                  c->Tbuf, ncols, phi_dev, ld, c->stream));
+  c->launches += 1 + (ncols + 31) / 32;
+  CK(cudaStreamSynchronize(c->stream));
+  return SDMD_OK;
+}
+
+int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
+                        int where) {
+  if (!c || (where != SDMD_HOST && where != SDMD_DEVICE && where != SDMD_HOST_ASYNC))
+    return SDMD_E_INVALID;
+  if (!c->cfg.background) return invalid(c, "background disabled in config");
+  CK(cudaSetDevice(c->dev));
+  const size_t n = c->cfg.n_local;
+  if (where == SDMD_HOST_ASYNC) {           // stream-ordered, no host wait; frame index unknown
+    if (frame) *frame = -1;
+    if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low, n * c->es, cudaMemcpyDeviceToHost, c->stream));
+    if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse, n * c->es, cudaMemcpyDeviceToHost, c->stream));
+    if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask, n, cudaMemcpyDeviceToHost, c->stream));
+    return SDMD_OK;
+  }
+  int st = sync_all(c);
+  if (st) return st;
+  DevState hs{};
+  CK(cudaMemcpy(&hs, c->dst, sizeof(hs), cudaMemcpyDeviceToHost));
+  long long bf = hs.bg_frame;
+  if (hs.committed == 0 || bf <= 0) bf = -1;
+  if (frame) *frame = bf;
+  if (bf < 0) return SDMD_E_STATE;
+  const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low, n * c->es, kind, c->stream));
+  if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse, n * c->es, kind, c->stream));
+  if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask, n, kind, c->stream));
+  if (where == SDMD_HOST) CK(cudaStreamSynchronize(c->stream));
+  return SDMD_OK;
+}
+
+int sdmd_set_timing(sdmd_ctx* c, int enable) {
+  if (!c) return SDMD_E_INVALID;
+  c->timing = enable != 0;
+  return SDMD_OK;
+}
+
+int sdmd_get_stats(sdmd_ctx* c, sdmd_stats* s, int reset) {
+  if (!c || !s) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  s->k1_launches = (int64_t)c->k1_ev.size();
+  s->k4_launches = (int64_t)c->k4_ev.size();
+  s->k1_ms = 0.0;
+  s->k4_ms = 0.0;
+  for (auto& pr : c->k1_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k1_ms += ms; }
+  for (auto& pr : c->k4_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k4_ms += ms; }
+  s->gpu_launches = c->launches;
+  if (reset) { destroy_timing(c); c->launches = 0; }
+  return SDMD_OK;
+}
+
+}  // extern "C"

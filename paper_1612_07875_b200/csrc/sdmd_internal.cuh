@@ -1,0 +1,170 @@
+// sdmd_internal.cuh — device-side data layout and kernel interfaces of libsdmd (sm_100a).
+// Layout (DESIGN.md §"Data layout in HBM"):
+//   ring   : NS slots x ld elements (fp32|fp64), slot of frame f = f mod NS, ld = n_local rounded
+//            up to 256 elements (padding rows are zero, so vector loads need no row guards)
+//   ghist  : NH x (m+1) fp64; ghist[f mod NH][k] = <x_{f-m+k}, x_f>   (the Gram column of frame f)
+//            G of the window ending at t:  G[i][j] (i<=j) = ghist[(t-m+j) mod NH][i-j+m]
+//            (the paper's "xtx[:-1,:-1] = xtx[1:,1:]" copy, Alg 1, becomes pure indexing)
+//   cbuf   : NC x m complex; background coefficients c_t = b_idx λ_idx^m V Σ⁻¹ w_idx of frame t
+//   DevState: poison status word + frame counters (device-authoritative)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sdmd {
+
+constexpr int kMaxM = 256;
+constexpr int kMaxR = 224;
+constexpr int kMaxWorkers = 8;
+constexpr int kSuperTile = 256;           // K1 rows per CTA iteration (32 lanes x 8 rows)
+
+struct DevState {
+  int status;                 // 0 = OK, else SDMD_E_NONFINITE (stream poisoned until sync)
+  int pad0;
+  long long failed_frame;     // rejected frame index
+  long long committed;        // frames committed (device authoritative)
+  long long bg_frame;         // frame index of the newest background column written
+  unsigned int k1_done;       // last-block counter of K1
+  unsigned int k3_done;       // last-block counter of K3
+  unsigned int pad1[2];
+};
+
+struct K1Params {
+  const void* ring;
+  long long ld;               // slot stride (elements)
+  int NS;                     // ring slots
+  int m;
+  long long n;                // local rows (valid rows; ld >= n)
+  long long f_new;            // frame being pushed (slot f_new % NS)
+  int nd;                     // dot columns: frames f_new-nd+1 .. f_new
+  int bg;                     // compute the background column of frame f_bg in this pass
+  long long f_bg;
+  const double2* cbg;         // m coefficients of frame f_bg (column k <-> frame f_bg-m+1+k)
+  void* lowrank;              // n (dtype)
+  void* sparse;               // n (dtype)
+  unsigned char* mask;        // n
+  float thr;
+  double* partials;           // [gridDim.x][kMaxM + 16]
+  double* gout;               // nd reduced values (pre-allreduce)
+  int do_commit;              // nranks == 1: commit inside the kernel's last block
+  double* ghist;
+  int NH;
+  DevState* st;
+};
+
+struct K4Result {
+  long long frame;
+  int status;                 // 0 OK or sdmd_status of this frame's DMD
+  int r;
+  int idx;
+  int sweeps;
+  int qr_its;
+  int pad;
+  double lam_idx[2];
+  double b_idx[2];
+  double sigma1;
+};
+
+struct K4Params {
+  const double* ghist;
+  int NH;
+  int m;
+  long long f;                // frame whose window is decomposed
+  int r_max;
+  double rank_tol;
+  DevState* st;
+  // per-worker workspace
+  double* A;                  // m*m  (one-sided Jacobi, column-major)
+  double* Gxy;                // m*m  (XᵀX', column-major)
+  double* V;                  // m*m  (eigenvectors of S, sorted, column-major)
+  double* sigma;              // m
+  double* Y;                  // m*kMaxR  V Σ⁻¹ (column-major, ld m)
+  double* B;                  // m*kMaxR  Gxy Y
+  double* H;                  // kMaxR*kMaxR row-major: Ã, then its Hessenberg form
+  double* Qv;                 // kMaxR*kMaxR row-major: Householder vector k in row k
+  double* tau;                // kMaxR
+  double2* M;                 // kMaxR*kMaxR complex row-major (inverse-iteration LU)
+  double2* lam;               // kMaxR sorted eigenvalues of Ã
+  double2* w;                 // kMaxR right eigenvector (background mode)
+  double2* y;                 // kMaxR left eigenvector
+  double* alpha1;             // kMaxR
+  K4Result* res;
+  double2* cout;              // m background coefficients (cbuf slot), zero on failure
+};
+
+// per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)
+struct K4VecParams {
+  int r;
+  const double* H;
+  const double* Qv;
+  const double* tau;
+  const double2* lam;
+  const double* alpha1;
+  double2* Mws;               // chunk x r*r complex workspace
+  double2* W;                 // r*r column-major (output)
+  double2* b;                 // r (output)
+  int j0;                     // first eigenvalue of this launch
+};
+
+struct K3Params {             // sparse Gram column
+  const int* idx;             // NS x nnz_cap
+  const double* val;          // NS x nnz_cap
+  const int* nnz;             // NS (device)
+  int nnz_cap;
+  int NS;
+  int m;
+  long long f_new;
+  int nd;
+  double* scratch;            // dense n_local fp64 scatter target (kept zero between pushes)
+  long long row_begin;
+  double* partials;           // [nd][chunks]
+  int chunks;
+  double* gout;
+  int do_commit;
+  double* ghist;
+  int NH;
+  DevState* st;
+};
+
+// Commit (Alg 1 else-branch P:293-295, rejection S:285): called by one whole block.
+static __device__ __forceinline__ void commit_block(const double* gout, int nd, int m, long long f_new, double* ghist,
+                             int NH, DevState* st) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int k = threadIdx.x; k < nd; k += blockDim.x)
+    if (!isfinite(gout[k])) bad = 1;
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f_new; }
+    return;
+  }
+  double* row = ghist + (long long)(f_new % NH) * (m + 1);
+  const int off = m + 1 - nd;
+  for (int k = threadIdx.x; k < m + 1; k += blockDim.x) row[k] = (k >= off) ? gout[k - off] : 0.0;
+  if (threadIdx.x == 0) st->committed = f_new + 1;
+}
+
+
+// kernels (defined in k1_gram.cu, k3_sparse.cu, k4_eigen.cu, k2_dmma.cu)
+cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s);
+cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
+cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
+cudaError_t launch_k4(const K4Params& p, cudaStream_t s);
+size_t k4_smem_bytes(int r_max);
+cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
+cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
+                             double* Gout, double* work, cudaStream_t s);
+size_t init_gram_work_elems(long long n, int k);
+cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long long n,
+                         long long first_frame, int m, const double* T /*m x nc complex*/,
+                         int nc, double* phi, long long ldphi, cudaStream_t s);
+cudaError_t launch_ghist_from_gram(const double* G, int k, double* ghist, int NH, int m,
+                                   long long first_frame, cudaStream_t s);
+cudaError_t launch_gather_gram(const double* ghist, int NH, int m, long long f_last, int k,
+                               double* Gout, cudaStream_t s);
+cudaError_t launch_set_int(int* p, int v, cudaStream_t s);
+cudaError_t launch_make_T(const double* Y, int m, int r, const double2* W, const int* cols,
+                          int nc, double* T, cudaStream_t s);
+
+}  // namespace sdmd

@@ -1,0 +1,375 @@
+"""Thin Python binding of libsdmd (include/sdmd.h) — argument marshalling only.
+
+Every step of the streaming SVD/DMD path runs in the CUDA library; this module only converts
+torch tensors / numpy arrays to pointers and status codes to exceptions.  There is no CPU
+fallback: if ``libsdmd.so`` is missing or no CUDA device is present, the calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsdmd.so")
+
+OK, E_INVALID, E_NONFINITE, E_WINDOW_NOT_FULL, E_ZERO_MATRIX = 0, 1, 2, 3, 4
+E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE, E_CUDA, E_NCCL, E_OOM, E_STATE = (
+    5, 6, 7, 8, 9, 10, 11)
+F32, F64 = 0, 1
+DENSE, SPARSE = 0, 1
+HOST, DEVICE, HOST_ASYNC = 0, 1, 2
+MAX_M, MAX_R = 256, 224
+
+# every symbol include/sdmd.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "sdmd_config_init", "sdmd_create", "sdmd_destroy", "sdmd_init_window", "sdmd_push_dense",
+    "sdmd_push_sparse", "sdmd_acquire_slot", "sdmd_commit_slot", "sdmd_join", "sdmd_sync",
+    "sdmd_get_info",
+    "sdmd_get_gram", "sdmd_get_partial_gram_column", "sdmd_get_svd", "sdmd_get_spectrum",
+    "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_set_timing",
+    "sdmd_get_stats", "sdmd_nccl_unique_id", "sdmd_status_string", "sdmd_last_error",
+    "sdmd_abi_version",
+]
+
+
+class Config(ctypes.Structure):
+    _fields_ = [
+        ("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("n_local", ctypes.c_int64),
+        ("m", ctypes.c_int32), ("dtype", ctypes.c_int32), ("storage", ctypes.c_int32),
+        ("nnz_cap", ctypes.c_int32), ("r_max", ctypes.c_int32), ("rank_tol", ctypes.c_double),
+        ("threshold", ctypes.c_float), ("background", ctypes.c_int32), ("dmd", ctypes.c_int32),
+        ("workers", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
+        ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
+    ]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [("frames", ctypes.c_int64), ("window", ctypes.c_int32), ("lag", ctypes.c_int32),
+                ("ring_slots", ctypes.c_int32), ("workers", ctypes.c_int32),
+                ("ring_bytes", ctypes.c_int64), ("ld", ctypes.c_int64)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("k1_launches", ctypes.c_int64), ("k1_ms", ctypes.c_double),
+                ("k4_launches", ctypes.c_int64), ("k4_ms", ctypes.c_double),
+                ("gpu_launches", ctypes.c_int64)]
+
+
+class SDMDError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        super().__init__(f"sdmd status {status} ({status_string(status)}): {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libsdmd.so (raises if it was not built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} not built — run `python -m paper_1612_07875_b200.build`; "
+                           "the streaming DMD path has no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64, dp = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+    sig = {
+        "sdmd_config_init": [ctypes.POINTER(Config)],
+        "sdmd_create": [ctypes.POINTER(Config), ctypes.POINTER(vp)],
+        "sdmd_destroy": [vp],
+        "sdmd_init_window": [vp, vp, i64, ctypes.c_int],
+        "sdmd_push_dense": [vp, vp, ctypes.c_int],
+        "sdmd_push_sparse": [vp, i32, vp, vp, ctypes.c_int],
+        "sdmd_acquire_slot": [vp, ctypes.POINTER(vp)],
+        "sdmd_commit_slot": [vp],
+        "sdmd_join": [vp],
+        "sdmd_sync": [vp, ctypes.POINTER(i64)],
+        "sdmd_get_info": [vp, ctypes.POINTER(Info)],
+        "sdmd_get_gram": [vp, dp, ctypes.POINTER(i32)],
+        "sdmd_get_partial_gram_column": [vp, dp, ctypes.POINTER(i32)],
+        "sdmd_get_svd": [vp, ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i64)],
+        "sdmd_get_spectrum": [vp, ctypes.POINTER(i32), dp, dp, ctypes.POINTER(i32),
+                              ctypes.POINTER(i64)],
+        "sdmd_get_eigvecs": [vp, dp, ctypes.POINTER(i32)],
+        "sdmd_get_modes": [vp, vp, i32, vp, i64],
+        "sdmd_get_background": [vp, vp, vp, vp, ctypes.POINTER(i64), ctypes.c_int],
+        "sdmd_set_timing": [vp, ctypes.c_int],
+        "sdmd_get_stats": [vp, ctypes.POINTER(Stats), ctypes.c_int],
+        "sdmd_nccl_unique_id": [vp],
+        "sdmd_status_string": [ctypes.c_int],
+        "sdmd_last_error": [vp],
+        "sdmd_abi_version": [],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_char_p if name in ("sdmd_status_string", "sdmd_last_error") \
+            else ctypes.c_int
+    _lib = L
+    return L
+
+
+def status_string(st: int) -> str:
+    try:
+        return lib().sdmd_status_string(st).decode()
+    except Exception:
+        return str(st)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    st = lib().sdmd_nccl_unique_id(ctypes.cast(buf, ctypes.c_void_p))
+    if st:
+        raise SDMDError(st, "nccl unique id")
+    return bytes(buf)
+
+
+def _ptr(a):
+    """(pointer, where) of a torch tensor or numpy array (no copies are made here)."""
+    if hasattr(a, "data_ptr"):
+        return ctypes.c_void_p(a.data_ptr()), (DEVICE if a.is_cuda else HOST)
+    a = np.asarray(a)
+    return ctypes.c_void_p(a.ctypes.data), HOST
+
+
+def _dp(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class StreamingDMD:
+    """Streaming method-of-snapshots SVD / DMD / background subtraction on one GPU (or one row
+    shard).  Mirrors the C ABI one-to-one; see include/sdmd.h for semantics."""
+
+    def __init__(self, n: int, m: int, dtype: str = "f32", storage: str = "dense",
+                 nnz_cap: int = 0, r_max: int = 0, rank_tol: float = 1e-7,
+                 threshold: float = 0.2, background: bool = False, dmd: bool = True,
+                 workers: int = 4, device: int = 0, stream="torch", rank: int = 0,
+                 nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
+                 nccl_uid: bytes | None = None):
+        L = lib()
+        cfg = Config()
+        L.sdmd_config_init(ctypes.byref(cfg))
+        cfg.n_local = int(n)
+        cfg.row_begin = int(row_begin)
+        cfg.n_global = int(n_global if n_global is not None else row_begin + n)
+        cfg.m = int(m)
+        cfg.dtype = F32 if dtype in ("f32", "float32") else F64
+        cfg.storage = SPARSE if storage == "sparse" else DENSE
+        cfg.nnz_cap = int(nnz_cap)
+        cfg.r_max = int(r_max)
+        cfg.rank_tol = float(rank_tol)
+        cfg.threshold = float(threshold)
+        cfg.background = 1 if background else 0
+        cfg.dmd = 1 if dmd else 0
+        cfg.workers = int(workers)
+        cfg.device = int(device)
+        if isinstance(stream, str) and stream == "torch":
+            # order library work after the caller's torch stream (device inputs are read in
+            # stream order); torch's legacy default stream (handle 0) maps to cudaStreamLegacy
+            import torch
+            s = int(torch.cuda.current_stream(int(device)).cuda_stream)
+            stream = s if s != 0 else 1
+        elif stream is not None and hasattr(stream, "cuda_stream"):
+            stream = int(stream.cuda_stream) or 1
+        cfg.stream = ctypes.c_void_p(int(stream)) if stream is not None else None
+        cfg.rank = int(rank)
+        cfg.nranks = int(nranks)
+        self._uid = None
+        if nccl_uid is not None:
+            self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)
+            cfg.nccl_uid = ctypes.cast(self._uid, ctypes.c_void_p)
+        self.cfg = cfg
+        self.n, self.m = int(n), int(m)
+        self.np_dtype = np.float32 if cfg.dtype == F32 else np.float64
+        h = ctypes.c_void_p()
+        st = L.sdmd_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st:
+            raise SDMDError(st, "sdmd_create")
+        self.h = h
+
+    # ----------------------------------------------------------------------------------
+    def _check(self, st, what, ok=(OK,)):
+        if st not in ok:
+            msg = lib().sdmd_last_error(self.h).decode() if self.h else ""
+            raise SDMDError(st, f"{what}: {msg}")
+        return st
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().sdmd_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---------------------------------------------------------------- ingest ----------
+    def init_window(self, Z, ldz: int | None = None):
+        """Z: (m+1) columns of n values, column-major (a torch (m+1, n) row-major tensor or an
+        (n, m+1) Fortran array both work; pass ldz for padded layouts)."""
+        p, where = _ptr(Z)
+        if ldz is None:
+            ldz = self.n
+        self._keep = Z
+        return self._check(lib().sdmd_init_window(self.h, p, int(ldz), where), "init_window")
+
+    def push(self, x):
+        p, where = _ptr(x)
+        self._keep = x
+        return self._check(lib().sdmd_push_dense(self.h, p, where), "push_dense")
+
+    def push_sparse(self, idx, val):
+        pi, wi = _ptr(idx)
+        pv, wv = _ptr(val)
+        self._keep = (idx, val)
+        nnz = int(idx.shape[0]) if hasattr(idx, "shape") else len(idx)
+        return self._check(lib().sdmd_push_sparse(self.h, nnz, pi, pv, wi), "push_sparse")
+
+    def acquire_slot(self) -> int:
+        p = ctypes.c_void_p()
+        self._check(lib().sdmd_acquire_slot(self.h, ctypes.byref(p)), "acquire_slot")
+        return int(p.value)
+
+    def commit_slot(self):
+        return self._check(lib().sdmd_commit_slot(self.h), "commit_slot")
+
+    def join(self):
+        """Device-side join of the eigen workers into the ctx stream (no host wait)."""
+        return self._check(lib().sdmd_join(self.h), "join")
+
+    def background_async(self, mask=None, lowrank=None, sparse=None):
+        """Stream-ordered D2H of the newest background outputs into pinned host tensors."""
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        fr = ctypes.c_int64(-1)
+        return self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
+                                                      ctypes.byref(fr), HOST_ASYNC),
+                           "get_background")
+
+    def sync(self) -> int:
+        """Wait for all work; returns -1, or raises SDMDError(E_NONFINITE) with .failed_frame."""
+        f = ctypes.c_int64(-1)
+        st = lib().sdmd_sync(self.h, ctypes.byref(f))
+        if st:
+            e = SDMDError(st, lib().sdmd_last_error(self.h).decode())
+            e.failed_frame = int(f.value)
+            raise e
+        return -1
+
+    # ---------------------------------------------------------------- getters ---------
+    def info(self) -> dict:
+        i = Info()
+        self._check(lib().sdmd_get_info(self.h, ctypes.byref(i)), "get_info")
+        return {k: getattr(i, k) for k, _ in Info._fields_}
+
+    def gram(self) -> np.ndarray:
+        k = self.m + 1
+        G = np.zeros((k, k), dtype=np.float64, order="F")
+        kk = ctypes.c_int32()
+        self._check(lib().sdmd_get_gram(self.h, _dp(G), ctypes.byref(kk)), "get_gram")
+        kk = kk.value
+        return np.asfortranarray(G.ravel(order="F")[: kk * kk].reshape((kk, kk), order="F"))
+
+    def partial_gram_column(self) -> np.ndarray:
+        g = np.zeros(self.m + 1, dtype=np.float64)
+        kk = ctypes.c_int32()
+        self._check(lib().sdmd_get_partial_gram_column(self.h, _dp(g), ctypes.byref(kk)),
+                    "get_partial_gram_column")
+        return g[: kk.value]
+
+    def svd(self, with_V: bool = True):
+        m = self.m
+        sigma = np.zeros(m, dtype=np.float64)
+        V = np.zeros((m, MAX_R), dtype=np.float64, order="F") if with_V else None
+        r = ctypes.c_int32()
+        fr = ctypes.c_int64()
+        st = lib().sdmd_get_svd(self.h, ctypes.byref(r), _dp(sigma),
+                                _dp(V) if with_V else None, ctypes.byref(fr))
+        self._check(st, "get_svd", ok=(OK, E_NO_CONVERGENCE))
+        rr = r.value
+        if with_V:
+            V = V.ravel(order="F")[: m * rr].reshape((m, rr), order="F")
+        return dict(sigma=sigma, V=V, r=rr, frame=fr.value, status=st)
+
+    def spectrum(self, with_b: bool = False) -> dict:
+        lam = np.zeros(2 * MAX_R, dtype=np.float64)
+        b = np.zeros(2 * MAX_R, dtype=np.float64) if with_b else None
+        r = ctypes.c_int32()
+        idx = ctypes.c_int32()
+        fr = ctypes.c_int64()
+        st = lib().sdmd_get_spectrum(self.h, ctypes.byref(r), _dp(lam),
+                                     _dp(b) if with_b else None, ctypes.byref(idx),
+                                     ctypes.byref(fr))
+        self._check(st, "get_spectrum", ok=(OK, E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE))
+        rr = r.value
+        out = dict(r=rr, idx=idx.value, frame=fr.value, status=st,
+                   lam=lam[: 2 * rr].view(np.complex128).copy())
+        if with_b:
+            out["b"] = b[: 2 * rr].view(np.complex128).copy()
+        return out
+
+    def eigvecs(self) -> np.ndarray:
+        W = np.zeros(2 * MAX_R * MAX_R, dtype=np.float64)
+        r = ctypes.c_int32()
+        self._check(lib().sdmd_get_eigvecs(self.h, _dp(W), ctypes.byref(r)), "get_eigvecs")
+        rr = r.value
+        return W[: 2 * rr * rr].view(np.complex128).reshape((rr, rr), order="F").copy()
+
+    def modes(self, cols, out=None):
+        """Φ[:, cols] for this rank's rows as a torch complex128 CUDA tensor (n, len(cols))."""
+        import torch
+        cols = np.ascontiguousarray(np.asarray(cols, dtype=np.int32))
+        nc = int(cols.size)
+        if out is None:
+            out = torch.empty((nc, self.n), dtype=torch.complex128,
+                              device=f"cuda:{self.cfg.device}")
+        self._check(lib().sdmd_get_modes(self.h, _dp(cols), nc, ctypes.c_void_p(out.data_ptr()),
+                                         self.n), "get_modes")
+        return out.T
+
+    def background(self):
+        """(lowrank, sparse, mask, frame) as numpy arrays (host copy)."""
+        low = np.zeros(self.n, dtype=self.np_dtype)
+        sp = np.zeros(self.n, dtype=self.np_dtype)
+        mask = np.zeros(self.n, dtype=np.uint8)
+        fr = ctypes.c_int64(-1)
+        self._check(lib().sdmd_get_background(self.h, _dp(low), _dp(sp), _dp(mask),
+                                               ctypes.byref(fr), HOST), "get_background")
+        return low, sp, mask.astype(bool), fr.value
+
+    def background_device(self, lowrank=None, sparse=None, mask=None) -> int:
+        fr = ctypes.c_int64(-1)
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
+                                               ctypes.byref(fr), DEVICE), "get_background")
+        return fr.value
+
+    def set_timing(self, on: bool = True):
+        return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")
+
+    def stats(self, reset: bool = False) -> dict:
+        s = Stats()
+        self._check(lib().sdmd_get_stats(self.h, ctypes.byref(s), 1 if reset else 0), "get_stats")
+        return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+
+def row_partition(n: int, nranks: int, rank: int, align: int = 32) -> tuple[int, int]:
+    """Contiguous row slice [begin, end) of rank ``rank``: equal shares rounded to
+    ``align``-element boundaries, the remainder on the last rank."""
+    if nranks < 1 or not (0 <= rank < nranks):
+        raise ValueError("bad rank/nranks")
+    base = n // nranks
+    base = (base // align) * align if base >= align else base
+    b = rank * base
+    e = n if rank == nranks - 1 else (rank + 1) * base
+    return b, e

@@ -1,0 +1,87 @@
+"""CPU checks of the C-ABI boundary: libsdmd.so loads and exports every symbol include/sdmd.h
+declares; host-side argument validation fails before any device work; the binding's config
+struct matches the header layout.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sdmd.h")
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_1612_07875_b200.build import build
+    return build()
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(sdmd_\w+)\s*\(", txt, re.M)))
+
+
+def test_header_declares_expected_symbols():
+    from paper_1612_07875_b200 import EXPORTS
+    assert header_symbols() == sorted(EXPORTS)
+
+
+def test_library_exports_every_header_symbol(libpath):
+    out = subprocess.run(["nm", "-D", "--defined-only", libpath], capture_output=True, text=True)
+    syms = set(re.findall(r"\sT\s(sdmd_\w+)", out.stdout))
+    missing = [s for s in header_symbols() if s not in syms]
+    assert not missing, missing
+    L = ctypes.CDLL(libpath)
+    for s in header_symbols():
+        assert getattr(L, s) is not None
+
+
+def test_sm100a_code_present(libpath):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libpath],
+                         capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_status_strings_and_version(libpath):
+    from paper_1612_07875_b200 import sdmd
+    L = sdmd.lib()
+    assert L.sdmd_abi_version() == 1
+    assert L.sdmd_status_string(2).decode() == "non-finite frame rejected"
+    assert L.sdmd_status_string(999).decode() == "unknown status"
+
+
+def test_config_layout_and_validation(libpath):
+    from paper_1612_07875_b200 import sdmd
+    L = sdmd.lib()
+    cfg = sdmd.Config()
+    assert L.sdmd_config_init(ctypes.byref(cfg)) == 0
+    assert abs(cfg.rank_tol - 1e-7) < 1e-20 and abs(cfg.threshold - 0.2) < 1e-7
+    assert cfg.dmd == 1 and cfg.workers == 4 and cfg.nranks == 1
+    assert ctypes.sizeof(sdmd.Config) == 104
+    h = ctypes.c_void_p()
+    # invalid shapes are rejected before any CUDA call (works without a GPU)
+    cfg.n_local = cfg.n_global = 100
+    cfg.m = 1
+    assert L.sdmd_create(ctypes.byref(cfg), ctypes.byref(h)) == sdmd.E_INVALID
+    cfg.m = 300
+    assert L.sdmd_create(ctypes.byref(cfg), ctypes.byref(h)) == sdmd.E_INVALID
+    cfg.m = 10
+    cfg.nranks = 2
+    cfg.nccl_uid = None
+    assert L.sdmd_create(ctypes.byref(cfg), ctypes.byref(h)) == sdmd.E_INVALID
+    assert L.sdmd_push_dense(None, None, 0) == sdmd.E_INVALID
+    assert L.sdmd_sync(None, None) == sdmd.E_INVALID
+
+
+def test_row_partition_covers_rows():
+    from paper_1612_07875_b200 import row_partition
+    for n in (24883200, 1000, 89351):
+        for P in (1, 2, 4, 8):
+            spans = [row_partition(n, P, r) for r in range(P)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c and a < b
+            if P > 1 and n >= 32 * P:
+                assert all(a % 32 == 0 for a, _ in spans)

@@ -373,3 +373,19 @@ def test_c2_wake_rank_and_lambda():
     ref = [1.0] + [np.exp(s * 1j * k * 2 * np.pi / 30) for k in range(1, 11) for s in (1, -1)]
     assert match_eigs(out["lam"], np.array(ref)) < 1e-10
     assert abs(out["lam"][out["idx"]] - 1.0) < 1e-10
+
+
+def test_oracle_init_window_equals_streamed():
+    """Alg 1 first branch (batch Gram of the first window) == warm-up appends."""
+    pm = synth.planted_c1()
+    m = 16
+    Z = pm.frames(0, m + 1)
+    a = O.StreamingDMD(m, background=False)
+    out_a = a.init_window(Z)
+    b = O.StreamingDMD(m, background=False)
+    for t in range(m + 1):
+        out_b = b.push(Z[:, t])
+    assert normwise(a.gram.G, b.gram.G) < 1e-14
+    assert match_eigs(out_a["lam"], out_b["lam"]) < 1e-12
+    x = pm.frames(m + 1, m + 2)[:, 0]
+    assert match_eigs(a.push(x)["lam"], b.push(x)["lam"]) < 1e-12
