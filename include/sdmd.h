@@ -192,6 +192,11 @@ int sdmd_get_modes(sdmd_ctx* ctx, const int32_t* cols, int32_t ncols, double* ph
 int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
                         int where);
 
+/* Diagnostics of the newest DMD frame: out[0]=frame, [1]=status, [2]=r, [3]=idx, [4]=Jacobi
+ * sweeps, [5]=QR iterations, [6..12]=SM cycles spent in the K4 phases (build S, Jacobi, sort/V,
+ * Ã, Hessenberg, QR, eigenvectors+c).  Synchronises. */
+int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[16]);
+
 /* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */
 int sdmd_set_timing(sdmd_ctx* ctx, int enable);
 int sdmd_get_stats(sdmd_ctx* ctx, sdmd_stats* stats, int reset);

@@ -18,7 +18,7 @@
 
 namespace sdmd {
 
-constexpr int K1_THREADS = 256;
+constexpr int K1_THREADS = 512;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_MAXU = kMaxM + kMaxWorkers + 8;   // union columns: m + lag (lag <= workers+1)
 constexpr int PSTRIDE = kMaxM + 16;                // partials row stride (doubles)
@@ -39,15 +39,16 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 template <typename T, bool BG>
-// (K1_THREADS, 2): <= 128 registers so an eigen-worker CTA (K4) can co-reside on the SM
-__global__ void __launch_bounds__(K1_THREADS, 2) k1_gram_kernel(const K1Params p) {
+// One 512-thread CTA per SM (<= 128 registers): 16 warps x 8 LDG.128 per lane in flight ≈ 64 KB
+// per SM.  The grid leaves `workers` SMs free for the concurrent eigen-worker CTAs (K4).
+__global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p) {
   using VT = typename VecOf<T>::type;
   constexpr int EPV = VecOf<T>::E;          // elements per 16-byte vector
   constexpr int VPL = 8 / EPV;              // vectors per lane per column (8 rows per lane)
   constexpr int CB = sizeof(T) == 4 ? 4 : 2;  // columns in flight per batch
   __shared__ double acc_s[K1_MAXU];
   __shared__ double2 c_s[BG ? kMaxM : 1];
-  __shared__ double2 red[BG ? K1_WARPS * kSuperTile : 1];
+  extern __shared__ __align__(16) double2 red[];          // BG: [K1_WARPS][kSuperTile]
   __shared__ int am_last;
 
   if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_gram_kernel(const K1Params p
         red[warp * kSuperTile + rt] = make_double2(bre[e], bim[e]);
       }
       __syncthreads();
+      if (tid < kSuperTile) {
       double2 s = make_double2(0.0, 0.0);
 #pragma unroll
       for (int w = 0; w < K1_WARPS; ++w) {
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_gram_kernel(const K1Params p
         ((T*)p.lowrank)[row] = (T)l;
         ((T*)p.sparse)[row] = (T)sp;
         p.mask[row] = (sp > (double)p.thr) ? 1 : 0;             // strict '>'
+      }
       }
       __syncthreads();
     }
@@ -182,13 +185,24 @@ __global__ void commit_kernel(const K1Params p) {
 }
 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
+  const int smem = p.bg ? (int)(K1_WARPS * kSuperTile * sizeof(double2)) : 0;
+  cudaError_t e = cudaSuccess;
   if (dtype == 0) {
-    if (p.bg) k1_gram_kernel<float, true><<<grid, K1_THREADS, 0, s>>>(p);
-    else k1_gram_kernel<float, false><<<grid, K1_THREADS, 0, s>>>(p);
+    if (p.bg) {
+      e = cudaFuncSetAttribute(k1_gram_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) k1_gram_kernel<float, true><<<grid, K1_THREADS, smem, s>>>(p);
+    } else {
+      k1_gram_kernel<float, false><<<grid, K1_THREADS, 0, s>>>(p);
+    }
   } else {
-    if (p.bg) k1_gram_kernel<double, true><<<grid, K1_THREADS, 0, s>>>(p);
-    else k1_gram_kernel<double, false><<<grid, K1_THREADS, 0, s>>>(p);
+    if (p.bg) {
+      e = cudaFuncSetAttribute(k1_gram_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) k1_gram_kernel<double, true><<<grid, K1_THREADS, smem, s>>>(p);
+    } else {
+      k1_gram_kernel<double, false><<<grid, K1_THREADS, 0, s>>>(p);
+    }
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@
 
 namespace sdmd {
 
-constexpr int K4_THREADS = 256;
+constexpr int K4_THREADS = 512;
 constexpr int K4_WARPS = K4_THREADS / 32;
 constexpr int JACOBI_MAX_SWEEPS = 60;
 constexpr int QR_MAXITS = 60;
@@ -66,21 +66,22 @@ static __device__ __forceinline__ int rr_player(int pos, int step, int mp) {
   return pos == 0 ? 0 : 1 + (pos - 1 + step) % (mp - 1);
 }
 
-// Packed upper-Hessenberg storage with 3 sub-diagonals of slack for the double-shift bulge.
+// Packed upper-Hessenberg storage with 3 sub-diagonals of slack for the double-shift bulge:
+// row i holds columns max(0, i-3) .. r-1; its offset is computed arithmetically (no lookup table).
+__host__ __device__ __forceinline__ long long hs_off(int i, int r) {
+  return i <= 4 ? (long long)i * r
+                : 4LL * r + (long long)(i - 4) * (r + 3) - ((long long)(i - 1) * i / 2 - 6);
+}
 struct HsAcc {
   double* hs;
-  const int* off;
+  int r;
   __device__ __forceinline__ double& operator()(int i, int j) const {
     const int lo = i > 3 ? i - 3 : 0;
-    return hs[off[i] + j - lo];
+    return hs[hs_off(i, r) + j - lo];
   }
 };
 
-__host__ __device__ inline long long hs_elems(int r) {
-  long long s = 0;
-  for (int i = 0; i < r; ++i) s += r - (i > 3 ? i - 3 : 0);
-  return s;
-}
+__host__ __device__ inline long long hs_elems(int r) { return hs_off(r, r); }
 
 // Eigenvalues of an upper Hessenberg matrix by the Francis double-shift QR iteration with
 // deflation on negligible sub-diagonals and ad-hoc exceptional shifts every 10 iterations
@@ -150,7 +151,10 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
             q = a(mm + 1, mm + 1) - z - r - s;
             r = a(mm + 2, mm + 1);
             s = fabs(p) + fabs(q) + fabs(r);
-            p /= s; q /= s; r /= s;
+            {
+              const double is = 1.0 / s;
+              p *= is; q *= is; r *= is;
+            }
             if (mm == l) break;
             const double u = fabs(a(mm, mm - 1)) * (fabs(q) + fabs(r));
             const double v = fabs(p) * (fabs(a(mm - 1, mm - 1)) + fabs(z) + fabs(a(mm + 1, mm + 1)));
@@ -168,7 +172,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
               q = a(k + 1, k - 1);
               r = (k != nn - 1) ? a(k + 2, k - 1) : 0.0;
               x = fabs(p) + fabs(q) + fabs(r);
-              if (x != 0.0) { p /= x; q /= x; r /= x; }
+              if (x != 0.0) { const double ix = 1.0 / x; p *= ix; q *= ix; r *= ix; }
             }
             const double s = copysign(sqrt(p * p + q * q + r * r), p);
             if (s != 0.0) {
@@ -179,14 +183,24 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
                 a(k, k - 1) = -s * x;
               }
               p += s;
-              x = p / s; y = q / s; z = r / s;
-              q /= p; r /= p;
+              {
+                const double is = 1.0 / s, ip = 1.0 / p;
+                x = p * is; y = q * is; z = r * is;
+                q *= ip; r *= ip;
+              }
               __syncwarp();
-              for (int j = k + lane; j <= nn; j += 32) {   // row modification
-                double pp = a(k, j) + q * a(k + 1, j);
-                if (k != nn - 1) { pp += r * a(k + 2, j); a(k + 2, j) -= pp * z; }
-                a(k + 1, j) -= pp * y;
-                a(k, j) -= pp * x;
+              {                                             // row modification
+                double* r0 = &a(k, 0);
+                double* r1 = &a(k + 1, 0);
+                double* r2 = &a(k + 2 <= nn ? k + 2 : k + 1, 0);
+                const bool three = (k != nn - 1);
+                for (int j = k + lane; j <= nn; j += 32) {
+                  const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
+                  const double pp = a0 + q * a1 + (three ? r * a2 : 0.0);
+                  if (three) r2[j] = a2 - pp * z;
+                  r1[j] = a1 - pp * y;
+                  r0[j] = a0 - pp * x;
+                }
               }
               __syncwarp();
               const int mmin = nn < k + 3 ? nn : k + 3;
@@ -373,102 +387,146 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
 }
 
 // ------------------------------------------------------------------ the per-frame kernel ------
-__global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params p) {
+// One thread-block cluster of K4_CLUSTER CTAs per frame (= per eigen worker).  The parallel phases
+// (Gram gather, one-sided Jacobi, sort, VΣ⁻¹, the two small GEMMs, Householder-Hessenberg) are
+// spread over all warps of the cluster with cluster barriers between dependent steps; the
+// workspace lives in global memory (L2-resident, read with ld.global.cg so that no SM sees stale
+// L1 lines).  The inherently sequential Francis QR, the eigenvector solves and the background
+// coefficients then run on CTA 0.
+constexpr int K4_CLUSTER = 4;
+constexpr int K4_GW = K4_WARPS * K4_CLUSTER;           // warps in the cluster
+constexpr int K4_GT = K4_THREADS * K4_CLUSTER;         // threads in the cluster
+
+static __device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+static __device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __cluster_dims__(K4_CLUSTER, 1, 1) __launch_bounds__(K4_THREADS, 1)
+k4_frame_kernel(const K4Params p) {
   extern __shared__ __align__(16) unsigned char k4_smem[];
   __shared__ double mu[kMaxM];
   __shared__ double sig[kMaxM];
   __shared__ int perm[kMaxM];
-  __shared__ double vbuf[kMaxR];
-  __shared__ int hoff[kMaxR + 1];
   __shared__ int sh_r, sh_status, sh_idx, sh_its;
-  __shared__ double sh_tau;
+  __shared__ long long ph[8];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int crank = (int)cl_rank();
+  const int gtid = crank * K4_THREADS + tid, gwarp = crank * K4_WARPS + warp;
   const int m = p.m;
   const long long f = p.f;
   K4Result* res = p.res;
   {
     volatile DevState* st = p.st;
-    if (st->status != 0 && st->failed_frame <= f) {   // frame discarded by the poison contract
-      if (tid == 0) { res->frame = f; res->status = -1; }
-      return;
-    }
+    // frame discarded by the poison contract (uniform across the cluster: st is read-only here)
+    if (st->status != 0 && st->failed_frame <= f) return;
   }
-  // ---- a5: S and XᵀX' from the Gram history
-  for (int idx = tid; idx < m * m; idx += K4_THREADS) {
+  if (tid == 0) ph[0] = clock64();
+  // ---- a5: S = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1] from the Gram history
+  for (int idx = gtid; idx < m * m; idx += K4_GT) {
     const int i = idx % m, j = idx / m;
     p.A[idx] = gram_at(p.ghist, p.NH, m, f, i, j);
     p.Gxy[idx] = gram_at(p.ghist, p.NH, m, f, i, j + 1);
   }
-  __syncthreads();
+  if (gtid < JACOBI_MAX_SWEEPS) p.flags[gtid] = 0;
+  cl_sync();
+  if (tid == 0) ph[1] = clock64();
 
-  // ---- a5: one-sided Jacobi, round-robin (circle) ordering of column pairs
+  // ---- a5: one-sided (Hestenes) Jacobi on S, round-robin ordering; ≤2 pairs per warp per step
   const int mp = m + (m & 1);
   const int npairs = mp / 2;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
+  constexpr int EL = kMaxM / 32;
   int sweeps = 0;
   bool converged = false;
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
     int rot = 0;
     for (int s = 0; s < mp - 1; ++s) {
-      for (int k = warp; k < npairs; k += K4_WARPS) {
-        const int pp = rr_player(k, s, mp), qq = rr_player(mp - 1 - k, s, mp);
-        if (pp >= m || qq >= m) continue;
-        double* cp = p.A + (long long)pp * m;
-        double* cq = p.A + (long long)qq * m;
-        double ap[kMaxM / 32], aq[kMaxM / 32];
-        double al = 0.0, be = 0.0, ga = 0.0;
+      for (int k0 = gwarp; k0 < npairs; k0 += 2 * K4_GW) {
+        const int k1 = k0 + K4_GW;
+        int P[2], Q[2];
+        bool act[2];
+        P[0] = rr_player(k0, s, mp); Q[0] = rr_player(mp - 1 - k0, s, mp);
+        act[0] = P[0] < m && Q[0] < m;
+        if (k1 < npairs) { P[1] = rr_player(k1, s, mp); Q[1] = rr_player(mp - 1 - k1, s, mp); act[1] = P[1] < m && Q[1] < m; }
+        else { P[1] = Q[1] = 0; act[1] = false; }
+        double ap[2][EL], aq[2][EL];
 #pragma unroll
-        for (int e = 0; e < kMaxM / 32; ++e) {
-          const int i = lane + 32 * e;
-          ap[e] = (i < m) ? cp[i] : 0.0;
-          aq[e] = (i < m) ? cq[i] : 0.0;
-          al = fma(ap[e], ap[e], al);
-          be = fma(aq[e], aq[e], be);
-          ga = fma(ap[e], aq[e], ga);
-        }
-        al = wsum(al); be = wsum(be); ga = wsum(ga);
-        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+        for (int u = 0; u < 2; ++u) {
+          const double* cp = p.A + (long long)P[u] * m;
+          const double* cq = p.A + (long long)Q[u] * m;
 #pragma unroll
-          for (int e = 0; e < kMaxM / 32; ++e) {
+          for (int e = 0; e < EL; ++e) {
             const int i = lane + 32 * e;
-            if (i < m) {
-              cp[i] = c * ap[e] - sn * aq[e];
-              cq[i] = sn * ap[e] + c * aq[e];
-            }
+            const bool ok = act[u] && i < m;
+            ap[u][e] = ok ? __ldcg(cp + i) : 0.0;
+            aq[u][e] = ok ? __ldcg(cq + i) : 0.0;
           }
-          rot = 1;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!act[u]) continue;
+          double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+          for (int e = 0; e < EL; ++e) {
+            al = fma(ap[u][e], ap[u][e], al);
+            be = fma(aq[u][e], aq[u][e], be);
+            ga = fma(ap[u][e], aq[u][e], ga);
+          }
+          al = wsum(al); be = wsum(be); ga = wsum(ga);
+          if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
+            double* cp = p.A + (long long)P[u] * m;
+            double* cq = p.A + (long long)Q[u] * m;
+#pragma unroll
+            for (int e = 0; e < EL; ++e) {
+              const int i = lane + 32 * e;
+              if (i < m) {
+                cp[i] = c * ap[u][e] - sn * aq[u][e];
+                cq[i] = sn * ap[u][e] + c * aq[u][e];
+              }
+            }
+            rot = 1;
+          }
         }
       }
-      __syncthreads();
+      cl_sync();
     }
     ++sweeps;
-    if (!__syncthreads_or(rot)) { converged = true; break; }
+    if (rot && lane == 0) atomicOr(p.flags + sweep, 1);
+    cl_sync();
+    if (*(volatile int*)(p.flags + sweep) == 0) { converged = true; break; }
   }
+  if (tid == 0) ph[2] = clock64();
 
-  // ---- a6: μ_j = ‖a_j‖ = |eig_j(S)|, sort descending, σ = sqrt(|μ|), rank, V
-  for (int j = warp; j < m; j += K4_WARPS) {
+  // ---- a6: μ_j = ‖a_j‖ = |eig_j(S)|, σ = sqrt(|μ|) sorted desc, rank r, V (sign-normalised)
+  for (int j = gwarp; j < m; j += K4_GW) {
     const double* cj = p.A + (long long)j * m;
     double s = 0.0;
-    for (int i = lane; i < m; i += 32) s = fma(cj[i], cj[i], s);
+    for (int i = lane; i < m; i += 32) { const double v = __ldcg(cj + i); s = fma(v, v, s); }
     s = wsum(s);
-    if (lane == 0) mu[j] = sqrt(s);
+    if (lane == 0) p.mu[j] = sqrt(s);
   }
+  cl_sync();
+  for (int j = tid; j < m; j += K4_THREADS) mu[j] = __ldcg(p.mu + j);
   __syncthreads();
-  for (int j = tid; j < m; j += K4_THREADS) {
-    int rank = 0;
+  for (int j = tid; j < m; j += K4_THREADS) {                // every CTA: identical permutation
+    int rk = 0;
     const double mj = mu[j];
-    for (int i = 0; i < m; ++i) rank += (mu[i] > mj || (mu[i] == mj && i < j)) ? 1 : 0;
-    perm[rank] = j;
+    for (int i = 0; i < m; ++i) rk += (mu[i] > mj || (mu[i] == mj && i < j)) ? 1 : 0;
+    perm[rk] = j;
   }
   __syncthreads();
   for (int i = tid; i < m; i += K4_THREADS) {
-    const double s = sqrt(mu[perm[i]]);
-    sig[i] = s;
-    p.sigma[i] = s;
+    sig[i] = sqrt(mu[perm[i]]);
+    if (crank == 0) p.sigma[i] = sig[i];
   }
   __syncthreads();
   if (tid == 0) {
@@ -481,23 +539,28 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
   }
   __syncthreads();
   const int r = sh_r;
-  if (sh_status == 4) {
-    for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
-    if (tid == 0) {
-      res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps;
-      res->qr_its = 0; res->sigma1 = sig[0];
+  if (sh_status == 4) {                                     // uniform across the cluster
+    if (crank == 0) {
+      for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
+      if (tid == 0) {
+        res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps;
+        res->qr_its = 0; res->sigma1 = sig[0];
+      }
     }
     return;
   }
-  for (int i = warp; i < m; i += K4_WARPS) {
+  for (int i = gwarp; i < m; i += K4_GW) {
     const int src = perm[i];
     const double inv = mu[src] > 0.0 ? 1.0 / mu[src] : 0.0;
     const double* cj = p.A + (long long)src * m;
+    double v[EL];
     double best = -1.0;
     int bi = 0;
-    for (int k = lane; k < m; k += 32) {
-      const double a = fabs(cj[k]);
-      if (a > best) { best = a; bi = k; }
+#pragma unroll
+    for (int e = 0; e < EL; ++e) {
+      const int k = lane + 32 * e;
+      v[e] = k < m ? __ldcg(cj + k) : 0.0;
+      if (k < m && fabs(v[e]) > best) { best = fabs(v[e]); bi = k; }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -505,47 +568,54 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    const double sgn = (cj[bi] < 0.0) ? -inv : inv;         // reading Q6
-    for (int k = lane; k < m; k += 32) p.V[(long long)i * m + k] = cj[k] * sgn;
+    const double sgn_src = __ldcg(cj + bi);
+    const double sgn = (sgn_src < 0.0) ? -inv : inv;        // reading Q6
+#pragma unroll
+    for (int e = 0; e < EL; ++e) {
+      const int k = lane + 32 * e;
+      if (k < m) {
+        const double vv = v[e] * sgn;
+        p.V[(long long)i * m + k] = vv;
+        if (i < r) p.Y[(long long)i * m + k] = vv / sig[i];  // Y = V Σ⁻¹ ("vsi")
+      }
+    }
+    if (lane == 0 && i < r) p.alpha1[i] = sig[i] * (v[0] * sgn);   // α₁ = σ ⊙ V[0,:] (Q3)
   }
-  __syncthreads();
+  cl_sync();
+  if (tid == 0) ph[3] = clock64();
 
-  // ---- a6/a7: Y = V Σ⁻¹, B = (XᵀX') Y, Ã = Yᵀ B  (zero n-length dots)
-  for (int idx = tid; idx < m * r; idx += K4_THREADS) {
-    const int j = idx / m;
-    p.Y[idx] = p.V[idx] / sig[j];
-  }
-  __syncthreads();
-  for (int idx = tid; idx < m * r; idx += K4_THREADS) {
+  // ---- a7: B = (XᵀX') Y (m x r), Ã = Yᵀ B (r x r, row-major into H) — zero n-length dots
+  for (int idx = gtid; idx < m * r; idx += K4_GT) {
     const int i = idx % m, j = idx / m;
     const double* yj = p.Y + (long long)j * m;
     double s = 0.0;
-    for (int k = 0; k < m; ++k) s = fma(p.Gxy[(long long)k * m + i], yj[k], s);
+    for (int k = 0; k < m; ++k) s = fma(__ldcg(p.Gxy + (long long)k * m + i), __ldcg(yj + k), s);
     p.B[idx] = s;
   }
-  __syncthreads();
-  for (int idx = tid; idx < r * r; idx += K4_THREADS) {
-    const int i = idx % r, j = idx / r;
+  cl_sync();
+  for (int idx = gwarp; idx < r * r; idx += K4_GW) {         // warp per entry: coalesced dots
+    const int i = idx / r, j = idx % r;
     const double* yi = p.Y + (long long)i * m;
     const double* bj = p.B + (long long)j * m;
     double s = 0.0;
-    for (int k = 0; k < m; ++k) s = fma(yi[k], bj[k], s);
-    p.H[(long long)i * r + j] = s;
+    for (int k = lane; k < m; k += 32) s = fma(__ldcg(yi + k), __ldcg(bj + k), s);
+    s = wsum(s);
+    if (lane == 0) p.H[(long long)i * r + j] = s;
   }
-  for (int j = tid; j < r; j += K4_THREADS) p.alpha1[j] = sig[j] * p.V[(long long)j * m];  // Q3
-  __syncthreads();
+  cl_sync();
+  if (tid == 0) ph[4] = clock64();
 
-  // ---- a8: Householder reduction of Ã to upper Hessenberg form (H row-major, ld r)
+  // ---- a8: Householder reduction to upper Hessenberg form, rank-1 updates spread over the cluster
   double* H = p.H;
   for (int k = 0; k < r - 2; ++k) {
     const int L = r - k - 1;
-    if (warp == 0) {
+    if (crank == 0 && warp == 0) {
       double x[kMaxR / 32];
       double s2 = 0.0, x0 = 0.0;
 #pragma unroll
       for (int e = 0; e < kMaxR / 32; ++e) {
         const int i = lane + 32 * e;
-        x[e] = (i < L) ? H[(long long)(k + 1 + i) * r + k] : 0.0;
+        x[e] = (i < L) ? __ldcg(H + (long long)(k + 1 + i) * r + k) : 0.0;
         if (i == 0) x0 = x[e];
         else s2 = fma(x[e], x[e], s2);
       }
@@ -563,72 +633,87 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
         const int i = lane + 32 * e;
         if (i < L) {
           const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? x[e] / v0 : 0.0);
-          vbuf[i] = v;
           p.Qv[(long long)k * r + k + 1 + i] = v;
           H[(long long)(k + 1 + i) * r + k] = (i == 0) ? beta : 0.0;
         }
       }
-      if (lane == 0) { p.tau[k] = tauk; sh_tau = tauk; }
+      if (lane == 0) p.tau[k] = tauk;
     }
-    __syncthreads();
-    const double tk = sh_tau;
+    cl_sync();
+    const double tk = __ldcg(p.tau + k);
     if (tk != 0.0) {
-      for (int j = k + 1 + tid; j < r; j += K4_THREADS) {          // left: (I - τvvᵀ) H
+      const double* v = p.Qv + (long long)k * r + k + 1;
+      // w_j = Σ_i v_i H[k+1+i][j], j = k+1..r-1 (warp per column)
+      for (int j = k + 1 + gwarp; j < r; j += K4_GW) {
         double s = 0.0;
-        for (int i = 0; i < L; ++i) s = fma(vbuf[i], H[(long long)(k + 1 + i) * r + j], s);
-        s *= tk;
-        for (int i = 0; i < L; ++i) H[(long long)(k + 1 + i) * r + j] -= s * vbuf[i];
+        for (int i = lane; i < L; i += 32) s = fma(__ldcg(v + i), __ldcg(H + (long long)(k + 1 + i) * r + j), s);
+        s = wsum(s);
+        if (lane == 0) p.wv[j] = s * tk;
       }
-      __syncthreads();
-      for (int i = warp; i < r; i += K4_WARPS) {                   // right: H (I - τvvᵀ)
-        double* hi = H + (long long)i * r + k + 1;
+      cl_sync();
+      for (int e = gtid; e < L * L; e += K4_GT) {            // H[k+1+i][k+1+jj] -= v_i w_j
+        const int i = e / L, jj = e % L;
+        const long long o = (long long)(k + 1 + i) * r + k + 1 + jj;
+        H[o] = __ldcg(H + o) - __ldcg(v + i) * __ldcg(p.wv + k + 1 + jj);
+      }
+      cl_sync();
+      // u_i = τ Σ_jj H[i][k+1+jj] v_jj, all rows (warp per row)
+      for (int i = gwarp; i < r; i += K4_GW) {
+        const double* hi = H + (long long)i * r + k + 1;
         double s = 0.0;
-        for (int jj = lane; jj < L; jj += 32) s = fma(hi[jj], vbuf[jj], s);
-        s = wsum(s) * tk;
-        for (int jj = lane; jj < L; jj += 32) hi[jj] -= s * vbuf[jj];
+        for (int jj = lane; jj < L; jj += 32) s = fma(__ldcg(hi + jj), __ldcg(v + jj), s);
+        s = wsum(s);
+        if (lane == 0) p.uv[i] = s * tk;
       }
+      cl_sync();
+      for (int e = gtid; e < r * L; e += K4_GT) {            // H[i][k+1+jj] -= u_i v_jj
+        const int i = e / L, jj = e % L;
+        const long long o = (long long)i * r + k + 1 + jj;
+        H[o] = __ldcg(H + o) - __ldcg(p.uv + i) * __ldcg(v + jj);
+      }
+      cl_sync();
     }
-    __syncthreads();
   }
-  if (r >= 2 && tid == 0) p.tau[r - 2] = 0.0;
-  if (tid == 0) { p.tau[r > 0 ? r - 1 : 0] = 0.0; }
+  if (crank != 0) return;                                   // the rest runs on CTA 0
+  if (tid == 0) {
+    if (r >= 2) p.tau[r - 2] = 0.0;
+    p.tau[r > 0 ? r - 1 : 0] = 0.0;
+    ph[5] = clock64();
+  }
 
   // ---- a8: eigenvalues by Francis double-shift QR in shared memory (warp 0)
   double* hs = reinterpret_cast<double*>(k4_smem);
   const long long hsz = hs_elems(r);
   double2* lam_raw = reinterpret_cast<double2*>(hs + ((hsz + 1) & ~1LL));
-  if (tid == 0) {
-    int o = 0;
-    for (int i = 0; i < r; ++i) { hoff[i] = o; o += r - (i > 3 ? i - 3 : 0); }
-    hoff[r] = o;
-  }
-  __syncthreads();
   for (int i = warp; i < r; i += K4_WARPS) {
     const int lo = i > 3 ? i - 3 : 0;
+    const long long o = hs_off(i, r);
     for (int j = lo + lane; j < r; j += 32)
-      hs[hoff[i] + j - lo] = (j >= i - 1) ? H[(long long)i * r + j] : 0.0;
+      hs[o + j - lo] = (j >= i - 1) ? __ldcg(H + (long long)i * r + j) : 0.0;
   }
+  for (int i = tid; i < r; i += K4_THREADS) lam_raw[i] = make_double2(0.0, 0.0);
   __syncthreads();
   if (warp == 0) {
     int its = 0;
-    const int rc = hessenberg_qr(HsAcc{hs, hoff}, r, lam_raw, lane, &its);
+    const int rc = hessenberg_qr(HsAcc{hs, r}, r, lam_raw, lane, &its);
     if (lane == 0) { sh_its = its; if (rc != 0) sh_status = 5; }
   }
   __syncthreads();
+  if (tid == 0) ph[6] = clock64();
 
   // ---- sort λ: |λ| desc, Re desc, Im desc (reading Q12)
   for (int j = tid; j < r; j += K4_THREADS) {
     const double2 lj = lam_raw[j];
     const double aj = hypot(lj.x, lj.y);
-    int rank = 0;
+    int rk = 0;
     for (int i = 0; i < r; ++i) {
       const double2 li = lam_raw[i];
       const double ai = hypot(li.x, li.y);
       const bool before = (ai > aj) || (ai == aj && (li.x > lj.x || (li.x == lj.x && (li.y > lj.y ||
                           (li.y == lj.y && i < j)))));
-      rank += before ? 1 : 0;
+      rk += before ? 1 : 0;
     }
-    p.lam[rank] = lj;
+    p.lam[rk] = lj;
   }
   __syncthreads();
 
@@ -653,8 +738,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
   __syncthreads();
   const int idx = sh_idx;
 
-  // ---- a8/a9: eigenvectors of the background mode, b_idx, and c (warp 0)
-  // scratch aliases the (now free) packed Hessenberg area
+  // ---- a8/a9: eigenvectors of the background mode, b_idx, and c (warp 0); scratch aliases the
+  // (now free) packed Hessenberg area
   double2* z = reinterpret_cast<double2*>(k4_smem);
   double2* rhs = z + kMaxR;
   double2* lk = rhs + kMaxR;
@@ -662,7 +747,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
   if (idx >= 0 && warp == 0) {
     const double2 lam = p.lam[idx];
     inverse_iteration(H, p.Qv, p.tau, r, lam, p.M, z, rhs, lk, swk, p.w, p.y, lane);
-    // b_idx = yᴴα₁ / (λ yᴴw)
     double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
     for (int i = lane; i < r; i += 32) {
       const double2 yc = cconj(p.y[i]);
@@ -676,8 +760,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
     int st = sh_status;
     if (cabs2(den) > 1e-300) b = cdiv(ya, den);
     else if (st == 0) st = 6;
-    // λ^m by binary powering
-    double2 pw = make_double2(1.0, 0.0), base = lam;
+    double2 pw = make_double2(1.0, 0.0), base = lam;       // λ^m by binary powering
     for (int e = m; e > 0; e >>= 1) {
       if (e & 1) pw = cmul(pw, base);
       base = cmul(base, base);
@@ -692,6 +775,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4_frame_kernel(const K4Params 
       p.cout[i] = cmul(coef, s);
     }
     if (lane == 0) {
+      ph[7] = clock64();
+      for (int q = 0; q < 8; ++q) res->phase[q] = ph[q];
       res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
       res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sig[0];
@@ -717,9 +802,11 @@ cudaError_t launch_k4(const K4Params& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k4_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  k4_frame_kernel<<<1, K4_THREADS, smem, s>>>(p);
+  k4_frame_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
+
+int k4_cluster_size() { return K4_CLUSTER; }
 
 // ------------------------------------------------------- on-demand eigenvectors and b --------
 __global__ void __launch_bounds__(32) k4_vecs_kernel(const K4VecParams p) {

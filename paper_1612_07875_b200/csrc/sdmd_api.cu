@@ -56,6 +56,8 @@ struct Worker {
   double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
   double2 *M = nullptr, *lam = nullptr, *w = nullptr, *y = nullptr;
   K4Result* res = nullptr;
+  int* flags = nullptr;
+  double *mu = nullptr, *wv = nullptr, *uv = nullptr;
   long long vecs_frame = -1;            // frame whose full W/b are cached in Wall/ball
 };
 
@@ -66,7 +68,8 @@ struct sdmd_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148;
+  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148;
+  bool k1_ldg = false;                  // SDMD_K1=ldg selects the register-streaming K1 (A/B)
   long long ld = 0;
   size_t es = 4;
   void* ring = nullptr;
@@ -241,6 +244,13 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   cudaError_t e = cudaSetDevice(c->dev);
   if (e != cudaSuccess) { c->err = cudaGetErrorString(e); delete c; return SDMD_E_CUDA; }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->dev);
+  // persistent K1 grid: one CTA per SM, leaving one SM per eigen worker (K4 runs concurrently)
+  c->k1_grid = c->cfg.dmd ? c->nsm - c->W * k4_cluster_size() : c->nsm;
+  {
+    const char* ev = std::getenv("SDMD_K1");
+    c->k1_ldg = ev && std::strcmp(ev, "ldg") == 0;
+  }
+  if (c->k1_grid < 1) c->k1_grid = 1;
   if (c->cfg.stream) {
     c->stream = (cudaStream_t)c->cfg.stream;
   } else {
@@ -301,6 +311,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(k.w, (size_t)R);
     AL(k.y, (size_t)R);
     AL(k.res, 1);
+    AL(k.flags, 64);
+    AL(k.mu, (size_t)kMaxM);
+    AL(k.wv, (size_t)R);
+    AL(k.uv, (size_t)R);
     cudaMemsetAsync(k.res, 0, sizeof(K4Result), c->stream);
   }
   for (int i = 0; i < kEvents; ++i) {
@@ -353,7 +367,7 @@ int sdmd_destroy(sdmd_ctx* c) {
   for (int w = 0; w < kMaxWorkers; ++w) {
     Worker& k = c->wk[w];
     void* wp[] = {k.A, k.Gxy, k.V, k.sigma, k.Y, k.B, k.H, k.Qv, k.tau, k.alpha1, k.M, k.lam, k.w,
-                  k.y, k.res};
+                  k.y, k.res, k.flags, k.mu, k.wv, k.uv};
     for (void* p : wp)
       if (p) cudaFree(p);
     if (k.s) cudaStreamDestroy(k.s);
@@ -372,6 +386,7 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.Qv = k.Qv; p.tau = k.tau; p.M = k.M; p.lam = k.lam; p.w = k.w; p.y = k.y; p.alpha1 = k.alpha1;
   p.res = k.res;
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
+  p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
   return p;
 }
 
@@ -398,7 +413,8 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.lowrank = c->bg_low; p.sparse = c->bg_sparse; p.mask = c->bg_mask; p.thr = c->cfg.threshold;
     p.partials = c->partials; p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist;
     p.NH = c->NH; p.st = c->dst;
-    CK(launch_k1(p, c->cfg.dtype, c->nsm, c->stream));
+    if (c->k1_ldg) CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));
+    else CK(launch_k1_tma(p, c->cfg.dtype, c->k1_grid, c->stream));
     c->launches += 1;
     if (c->timing) { CK(cudaEventRecord(tp.second, c->stream)); c->k1_ev.push_back(tp); }
     if (c->cfg.nranks > 1) {
@@ -776,6 +792,19 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse, n * c->es, kind, c->stream));
   if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask, n, kind, c->stream));
   if (where == SDMD_HOST) CK(cudaStreamSynchronize(c->stream));
+  return SDMD_OK;
+}
+
+int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[16]) {
+  if (!c || !out) return SDMD_E_INVALID;
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);
+  if (st) return st;
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  out[0] = res.frame; out[1] = res.status; out[2] = res.r; out[3] = res.idx;
+  out[4] = res.sweeps; out[5] = res.qr_its;
+  for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q + 1] - res.phase[q];
   return SDMD_OK;
 }
 

@@ -63,6 +63,7 @@ struct K4Result {
   double lam_idx[2];
   double b_idx[2];
   double sigma1;
+  long long phase[8];         // clock64() at phase boundaries (diagnostics)
 };
 
 struct K4Params {
@@ -90,6 +91,10 @@ struct K4Params {
   double* alpha1;             // kMaxR
   K4Result* res;
   double2* cout;              // m background coefficients (cbuf slot), zero on failure
+  int* flags;                 // per-sweep "rotated" flags (cluster-wide OR)
+  double* mu;                 // m column norms
+  double* wv;                 // kMaxR Householder scratch
+  double* uv;                 // kMaxR Householder scratch
 };
 
 // per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)
@@ -148,10 +153,13 @@ static __device__ __forceinline__ void commit_block(const double* gout, int nd, 
 
 // kernels (defined in k1_gram.cu, k3_sparse.cu, k4_eigen.cu, k2_dmma.cu)
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s);
+cudaError_t launch_k1_tma(const K1Params& p, int dtype, int grid, cudaStream_t s);
+size_t k1_tma_smem_bytes(int dtype, int bg);
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_k4(const K4Params& p, cudaStream_t s);
 size_t k4_smem_bytes(int r_max);
+int k4_cluster_size();
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
 cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
                              double* Gout, double* work, cudaStream_t s);

@@ -28,7 +28,8 @@ EXPORTS = [
     "sdmd_push_sparse", "sdmd_acquire_slot", "sdmd_commit_slot", "sdmd_join", "sdmd_sync",
     "sdmd_get_info",
     "sdmd_get_gram", "sdmd_get_partial_gram_column", "sdmd_get_svd", "sdmd_get_spectrum",
-    "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_set_timing",
+    "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_get_frame_diag",
+    "sdmd_set_timing",
     "sdmd_get_stats", "sdmd_nccl_unique_id", "sdmd_status_string", "sdmd_last_error",
     "sdmd_abi_version",
 ]
@@ -96,6 +97,7 @@ def lib():
         "sdmd_get_eigvecs": [vp, dp, ctypes.POINTER(i32)],
         "sdmd_get_modes": [vp, vp, i32, vp, i64],
         "sdmd_get_background": [vp, vp, vp, vp, ctypes.POINTER(i64), ctypes.c_int],
+        "sdmd_get_frame_diag": [vp, dp],
         "sdmd_set_timing": [vp, ctypes.c_int],
         "sdmd_get_stats": [vp, ctypes.POINTER(Stats), ctypes.c_int],
         "sdmd_nccl_unique_id": [vp],
@@ -353,6 +355,14 @@ class StreamingDMD:
         self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
                                                ctypes.byref(fr), DEVICE), "get_background")
         return fr.value
+
+    def frame_diag(self) -> dict:
+        o = np.zeros(16, dtype=np.int64)
+        self._check(lib().sdmd_get_frame_diag(self.h, _dp(o)), "get_frame_diag")
+        names = ["build_S", "jacobi", "sort_V", "atilde", "hessenberg", "qr", "eigvec_c"]
+        return dict(frame=int(o[0]), status=int(o[1]), r=int(o[2]), idx=int(o[3]),
+                    sweeps=int(o[4]), qr_its=int(o[5]),
+                    cycles={k: int(v) for k, v in zip(names, o[6:13])})
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")

@@ -369,3 +369,30 @@ def test_c4_full_size_sampled():
     tp = np.sum(mask & gt)
     assert 2 * tp / (mask.sum() + gt.sum()) > 0.85
     eng.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_k1_tma_and_ldg_variants_agree(dtype, monkeypatch):
+    """The TMA-pipelined K1 (default) and the register-streaming K1 (SDMD_K1=ldg) compute the
+    same Gram columns and background (different fixed summation orders)."""
+    vs = synth.video_config("C3s")
+    m, T = 24, 40
+    npdt = np.float32 if dtype == "f32" else np.float64
+    frames = vs.frames(0, T).numpy().astype(npdt)
+    Xd = dev_cols(frames, npdt)
+    outs = []
+    for mode in ("tma", "ldg"):
+        if mode == "ldg":
+            monkeypatch.setenv("SDMD_K1", "ldg")
+        else:
+            monkeypatch.delenv("SDMD_K1", raising=False)
+        eng = Eng(vs.n, m, dtype=dtype, background=True, workers=2)
+        for t in range(T):
+            eng.push(Xd[t])
+        eng.sync()
+        outs.append((eng.gram(), eng.background()))
+        eng.close()
+    assert normwise(outs[0][0], outs[1][0]) < 1e-14
+    la, lb = outs[0][1][0].astype(np.float64), outs[1][1][0].astype(np.float64)
+    assert np.max(np.abs(la - lb)) < 1e-5 * np.max(np.abs(lb))
+    assert outs[0][1][3] == outs[1][1][3]
