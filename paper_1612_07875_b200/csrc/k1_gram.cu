@@ -14,6 +14,8 @@
 // dots are warp-reduced per tile into shared memory (deterministic order), written per CTA, and
 // the last CTA to finish reduces the CTA partials in fixed order and commits the column into the
 // Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
+#include <type_traits>
+
 #include "sdmd_internal.cuh"
 
 namespace sdmd {
@@ -40,15 +42,20 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 template <typename T, bool BG>
 // One 512-thread CTA per SM (<= 128 registers): 16 warps x 8 LDG.128 per lane in flight ≈ 64 KB
-// per SM.  The grid leaves `workers` SMs free for the concurrent eigen-worker CTAs (K4).
+// per SM.  The grid leaves the eigen-worker SMs free (K4 runs concurrently on its own SMs).
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p) {
   using VT = typename VecOf<T>::type;
   constexpr int EPV = VecOf<T>::E;          // elements per 16-byte vector
   constexpr int VPL = 8 / EPV;              // vectors per lane per column (8 rows per lane)
-  constexpr int CB = sizeof(T) == 4 ? 4 : 2;  // columns in flight per batch
-  __shared__ double acc_s[K1_MAXU];
-  __shared__ double2 c_s[BG ? kMaxM : 1];
-  extern __shared__ __align__(16) double2 red[];          // BG: [K1_WARPS][kSuperTile]
+  constexpr int CB = sizeof(T) == 4 ? 4 : (BG ? 1 : 2);  // columns in flight per batch
+  constexpr int MAXQ = (K1_MAXU + K1_WARPS - 1) / K1_WARPS;
+  // background partials: fp32 for fp32 storage (per-warp sums of ~m/16 terms, then an fp64
+  // cross-warp sum; error ~1e-6 relative, inside the fp32-path tolerance), fp64 for fp64 storage
+  using BT = T;
+  using BT2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+  __shared__ BT2 c_s[BG ? kMaxM : 1];
+  extern __shared__ __align__(16) unsigned char red_raw[];  // BG: 2 x [K1_WARPS][kSuperTile] BT2
+  BT2* red = reinterpret_cast<BT2*>(red_raw);
   __shared__ int am_last;
 
   if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
@@ -57,15 +64,24 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   const long long f_bg0 = p.f_bg - p.m + 1;         // first column of X'_{f_bg}
   const long long F0 = BG ? (f_dot0 < f_bg0 ? f_dot0 : f_bg0) : f_dot0;
   const int U = (int)(p.f_new - F0 + 1);
-  for (int j = tid; j < U; j += K1_THREADS) acc_s[j] = 0.0;
   if (BG)
-    for (int k = tid; k < p.m; k += K1_THREADS) c_s[k] = p.cbg[k];
+    for (int k = tid; k < p.m; k += K1_THREADS) {
+      const double2 c = p.cbg[k];
+      c_s[k].x = (BT)c.x;
+      c_s[k].y = (BT)c.y;
+    }
   __syncthreads();
 
   const int cnt = (U > warp) ? (U - warp + K1_WARPS - 1) / K1_WARPS : 0;
   const T* __restrict__ ring = (const T*)p.ring;
   const long long NT = p.ld / kSuperTile;
   const T* xslot = ring + (p.f_new % p.NS) * p.ld;
+
+  // per-lane fp64 partial dots of this warp's columns, kept in registers for the whole pass
+  double accv[MAXQ];
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) accv[q] = 0.0;
+  int buf = 0;
 
   for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x) {
     const long long row0 = tile * kSuperTile;
@@ -75,47 +91,53 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
       to_double(xv, xd + v * EPV);
     }
-    double bre[8], bim[8];
+    BT bre[BG ? 8 : 1], bim[BG ? 8 : 1];
+    // prefetch this tile's x_{f_bg} row for the reduction step (its latency hides behind the
+    // column stream instead of stalling the whole CTA after the barrier)
+    T xbg = (T)0;
+    if (BG && tid < kSuperTile) xbg = __ldcs(ring + (p.f_bg % p.NS) * p.ld + row0 + tid);
     if (BG) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) { bre[e] = 0.0; bim[e] = 0.0; }
+      for (int e = 0; e < 8; ++e) { bre[e] = (BT)0; bim[e] = (BT)0; }
     }
-    for (int q0 = 0; q0 < cnt; q0 += CB) {
-      VT z[CB][VPL];
 #pragma unroll
-      for (int b = 0; b < CB; ++b) {
-        const int q = q0 + b;
-        if (q < cnt) {
-          const long long f = F0 + warp + K1_WARPS * q;
-          const VT* zp = reinterpret_cast<const VT*>(ring + (f % p.NS) * p.ld + row0);
+    for (int q0 = 0; q0 < MAXQ; q0 += CB) {
+      if (q0 < cnt) {
+        VT z[CB][VPL];
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
-        }
-      }
+        for (int b = 0; b < CB; ++b) {
+          const int q = q0 + b;
+          if (q < MAXQ && q < cnt) {
+            const long long f = F0 + warp + K1_WARPS * q;
+            const VT* zp = reinterpret_cast<const VT*>(ring + (f % p.NS) * p.ld + row0);
 #pragma unroll
-      for (int b = 0; b < CB; ++b) {
-        const int q = q0 + b;
-        if (q < cnt) {
-          const int j = warp + K1_WARPS * q;
-          const long long f = F0 + j;
-          double zd[8];
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
-          if (f >= f_dot0) {
-            double s = 0.0;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) s = fma(xd[e], zd[e], s);
-            s = warp_sum(s);
-            if (lane == 0) acc_s[j] += s;
+            for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
           }
-          if (BG) {
-            const long long kb = f - f_bg0;
-            if (kb >= 0 && kb < p.m) {
-              const double2 c = c_s[kb];
+        }
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                bre[e] = fma(c.x, zd[e], bre[e]);
-                bim[e] = fma(c.y, zd[e], bim[e]);
+        for (int b = 0; b < CB; ++b) {
+          const int q = q0 + b;
+          if (q < MAXQ && q < cnt) {
+            const long long f = F0 + warp + K1_WARPS * q;
+            double zd[8];
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
+            if (f >= f_dot0) {
+              double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
+              accv[q] += s0 + s1;
+            }
+            if (BG) {
+              const long long kb = f - f_bg0;
+              if (kb >= 0 && kb < p.m) {
+                const BT2 c = c_s[kb];
+                const T* zr = reinterpret_cast<const T*>(&z[b][0]);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  bre[e] = fma(c.x, (BT)zr[e], bre[e]);
+                  bim[e] = fma(c.y, (BT)zr[e], bim[e]);
+                }
               }
             }
           }
@@ -123,37 +145,42 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       }
     }
     if (BG) {
+      BT2* rb = red + buf * (K1_WARPS * kSuperTile);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int rt = (e / EPV) * (32 * EPV) + lane * EPV + (e % EPV);
-        red[warp * kSuperTile + rt] = make_double2(bre[e], bim[e]);
+        BT2 v;
+        v.x = bre[e];
+        v.y = bim[e];
+        rb[warp * kSuperTile + rt] = v;
       }
-      __syncthreads();
+      __syncthreads();                     // one barrier per tile (double-buffered partials)
       if (tid < kSuperTile) {
-      double2 s = make_double2(0.0, 0.0);
+        double sx = 0.0, sy = 0.0;
 #pragma unroll
-      for (int w = 0; w < K1_WARPS; ++w) {
-        const double2 v = red[w * kSuperTile + tid];
-        s.x += v.x; s.y += v.y;
+        for (int w = 0; w < K1_WARPS; ++w) { const BT2 v = rb[w * kSuperTile + tid]; sx += (double)v.x; sy += (double)v.y; }
+        const long long row = row0 + tid;
+        if (row < p.n) {
+          const double l = sqrt(sx * sx + sy * sy);               // |l| (Q8)
+          const double xv = (double)xbg;
+          const double sp = xv - l;                               // s = x - |l|
+          ((T*)p.lowrank)[row] = (T)l;
+          ((T*)p.sparse)[row] = (T)sp;
+          p.mask[row] = (sp > (double)p.thr) ? 1 : 0;             // strict '>'
+        }
       }
-      const long long row = row0 + tid;
-      if (row < p.n) {
-        const double l = hypot(s.x, s.y);                       // |l| (Q8)
-        const double xv = (double)ring[(p.f_bg % p.NS) * p.ld + row];
-        const double sp = xv - l;                               // s = x - |l|
-        ((T*)p.lowrank)[row] = (T)l;
-        ((T*)p.sparse)[row] = (T)sp;
-        p.mask[row] = (sp > (double)p.thr) ? 1 : 0;             // strict '>'
-      }
-      }
-      __syncthreads();
+      buf ^= 1;
     }
   }
 
-  __syncthreads();
-  for (int j = tid; j < U; j += K1_THREADS) {
-    const long long f = F0 + j;
-    if (f >= f_dot0) p.partials[(long long)blockIdx.x * PSTRIDE + (f - f_dot0)] = acc_s[j];
+  // per-column warp reduction of the lane partials (fixed order) -> this CTA's partials
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    if (q < cnt) {
+      const long long f = F0 + warp + K1_WARPS * q;
+      const double s = warp_sum(accv[q]);
+      if (lane == 0 && f >= f_dot0) p.partials[(long long)blockIdx.x * PSTRIDE + (f - f_dot0)] = s;
+    }
   }
   __threadfence();
   __syncthreads();
@@ -185,7 +212,7 @@ __global__ void commit_kernel(const K1Params p) {
 }
 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
-  const int smem = p.bg ? (int)(K1_WARPS * kSuperTile * sizeof(double2)) : 0;
+  const int smem = p.bg ? (int)(2 * K1_WARPS * kSuperTile * (dtype == 0 ? sizeof(float2) : sizeof(double2))) : 0;
   cudaError_t e = cudaSuccess;
   if (dtype == 0) {
     if (p.bg) {

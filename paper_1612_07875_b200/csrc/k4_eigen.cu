@@ -89,7 +89,9 @@ __host__ __device__ inline long long hs_elems(int r) { return hs_off(r, r); }
 // runs the scalar recurrences redundantly on identical shared-memory data; lanes split the row
 // and column updates of each 3x3 reflector.  Returns 0, or -1 when an eigenvalue needs more than
 // QR_MAXITS iterations.
-static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* total_its) {
+static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* total_its,
+                                    int* cnt) {
+  int c_steps = 0, c_scan = 0, c_mscan = 0;
   double an = 0.0;
   for (int i = 0; i < n; ++i)
     for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(a(i, j));
@@ -100,6 +102,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
     int its = 0, l;
     do {
       for (l = nn; l >= 1; --l) {
+        ++c_scan;
         double s = fabs(a(l - 1, l - 1)) + fabs(a(l, l));
         if (s == 0.0) s = an;
         if (fabs(a(l, l - 1)) + s == s) {
@@ -144,6 +147,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
           int mm;
           double p = 0.0, q = 0.0, r = 0.0, z = 0.0;
           for (mm = nn - 2; mm >= l; --mm) {           // two small consecutive sub-diagonals?
+            ++c_mscan;
             z = a(mm, mm);
             r = x - z;
             double s = y - z;
@@ -167,6 +171,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
           }
           __syncwarp();
           for (int k = mm; k <= nn - 1; ++k) {          // chase the bulge
+            ++c_steps;
             if (k != mm) {
               p = a(k, k - 1);
               q = a(k + 1, k - 1);
@@ -218,6 +223,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
     } while (l < nn - 1);
   }
   *total_its = tot;
+  if (cnt) { cnt[0] = c_steps; cnt[1] = c_scan; cnt[2] = c_mscan; }
   return 0;
 }
 
@@ -695,8 +701,13 @@ k4_frame_kernel(const K4Params p) {
   __syncthreads();
   if (warp == 0) {
     int its = 0;
-    const int rc = hessenberg_qr(HsAcc{hs, r}, r, lam_raw, lane, &its);
-    if (lane == 0) { sh_its = its; if (rc != 0) sh_status = 5; }
+    int qc[3] = {0, 0, 0};
+    const int rc = hessenberg_qr(HsAcc{hs, r}, r, lam_raw, lane, &its, qc);
+    if (lane == 0) {
+      sh_its = its;
+      if (rc != 0) sh_status = 5;
+      res->qr_cnt[0] = qc[0]; res->qr_cnt[1] = qc[1]; res->qr_cnt[2] = qc[2];
+    }
   }
   __syncthreads();
   if (tid == 0) ph[6] = clock64();

@@ -69,7 +69,8 @@ struct sdmd_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148;
-  bool k1_ldg = false;                  // SDMD_K1=ldg selects the register-streaming K1 (A/B)
+  bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
+  bool k1_ldg = true;                   // SDMD_K1=tma selects the bulk-copy (TMA) K1 variant (A/B)
   long long ld = 0;
   size_t es = 4;
   void* ring = nullptr;
@@ -248,7 +249,9 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   c->k1_grid = c->cfg.dmd ? c->nsm - c->W * k4_cluster_size() : c->nsm;
   {
     const char* ev = std::getenv("SDMD_K1");
-    c->k1_ldg = ev && std::strcmp(ev, "ldg") == 0;
+    c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
+    const char* eb = std::getenv("SDMD_BG_NODMD");
+    c->bg_nodmd = eb && eb[0] == '1';
   }
   if (c->k1_grid < 1) c->k1_grid = 1;
   if (c->cfg.stream) {
@@ -396,9 +399,10 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   const int nd = (int)(t + 1 < m + 1 ? t + 1 : m + 1);
   const bool do_dmd = c->cfg.dmd && t >= m;
   const bool sparse = c->cfg.storage == SDMD_SPARSE;
-  const bool bg = c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
-                  (t - c->L) <= c->last_dmd;
-  if (bg) CK(cudaStreamWaitEvent(c->stream, c->ev_done[(t - c->L) % kEvents], 0));
+  const bool bg = (c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
+                   (t - c->L) <= c->last_dmd) ||
+                  (c->bg_nodmd && c->cfg.background && !sparse && (t - c->L) >= m);
+  if (bg && c->cfg.dmd) CK(cudaStreamWaitEvent(c->stream, c->ev_done[(t - c->L) % kEvents], 0));
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
   if (c->timing) {
     tp = new_pair();
@@ -805,6 +809,7 @@ int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[16]) {
   out[0] = res.frame; out[1] = res.status; out[2] = res.r; out[3] = res.idx;
   out[4] = res.sweeps; out[5] = res.qr_its;
   for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q + 1] - res.phase[q];
+  out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[2];
   return SDMD_OK;
 }
 

@@ -64,6 +64,7 @@ struct K4Result {
   double b_idx[2];
   double sigma1;
   long long phase[8];         // clock64() at phase boundaries (diagnostics)
+  int qr_cnt[4];              // QR: bulge-chase steps, deflation-scan and shift-search iterations
 };
 
 struct K4Params {

@@ -362,7 +362,8 @@ class StreamingDMD:
         names = ["build_S", "jacobi", "sort_V", "atilde", "hessenberg", "qr", "eigvec_c"]
         return dict(frame=int(o[0]), status=int(o[1]), r=int(o[2]), idx=int(o[3]),
                     sweeps=int(o[4]), qr_its=int(o[5]),
-                    cycles={k: int(v) for k, v in zip(names, o[6:13])})
+                    cycles={k: int(v) for k, v in zip(names, o[6:13])},
+                    qr_steps=int(o[13]), qr_scan=int(o[14]), qr_shift_search=int(o[15]))
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")

@@ -373,7 +373,7 @@ def test_c4_full_size_sampled():
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_k1_tma_and_ldg_variants_agree(dtype, monkeypatch):
-    """The TMA-pipelined K1 (default) and the register-streaming K1 (SDMD_K1=ldg) compute the
+    """The register-streaming K1 (default) and the TMA bulk-copy K1 (SDMD_K1=tma) compute the
     same Gram columns and background (different fixed summation orders)."""
     vs = synth.video_config("C3s")
     m, T = 24, 40
@@ -381,9 +381,9 @@ def test_k1_tma_and_ldg_variants_agree(dtype, monkeypatch):
     frames = vs.frames(0, T).numpy().astype(npdt)
     Xd = dev_cols(frames, npdt)
     outs = []
-    for mode in ("tma", "ldg"):
-        if mode == "ldg":
-            monkeypatch.setenv("SDMD_K1", "ldg")
+    for mode in ("ldg", "tma"):
+        if mode == "tma":
+            monkeypatch.setenv("SDMD_K1", "tma")
         else:
             monkeypatch.delenv("SDMD_K1", raising=False)
         eng = Eng(vs.n, m, dtype=dtype, background=True, workers=2)
