@@ -34,6 +34,32 @@ __device__ __forceinline__ void to_double(const float4& v, double* d) {
 }
 __device__ __forceinline__ void to_double(const double2& v, double* d) { d[0] = v.x; d[1] = v.y; }
 
+static __device__ __forceinline__ unsigned k1_smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+static __device__ __forceinline__ void k1_mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(k1_smem_u32(bar)), "r"(count));
+}
+static __device__ __forceinline__ void k1_mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(k1_smem_u32(bar)) : "memory");
+}
+static __device__ __forceinline__ void k1_mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "K1_WAIT:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra K1_DONE;\n\t"
+      "bra K1_WAIT;\n"
+      "K1_DONE:\n\t}" ::"r"(k1_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Background partial-sum slots: [K1_WARPS][8 elements x 40 lanes(32 + 8 pad)], conflict-free for
+// both the per-warp writes (lanes contiguous) and the per-row reads of the reduction.
+constexpr int BG_LSTRIDE = 40;
+constexpr int BG_WSTRIDE = 8 * BG_LSTRIDE;
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -54,8 +80,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   using BT = T;
   using BT2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
   __shared__ BT2 c_s[BG ? kMaxM : 1];
-  extern __shared__ __align__(16) unsigned char red_raw[];  // BG: 2 x [K1_WARPS][kSuperTile] BT2
+  // BG: NSLOT slots of per-warp partials; warps publish tile i into slot i % NSLOT and reduce
+  // their 16-row share of tile i - LAGR, synchronised only by per-slot mbarriers (no CTA barrier)
+  constexpr int NSLOT = sizeof(T) == 4 ? 4 : 2;
+  constexpr int LAGR = NSLOT / 2;
+  extern __shared__ __align__(16) unsigned char red_raw[];
   BT2* red = reinterpret_cast<BT2*>(red_raw);
+  __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
   __shared__ int am_last;
 
   if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
@@ -64,12 +95,15 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   const long long f_bg0 = p.f_bg - p.m + 1;         // first column of X'_{f_bg}
   const long long F0 = BG ? (f_dot0 < f_bg0 ? f_dot0 : f_bg0) : f_dot0;
   const int U = (int)(p.f_new - F0 + 1);
-  if (BG)
+  if (BG) {
     for (int k = tid; k < p.m; k += K1_THREADS) {
       const double2 c = p.cbg[k];
       c_s[k].x = (BT)c.x;
       c_s[k].y = (BT)c.y;
     }
+    if (tid == 0)
+      for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], K1_WARPS); }
+  }
   __syncthreads();
 
   const int cnt = (U > warp) ? (U - warp + K1_WARPS - 1) / K1_WARPS : 0;
@@ -81,9 +115,43 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   double accv[MAXQ];
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) accv[q] = 0.0;
-  int buf = 0;
+  // reduction share of this lane: row rt of a tile <- element e_src of lane l_src, source warps
+  // [8·(lane>>4), +8); lanes 0..15 write the outputs of rows 16·warp + lane
+  const int rt_red = 16 * warp + (lane & 15);
+  const int e_src = (rt_red / (32 * EPV)) * EPV + rt_red % EPV;
+  const int l_src = (rt_red % (32 * EPV)) / EPV;
+  const long long bg_slot = BG ? (p.f_bg % p.NS) * p.ld : 0;
+  auto bg_reduce = [&](long long jt, T xv_t) {       // reduce CTA-local tile jt (BG only)
+    const int slot = (int)(jt % NSLOT);
+    k1_mbar_wait(&fullb[slot], (unsigned)((jt / NSLOT) & 1));
+    const BT2* rb = red + slot * (K1_WARPS * BG_WSTRIDE);
+    double sx = 0.0, sy = 0.0;
+    const int w0 = 8 * (lane >> 4);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const BT2 v = rb[(w0 + w) * BG_WSTRIDE + e_src * BG_LSTRIDE + l_src];
+      sx += (double)v.x;
+      sy += (double)v.y;
+    }
+    sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+    sy += __shfl_xor_sync(0xffffffffu, sy, 16);
+    const long long row = (blockIdx.x + jt * (long long)gridDim.x) * kSuperTile + rt_red;
+    if (lane < 16 && row < p.n) {
+      const double l = sqrt(sx * sx + sy * sy);                   // |l| (Q8)
+      const double sp = (double)xv_t - l;                         // s = x - |l|
+      ((T*)p.lowrank)[row] = (T)l;
+      ((T*)p.sparse)[row] = (T)sp;
+      p.mask[row] = (sp > (double)p.thr) ? 1 : 0;                 // strict '>'
+    }
+    __syncwarp();
+    if (lane == 0) k1_mbar_arrive(&emptyb[slot]);
+  };
+  T xq[LAGR + 1];                                    // prefetched x_{f_bg} rows of pending tiles
+#pragma unroll
+  for (int q = 0; q <= LAGR; ++q) xq[q] = (T)0;
 
-  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x) {
+  long long it = 0;
+  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
     const long long row0 = tile * kSuperTile;
     double xd[8];
 #pragma unroll
@@ -92,10 +160,11 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       to_double(xv, xd + v * EPV);
     }
     BT bre[BG ? 8 : 1], bim[BG ? 8 : 1];
-    // prefetch this tile's x_{f_bg} row for the reduction step (its latency hides behind the
-    // column stream instead of stalling the whole CTA after the barrier)
-    T xbg = (T)0;
-    if (BG && tid < kSuperTile) xbg = __ldcs(ring + (p.f_bg % p.NS) * p.ld + row0 + tid);
+    if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
+#pragma unroll
+      for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
+      xq[0] = (lane < 16) ? __ldcs(ring + bg_slot + row0 + rt_red) : (T)0;
+    }
     if (BG) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) { bre[e] = (BT)0; bim[e] = (BT)0; }
@@ -145,32 +214,25 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       }
     }
     if (BG) {
-      BT2* rb = red + buf * (K1_WARPS * kSuperTile);
+      const int slot = (int)(it % NSLOT);
+      if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
+      BT2* rb = red + slot * (K1_WARPS * BG_WSTRIDE) + warp * BG_WSTRIDE;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int rt = (e / EPV) * (32 * EPV) + lane * EPV + (e % EPV);
         BT2 v;
         v.x = bre[e];
         v.y = bim[e];
-        rb[warp * kSuperTile + rt] = v;
+        rb[e * BG_LSTRIDE + lane] = v;
       }
-      __syncthreads();                     // one barrier per tile (double-buffered partials)
-      if (tid < kSuperTile) {
-        double sx = 0.0, sy = 0.0;
-#pragma unroll
-        for (int w = 0; w < K1_WARPS; ++w) { const BT2 v = rb[w * kSuperTile + tid]; sx += (double)v.x; sy += (double)v.y; }
-        const long long row = row0 + tid;
-        if (row < p.n) {
-          const double l = sqrt(sx * sx + sy * sy);               // |l| (Q8)
-          const double xv = (double)xbg;
-          const double sp = xv - l;                               // s = x - |l|
-          ((T*)p.lowrank)[row] = (T)l;
-          ((T*)p.sparse)[row] = (T)sp;
-          p.mask[row] = (sp > (double)p.thr) ? 1 : 0;             // strict '>'
-        }
-      }
-      buf ^= 1;
+      __syncwarp();
+      if (lane == 0) k1_mbar_arrive(&fullb[slot]);
+      if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
     }
+  }
+  if (BG) {                                   // drain the last LAGR tiles
+#pragma unroll
+    for (int q = LAGR - 1; q >= 0; --q)
+      if (it - 1 - q >= 0) bg_reduce(it - 1 - q, xq[q]);
   }
 
   // per-column warp reduction of the lane partials (fixed order) -> this CTA's partials
@@ -212,7 +274,8 @@ __global__ void commit_kernel(const K1Params p) {
 }
 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
-  const int smem = p.bg ? (int)(2 * K1_WARPS * kSuperTile * (dtype == 0 ? sizeof(float2) : sizeof(double2))) : 0;
+  const int smem = p.bg ? (int)((dtype == 0 ? 4 : 2) * K1_WARPS * BG_WSTRIDE *
+                                (dtype == 0 ? sizeof(float2) : sizeof(double2))) : 0;
   cudaError_t e = cudaSuccess;
   if (dtype == 0) {
     if (p.bg) {

@@ -101,16 +101,24 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
   while (nn >= 0) {
     int its = 0, l;
     do {
-      for (l = nn; l >= 1; --l) {
+      // largest l in [1, nn] with a negligible sub-diagonal a(l, l-1) (lanes test 32 at a time)
+      l = 0;
+      for (int base = nn; base >= 1; base -= 32) {
         ++c_scan;
-        double s = fabs(a(l - 1, l - 1)) + fabs(a(l, l));
-        if (s == 0.0) s = an;
-        if (fabs(a(l, l - 1)) + s == s) {
-          __syncwarp();
-          if (lane == 0) a(l, l - 1) = 0.0;
-          __syncwarp();
-          break;
+        const int li = base - lane;
+        bool neg = false;
+        if (li >= 1) {
+          double s = fabs(a(li - 1, li - 1)) + fabs(a(li, li));
+          if (s == 0.0) s = an;
+          neg = (fabs(a(li, li - 1)) + s == s);
         }
+        const unsigned bal = __ballot_sync(0xffffffffu, neg);
+        if (bal) { l = base - (__ffs(bal) - 1); break; }
+      }
+      if (l >= 1) {
+        __syncwarp();
+        if (lane == 0) a(l, l - 1) = 0.0;
+        __syncwarp();
       }
       double x = a(nn, nn);
       if (l == nn) {                                   // one root
@@ -144,25 +152,41 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
           }
           ++its;
           ++tot;
-          int mm;
-          double p = 0.0, q = 0.0, r = 0.0, z = 0.0;
-          for (mm = nn - 2; mm >= l; --mm) {           // two small consecutive sub-diagonals?
+          // start of the bulge: the largest mm in [l, nn-2] where two consecutive sub-diagonals
+          // are negligible relative to the shifted first column (or mm = l); lanes test 32 at a time
+          int mm = l;
+          for (int base = nn - 2; base >= l; base -= 32) {
             ++c_mscan;
+            const int mi = base - lane;
+            bool ok = false;
+            if (mi >= l) {
+              if (mi == l) {
+                ok = true;
+              } else {
+                const double zz = a(mi, mi), rr = x - zz, ss = y - zz;
+                double pp = (rr * ss - w) / a(mi + 1, mi) + a(mi, mi + 1);
+                double qq = a(mi + 1, mi + 1) - zz - rr - ss;
+                double r3 = a(mi + 2, mi + 1);
+                const double sc = fabs(pp) + fabs(qq) + fabs(r3);
+                pp /= sc; qq /= sc; r3 /= sc;
+                const double u = fabs(a(mi, mi - 1)) * (fabs(qq) + fabs(r3));
+                const double v = fabs(pp) * (fabs(a(mi - 1, mi - 1)) + fabs(zz) + fabs(a(mi + 1, mi + 1)));
+                ok = (u + v == v);
+              }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, ok);
+            if (bal) { mm = base - (__ffs(bal) - 1); break; }
+          }
+          double p, q, r, z;
+          {
             z = a(mm, mm);
             r = x - z;
-            double s = y - z;
+            const double s = y - z;
             p = (r * s - w) / a(mm + 1, mm) + a(mm, mm + 1);
             q = a(mm + 1, mm + 1) - z - r - s;
             r = a(mm + 2, mm + 1);
-            s = fabs(p) + fabs(q) + fabs(r);
-            {
-              const double is = 1.0 / s;
-              p *= is; q *= is; r *= is;
-            }
-            if (mm == l) break;
-            const double u = fabs(a(mm, mm - 1)) * (fabs(q) + fabs(r));
-            const double v = fabs(p) * (fabs(a(mm - 1, mm - 1)) + fabs(z) + fabs(a(mm + 1, mm + 1)));
-            if (u + v == v) break;
+            const double is = 1.0 / (fabs(p) + fabs(q) + fabs(r));
+            p *= is; q *= is; r *= is;
           }
           __syncwarp();
           for (int i = mm + 2 + lane; i <= nn; i += 32) {
@@ -193,27 +217,48 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
                 x = p * is; y = q * is; z = r * is;
                 q *= ip; r *= ip;
               }
+              const bool three = (k != nn - 1);
               __syncwarp();
-              {                                             // row modification
+              {                                         // row modification (2 columns per lane in flight)
                 double* r0 = &a(k, 0);
                 double* r1 = &a(k + 1, 0);
-                double* r2 = &a(k + 2 <= nn ? k + 2 : k + 1, 0);
-                const bool three = (k != nn - 1);
-                for (int j = k + lane; j <= nn; j += 32) {
+                double* r2 = &a(three ? k + 2 : k + 1, 0);
+                for (int j = k + lane; j <= nn; j += 64) {
+                  const int j2 = j + 32;
+                  const bool h2 = j2 <= nn;
                   const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
-                  const double pp = a0 + q * a1 + (three ? r * a2 : 0.0);
-                  if (three) r2[j] = a2 - pp * z;
-                  r1[j] = a1 - pp * y;
-                  r0[j] = a0 - pp * x;
+                  const double b0 = h2 ? r0[j2] : 0.0, b1 = h2 ? r1[j2] : 0.0;
+                  const double b2 = (h2 && three) ? r2[j2] : 0.0;
+                  const double pa = a0 + q * a1 + r * a2, pb = b0 + q * b1 + r * b2;
+                  if (three) r2[j] = a2 - pa * z;
+                  r1[j] = a1 - pa * y;
+                  r0[j] = a0 - pa * x;
+                  if (h2) {
+                    if (three) r2[j2] = b2 - pb * z;
+                    r1[j2] = b1 - pb * y;
+                    r0[j2] = b0 - pb * x;
+                  }
                 }
               }
               __syncwarp();
               const int mmin = nn < k + 3 ? nn : k + 3;
-              for (int i = l + lane; i <= mmin; i += 32) { // column modification
-                double pp = x * a(i, k) + y * a(i, k + 1);
-                if (k != nn - 1) { pp += z * a(i, k + 2); a(i, k + 2) -= pp * r; }
-                a(i, k + 1) -= pp * q;
-                a(i, k) -= pp;
+              for (int i = l + lane; i <= mmin; i += 64) { // column modification (2 rows per lane)
+                const int i2 = i + 32;
+                const bool h2 = i2 <= mmin;
+                double* ri = &a(i, 0);
+                double* rj = &a(h2 ? i2 : i, 0);
+                const double c0 = ri[k], c1 = ri[k + 1], c2 = three ? ri[k + 2] : 0.0;
+                const double d0 = h2 ? rj[k] : 0.0, d1 = h2 ? rj[k + 1] : 0.0;
+                const double d2 = (h2 && three) ? rj[k + 2] : 0.0;
+                const double pp = x * c0 + y * c1 + z * c2, pq = x * d0 + y * d1 + z * d2;
+                if (three) ri[k + 2] = c2 - pp * r;
+                ri[k + 1] = c1 - pp * q;
+                ri[k] = c0 - pp;
+                if (h2) {
+                  if (three) rj[k + 2] = d2 - pq * r;
+                  rj[k + 1] = d1 - pq * q;
+                  rj[k] = d0 - pq;
+                }
               }
               __syncwarp();
             }
@@ -443,65 +488,89 @@ k4_frame_kernel(const K4Params p) {
   cl_sync();
   if (tid == 0) ph[1] = clock64();
 
-  // ---- a5: one-sided (Hestenes) Jacobi on S, round-robin ordering; ≤2 pairs per warp per step
-  const int mp = m + (m & 1);
-  const int npairs = mp / 2;
+  // ---- a5: one-sided (Hestenes) block Jacobi on S.  The m columns form 8 blocks; a block sweep
+  // is the round-robin tournament of the 8 blocks (7 rounds).  In each round CTA c of the cluster
+  // holds block pair c in shared memory and rotates every column pair that crosses the two
+  // blocks (round 0 also the pairs inside each block), so every pair of columns meets once per
+  // block sweep.  Only the round boundaries need cluster barriers.
+  const int bs = (m + 7) / 8;                     // block size (columns)
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
   constexpr int EL = kMaxM / 32;
+  double* sA = reinterpret_cast<double*>(k4_smem); // 2*bs columns x m, column-major
   int sweeps = 0;
   bool converged = false;
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
     int rot = 0;
-    for (int s = 0; s < mp - 1; ++s) {
-      for (int k0 = gwarp; k0 < npairs; k0 += 2 * K4_GW) {
-        const int k1 = k0 + K4_GW;
-        int P[2], Q[2];
-        bool act[2];
-        P[0] = rr_player(k0, s, mp); Q[0] = rr_player(mp - 1 - k0, s, mp);
-        act[0] = P[0] < m && Q[0] < m;
-        if (k1 < npairs) { P[1] = rr_player(k1, s, mp); Q[1] = rr_player(mp - 1 - k1, s, mp); act[1] = P[1] < m && Q[1] < m; }
-        else { P[1] = Q[1] = 0; act[1] = false; }
-        double ap[2][EL], aq[2][EL];
+    for (int rd = 0; rd < 7; ++rd) {
+      const int PB = rr_player(crank, rd, 8), QB = rr_player(7 - crank, rd, 8);
+      // local column lc in [0, 2bs): global column gc(lc)
+      auto gcol = [&](int lc) { return lc < bs ? PB * bs + lc : QB * bs + (lc - bs); };
+      for (int e = tid; e < 2 * bs * m; e += K4_THREADS) {
+        const int lc = e / m, i = e % m, gc = gcol(lc);
+        sA[e] = gc < m ? __ldcg(p.A + (long long)gc * m + i) : 0.0;
+      }
+      __syncthreads();
+      const int nsteps = (rd == 0) ? 2 * bs - 1 : bs;
+      for (int st = 0; st < nsteps; ++st) {
+        for (int k0 = warp; k0 < bs; k0 += 2 * K4_WARPS) {
+          int P[2], Q[2];
+          bool act[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const double* cp = p.A + (long long)P[u] * m;
-          const double* cq = p.A + (long long)Q[u] * m;
-#pragma unroll
-          for (int e = 0; e < EL; ++e) {
-            const int i = lane + 32 * e;
-            const bool ok = act[u] && i < m;
-            ap[u][e] = ok ? __ldcg(cp + i) : 0.0;
-            aq[u][e] = ok ? __ldcg(cq + i) : 0.0;
+          for (int u = 0; u < 2; ++u) {
+            const int kk = k0 + u * K4_WARPS;
+            if (kk < bs) {
+              if (rd == 0) { P[u] = rr_player(kk, st, 2 * bs); Q[u] = rr_player(2 * bs - 1 - kk, st, 2 * bs); }
+              else { P[u] = kk; Q[u] = bs + (kk + st) % bs; }
+              act[u] = gcol(P[u]) < m && gcol(Q[u]) < m;
+            } else { P[u] = Q[u] = 0; act[u] = false; }
           }
-        }
+          double ap[2][EL], aq[2][EL];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (!act[u]) continue;
-          double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-          for (int e = 0; e < EL; ++e) {
-            al = fma(ap[u][e], ap[u][e], al);
-            be = fma(aq[u][e], aq[u][e], be);
-            ga = fma(ap[u][e], aq[u][e], ga);
-          }
-          al = wsum(al); be = wsum(be); ga = wsum(ga);
-          if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-            const double zeta = (be - al) / (2.0 * ga);
-            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
-            double* cp = p.A + (long long)P[u] * m;
-            double* cq = p.A + (long long)Q[u] * m;
+          for (int u = 0; u < 2; ++u) {
+            const double* cp = sA + P[u] * m;
+            const double* cq = sA + Q[u] * m;
 #pragma unroll
             for (int e = 0; e < EL; ++e) {
               const int i = lane + 32 * e;
-              if (i < m) {
-                cp[i] = c * ap[u][e] - sn * aq[u][e];
-                cq[i] = sn * ap[u][e] + c * aq[u][e];
-              }
+              const bool ok = act[u] && i < m;
+              ap[u][e] = ok ? cp[i] : 0.0;
+              aq[u][e] = ok ? cq[i] : 0.0;
             }
-            rot = 1;
+          }
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            if (!act[u]) continue;
+            double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+            for (int e = 0; e < EL; ++e) {
+              al = fma(ap[u][e], ap[u][e], al);
+              be = fma(aq[u][e], aq[u][e], be);
+              ga = fma(ap[u][e], aq[u][e], ga);
+            }
+            al = wsum(al); be = wsum(be); ga = wsum(ga);
+            if (ga != 0.0 && ga * ga > tol * tol * (al * be)) {
+              const double zeta = (be - al) * (0.5 / ga);
+              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+              double* cp = sA + P[u] * m;
+              double* cq = sA + Q[u] * m;
+#pragma unroll
+              for (int e = 0; e < EL; ++e) {
+                const int i = lane + 32 * e;
+                if (i < m) {
+                  cp[i] = c * ap[u][e] - sn * aq[u][e];
+                  cq[i] = sn * ap[u][e] + c * aq[u][e];
+                }
+              }
+              rot = 1;
+            }
           }
         }
+        __syncthreads();
+      }
+      for (int e = tid; e < 2 * bs * m; e += K4_THREADS) {
+        const int lc = e / m, i = e % m, gc = gcol(lc);
+        if (gc < m) p.A[(long long)gc * m + i] = sA[e];
       }
       cl_sync();
     }
@@ -611,75 +680,90 @@ k4_frame_kernel(const K4Params p) {
   cl_sync();
   if (tid == 0) ph[4] = clock64();
 
-  // ---- a8: Householder reduction to upper Hessenberg form, rank-1 updates spread over the cluster
-  double* H = p.H;
-  for (int k = 0; k < r - 2; ++k) {
-    const int L = r - k - 1;
-    if (crank == 0 && warp == 0) {
-      double x[kMaxR / 32];
-      double s2 = 0.0, x0 = 0.0;
-#pragma unroll
-      for (int e = 0; e < kMaxR / 32; ++e) {
-        const int i = lane + 32 * e;
-        x[e] = (i < L) ? __ldcg(H + (long long)(k + 1 + i) * r + k) : 0.0;
-        if (i == 0) x0 = x[e];
-        else s2 = fma(x[e], x[e], s2);
-      }
-      s2 = wsum(s2);
-      x0 = __shfl_sync(0xffffffffu, x0, 0);
-      double tauk = 0.0, beta = x0, v0 = 1.0;
-      if (s2 != 0.0) {
-        const double mu_ = sqrt(x0 * x0 + s2);
-        v0 = (x0 <= 0.0) ? x0 - mu_ : -s2 / (x0 + mu_);
-        tauk = 2.0 * v0 * v0 / (s2 + v0 * v0);
-        beta = mu_;
-      }
-#pragma unroll
-      for (int e = 0; e < kMaxR / 32; ++e) {
-        const int i = lane + 32 * e;
-        if (i < L) {
-          const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? x[e] / v0 : 0.0);
-          p.Qv[(long long)k * r + k + 1 + i] = v;
-          H[(long long)(k + 1 + i) * r + k] = (i == 0) ? beta : 0.0;
+  // ---- a8: Householder reduction to upper Hessenberg form.  The rows of Ã are distributed over
+  // the cluster's shared memory (CTA c owns rows [c·rb, (c+1)·rb)); per reflector only the pivot
+  // column and the partial row-sums wᵀ = vᵀH cross CTAs (two cluster barriers per step).
+  {
+    const int rb = (r + K4_CLUSTER - 1) / K4_CLUSTER;
+    const int r0 = crank * rb, r1 = min(r, r0 + rb);
+    const int nr = r1 > r0 ? r1 - r0 : 0;
+    double* sH = reinterpret_cast<double*>(k4_smem);        // nr x r, row-major
+    double* sv = sH + (size_t)rb * r;                        // v  (kMaxR)
+    double* sw = sv + kMaxR;                                 // τw (kMaxR)
+    double* colk = p.B;                                      // published pivot column
+    double* wpart = p.B + kMaxR;                             // [K4_CLUSTER][kMaxR] partial wᵀ
+    __shared__ double sh_tk, sh_beta;
+    for (int e = tid; e < nr * r; e += K4_THREADS) sH[e] = __ldcg(p.H + (long long)r0 * r + e);
+    __syncthreads();
+    for (int k = 0; k < r - 2; ++k) {
+      const int L = r - k - 1;
+      const int i0 = r0 > k + 1 ? r0 : k + 1;                // my rows taking part in the reflector
+      for (int i = i0 + tid; i < r1; i += K4_THREADS) colk[i] = sH[(size_t)(i - r0) * r + k];
+      cl_sync();
+      if (warp == 0) {                                       // identical on every CTA
+        double s2 = 0.0;
+        for (int i = 1 + lane; i < L; i += 32) { const double x = __ldcg(colk + k + 1 + i); s2 = fma(x, x, s2); }
+        s2 = wsum(s2);
+        const double x0 = __ldcg(colk + k + 1);
+        double tauk = 0.0, beta = x0, v0 = 1.0;
+        if (s2 != 0.0) {
+          const double mu_ = sqrt(x0 * x0 + s2);
+          v0 = (x0 <= 0.0) ? x0 - mu_ : -s2 / (x0 + mu_);
+          tauk = 2.0 * v0 * v0 / (s2 + v0 * v0);
+          beta = mu_;
+        }
+        for (int i = lane; i < L; i += 32) {
+          const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? __ldcg(colk + k + 1 + i) / v0 : 0.0);
+          sv[i] = v;
+          if (crank == 0) p.Qv[(long long)k * r + k + 1 + i] = v;
+        }
+        if (lane == 0) {
+          sh_tk = tauk;
+          sh_beta = beta;
+          if (crank == 0) p.tau[k] = tauk;
         }
       }
-      if (lane == 0) p.tau[k] = tauk;
+      __syncthreads();
+      const double tk = sh_tk;
+      for (int i = i0 + tid; i < r1; i += K4_THREADS)
+        sH[(size_t)(i - r0) * r + k] = (i == k + 1) ? sh_beta : 0.0;
+      if (tk != 0.0) {
+        for (int j = k + 1 + tid; j < r; j += K4_THREADS) {  // partial wᵀ = vᵀ H over my rows
+          double s = 0.0;
+          for (int i = i0; i < r1; ++i) s = fma(sv[i - k - 1], sH[(size_t)(i - r0) * r + j], s);
+          wpart[crank * kMaxR + j] = s;
+        }
+        cl_sync();
+        for (int j = k + 1 + tid; j < r; j += K4_THREADS) {
+          double s = 0.0;
+          for (int c = 0; c < K4_CLUSTER; ++c) s += __ldcg(wpart + c * kMaxR + j);
+          sw[j] = s * tk;
+        }
+        __syncthreads();
+        if (r1 > i0) {                                       // left: H[i][j] -= v_i (τw)_j
+          const int nrow = r1 - i0;
+          for (int e = tid; e < nrow * L; e += K4_THREADS) {
+            const int i = i0 + e / L, j = k + 1 + e % L;
+            sH[(size_t)(i - r0) * r + j] -= sv[i - k - 1] * sw[j];
+          }
+        }
+        __syncthreads();
+        for (int i = r0 + warp; i < r1; i += K4_WARPS) {     // right: H[i][:] -= (τ H v)_i vᵀ
+          double* hi = sH + (size_t)(i - r0) * r + k + 1;
+          double s = 0.0;
+          for (int jj = lane; jj < L; jj += 32) s = fma(hi[jj], sv[jj], s);
+          s = wsum(s) * tk;
+          for (int jj = lane; jj < L; jj += 32) hi[jj] -= s * sv[jj];
+        }
+        __syncthreads();
+      } else {
+        cl_sync();                                           // keep the barrier sequence uniform
+      }
     }
+    for (int e = tid; e < nr * r; e += K4_THREADS) p.H[(long long)r0 * r + e] = sH[e];
     cl_sync();
-    const double tk = __ldcg(p.tau + k);
-    if (tk != 0.0) {
-      const double* v = p.Qv + (long long)k * r + k + 1;
-      // w_j = Σ_i v_i H[k+1+i][j], j = k+1..r-1 (warp per column)
-      for (int j = k + 1 + gwarp; j < r; j += K4_GW) {
-        double s = 0.0;
-        for (int i = lane; i < L; i += 32) s = fma(__ldcg(v + i), __ldcg(H + (long long)(k + 1 + i) * r + j), s);
-        s = wsum(s);
-        if (lane == 0) p.wv[j] = s * tk;
-      }
-      cl_sync();
-      for (int e = gtid; e < L * L; e += K4_GT) {            // H[k+1+i][k+1+jj] -= v_i w_j
-        const int i = e / L, jj = e % L;
-        const long long o = (long long)(k + 1 + i) * r + k + 1 + jj;
-        H[o] = __ldcg(H + o) - __ldcg(v + i) * __ldcg(p.wv + k + 1 + jj);
-      }
-      cl_sync();
-      // u_i = τ Σ_jj H[i][k+1+jj] v_jj, all rows (warp per row)
-      for (int i = gwarp; i < r; i += K4_GW) {
-        const double* hi = H + (long long)i * r + k + 1;
-        double s = 0.0;
-        for (int jj = lane; jj < L; jj += 32) s = fma(__ldcg(hi + jj), __ldcg(v + jj), s);
-        s = wsum(s);
-        if (lane == 0) p.uv[i] = s * tk;
-      }
-      cl_sync();
-      for (int e = gtid; e < r * L; e += K4_GT) {            // H[i][k+1+jj] -= u_i v_jj
-        const int i = e / L, jj = e % L;
-        const long long o = (long long)i * r + k + 1 + jj;
-        H[o] = __ldcg(H + o) - __ldcg(p.uv + i) * __ldcg(v + jj);
-      }
-      cl_sync();
-    }
   }
+  double* H = p.H;
   if (crank != 0) return;                                   // the rest runs on CTA 0
   if (tid == 0) {
     if (r >= 2) p.tau[r - 2] = 0.0;
@@ -801,15 +885,19 @@ k4_frame_kernel(const K4Params p) {
   }
 }
 
-size_t k4_smem_bytes(int r_max) {
+size_t k4_smem_bytes(int r_max, int m) {
   const long long hs = hs_elems(r_max);
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);
-  return a > b ? a : b;
+  const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
+  const size_t d = ((size_t)((r_max + 3) / 4) * r_max + 2 * kMaxR) * sizeof(double);  // Hessenberg rows
+  size_t s = a > b ? a : b;
+  s = s > c ? s : c;
+  return s > d ? s : d;
 }
 
 cudaError_t launch_k4(const K4Params& p, cudaStream_t s) {
-  const size_t smem = k4_smem_bytes(p.r_max);
+  const size_t smem = k4_smem_bytes(p.r_max, p.m);
   cudaError_t e = cudaFuncSetAttribute(k4_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;

@@ -304,7 +304,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(k.V, (size_t)m * m);
     AL(k.sigma, (size_t)m);
     AL(k.Y, (size_t)m * R);
-    AL(k.B, (size_t)m * R);
+    AL(k.B, (size_t)(m > 8 ? m : 8) * R);   // also the Hessenberg exchange scratch (5 x R)
     AL(k.H, (size_t)R * R);
     AL(k.Qv, (size_t)R * R);
     AL(k.tau, (size_t)R);

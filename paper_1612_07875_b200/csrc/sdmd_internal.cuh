@@ -159,7 +159,7 @@ size_t k1_tma_smem_bytes(int dtype, int bg);
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_k4(const K4Params& p, cudaStream_t s);
-size_t k4_smem_bytes(int r_max);
+size_t k4_smem_bytes(int r_max, int m);
 int k4_cluster_size();
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
 cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
