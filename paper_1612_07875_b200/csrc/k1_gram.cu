@@ -66,24 +66,61 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+static __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&d);
+}
+
+template <typename T> struct BgAcc;     // per-lane background accumulator of one row (re, im)
+template <> struct BgAcc<float> {
+  // fp32 (re, im) pairs with packed FFMA2: per-warp sums of ~m/16 terms, followed by an fp64
+  // cross-warp sum; error ~1e-6 relative, inside the fp32-path tolerance (1e-4)
+  using C2 = float2;
+  float2 v[8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = make_float2(0.f, 0.f);
+  }
+  __device__ __forceinline__ void add(const float2 c, const float* z) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = ffma2(c, make_float2(z[e], z[e]), v[e]);
+  }
+};
+template <> struct BgAcc<double> {
+  using C2 = double2;
+  double2 v[8];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = make_double2(0.0, 0.0);
+  }
+  __device__ __forceinline__ void add(const double2 c, const double* z) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { v[e].x = fma(c.x, z[e], v[e].x); v[e].y = fma(c.y, z[e], v[e].y); }
+  }
+};
+
 template <typename T, bool BG>
 // One 512-thread CTA per SM (<= 128 registers): 16 warps x 8 LDG.128 per lane in flight ≈ 64 KB
 // per SM.  The grid leaves the eigen-worker SMs free (K4 runs concurrently on its own SMs).
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p) {
   using VT = typename VecOf<T>::type;
+  using BT2 = typename BgAcc<T>::C2;
   constexpr int EPV = VecOf<T>::E;          // elements per 16-byte vector
   constexpr int VPL = 8 / EPV;              // vectors per lane per column (8 rows per lane)
   constexpr int CB = sizeof(T) == 4 ? 4 : (BG ? 1 : 2);  // columns in flight per batch
   constexpr int MAXQ = (K1_MAXU + K1_WARPS - 1) / K1_WARPS;
-  // background partials: fp32 for fp32 storage (per-warp sums of ~m/16 terms, then an fp64
-  // cross-warp sum; error ~1e-6 relative, inside the fp32-path tolerance), fp64 for fp64 storage
-  using BT = T;
-  using BT2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
-  __shared__ BT2 c_s[BG ? kMaxM : 1];
   // BG: NSLOT slots of per-warp partials; warps publish tile i into slot i % NSLOT and reduce
   // their 16-row share of tile i - LAGR, synchronised only by per-slot mbarriers (no CTA barrier)
   constexpr int NSLOT = sizeof(T) == 4 ? 4 : 2;
   constexpr int LAGR = NSLOT / 2;
+  __shared__ BT2 c_s[BG ? kMaxM : 1];
+  __shared__ long long col_off[K1_WARPS][MAXQ];   // ring offset (slot * ld) of each warp column
+  __shared__ int col_kd[K1_WARPS][MAXQ];          // Gram-column index, or -1
+  __shared__ int col_kb[K1_WARPS][MAXQ];          // background coefficient index, or -1
   extern __shared__ __align__(16) unsigned char red_raw[];
   BT2* red = reinterpret_cast<BT2*>(red_raw);
   __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
@@ -95,11 +132,18 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   const long long f_bg0 = p.f_bg - p.m + 1;         // first column of X'_{f_bg}
   const long long F0 = BG ? (f_dot0 < f_bg0 ? f_dot0 : f_bg0) : f_dot0;
   const int U = (int)(p.f_new - F0 + 1);
+  for (int e = tid; e < K1_WARPS * MAXQ; e += K1_THREADS) {
+    const int w = e / MAXQ, q = e % MAXQ, j = w + K1_WARPS * q;
+    const long long f = F0 + j;
+    col_off[w][q] = (j < U) ? (f % p.NS) * p.ld : 0;
+    col_kd[w][q] = (j < U && f >= f_dot0) ? (int)(f - f_dot0) : -1;
+    col_kb[w][q] = (BG && j < U && f >= f_bg0 && f - f_bg0 < p.m) ? (int)(f - f_bg0) : -1;
+  }
   if (BG) {
     for (int k = tid; k < p.m; k += K1_THREADS) {
       const double2 c = p.cbg[k];
-      c_s[k].x = (BT)c.x;
-      c_s[k].y = (BT)c.y;
+      c_s[k].x = c.x;
+      c_s[k].y = c.y;
     }
     if (tid == 0)
       for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], K1_WARPS); }
@@ -120,7 +164,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   const int rt_red = 16 * warp + (lane & 15);
   const int e_src = (rt_red / (32 * EPV)) * EPV + rt_red % EPV;
   const int l_src = (rt_red % (32 * EPV)) / EPV;
-  const long long bg_slot = BG ? (p.f_bg % p.NS) * p.ld : 0;
+  const T* bg_col = BG ? ring + (p.f_bg % p.NS) * p.ld : ring;
   auto bg_reduce = [&](long long jt, T xv_t) {       // reduce CTA-local tile jt (BG only)
     const int slot = (int)(jt % NSLOT);
     k1_mbar_wait(&fullb[slot], (unsigned)((jt / NSLOT) & 1));
@@ -159,16 +203,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
       to_double(xv, xd + v * EPV);
     }
-    BT bre[BG ? 8 : 1], bim[BG ? 8 : 1];
+    BgAcc<T> bacc;
     if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
+      bacc.zero();
 #pragma unroll
       for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
-      xq[0] = (lane < 16) ? __ldcs(ring + bg_slot + row0 + rt_red) : (T)0;
+      xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
     }
-    if (BG) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) { bre[e] = (BT)0; bim[e] = (BT)0; }
-    }
+    const T* base = ring + row0;
 #pragma unroll
     for (int q0 = 0; q0 < MAXQ; q0 += CB) {
       if (q0 < cnt) {
@@ -177,8 +219,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
         for (int b = 0; b < CB; ++b) {
           const int q = q0 + b;
           if (q < MAXQ && q < cnt) {
-            const long long f = F0 + warp + K1_WARPS * q;
-            const VT* zp = reinterpret_cast<const VT*>(ring + (f % p.NS) * p.ld + row0);
+            const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
 #pragma unroll
             for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
           }
@@ -187,27 +228,18 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
         for (int b = 0; b < CB; ++b) {
           const int q = q0 + b;
           if (q < MAXQ && q < cnt) {
-            const long long f = F0 + warp + K1_WARPS * q;
-            double zd[8];
+            if (col_kd[warp][q] >= 0) {
+              double zd[8];
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
-            if (f >= f_dot0) {
+              for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
               double s0 = 0.0, s1 = 0.0;
 #pragma unroll
               for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
               accv[q] += s0 + s1;
             }
             if (BG) {
-              const long long kb = f - f_bg0;
-              if (kb >= 0 && kb < p.m) {
-                const BT2 c = c_s[kb];
-                const T* zr = reinterpret_cast<const T*>(&z[b][0]);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  bre[e] = fma(c.x, (BT)zr[e], bre[e]);
-                  bim[e] = fma(c.y, (BT)zr[e], bim[e]);
-                }
-              }
+              const int kb = col_kb[warp][q];
+              if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&z[b][0]));
             }
           }
         }
@@ -218,12 +250,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
       BT2* rb = red + slot * (K1_WARPS * BG_WSTRIDE) + warp * BG_WSTRIDE;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        BT2 v;
-        v.x = bre[e];
-        v.y = bim[e];
-        rb[e * BG_LSTRIDE + lane] = v;
-      }
+      for (int e = 0; e < 8; ++e) rb[e * BG_LSTRIDE + lane] = bacc.v[e];
       __syncwarp();
       if (lane == 0) k1_mbar_arrive(&fullb[slot]);
       if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
@@ -239,9 +266,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) {
     if (q < cnt) {
-      const long long f = F0 + warp + K1_WARPS * q;
+      const int kd = col_kd[warp][q];
       const double s = warp_sum(accv[q]);
-      if (lane == 0 && f >= f_dot0) p.partials[(long long)blockIdx.x * PSTRIDE + (f - f_dot0)] = s;
+      if (lane == 0 && kd >= 0) p.partials[(long long)blockIdx.x * PSTRIDE + kd] = s;
     }
   }
   __threadfence();

@@ -89,25 +89,25 @@ __host__ __device__ inline long long hs_elems(int r) { return hs_off(r, r); }
 // runs the scalar recurrences redundantly on identical shared-memory data; lanes split the row
 // and column updates of each 3x3 reflector.  Returns 0, or -1 when an eigenvalue needs more than
 // QR_MAXITS iterations.
-static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* total_its,
-                                    int* cnt) {
+static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, int* total_its,
+                               int* cnt) {
   int c_steps = 0, c_scan = 0, c_mscan = 0;
   double an = 0.0;
-  for (int i = 0; i < n; ++i)
-    for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(a(i, j));
+  for (int i = lo; i <= hi; ++i)
+    for (int j = (i > lo ? i - 1 : lo) + lane; j <= hi; j += 32) an += fabs(a(i, j));
   an = wsum(an);
-  int nn = n - 1, tot = 0;
+  int nn = hi, tot = 0;
   double t = 0.0;
-  while (nn >= 0) {
+  while (nn >= lo) {
     int its = 0, l;
     do {
-      // largest l in [1, nn] with a negligible sub-diagonal a(l, l-1) (lanes test 32 at a time)
-      l = 0;
-      for (int base = nn; base >= 1; base -= 32) {
+      // largest l in [lo+1, nn] with a negligible sub-diagonal a(l, l-1) (lanes test 32 at a time)
+      l = lo;
+      for (int base = nn; base >= lo + 1; base -= 32) {
         ++c_scan;
         const int li = base - lane;
         bool neg = false;
-        if (li >= 1) {
+        if (li >= lo + 1) {
           double s = fabs(a(li - 1, li - 1)) + fabs(a(li, li));
           if (s == 0.0) s = an;
           neg = (fabs(a(li, li - 1)) + s == s);
@@ -115,7 +115,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
         const unsigned bal = __ballot_sync(0xffffffffu, neg);
         if (bal) { l = base - (__ffs(bal) - 1); break; }
       }
-      if (l >= 1) {
+      if (l >= lo + 1) {
         __syncwarp();
         if (lane == 0) a(l, l - 1) = 0.0;
         __syncwarp();
@@ -144,7 +144,7 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
           if (its > 0 && its % 10 == 0) {              // exceptional shift
             t += x;
             __syncwarp();
-            for (int i = lane; i <= nn; i += 32) a(i, i) -= x;
+            for (int i = lo + lane; i <= nn; i += 32) a(i, i) -= x;
             __syncwarp();
             const double s = fabs(a(nn, nn - 1)) + fabs(a(nn - 1, nn - 2));
             y = x = 0.75 * s;
@@ -196,12 +196,16 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
           __syncwarp();
           for (int k = mm; k <= nn - 1; ++k) {          // chase the bulge
             ++c_steps;
+            double xs = 1.0;                            // scale of (p, q, r)
             if (k != mm) {
               p = a(k, k - 1);
               q = a(k + 1, k - 1);
               r = (k != nn - 1) ? a(k + 2, k - 1) : 0.0;
-              x = fabs(p) + fabs(q) + fabs(r);
-              if (x != 0.0) { const double ix = 1.0 / x; p *= ix; q *= ix; r *= ix; }
+              const double ss = p * p + q * q + r * r;
+              if (!(ss > 1e-280 && ss < 1e280)) {       // rescale only when squares leave range
+                x = fabs(p) + fabs(q) + fabs(r);
+                if (x != 0.0) { const double ix = 1.0 / x; p *= ix; q *= ix; r *= ix; xs = x; }
+              }
             }
             const double s = copysign(sqrt(p * p + q * q + r * r), p);
             if (s != 0.0) {
@@ -209,11 +213,12 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
               if (k == mm) {
                 if (l != mm && lane == 0) a(k, k - 1) = -a(k, k - 1);
               } else if (lane == 0) {
-                a(k, k - 1) = -s * x;
+                a(k, k - 1) = -s * xs;
               }
               p += s;
-              {
-                const double is = 1.0 / s, ip = 1.0 / p;
+              {                                         // one division for 1/s and 1/p
+                const double inv = 1.0 / (s * p);
+                const double is = p * inv, ip = s * inv;
                 x = p * is; y = q * is; z = r * is;
                 q *= ip; r *= ip;
               }
@@ -267,9 +272,240 @@ static __device__ int hessenberg_qr(HsAcc a, int n, double2* wv, int lane, int* 
       }
     } while (l < nn - 1);
   }
-  *total_its = tot;
-  if (cnt) { cnt[0] = c_steps; cnt[1] = c_scan; cnt[2] = c_mscan; }
+  *total_its += tot;
+  if (cnt && lane == 0) { cnt[0] += c_steps; cnt[1] += c_scan; cnt[2] += c_mscan; }
   return 0;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Multishift QR (eigenvalues only), CTA-level.  Each sweep takes ns = 2·NB shifts — the
+// eigenvalues of the trailing ns x ns block, computed by qr_block on a small copy — and chases NB
+// double-shift bulges down the active block in lockstep, bulge b on warp b, 4 positions apart.
+// Per global step: (A) every active bulge forms its 3x3 reflector, (B) row updates, (C) column
+// updates, each phase followed by a CTA barrier.  Concurrent bulges act on disjoint rows in (B) and
+// disjoint columns in (C), and left and right reflections commute, so a sweep is exactly NB
+// successive Francis double-shift steps with the given shifts.  Small or stagnating blocks fall
+// back to the single-bulge qr_block.  (Golub–Van Loan §7.5; small-bulge multishift idea of
+// Braman–Byers–Mathias; no aggressive early deflation.)
+constexpr int MS_NB = 8;           // bulges per sweep (<= K4_WARPS)
+constexpr int MS_SMALL = 32;       // blocks up to this size use the single-bulge iteration
+constexpr int MS_STALL = 6;        // sweeps without deflation before falling back
+constexpr int MS_SPACING = 4;
+
+struct MsShared {
+  double bx[MS_NB], by[MS_NB], bz[MS_NB], bq[MS_NB], br[MS_NB];
+  int bk[MS_NB], bon[MS_NB], bthree[MS_NB];
+  double st[MS_NB], sd[MS_NB];
+  double2 sw[2 * MS_NB];
+  double small_hs[200];            // packed (with slack) ns x ns trailing block, ns <= 16
+  int l, nbe, fail, defl;
+};
+
+static __device__ void ms_two_roots(HsAcc a, int nn, double2* wv) {
+  const double x = a(nn, nn), y = a(nn - 1, nn - 1), w = a(nn, nn - 1) * a(nn - 1, nn);
+  const double p = 0.5 * (y - x), q = p * p + w;
+  double z = sqrt(fabs(q));
+  if (q >= 0.0) {
+    z = p + copysign(z, p);
+    const double e1 = x + z, e2 = (z != 0.0) ? x - w / z : e1;
+    wv[nn - 1] = make_double2(e1, 0.0);
+    wv[nn] = make_double2(e2, 0.0);
+  } else {
+    wv[nn - 1] = make_double2(x + p, z);
+    wv[nn] = make_double2(x + p, -z);
+  }
+}
+
+static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, int tid, int warp,
+                                    int lane, int* total_its, int* cnt) {
+  double an = 0.0;
+  if (warp == 0) {
+    for (int i = 0; i < n; ++i)
+      for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(a(i, j));
+    an = wsum(an);
+  }
+  int nn = n - 1, stall = 0, status = 0;
+  while (nn >= 0) {
+    // ---- deflation at the bottom of the active block (warp 0)
+    if (warp == 0) {
+      int l = 0;
+      for (int base = nn; base >= 1; base -= 32) {
+        const int li = base - lane;
+        bool neg = false;
+        if (li >= 1) {
+          double s = fabs(a(li - 1, li - 1)) + fabs(a(li, li));
+          if (s == 0.0) s = an;
+          neg = (fabs(a(li, li - 1)) + s == s);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, neg);
+        if (bal) { l = base - (__ffs(bal) - 1); break; }
+      }
+      if (lane == 0) {
+        if (l >= 1) a(l, l - 1) = 0.0;
+        sh->l = l;
+        if (l == nn) wv[nn] = make_double2(a(nn, nn), 0.0);
+        else if (l == nn - 1) ms_two_roots(a, nn, wv);
+      }
+    }
+    __syncthreads();
+    const int l = sh->l;
+    if (l >= nn - 1) {                                   // 1 or 2 eigenvalues deflated
+      nn = l - 1;
+      stall = 0;
+      __syncthreads();
+      continue;
+    }
+    const int nact = nn - l + 1;
+    if (nact <= MS_SMALL || stall >= MS_STALL) {        // single-bulge iteration on [l, nn]
+      if (warp == 0) {
+        const int rc = qr_block(a, l, nn, wv, lane, total_its, cnt);
+        if (lane == 0) sh->fail = rc;
+      }
+      __syncthreads();
+      if (sh->fail != 0) status = -1;
+      nn = l - 1;
+      stall = 0;
+      __syncthreads();
+      if (status) return status;
+      continue;
+    }
+    // ---- shifts: eigenvalues of the trailing ns x ns block (warp 0, small packed copy)
+    int ns = 2 * MS_NB;
+    if (ns > ((nact - 2) & ~1)) ns = (nact - 2) & ~1;
+    if (warp == 0) {
+      const int b0 = nn - ns + 1;
+      HsAcc sm{sh->small_hs, ns};
+      for (int i = 0; i < ns; ++i) {
+        const int lo_i = i > 3 ? i - 3 : 0;
+        for (int j = lo_i + lane; j < ns; j += 32) sm(i, j) = (j >= i - 1) ? a(b0 + i, b0 + j) : 0.0;
+      }
+      __syncwarp();
+      int its_s = 0;
+      const int rc = qr_block(sm, 0, ns - 1, sh->sw, lane, &its_s, nullptr);
+      __syncwarp();
+      if (lane == 0) {
+        int nb = 0;
+        if (rc == 0) {
+          double rl = 0.0;
+          bool have_real = false;
+          for (int i = 0; i < ns && nb < MS_NB; ++i) {
+            const double2 e = sh->sw[i];
+            if (e.y != 0.0) {                            // conjugate pair (i, i+1)
+              sh->st[nb] = 2.0 * e.x;
+              sh->sd[nb] = e.x * e.x + e.y * e.y;
+              ++nb;
+              ++i;
+            } else if (have_real) {
+              sh->st[nb] = rl + e.x;
+              sh->sd[nb] = rl * e.x;
+              ++nb;
+              have_real = false;
+            } else {
+              rl = e.x;
+              have_real = true;
+            }
+          }
+        }
+        sh->nbe = nb;
+      }
+    }
+    __syncthreads();
+    const int nbe = sh->nbe;
+    if (nbe == 0) { stall = MS_STALL; continue; }
+    // ---- chase nbe bulges in lockstep
+    const int G = (nn - 1 - l) + MS_SPACING * (nbe - 1);
+    for (int g = 0; g <= G; ++g) {
+      // (A) reflectors
+      if (warp < nbe) {
+        const int b = warp;
+        const int k = l + g - MS_SPACING * b;
+        const bool act = (k >= l && k <= nn - 1);
+        if (act) {
+          const bool three = (k != nn - 1);
+          double P, Q, R;
+          if (k == l) {
+            const double h00 = a(l, l), h10 = a(l + 1, l), h01 = a(l, l + 1), h11 = a(l + 1, l + 1);
+            const double h21 = a(l + 2, l + 1);
+            P = h00 * (h00 - sh->st[b]) + sh->sd[b] + h01 * h10;
+            Q = h10 * (h00 + h11 - sh->st[b]);
+            R = h10 * h21;
+          } else {
+            P = a(k, k - 1);
+            Q = a(k + 1, k - 1);
+            R = three ? a(k + 2, k - 1) : 0.0;
+          }
+          double xs = 1.0;
+          const double sc = fabs(P) + fabs(Q) + fabs(R);
+          const double ss0 = P * P + Q * Q + R * R;
+          if (!(ss0 > 1e-280 && ss0 < 1e280) && sc != 0.0) {
+            const double isc = 1.0 / sc;
+            P *= isc; Q *= isc; R *= isc;
+            xs = sc;
+          }
+          const double s = copysign(sqrt(P * P + Q * Q + R * R), P);
+          if (lane == 0) {
+            sh->bk[b] = k;
+            sh->bthree[b] = three ? 1 : 0;
+            sh->bon[b] = (s != 0.0) ? 1 : 0;
+            if (s != 0.0) {
+              if (k > l) {
+                a(k, k - 1) = -s * xs;
+                a(k + 1, k - 1) = 0.0;
+                if (three) a(k + 2, k - 1) = 0.0;
+              }
+              const double pp = P + s;
+              const double inv = 1.0 / (s * pp);
+              const double is = pp * inv, ip = s * inv;
+              sh->bx[b] = pp * is;
+              sh->by[b] = Q * is;
+              sh->bz[b] = R * is;
+              sh->bq[b] = Q * ip;
+              sh->br[b] = R * ip;
+            }
+          }
+        } else if (lane == 0) {
+          sh->bon[b] = 0;
+        }
+      }
+      __syncthreads();
+      // (B) row updates: rows k..k+2, columns k..nn
+      if (warp < nbe && sh->bon[warp]) {
+        const int b = warp, k = sh->bk[b];
+        const bool three = sh->bthree[b] != 0;
+        const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
+        double* r0 = &a(k, 0);
+        double* r1 = &a(k + 1, 0);
+        double* r2 = &a(three ? k + 2 : k + 1, 0);
+        for (int j = k + lane; j <= nn; j += 32) {
+          const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
+          const double pp = a0 + q * a1 + r * a2;
+          if (three) r2[j] = a2 - pp * z;
+          r1[j] = a1 - pp * y;
+          r0[j] = a0 - pp * x;
+        }
+      }
+      __syncthreads();
+      // (C) column updates: columns k..k+2, rows l..min(nn, k+3)
+      if (warp < nbe && sh->bon[warp]) {
+        const int b = warp, k = sh->bk[b];
+        const bool three = sh->bthree[b] != 0;
+        const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
+        const int mmin = nn < k + 3 ? nn : k + 3;
+        for (int i = l + lane; i <= mmin; i += 32) {
+          double* ri = &a(i, 0);
+          const double c0 = ri[k], c1 = ri[k + 1], c2 = three ? ri[k + 2] : 0.0;
+          const double pp = x * c0 + y * c1 + z * c2;
+          if (three) ri[k + 2] = c2 - pp * r;
+          ri[k + 1] = c1 - pp * q;
+          ri[k] = c0 - pp;
+        }
+      }
+      __syncthreads();
+    }
+    if (tid == 0) { *total_its += 1; if (cnt) cnt[3] += 1; }
+    ++stall;
+  }
+  return status;
 }
 
 // Inverse iteration on the Hessenberg form H (row-major r x r, global) for eigenvalue lam, one
@@ -549,8 +785,11 @@ k4_frame_kernel(const K4Params p) {
             }
             al = wsum(al); be = wsum(be); ga = wsum(ga);
             if (ga != 0.0 && ga * ga > tol * tol * (al * be)) {
-              const double zeta = (be - al) * (0.5 / ga);
-              const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+              // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
+              // one division: t = sign(β-α)·2γ / (|β-α| + sqrt((β-α)² + 4γ²))
+              const double d = be - al;
+              const double sq = sqrt(fma(d, d, 4.0 * ga * ga));
+              const double t = (d >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(d) + sq);
               const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
               double* cp = sA + P[u] * m;
               double* cq = sA + Q[u] * m;
@@ -783,14 +1022,23 @@ k4_frame_kernel(const K4Params p) {
   }
   for (int i = tid; i < r; i += K4_THREADS) lam_raw[i] = make_double2(0.0, 0.0);
   __syncthreads();
-  if (warp == 0) {
-    int its = 0;
-    int qc[3] = {0, 0, 0};
-    const int rc = hessenberg_qr(HsAcc{hs, r}, r, lam_raw, lane, &its, qc);
-    if (lane == 0) {
-      sh_its = its;
+  {
+    __shared__ MsShared ms_sh;
+    __shared__ int qc_sh[4];
+    if (tid < 4) qc_sh[tid] = 0;
+    __shared__ int its_sh;
+    if (tid == 0) its_sh = 0;
+    __syncthreads();
+    int its_local = 0;
+    const int rc = multishift_qr(HsAcc{hs, r}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
+                                 warp == 0 ? qc_sh : nullptr);
+    if (warp == 0 && lane == 0) atomicAdd(&its_sh, its_local);
+    __syncthreads();
+    if (tid == 0) {
+      sh_its = its_sh;
       if (rc != 0) sh_status = 5;
-      res->qr_cnt[0] = qc[0]; res->qr_cnt[1] = qc[1]; res->qr_cnt[2] = qc[2];
+      res->qr_cnt[0] = qc_sh[0]; res->qr_cnt[1] = qc_sh[1]; res->qr_cnt[2] = qc_sh[2];
+      res->qr_cnt[3] = qc_sh[3];
     }
   }
   __syncthreads();
