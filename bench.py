@@ -35,6 +35,17 @@ M = 200
 WORKLOAD = "C4: 3840x2160x3 planar fp32 video stream, window m=200, background subtraction"
 
 
+def k1_traffic(kernel: str):
+    """dram bytes (read + write) per launch of `kernel` from the committed ncu capture summary
+    (profiles/k1_traffic.json, written from `ncu --set full`), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as fh:
+            d = json.load(fh)[kernel]
+        return int(d["dram_bytes_read"] + d["dram_bytes_write"])
+    except Exception:
+        return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -186,7 +197,7 @@ def run_ours(args):
         # device-resident pool of distinct frames (cycled only if HBM cannot hold them all)
         free, _ = torch.cuda.mem_get_info(dev)
         frame_bytes = n_loc * 4
-        ring_bytes = (M + args.workers + 2 + 1) * ((n_loc + 255) // 256 * 256) * 4
+        ring_bytes = (M + max(args.lag, args.workers + 1) + 1) * ((n_loc + 255) // 256 * 256) * 4
         budget = free - ring_bytes - 12 * 2**30
         need = M + 1 + W + K
         P = int(min(need, max(M + 2, budget // frame_bytes)))
@@ -195,7 +206,7 @@ def run_ours(args):
             pool[t].copy_(vs.frame(t, device=dev, row_slice=(b, e)))
         eng = StreamingDMD(n_loc, M, dtype="f32", background=True, workers=args.workers,
                            device=local, stream=stream, rank=rank, nranks=N, row_begin=b,
-                           n_global=n, nccl_uid=uid)
+                           n_global=n, nccl_uid=uid, lag=args.lag)
         info = eng.info()
         eng.init_window(pool[: M + 1])
         t = M + 1
@@ -276,7 +287,9 @@ def run_ours(args):
                    "ring_slots": info["ring_slots"], "pool_frames": P,
                    "l2": "no flush: every step streams the 20 GB ring (>> 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk,
-                     "unit": "GB/s", "frac": round(achieved / pk, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / pk, 4),
+                     "traffic": k1_traffic("k1_gram_kernel<float,true>"),
+                     "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
                      "kernel": "k1_gram_kernel<float,true>", "k1_ms_avg": round(k1_ms, 4),
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": pk_src,
                      "k1_share_of_step": round(k1_ms / (ms / K), 4),
@@ -327,7 +340,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workers", type=int, default=4)
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--lag", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -93,6 +93,9 @@ typedef struct sdmd_config {
   int32_t rank;       /* this rank, 0..nranks-1                                                 */
   int32_t nranks;     /* row shards; > 1 needs NCCL (uid from sdmd_nccl_unique_id on rank 0)   */
   const uint8_t* nccl_uid; /* 128 bytes, identical on all ranks; ignored when nranks == 1       */
+  int32_t lag;        /* background lag in frames (>= 1); 0 → workers + 1.  K1(t+lag) consumes the
+                       * background coefficients of frame t, so K4 may take up to lag frame periods */
+  int32_t pad_;
 } sdmd_config;
 
 typedef struct sdmd_info {

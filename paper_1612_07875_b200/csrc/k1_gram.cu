@@ -55,10 +55,16 @@ static __device__ __forceinline__ void k1_mbar_wait(unsigned long long* bar, uns
       : "memory");
 }
 
+static __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(k1_smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+static __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+static __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // Background partial-sum slots: [K1_WARPS][8 elements x 40 lanes(32 + 8 pad)], conflict-free for
 // both the per-warp writes (lanes contiguous) and the per-row reads of the reduction.
-constexpr int BG_LSTRIDE = 40;
-constexpr int BG_WSTRIDE = 8 * BG_LSTRIDE;
+template <typename T> struct BgLayout { static constexpr int L = sizeof(T) == 4 ? 40 : 36; static constexpr int W = 8 * L; };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -115,14 +121,21 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   constexpr int MAXQ = (K1_MAXU + K1_WARPS - 1) / K1_WARPS;
   // BG: NSLOT slots of per-warp partials; warps publish tile i into slot i % NSLOT and reduce
   // their 16-row share of tile i - LAGR, synchronised only by per-slot mbarriers (no CTA barrier)
-  constexpr int NSLOT = sizeof(T) == 4 ? 4 : 2;
+  constexpr int NSLOT = 2;
   constexpr int LAGR = NSLOT / 2;
+  // per-warp cp.async ring: DEPTH column chunks (one chunk = the warp's 256 rows of one column,
+  // 1 KB fp32 / 2 KB fp64) in flight across tile boundaries; each lane consumes exactly the bytes
+  // it copied, so no intra-warp synchronisation is needed
+  constexpr int CHUNK = kSuperTile * (int)sizeof(T);
+  constexpr int DEPTH = sizeof(T) == 4 ? 8 : (BG ? 2 : 4);
+  constexpr int LPC = CHUNK / 512;                     // 16-byte copies per lane per chunk
   __shared__ BT2 c_s[BG ? kMaxM : 1];
   __shared__ long long col_off[K1_WARPS][MAXQ];   // ring offset (slot * ld) of each warp column
   __shared__ int col_kd[K1_WARPS][MAXQ];          // Gram-column index, or -1
   __shared__ int col_kb[K1_WARPS][MAXQ];          // background coefficient index, or -1
   extern __shared__ __align__(16) unsigned char red_raw[];
-  BT2* red = reinterpret_cast<BT2*>(red_raw);
+  unsigned char* zring = red_raw;                                       // [K1_WARPS][DEPTH][CHUNK]
+  BT2* red = reinterpret_cast<BT2*>(red_raw + K1_WARPS * DEPTH * CHUNK);
   __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
   __shared__ int am_last;
 
@@ -168,12 +181,12 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   auto bg_reduce = [&](long long jt, T xv_t) {       // reduce CTA-local tile jt (BG only)
     const int slot = (int)(jt % NSLOT);
     k1_mbar_wait(&fullb[slot], (unsigned)((jt / NSLOT) & 1));
-    const BT2* rb = red + slot * (K1_WARPS * BG_WSTRIDE);
+    const BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W);
     double sx = 0.0, sy = 0.0;
     const int w0 = 8 * (lane >> 4);
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      const BT2 v = rb[(w0 + w) * BG_WSTRIDE + e_src * BG_LSTRIDE + l_src];
+      const BT2 v = rb[(w0 + w) * BgLayout<T>::W + e_src * BgLayout<T>::L + l_src];
       sx += (double)v.x;
       sy += (double)v.y;
     }
@@ -194,14 +207,44 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
 #pragma unroll
   for (int q = 0; q <= LAGR; ++q) xq[q] = (T)0;
 
+  // ---- chunk stream of this warp: s = (local tile) * cnt + q ------------------------------------
+  const long long ntl = (NT > blockIdx.x) ? (NT - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long long S = ntl * cnt;
+  unsigned char* wring = zring + warp * (DEPTH * CHUNK);
+  long long s_iss = 0;                    // next chunk to issue
+  long long t_iss = 0;                    // its local tile
+  int q_iss = 0;                          // its column
+  auto issue = [&]() {
+    if (s_iss < S) {
+      const char* g = reinterpret_cast<const char*>(ring + col_off[warp][q_iss] +
+                                                    (blockIdx.x + t_iss * gridDim.x) * (long long)kSuperTile);
+      unsigned char* d = wring + (int)(s_iss % DEPTH) * CHUNK;
+#pragma unroll
+      for (int c = 0; c < LPC; ++c) cp_async16(d + c * 512 + lane * 16, g + c * 512 + lane * 16);
+      if (++q_iss == cnt) { q_iss = 0; ++t_iss; }
+    }
+    ++s_iss;
+    cp_async_commit();                    // one group per chunk slot, empty at the tail
+  };
+#pragma unroll 1
+  for (int d = 0; d < DEPTH; ++d) issue();
+  VT xn[VPL];                             // x_t of the next tile (prefetched one tile ahead)
+  if (ntl > 0) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+      xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + (long long)blockIdx.x * kSuperTile + v * 32 * EPV) + lane);
+  }
+
   long long it = 0;
   for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
     const long long row0 = tile * kSuperTile;
     double xd[8];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
-      to_double(xv, xd + v * EPV);
+    for (int v = 0; v < VPL; ++v) to_double(xn[v], xd + v * EPV);
+    if (tile + gridDim.x < NT) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + row0 + (long long)gridDim.x * kSuperTile + v * 32 * EPV) + lane);
     }
     BgAcc<T> bacc;
     if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
@@ -210,52 +253,44 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
       xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
     }
-    const T* base = ring + row0;
+    const long long s0 = it * cnt;
 #pragma unroll
-    for (int q0 = 0; q0 < MAXQ; q0 += CB) {
-      if (q0 < cnt) {
-        VT z[CB][VPL];
+    for (int q = 0; q < MAXQ; ++q) {
+      if (q < cnt) {
+        cp_async_wait<DEPTH - 1>();                   // chunk s0 + q has landed (own bytes)
+        const unsigned char* src = wring + (int)((s0 + q) % DEPTH) * CHUNK;
+        VT zv[VPL];
 #pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          const int q = q0 + b;
-          if (q < MAXQ && q < cnt) {
-            const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
+        for (int v = 0; v < VPL; ++v)
+          zv[v] = *reinterpret_cast<const VT*>(src + v * 512 + lane * 16);
+        if (col_kd[warp][q] >= 0) {
+          double zd[8];
 #pragma unroll
-            for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
-          }
+          for (int v = 0; v < VPL; ++v) to_double(zv[v], zd + v * EPV);
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) { a0 = fma(xd[e], zd[e], a0); a1 = fma(xd[e + 1], zd[e + 1], a1); }
+          accv[q] += a0 + a1;
         }
-#pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          const int q = q0 + b;
-          if (q < MAXQ && q < cnt) {
-            if (col_kd[warp][q] >= 0) {
-              double zd[8];
-#pragma unroll
-              for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
-              double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-              for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
-              accv[q] += s0 + s1;
-            }
-            if (BG) {
-              const int kb = col_kb[warp][q];
-              if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&z[b][0]));
-            }
-          }
+        if (BG) {
+          const int kb = col_kb[warp][q];
+          if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&zv[0]));
         }
+        issue();                                      // refill the slot just consumed
       }
     }
     if (BG) {
       const int slot = (int)(it % NSLOT);
       if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
-      BT2* rb = red + slot * (K1_WARPS * BG_WSTRIDE) + warp * BG_WSTRIDE;
+      BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W) + warp * BgLayout<T>::W;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) rb[e * BG_LSTRIDE + lane] = bacc.v[e];
+      for (int e = 0; e < 8; ++e) rb[e * BgLayout<T>::L + lane] = bacc.v[e];
       __syncwarp();
       if (lane == 0) k1_mbar_arrive(&fullb[slot]);
       if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
     }
   }
+  cp_async_wait<0>();
   if (BG) {                                   // drain the last LAGR tiles
 #pragma unroll
     for (int q = LAGR - 1; q >= 0; --q)
@@ -301,22 +336,26 @@ __global__ void commit_kernel(const K1Params p) {
 }
 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
-  const int smem = p.bg ? (int)((dtype == 0 ? 4 : 2) * K1_WARPS * BG_WSTRIDE *
-                                (dtype == 0 ? sizeof(float2) : sizeof(double2))) : 0;
+  const int es = dtype == 0 ? 4 : 8;
+  const int depth = dtype == 0 ? 8 : (p.bg ? 2 : 4);
+  int smem = K1_WARPS * depth * kSuperTile * es;                  // cp.async rings
+  if (p.bg) smem += 2 * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
   cudaError_t e = cudaSuccess;
   if (dtype == 0) {
     if (p.bg) {
       e = cudaFuncSetAttribute(k1_gram_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e == cudaSuccess) k1_gram_kernel<float, true><<<grid, K1_THREADS, smem, s>>>(p);
     } else {
-      k1_gram_kernel<float, false><<<grid, K1_THREADS, 0, s>>>(p);
+      e = cudaFuncSetAttribute(k1_gram_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) k1_gram_kernel<float, false><<<grid, K1_THREADS, smem, s>>>(p);
     }
   } else {
     if (p.bg) {
       e = cudaFuncSetAttribute(k1_gram_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e == cudaSuccess) k1_gram_kernel<double, true><<<grid, K1_THREADS, smem, s>>>(p);
     } else {
-      k1_gram_kernel<double, false><<<grid, K1_THREADS, 0, s>>>(p);
+      e = cudaFuncSetAttribute(k1_gram_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess) k1_gram_kernel<double, false><<<grid, K1_THREADS, smem, s>>>(p);
     }
   }
   if (e != cudaSuccess) return e;

@@ -289,7 +289,7 @@ static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, i
 // Braman–Byers–Mathias; no aggressive early deflation.)
 constexpr int MS_NB = 8;           // bulges per sweep (<= K4_WARPS)
 constexpr int MS_SMALL = 32;       // blocks up to this size use the single-bulge iteration
-constexpr int MS_STALL = 6;        // sweeps without deflation before falling back
+constexpr int MS_STALL = 30;       // sweeps without deflation before falling back
 constexpr int MS_SPACING = 4;
 
 struct MsShared {
@@ -468,15 +468,15 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
         }
       }
       __syncthreads();
-      // (B) row updates: rows k..k+2, columns k..nn
-      if (warp < nbe && sh->bon[warp]) {
-        const int b = warp, k = sh->bk[b];
+      // (B) row updates: rows k..k+2, columns k..nn (two warps per bulge)
+      if ((warp >> 1) < nbe && sh->bon[warp >> 1]) {
+        const int b = warp >> 1, k = sh->bk[b];
         const bool three = sh->bthree[b] != 0;
         const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
         double* r0 = &a(k, 0);
         double* r1 = &a(k + 1, 0);
         double* r2 = &a(three ? k + 2 : k + 1, 0);
-        for (int j = k + lane; j <= nn; j += 32) {
+        for (int j = k + (warp & 1) * 32 + lane; j <= nn; j += 64) {
           const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
           const double pp = a0 + q * a1 + r * a2;
           if (three) r2[j] = a2 - pp * z;
@@ -485,13 +485,13 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
         }
       }
       __syncthreads();
-      // (C) column updates: columns k..k+2, rows l..min(nn, k+3)
-      if (warp < nbe && sh->bon[warp]) {
-        const int b = warp, k = sh->bk[b];
+      // (C) column updates: columns k..k+2, rows l..min(nn, k+3) (two warps per bulge)
+      if ((warp >> 1) < nbe && sh->bon[warp >> 1]) {
+        const int b = warp >> 1, k = sh->bk[b];
         const bool three = sh->bthree[b] != 0;
         const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
         const int mmin = nn < k + 3 ? nn : k + 3;
-        for (int i = l + lane; i <= mmin; i += 32) {
+        for (int i = l + (warp & 1) * 32 + lane; i <= mmin; i += 64) {
           double* ri = &a(i, 0);
           const double c0 = ri[k], c1 = ri[k + 1], c2 = three ? ri[k + 2] : 0.0;
           const double pp = x * c0 + y * c1 + z * c2;
@@ -511,100 +511,136 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
 // Inverse iteration on the Hessenberg form H (row-major r x r, global) for eigenvalue lam, one
 // warp.  Returns the right eigenvector w = Q z and (if yout) the left eigenvector y = Q u of the
 // ORIGINAL matrix Ã = Q H Qᵀ, both unit 2-norm; w additionally has its largest entry real > 0.
-// M: r*r complex workspace; smem: z, rhs (r complex each), lk (r complex), sw (r ints).
+// (H - λI) = P L U with adjacent-row pivoting is formed in one streaming pass: the pivot row is
+// carried in registers (lane j%32 owns column j), the rows of U are written once to the global
+// workspace M and read back by the triangular solves; l_k and the swap flags go to shared memory.
+// smem: z, rhs (r complex each), lk (r complex), sw (r ints).
+constexpr int IV_S = (kMaxR + 31) / 32;            // column slots per lane
+
+static __device__ __forceinline__ double2 iv_pick(const double2 (&v)[IV_S], int slot) {
+  double2 out = v[0];
+#pragma unroll
+  for (int s = 1; s < IV_S; ++s)
+    if (s == slot) out = v[s];
+  return out;
+}
+static __device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+static __device__ void iv_normalise(double2* z, int r, int lane) {
+  double nrm = 0.0;
+  for (int i = lane; i < r; i += 32) nrm = fmax(nrm, cabs2(z[i]));
+  nrm = wmax(nrm);
+  if (nrm == 0.0) nrm = 1.0;
+  const double in = 1.0 / nrm;
+  double ss = 0.0;
+  for (int i = lane; i < r; i += 32) { const double2 v = z[i]; ss += (v.x * in) * (v.x * in) + (v.y * in) * (v.y * in); }
+  ss = wsum(ss);
+  const double inv = in / sqrt(ss);
+  __syncwarp();
+  for (int i = lane; i < r; i += 32) z[i] = make_double2(z[i].x * inv, z[i].y * inv);
+  __syncwarp();
+}
+
+static __device__ void iv_apply_q(const double* Qv, const double* tau, int r, double2* v, int lane) {
+  for (int k = r - 3; k >= 0; --k) {                 // v <- P_k v, k = r-3 .. 0  (Q = P_0 … P_{r-3})
+    const double tk = tau[k];
+    if (tk == 0.0) continue;
+    const double* q = Qv + (long long)k * r;
+    double2 s = make_double2(0.0, 0.0);
+    for (int i = k + 1 + lane; i < r; i += 32) { const double qi = __ldcg(q + i); s.x = fma(qi, v[i].x, s.x); s.y = fma(qi, v[i].y, s.y); }
+    s = wsum2(s);
+    __syncwarp();
+    for (int i = k + 1 + lane; i < r; i += 32) {
+      const double qi = __ldcg(q + i);
+      v[i] = make_double2(v[i].x - tk * s.x * qi, v[i].y - tk * s.y * qi);
+    }
+    __syncwarp();
+  }
+}
+
 static __device__ void inverse_iteration(const double* H, const double* Qv, const double* tau, int r,
                                          double2 lam, double2* M, double2* z, double2* rhs,
                                          double2* lk, int* sw, double2* wout, double2* yout,
                                          int lane) {
   double hn = 0.0;
   for (int i = 0; i < r; ++i)
-    for (int j = (i > 0 ? i - 1 : 0) + lane; j < r; j += 32) {
-      const double h = H[(long long)i * r + j];
-      hn = fmax(hn, fabs(h));
-      double2 v = make_double2(h, 0.0);
-      if (i == j) v = csub(v, lam);
-      M[(long long)i * r + j] = v;
-    }
+    for (int j = (i > 0 ? i - 1 : 0) + lane; j < r; j += 32) hn = fmax(hn, fabs(__ldcg(H + (long long)i * r + j)));
   hn = wmax(hn);
   const double small = (hn > 0.0 ? hn : 1.0) * DBL_EPSILON;
+  // ---- streaming LU of (H - λI); U rows -> M (row-major, entries j >= k of row k)
+  double2 cur[IV_S], nxt[IV_S];
+  double pre[IV_S];
+#pragma unroll
+  for (int s = 0; s < IV_S; ++s) {
+    const int j = lane + 32 * s;
+    double h = (j < r) ? __ldcg(H + j) : 0.0;
+    cur[s] = make_double2(h - (j == 0 ? lam.x : 0.0), j == 0 ? -lam.y : 0.0);
+    pre[s] = (r > 1 && j < r) ? __ldcg(H + r + j) : 0.0;           // row 1, prefetched
+  }
+  for (int k = 0; k < r - 1; ++k) {
+#pragma unroll
+    for (int s = 0; s < IV_S; ++s) {                                 // row k+1 of H - λI
+      const int j = lane + 32 * s;
+      nxt[s] = make_double2(pre[s] - (j == k + 1 ? lam.x : 0.0), j == k + 1 ? -lam.y : 0.0);
+      pre[s] = (k + 2 < r && j < r) ? __ldcg(H + (long long)(k + 2) * r + j) : 0.0;
+    }
+    const double2 a = shfl2(iv_pick(cur, k >> 5), k & 31);
+    const double2 b = shfl2(iv_pick(nxt, k >> 5), k & 31);
+    const bool swp = cabs2(b) > cabs2(a);
+    double2 piv = swp ? b : a;
+    const double2 other = swp ? a : b;
+    if (cabs2(piv) == 0.0) piv = make_double2(small, 0.0);
+    const double2 l = cdiv(other, piv);
+#pragma unroll
+    for (int s = 0; s < IV_S; ++s) {
+      const int j = lane + 32 * s;
+      const double2 urow = swp ? nxt[s] : cur[s];
+      const double2 crow = swp ? cur[s] : nxt[s];
+      if (j >= k && j < r) M[(long long)k * r + j] = (j == k) ? piv : urow;
+      cur[s] = (j > k) ? csub(crow, cmul(l, urow)) : make_double2(0.0, 0.0);
+    }
+    if (lane == 0) { lk[k] = l; sw[k] = swp ? 1 : 0; }
+  }
+  {
+    const double2 d = shfl2(iv_pick(cur, (r - 1) >> 5), (r - 1) & 31);
+    if (lane == ((r - 1) & 31)) M[(long long)(r - 1) * r + r - 1] = (cabs2(d) == 0.0) ? make_double2(small, 0.0) : d;
+  }
+  __syncwarp();
+  // ---- right vector: two solves U z = (L⁻¹P) rhs, rhs = e then the normalised z
   for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
   __syncwarp();
-  // LU with adjacent-row partial pivoting (Hessenberg: one sub-diagonal)
-  for (int k = 0; k < r - 1; ++k) {
-    double2* Mk = M + (long long)k * r;
-    double2* Mk1 = M + (long long)(k + 1) * r;
-    const bool swp = cabs2(Mk1[k]) > cabs2(Mk[k]);
-    __syncwarp();
-    if (swp) {
-      for (int j = k + lane; j < r; j += 32) { const double2 t = Mk[j]; Mk[j] = Mk1[j]; Mk1[j] = t; }
-      if (lane == 0) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
-    }
-    __syncwarp();
-    double2 piv = Mk[k];
-    if (cabs2(piv) == 0.0) piv = make_double2(small, 0.0);
-    const double2 l = cdiv(Mk1[k], piv);
-    __syncwarp();
-    if (lane == 0) { Mk[k] = piv; lk[k] = l; sw[k] = swp ? 1 : 0; rhs[k + 1] = csub(rhs[k + 1], cmul(l, rhs[k])); }
-    for (int j = k + 1 + lane; j < r; j += 32) Mk1[j] = csub(Mk1[j], cmul(l, Mk[j]));
-    __syncwarp();
-  }
-  if (lane == 0 && cabs2(M[(long long)(r - 1) * r + r - 1]) == 0.0)
-    M[(long long)(r - 1) * r + r - 1] = make_double2(small, 0.0);
-  __syncwarp();
-
-  // ---- right vector: two solves U z = (L⁻¹P) rhs
   for (int it = 0; it < 2; ++it) {
-    if (it == 1) {   // rhs = z normalised, transformed by the stored row operations
-      if (lane == 0) {
-        for (int k = 0; k < r - 1; ++k) {
-          if (sw[k]) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
-          rhs[k + 1] = csub(rhs[k + 1], cmul(lk[k], rhs[k]));
-        }
+    if (lane == 0) {
+      for (int k = 0; k < r - 1; ++k) {
+        if (sw[k]) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
+        rhs[k + 1] = csub(rhs[k + 1], cmul(lk[k], rhs[k]));
       }
-      __syncwarp();
     }
+    __syncwarp();
     for (int i = r - 1; i >= 0; --i) {
       double2 s = make_double2(0.0, 0.0);
-      for (int j = i + 1 + lane; j < r; j += 32) s = cadd(s, cmul(M[(long long)i * r + j], z[j]));
+      for (int j = i + 1 + lane; j < r; j += 32) s = cadd(s, cmul(__ldcg(M + (long long)i * r + j), z[j]));
       s = wsum2(s);
-      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), M[(long long)i * r + i]);
+      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), __ldcg(M + (long long)i * r + i));
       __syncwarp();
     }
-    double nrm = 0.0;
-    for (int i = lane; i < r; i += 32) nrm = fmax(nrm, cabs2(z[i]));
-    nrm = wmax(nrm);
-    double ss = 0.0;
-    for (int i = lane; i < r; i += 32) { const double2 v = z[i]; ss += (v.x / nrm) * (v.x / nrm) + (v.y / nrm) * (v.y / nrm); }
-    ss = wsum(ss);
-    const double inv = 1.0 / (nrm * sqrt(ss));
-    __syncwarp();
-    for (int i = lane; i < r; i += 32) { z[i] = make_double2(z[i].x * inv, z[i].y * inv); rhs[i] = z[i]; }
+    iv_normalise(z, r, lane);
+    for (int i = lane; i < r; i += 32) rhs[i] = z[i];
     __syncwarp();
   }
-  // w = Q z  (Q = P_0 P_1 … P_{r-3}; apply P_{r-3} first)
   for (int i = lane; i < r; i += 32) wout[i] = z[i];
   __syncwarp();
-  for (int k = r - 3; k >= 0; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* v = Qv + (long long)k * r;
-    double2 s = make_double2(0.0, 0.0);
-    for (int i = k + 1 + lane; i < r; i += 32) s = cadd(s, make_double2(v[i] * wout[i].x, v[i] * wout[i].y));
-    s = wsum2(s);
-    __syncwarp();
-    for (int i = k + 1 + lane; i < r; i += 32)
-      wout[i] = csub(wout[i], make_double2(tk * s.x * v[i], tk * s.y * v[i]));
-    __syncwarp();
-  }
-  // normalise: unit norm, largest-|.| entry real positive (reading Q12)
-  {
+  iv_apply_q(Qv, tau, r, wout, lane);
+  {                                                  // unit norm, largest-|.| entry real > 0 (Q12)
     double best = -1.0;
     int bi = 0;
     double ss = 0.0;
     for (int i = lane; i < r; i += 32) {
-      const double a = cabs2(wout[i]);
-      ss += a * a;
-      if (a > best) { best = a; bi = i; }
+      const double av = cabs2(wout[i]);
+      ss += av * av;
+      if (av > best) { best = av; bi = i; }
     }
     ss = wsum(ss);
 #pragma unroll
@@ -613,9 +649,9 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
     }
-    const double2 piv = wout[bi];
-    const double ap = cabs2(piv);
-    const double2 ph = make_double2(piv.x / ap, -piv.y / ap);      // conj(piv)/|piv|
+    const double2 pv = wout[bi];
+    const double ap = cabs2(pv);
+    const double2 ph = make_double2(pv.x / ap, -pv.y / ap);
     const double inv = 1.0 / sqrt(ss);
     __syncwarp();
     for (int i = lane; i < r; i += 32) {
@@ -627,16 +663,15 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
     __syncwarp();
   }
   if (yout == nullptr) return;
-
-  // ---- left vector: Mᴴ u = e  →  Uᴴ a = e, then a ← S_k E_kᴴ a for k = r-2 … 0
+  // ---- left vector: Mᴴ u = e  →  Uᴴ a = rhs (forward), then a ← S_k E_kᴴ a for k = r-2 … 0
   for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
   __syncwarp();
   for (int it = 0; it < 2; ++it) {
     for (int i = 0; i < r; ++i) {
       double2 s = make_double2(0.0, 0.0);
-      for (int j = lane; j < i; j += 32) s = cadd(s, cmul(cconj(M[(long long)j * r + i]), z[j]));
+      for (int j = lane; j < i; j += 32) s = cadd(s, cmul(cconj(__ldcg(M + (long long)j * r + i)), z[j]));
       s = wsum2(s);
-      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), cconj(M[(long long)i * r + i]));
+      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), cconj(__ldcg(M + (long long)i * r + i)));
       __syncwarp();
     }
     if (lane == 0) {
@@ -646,31 +681,13 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
       }
     }
     __syncwarp();
-    double nrm = 0.0;
-    for (int i = lane; i < r; i += 32) nrm = fmax(nrm, cabs2(z[i]));
-    nrm = wmax(nrm);
-    double ss = 0.0;
-    for (int i = lane; i < r; i += 32) { const double2 v = z[i]; ss += (v.x / nrm) * (v.x / nrm) + (v.y / nrm) * (v.y / nrm); }
-    ss = wsum(ss);
-    const double inv = 1.0 / (nrm * sqrt(ss));
-    __syncwarp();
-    for (int i = lane; i < r; i += 32) { z[i] = make_double2(z[i].x * inv, z[i].y * inv); rhs[i] = z[i]; }
+    iv_normalise(z, r, lane);
+    for (int i = lane; i < r; i += 32) rhs[i] = z[i];
     __syncwarp();
   }
   for (int i = lane; i < r; i += 32) yout[i] = z[i];
   __syncwarp();
-  for (int k = r - 3; k >= 0; --k) {
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* v = Qv + (long long)k * r;
-    double2 s = make_double2(0.0, 0.0);
-    for (int i = k + 1 + lane; i < r; i += 32) s = cadd(s, make_double2(v[i] * yout[i].x, v[i] * yout[i].y));
-    s = wsum2(s);
-    __syncwarp();
-    for (int i = k + 1 + lane; i < r; i += 32)
-      yout[i] = csub(yout[i], make_double2(tk * s.x * v[i], tk * s.y * v[i]));
-    __syncwarp();
-  }
+  iv_apply_q(Qv, tau, r, yout, lane);
 }
 
 // ------------------------------------------------------------------ the per-frame kernel ------
@@ -748,61 +765,58 @@ k4_frame_kernel(const K4Params p) {
       __syncthreads();
       const int nsteps = (rd == 0) ? 2 * bs - 1 : bs;
       for (int st = 0; st < nsteps; ++st) {
-        for (int k0 = warp; k0 < bs; k0 += 2 * K4_WARPS) {
-          int P[2], Q[2];
-          bool act[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int kk = k0 + u * K4_WARPS;
-            if (kk < bs) {
-              if (rd == 0) { P[u] = rr_player(kk, st, 2 * bs); Q[u] = rr_player(2 * bs - 1 - kk, st, 2 * bs); }
-              else { P[u] = kk; Q[u] = bs + (kk + st) % bs; }
-              act[u] = gcol(P[u]) < m && gcol(Q[u]) < m;
-            } else { P[u] = Q[u] = 0; act[u] = false; }
+        {
+          // one column pair per half-warp (bs <= 32 pairs, 32 half-warps): 16 lanes x <=16 rows
+          constexpr int EH = kMaxM / 16;
+          const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
+          int P = 0, Q = 0;
+          bool act = false;
+          if (hw < bs) {
+            if (rd == 0) { P = rr_player(hw, st, 2 * bs); Q = rr_player(2 * bs - 1 - hw, st, 2 * bs); }
+            else { P = hw; Q = bs + (hw + st) % bs; }
+            act = gcol(P) < m && gcol(Q) < m;
           }
-          double ap[2][EL], aq[2][EL];
+          double ap[EH], aq[EH];
+          const double* cp = sA + P * m;
+          const double* cq = sA + Q * m;
+          double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const double* cp = sA + P[u] * m;
-            const double* cq = sA + Q[u] * m;
-#pragma unroll
-            for (int e = 0; e < EL; ++e) {
-              const int i = lane + 32 * e;
-              const bool ok = act[u] && i < m;
-              ap[u][e] = ok ? cp[i] : 0.0;
-              aq[u][e] = ok ? cq[i] : 0.0;
-            }
+          for (int e = 0; e < EH; ++e) {
+            const int i = hl + 16 * e;
+            const bool ok = act && i < m;
+            ap[e] = ok ? cp[i] : 0.0;
+            aq[e] = ok ? cq[i] : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            if (!act[u]) continue;
-            double al = 0.0, be = 0.0, ga = 0.0;
+          for (int e = 0; e < EH; ++e) {
+            al = fma(ap[e], ap[e], al);
+            be = fma(aq[e], aq[e], be);
+            ga = fma(ap[e], aq[e], ga);
+          }
 #pragma unroll
-            for (int e = 0; e < EL; ++e) {
-              al = fma(ap[u][e], ap[u][e], al);
-              be = fma(aq[u][e], aq[u][e], be);
-              ga = fma(ap[u][e], aq[u][e], ga);
-            }
-            al = wsum(al); be = wsum(be); ga = wsum(ga);
-            if (ga != 0.0 && ga * ga > tol * tol * (al * be)) {
-              // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
-              // one division: t = sign(β-α)·2γ / (|β-α| + sqrt((β-α)² + 4γ²))
-              const double d = be - al;
-              const double sq = sqrt(fma(d, d, 4.0 * ga * ga));
-              const double t = (d >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(d) + sq);
-              const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-              double* cp = sA + P[u] * m;
-              double* cq = sA + Q[u] * m;
+          for (int o = 8; o > 0; o >>= 1) {                 // reduce within the half-warp
+            al += __shfl_xor_sync(0xffffffffu, al, o);
+            be += __shfl_xor_sync(0xffffffffu, be, o);
+            ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          }
+          if (act && ga != 0.0 && ga * ga > tol * tol * (al * be)) {
+            // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
+            // one division: t = sign(β-α)·2γ / (|β-α| + sqrt((β-α)² + 4γ²))
+            const double d = be - al;
+            const double sq = sqrt(fma(d, d, 4.0 * ga * ga));
+            const double t = (d >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(d) + sq);
+            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+            double* wp = sA + P * m;
+            double* wq = sA + Q * m;
 #pragma unroll
-              for (int e = 0; e < EL; ++e) {
-                const int i = lane + 32 * e;
-                if (i < m) {
-                  cp[i] = c * ap[u][e] - sn * aq[u][e];
-                  cq[i] = sn * ap[u][e] + c * aq[u][e];
-                }
+            for (int e = 0; e < EH; ++e) {
+              const int i = hl + 16 * e;
+              if (i < m) {
+                wp[i] = c * ap[e] - sn * aq[e];
+                wq[i] = sn * ap[e] + c * aq[e];
               }
-              rot = 1;
             }
+            rot = 1;
           }
         }
         __syncthreads();

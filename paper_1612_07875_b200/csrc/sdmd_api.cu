@@ -220,7 +220,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       (cfg.dtype != SDMD_F32 && cfg.dtype != SDMD_F64) ||
       (cfg.storage != SDMD_DENSE && cfg.storage != SDMD_SPARSE) || cfg.nranks < 1 ||
       cfg.rank < 0 || cfg.rank >= cfg.nranks || cfg.r_max < 0 || cfg.workers < 0 ||
-      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0))
+      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxWorkers + 1)
     return SDMD_E_INVALID;
   if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
@@ -233,7 +233,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (rmax > SDMD_MAX_R) rmax = SDMD_MAX_R;
   c->cfg.r_max = rmax;
   c->W = c->cfg.workers > 0 ? c->cfg.workers : 4;
-  c->L = c->W + 1;
+  c->L = c->cfg.lag > 0 ? c->cfg.lag : c->W + 1;
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
   c->NH = 2 * (m + c->L + 4);

@@ -43,6 +43,7 @@ class Config(ctypes.Structure):
         ("threshold", ctypes.c_float), ("background", ctypes.c_int32), ("dmd", ctypes.c_int32),
         ("workers", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
+        ("lag", ctypes.c_int32), ("pad_", ctypes.c_int32),
     ]
 
 
@@ -150,7 +151,7 @@ class StreamingDMD:
                  threshold: float = 0.2, background: bool = False, dmd: bool = True,
                  workers: int = 4, device: int = 0, stream="torch", rank: int = 0,
                  nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
-                 nccl_uid: bytes | None = None):
+                 nccl_uid: bytes | None = None, lag: int = 0):
         L = lib()
         cfg = Config()
         L.sdmd_config_init(ctypes.byref(cfg))
@@ -179,6 +180,7 @@ class StreamingDMD:
         cfg.stream = ctypes.c_void_p(int(stream)) if stream is not None else None
         cfg.rank = int(rank)
         cfg.nranks = int(nranks)
+        cfg.lag = int(lag)
         self._uid = None
         if nccl_uid is not None:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)

@@ -59,7 +59,7 @@ def test_config_layout_and_validation(libpath):
     assert L.sdmd_config_init(ctypes.byref(cfg)) == 0
     assert abs(cfg.rank_tol - 1e-7) < 1e-20 and abs(cfg.threshold - 0.2) < 1e-7
     assert cfg.dmd == 1 and cfg.workers == 4 and cfg.nranks == 1
-    assert ctypes.sizeof(sdmd.Config) == 104
+    assert ctypes.sizeof(sdmd.Config) == 112
     h = ctypes.c_void_p()
     # invalid shapes are rejected before any CUDA call (works without a GPU)
     cfg.n_local = cfg.n_global = 100
