@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   // 1 KB fp32 / 2 KB fp64) in flight across tile boundaries; each lane consumes exactly the bytes
   // it copied, so no intra-warp synchronisation is needed
   constexpr int CHUNK = kSuperTile * (int)sizeof(T);
-  constexpr int DEPTH = sizeof(T) == 4 ? 8 : (BG ? 2 : 4);
+  constexpr int DEPTH = BG ? (sizeof(T) == 4 ? 8 : 2) : 1;
   constexpr int LPC = CHUNK / 512;                     // 16-byte copies per lane per chunk
   __shared__ BT2 c_s[BG ? kMaxM : 1];
   __shared__ long long col_off[K1_WARPS][MAXQ];   // ring offset (slot * ld) of each warp column
@@ -207,6 +207,71 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
 #pragma unroll
   for (int q = 0; q <= LAGR; ++q) xq[q] = (T)0;
 
+  long long it = 0;
+  if constexpr (!BG) {
+    // ---- no background: register streaming, CB columns (2 LDG.128 each) in flight per lane
+  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
+    const long long row0 = tile * kSuperTile;
+    double xd[8];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
+      to_double(xv, xd + v * EPV);
+    }
+    BgAcc<T> bacc;
+    if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
+      bacc.zero();
+#pragma unroll
+      for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
+      xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
+    }
+    const T* base = ring + row0;
+#pragma unroll
+    for (int q0 = 0; q0 < MAXQ; q0 += CB) {
+      if (q0 < cnt) {
+        VT z[CB][VPL];
+#pragma unroll
+        for (int b = 0; b < CB; ++b) {
+          const int q = q0 + b;
+          if (q < MAXQ && q < cnt) {
+            const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < CB; ++b) {
+          const int q = q0 + b;
+          if (q < MAXQ && q < cnt) {
+            if (col_kd[warp][q] >= 0) {
+              double zd[8];
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
+              double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
+              accv[q] += s0 + s1;
+            }
+            if (BG) {
+              const int kb = col_kb[warp][q];
+              if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&z[b][0]));
+            }
+          }
+        }
+      }
+    }
+    if (BG) {
+      const int slot = (int)(it % NSLOT);
+      if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
+      BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W) + warp * BgLayout<T>::W;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) rb[e * BgLayout<T>::L + lane] = bacc.v[e];
+      __syncwarp();
+      if (lane == 0) k1_mbar_arrive(&fullb[slot]);
+      if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
+    }
+  }
+  } else {
   // ---- chunk stream of this warp: s = (local tile) * cnt + q ------------------------------------
   const long long ntl = (NT > blockIdx.x) ? (NT - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const long long S = ntl * cnt;
@@ -235,7 +300,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + (long long)blockIdx.x * kSuperTile + v * 32 * EPV) + lane);
   }
 
-  long long it = 0;
   for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
     const long long row0 = tile * kSuperTile;
     double xd[8];
@@ -291,6 +355,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
     }
   }
   cp_async_wait<0>();
+  }
   if (BG) {                                   // drain the last LAGR tiles
 #pragma unroll
     for (int q = LAGR - 1; q >= 0; --q)
@@ -337,8 +402,8 @@ __global__ void commit_kernel(const K1Params p) {
 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
   const int es = dtype == 0 ? 4 : 8;
-  const int depth = dtype == 0 ? 8 : (p.bg ? 2 : 4);
-  int smem = K1_WARPS * depth * kSuperTile * es;                  // cp.async rings
+  const int depth = p.bg ? (dtype == 0 ? 8 : 2) : 0;
+  int smem = K1_WARPS * depth * kSuperTile * es;                  // cp.async rings (background path)
   if (p.bg) smem += 2 * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
   cudaError_t e = cudaSuccess;
   if (dtype == 0) {

@@ -711,7 +711,7 @@ static __device__ __forceinline__ void cl_sync() {
 }
 
 __global__ void __cluster_dims__(K4_CLUSTER, 1, 1) __launch_bounds__(K4_THREADS, 1)
-k4_frame_kernel(const K4Params p) {
+k4a_kernel(const K4Params p) {
   extern __shared__ __align__(16) unsigned char k4_smem[];
   __shared__ double mu[kMaxM];
   __shared__ double sig[kMaxM];
@@ -1016,13 +1016,45 @@ k4_frame_kernel(const K4Params p) {
     for (int e = tid; e < nr * r; e += K4_THREADS) p.H[(long long)r0 * r + e] = sH[e];
     cl_sync();
   }
-  double* H = p.H;
-  if (crank != 0) return;                                   // the rest runs on CTA 0
-  if (tid == 0) {
+  // K4a done: publish the factors' summary for K4b (same stream order via events)
+  if (crank == 0 && tid == 0) {
     if (r >= 2) p.tau[r - 2] = 0.0;
     p.tau[r > 0 ? r - 1 : 0] = 0.0;
     ph[5] = clock64();
+    res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
+    res->qr_its = 0; res->sigma1 = sig[0];
+    for (int q = 0; q < 5; ++q) res->phase[q] = ph[q + 1] - ph[q];
+    res->phase[5] = res->phase[6] = 0;
   }
+}
+
+// ------------------------------------------------------------------ K4b: eigen(Ã) and c -------
+// Single CTA: Francis multishift QR on the Hessenberg form (shared memory), ordering of λ, the
+// background index, inverse iteration for w_idx / y_idx, b_idx and the background coefficients.
+__global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
+  extern __shared__ __align__(16) unsigned char k4_smem[];
+  __shared__ int sh_status, sh_idx, sh_its, sh_go;
+  __shared__ long long ph[8];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = p.m;
+  const long long f = p.f;
+  K4Result* res = p.res;
+  {
+    volatile DevState* st = p.st;
+    if (st->status != 0 && st->failed_frame <= f) return;
+  }
+  if (tid == 0) {
+    const volatile K4Result* vr = res;
+    sh_go = (vr->frame == f && vr->status != 4 && vr->r > 0) ? 1 : 0;
+    sh_status = vr->status;
+    ph[5] = clock64();
+  }
+  __syncthreads();
+  if (!sh_go) return;                                      // K4a found a zero window (c = 0)
+  const int r = res->r;
+  const int sweeps = res->sweeps;
+  const double sigma1 = res->sigma1;
+  double* H = p.H;
 
   // ---- a8: eigenvalues by Francis double-shift QR in shared memory (warp 0)
   double* hs = reinterpret_cast<double*>(k4_smem);
@@ -1133,16 +1165,17 @@ k4_frame_kernel(const K4Params p) {
     }
     if (lane == 0) {
       ph[7] = clock64();
-      for (int q = 0; q < 8; ++q) res->phase[q] = ph[q];
+      res->phase[5] = ph[6] - ph[5];
+      res->phase[6] = ph[7] - ph[6];
       res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
-      res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sig[0];
+      res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sigma1;
     }
   } else if (idx < 0) {
     for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
     if (tid == 0) {
       res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
-      res->qr_its = sh_its; res->sigma1 = sig[0];
+      res->qr_its = sh_its; res->sigma1 = sigma1;
     }
   }
 }
@@ -1158,12 +1191,19 @@ size_t k4_smem_bytes(int r_max, int m) {
   return s > d ? s : d;
 }
 
-cudaError_t launch_k4(const K4Params& p, cudaStream_t s) {
+cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
   const size_t smem = k4_smem_bytes(p.r_max, p.m);
-  cudaError_t e = cudaFuncSetAttribute(k4_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k4a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k4_frame_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
+  k4a_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_k4b(const K4Params& p, cudaStream_t s) {
+  const size_t smem = k4_smem_bytes(p.r_max, p.m);
+  cudaError_t e = cudaFuncSetAttribute(k4b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k4b_kernel<<<1, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 

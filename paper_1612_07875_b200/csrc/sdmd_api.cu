@@ -50,8 +50,10 @@ NcclApi* nccl_api() {
 
 constexpr int kEvents = 64;
 
-struct Worker {
-  cudaStream_t s = nullptr;
+// Per-frame eigen workspace (K4a writes the factors, K4b reads them); indexed by frame mod NWS so
+// that K4a of a later frame never overwrites a workspace whose K4b is still pending.
+constexpr int kMaxWS = kMaxWorkers + 8;
+struct Workspace {
   double *A = nullptr, *Gxy = nullptr, *V = nullptr, *sigma = nullptr, *Y = nullptr, *B = nullptr;
   double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
   double2 *M = nullptr, *lam = nullptr, *w = nullptr, *y = nullptr;
@@ -92,7 +94,11 @@ struct sdmd_ctx {
   void* bg_sparse = nullptr;
   unsigned char* bg_mask = nullptr;
   // workers
-  Worker wk[kMaxWorkers];
+  Workspace ws[kMaxWS];
+  int NWS = 0, Wa = 1, Wb = 4;
+  cudaStream_t sa[kMaxWorkers]{};      // cluster eigen workers (K4a: Jacobi .. Hessenberg)
+  cudaStream_t sb[kMaxWorkers]{};      // single-CTA eigen workers (K4b: QR .. background coeffs)
+  cudaEvent_t ev_a[kEvents]{};
   cudaEvent_t ev_commit[kEvents]{};
   cudaEvent_t ev_done[kEvents]{};
   cudaEvent_t ev_k1[kEvents]{};         // after K1(t) on the main stream (slot-reuse fence)
@@ -158,7 +164,8 @@ static std::pair<cudaEvent_t, cudaEvent_t> new_pair() {
 static int sync_all(sdmd_ctx* c) {
   CK(cudaStreamSynchronize(c->copy_stream));
   CK(cudaStreamSynchronize(c->stream));
-  for (int w = 0; w < c->W; ++w) CK(cudaStreamSynchronize(c->wk[w].s));
+  for (int w = 0; w < c->Wa; ++w) CK(cudaStreamSynchronize(c->sa[w]));
+  for (int w = 0; w < c->Wb; ++w) CK(cudaStreamSynchronize(c->sb[w]));
   return SDMD_OK;
 }
 
@@ -220,7 +227,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       (cfg.dtype != SDMD_F32 && cfg.dtype != SDMD_F64) ||
       (cfg.storage != SDMD_DENSE && cfg.storage != SDMD_SPARSE) || cfg.nranks < 1 ||
       cfg.rank < 0 || cfg.rank >= cfg.nranks || cfg.r_max < 0 || cfg.workers < 0 ||
-      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxWorkers + 1)
+      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxWorkers + 4)
     return SDMD_E_INVALID;
   if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
@@ -233,7 +240,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (rmax > SDMD_MAX_R) rmax = SDMD_MAX_R;
   c->cfg.r_max = rmax;
   c->W = c->cfg.workers > 0 ? c->cfg.workers : 4;
-  c->L = c->cfg.lag > 0 ? c->cfg.lag : c->W + 1;
+  c->L = c->cfg.lag > 0 ? c->cfg.lag : c->W + 2;
+  c->Wb = c->W;
+  c->Wa = (c->W + 2) / 3;
+  c->NWS = c->L + 4;
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
   c->NH = 2 * (m + c->L + 4);
@@ -246,7 +256,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (e != cudaSuccess) { c->err = cudaGetErrorString(e); delete c; return SDMD_E_CUDA; }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->dev);
   // persistent K1 grid: one CTA per SM, leaving one SM per eigen worker (K4 runs concurrently)
-  c->k1_grid = c->cfg.dmd ? c->nsm - c->W * k4_cluster_size() : c->nsm;
+  c->k1_grid = c->cfg.dmd ? c->nsm - c->Wa * k4_cluster_size() - c->Wb : c->nsm;
   {
     const char* ev = std::getenv("SDMD_K1");
     c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
@@ -296,9 +306,12 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(c->bg_mask, (size_t)c->cfg.n_local);
   }
   const int R = kMaxR;
-  for (int w = 0; w < c->W; ++w) {
-    Worker& k = c->wk[w];
-    if (cudaStreamCreateWithFlags(&k.s, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+  for (int w = 0; w < c->Wa; ++w)
+    if (cudaStreamCreateWithFlags(&c->sa[w], cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+  for (int w = 0; w < c->Wb; ++w)
+    if (cudaStreamCreateWithFlags(&c->sb[w], cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+  for (int w = 0; w < c->NWS; ++w) {
+    Workspace& k = c->ws[w];
     AL(k.A, (size_t)m * m);
     AL(k.Gxy, (size_t)m * m);
     AL(k.V, (size_t)m * m);
@@ -324,7 +337,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     if (cudaEventCreateWithFlags(&c->ev_commit[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_k1[i], cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&c->ev_copy[i], cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_a[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(SDMD_E_CUDA);
   }
   if (c->cfg.nranks > 1) {
@@ -347,8 +361,10 @@ int sdmd_destroy(sdmd_ctx* c) {
   if (!c) return SDMD_OK;
   cudaSetDevice(c->dev);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (int w = 0; w < kMaxWorkers; ++w)
-    if (c->wk[w].s) cudaStreamSynchronize(c->wk[w].s);
+  for (int w = 0; w < kMaxWorkers; ++w) {
+    if (c->sa[w]) cudaStreamSynchronize(c->sa[w]);
+    if (c->sb[w]) cudaStreamSynchronize(c->sb[w]);
+  }
   if (c->comm) {
     NcclApi* api = nccl_api();
     if (api) api->CommDestroy(c->comm);
@@ -359,6 +375,7 @@ int sdmd_destroy(sdmd_ctx* c) {
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
     if (c->ev_k1[i]) cudaEventDestroy(c->ev_k1[i]);
     if (c->ev_copy[i]) cudaEventDestroy(c->ev_copy[i]);
+    if (c->ev_a[i]) cudaEventDestroy(c->ev_a[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
@@ -367,13 +384,16 @@ int sdmd_destroy(sdmd_ctx* c) {
                   c->Gtmp, c->init_work};
   for (void* p : ptrs)
     if (p) cudaFree(p);
-  for (int w = 0; w < kMaxWorkers; ++w) {
-    Worker& k = c->wk[w];
+  for (int w = 0; w < kMaxWS; ++w) {
+    Workspace& k = c->ws[w];
     void* wp[] = {k.A, k.Gxy, k.V, k.sigma, k.Y, k.B, k.H, k.Qv, k.tau, k.alpha1, k.M, k.lam, k.w,
                   k.y, k.res, k.flags, k.mu, k.wv, k.uv};
     for (void* p : wp)
       if (p) cudaFree(p);
-    if (k.s) cudaStreamDestroy(k.s);
+  }
+  for (int w = 0; w < kMaxWorkers; ++w) {
+    if (c->sa[w]) cudaStreamDestroy(c->sa[w]);
+    if (c->sb[w]) cudaStreamDestroy(c->sb[w]);
   }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -381,7 +401,7 @@ int sdmd_destroy(sdmd_ctx* c) {
 }
 
 static K4Params k4_params(sdmd_ctx* c, long long f) {
-  Worker& k = c->wk[f % c->W];
+  Workspace& k = c->ws[f % c->NWS];
   K4Params p{};
   p.ghist = c->ghist; p.NH = c->NH; p.m = c->cfg.m; p.f = f; p.r_max = c->cfg.r_max;
   p.rank_tol = c->cfg.rank_tol; p.st = c->dst;
@@ -391,6 +411,30 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
   return p;
+}
+
+// K4a (cluster) then K4b (single CTA) for frame t on the round-robin worker streams.
+static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
+  cudaError_t e;
+  cudaStream_t A = c->sa[t % c->Wa], B = c->sb[t % c->Wb];
+  if ((e = cudaStreamWaitEvent(A, c->ev_commit[t % kEvents], 0)) != cudaSuccess) return e;
+  if (t - c->NWS >= c->cfg.m)                  // workspace reuse: frame t-NWS must be finished
+    if ((e = cudaStreamWaitEvent(A, c->ev_done[(t - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
+  const K4Params p = k4_params(c, t);
+  std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
+  if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
+  if ((e = launch_k4a(p, A)) != cudaSuccess) return e;
+  if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); }
+  if ((e = cudaEventRecord(c->ev_a[t % kEvents], A)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(B, c->ev_a[t % kEvents], 0)) != cudaSuccess) return e;
+  if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
+  if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
+  if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); }
+  if ((e = cudaEventRecord(c->ev_done[t % kEvents], B)) != cudaSuccess) return e;
+  c->launches += 2;
+  c->ws[t % c->NWS].vecs_frame = -1;
+  c->last_dmd = t;
+  return cudaSuccess;
 }
 
 // Everything after the frame data sits in its slot: Gram column, reduction, DMD, events.
@@ -456,18 +500,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   c->last_nd = nd;
   CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
   CK(cudaEventRecord(c->ev_k1[t % kEvents], c->stream));
-  if (do_dmd) {
-    Worker& k = c->wk[t % c->W];
-    CK(cudaStreamWaitEvent(k.s, c->ev_commit[t % kEvents], 0));
-    std::pair<cudaEvent_t, cudaEvent_t> kp{};
-    if (c->timing) { kp = new_pair(); CK(cudaEventRecord(kp.first, k.s)); }
-    CK(launch_k4(k4_params(c, t), k.s));
-    c->launches += 1;
-    if (c->timing) { CK(cudaEventRecord(kp.second, k.s)); c->k4_ev.push_back(kp); }
-    CK(cudaEventRecord(c->ev_done[t % kEvents], k.s));
-    k.vecs_frame = -1;
-    c->last_dmd = t;
-  }
+  if (do_dmd) CK(enqueue_k4(c, t));
   c->frames = t + 1;
   return SDMD_OK;
 }
@@ -575,13 +608,7 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   if (c->cfg.dmd) {
     const long long t = m;
     CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
-    Worker& w = c->wk[t % c->W];
-    CK(cudaStreamWaitEvent(w.s, c->ev_commit[t % kEvents], 0));
-    CK(launch_k4(k4_params(c, t), w.s));
-    c->launches += 1;
-    CK(cudaEventRecord(c->ev_done[t % kEvents], w.s));
-    w.vecs_frame = -1;
-    c->last_dmd = t;
+    CK(enqueue_k4(c, t));
   }
   return SDMD_OK;
 }
@@ -590,7 +617,7 @@ int sdmd_join(sdmd_ctx* c) {
   if (!c) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   if (c->last_dmd < 0) return SDMD_OK;
-  for (long long f = c->last_dmd; f > c->last_dmd - c->W && f >= c->cfg.m; --f)
+  for (long long f = c->last_dmd; f > c->last_dmd - c->NWS && f >= c->cfg.m; --f)
     CK(cudaStreamWaitEvent(c->stream, c->ev_done[f % kEvents], 0));
   return SDMD_OK;
 }
@@ -660,7 +687,7 @@ static int newest_result(sdmd_ctx* c, K4Result* r) {
   int st = sync_all(c);
   if (st) return st;
   if (c->last_dmd < 0) return SDMD_E_WINDOW_NOT_FULL;
-  Worker& k = c->wk[c->last_dmd % c->W];
+  Workspace& k = c->ws[c->last_dmd % c->NWS];
   CK(cudaMemcpy(r, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
   if (r->frame != c->last_dmd) { c->err = "stale worker result"; return SDMD_E_STATE; }
   return SDMD_OK;
@@ -672,7 +699,7 @@ int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* fra
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  Worker& k = c->wk[c->last_dmd % c->W];
+  Workspace& k = c->ws[c->last_dmd % c->NWS];
   if (r) *r = res.r;
   if (frame) *frame = res.frame;
   const int m = c->cfg.m;
@@ -682,7 +709,7 @@ int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* fra
 }
 
 static int ensure_vecs(sdmd_ctx* c) {
-  Worker& k = c->wk[c->last_dmd % c->W];
+  Workspace& k = c->ws[c->last_dmd % c->NWS];
   if (k.vecs_frame == c->last_dmd) return SDMD_OK;
   K4Result res{};
   CK(cudaMemcpy(&res, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
@@ -714,7 +741,7 @@ int sdmd_get_spectrum(sdmd_ctx* c, int32_t* r, double* lambda, double* b, int32_
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  Worker& k = c->wk[c->last_dmd % c->W];
+  Workspace& k = c->ws[c->last_dmd % c->NWS];
   if (r) *r = res.r;
   if (idx) *idx = res.idx;
   if (frame) *frame = res.frame;
@@ -759,7 +786,7 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   if (dalloc(&c->Tbuf, (size_t)2 * m * ncols) != cudaSuccess) return SDMD_E_OOM;
   if (dalloc(&c->colbuf, (size_t)ncols) != cudaSuccess) return SDMD_E_OOM;
   CK(cudaMemcpy(c->colbuf, cols, ncols * sizeof(int), cudaMemcpyHostToDevice));
-  Worker& k = c->wk[c->last_dmd % c->W];
+  Workspace& k = c->ws[c->last_dmd % c->NWS];
   CK(launch_make_T(k.Y, m, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
   // X' of the frame's window = frames last_dmd-m+1 .. last_dmd
   CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - m + 1, m,
@@ -808,7 +835,7 @@ int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[16]) {
   for (int i = 0; i < 16; ++i) out[i] = 0;
   out[0] = res.frame; out[1] = res.status; out[2] = res.r; out[3] = res.idx;
   out[4] = res.sweeps; out[5] = res.qr_its;
-  for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q + 1] - res.phase[q];
+  for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q];
   out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[2];
   return SDMD_OK;
 }

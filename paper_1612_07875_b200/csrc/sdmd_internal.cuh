@@ -63,7 +63,7 @@ struct K4Result {
   double lam_idx[2];
   double b_idx[2];
   double sigma1;
-  long long phase[8];         // clock64() at phase boundaries (diagnostics)
+  long long phase[8];         // SM cycles per K4 phase: build S, Jacobi, sort/V, Ã, Hessenberg (K4a), QR, eigvec+c (K4b)
   int qr_cnt[4];              // QR: bulge-chase steps, deflation-scan and shift-search iterations
 };
 
@@ -158,7 +158,8 @@ cudaError_t launch_k1_tma(const K1Params& p, int dtype, int grid, cudaStream_t s
 size_t k1_tma_smem_bytes(int dtype, int bg);
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
-cudaError_t launch_k4(const K4Params& p, cudaStream_t s);
+cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
+cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
 size_t k4_smem_bytes(int r_max, int m);
 int k4_cluster_size();
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);

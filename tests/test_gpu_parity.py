@@ -345,9 +345,10 @@ def test_c4_full_size_sampled():
     configuration; the oracle recomputes sampled Gram entries one by one (fp64 dots of
     CPU-regenerated frames) and the background is checked by properties that hold at any size."""
     vs = synth.video_config("C4")
-    m, T = 200, 206
+    m = 200
     eng = Eng(vs.n, m, dtype="f32", background=True, workers=4)
     lag = eng.info()["lag"]
+    T = m + lag + 4
     for t in range(T):
         eng.push(vs.frame(t, device="cuda:0"))
     eng.sync()
@@ -422,4 +423,51 @@ def test_noisy_video_full_rank_spectrum(m):
     sv = eng.svd(with_V=False)
     keep = out["sigma"] / out["sigma"][0] >= 1e-4
     assert np.max(np.abs(sv["sigma"][keep] - out["sigma"][keep]) / out["sigma"][keep]) < 1e-10
+    eng.close()
+
+
+def test_constant_stream_fixed_point():
+    """S:346, S:353, S:377 on the device: a constant video has σ₁ = √m‖x‖, r = 1, λ_idx = 1 and
+    an all-background foreground (sparse ≈ 0, empty mask)."""
+    vs = synth.VideoStream(72, 96, 1, seed=5, n_squares=0, noise_sigma=0.0)
+    x = vs.frame(0).cuda()
+    m = 20
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+    lag = eng.info()["lag"]
+    for _ in range(m + lag + 3):
+        eng.push(x)
+    eng.sync()
+    sv = eng.svd(with_V=False)
+    xn = float(torch.linalg.norm(x.double()))
+    assert sv["r"] == 1
+    assert abs(sv["sigma"][0] - math.sqrt(m) * xn) < 1e-10 * sv["sigma"][0]
+    sp = eng.spectrum()
+    assert abs(sp["lam"][sp["idx"]] - 1.0) < 1e-9
+    low, spr, mask, fb = eng.background()
+    assert np.max(np.abs(spr)) < 1e-5 and not mask.any()
+    eng.close()
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled():
+    """BASELINE config 3 at full size (1920x1080 grey, m=100, fp32): sampled Gram entries vs CPU
+    fp64 dots of regenerated frames; background additivity and F-measure sanity."""
+    vs = synth.video_config("C3")
+    m = 100
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=4)
+    T = m + eng.info()["lag"] + 4
+    for t in range(T):
+        eng.push(vs.frame(t, device="cuda:0"))
+    eng.sync()
+    G = eng.gram()
+    t = T - 1
+    x_t = vs.frame(t).numpy().astype(np.float64)
+    for k in (0, 33, 99, 100):
+        z = vs.frame(t - m + k).numpy().astype(np.float64)
+        assert abs(G[k, m] - float(np.dot(z, x_t))) <= 1e-12 * math.sqrt(G[k, k] * G[m, m]), k
+    low, sp, mask, fb = eng.background()
+    x = vs.frame(fb).numpy().astype(np.float64)
+    assert np.max(np.abs(low.astype(np.float64) + sp - x)) < 1e-6
+    gt = vs.truth_mask(fb)
+    assert 2 * np.sum(mask & gt) / (mask.sum() + gt.sum()) > 0.85
     eng.close()
