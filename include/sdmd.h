@@ -48,6 +48,7 @@ extern "C" {
 
 #define SDMD_ABI_VERSION 1
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
+#define SDMD_MAX_LAG 16  /* largest background lag (frames)                                     */
 #define SDMD_MAX_R 224   /* largest rank r (shared-memory Hessenberg QR)    */
 
 enum sdmd_status {
@@ -87,14 +88,19 @@ typedef struct sdmd_config {
   int32_t background; /* 1: compute the newest background column every push (fused into the Gram
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
-  int32_t workers;    /* concurrent eigen-worker streams (0 → 4); lag = workers + 1           */
+  int32_t workers;    /* eigen-worker streams for the single-CTA stage (0 → 4); the cluster
+                       * stage uses max(1, workers / 2) streams.  The context uses about
+                       * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that
+                       * (e.g. 32) before CUDA initialises, else streams share hardware queues
+                       * and the eigen stages serialise behind unrelated waits                  */
   int32_t device;     /* CUDA device ordinal                                                   */
   void* stream;       /* cudaStream_t to order work on, or NULL (the ctx creates one)          */
   int32_t rank;       /* this rank, 0..nranks-1                                                 */
   int32_t nranks;     /* row shards; > 1 needs NCCL (uid from sdmd_nccl_unique_id on rank 0)   */
   const uint8_t* nccl_uid; /* 128 bytes, identical on all ranks; ignored when nranks == 1       */
-  int32_t lag;        /* background lag in frames (>= 1); 0 → workers + 1.  K1(t+lag) consumes the
-                       * background coefficients of frame t, so K4 may take up to lag frame periods */
+  int32_t lag;        /* background lag in frames, 1..16; 0 → min(2·workers, 16).  K1(t+lag)
+                       * consumes the background coefficients of frame t, so K4 may take up to
+                       * lag frame periods before the Gram pass waits                          */
   int32_t pad_;
 } sdmd_config;
 
@@ -103,9 +109,11 @@ typedef struct sdmd_info {
   int32_t window;       /* columns currently held (<= m+1)                                       */
   int32_t lag;          /* background of frame t is produced by the push of frame t + lag        */
   int32_t ring_slots;   /* HBM ring slots                                                        */
-  int32_t workers;      /* eigen-worker streams                                                  */
+  int32_t workers;      /* single-CTA eigen-stage streams (K4b)                                  */
   int64_t ring_bytes;   /* device bytes of the ring                                              */
   int64_t ld;           /* ring slot stride in elements                                          */
+  int32_t cluster_workers; /* streams of the 4-CTA cluster eigen stage (K4a)                     */
+  int32_t k1_grid;      /* CTAs per Gram pass                                                    */
 } sdmd_info;
 
 typedef struct sdmd_stats {
@@ -114,6 +122,8 @@ typedef struct sdmd_stats {
   int64_t k4_launches;  /* per-frame eigen (K4) launches                                         */
   double k4_ms;         /* summed device time of K4 (events on the worker streams)               */
   int64_t gpu_launches; /* all kernels this ctx launched since the last reset                   */
+  double k1_gap_ms;     /* summed ctx-stream time between consecutive Gram passes (ingest, waits) */
+  double k1_wait_ms;    /* part of k1_gap_ms spent waiting for background coefficients (K4)     */
 } sdmd_stats;
 
 /* Fill *cfg with defaults (rank_tol 1e-7, threshold 0.2, dmd 1, background 0, workers 4, …).
@@ -204,6 +214,12 @@ int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[16]);
 /* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */
 int sdmd_set_timing(sdmd_ctx* ctx, int enable);
 int sdmd_get_stats(sdmd_ctx* ctx, sdmd_stats* stats, int reset);
+/* Device timeline of the timed launches since the last stats reset (tracing aid).  Writes
+ * min(cap, count) records of 4 doubles {frame, kind, start_ms, end_ms} to host `out`; kind 0 = Gram
+ * pass (K1/K3), 1 = K4a, 2 = K4b, 3 = ctx-stream wait for background coefficients; times are
+ * relative to the first record's start.  *count = records available.  Synchronises the context.
+ * Errors: SDMD_E_INVALID (null ctx/count, cap < 0, out null with cap > 0). */
+int sdmd_get_timeline(sdmd_ctx* ctx, double* out, int cap, int* count);
 
 /* NCCL bootstrap: rank 0 calls this and broadcasts the 128 bytes (e.g. torch.distributed). */
 int sdmd_nccl_unique_id(uint8_t out[128]);

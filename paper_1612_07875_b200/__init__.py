@@ -4,5 +4,13 @@ The product is the C-ABI library ``libsdmd.so`` (include/sdmd.h) built from ``cs
 ``sdmd`` is its thin ctypes binding.  Importing this package does not load the library; the first
 call does, and fails loudly if it was not built (there is no CPU fallback).
 """
+import os as _os
+
+# The engine runs the Gram pass, the copy stream and up to 2·workers eigen streams concurrently;
+# CUDA's default of 8 hardware work queues makes some of them share a queue, so an eigen stage
+# waits behind an unrelated stream-wait (measured +5.5 ms per frame of K4 latency).  Only
+# effective if set before CUDA initialises in this process; an explicit user setting wins.
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .sdmd import (StreamingDMD, SDMDError, lib, nccl_unique_id, row_partition,  # noqa: F401
                    LIB_PATH, EXPORTS)

@@ -22,8 +22,7 @@ namespace sdmd {
 
 constexpr int K1_THREADS = 512;
 constexpr int K1_WARPS = K1_THREADS / 32;
-constexpr int K1_MAXU = kMaxM + kMaxWorkers + 8;   // union columns: m + lag (lag <= workers+1)
-constexpr int PSTRIDE = kMaxM + 16;                // partials row stride (doubles)
+constexpr int K1_MAXU = kMaxM + kMaxLag;          // union columns: m + lag
 
 template <typename T> struct VecOf;
 template <> struct VecOf<float> { using type = float4; static constexpr int E = 4; };
@@ -368,7 +367,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
     if (q < cnt) {
       const int kd = col_kd[warp][q];
       const double s = warp_sum(accv[q]);
-      if (lane == 0 && kd >= 0) p.partials[(long long)blockIdx.x * PSTRIDE + kd] = s;
+      if (lane == 0 && kd >= 0) p.partials[(long long)kd * p.pgrid + blockIdx.x] = s;
     }
   }
   __threadfence();
@@ -380,10 +379,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   __syncthreads();
   if (!am_last) return;
   __threadfence();
-  for (int k = tid; k < p.nd; k += K1_THREADS) {
+  // warp per Gram column, lanes stride over the CTA partials, fixed-order butterfly: deterministic
+  for (int k = warp; k < p.nd; k += K1_WARPS) {
+    const double* pk = p.partials + (long long)k * p.pgrid;
     double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += __ldcg(&p.partials[(long long)b * PSTRIDE + k]);
-    p.gout[k] = s;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(pk + b);
+    s = warp_sum(s);
+    if (lane == 0) p.gout[k] = s;
   }
   if (tid == 0) {
     p.st->k1_done = 0;
@@ -425,6 +427,17 @@ cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
   }
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+// Load every K1 instance at context creation: with lazy module loading the first launch of a
+// kernel otherwise loads it mid-stream (measured: a 26 ms stall on the first background pass).
+void preload_k1_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, false>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, true>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, false>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, true>);
+  cudaFuncGetAttributes(&a, commit_kernel);
 }
 
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s) {

@@ -22,7 +22,7 @@ constexpr int KT_THREADS = (KT_CONSUMERS + 1) * 32;    // + 1 producer warp
 constexpr int KT_STAGES = 5;
 constexpr int KT_CHUNK = 1024;                         // bytes per column chunk
 constexpr int KT_STAGE_BYTES = KT_CONSUMERS * KT_CHUNK;
-constexpr int KT_MAXU = kMaxM + kMaxWorkers + 8;
+constexpr int KT_MAXU = kMaxM + kMaxLag;
 constexpr int KT_MAXG = (KT_MAXU + KT_CONSUMERS - 1) / KT_CONSUMERS;
 constexpr int KT_PSTRIDE = kMaxM + 16;
 

@@ -1191,6 +1191,12 @@ size_t k4_smem_bytes(int r_max, int m) {
   return s > d ? s : d;
 }
 
+void preload_k4_kernels() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k4a_kernel);
+  cudaFuncGetAttributes(&a, k4b_kernel);
+}
+
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
   const size_t smem = k4_smem_bytes(p.r_max, p.m);
   cudaError_t e = cudaFuncSetAttribute(k4a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

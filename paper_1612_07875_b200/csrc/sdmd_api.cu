@@ -52,7 +52,7 @@ constexpr int kEvents = 64;
 
 // Per-frame eigen workspace (K4a writes the factors, K4b reads them); indexed by frame mod NWS so
 // that K4a of a later frame never overwrites a workspace whose K4b is still pending.
-constexpr int kMaxWS = kMaxWorkers + 8;
+constexpr int kMaxWS = kMaxLag + 4;      // per-frame eigen workspaces (NWS = lag + 4)
 struct Workspace {
   double *A = nullptr, *Gxy = nullptr, *V = nullptr, *sigma = nullptr, *Y = nullptr, *B = nullptr;
   double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
@@ -70,7 +70,7 @@ struct sdmd_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148;
+  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148;
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   bool k1_ldg = true;                   // SDMD_K1=tma selects the bulk-copy (TMA) K1 variant (A/B)
   long long ld = 0;
@@ -119,7 +119,9 @@ struct sdmd_ctx {
   long long last_dmd = -1;
   // timing
   bool timing = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev, wait_ev;
+  struct TL { long long f; int kind; cudaEvent_t a, b; };   // timeline view of the events above
+  std::vector<TL> tl;
   long long launches = 0;
   // nccl
   ncclComm_t comm = nullptr;
@@ -150,8 +152,11 @@ static cudaError_t dalloc(T** p, size_t count) {
 static void destroy_timing(sdmd_ctx* c) {
   for (auto& pr : c->k1_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   for (auto& pr : c->k4_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+  for (auto& pr : c->wait_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
   c->k1_ev.clear();
   c->k4_ev.clear();
+  c->wait_ev.clear();
+  c->tl.clear();
 }
 
 static std::pair<cudaEvent_t, cudaEvent_t> new_pair() {
@@ -227,7 +232,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       (cfg.dtype != SDMD_F32 && cfg.dtype != SDMD_F64) ||
       (cfg.storage != SDMD_DENSE && cfg.storage != SDMD_SPARSE) || cfg.nranks < 1 ||
       cfg.rank < 0 || cfg.rank >= cfg.nranks || cfg.r_max < 0 || cfg.workers < 0 ||
-      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxWorkers + 4)
+      cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxLag)
     return SDMD_E_INVALID;
   if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
@@ -240,9 +245,17 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (rmax > SDMD_MAX_R) rmax = SDMD_MAX_R;
   c->cfg.r_max = rmax;
   c->W = c->cfg.workers > 0 ? c->cfg.workers : 4;
-  c->L = c->cfg.lag > 0 ? c->cfg.lag : c->W + 2;
+  // default lag: two frame periods per worker; K4 latency (K4a + K4b ≈ 33 ms at m = 200) must
+  // fit in lag·t_K1 for the Gram pass never to wait
+  c->L = c->cfg.lag > 0 ? c->cfg.lag : (2 * c->W < kMaxLag ? 2 * c->W : kMaxLag);
   c->Wb = c->W;
-  c->Wa = (c->W + 2) / 3;
+  // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams
+  // keeps both stages' throughput above one frame per Gram pass (measured)
+  c->Wa = c->W / 2 > 0 ? c->W / 2 : 1;
+  if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
+    const int v = std::atoi(ea);
+    if (v >= 1 && v <= kMaxWorkers) c->Wa = v;
+  }
   c->NWS = c->L + 4;
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
@@ -255,8 +268,25 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   cudaError_t e = cudaSetDevice(c->dev);
   if (e != cudaSuccess) { c->err = cudaGetErrorString(e); delete c; return SDMD_E_CUDA; }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->dev);
-  // persistent K1 grid: one CTA per SM, leaving one SM per eigen worker (K4 runs concurrently)
-  c->k1_grid = c->cfg.dmd ? c->nsm - c->Wa * k4_cluster_size() - c->Wb : c->nsm;
+  preload_k1_kernels();
+  if (c->cfg.dmd) preload_k4_kernels();
+  // K1 grid.  Without DMD: persistent, one CTA per SM.  With DMD the eigen kernels (K4a/K4b) run
+  // concurrently on high-priority streams, so K1 is launched as `waves` x nsm short-lived CTAs
+  // (one resident per SM): whenever a K1 CTA retires, a pending K4 CTA or cluster takes the SM
+  // first, and the remaining K1 CTAs flow around it.  A persistent K1 would pin its SMs for the
+  // whole pass and make every K4 launch wait for a pass boundary (4-CTA clusters need 4 free SMs
+  // inside one GPC).
+  c->pgrid = c->nsm * kK1MaxWaves;
+  {
+    int waves = 8;
+    if (const char* ew = std::getenv("SDMD_K1_WAVES")) waves = std::atoi(ew);
+    if (waves < 0) waves = 0;
+    if (waves > kK1MaxWaves) waves = kK1MaxWaves;
+    // waves == 0: the persistent grid that leaves the eigen workers' SMs free
+    c->k1_grid = !c->cfg.dmd ? c->nsm
+                 : waves > 0 ? c->nsm * waves
+                             : c->nsm - c->Wa * k4_cluster_size() - c->Wb;
+  }
   {
     const char* ev = std::getenv("SDMD_K1");
     c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
@@ -294,7 +324,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   cudaMemsetAsync(c->ghist, 0, (size_t)c->NH * (m + 1) * sizeof(double), c->stream);
   AL(c->cbuf, (size_t)c->NC * m);
   cudaMemsetAsync(c->cbuf, 0, (size_t)c->NC * m * sizeof(double2), c->stream);
-  const size_t np = (size_t)(c->nsm > 0 ? c->nsm : 148) * (kMaxM + 16);
+  const size_t np = (size_t)c->pgrid * (kMaxM + 16);
   const size_t np3 = (size_t)(m + 1) * c->k3_chunks;
   AL(c->partials, np > np3 ? np : np3);
   AL(c->gout, (size_t)(m + 1));
@@ -306,10 +336,12 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(c->bg_mask, (size_t)c->cfg.n_local);
   }
   const int R = kMaxR;
+  int prio_lo = 0, prio_hi = 0;                     // eigen workers: highest stream priority
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
   for (int w = 0; w < c->Wa; ++w)
-    if (cudaStreamCreateWithFlags(&c->sa[w], cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+    if (cudaStreamCreateWithPriority(&c->sa[w], cudaStreamNonBlocking, prio_hi) != cudaSuccess) return bail(SDMD_E_CUDA);
   for (int w = 0; w < c->Wb; ++w)
-    if (cudaStreamCreateWithFlags(&c->sb[w], cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+    if (cudaStreamCreateWithPriority(&c->sb[w], cudaStreamNonBlocking, prio_hi) != cudaSuccess) return bail(SDMD_E_CUDA);
   for (int w = 0; w < c->NWS; ++w) {
     Workspace& k = c->ws[w];
     AL(k.A, (size_t)m * m);
@@ -424,12 +456,12 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
   if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
   if ((e = launch_k4a(p, A)) != cudaSuccess) return e;
-  if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); }
+  if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); c->tl.push_back({t, 1, ka.first, ka.second}); }
   if ((e = cudaEventRecord(c->ev_a[t % kEvents], A)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(B, c->ev_a[t % kEvents], 0)) != cudaSuccess) return e;
   if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
   if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
-  if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); }
+  if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); c->tl.push_back({t, 2, kb.first, kb.second}); }
   if ((e = cudaEventRecord(c->ev_done[t % kEvents], B)) != cudaSuccess) return e;
   c->launches += 2;
   c->ws[t % c->NWS].vecs_frame = -1;
@@ -446,9 +478,16 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   const bool bg = (c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
                    (t - c->L) <= c->last_dmd) ||
                   (c->bg_nodmd && c->cfg.background && !sparse && (t - c->L) >= m);
+  std::pair<cudaEvent_t, cudaEvent_t> tp{}, tw{};
+  if (c->timing) {                                // wait_ev: time the ctx stream spends waiting
+    tw = new_pair();                              // for the background coefficients of t - L
+    CK(cudaEventRecord(tw.first, c->stream));
+  }
   if (bg && c->cfg.dmd) CK(cudaStreamWaitEvent(c->stream, c->ev_done[(t - c->L) % kEvents], 0));
-  std::pair<cudaEvent_t, cudaEvent_t> tp{};
   if (c->timing) {
+    CK(cudaEventRecord(tw.second, c->stream));
+    c->wait_ev.push_back(tw);
+    c->tl.push_back({t, 3, tw.first, tw.second});
     tp = new_pair();
     CK(cudaEventRecord(tp.first, c->stream));
   }
@@ -459,12 +498,16 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.nd = nd; p.bg = bg ? 1 : 0; p.f_bg = bg ? t - c->L : 0;
     p.cbg = bg ? c->cbuf + ((t - c->L) % c->NC) * m : nullptr;
     p.lowrank = c->bg_low; p.sparse = c->bg_sparse; p.mask = c->bg_mask; p.thr = c->cfg.threshold;
-    p.partials = c->partials; p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist;
-    p.NH = c->NH; p.st = c->dst;
+    p.partials = c->partials; p.pgrid = c->pgrid; p.gout = c->gout; p.do_commit = do_commit;
+    p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
     if (c->k1_ldg) CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));
     else CK(launch_k1_tma(p, c->cfg.dtype, c->k1_grid, c->stream));
     c->launches += 1;
-    if (c->timing) { CK(cudaEventRecord(tp.second, c->stream)); c->k1_ev.push_back(tp); }
+    if (c->timing) {
+      CK(cudaEventRecord(tp.second, c->stream));
+      c->k1_ev.push_back(tp);
+      c->tl.push_back({t, 0, tp.first, tp.second});
+    }
     if (c->cfg.nranks > 1) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
       NcclApi* api = nccl_api();
@@ -483,7 +526,11 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
     CK(launch_k3(p, c->stream));
     c->launches += 2;
-    if (c->timing) { CK(cudaEventRecord(tp.second, c->stream)); c->k1_ev.push_back(tp); }
+    if (c->timing) {
+      CK(cudaEventRecord(tp.second, c->stream));
+      c->k1_ev.push_back(tp);
+      c->tl.push_back({t, 0, tp.first, tp.second});
+    }
     if (c->cfg.nranks > 1) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
       NcclApi* api = nccl_api();
@@ -653,6 +700,8 @@ int sdmd_get_info(sdmd_ctx* c, sdmd_info* info) {
   info->ring_bytes = c->cfg.storage == SDMD_DENSE ? (int64_t)c->NS * c->ld * c->es
                                                    : (int64_t)c->NS * c->cfg.nnz_cap * 12;
   info->ld = c->ld;
+  info->cluster_workers = c->Wa;
+  info->k1_grid = c->k1_grid;
   return SDMD_OK;
 }
 
@@ -856,9 +905,38 @@ int sdmd_get_stats(sdmd_ctx* c, sdmd_stats* s, int reset) {
   s->k1_ms = 0.0;
   s->k4_ms = 0.0;
   for (auto& pr : c->k1_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k1_ms += ms; }
+  s->k1_gap_ms = 0.0;                    // main-stream time between consecutive Gram passes
+  for (size_t i = 1; i < c->k1_ev.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, c->k1_ev[i - 1].second, c->k1_ev[i].first);
+    s->k1_gap_ms += ms;
+  }
   for (auto& pr : c->k4_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k4_ms += ms; }
+  s->k1_wait_ms = 0.0;
+  for (auto& pr : c->wait_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k1_wait_ms += ms; }
   s->gpu_launches = c->launches;
   if (reset) { destroy_timing(c); c->launches = 0; }
+  return SDMD_OK;
+}
+
+int sdmd_get_timeline(sdmd_ctx* c, double* out, int cap, int* count) {
+  if (!c || !count || cap < 0 || (cap > 0 && !out)) return invalid(c, "get_timeline: bad argument");
+  CK(cudaSetDevice(c->dev));
+  int st = sync_all(c);
+  if (st) return st;
+  *count = (int)c->tl.size();
+  if (c->tl.empty()) return SDMD_OK;
+  const cudaEvent_t t0 = c->tl.front().a;
+  const int k = cap < (int)c->tl.size() ? cap : (int)c->tl.size();
+  for (int i = 0; i < k; ++i) {
+    float s = 0, e = 0;
+    cudaEventElapsedTime(&s, t0, c->tl[i].a);
+    cudaEventElapsedTime(&e, t0, c->tl[i].b);
+    out[4 * i + 0] = (double)c->tl[i].f;
+    out[4 * i + 1] = (double)c->tl[i].kind;
+    out[4 * i + 2] = s;
+    out[4 * i + 3] = e;
+  }
   return SDMD_OK;
 }
 

@@ -16,6 +16,8 @@ namespace sdmd {
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
 constexpr int kMaxWorkers = 8;
+constexpr int kMaxLag = 16;              // background lag cap (frames); union columns m + lag
+constexpr int kK1MaxWaves = 32;           // K1 grid <= kK1MaxWaves x SM count
 constexpr int kSuperTile = 256;           // K1 rows per CTA iteration (32 lanes x 8 rows)
 
 struct DevState {
@@ -44,7 +46,8 @@ struct K1Params {
   void* sparse;               // n (dtype)
   unsigned char* mask;        // n
   float thr;
-  double* partials;           // [gridDim.x][kMaxM + 16]
+  double* partials;           // K1: [nd][pgrid] (column-major, coalesced reduction); TMA: [grid][kMaxM+16]
+  int pgrid;                  // partials stride of K1 (>= gridDim.x)
   double* gout;               // nd reduced values (pre-allreduce)
   int do_commit;              // nranks == 1: commit inside the kernel's last block
   double* ghist;
@@ -156,6 +159,8 @@ static __device__ __forceinline__ void commit_block(const double* gout, int nd, 
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s);
 cudaError_t launch_k1_tma(const K1Params& p, int dtype, int grid, cudaStream_t s);
 size_t k1_tma_smem_bytes(int dtype, int bg);
+void preload_k1_kernels();
+void preload_k4_kernels();
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);

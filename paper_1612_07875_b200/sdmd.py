@@ -30,7 +30,7 @@ EXPORTS = [
     "sdmd_get_gram", "sdmd_get_partial_gram_column", "sdmd_get_svd", "sdmd_get_spectrum",
     "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_get_frame_diag",
     "sdmd_set_timing",
-    "sdmd_get_stats", "sdmd_nccl_unique_id", "sdmd_status_string", "sdmd_last_error",
+    "sdmd_get_stats", "sdmd_get_timeline", "sdmd_nccl_unique_id", "sdmd_status_string", "sdmd_last_error",
     "sdmd_abi_version",
 ]
 
@@ -50,13 +50,15 @@ class Config(ctypes.Structure):
 class Info(ctypes.Structure):
     _fields_ = [("frames", ctypes.c_int64), ("window", ctypes.c_int32), ("lag", ctypes.c_int32),
                 ("ring_slots", ctypes.c_int32), ("workers", ctypes.c_int32),
-                ("ring_bytes", ctypes.c_int64), ("ld", ctypes.c_int64)]
+                ("ring_bytes", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("cluster_workers", ctypes.c_int32), ("k1_grid", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = [("k1_launches", ctypes.c_int64), ("k1_ms", ctypes.c_double),
                 ("k4_launches", ctypes.c_int64), ("k4_ms", ctypes.c_double),
-                ("gpu_launches", ctypes.c_int64)]
+                ("gpu_launches", ctypes.c_int64), ("k1_gap_ms", ctypes.c_double),
+                ("k1_wait_ms", ctypes.c_double)]
 
 
 class SDMDError(RuntimeError):
@@ -101,6 +103,8 @@ def lib():
         "sdmd_get_frame_diag": [vp, dp],
         "sdmd_set_timing": [vp, ctypes.c_int],
         "sdmd_get_stats": [vp, ctypes.POINTER(Stats), ctypes.c_int],
+        "sdmd_get_timeline": [vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
+                              ctypes.POINTER(ctypes.c_int)],
         "sdmd_nccl_unique_id": [vp],
         "sdmd_status_string": [ctypes.c_int],
         "sdmd_last_error": [vp],
@@ -374,6 +378,16 @@ class StreamingDMD:
         s = Stats()
         self._check(lib().sdmd_get_stats(self.h, ctypes.byref(s), 1 if reset else 0), "get_stats")
         return {k: getattr(s, k) for k, _ in Stats._fields_}
+
+    def timeline(self) -> np.ndarray:
+        """Device timeline since the last stats reset: rows {frame, kind, start_ms, end_ms}, kind
+        0 = Gram pass, 1 = K4a, 2 = K4b, 3 = wait for background coefficients."""
+        n = ctypes.c_int(0)
+        self._check(lib().sdmd_get_timeline(self.h, None, 0, ctypes.byref(n)), "get_timeline")
+        out = np.zeros((max(n.value, 1), 4), dtype=np.float64)
+        self._check(lib().sdmd_get_timeline(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                            n.value, ctypes.byref(n)), "get_timeline")
+        return out[:n.value]
 
 
 def row_partition(n: int, nranks: int, rank: int, align: int = 32) -> tuple[int, int]:

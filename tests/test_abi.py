@@ -60,6 +60,7 @@ def test_config_layout_and_validation(libpath):
     assert abs(cfg.rank_tol - 1e-7) < 1e-20 and abs(cfg.threshold - 0.2) < 1e-7
     assert cfg.dmd == 1 and cfg.workers == 4 and cfg.nranks == 1
     assert ctypes.sizeof(sdmd.Config) == 112
+    assert ctypes.sizeof(sdmd.Info) == 48 and ctypes.sizeof(sdmd.Stats) == 56
     h = ctypes.c_void_p()
     # invalid shapes are rejected before any CUDA call (works without a GPU)
     cfg.n_local = cfg.n_global = 100
