@@ -14,15 +14,32 @@
 // dots are warp-reduced per tile into shared memory (deterministic order), written per CTA, and
 // the last CTA to finish reduces the CTA partials in fixed order and commits the column into the
 // Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
+#include <cstdlib>
 #include <type_traits>
 
 #include "sdmd_internal.cuh"
 
 namespace sdmd {
 
+#ifndef K1_NSLOT
+#define K1_NSLOT 2        // background partial slots (tiles in flight between warps)
+#endif
+#ifndef K1_LAGR
+#define K1_LAGR 1         // tiles between publishing and reducing
+#endif
+#ifndef K1_BG_LDG
+#define K1_BG_LDG 1       // background path: 1 = register (LDG) streaming, 0 = bulk-copy rings
+#endif
+#ifndef K1_CB32
+#define K1_CB32 4         // fp32 background LDG path: columns (2 LDG.128 each) in flight per lane
+#endif
+#ifndef K1_DEPTH32
+#define K1_DEPTH32 8      // per-warp bulk-copy ring depth (fp32 chunks of 1 KB)
+#endif
 constexpr int K1_THREADS = 512;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_MAXU = kMaxM + kMaxLag;          // union columns: m + lag
+constexpr int K1_NQMAX = (K1_MAXU + K1_WARPS - 1) / K1_WARPS;
 
 template <typename T> struct VecOf;
 template <> struct VecOf<float> { using type = float4; static constexpr int E = 4; };
@@ -54,12 +71,6 @@ static __device__ __forceinline__ void k1_mbar_wait(unsigned long long* bar, uns
       : "memory");
 }
 
-static __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(k1_smem_u32(sdst)), "l"(gsrc) : "memory");
-}
-static __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-static __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Background partial-sum slots: [K1_WARPS][8 elements x 40 lanes(32 + 8 pad)], conflict-free for
 // both the per-warp writes (lanes contiguous) and the per-row reads of the reduction.
@@ -80,62 +91,106 @@ static __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return *reinterpret_cast<float2*>(&d);
 }
 
-template <typename T> struct BgAcc;     // per-lane background accumulator of one row (re, im)
+template <typename T> struct BgAcc;     // per-lane background accumulators of 8 rows (re, im)
 template <> struct BgAcc<float> {
-  // fp32 (re, im) pairs with packed FFMA2: per-warp sums of ~m/16 terms, followed by an fp64
-  // cross-warp sum; error ~1e-6 relative, inside the fp32-path tolerance (1e-4)
-  using C2 = float2;
-  float2 v[8];
+  // fp32 with packed FFMA2 on natural register pairs: re/im of rows (e, e+1); per-warp sums of
+  // ~m/16 terms, then an fp64 cross-warp sum: error ~1e-6 relative, inside the fp32-path
+  // tolerance (1e-4)
+  using C2 = float2;                   // reduction-slot element (re, im) of one row
+  using CW = float4;                   // per-column coefficient entry (c.x, c.x, c.y, c.y)
+  float2 re[4], im[4];
+  static __device__ __forceinline__ CW make(double2 c) {
+    return make_float4((float)c.x, (float)c.x, (float)c.y, (float)c.y);
+  }
   __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = make_float2(0.f, 0.f);
+    for (int i = 0; i < 4; ++i) { re[i] = make_float2(0.f, 0.f); im[i] = make_float2(0.f, 0.f); }
   }
-  __device__ __forceinline__ void add(const float2 c, const float* z) {
+  __device__ __forceinline__ void add(const CW c, const float* z) {
+    const float2 cr = make_float2(c.x, c.y), ci = make_float2(c.z, c.w);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = ffma2(c, make_float2(z[e], z[e]), v[e]);
+    for (int i = 0; i < 4; ++i) {
+      const float2 zz = make_float2(z[2 * i], z[2 * i + 1]);
+      re[i] = ffma2(cr, zz, re[i]);
+      im[i] = ffma2(ci, zz, im[i]);
+    }
+  }
+  __device__ __forceinline__ C2 get(int e) const {
+    return (e & 1) ? make_float2(re[e >> 1].y, im[e >> 1].y) : make_float2(re[e >> 1].x, im[e >> 1].x);
   }
 };
 template <> struct BgAcc<double> {
   using C2 = double2;
+  using CW = double2;
   double2 v[8];
+  static __device__ __forceinline__ CW make(double2 c) { return c; }
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int e = 0; e < 8; ++e) v[e] = make_double2(0.0, 0.0);
   }
-  __device__ __forceinline__ void add(const double2 c, const double* z) {
+  __device__ __forceinline__ void add(const CW c, const double* z) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) { v[e].x = fma(c.x, z[e], v[e].x); v[e].y = fma(c.y, z[e], v[e].y); }
   }
+  __device__ __forceinline__ C2 get(int e) const { return v[e]; }
 };
 
-template <typename T, bool BG>
-// One 512-thread CTA per SM (<= 128 registers): 16 warps x 8 LDG.128 per lane in flight ≈ 64 KB
-// per SM.  The grid leaves the eigen-worker SMs free (K4 runs concurrently on its own SMs).
+static __device__ __forceinline__ void k1_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(k1_smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// try_wait spin without the release/acquire sem of k1_mbar_wait (the bulk copy's complete_tx
+// makes the bytes visible to the waiting threads)
+static __device__ __forceinline__ void k1_mbar_wait_tx(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "K1_WAIT_TX:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra K1_DONE_TX;\n\t"
+      "bra K1_WAIT_TX;\n"
+      "K1_DONE_TX:\n\t}" ::"r"(k1_smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+static __device__ __forceinline__ void k1_bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                                   unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(k1_smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(k1_smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
+template <typename T, bool BG, int NQ>
+// One 512-thread CTA per SM (<= 128 registers).  Without the background: register streaming,
+// 16 warps x CB columns x 2 LDG.128 per lane in flight.  With the background: per-warp rings of
+// DEPTH column chunks filled by one-instruction bulk copies (cp.async.bulk, mbarrier complete_tx)
+// so that address generation costs one lane per 1 KB instead of every lane per 16 bytes.
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p) {
   using VT = typename VecOf<T>::type;
   using BT2 = typename BgAcc<T>::C2;
+  using CW = typename BgAcc<T>::CW;
   constexpr int EPV = VecOf<T>::E;          // elements per 16-byte vector
   constexpr int VPL = 8 / EPV;              // vectors per lane per column (8 rows per lane)
-  constexpr int CB = sizeof(T) == 4 ? 4 : (BG ? 1 : 2);  // columns in flight per batch
-  constexpr int MAXQ = (K1_MAXU + K1_WARPS - 1) / K1_WARPS;
+  constexpr int CB = sizeof(T) == 4 ? (BG ? K1_CB32 : 4) : 2;   // columns in flight per batch (LDG)
+  constexpr int MAXQ = NQ;                  // columns per warp (union U <= 16·NQ, host-checked)
   // BG: NSLOT slots of per-warp partials; warps publish tile i into slot i % NSLOT and reduce
   // their 16-row share of tile i - LAGR, synchronised only by per-slot mbarriers (no CTA barrier)
-  constexpr int NSLOT = 2;
-  constexpr int LAGR = NSLOT / 2;
-  // per-warp cp.async ring: DEPTH column chunks (one chunk = the warp's 256 rows of one column,
-  // 1 KB fp32 / 2 KB fp64) in flight across tile boundaries; each lane consumes exactly the bytes
-  // it copied, so no intra-warp synchronisation is needed
+  constexpr int NSLOT = K1_NSLOT;
+  constexpr int LAGR = K1_LAGR;
+  static_assert(LAGR >= 1 && LAGR < NSLOT, "reduction lag must leave a free slot");
+  // BG: per-warp ring of DEPTH chunks (one chunk = the warp's 256 rows of one column, 1 KB fp32 /
+  // 2 KB fp64), in flight across tile boundaries
   constexpr int CHUNK = kSuperTile * (int)sizeof(T);
-  constexpr int DEPTH = BG ? (sizeof(T) == 4 ? 8 : 2) : 1;
-  constexpr int LPC = CHUNK / 512;                     // 16-byte copies per lane per chunk
-  __shared__ BT2 c_s[BG ? kMaxM : 1];
+  constexpr int DEPTH = (BG && !K1_BG_LDG) ? (sizeof(T) == 4 ? K1_DEPTH32 : 2) : 0;
+  __shared__ __align__(16) CW cw_s[BG ? K1_WARPS : 1][BG ? MAXQ : 1];   // coefficient per warp column
   __shared__ long long col_off[K1_WARPS][MAXQ];   // ring offset (slot * ld) of each warp column
   __shared__ int col_kd[K1_WARPS][MAXQ];          // Gram-column index, or -1
-  __shared__ int col_kb[K1_WARPS][MAXQ];          // background coefficient index, or -1
-  extern __shared__ __align__(16) unsigned char red_raw[];
+  extern __shared__ __align__(128) unsigned char red_raw[];
   unsigned char* zring = red_raw;                                       // [K1_WARPS][DEPTH][CHUNK]
   BT2* red = reinterpret_cast<BT2*>(red_raw + K1_WARPS * DEPTH * CHUNK);
   __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
+  __shared__ unsigned long long zbar[DEPTH > 0 ? K1_WARPS * DEPTH : 1];
   __shared__ int am_last;
 
   if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
@@ -149,16 +204,16 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
     const long long f = F0 + j;
     col_off[w][q] = (j < U) ? (f % p.NS) * p.ld : 0;
     col_kd[w][q] = (j < U && f >= f_dot0) ? (int)(f - f_dot0) : -1;
-    col_kb[w][q] = (BG && j < U && f >= f_bg0 && f - f_bg0 < p.m) ? (int)(f - f_bg0) : -1;
+    if (BG) {
+      const bool inb = j < U && f >= f_bg0 && f - f_bg0 < p.m;
+      cw_s[w][q] = BgAcc<T>::make(inb ? p.cbg[f - f_bg0] : make_double2(0.0, 0.0));
+    }
   }
   if (BG) {
-    for (int k = tid; k < p.m; k += K1_THREADS) {
-      const double2 c = p.cbg[k];
-      c_s[k].x = c.x;
-      c_s[k].y = c.y;
-    }
     if (tid == 0)
       for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], K1_WARPS); }
+    if (tid < K1_WARPS * DEPTH) k1_mbar_init(&zbar[tid], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
@@ -171,78 +226,36 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   double accv[MAXQ];
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) accv[q] = 0.0;
-  // reduction share of this lane: row rt of a tile <- element e_src of lane l_src, source warps
-  // [8·(lane>>4), +8); lanes 0..15 write the outputs of rows 16·warp + lane
-  const int rt_red = 16 * warp + (lane & 15);
-  const int e_src = (rt_red / (32 * EPV)) * EPV + rt_red % EPV;
-  const int l_src = (rt_red % (32 * EPV)) / EPV;
-  const T* bg_col = BG ? ring + (p.f_bg % p.NS) * p.ld : ring;
-  auto bg_reduce = [&](long long jt, T xv_t) {       // reduce CTA-local tile jt (BG only)
-    const int slot = (int)(jt % NSLOT);
-    k1_mbar_wait(&fullb[slot], (unsigned)((jt / NSLOT) & 1));
-    const BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W);
-    double sx = 0.0, sy = 0.0;
-    const int w0 = 8 * (lane >> 4);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const BT2 v = rb[(w0 + w) * BgLayout<T>::W + e_src * BgLayout<T>::L + l_src];
-      sx += (double)v.x;
-      sy += (double)v.y;
-    }
-    sx += __shfl_xor_sync(0xffffffffu, sx, 16);
-    sy += __shfl_xor_sync(0xffffffffu, sy, 16);
-    const long long row = (blockIdx.x + jt * (long long)gridDim.x) * kSuperTile + rt_red;
-    if (lane < 16 && row < p.n) {
-      const double l = sqrt(sx * sx + sy * sy);                   // |l| (Q8)
-      const double sp = (double)xv_t - l;                         // s = x - |l|
-      ((T*)p.lowrank)[row] = (T)l;
-      ((T*)p.sparse)[row] = (T)sp;
-      p.mask[row] = (sp > (double)p.thr) ? 1 : 0;                 // strict '>'
-    }
-    __syncwarp();
-    if (lane == 0) k1_mbar_arrive(&emptyb[slot]);
-  };
-  T xq[LAGR + 1];                                    // prefetched x_{f_bg} rows of pending tiles
-#pragma unroll
-  for (int q = 0; q <= LAGR; ++q) xq[q] = (T)0;
 
   long long it = 0;
   if constexpr (!BG) {
-    // ---- no background: register streaming, CB columns (2 LDG.128 each) in flight per lane
-  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
-    const long long row0 = tile * kSuperTile;
-    double xd[8];
+    // ---- no background: register streaming, CB columns (VPL LDG.128 each) in flight per lane
+    for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
+      const long long row0 = tile * kSuperTile;
+      double xd[8];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
-      to_double(xv, xd + v * EPV);
-    }
-    BgAcc<T> bacc;
-    if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
-      bacc.zero();
+      for (int v = 0; v < VPL; ++v) {
+        VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
+        to_double(xv, xd + v * EPV);
+      }
+      const T* base = ring + row0;
 #pragma unroll
-      for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
-      xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
-    }
-    const T* base = ring + row0;
+      for (int q0 = 0; q0 < MAXQ; q0 += CB) {
+        if (q0 < cnt) {
+          VT z[CB][VPL];
 #pragma unroll
-    for (int q0 = 0; q0 < MAXQ; q0 += CB) {
-      if (q0 < cnt) {
-        VT z[CB][VPL];
+          for (int b = 0; b < CB; ++b) {
+            const int q = q0 + b;
+            if (q < MAXQ && q < cnt) {
+              const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
 #pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          const int q = q0 + b;
-          if (q < MAXQ && q < cnt) {
-            const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
+              for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
+            }
           }
-        }
 #pragma unroll
-        for (int b = 0; b < CB; ++b) {
-          const int q = q0 + b;
-          if (q < MAXQ && q < cnt) {
-            if (col_kd[warp][q] >= 0) {
+          for (int b = 0; b < CB; ++b) {
+            const int q = q0 + b;
+            if (q < MAXQ && q < cnt) {
               double zd[8];
 #pragma unroll
               for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
@@ -251,114 +264,193 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
               for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
               accv[q] += s0 + s1;
             }
-            if (BG) {
-              const int kb = col_kb[warp][q];
-              if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&z[b][0]));
-            }
           }
         }
       }
     }
-    if (BG) {
-      const int slot = (int)(it % NSLOT);
-      if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
+  } else {
+    // reduction share of this lane: row rt of a tile <- element e_src of lane l_src, source warps
+    // [8·(lane>>4), +8); lanes 0..15 write the outputs of rows 16·warp + lane
+    const int rt_red = 16 * warp + (lane & 15);
+    const int e_src = (rt_red / (32 * EPV)) * EPV + rt_red % EPV;
+    const int l_src = (rt_red % (32 * EPV)) / EPV;
+    const T* bg_col = ring + (p.f_bg % p.NS) * p.ld;
+    int rd_slot = 0;                                 // slot / phase of the next tile to reduce
+    unsigned rd_par = 0;
+    auto bg_reduce = [&](long long jt, T xv_t) {       // reduce CTA-local tile jt (in order)
+      const int slot = rd_slot;
+      k1_mbar_wait(&fullb[slot], rd_par);
+      if (++rd_slot == NSLOT) { rd_slot = 0; rd_par ^= 1u; }
+      const BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W);
+      double sx = 0.0, sy = 0.0;
+      const int w0 = 8 * (lane >> 4);
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const BT2 v = rb[(w0 + w) * BgLayout<T>::W + e_src * BgLayout<T>::L + l_src];
+        sx += (double)v.x;
+        sy += (double)v.y;
+      }
+      sx += __shfl_xor_sync(0xffffffffu, sx, 16);
+      sy += __shfl_xor_sync(0xffffffffu, sy, 16);
+      const long long row = (blockIdx.x + jt * (long long)gridDim.x) * kSuperTile + rt_red;
+      if (lane < 16 && row < p.n) {
+        const double l = sqrt(sx * sx + sy * sy);                   // |l| (Q8)
+        const double sp = (double)xv_t - l;                         // s = x - |l|
+        ((T*)p.lowrank)[row] = (T)l;
+        ((T*)p.sparse)[row] = (T)sp;
+        p.mask[row] = (sp > (double)p.thr) ? 1 : 0;                 // strict '>'
+      }
+      __syncwarp();
+      if (lane == 0) k1_mbar_arrive(&emptyb[slot]);
+    };
+    T xq[LAGR + 1];                                  // prefetched x_{f_bg} rows of pending tiles
+#pragma unroll
+    for (int q = 0; q <= LAGR; ++q) xq[q] = (T)0;
+    int p_slot = 0, p_round = 0;            // partial slot of this tile, tiles / NSLOT
+    // end of tile `it`: publish this warp's per-row partials, reduce tile it - LAGR
+    auto tile_end = [&](const BgAcc<T>& bacc) {
+      const int slot = p_slot;
+      if (p_round > 0) k1_mbar_wait(&emptyb[slot], (unsigned)((p_round - 1) & 1));
+      if (++p_slot == NSLOT) { p_slot = 0; ++p_round; }
       BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W) + warp * BgLayout<T>::W;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) rb[e * BgLayout<T>::L + lane] = bacc.v[e];
+      for (int e = 0; e < 8; ++e) rb[e * BgLayout<T>::L + lane] = bacc.get(e);
       __syncwarp();
       if (lane == 0) k1_mbar_arrive(&fullb[slot]);
       if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
-    }
-  }
-  } else {
-  // ---- chunk stream of this warp: s = (local tile) * cnt + q ------------------------------------
-  const long long ntl = (NT > blockIdx.x) ? (NT - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const long long S = ntl * cnt;
-  unsigned char* wring = zring + warp * (DEPTH * CHUNK);
-  long long s_iss = 0;                    // next chunk to issue
-  long long t_iss = 0;                    // its local tile
-  int q_iss = 0;                          // its column
-  auto issue = [&]() {
-    if (s_iss < S) {
-      const char* g = reinterpret_cast<const char*>(ring + col_off[warp][q_iss] +
-                                                    (blockIdx.x + t_iss * gridDim.x) * (long long)kSuperTile);
-      unsigned char* d = wring + (int)(s_iss % DEPTH) * CHUNK;
-#pragma unroll
-      for (int c = 0; c < LPC; ++c) cp_async16(d + c * 512 + lane * 16, g + c * 512 + lane * 16);
-      if (++q_iss == cnt) { q_iss = 0; ++t_iss; }
-    }
-    ++s_iss;
-    cp_async_commit();                    // one group per chunk slot, empty at the tail
-  };
-#pragma unroll 1
-  for (int d = 0; d < DEPTH; ++d) issue();
-  VT xn[VPL];                             // x_t of the next tile (prefetched one tile ahead)
-  if (ntl > 0) {
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-      xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + (long long)blockIdx.x * kSuperTile + v * 32 * EPV) + lane);
-  }
-
-  for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
-    const long long row0 = tile * kSuperTile;
-    double xd[8];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) to_double(xn[v], xd + v * EPV);
-    if (tile + gridDim.x < NT) {
-#pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + row0 + (long long)gridDim.x * kSuperTile + v * 32 * EPV) + lane);
-    }
-    BgAcc<T> bacc;
-    if (BG) {                       // x_{f_bg} of this tile's reduction rows, consumed LAGR tiles later
-      bacc.zero();
+    };
+    auto tile_begin = [&](long long row0) {  // x_{f_bg} of this tile's reduction rows
 #pragma unroll
       for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
       xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
-    }
-    const long long s0 = it * cnt;
+    };
+#if K1_BG_LDG
+    // ---- background, register streaming: CB columns (VPL LDG.128 each) in flight per lane
+    for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
+      const long long row0 = tile * kSuperTile;
+      double xd[8];
 #pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      if (q < cnt) {
-        cp_async_wait<DEPTH - 1>();                   // chunk s0 + q has landed (own bytes)
-        const unsigned char* src = wring + (int)((s0 + q) % DEPTH) * CHUNK;
-        VT zv[VPL];
+      for (int v = 0; v < VPL; ++v) {
+        VT xv = __ldg(reinterpret_cast<const VT*>(xslot + row0 + v * 32 * EPV) + lane);
+        to_double(xv, xd + v * EPV);
+      }
+      tile_begin(row0);
+      BgAcc<T> bacc;
+      bacc.zero();
+      const T* base = ring + row0;
+#pragma unroll
+      for (int q0 = 0; q0 < MAXQ; q0 += CB) {
+        if (q0 < cnt) {
+          VT z[CB][VPL];
+#pragma unroll
+          for (int b = 0; b < CB; ++b) {
+            const int q = q0 + b;
+            if (q < MAXQ && q < cnt) {
+              const VT* zp = reinterpret_cast<const VT*>(base + col_off[warp][q]);
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) z[b][v] = __ldcs(zp + v * 32 + lane);
+            }
+          }
+#pragma unroll
+          for (int b = 0; b < CB; ++b) {
+            const int q = q0 + b;
+            if (q < MAXQ && q < cnt) {
+              double zd[8];
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) to_double(z[b][v], zd + v * EPV);
+              double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) { s0 = fma(xd[e], zd[e], s0); s1 = fma(xd[e + 1], zd[e + 1], s1); }
+              accv[q] += s0 + s1;
+              bacc.add(cw_s[warp][q], reinterpret_cast<const T*>(&z[b][0]));
+            }
+          }
+        }
+      }
+      tile_end(bacc);
+    }
+#else
+    // ---- background, per-warp bulk-copy rings: s = (local tile) * cnt + q
+    const long long ntl = (NT > blockIdx.x) ? (NT - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    const long long S = ntl * cnt;
+    unsigned char* wring = zring + warp * (DEPTH * CHUNK);
+    unsigned long long* wbar = zbar + warp * DEPTH;
+    unsigned long long pol = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    const long long tstride = (long long)gridDim.x * kSuperTile;
+    long long s_iss = 0;                    // next chunk to issue
+    int q_iss = 0;                          // its column
+    int i_slot = 0;                         // its ring slot
+    const T* tile_iss = ring + (long long)blockIdx.x * kSuperTile;   // its tile's row 0
+    auto issue = [&]() {
+      if (s_iss < S) {
+        if (lane == 0) {
+          k1_mbar_expect_tx(wbar + i_slot, CHUNK);
+          k1_bulk_g2s(wring + i_slot * CHUNK, tile_iss + col_off[warp][q_iss], CHUNK, wbar + i_slot, pol);
+        }
+        if (++q_iss == cnt) { q_iss = 0; tile_iss += tstride; }
+        if (++i_slot == DEPTH) i_slot = 0;
+      }
+      ++s_iss;
+    };
+#pragma unroll 1
+    for (int d = 0; d < DEPTH; ++d) issue();
+    VT xn[VPL];                             // x_t of the next tile (prefetched one tile ahead)
+    if (ntl > 0) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + (long long)blockIdx.x * kSuperTile + v * 32 * EPV) + lane);
+    }
+    int c_slot = 0;                         // ring slot / phase of the next chunk to consume
+    unsigned c_par = 0;
+    for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
+      const long long row0 = tile * kSuperTile;
+      double xd[8];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) to_double(xn[v], xd + v * EPV);
+      if (tile + gridDim.x < NT) {
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
-          zv[v] = *reinterpret_cast<const VT*>(src + v * 512 + lane * 16);
-        if (col_kd[warp][q] >= 0) {
+          xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + row0 + (long long)gridDim.x * kSuperTile + v * 32 * EPV) + lane);
+      }
+      tile_begin(row0);
+      BgAcc<T> bacc;
+      bacc.zero();
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        if (q < cnt) {
+          k1_mbar_wait_tx(wbar + c_slot, c_par);          // the chunk has landed
+          const unsigned char* src = wring + c_slot * CHUNK;
+          if (++c_slot == DEPTH) { c_slot = 0; c_par ^= 1u; }
+          VT zv[VPL];
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) zv[v] = *reinterpret_cast<const VT*>(src + v * 512 + lane * 16);
+          const CW c = cw_s[warp][q];
           double zd[8];
 #pragma unroll
           for (int v = 0; v < VPL; ++v) to_double(zv[v], zd + v * EPV);
           double a0 = 0.0, a1 = 0.0;
 #pragma unroll
           for (int e = 0; e < 8; e += 2) { a0 = fma(xd[e], zd[e], a0); a1 = fma(xd[e + 1], zd[e + 1], a1); }
-          accv[q] += a0 + a1;
+          accv[q] += a0 + a1;                     // non-Gram columns are discarded at the end
+          if (!(p.dbg & 2)) bacc.add(c, reinterpret_cast<const T*>(&zv[0]));   // c = 0 outside X'_{f_bg}
+          __syncwarp();                           // every lane has read the slot: refill it
+          issue();
         }
-        if (BG) {
-          const int kb = col_kb[warp][q];
-          if (kb >= 0) bacc.add(c_s[kb], reinterpret_cast<const T*>(&zv[0]));
-        }
-        issue();                                      // refill the slot just consumed
       }
+      if (p.dbg & 1) {
+        if (bacc.get(0).x == 12345.f) p.mask[0] = 7;      // keep the accumulators live
+        continue;
+      }
+      tile_end(bacc);
     }
-    if (BG) {
-      const int slot = (int)(it % NSLOT);
-      if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
-      BT2* rb = red + slot * (K1_WARPS * BgLayout<T>::W) + warp * BgLayout<T>::W;
+#endif
+    // drain the last LAGR tiles
+    if (!(p.dbg & 1)) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) rb[e * BgLayout<T>::L + lane] = bacc.v[e];
-      __syncwarp();
-      if (lane == 0) k1_mbar_arrive(&fullb[slot]);
-      if (it >= LAGR) bg_reduce(it - LAGR, xq[LAGR]);
+      for (int q = LAGR - 1; q >= 0; --q)
+        if (it - 1 - q >= 0) bg_reduce(it - 1 - q, xq[q]);
     }
-  }
-  cp_async_wait<0>();
-  }
-  if (BG) {                                   // drain the last LAGR tiles
-#pragma unroll
-    for (int q = LAGR - 1; q >= 0; --q)
-      if (it - 1 - q >= 0) bg_reduce(it - 1 - q, xq[q]);
   }
 
   // per-column warp reduction of the lane partials (fixed order) -> this CTA's partials
@@ -402,29 +494,34 @@ __global__ void commit_kernel(const K1Params p) {
   commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
 }
 
+template <typename T, bool BG, int NQ>
+static cudaError_t launch_k1_inst(const K1Params& p, int grid, int smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k1_gram_kernel<T, BG, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  static const int carve = [] { const char* c = std::getenv("SDMD_K1_CARVEOUT"); return c ? std::atoi(c) : -1; }();
+  if (e == cudaSuccess && carve >= 0)      // experiment knob: shared-memory carveout (percent)
+    e = cudaFuncSetAttribute(k1_gram_kernel<T, BG, NQ>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+  if (e == cudaSuccess) k1_gram_kernel<T, BG, NQ><<<grid, K1_THREADS, smem, s>>>(p);
+  return e;
+}
+
+template <typename T, bool BG>
+static cudaError_t launch_k1_nq(const K1Params& p, int grid, int smem, int U, cudaStream_t s) {
+  // columns per warp: 14 covers m + lag <= 224 (e.g. m = 200, lag <= 24) with 6 fewer live registers
+  return U <= K1_WARPS * 14 ? launch_k1_inst<T, BG, 14>(p, grid, smem, s)
+                            : launch_k1_inst<T, BG, K1_NQMAX>(p, grid, smem, s);
+}
+
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
   const int es = dtype == 0 ? 4 : 8;
-  const int depth = p.bg ? (dtype == 0 ? 8 : 2) : 0;
-  int smem = K1_WARPS * depth * kSuperTile * es;                  // cp.async rings (background path)
-  if (p.bg) smem += 2 * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
-  cudaError_t e = cudaSuccess;
-  if (dtype == 0) {
-    if (p.bg) {
-      e = cudaFuncSetAttribute(k1_gram_kernel<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) k1_gram_kernel<float, true><<<grid, K1_THREADS, smem, s>>>(p);
-    } else {
-      e = cudaFuncSetAttribute(k1_gram_kernel<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) k1_gram_kernel<float, false><<<grid, K1_THREADS, smem, s>>>(p);
-    }
-  } else {
-    if (p.bg) {
-      e = cudaFuncSetAttribute(k1_gram_kernel<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) k1_gram_kernel<double, true><<<grid, K1_THREADS, smem, s>>>(p);
-    } else {
-      e = cudaFuncSetAttribute(k1_gram_kernel<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e == cudaSuccess) k1_gram_kernel<double, false><<<grid, K1_THREADS, smem, s>>>(p);
-    }
-  }
+  const int depth = (p.bg && !K1_BG_LDG) ? (dtype == 0 ? K1_DEPTH32 : 2) : 0;
+  int smem = K1_WARPS * depth * kSuperTile * es;                  // bulk-copy rings (background path)
+  if (p.bg) smem += K1_NSLOT * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
+  // union of the Gram window and X' of the background frame
+  const int U = p.bg ? (p.nd > (int)(p.f_new - p.f_bg) + p.m ? p.nd : (int)(p.f_new - p.f_bg) + p.m) : p.nd;
+  if (U > K1_MAXU) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (dtype == 0) e = p.bg ? launch_k1_nq<float, true>(p, grid, smem, U, s) : launch_k1_nq<float, false>(p, grid, smem, U, s);
+  else e = p.bg ? launch_k1_nq<double, true>(p, grid, smem, U, s) : launch_k1_nq<double, false>(p, grid, smem, U, s);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -433,10 +530,14 @@ cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
 // kernel otherwise loads it mid-stream (measured: a 26 ms stall on the first background pass).
 void preload_k1_kernels() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, k1_gram_kernel<float, false>);
-  cudaFuncGetAttributes(&a, k1_gram_kernel<float, true>);
-  cudaFuncGetAttributes(&a, k1_gram_kernel<double, false>);
-  cudaFuncGetAttributes(&a, k1_gram_kernel<double, true>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, false, 14>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, true, 14>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, false, 14>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, true, 14>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, false, K1_NQMAX>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<float, true, K1_NQMAX>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, false, K1_NQMAX>);
+  cudaFuncGetAttributes(&a, k1_gram_kernel<double, true, K1_NQMAX>);
   cudaFuncGetAttributes(&a, commit_kernel);
 }
 

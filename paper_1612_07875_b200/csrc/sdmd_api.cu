@@ -70,7 +70,7 @@ struct sdmd_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
-  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148;
+  int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   bool k1_ldg = true;                   // SDMD_K1=tma selects the bulk-copy (TMA) K1 variant (A/B)
   long long ld = 0;
@@ -290,6 +290,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   {
     const char* ev = std::getenv("SDMD_K1");
     c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
+    const char* ed = std::getenv("SDMD_K1_DBG");
+    c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* eb = std::getenv("SDMD_BG_NODMD");
     c->bg_nodmd = eb && eb[0] == '1';
   }
@@ -498,6 +500,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.nd = nd; p.bg = bg ? 1 : 0; p.f_bg = bg ? t - c->L : 0;
     p.cbg = bg ? c->cbuf + ((t - c->L) % c->NC) * m : nullptr;
     p.lowrank = c->bg_low; p.sparse = c->bg_sparse; p.mask = c->bg_mask; p.thr = c->cfg.threshold;
+    p.dbg = c->k1_dbg;
     p.partials = c->partials; p.pgrid = c->pgrid; p.gout = c->gout; p.do_commit = do_commit;
     p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
     if (c->k1_ldg) CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));

@@ -48,6 +48,7 @@ struct K1Params {
   float thr;
   double* partials;           // K1: [nd][pgrid] (column-major, coalesced reduction); TMA: [grid][kMaxM+16]
   int pgrid;                  // partials stride of K1 (>= gridDim.x)
+  int dbg;                    // microbenchmark knob (SDMD_K1_DBG): 1 skip bg reduction, 2 skip bg FMAs
   double* gout;               // nd reduced values (pre-allreduce)
   int do_commit;              // nranks == 1: commit inside the kernel's last block
   double* ghist;

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsdmd.so")
+# SDMD_LIB: load a variant build of the same library (kernel-tuning experiments only)
+LIB_PATH = os.environ.get("SDMD_LIB") or os.path.join(_HERE, "libsdmd.so")
 
 OK, E_INVALID, E_NONFINITE, E_WINDOW_NOT_FULL, E_ZERO_MATRIX = 0, 1, 2, 3, 4
 E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE, E_CUDA, E_NCCL, E_OOM, E_STATE = (
