@@ -207,9 +207,10 @@ int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mas
 
 /* Diagnostics of the newest DMD frame: out[0]=frame, [1]=status, [2]=r, [3]=idx, [4]=Jacobi
  * sweeps, [5]=QR iterations, [6..12]=SM cycles spent in the K4 phases (build S, Jacobi, sort/V,
- * Ã, Hessenberg, QR, eigenvectors+c), [13..15]=QR bulge-chase steps, deflation-scan and
- * shift-search iterations.  Synchronises. */
-int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[16]);
+ * Ã, Hessenberg, QR, eigenvectors+c), [13]=single-bulge chase steps, [14]=multishift global
+ * steps, [15]=multishift sweeps, [16]=SM cycles spent computing multishift shifts, [17]=single-
+ * bulge iterations.  Synchronises. */
+int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[20]);
 
 /* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */
 int sdmd_set_timing(sdmd_ctx* ctx, int enable);

@@ -15,6 +15,7 @@
 // the last CTA to finish reduces the CTA partials in fixed order and commits the column into the
 // Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "sdmd_internal.cuh"
@@ -32,6 +33,18 @@ namespace sdmd {
 #endif
 #ifndef K1_CB32
 #define K1_CB32 4         // fp32 background LDG path: columns (2 LDG.128 each) in flight per lane
+#endif
+#ifndef K1V2_NBDIV
+#define K1V2_NBDIV 16     // v2: batches per tile = 2·ceil(NQ / K1V2_NBDIV) (register budget)
+#endif
+#ifndef K1V2_LAGR
+#define K1V2_LAGR 3       // v2: tiles between publishing background partials and reducing them
+#endif
+#ifndef K1V2_SLACK
+#define K1V2_SLACK 1      // v2: extra reduction slots beyond the lag
+#endif
+#ifndef K1V2_DBG
+#define K1V2_DBG 0        // v2 experiments: 1 = skip the background reduction, 2 = skip its FMAs
 #endif
 #ifndef K1_DEPTH32
 #define K1_DEPTH32 8      // per-warp bulk-copy ring depth (fp32 chunks of 1 KB)
@@ -489,6 +502,247 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K1 v2: the same pass with one 16-byte vector per lane per column (a 32·EPV-row tile: 128 fp32 /
+// 64 fp64 rows), column batches double-buffered in registers (the next batch — or the next tile's
+// first batch — is in flight while the current one is reduced), and a branch-free column loop:
+// every warp walks exactly NQ columns, the ones past the union U pointing at the (L1-resident)
+// x_t tile with a zero background coefficient and a discarded dot.  Column offsets are 32-bit, in
+// 16-byte units.
+template <typename T> struct BgAcc2;
+template <> struct BgAcc2<float> {              // rows (0,1) and (2,3) of the lane, packed FFMA2
+  using C2 = float2;
+  using CW = float4;                           // (c.x, c.x, c.y, c.y)
+  float2 re[2], im[2];
+  static __device__ __forceinline__ CW make(double2 c) {
+    return make_float4((float)c.x, (float)c.x, (float)c.y, (float)c.y);
+  }
+  __device__ __forceinline__ void zero() { re[0] = re[1] = im[0] = im[1] = make_float2(0.f, 0.f); }
+  __device__ __forceinline__ void add(const CW c, const float4 z) {
+    const float2 cr = make_float2(c.x, c.y), ci = make_float2(c.z, c.w);
+    const float2 z01 = make_float2(z.x, z.y), z23 = make_float2(z.z, z.w);
+    re[0] = __ffma2_rn(cr, z01, re[0]);
+    re[1] = __ffma2_rn(cr, z23, re[1]);
+    im[0] = __ffma2_rn(ci, z01, im[0]);
+    im[1] = __ffma2_rn(ci, z23, im[1]);
+  }
+  __device__ __forceinline__ C2 get(int e) const {
+    return (e & 1) ? make_float2(re[e >> 1].y, im[e >> 1].y) : make_float2(re[e >> 1].x, im[e >> 1].x);
+  }
+};
+template <> struct BgAcc2<double> {
+  using C2 = double2;
+  using CW = double2;
+  double2 v[2];
+  static __device__ __forceinline__ CW make(double2 c) { return c; }
+  __device__ __forceinline__ void zero() { v[0] = v[1] = make_double2(0.0, 0.0); }
+  __device__ __forceinline__ void add(const CW c, const double2 z) {
+    v[0].x = fma(c.x, z.x, v[0].x); v[0].y = fma(c.y, z.x, v[0].y);
+    v[1].x = fma(c.x, z.y, v[1].x); v[1].y = fma(c.y, z.y, v[1].y);
+  }
+  __device__ __forceinline__ C2 get(int e) const { return v[e]; }
+};
+
+template <int NQ> struct K1v2Shape {
+  static constexpr int NB = NQ <= 8 ? 1 : 2 * ((NQ + K1V2_NBDIV - 1) / K1V2_NBDIV);     // batches per tile (even if > 1)
+  static constexpr int CB = (NQ + NB - 1) / NB;                     // columns per batch
+};
+
+template <typename T, bool BG, int NQ>
+__global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
+  using VT = typename VecOf<T>::type;
+  using Acc = BgAcc2<T>;
+  using BT2 = typename Acc::C2;
+  using CW = typename Acc::CW;
+  constexpr int EPV = VecOf<T>::E;             // rows per lane per tile
+  constexpr int TILE = 32 * EPV;               // rows per tile
+  constexpr int NB = K1v2Shape<NQ>::NB, CB = K1v2Shape<NQ>::CB;
+  constexpr int LAGR = K1V2_LAGR;             // tiles between publishing and reducing
+  constexpr int NSLOT = LAGR + K1V2_SLACK;     // reduction slots
+  constexpr int RL = 33;                       // padded lane stride of the reduction slots
+  constexpr int SLOTW = K1_WARPS * EPV * RL;   // BT2 elements per slot
+  __shared__ unsigned col_off[K1_WARPS][NQ];   // ring offset of each warp column (16-byte units)
+  __shared__ int col_kd[K1_WARPS][NQ];         // Gram-column index, or -1
+  __shared__ __align__(16) CW cw_s[BG ? K1_WARPS : 1][BG ? NQ : 1];
+  extern __shared__ __align__(16) unsigned char k1v2_dyn[];
+  BT2* red = reinterpret_cast<BT2*>(k1v2_dyn);     // [NSLOT][K1_WARPS][EPV][RL]
+  __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
+  __shared__ int am_last;
+
+  if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long f_dot0 = p.f_new - p.nd + 1;
+  const long long f_bg0 = p.f_bg - p.m + 1;
+  const long long F0 = BG ? (f_dot0 < f_bg0 ? f_dot0 : f_bg0) : f_dot0;
+  const int U = (int)(p.f_new - F0 + 1);
+  const unsigned xoff = (unsigned)((p.f_new % p.NS) * p.ld / EPV);
+  for (int e = tid; e < K1_WARPS * NQ; e += K1_THREADS) {
+    const int w = e / NQ, q = e % NQ, j = w + K1_WARPS * q;
+    const long long f = F0 + j;
+    col_off[w][q] = (j < U) ? (unsigned)((f % p.NS) * p.ld / EPV) : xoff;
+    col_kd[w][q] = (j < U && f >= f_dot0) ? (int)(f - f_dot0) : -1;
+    if (BG) {
+      const bool inb = j < U && f >= f_bg0 && f - f_bg0 < p.m;
+      cw_s[w][q] = Acc::make(inb ? p.cbg[f - f_bg0] : make_double2(0.0, 0.0));
+    }
+  }
+  if (BG && tid == 0) {
+    for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const VT* __restrict__ ringv = (const VT*)p.ring;
+  const long long NT = p.ld / TILE;
+  const unsigned* my_off = col_off[warp];
+  double acc[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
+
+  // background: every warp publishes its per-row (re, im) partials of each tile into slot
+  // tile % NSLOT; the sums over the 16 warps are formed by ONE designated warp per tile
+  // (tile & 15), LAGR tiles later, so the reductions are spread over the warps instead of all
+  // warps reducing every tile in lockstep.  Fixed summation order: bitwise reproducible.
+  const T* bg_col = (const T*)p.ring + (p.f_bg % p.NS) * p.ld;
+  VT xbg;                                      // x_{f_bg} rows of the tile this warp reduces next
+  auto bg_load_x = [&](long long jt) {
+    const long long row0 = (blockIdx.x + jt * (long long)gridDim.x) * TILE;
+    xbg = __ldcs(reinterpret_cast<const VT*>(bg_col + row0) + lane);
+  };
+  auto bg_reduce = [&](long long jt) {
+    const int rs = (int)(jt % NSLOT);
+    k1_mbar_wait(&fullb[rs], (unsigned)((jt / NSLOT) & 1));
+    const BT2* rr = red + rs * SLOTW + lane;
+    double sx[EPV], sy[EPV];
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) { sx[e] = 0.0; sy[e] = 0.0; }
+#pragma unroll
+    for (int w = 0; w < K1_WARPS; ++w) {
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) {
+        const BT2 v = rr[w * (EPV * RL) + e * RL];
+        sx[e] += (double)v.x;
+        sy[e] += (double)v.y;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) k1_mbar_arrive(&emptyb[rs]);          // slot may be refilled
+    const long long row0 = (blockIdx.x + jt * (long long)gridDim.x) * TILE + lane * EPV;
+    T xs[EPV], lo[EPV], sp[EPV];
+    *reinterpret_cast<VT*>(xs) = xbg;
+    unsigned char mk[EPV];
+#pragma unroll
+    for (int e = 0; e < EPV; ++e) {
+      const double l = sqrt(sx[e] * sx[e] + sy[e] * sy[e]);   // |l| (Q8)
+      const double sv = (double)xs[e] - l;                    // s = x - |l|
+      lo[e] = (T)l;
+      sp[e] = (T)sv;
+      mk[e] = (sv > (double)p.thr) ? 1 : 0;                   // strict '>'
+    }
+    // outputs hold ld rows (padding rows come out as l = s = 0): whole vectors, no row guards
+    *reinterpret_cast<VT*>((T*)p.lowrank + row0) = *reinterpret_cast<const VT*>(lo);
+    *reinterpret_cast<VT*>((T*)p.sparse + row0) = *reinterpret_cast<const VT*>(sp);
+    if constexpr (EPV == 4) {
+      *reinterpret_cast<uchar4*>(p.mask + row0) = make_uchar4(mk[0], mk[1], mk[2], mk[3]);
+    } else {
+      *reinterpret_cast<uchar2*>(p.mask + row0) = make_uchar2(mk[0], mk[1]);
+    }
+  };
+
+  auto load_batch = [&](VT (&z)[CB], int b, long long tile) {
+    const VT* base = ringv + tile * 32 + lane;
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const int q = b * CB + c;
+      if (q < NQ) z[c] = __ldcs(base + my_off[q]);
+    }
+  };
+  VT za[CB], zb[CB];
+  long long tile = blockIdx.x;
+  long long it = 0;
+  if (tile < NT) load_batch(za, 0, tile);
+  for (; tile < NT; tile += gridDim.x, ++it) {
+    double xd[EPV];
+    {
+      const VT xv = __ldg(ringv + xoff + tile * 32 + lane);
+      to_double(xv, xd);
+    }
+    if (BG && !(K1V2_DBG & 1) && it >= LAGR && (((it - LAGR) & (K1_WARPS - 1)) == warp)) bg_load_x(it - LAGR);
+    Acc bacc;
+    if (BG) bacc.zero();
+    const long long next = tile + gridDim.x;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      VT (&cur)[CB] = (b & 1) ? zb : za;
+      VT (&nxt)[CB] = (b & 1) ? za : zb;
+      if (b + 1 < NB) load_batch(nxt, b + 1, tile);
+      else if (NB > 1 && next < NT) load_batch(nxt, 0, next);     // next tile's first batch
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        const int q = b * CB + c;
+        if (q < NQ) {
+          double zd[EPV];
+          to_double(cur[c], zd);
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) acc[q] = fma(xd[e], zd[e], acc[q]);
+          if (BG && !(K1V2_DBG & 2)) bacc.add(cw_s[warp][q], cur[c]);
+        }
+      }
+    }
+    if (NB == 1 && next < NT) load_batch(za, 0, next);
+    if (BG && (K1V2_DBG & 1)) {
+      if (bacc.get(0).x == 12345.0) p.mask[0] = 7;      // keep the accumulators live
+    } else if (BG) {
+      // publish this warp's per-row (re, im) partials of the tile; the designated warp of tile
+      // it - LAGR reduces it
+      const int slot = (int)(it % NSLOT);
+      if (it >= NSLOT) k1_mbar_wait(&emptyb[slot], (unsigned)(((it / NSLOT) - 1) & 1));
+      BT2* rb = red + slot * SLOTW + warp * (EPV * RL);
+#pragma unroll
+      for (int e = 0; e < EPV; ++e) rb[e * RL + lane] = bacc.get(e);
+      __syncwarp();
+      if (lane == 0) k1_mbar_arrive(&fullb[slot]);
+      if (it >= LAGR && (((it - LAGR) & (K1_WARPS - 1)) == warp)) bg_reduce(it - LAGR);
+    }
+  }
+  if (BG && !(K1V2_DBG & 1)) {                 // drain the last LAGR tiles
+    for (long long jt = it - LAGR > 0 ? it - LAGR : 0; jt < it; ++jt)
+      if ((jt & (K1_WARPS - 1)) == warp) { bg_load_x(jt); bg_reduce(jt); }
+  }
+
+  // per-column warp reduction of the lane partials (fixed order) -> this CTA's partials
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int kd = col_kd[warp][q];
+    const double s = warp_sum(acc[q]);
+    if (lane == 0 && kd >= 0) p.partials[(long long)kd * p.pgrid + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) {
+    const unsigned prev = atomicAdd(&p.st->k1_done, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int k = warp; k < p.nd; k += K1_WARPS) {
+    const double* pk = p.partials + (long long)k * p.pgrid;
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(pk + b);
+    s = warp_sum(s);
+    if (lane == 0) p.gout[k] = s;
+  }
+  if (tid == 0) {
+    p.st->k1_done = 0;
+    if (BG) p.st->bg_frame = p.f_bg;
+  }
+  if (p.do_commit) {
+    __syncthreads();
+    commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
+  }
+}
+
 __global__ void commit_kernel(const K1Params p) {
   if (*(volatile int*)&p.st->status != 0) return;
   commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
@@ -511,8 +765,45 @@ static cudaError_t launch_k1_nq(const K1Params& p, int grid, int smem, int U, cu
                             : launch_k1_inst<T, BG, K1_NQMAX>(p, grid, smem, s);
 }
 
+template <typename T, bool BG, int NQ>
+static cudaError_t launch_k1v2_inst(const K1Params& p, int grid, cudaStream_t s) {
+  constexpr int EPV = VecOf<T>::E;
+  const int smem = BG ? (K1V2_LAGR + K1V2_SLACK) * K1_WARPS * EPV * 33 * (int)(2 * sizeof(T)) : 0;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k1v2_kernel<T, BG, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  k1v2_kernel<T, BG, NQ><<<grid, K1_THREADS, smem, s>>>(p);
+  return cudaSuccess;
+}
+
+template <typename T, bool BG>
+static cudaError_t launch_k1v2_nq(const K1Params& p, int grid, int U, cudaStream_t s) {
+  const int need = (U + K1_WARPS - 1) / K1_WARPS;
+  if (need <= 2) return launch_k1v2_inst<T, BG, 2>(p, grid, s);
+  if (need <= 4) return launch_k1v2_inst<T, BG, 4>(p, grid, s);
+  if (need <= 8) return launch_k1v2_inst<T, BG, 8>(p, grid, s);
+  if (need <= 13) return launch_k1v2_inst<T, BG, 13>(p, grid, s);
+  if (need <= 14) return launch_k1v2_inst<T, BG, 14>(p, grid, s);
+  return launch_k1v2_inst<T, BG, K1_NQMAX>(p, grid, s);
+}
+
+static bool k1_use_v1() {
+  static const bool v1 = [] { const char* e = std::getenv("SDMD_K1"); return e && std::strcmp(e, "v1") == 0; }();
+  return v1;
+}
+
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
   const int es = dtype == 0 ? 4 : 8;
+  if (!k1_use_v1() && (unsigned long long)p.NS * (unsigned long long)p.ld * es / 16 < (1ull << 32)) {
+    const int U = p.bg ? (p.nd > (int)(p.f_new - p.f_bg) + p.m ? p.nd : (int)(p.f_new - p.f_bg) + p.m) : p.nd;
+    if (U > K1_MAXU) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if (dtype == 0) e = p.bg ? launch_k1v2_nq<float, true>(p, grid, U, s) : launch_k1v2_nq<float, false>(p, grid, U, s);
+    else e = p.bg ? launch_k1v2_nq<double, true>(p, grid, U, s) : launch_k1v2_nq<double, false>(p, grid, U, s);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   const int depth = (p.bg && !K1_BG_LDG) ? (dtype == 0 ? K1_DEPTH32 : 2) : 0;
   int smem = K1_WARPS * depth * kSuperTile * es;                  // bulk-copy rings (background path)
   if (p.bg) smem += K1_NSLOT * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
@@ -539,6 +830,14 @@ void preload_k1_kernels() {
   cudaFuncGetAttributes(&a, k1_gram_kernel<double, false, K1_NQMAX>);
   cudaFuncGetAttributes(&a, k1_gram_kernel<double, true, K1_NQMAX>);
   cudaFuncGetAttributes(&a, commit_kernel);
+#define K1V2_PRELOAD(NQ)                                          \
+  cudaFuncGetAttributes(&a, k1v2_kernel<float, false, NQ>);      \
+  cudaFuncGetAttributes(&a, k1v2_kernel<float, true, NQ>);       \
+  cudaFuncGetAttributes(&a, k1v2_kernel<double, false, NQ>);     \
+  cudaFuncGetAttributes(&a, k1v2_kernel<double, true, NQ>);
+  K1V2_PRELOAD(2) K1V2_PRELOAD(4) K1V2_PRELOAD(8) K1V2_PRELOAD(13) K1V2_PRELOAD(14)
+  K1V2_PRELOAD(K1_NQMAX)
+#undef K1V2_PRELOAD
 }
 
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s) {

@@ -273,7 +273,8 @@ static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, i
     } while (l < nn - 1);
   }
   *total_its += tot;
-  if (cnt && lane == 0) { cnt[0] += c_steps; cnt[1] += c_scan; cnt[2] += c_mscan; }
+  if (cnt && lane == 0) { cnt[0] += c_steps; cnt[2] += tot; }
+  (void)c_scan; (void)c_mscan;
   return 0;
 }
 
@@ -317,7 +318,7 @@ static __device__ void ms_two_roots(HsAcc a, int nn, double2* wv) {
 }
 
 static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, int tid, int warp,
-                                    int lane, int* total_its, int* cnt) {
+                                    int lane, int* total_its, int* cnt, long long* shift_cycles) {
   double an = 0.0;
   if (warp == 0) {
     for (int i = 0; i < n; ++i)
@@ -372,6 +373,7 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
     // ---- shifts: eigenvalues of the trailing ns x ns block (warp 0, small packed copy)
     int ns = 2 * MS_NB;
     if (ns > ((nact - 2) & ~1)) ns = (nact - 2) & ~1;
+    const long long t_sh0 = clock64();
     if (warp == 0) {
       const int b0 = nn - ns + 1;
       HsAcc sm{sh->small_hs, ns};
@@ -410,6 +412,7 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
       }
     }
     __syncthreads();
+    if (tid == 0 && shift_cycles) *shift_cycles += clock64() - t_sh0;
     const int nbe = sh->nbe;
     if (nbe == 0) { stall = MS_STALL; continue; }
     // ---- chase nbe bulges in lockstep
@@ -502,7 +505,7 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
       }
       __syncthreads();
     }
-    if (tid == 0) { *total_its += 1; if (cnt) cnt[3] += 1; }
+    if (tid == 0) { *total_its += 1; if (cnt) { cnt[1] += G + 1; cnt[3] += 1; } }
     ++stall;
   }
   return status;
@@ -1076,8 +1079,9 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     if (tid == 0) its_sh = 0;
     __syncthreads();
     int its_local = 0;
+    long long shift_cyc = 0;
     const int rc = multishift_qr(HsAcc{hs, r}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
-                                 warp == 0 ? qc_sh : nullptr);
+                                 warp == 0 ? qc_sh : nullptr, &shift_cyc);
     if (warp == 0 && lane == 0) atomicAdd(&its_sh, its_local);
     __syncthreads();
     if (tid == 0) {
@@ -1085,6 +1089,7 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       if (rc != 0) sh_status = 5;
       res->qr_cnt[0] = qc_sh[0]; res->qr_cnt[1] = qc_sh[1]; res->qr_cnt[2] = qc_sh[2];
       res->qr_cnt[3] = qc_sh[3];
+      res->phase[7] = shift_cyc;
     }
   }
   __syncthreads();

@@ -333,9 +333,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   AL(c->gpart, (size_t)(m + 1));
   AL(c->Gtmp, (size_t)(m + 1) * (m + 1));
   if (c->cfg.background) {
-    if (cudaMalloc(&c->bg_low, c->cfg.n_local * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
-    if (cudaMalloc(&c->bg_sparse, c->cfg.n_local * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
-    AL(c->bg_mask, (size_t)c->cfg.n_local);
+    // ld rows (padding included): K1 writes whole 16-byte vectors of its tiles without row guards
+    if (cudaMalloc(&c->bg_low, c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+    if (cudaMalloc(&c->bg_sparse, c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+    AL(c->bg_mask, (size_t)c->ld);
   }
   const int R = kMaxR;
   int prio_lo = 0, prio_hi = 0;                     // eigen workers: highest stream priority
@@ -878,17 +879,18 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   return SDMD_OK;
 }
 
-int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[16]) {
+int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[20]) {
   if (!c || !out) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  for (int i = 0; i < 16; ++i) out[i] = 0;
+  for (int i = 0; i < 20; ++i) out[i] = 0;
   out[0] = res.frame; out[1] = res.status; out[2] = res.r; out[3] = res.idx;
   out[4] = res.sweeps; out[5] = res.qr_its;
   for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q];
-  out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[2];
+  out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[3];
+  out[16] = res.phase[7]; out[17] = res.qr_cnt[2];
   return SDMD_OK;
 }
 

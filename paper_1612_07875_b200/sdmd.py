@@ -364,13 +364,14 @@ class StreamingDMD:
         return fr.value
 
     def frame_diag(self) -> dict:
-        o = np.zeros(16, dtype=np.int64)
+        o = np.zeros(20, dtype=np.int64)
         self._check(lib().sdmd_get_frame_diag(self.h, _dp(o)), "get_frame_diag")
         names = ["build_S", "jacobi", "sort_V", "atilde", "hessenberg", "qr", "eigvec_c"]
         return dict(frame=int(o[0]), status=int(o[1]), r=int(o[2]), idx=int(o[3]),
                     sweeps=int(o[4]), qr_its=int(o[5]),
                     cycles={k: int(v) for k, v in zip(names, o[6:13])},
-                    qr_steps=int(o[13]), qr_scan=int(o[14]), qr_shift_search=int(o[15]))
+                    qr_steps=int(o[13]), ms_steps=int(o[14]), ms_sweeps=int(o[15]),
+                    ms_shift_cycles=int(o[16]), qr_block_its=int(o[17]))
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")
