@@ -305,9 +305,9 @@ def run_ours(args):
                    "l2": "no flush: every step streams the 20 GB ring (>> 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk,
                      "unit": "GB/s", "frac": round(achieved / pk, 4),
-                     "traffic": k1_traffic("k1_gram_kernel<float,true>"),
+                     "traffic": k1_traffic("k1v2_kernel<float,true>"),
                      "traffic_source": "profiles/k1_traffic.json (ncu --set full, one launch)",
-                     "kernel": "k1_gram_kernel<float,true>", "k1_ms_avg": round(k1_ms, 4),
+                     "kernel": "k1v2_kernel<float,true>", "k1_ms_avg": round(k1_ms, 4),
                      "algorithmic_bytes_per_launch": alg_bytes, "peak_source": pk_src,
                      "k1_share_of_step": round(k1_ms / (ms / K), 4),
                      "k4_ms_avg": round(st["k4_ms"] / max(1, st["k4_launches"]), 3),
@@ -356,7 +356,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workers", type=int, default=6)

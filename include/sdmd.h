@@ -209,7 +209,7 @@ int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mas
  * sweeps, [5]=QR iterations, [6..12]=SM cycles spent in the K4 phases (build S, Jacobi, sort/V,
  * Ã, Hessenberg, QR, eigenvectors+c), [13]=single-bulge chase steps, [14]=multishift global
  * steps, [15]=multishift sweeps, [16]=SM cycles spent computing multishift shifts, [17]=single-
- * bulge iterations.  Synchronises. */
+ * bulge iterations, [18..19]=SM cycles of the multishift chase phases.  Synchronises. */
 int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[20]);
 
 /* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */

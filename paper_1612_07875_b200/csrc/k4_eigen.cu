@@ -79,6 +79,21 @@ struct HsAcc {
     const int lo = i > 3 ? i - 3 : 0;
     return hs[hs_off(i, r) + j - lo];
   }
+  __device__ __forceinline__ double* row(int i) const { return hs + (hs_off(i, r) - (i > 3 ? i - 3 : 0)); }
+};
+// Packed Hessenberg through a per-row offset table in shared memory (one LDS per row access)
+struct RowAcc {
+  double* hs;
+  const int* roff;            // roff[i] = hs_off(i) - max(0, i-3)
+  __device__ __forceinline__ double& operator()(int i, int j) const { return hs[roff[i] + j]; }
+  __device__ __forceinline__ double* row(int i) const { return hs + roff[i]; }
+};
+// Dense row-major small block (leading dimension ld)
+struct DenseAcc {
+  double* a;
+  int ld;
+  __device__ __forceinline__ double& operator()(int i, int j) const { return a[i * ld + j]; }
+  __device__ __forceinline__ double* row(int i) const { return a + i * ld; }
 };
 
 __host__ __device__ inline long long hs_elems(int r) { return hs_off(r, r); }
@@ -89,7 +104,8 @@ __host__ __device__ inline long long hs_elems(int r) { return hs_off(r, r); }
 // runs the scalar recurrences redundantly on identical shared-memory data; lanes split the row
 // and column updates of each 3x3 reflector.  Returns 0, or -1 when an eigenvalue needs more than
 // QR_MAXITS iterations.
-static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, int* total_its,
+template <class Acc>
+static __device__ int qr_block(Acc a, int lo, int hi, double2* wv, int lane, int* total_its,
                                int* cnt) {
   int c_steps = 0, c_scan = 0, c_mscan = 0;
   double an = 0.0;
@@ -225,9 +241,9 @@ static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, i
               const bool three = (k != nn - 1);
               __syncwarp();
               {                                         // row modification (2 columns per lane in flight)
-                double* r0 = &a(k, 0);
-                double* r1 = &a(k + 1, 0);
-                double* r2 = &a(three ? k + 2 : k + 1, 0);
+                double* r0 = a.row(k);
+                double* r1 = a.row(k + 1);
+                double* r2 = a.row(three ? k + 2 : k + 1);
                 for (int j = k + lane; j <= nn; j += 64) {
                   const int j2 = j + 32;
                   const bool h2 = j2 <= nn;
@@ -250,8 +266,8 @@ static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, i
               for (int i = l + lane; i <= mmin; i += 64) { // column modification (2 rows per lane)
                 const int i2 = i + 32;
                 const bool h2 = i2 <= mmin;
-                double* ri = &a(i, 0);
-                double* rj = &a(h2 ? i2 : i, 0);
+                double* ri = a.row(i);
+                double* rj = a.row(h2 ? i2 : i);
                 const double c0 = ri[k], c1 = ri[k + 1], c2 = three ? ri[k + 2] : 0.0;
                 const double d0 = h2 ? rj[k] : 0.0, d1 = h2 ? rj[k + 1] : 0.0;
                 const double d2 = (h2 && three) ? rj[k + 2] : 0.0;
@@ -288,21 +304,53 @@ static __device__ int qr_block(HsAcc a, int lo, int hi, double2* wv, int lane, i
 // successive Francis double-shift steps with the given shifts.  Small or stagnating blocks fall
 // back to the single-bulge qr_block.  (Golub–Van Loan §7.5; small-bulge multishift idea of
 // Braman–Byers–Mathias; no aggressive early deflation.)
-constexpr int MS_NB = 8;           // bulges per sweep (<= K4_WARPS)
+constexpr int MS_NB = 8;           // bulges per sweep (2 warps each)
 constexpr int MS_SMALL = 32;       // blocks up to this size use the single-bulge iteration
 constexpr int MS_STALL = 30;       // sweeps without deflation before falling back
 constexpr int MS_SPACING = 4;
+constexpr int MS_DLD = MS_SMALL + 1;   // leading dimension of the dense small-block copy
+
+// 3x3 (or 2x2) Householder reflector of the double-shift chase in the hqr form: applied to
+// (a0, a1, a2) as pr = a0 + q a1 + r a2; a0 -= pr x; a1 -= pr y; a2 -= pr z (rows), and with
+// (x, y, z) / (1, q, r) swapped for columns; sxs = the new bulge-column head -s·scale.
+struct MsRefl {
+  double x, y, z, q, r, sxs;
+  bool on;
+};
+static __device__ __forceinline__ MsRefl ms_reflector(double P, double Q, double R) {
+  MsRefl f;
+  double xs = 1.0;
+  const double sc = fabs(P) + fabs(Q) + fabs(R);
+  const double ss0 = P * P + Q * Q + R * R;
+  if (!(ss0 > 1e-280 && ss0 < 1e280) && sc != 0.0) {     // rescale only when squares leave range
+    const double isc = 1.0 / sc;
+    P *= isc; Q *= isc; R *= isc;
+    xs = sc;
+  }
+  const double s = copysign(sqrt(P * P + Q * Q + R * R), P);
+  f.on = (s != 0.0);
+  if (f.on) {
+    f.sxs = -s * xs;
+    const double pp = P + s;
+    const double inv = 1.0 / (s * pp);                  // one division for 1/s and 1/pp
+    const double is = pp * inv, ip = s * inv;
+    f.x = pp * is; f.y = Q * is; f.z = R * is;
+    f.q = Q * ip; f.r = R * ip;
+  } else {
+    f.x = f.y = f.z = f.q = f.r = f.sxs = 0.0;
+  }
+  return f;
+}
 
 struct MsShared {
-  double bx[MS_NB], by[MS_NB], bz[MS_NB], bq[MS_NB], br[MS_NB];
-  int bk[MS_NB], bon[MS_NB], bthree[MS_NB];
+  double dense[MS_SMALL * MS_DLD]; // dense copy of the shift block (ns x ns) or of a tail block
   double st[MS_NB], sd[MS_NB];
-  double2 sw[2 * MS_NB];
-  double small_hs[200];            // packed (with slack) ns x ns trailing block, ns <= 16
-  int l, nbe, fail, defl;
+  double2 sw[MS_SMALL];
+  int l, nbe, fail;
 };
 
-static __device__ void ms_two_roots(HsAcc a, int nn, double2* wv) {
+template <class Acc>
+static __device__ void ms_two_roots(Acc a, int nn, double2* wv) {
   const double x = a(nn, nn), y = a(nn - 1, nn - 1), w = a(nn, nn - 1) * a(nn - 1, nn);
   const double p = 0.5 * (y - x), q = p * p + w;
   double z = sqrt(fabs(q));
@@ -317,12 +365,29 @@ static __device__ void ms_two_roots(HsAcc a, int nn, double2* wv) {
   }
 }
 
-static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, int tid, int warp,
-                                    int lane, int* total_its, int* cnt, long long* shift_cycles) {
+// copy the Hessenberg block [b0, b0+nb) of a into the dense small buffer (all threads)
+static __device__ void ms_copy_block(RowAcc a, int b0, int nb, double* dense, int tid) {
+  for (int e = tid; e < nb * nb; e += K4_THREADS) {
+    const int i = e / nb, j = e % nb;
+    dense[i * MS_DLD + j] = (j >= i - 1) ? a(b0 + i, b0 + j) : 0.0;
+  }
+}
+
+// Per global step of the lockstep chase: (AB) the two warps of each active bulge form its 3x3
+// reflector redundantly in registers and apply it to rows k..k+2 (columns k..nn, split between
+// the warps); CTA barrier; (C) they apply it to columns k..k+2 (rows l..min(nn,k+3)) and write
+// the annihilated bulge column k-1; CTA barrier.  Concurrent bulges (MS_SPACING apart) touch
+// disjoint rows in (AB) and disjoint columns in (C), and a bulge's reflector input (column k-1)
+// is written only by its own warps in the previous (C), so two barriers per step suffice.
+static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, int tid, int warp,
+                                    int lane, int* total_its, int* cnt, long long* shift_cycles,
+                                    long long* chase_cycles) {
   double an = 0.0;
   if (warp == 0) {
-    for (int i = 0; i < n; ++i)
-      for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(a(i, j));
+    for (int i = 0; i < n; ++i) {
+      const double* ri = a.row(i);
+      for (int j = (i > 0 ? i - 1 : 0) + lane; j < n; j += 32) an += fabs(ri[j]);
+    }
     an = wsum(an);
   }
   int nn = n - 1, stall = 0, status = 0;
@@ -358,7 +423,14 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
     }
     const int nact = nn - l + 1;
     if (nact <= MS_SMALL || stall >= MS_STALL) {        // single-bulge iteration on [l, nn]
-      if (warp == 0) {
+      if (nact <= MS_SMALL) {
+        ms_copy_block(a, l, nact, sh->dense, tid);
+        __syncthreads();
+        if (warp == 0) {
+          const int rc = qr_block(DenseAcc{sh->dense, MS_DLD}, 0, nact - 1, wv + l, lane, total_its, cnt);
+          if (lane == 0) sh->fail = rc;
+        }
+      } else if (warp == 0) {
         const int rc = qr_block(a, l, nn, wv, lane, total_its, cnt);
         if (lane == 0) sh->fail = rc;
       }
@@ -370,20 +442,15 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
       if (status) return status;
       continue;
     }
-    // ---- shifts: eigenvalues of the trailing ns x ns block (warp 0, small packed copy)
+    // ---- shifts: eigenvalues of the trailing ns x ns block (dense copy, warp 0)
     int ns = 2 * MS_NB;
     if (ns > ((nact - 2) & ~1)) ns = (nact - 2) & ~1;
     const long long t_sh0 = clock64();
+    ms_copy_block(a, nn - ns + 1, ns, sh->dense, tid);
+    __syncthreads();
     if (warp == 0) {
-      const int b0 = nn - ns + 1;
-      HsAcc sm{sh->small_hs, ns};
-      for (int i = 0; i < ns; ++i) {
-        const int lo_i = i > 3 ? i - 3 : 0;
-        for (int j = lo_i + lane; j < ns; j += 32) sm(i, j) = (j >= i - 1) ? a(b0 + i, b0 + j) : 0.0;
-      }
-      __syncwarp();
       int its_s = 0;
-      const int rc = qr_block(sm, 0, ns - 1, sh->sw, lane, &its_s, nullptr);
+      const int rc = qr_block(DenseAcc{sh->dense, MS_DLD}, 0, ns - 1, sh->sw, lane, &its_s, nullptr);
       __syncwarp();
       if (lane == 0) {
         int nb = 0;
@@ -415,96 +482,64 @@ static __device__ int multishift_qr(HsAcc a, int n, double2* wv, MsShared* sh, i
     if (tid == 0 && shift_cycles) *shift_cycles += clock64() - t_sh0;
     const int nbe = sh->nbe;
     if (nbe == 0) { stall = MS_STALL; continue; }
-    // ---- chase nbe bulges in lockstep
+    // ---- chase nbe bulges in lockstep, bulge b on warps 2b (half 0) and 2b+1 (half 1)
+    const int b = warp >> 1, half = warp & 1;
+    const double st_b = (b < nbe) ? sh->st[b] : 0.0, sd_b = (b < nbe) ? sh->sd[b] : 0.0;
     const int G = (nn - 1 - l) + MS_SPACING * (nbe - 1);
+    MsRefl rf{};                       // reflector of the current step (both halves)
+    long long t_ab = 0, t_c = 0;
     for (int g = 0; g <= G; ++g) {
-      // (A) reflectors
-      if (warp < nbe) {
-        const int b = warp;
-        const int k = l + g - MS_SPACING * b;
-        const bool act = (k >= l && k <= nn - 1);
-        if (act) {
-          const bool three = (k != nn - 1);
-          double P, Q, R;
-          if (k == l) {
-            const double h00 = a(l, l), h10 = a(l + 1, l), h01 = a(l, l + 1), h11 = a(l + 1, l + 1);
-            const double h21 = a(l + 2, l + 1);
-            P = h00 * (h00 - sh->st[b]) + sh->sd[b] + h01 * h10;
-            Q = h10 * (h00 + h11 - sh->st[b]);
-            R = h10 * h21;
-          } else {
-            P = a(k, k - 1);
-            Q = a(k + 1, k - 1);
-            R = three ? a(k + 2, k - 1) : 0.0;
+      const long long t0 = clock64();
+      const int k = l + g - MS_SPACING * b;
+      const bool act = (b < nbe) && (k >= l && k <= nn - 1);
+      const bool three = (k != nn - 1);
+      if (act) {
+        if (k == l) {                  // introduce the bulge: first column of (H - s1)(H - s2)
+          const double* rl0 = a.row(l);
+          const double* rl1 = a.row(l + 1);
+          const double h00 = rl0[l], h01 = rl0[l + 1], h10 = rl1[l], h11 = rl1[l + 1];
+          const double h21 = a(l + 2, l + 1);
+          rf = ms_reflector(h00 * (h00 - st_b) + sd_b + h01 * h10, h10 * (h00 + h11 - st_b), h10 * h21);
+        } else {                       // both halves, redundantly, from the bulge column k-1
+          rf = ms_reflector(a(k, k - 1), a(k + 1, k - 1), three ? a(k + 2, k - 1) : 0.0);
+        }
+        if (rf.on) {                   // (AB) rows k..k+2, columns k..nn
+          double* r0 = a.row(k);
+          double* r1 = a.row(k + 1);
+          double* r2 = three ? a.row(k + 2) : r1;
+          for (int j = k + half * 32 + lane; j <= nn; j += 64) {
+            const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
+            const double pr = a0 + rf.q * a1 + rf.r * a2;
+            if (three) r2[j] = a2 - pr * rf.z;
+            r1[j] = a1 - pr * rf.y;
+            r0[j] = a0 - pr * rf.x;
           }
-          double xs = 1.0;
-          const double sc = fabs(P) + fabs(Q) + fabs(R);
-          const double ss0 = P * P + Q * Q + R * R;
-          if (!(ss0 > 1e-280 && ss0 < 1e280) && sc != 0.0) {
-            const double isc = 1.0 / sc;
-            P *= isc; Q *= isc; R *= isc;
-            xs = sc;
-          }
-          const double s = copysign(sqrt(P * P + Q * Q + R * R), P);
-          if (lane == 0) {
-            sh->bk[b] = k;
-            sh->bthree[b] = three ? 1 : 0;
-            sh->bon[b] = (s != 0.0) ? 1 : 0;
-            if (s != 0.0) {
-              if (k > l) {
-                a(k, k - 1) = -s * xs;
-                a(k + 1, k - 1) = 0.0;
-                if (three) a(k + 2, k - 1) = 0.0;
-              }
-              const double pp = P + s;
-              const double inv = 1.0 / (s * pp);
-              const double is = pp * inv, ip = s * inv;
-              sh->bx[b] = pp * is;
-              sh->by[b] = Q * is;
-              sh->bz[b] = R * is;
-              sh->bq[b] = Q * ip;
-              sh->br[b] = R * ip;
-            }
-          }
-        } else if (lane == 0) {
-          sh->bon[b] = 0;
         }
       }
       __syncthreads();
-      // (B) row updates: rows k..k+2, columns k..nn (two warps per bulge)
-      if ((warp >> 1) < nbe && sh->bon[warp >> 1]) {
-        const int b = warp >> 1, k = sh->bk[b];
-        const bool three = sh->bthree[b] != 0;
-        const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
-        double* r0 = &a(k, 0);
-        double* r1 = &a(k + 1, 0);
-        double* r2 = &a(three ? k + 2 : k + 1, 0);
-        for (int j = k + (warp & 1) * 32 + lane; j <= nn; j += 64) {
-          const double a0 = r0[j], a1 = r1[j], a2 = three ? r2[j] : 0.0;
-          const double pp = a0 + q * a1 + r * a2;
-          if (three) r2[j] = a2 - pp * z;
-          r1[j] = a1 - pp * y;
-          r0[j] = a0 - pp * x;
+      const long long t1 = clock64();
+      if (act && rf.on) {
+        // (C) columns k..k+2, rows l..min(nn, k+3); bulge column k-1
+        if (half == 0 && lane == 0 && k > l) {
+          a(k, k - 1) = rf.sxs;
+          a(k + 1, k - 1) = 0.0;
+          if (three) a(k + 2, k - 1) = 0.0;
         }
-      }
-      __syncthreads();
-      // (C) column updates: columns k..k+2, rows l..min(nn, k+3) (two warps per bulge)
-      if ((warp >> 1) < nbe && sh->bon[warp >> 1]) {
-        const int b = warp >> 1, k = sh->bk[b];
-        const bool three = sh->bthree[b] != 0;
-        const double x = sh->bx[b], y = sh->by[b], z = sh->bz[b], q = sh->bq[b], r = sh->br[b];
         const int mmin = nn < k + 3 ? nn : k + 3;
-        for (int i = l + (warp & 1) * 32 + lane; i <= mmin; i += 64) {
-          double* ri = &a(i, 0);
+        for (int i = l + half * 32 + lane; i <= mmin; i += 64) {
+          double* ri = a.row(i);
           const double c0 = ri[k], c1 = ri[k + 1], c2 = three ? ri[k + 2] : 0.0;
-          const double pp = x * c0 + y * c1 + z * c2;
-          if (three) ri[k + 2] = c2 - pp * r;
-          ri[k + 1] = c1 - pp * q;
-          ri[k] = c0 - pp;
+          const double pc = rf.x * c0 + rf.y * c1 + rf.z * c2;
+          if (three) ri[k + 2] = c2 - pc * rf.r;
+          ri[k + 1] = c1 - pc * rf.q;
+          ri[k] = c0 - pc;
         }
       }
       __syncthreads();
+      t_ab += t1 - t0;
+      t_c += clock64() - t1;
     }
+    if (tid == 0 && chase_cycles) { chase_cycles[0] += t_ab; chase_cycles[1] += t_c; }
     if (tid == 0) { *total_its += 1; if (cnt) { cnt[1] += G + 1; cnt[3] += 1; } }
     ++stall;
   }
@@ -742,6 +777,41 @@ k4a_kernel(const K4Params p) {
   }
   if (gtid < JACOBI_MAX_SWEEPS) p.flags[gtid] = 0;
   cl_sync();
+  // ---- warm start (one-sided Jacobi is applied to S·Q0 for any orthogonal Q0: its converged
+  // columns are still V·Λ).  Q0 = the previous frame's eigenvectors with rows shifted by the k
+  // frames the window moved (Q0[i][j] = V_prev[(i + k) mod m][j]), which leaves far fewer
+  // rotations to do than Q0 = I.
+  {
+    __shared__ int sh_warm;
+    if (tid == 0) {
+      const volatile K4Result* rp = p.res_prev;
+      sh_warm = (p.Vprev != nullptr && rp != nullptr && p.warm_k > 0 && rp->vframe == f - p.warm_k) ? 1 : 0;
+    }
+    __syncthreads();
+    if (sh_warm) {                              // uniform across the cluster (same inputs)
+      const int cb = (m + K4_CLUSTER - 1) / K4_CLUSTER;
+      const int j0 = crank * cb, j1 = min(m, j0 + cb);
+      const int nj = j1 > j0 ? j1 - j0 : 0;
+      double* q0 = reinterpret_cast<double*>(k4_smem);        // [nj][m]: Q0 columns j0..j1
+      for (int e = tid; e < nj * m; e += K4_THREADS) {
+        const int jj = e / m, i = e % m;
+        int src = i + p.warm_k;
+        src -= (src >= m) ? m : 0;
+        q0[e] = __ldcg(p.Vprev + (long long)(j0 + jj) * m + src);
+      }
+      __syncthreads();
+      for (int e = tid; e < nj * m; e += K4_THREADS) {        // B[:, j] = S Q0[:, j]
+        const int jj = e / m, i = e % m;
+        const double* qj = q0 + jj * m;
+        double acc = 0.0;
+        for (int kk = 0; kk < m; ++kk) acc = fma(__ldcg(p.A + (long long)kk * m + i), qj[kk], acc);
+        p.B[(long long)(j0 + jj) * m + i] = acc;
+      }
+      cl_sync();
+      for (int e = tid; e < nj * m; e += K4_THREADS) p.A[(long long)j0 * m + e] = __ldcg(p.B + (long long)j0 * m + e);
+      cl_sync();
+    }
+  }
   if (tid == 0) ph[1] = clock64();
 
   // ---- a5: one-sided (Hestenes) block Jacobi on S.  The m columns form 8 blocks; a block sweep
@@ -874,7 +944,7 @@ k4a_kernel(const K4Params p) {
     if (crank == 0) {
       for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
       if (tid == 0) {
-        res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps;
+        res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps; res->vframe = -1;
         res->qr_its = 0; res->sigma1 = sig[0];
       }
     }
@@ -1026,6 +1096,7 @@ k4a_kernel(const K4Params p) {
     ph[5] = clock64();
     res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
     res->qr_its = 0; res->sigma1 = sig[0];
+    res->vframe = converged ? f : -1;            // V usable as the next warm start
     for (int q = 0; q < 5; ++q) res->phase[q] = ph[q + 1] - ph[q];
     res->phase[5] = res->phase[6] = 0;
   }
@@ -1079,9 +1150,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     if (tid == 0) its_sh = 0;
     __syncthreads();
     int its_local = 0;
-    long long shift_cyc = 0;
-    const int rc = multishift_qr(HsAcc{hs, r}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
-                                 warp == 0 ? qc_sh : nullptr, &shift_cyc);
+    __shared__ int roff_sh[kMaxR];
+    for (int i = tid; i < r; i += K4_THREADS) roff_sh[i] = (int)(hs_off(i, r) - (i > 3 ? i - 3 : 0));
+    __syncthreads();
+    long long shift_cyc = 0, chase_cyc[2] = {0, 0};
+    const int rc = multishift_qr(RowAcc{hs, roff_sh}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
+                                 warp == 0 ? qc_sh : nullptr, &shift_cyc, chase_cyc);
     if (warp == 0 && lane == 0) atomicAdd(&its_sh, its_local);
     __syncthreads();
     if (tid == 0) {
@@ -1090,6 +1164,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       res->qr_cnt[0] = qc_sh[0]; res->qr_cnt[1] = qc_sh[1]; res->qr_cnt[2] = qc_sh[2];
       res->qr_cnt[3] = qc_sh[3];
       res->phase[7] = shift_cyc;
+      res->qr_dbg[0] = chase_cyc[0];
+      res->qr_dbg[1] = chase_cyc[1];
     }
   }
   __syncthreads();

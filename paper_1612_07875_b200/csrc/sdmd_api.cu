@@ -96,6 +96,7 @@ struct sdmd_ctx {
   // workers
   Workspace ws[kMaxWS];
   int NWS = 0, Wa = 1, Wb = 4;
+  bool warm = true;                     // Jacobi warm start (SDMD_WARM=0 disables, A/B)
   cudaStream_t sa[kMaxWorkers]{};      // cluster eigen workers (K4a: Jacobi .. Hessenberg)
   cudaStream_t sb[kMaxWorkers]{};      // single-CTA eigen workers (K4b: QR .. background coeffs)
   cudaEvent_t ev_a[kEvents]{};
@@ -292,6 +293,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
     const char* ed = std::getenv("SDMD_K1_DBG");
     c->k1_dbg = ed ? std::atoi(ed) : 0;
+    const char* ew = std::getenv("SDMD_WARM");
+    c->warm = !(ew && ew[0] == '0');
     const char* eb = std::getenv("SDMD_BG_NODMD");
     c->bg_nodmd = eb && eb[0] == '1';
   }
@@ -445,6 +448,11 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.res = k.res;
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
+  // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa)
+  if (c->warm && c->Wa < c->NWS && f - c->Wa >= c->cfg.m) {
+    const Workspace& kp = c->ws[(f - c->Wa) % c->NWS];
+    p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = c->Wa;
+  }
   return p;
 }
 
@@ -455,6 +463,9 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   if ((e = cudaStreamWaitEvent(A, c->ev_commit[t % kEvents], 0)) != cudaSuccess) return e;
   if (t - c->NWS >= c->cfg.m)                  // workspace reuse: frame t-NWS must be finished
     if ((e = cudaStreamWaitEvent(A, c->ev_done[(t - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
+  // ... and frame t+Wa-NWS (whose warm start reads this workspace's V) must have passed K4a
+  if (c->warm && c->Wa < c->NWS && t + c->Wa - c->NWS >= c->cfg.m)
+    if ((e = cudaStreamWaitEvent(A, c->ev_a[(t + c->Wa - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
   const K4Params p = k4_params(c, t);
   std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
   if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
@@ -890,7 +901,7 @@ int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[20]) {
   out[4] = res.sweeps; out[5] = res.qr_its;
   for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q];
   out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[3];
-  out[16] = res.phase[7]; out[17] = res.qr_cnt[2];
+  out[16] = res.phase[7]; out[17] = res.qr_cnt[2]; out[18] = res.qr_dbg[0]; out[19] = res.qr_dbg[1];
   return SDMD_OK;
 }
 

@@ -68,7 +68,9 @@ struct K4Result {
   double b_idx[2];
   double sigma1;
   long long phase[8];         // SM cycles per K4 phase: build S, Jacobi, sort/V, Ã, Hessenberg (K4a), QR, eigvec+c (K4b)
-  int qr_cnt[4];              // QR: bulge-chase steps, deflation-scan and shift-search iterations
+  int qr_cnt[4];              // QR: single-bulge steps, multishift steps, single-bulge its, multishift sweeps
+  long long qr_dbg[2];        // SM cycles of the multishift chase: (AB) phase + barrier, (C) phase + barrier (warp 0)
+  long long vframe;           // frame whose converged eigenvectors V this workspace holds (K4a), or -1
 };
 
 struct K4Params {
@@ -100,6 +102,11 @@ struct K4Params {
   double* mu;                 // m column norms
   double* wv;                 // kMaxR Householder scratch
   double* uv;                 // kMaxR Householder scratch
+  // Jacobi warm start: eigenvectors of frame f - warm_k (same cluster stream, so complete), used
+  // when res_prev->vframe == f - warm_k; else cold start from S
+  const double* Vprev;
+  const K4Result* res_prev;
+  int warm_k;
 };
 
 // per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)

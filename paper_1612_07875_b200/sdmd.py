@@ -371,7 +371,8 @@ class StreamingDMD:
                     sweeps=int(o[4]), qr_its=int(o[5]),
                     cycles={k: int(v) for k, v in zip(names, o[6:13])},
                     qr_steps=int(o[13]), ms_steps=int(o[14]), ms_sweeps=int(o[15]),
-                    ms_shift_cycles=int(o[16]), qr_block_its=int(o[17]))
+                    ms_shift_cycles=int(o[16]), qr_block_its=int(o[17]),
+                    ms_chase_ab_cycles=int(o[18]), ms_chase_c_cycles=int(o[19]))
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")
