@@ -8,12 +8,17 @@
 // mask = s > threshold: the columns of X'_{t'} are streamed anyway, so the
 // background costs no extra HBM reads beyond lag-1 columns.
 //
-// Work split: persistent grid (one 256-thread CTA per SM); a CTA walks 256-row super-tiles;
-// warp w owns union columns j ≡ w (mod 8); each lane holds 8 rows of the new frame x_t (fp64)
-// and streams 16-byte vectors of its columns (evict-first: the ring is ≫ L2).  Per-column partial
-// dots are warp-reduced per tile into shared memory (deterministic order), written per CTA, and
-// the last CTA to finish reduces the CTA partials in fixed order and commits the column into the
-// Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
+// Two implementations of the same pass (bitwise-deterministic, different fixed summation orders):
+//  * k1v2_kernel (default): 512-thread CTAs (one per SM), 128-row tiles, one 16-byte vector per
+//    lane per column, warp w owns union columns j ≡ w (mod 16) and walks exactly NQ of them
+//    (branch-free: columns past the union read the L1-resident x_t tile with a zero coefficient),
+//    column batches double-buffered in registers across tiles, 32-bit slot offsets.  Background
+//    partials are published per tile to shared memory and summed over the 16 warps by ONE
+//    designated warp per tile, K1V2_LAGR tiles later (no lockstep reduction).
+//  * k1_gram_kernel (v1, SDMD_K1=v1, A/B only): 8 rows per lane, all warps reduce every tile.
+// Per-column partial dots stay in registers for the whole pass, are warp-reduced once, written
+// per CTA, and the last CTA reduces the CTA partials in fixed order and commits the column into
+// the Gram history (nranks == 1).  No floating-point atomics: results are bitwise reproducible.
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -788,14 +793,9 @@ static cudaError_t launch_k1v2_nq(const K1Params& p, int grid, int U, cudaStream
   return launch_k1v2_inst<T, BG, K1_NQMAX>(p, grid, s);
 }
 
-static bool k1_use_v1() {
-  static const bool v1 = [] { const char* e = std::getenv("SDMD_K1"); return e && std::strcmp(e, "v1") == 0; }();
-  return v1;
-}
-
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
   const int es = dtype == 0 ? 4 : 8;
-  if (!k1_use_v1() && (unsigned long long)p.NS * (unsigned long long)p.ld * es / 16 < (1ull << 32)) {
+  if (!p.v1 && (unsigned long long)p.NS * (unsigned long long)p.ld * es / 16 < (1ull << 32)) {
     const int U = p.bg ? (p.nd > (int)(p.f_new - p.f_bg) + p.m ? p.nd : (int)(p.f_new - p.f_bg) + p.m) : p.nd;
     if (U > K1_MAXU) return cudaErrorInvalidValue;
     cudaError_t e;

@@ -72,7 +72,7 @@ struct sdmd_ctx {
   bool own_stream = false;
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
-  bool k1_ldg = true;                   // SDMD_K1=tma selects the bulk-copy (TMA) K1 variant (A/B)
+  int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
   long long ld = 0;
   size_t es = 4;
   void* ring = nullptr;
@@ -290,7 +290,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   }
   {
     const char* ev = std::getenv("SDMD_K1");
-    c->k1_ldg = !(ev && std::strcmp(ev, "tma") == 0);
+    c->k1_v1 = (ev && std::strcmp(ev, "v1") == 0) ? 1 : 0;
     const char* ed = std::getenv("SDMD_K1_DBG");
     c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* ew = std::getenv("SDMD_WARM");
@@ -515,8 +515,8 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.dbg = c->k1_dbg;
     p.partials = c->partials; p.pgrid = c->pgrid; p.gout = c->gout; p.do_commit = do_commit;
     p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
-    if (c->k1_ldg) CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));
-    else CK(launch_k1_tma(p, c->cfg.dtype, c->k1_grid, c->stream));
+    p.v1 = c->k1_v1;
+    CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));
     c->launches += 1;
     if (c->timing) {
       CK(cudaEventRecord(tp.second, c->stream));

@@ -46,9 +46,10 @@ struct K1Params {
   void* sparse;               // n (dtype)
   unsigned char* mask;        // n
   float thr;
-  double* partials;           // K1: [nd][pgrid] (column-major, coalesced reduction); TMA: [grid][kMaxM+16]
+  double* partials;           // K1: [nd][pgrid] (column-major, coalesced reduction)
   int pgrid;                  // partials stride of K1 (>= gridDim.x)
   int dbg;                    // microbenchmark knob (SDMD_K1_DBG): 1 skip bg reduction, 2 skip bg FMAs
+  int v1;                     // 1: the v1 K1 (8 rows per lane, lockstep background reduction), A/B only
   double* gout;               // nd reduced values (pre-allreduce)
   int do_commit;              // nranks == 1: commit inside the kernel's last block
   double* ghist;
@@ -165,8 +166,6 @@ static __device__ __forceinline__ void commit_block(const double* gout, int nd, 
 
 // kernels (defined in k1_gram.cu, k3_sparse.cu, k4_eigen.cu, k2_dmma.cu)
 cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s);
-cudaError_t launch_k1_tma(const K1Params& p, int dtype, int grid, cudaStream_t s);
-size_t k1_tma_smem_bytes(int dtype, int bg);
 void preload_k1_kernels();
 void preload_k4_kernels();
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);

@@ -1,0 +1,155 @@
+"""Snapshots/s of the streamed DMD on every BASELINE.json config, one GPU.
+
+    python scripts/bench_configs.py [--frames K] [--workers W] [--out profiles/x.md]
+
+C4 is bench.py's headline line; this script covers the other configs with the same protocol:
+init_window + a warm-up of 2(m+1) pushes (steady state), then K timed pushes from
+device-resident inputs (CUDA events on the library stream, device-side join of the eigen
+workers inside the timed region).  C1/C2 are fp64 planted-mode streams, C3 a 1920x1080 fp32
+video with background subtraction, C5 sparse orthonormal-DCT snapshots (K3).  Each line reports
+the binding resource: the Gram pass (K1/K3) average and the eigen-worker (K4a+K4b) average.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_1612_07875_b200 import StreamingDMD  # noqa: E402
+
+
+def timed(eng, push, K):
+    eng.sync()
+    eng.stats(reset=True)
+    eng.set_timing(True)
+    s = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    for j in range(K):
+        push(j)
+    eng.join()
+    e1.record(s)
+    e1.synchronize()
+    eng.sync()
+    ms = e0.elapsed_time(e1)
+    st = eng.stats(reset=True)
+    eng.set_timing(False)
+    return ms, st
+
+
+def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0):
+    P = frames_dev.shape[0]
+    eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max)
+    eng.init_window(frames_dev[: m + 1])
+    t = m + 1
+    for _ in range(2 * (m + 1)):
+        eng.push(frames_dev[t % P])
+        t += 1
+    base = t
+
+    def push(j):
+        eng.push(frames_dev[(base + j) % P])
+
+    ms, st = timed(eng, push, K)
+    sp = eng.spectrum()
+    es = 4 if dtype == "f32" else 8
+    k1 = st["k1_ms"] / max(1, st["k1_launches"])
+    alg = (m + 1) * n * es + (9 * n if background else 0)
+    out = {"config": name, "n": n, "m": m, "dtype": dtype, "frames": K, "workers": workers,
+           "snapshots_per_s": round(K / (ms / 1e3), 2), "ms_per_step": round(ms / K, 4),
+           "gram_pass_ms": round(k1, 4), "gram_pass_GBps": round(alg / (k1 / 1e3) / 1e9, 1),
+           "k4_ms_avg": round(st["k4_ms"] / max(1, st["k4_launches"]), 3),
+           "r": sp["r"], "idx": sp["idx"], "gpu_launches": int(st["gpu_launches"])}
+    eng.close()
+    return out
+
+
+def sparse_run(K, workers, pool=160):
+    ss = synth.SparseDCTStream()
+    m = 128
+    host = [ss.frame(t) for t in range(pool)]
+    cap = ss.nnz_cap
+    idx_d = [torch.from_numpy(np.ascontiguousarray(i)).cuda() for i, _ in host]
+    val_d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for _, v in host]
+    eng = StreamingDMD(ss.n, m, dtype="f64", storage="sparse", nnz_cap=cap, workers=workers)
+    t = 0
+    for _ in range(3 * (m + 1)):
+        eng.push_sparse(idx_d[t % pool], val_d[t % pool])
+        t += 1
+    base = t
+
+    def push(j):
+        q = (base + j) % pool
+        eng.push_sparse(idx_d[q], val_d[q])
+
+    ms, st = timed(eng, push, K)
+    sp = eng.spectrum()
+    k3 = st["k1_ms"] / max(1, st["k1_launches"])
+    nnz = float(np.mean([i.size for i, _ in host]))
+    out = {"config": "C5", "n": ss.n, "m": m, "dtype": "f64 sparse", "nnz_avg": round(nnz, 1),
+           "frames": K, "workers": workers, "snapshots_per_s": round(K / (ms / 1e3), 2),
+           "ms_per_step": round(ms / K, 4), "gram_pass_ms": round(k3, 4),
+           "k4_ms_avg": round(st["k4_ms"] / max(1, st["k4_launches"]), 3),
+           "r": sp["r"], "idx": sp["idx"], "gpu_launches": int(st["gpu_launches"]),
+           "note": "frames cycle through a pool of 160 pre-generated sparse frames (the same "
+                   "frame re-enters the window after 160 slides)"}
+    eng.close()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--frames", type=int, default=500)
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    res = []
+    # C1: 64 streamed frames (BASELINE configs[0])
+    pm = synth.planted_c1()
+    X = pm.frames(0, 16 + 1 + 64 + 2 * 17)
+    Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+    res.append(dense_run("C1", Xd, pm.n, 16, "f64", 64, 4))
+    print(json.dumps(res[-1]), flush=True)
+    # C2: cylinder-wake field, periodic (30 frames), fp64, m = 150, r = 21
+    cw = synth.cylinder_wake()
+    Xc = cw.frames(0, 300)
+    Xcd = torch.from_numpy(np.ascontiguousarray(Xc.T)).cuda()
+    res.append(dense_run("C2", Xcd, cw.n, 150, "f64", args.frames, args.workers, r_max=21))
+    print(json.dumps(res[-1]), flush=True)
+    del Xcd
+    # C3: 1920x1080 grey fp32 video, m = 100, background subtraction
+    vs = synth.video_config("C3")
+    Pn = 400
+    pool = torch.empty((Pn, vs.n), dtype=torch.float32, device="cuda")
+    for t in range(Pn):
+        pool[t].copy_(vs.frame(t, device="cuda"))
+    res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, args.workers, background=True))
+    print(json.dumps(res[-1]), flush=True)
+    del pool
+    torch.cuda.empty_cache()
+    # C5: sparse DCT, m = 128
+    res.append(sparse_run(args.frames, args.workers))
+    print(json.dumps(res[-1]), flush=True)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write("| config | n | m | dtype | frames | workers | snapshots/s | ms/step | Gram pass ms "
+                     "| Gram GB/s | K4 ms (per frame, concurrent) | r |\n|---|---|---|---|---|---|---|---|---|---|---|---|\n")
+            for r in res:
+                fh.write(f"| {r['config']} | {r['n']} | {r['m']} | {r['dtype']} | {r['frames']} | "
+                         f"{r['workers']} | {r['snapshots_per_s']} | {r['ms_per_step']} | "
+                         f"{r['gram_pass_ms']} | {r.get('gram_pass_GBps', '—')} | {r['k4_ms_avg']} | {r['r']} |\n")
+
+
+if __name__ == "__main__":
+    main()

@@ -13,7 +13,7 @@ from paper_1612_07875_b200 import StreamingDMD  # noqa: E402
 
 n, m = 3840 * 2160 * 3, 200
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 30
-modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["ldg", "tma"]
+modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["v2", "v1"]
 src = torch.rand(n, device="cuda:0")
 os.environ["SDMD_BG_NODMD"] = "1"
 for mode in modes:

@@ -373,18 +373,19 @@ def test_c4_full_size_sampled():
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
-def test_k1_tma_and_ldg_variants_agree(dtype, monkeypatch):
-    """The register-streaming K1 (default) and the TMA bulk-copy K1 (SDMD_K1=tma) compute the
-    same Gram columns and background (different fixed summation orders)."""
+def test_k1_v2_and_v1_variants_agree(dtype, monkeypatch):
+    """The default K1 (v2: one vector per lane, designated-warp background reduction) and the v1
+    K1 (SDMD_K1=v1: 8 rows per lane, lockstep reduction) compute the same Gram columns and
+    background (different fixed summation orders)."""
     vs = synth.video_config("C3s")
     m, T = 24, 40
     npdt = np.float32 if dtype == "f32" else np.float64
     frames = vs.frames(0, T).numpy().astype(npdt)
     Xd = dev_cols(frames, npdt)
     outs = []
-    for mode in ("ldg", "tma"):
-        if mode == "tma":
-            monkeypatch.setenv("SDMD_K1", "tma")
+    for mode in ("v2", "v1"):
+        if mode == "v1":
+            monkeypatch.setenv("SDMD_K1", "v1")
         else:
             monkeypatch.delenv("SDMD_K1", raising=False)
         eng = Eng(vs.n, m, dtype=dtype, background=True, workers=2)
