@@ -204,7 +204,7 @@ def run_ours(args):
         # device-resident pool of distinct frames (cycled only if HBM cannot hold them all)
         free, _ = torch.cuda.mem_get_info(dev)
         frame_bytes = n_loc * 4
-        lag = args.lag if args.lag > 0 else min(2 * args.workers, 16)   # library default
+        lag = args.lag if args.lag > 0 else min(2 * args.workers, 32)   # library default
         ring_bytes = (M + lag + 1) * ((n_loc + 255) // 256 * 256) * 4
         budget = free - ring_bytes - 12 * 2**30
         need = M + 1 + lag + W + K

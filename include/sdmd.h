@@ -48,7 +48,7 @@ extern "C" {
 
 #define SDMD_ABI_VERSION 1
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
-#define SDMD_MAX_LAG 16  /* largest background lag (frames)                                     */
+#define SDMD_MAX_LAG 32  /* largest background lag (frames)                                     */
 #define SDMD_MAX_R 224   /* largest rank r (shared-memory Hessenberg QR)    */
 
 enum sdmd_status {
@@ -88,7 +88,7 @@ typedef struct sdmd_config {
   int32_t background; /* 1: compute the newest background column every push (fused into the Gram
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
-  int32_t workers;    /* eigen-worker streams for the single-CTA stage (0 → 4); the cluster
+  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..16 (0 → 4); the cluster
                        * stage uses max(1, workers / 2) streams.  The context uses about
                        * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that
                        * (e.g. 32) before CUDA initialises, else streams share hardware queues
@@ -98,7 +98,7 @@ typedef struct sdmd_config {
   int32_t rank;       /* this rank, 0..nranks-1                                                 */
   int32_t nranks;     /* row shards; > 1 needs NCCL (uid from sdmd_nccl_unique_id on rank 0)   */
   const uint8_t* nccl_uid; /* 128 bytes, identical on all ranks; ignored when nranks == 1       */
-  int32_t lag;        /* background lag in frames, 1..16; 0 → min(2·workers, 16).  K1(t+lag)
+  int32_t lag;        /* background lag in frames, 1..32; 0 → min(2·workers, 32).  K1(t+lag)
                        * consumes the background coefficients of frame t, so K4 may take up to
                        * lag frame periods before the Gram pass waits                          */
   int32_t pad_;

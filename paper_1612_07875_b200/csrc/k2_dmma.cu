@@ -7,6 +7,9 @@
 //       Alg 2): a real n x m by complex m x nc product, computed as one real GEMM against
 //       the interleaved (re, im) columns of T = Y W.
 // tcgen05 has no f64 kind; the fp64 tensor path on sm_100a is DMMA (HMMA-class SASS "DMMA").
+#include <cstdlib>
+#include <cstring>
+
 #include "sdmd_internal.cuh"
 
 namespace sdmd {
@@ -27,7 +30,7 @@ constexpr int G_KC = 32;           // rows staged per step
 constexpr int G_THREADS = 256;     // 8 warps; warp w owns output rows 8w..8w+7 of the block
 
 template <typename T>
-__global__ void __launch_bounds__(G_THREADS) gram_dmma_kernel(const T* __restrict__ Z, long long ldz,
+__global__ void __launch_bounds__(G_THREADS) gram_dmma_v1_kernel(const T* __restrict__ Z, long long ldz,
                                                               long long n, int k, int nbk,
                                                               long long rows_per_split,
                                                               double* __restrict__ work) {
@@ -74,7 +77,7 @@ __global__ void __launch_bounds__(G_THREADS) gram_dmma_kernel(const T* __restric
   }
 }
 
-__global__ void gram_reduce_kernel(const double* __restrict__ work, int nblk, int nsplit, int nbk,
+__global__ void gram_reduce_v1_kernel(const double* __restrict__ work, int nblk, int nsplit, int nbk,
                                    int k, double* __restrict__ G) {
   const int b = blockIdx.x;
   int bidx = b, bi = 0;
@@ -98,13 +101,13 @@ static int g_nsplit(long long n) {
   return (int)s;
 }
 
-size_t init_gram_work_elems(long long n, int k) {
+static size_t init_gram_work_elems_v1(long long n, int k) {
   const int nbk = (k + G_BLK - 1) / G_BLK;
   const int nblk = nbk * (nbk + 1) / 2;
   return (size_t)g_nsplit(n) * nblk * G_BLK * G_BLK;
 }
 
-cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
+static cudaError_t launch_init_gram_v1(const void* Z, long long ldz, int dtype, long long n, int k,
                              double* Gout, double* work, cudaStream_t s) {
   const int nbk = (k + G_BLK - 1) / G_BLK;
   const int nblk = nbk * (nbk + 1) / 2;
@@ -113,12 +116,12 @@ cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long 
   rps = (rps + G_KC - 1) / G_KC * G_KC;
   dim3 grid(nblk, nsplit);
   if (dtype == 0)
-    gram_dmma_kernel<float><<<grid, G_THREADS, 0, s>>>((const float*)Z, ldz, n, k, nbk, rps, work);
+    gram_dmma_v1_kernel<float><<<grid, G_THREADS, 0, s>>>((const float*)Z, ldz, n, k, nbk, rps, work);
   else
-    gram_dmma_kernel<double><<<grid, G_THREADS, 0, s>>>((const double*)Z, ldz, n, k, nbk, rps, work);
+    gram_dmma_v1_kernel<double><<<grid, G_THREADS, 0, s>>>((const double*)Z, ldz, n, k, nbk, rps, work);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  gram_reduce_kernel<<<nblk, 256, 0, s>>>(work, nblk, nsplit, nbk, k, Gout);
+  gram_reduce_v1_kernel<<<nblk, 256, 0, s>>>(work, nblk, nsplit, nbk, k, Gout);
   return cudaGetLastError();
 }
 
@@ -129,7 +132,7 @@ constexpr int M_KC = 32;
 
 // T: m x nc complex, column-major (T[(j*m + k)] = (re, im)); phi: n x nc complex, column-major ld.
 template <typename T>
-__global__ void __launch_bounds__(256) modes_dmma_kernel(const T* __restrict__ ring, long long ld,
+__global__ void __launch_bounds__(256) modes_dmma_v1_kernel(const T* __restrict__ ring, long long ld,
                                                          int NS, long long n, long long first_frame,
                                                          int m, const double2* __restrict__ Tm,
                                                          int nc, int c0, double2* __restrict__ phi,
@@ -183,21 +186,361 @@ __global__ void __launch_bounds__(256) modes_dmma_kernel(const T* __restrict__ r
   }
 }
 
-cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long long n,
+static cudaError_t launch_modes_v1(const void* ring, long long ld, int NS, int dtype, long long n,
                          long long first_frame, int m, const double* T, int nc, double* phi,
                          long long ldphi, cudaStream_t s) {
   const int grid = (int)((n + M_ROWS - 1) / M_ROWS);
   for (int c0 = 0; c0 < nc; c0 += M_COLS / 2) {
     if (dtype == 0)
-      modes_dmma_kernel<float><<<grid, 256, 0, s>>>((const float*)ring, ld, NS, n, first_frame, m,
+      modes_dmma_v1_kernel<float><<<grid, 256, 0, s>>>((const float*)ring, ld, NS, n, first_frame, m,
                                                     (const double2*)T, nc, c0, (double2*)phi, ldphi);
     else
-      modes_dmma_kernel<double><<<grid, 256, 0, s>>>((const double*)ring, ld, NS, n, first_frame, m,
+      modes_dmma_v1_kernel<double><<<grid, 256, 0, s>>>((const double*)ring, ld, NS, n, first_frame, m,
                                                      (const double2*)T, nc, c0, (double2*)phi, ldphi);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ====================================================================== v2 (default) ==========
+// Both contractions: raw (fp32|fp64) tiles staged in shared memory by a 3-stage cp.async pipeline
+// (16-byte chunks, zero-fill outside the operand), fragments converted to fp64 when they are
+// loaded from shared memory (fp32 x fp32 products are exact in fp64, reading Q9), 32x32 warp tiles
+// = 4x4 DMMA m8n8k4 per 4-deep k step (16 DMMA per 8 fragment loads).  Shared-memory strides are
+// padded so that every fragment load is bank-conflict free (lane l reads row l%4, element l/4).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// ---- (a0) G = Zᵀ Z: 64x64 upper-triangular output blocks, 4 warps (2x2 warp tiles of 32x32);
+// warp tiles entirely below the diagonal or entirely past column k are skipped, and the rows are
+// split per block in proportion to its active warp tiles so that every CTA carries the same work
+// (one balanced wave).  Per-split partial blocks are reduced in fixed order (deterministic).
+constexpr int G2_KC = 32;                 // rows per stage
+constexpr int G2_ST = 3;                  // pipeline stages
+constexpr int G2_LDS = G2_KC + 4;         // staged column stride (elements): conflict-free frags
+constexpr int G2_THREADS = 128;
+constexpr int G2_MAXB = 21;               // upper-triangular 64-blocks for k <= 384
+constexpr int G2_MAXCTA_PER_SM = 8;
+
+struct GramPlan {
+  int nbk, nblk;
+  int split0[G2_MAXB + 1];                // CTA prefix per block
+  long long rps[G2_MAXB];                 // rows per split of each block (multiple of G2_KC)
+};
+
+template <typename T>
+__global__ void __launch_bounds__(G2_THREADS) gram_tc_kernel(const T* __restrict__ Z, long long ldz,
+                                                            long long nrows, int k, const GramPlan plan,
+                                                            double* __restrict__ work) {
+  extern __shared__ __align__(16) unsigned char g2_smem[];
+  T* sm = reinterpret_cast<T*>(g2_smem);  // [G2_ST][2 operands][64 columns][G2_LDS]
+  int b = 0;
+  while ((int)blockIdx.x >= plan.split0[b + 1]) ++b;
+  const long long sp = (long long)blockIdx.x - plan.split0[b];
+  int bi = 0, bidx = b;
+  while (bidx >= plan.nbk - bi) { bidx -= plan.nbk - bi; ++bi; }
+  const int bj = bi + bidx;
+  const bool diag = bi == bj;
+  const long long r0 = sp * plan.rps[b];
+  long long r1 = r0 + plan.rps[b];
+  if (r1 > nrows) r1 = nrows;
+  const int nsteps = r1 > r0 ? (int)((r1 - r0) / G2_KC) : 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wi = warp >> 1, wj = warp & 1;
+  const int ci0 = bi * 64 + wi * 32, cj0 = bj * 64 + wj * 32;
+  const bool active = !(diag && wi > wj) && ci0 < k && cj0 < k;
+  constexpr int EPC = 16 / (int)sizeof(T);     // elements per 16-byte chunk
+  constexpr int CPC = G2_KC / EPC;             // chunks per column per stage
+  const int nops = diag ? 1 : 2;               // a diagonal block stages its columns once
+  auto load = [&](int step, int buf) {
+    const long long row = r0 + (long long)step * G2_KC;
+    for (int o = 0; o < nops; ++o) {
+      const int cb = (o == 0 ? bi : bj) * 64;
+      T* dst = sm + (size_t)(buf * 2 + o) * 64 * G2_LDS;
+      for (int e = tid; e < 64 * CPC; e += G2_THREADS) {
+        const int c = e / CPC, ch = e % CPC;
+        const bool ok = cb + c < k;
+        const T* src = ok ? Z + (long long)(cb + c) * ldz + row + ch * EPC : Z;
+        cp_async16(dst + c * G2_LDS + ch * EPC, src, ok);
+      }
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < G2_ST - 1; ++s) {
+    if (s < nsteps) load(s, s);
+    cp_async_commit();
+  }
+  const int fr = (lane >> 2) * G2_LDS + (lane & 3);   // this lane's fragment offset
+  for (int step = 0; step < nsteps; ++step) {
+    cp_async_wait<G2_ST - 2>();
+    __syncthreads();
+    const int nx = step + G2_ST - 1;
+    if (nx < nsteps) load(nx, nx % G2_ST);
+    cp_async_commit();
+    if (active) {
+      const int buf = step % G2_ST;
+      const T* sa = sm + ((size_t)(buf * 2) * 64 + wi * 32) * G2_LDS + fr;
+      const T* sb = sm + ((size_t)(buf * 2 + (diag ? 0 : 1)) * 64 + wj * 32) * G2_LDS + fr;
+#pragma unroll
+      for (int kk = 0; kk < G2_KC; kk += 4) {
+        double a[4], bb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = (double)sa[i * 8 * G2_LDS + kk];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bb[j] = (double)sb[j * 8 * G2_LDS + kk];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  double* out = work + (size_t)blockIdx.x * 4096;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = wi * 32 + i * 8 + (lane >> 2), c = wj * 32 + j * 8 + 2 * (lane & 3);
+      *reinterpret_cast<double2*>(out + r * 64 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+__global__ void gram_tc_reduce_kernel(const double* __restrict__ work, const GramPlan plan, int k,
+                                      double* __restrict__ G) {
+  const int b = blockIdx.x;
+  int bi = 0, bidx = b;
+  while (bidx >= plan.nbk - bi) { bidx -= plan.nbk - bi; ++bi; }
+  const int bj = bi + bidx;
+  const int s0 = plan.split0[b], s1 = plan.split0[b + 1];
+  for (int e = threadIdx.x; e < 4096; e += blockDim.x) {
+    const int i = bi * 64 + e / 64, j = bj * 64 + e % 64;
+    if (i > j || j >= k) continue;             // upper triangle only; mirrored below
+    double s = 0.0;
+    for (int q = s0; q < s1; ++q) s += work[(size_t)q * 4096 + e];
+    G[(long long)j * k + i] = s;
+    G[(long long)i * k + j] = s;
+  }
+}
+
+static int g2_sm_count() {
+  static int nsm = [] {
+    int d = 0, v = 148;
+    cudaGetDevice(&d);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    return v;
+  }();
+  return nsm;
+}
+
+template <typename T>
+static size_t g2_smem() { return (size_t)G2_ST * 2 * 64 * G2_LDS * sizeof(T); }
+
+// Row splits per block proportional to the block's active warp tiles (equal work per CTA).
+static bool g2_plan(long long nrows, int k, int max_ctas, GramPlan& pl) {
+  pl.nbk = (k + 63) / 64;
+  pl.nblk = pl.nbk * (pl.nbk + 1) / 2;
+  if (pl.nblk > G2_MAXB) return false;
+  int act[G2_MAXB];
+  long long tot = 0;
+  for (int b = 0, bi = 0, bj = 0; b < pl.nblk; ++b) {
+    int a = 0;
+    for (int wi = 0; wi < 2; ++wi)
+      for (int wj = 0; wj < 2; ++wj)
+        if (!(bi == bj && wi > wj) && bi * 64 + wi * 32 < k && bj * 64 + wj * 32 < k) ++a;
+    act[b] = a;
+    tot += a;
+    if (++bj == pl.nbk) { ++bi; bj = bi; }
+  }
+  const long long steps = nrows / G2_KC;
+  // work per CTA (warp-tile steps), at least 8 steps of a full block
+  long long per = (tot * steps + max_ctas - 1) / max_ctas;
+  if (per < 32) per = 32;
+  // per-block rounding can exceed max_ctas (a partial second wave doubles the time): grow the
+  // per-CTA work until the whole grid is one wave
+  for (;;) {
+    pl.split0[0] = 0;
+    for (int b = 0; b < pl.nblk; ++b) {
+      long long sps = act[b] > 0 ? (per + act[b] - 1) / act[b] : steps;   // steps per split
+      if (sps < 1) sps = 1;
+      pl.rps[b] = sps * G2_KC;
+      const long long ns = act[b] > 0 ? (steps + sps - 1) / sps : 0;
+      pl.split0[b + 1] = pl.split0[b] + (int)ns;
+    }
+    if (pl.split0[pl.nblk] <= max_ctas) break;
+    per += per / 128 + 1;
+  }
+  for (int b = pl.nblk; b < G2_MAXB; ++b) pl.rps[b] = 0;
+  return true;
+}
+
+static int g2_max_ctas() { return g2_sm_count() * G2_MAXCTA_PER_SM + G2_MAXB; }
+
+size_t init_gram_work_elems(long long n, int k) {
+  (void)n; (void)k;
+  return (size_t)g2_max_ctas() * 4096;
+}
+
+// Z: ld-strided columns whose rows [n, roundup(n, 32)) are zero (the ring's padding).
+cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
+                             double* Gout, double* work, cudaStream_t s) {
+  static const bool v1 = [] { const char* e = std::getenv("SDMD_K2"); return e && std::strcmp(e, "v1") == 0; }();
+  if (v1) return launch_init_gram_v1(Z, ldz, dtype, n, k, Gout, work, s);
+  const long long nrows = (n + G2_KC - 1) / G2_KC * G2_KC;
+  if (nrows > ldz) return cudaErrorInvalidValue;
+  int occ = 1;
+  cudaError_t e;
+  const size_t smem = dtype == 0 ? g2_smem<float>() : g2_smem<double>();
+  if (dtype == 0) {
+    if ((e = cudaFuncSetAttribute(gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tc_kernel<float>, G2_THREADS, smem);
+  } else {
+    if ((e = cudaFuncSetAttribute(gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tc_kernel<double>, G2_THREADS, smem);
+  }
+  if (occ < 1) occ = 1;
+  if (occ > G2_MAXCTA_PER_SM) occ = G2_MAXCTA_PER_SM;
+  GramPlan pl{};
+  if (!g2_plan(nrows, k, g2_sm_count() * occ, pl)) return cudaErrorInvalidValue;
+  const int grid = pl.split0[pl.nblk];
+  if (grid > g2_max_ctas()) return cudaErrorInvalidValue;
+  if (grid > 0) {
+    if (dtype == 0)
+      gram_tc_kernel<float><<<grid, G2_THREADS, smem, s>>>((const float*)Z, ldz, nrows, k, pl, work);
+    else
+      gram_tc_kernel<double><<<grid, G2_THREADS, smem, s>>>((const double*)Z, ldz, nrows, k, pl, work);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  gram_tc_reduce_kernel<<<pl.nblk, 256, 0, s>>>(work, pl, k, Gout);
+  return cudaGetLastError();
+}
+
+// ---- (a12) Φ = X'(Y W): CTA = 128 rows x 32 complex modes (64 real columns), 8 warps (4x2 warp
+// tiles of 32x32), k = the m window columns of X' staged 16 at a time.  1-D grid, the mode
+// chunks of one row tile adjacent (they re-read the same X' rows from L2).
+constexpr int M2_ROWS = 128, M2_COLS = 64, M2_KC = 16, M2_ST = 3, M2_THREADS = 256;
+constexpr int M2_LDB = M2_COLS + 4;       // staged T stride (doubles)
+template <typename T> struct M2L { static constexpr int A = sizeof(T) == 4 ? M2_ROWS + 8 : M2_ROWS + 4; };
+
+template <typename T>
+static size_t m2_smem() { return (size_t)M2_ST * (M2_KC * M2L<T>::A * sizeof(T) + M2_KC * M2_LDB * sizeof(double)); }
+
+template <typename T>
+__global__ void __launch_bounds__(M2_THREADS) modes_tc_kernel(const T* __restrict__ ring, long long ld,
+                                                             int NS, long long n, long long first_frame,
+                                                             int m, const double2* __restrict__ Tm,
+                                                             int nc, double2* __restrict__ phi,
+                                                             long long ldphi, int nchunks) {
+  extern __shared__ __align__(16) unsigned char m2_smem_raw[];
+  constexpr int LDA = M2L<T>::A;
+  constexpr int ABYTES = M2_KC * LDA * (int)sizeof(T);
+  constexpr int SBYTES = ABYTES + M2_KC * M2_LDB * (int)sizeof(double);
+  const long long rt = blockIdx.x / nchunks;
+  const int q0 = (int)(blockIdx.x % nchunks) * (M2_COLS / 2);
+  const long long row0 = rt * M2_ROWS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wi = warp >> 1, wj = warp & 1;
+  constexpr int EPC = 16 / (int)sizeof(T);
+  constexpr int CPR = M2_ROWS / EPC;           // chunks per window column
+  const int nsteps = (m + M2_KC - 1) / M2_KC;
+  auto load = [&](int step, int buf) {
+    unsigned char* base = m2_smem_raw + (size_t)buf * SBYTES;
+    T* sA = reinterpret_cast<T*>(base);
+    double* sB = reinterpret_cast<double*>(base + ABYTES);
+    const int k0 = step * M2_KC;
+    for (int e = tid; e < M2_KC * CPR; e += M2_THREADS) {
+      const int kk = e / CPR, ch = e % CPR, kc = k0 + kk;
+      const bool ok = kc < m;
+      const T* src = ok ? ring + ((first_frame + kc) % NS) * ld + row0 + ch * EPC : ring;
+      cp_async16(sA + kk * LDA + ch * EPC, src, ok);
+    }
+    for (int e = tid; e < M2_KC * (M2_COLS / 2); e += M2_THREADS) {
+      const int kk = e / (M2_COLS / 2), q = e % (M2_COLS / 2), kc = k0 + kk;
+      const bool ok = kc < m && q0 + q < nc;
+      const double2* src = ok ? Tm + (long long)(q0 + q) * m + kc : Tm;
+      cp_async16(sB + kk * M2_LDB + 2 * q, src, ok);
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+  for (int s = 0; s < M2_ST - 1; ++s) {
+    if (s < nsteps) load(s, s);
+    cp_async_commit();
+  }
+  for (int step = 0; step < nsteps; ++step) {
+    cp_async_wait<M2_ST - 2>();
+    __syncthreads();
+    const int nx = step + M2_ST - 1;
+    if (nx < nsteps) load(nx, nx % M2_ST);
+    cp_async_commit();
+    const unsigned char* base = m2_smem_raw + (size_t)(step % M2_ST) * SBYTES;
+    const T* sa = reinterpret_cast<const T*>(base) + (lane & 3) * LDA + wi * 32 + (lane >> 2);
+    const double* sb = reinterpret_cast<const double*>(base + ABYTES) + (lane & 3) * M2_LDB + wj * 32 + (lane >> 2);
+#pragma unroll
+    for (int kk = 0; kk < M2_KC; kk += 4) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = (double)sa[kk * LDA + i * 8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = sb[kk * M2_LDB + j * 8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long long row = row0 + wi * 32 + i * 8 + (lane >> 2);
+    if (row >= n) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = q0 + (wj * 32 + j * 8) / 2 + (lane & 3);      // columns (2q, 2q+1) = (re, im)
+      if (q < nc) phi[(long long)q * ldphi + row] = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+  }
+}
+
+cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long long n,
+                         long long first_frame, int m, const double* T, int nc, double* phi,
+                         long long ldphi, cudaStream_t s) {
+  static const bool v1 = [] { const char* e = std::getenv("SDMD_K2"); return e && std::strcmp(e, "v1") == 0; }();
+  if (v1) return launch_modes_v1(ring, ld, NS, dtype, n, first_frame, m, T, nc, phi, ldphi, s);
+  const int nchunks = (nc + M2_COLS / 2 - 1) / (M2_COLS / 2);
+  const long long rts = (n + M2_ROWS - 1) / M2_ROWS;
+  if (rts * M2_ROWS > ld) return cudaErrorInvalidValue;
+  const long long grid = rts * nchunks;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidValue;
+  cudaError_t e;
+  if (dtype == 0) {
+    const size_t sm = m2_smem<float>();
+    if ((e = cudaFuncSetAttribute(modes_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
+    modes_tc_kernel<float><<<(unsigned)grid, M2_THREADS, sm, s>>>((const float*)ring, ld, NS, n, first_frame, m,
+                                                                  (const double2*)T, nc, (double2*)phi, ldphi, nchunks);
+  } else {
+    const size_t sm = m2_smem<double>();
+    if ((e = cudaFuncSetAttribute(modes_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
+    modes_tc_kernel<double><<<(unsigned)grid, M2_THREADS, sm, s>>>((const double*)ring, ld, NS, n, first_frame, m,
+                                                                   (const double2*)T, nc, (double2*)phi, ldphi, nchunks);
+  }
+  return cudaGetLastError();
 }
 
 // T = Y W[:, cols]  (m x nc complex): the "vsiw" product of Alg 2 P:315 for selected modes.

@@ -15,8 +15,8 @@ namespace sdmd {
 
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
-constexpr int kMaxWorkers = 8;
-constexpr int kMaxLag = 16;              // background lag cap (frames); union columns m + lag
+constexpr int kMaxWorkers = 16;
+constexpr int kMaxLag = 32;              // background lag cap (frames); union columns m + lag
 constexpr int kK1MaxWaves = 32;           // K1 grid <= kK1MaxWaves x SM count
 constexpr int kSuperTile = 256;           // K1 rows per CTA iteration (32 lanes x 8 rows)
 

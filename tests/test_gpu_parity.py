@@ -312,6 +312,80 @@ def test_init_window_dmma_gram(dtype):
     eng.close()
 
 
+def _planted_window(n, m, npairs, seed):
+    """n x (m+1) window of 2·npairs planted DMD modes x_t = Σ 2 Re(b_j φ_j λ_j^t) (fp64)."""
+    rng = np.random.default_rng(seed)
+    rho = rng.uniform(0.9, 1.0, npairs)
+    th = np.linspace(0.05, 3.0, npairs) + rng.uniform(-0.01, 0.01, npairs)
+    lam = rho * np.exp(1j * th)
+    phi = (rng.standard_normal((n, npairs)) + 1j * rng.standard_normal((n, npairs))) / np.sqrt(2 * n)
+    b = rng.standard_normal(npairs) + 1j * rng.standard_normal(npairs)
+    t = np.arange(m + 1)
+    return 2.0 * np.real((phi * b[None, :]) @ (lam[:, None] ** t[None, :]))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_modes_tensor_core_multi_chunk(dtype):
+    """K2 (a0 init Gram + a12 modes) on a ragged n with r = 40 > 32 modes (two mode chunks of
+    the modes kernel) and k = 71 (two Gram column blocks): b_j φ_j per mode and the
+    reconstruction Φ b against the oracle on the same (fp32-rounded) window."""
+    n, m, npairs = 20011, 70, 20
+    npdt = np.float32 if dtype == "f32" else np.float64
+    Z = _planted_window(n, m, npairs, seed=11).astype(npdt)
+    eng = Eng(n, m, dtype=dtype, workers=1, r_max=2 * npairs)
+    eng.init_window(dev_cols(Z, npdt))
+    eng.sync()
+    Zr = Z.astype(np.float64)
+    Gr = O.gram(Zr)
+    assert normwise(eng.gram(), Gr) < 1e-12
+    d = O.dmd_from_gram(Gr, r_max=2 * npairs)
+    b_ref, _ = O.amplitudes(d)
+    sp = eng.spectrum(with_b=True)
+    r = sp["r"]
+    assert r == d["r"] == 2 * npairs
+    err, perm = match(sp["lam"], d["lam"])
+    assert err < 1e-9
+    Phi = eng.modes(list(range(r))).cpu().numpy()
+    Phi_ref = O.modes([Zr[:, k] for k in range(1, m + 1)], d)
+    for j in range(r):
+        a = sp["b"][j] * Phi[:, j]
+        bb = b_ref[perm[j]] * Phi_ref[:, perm[j]]
+        assert np.linalg.norm(a - bb) < 1e-8 * np.linalg.norm(bb), j
+    rec, rec_ref = Phi @ sp["b"], Phi_ref @ b_ref
+    assert np.linalg.norm(rec - rec_ref) < 1e-9 * np.linalg.norm(rec_ref)
+    # a subset of columns in a non-contiguous order lands in the requested slots
+    cols = [r - 1, 0, 33, 5]
+    Ps = eng.modes(cols).cpu().numpy()
+    assert np.array_equal(Ps, Phi[:, cols])
+    eng.close()
+
+
+def test_init_window_c4_full_size_sampled():
+    """K2 init Gram at BASELINE config 4's full size (n = 24,883,200, m = 200, fp32): sampled
+    entries against fp64 dots of CPU-regenerated frames (normwise 1e-12, reading Q17)."""
+    vs = synth.video_config("C4")
+    m = 200
+    Zd = torch.empty((m + 1, vs.n), dtype=torch.float32, device="cuda:0")
+    for t in range(m + 1):
+        Zd[t] = vs.frame(t, device="cuda:0")
+    eng = Eng(vs.n, m, dtype="f32", workers=1)
+    eng.init_window(Zd)
+    eng.sync()
+    del Zd
+    G = eng.gram()
+    assert np.array_equal(G, G.T)
+    cache = {}
+
+    def fr(t):
+        if t not in cache:
+            cache[t] = vs.frame(t).numpy().astype(np.float64)
+        return cache[t]
+    for i, j in ((0, 0), (0, 200), (57, 123), (199, 200), (200, 200), (123, 123)):
+        ref = float(np.dot(fr(i), fr(j)))
+        assert abs(G[i, j] - ref) <= 1e-12 * math.sqrt(G[i, i] * G[j, j]), (i, j)
+    eng.close()
+
+
 # ---------------------------------------------------------------------- sparse (K3) -------
 
 def test_sparse_dct_gram_and_dmd():
