@@ -204,7 +204,9 @@ def run_ours(args):
         # device-resident pool of distinct frames (cycled only if HBM cannot hold them all)
         free, _ = torch.cuda.mem_get_info(dev)
         frame_bytes = n_loc * 4
-        lag = args.lag if args.lag > 0 else min(2 * args.workers, 32)   # library default
+        if args.lag < 0:
+            args.lag = 9 if N == 1 else 0
+        lag = args.lag if args.lag > 0 else min(2 * args.workers if N == 1 else args.workers * N + 6, 64)   # library default (eigen-sharded for N > 1)
         ring_bytes = (M + lag + 1) * ((n_loc + 255) // 256 * 256) * 4
         budget = free - ring_bytes - 12 * 2**30
         need = M + 1 + lag + W + K
@@ -298,7 +300,9 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded counter-based video generator, synth.video_config('C4'))",
         "config": {"workload": WORKLOAD, "n": n, "m": M, "n_local": n_loc, "storage": "f32",
-                   "parallelism": f"row-shard x{N}" + (" + NCCL allreduce of g" if N > 1 else ""),
+                   "parallelism": f"row-shard x{N}" + (" + NCCL allreduce of g; eigenproblems of frame t "
+                                                       "on rank t mod N + ncclBroadcast of c_t"
+                                                       if N > 1 else ""),
                    "eigen_workers": args.workers, "cluster_workers": info["cluster_workers"],
                    "k1_grid": info["k1_grid"], "lag": info["lag"],
                    "ring_slots": info["ring_slots"], "pool_frames": P,
@@ -360,7 +364,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workers", type=int, default=6)
-    ap.add_argument("--lag", type=int, default=0)
+    ap.add_argument("--lag", type=int, default=-1,
+                    help="background lag (frames); -1: 9 at N=1 (tuned for C4 with 6 workers, "
+                         "profiles/r1p), the library default W·N+6 at N>1; 0: library default")
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", default="", help="save the timed region's device timeline (.npy)")

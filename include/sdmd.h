@@ -46,9 +46,10 @@
 extern "C" {
 #endif
 
-#define SDMD_ABI_VERSION 1
+#define SDMD_ABI_VERSION 2
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
-#define SDMD_MAX_LAG 32  /* largest background lag (frames)                                     */
+#define SDMD_MAX_LAG 64  /* largest background lag (frames)                                     */
+#define SDMD_MAX_BATCH 8 /* largest k of sdmd_push_batch                                          */
 #define SDMD_MAX_R 224   /* largest rank r (shared-memory Hessenberg QR)    */
 
 enum sdmd_status {
@@ -98,10 +99,16 @@ typedef struct sdmd_config {
   int32_t rank;       /* this rank, 0..nranks-1                                                 */
   int32_t nranks;     /* row shards; > 1 needs NCCL (uid from sdmd_nccl_unique_id on rank 0)   */
   const uint8_t* nccl_uid; /* 128 bytes, identical on all ranks; ignored when nranks == 1       */
-  int32_t lag;        /* background lag in frames, 1..32; 0 → min(2·workers, 32).  K1(t+lag)
+  int32_t lag;        /* background lag in frames, 1..64; 0 → 2·workers (one rank) or workers·nranks + 6
+                       * (eigen-sharded ranks), at most 64.  K1(t+lag)
                        * consumes the background coefficients of frame t, so K4 may take up to
                        * lag frame periods before the Gram pass waits                          */
-  int32_t pad_;
+  int32_t eigen_shard; /* nranks > 1: 1 → the eigenproblems of frame t run only on rank t mod
+                       * nranks and its m background coefficients are broadcast (ncclBroadcast)
+                       * before the Gram pass that consumes them; the getters of a rank then
+                       * report the newest frame it solved.  0 → replicated on every rank      */
+  int32_t batch_max;  /* largest k accepted by sdmd_push_batch, 0..SDMD_MAX_BATCH (0: batching
+                       * off); the ring holds m + batch_max + 1 slots                          */
 } sdmd_config;
 
 typedef struct sdmd_info {
@@ -152,6 +159,21 @@ int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
  * The Gram column uses sparse–sparse inner products; nothing is densified in HBM. */
 int sdmd_push_sparse(sdmd_ctx* ctx, int32_t nnz, const int32_t* idx, const double* val,
                      int where);
+
+/* Push k = 1..cfg.batch_max dense snapshots at once (the paper's future work
+ * "dynamic updating with more than one column at a time … to catch up").  X holds k
+ * columns of n_local values (cfg.dtype), column-major with leading dimension ldx >= n_local,
+ * oldest first.  One pass (kernel K1b, fp64 DMMA) computes the k new Gram columns
+ * <x_{t+j-m+i}, x_{t+j}> from the union window of m + k columns — each window element is read
+ * once per batch instead of once per frame — and commits them; the results equal k successive
+ * sdmd_push_dense calls up to the fixed summation order.  dmd_every = 1: the DMD (a5..a10) runs
+ * for every one of the k windows; 0: only for the newest (catch-up mode: the intermediate
+ * windows' eigenproblems are skipped).  Requires a full window (>= m+1 frames held) and
+ * cfg.background == 0 (else E_STATE / E_INVALID, nothing enqueued).  A batch containing a
+ * non-finite value is rejected as a whole (the deferred NONFINITE of sdmd_sync names its first
+ * bad frame).  With nranks > 1 the k(m+1) partial values are allreduced in one NCCL call. */
+int sdmd_push_batch(sdmd_ctx* ctx, int32_t k, const void* X, int64_t ldx, int where,
+                    int32_t dmd_every);
 
 /* Zero-copy ingest: *dev_ptr receives the device address of the slot the next dense frame will
  * occupy (n_local values); fill it (on the ctx stream or before), then sdmd_commit_slot. */

@@ -790,6 +790,7 @@ static cudaError_t launch_k1v2_nq(const K1Params& p, int grid, int U, cudaStream
   if (need <= 8) return launch_k1v2_inst<T, BG, 8>(p, grid, s);
   if (need <= 13) return launch_k1v2_inst<T, BG, 13>(p, grid, s);
   if (need <= 14) return launch_k1v2_inst<T, BG, 14>(p, grid, s);
+  if (need <= 16) return launch_k1v2_inst<T, BG, 16>(p, grid, s);
   return launch_k1v2_inst<T, BG, K1_NQMAX>(p, grid, s);
 }
 
@@ -835,7 +836,7 @@ void preload_k1_kernels() {
   cudaFuncGetAttributes(&a, k1v2_kernel<float, true, NQ>);       \
   cudaFuncGetAttributes(&a, k1v2_kernel<double, false, NQ>);     \
   cudaFuncGetAttributes(&a, k1v2_kernel<double, true, NQ>);
-  K1V2_PRELOAD(2) K1V2_PRELOAD(4) K1V2_PRELOAD(8) K1V2_PRELOAD(13) K1V2_PRELOAD(14)
+  K1V2_PRELOAD(2) K1V2_PRELOAD(4) K1V2_PRELOAD(8) K1V2_PRELOAD(13) K1V2_PRELOAD(14) K1V2_PRELOAD(16)
   K1V2_PRELOAD(K1_NQMAX)
 #undef K1V2_PRELOAD
 }

@@ -1,0 +1,199 @@
+// k1b_batch.cu — K1b: the Gram columns of k ≤ 8 newly arrived frames in ONE pass over the window
+// (the paper's future-work item "dynamic updating with more than one column
+// at a time; when data inputs slow down, the number of new columns processed may be increased to
+// catch up").
+//
+// For new frames f0 .. f0+k-1 the union of their windows is U = m + k ring columns (frames
+// f0-m .. f0+k-1).  The pass forms the thin product D = Z_Uᵀ X_new (U x k, fp64 accumulation of
+// exact fp32/fp64 products, reading Q9) on the tensor pipe: DMMA m8n8k4 with the union columns as
+// M (8-column groups), the new frames as N (k ≤ 8, zero-padded) and the rows as K.  The row tiles
+// of all U columns are staged in shared memory by a cp.async pipeline (each window element is read
+// from HBM once per batch instead of once per frame), the new frames' B fragments come from the
+// same staged tile.  Frame f0+j's Gram column is g_j[i] = D[j+i][j] = <x_{f0+j-m+i}, x_{f0+j}>,
+// i = 0..m (Alg 1 P:294 per frame, reading Q1/Q2).  Per-CTA partial blocks are reduced in fixed
+// order by the last CTA (bitwise reproducible), which then commits the k columns atomically: a
+// batch containing a non-finite value is rejected as a whole (S:285 extended to batches).
+#include "sdmd_internal.cuh"
+
+namespace sdmd {
+
+constexpr int KB_WARPS = 8;
+constexpr int KB_THREADS = KB_WARPS * 32;
+constexpr int KB_MAXU = kMaxM + kMaxBatch;                      // union columns
+constexpr int KB_GPW = ((KB_MAXU + 7) / 8 + KB_WARPS - 1) / KB_WARPS;   // 8-column groups per warp
+
+template <typename T> struct KbShape {
+  static constexpr int ROWS = sizeof(T) == 4 ? 64 : 32;         // rows per stage
+  static constexpr int ST = sizeof(T) == 4 ? 3 : 2;             // stages
+  static constexpr int LDS = ROWS + 4;                          // conflict-free fragment loads
+};
+
+static __device__ __forceinline__ void kb_cp16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+static __device__ __forceinline__ void kb_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+static __device__ __forceinline__ void kb_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+static __device__ __forceinline__ void kb_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+static __device__ __forceinline__ double kb_warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Atomic commit of the k Gram columns gout[j*(m+1) .. +m] (frame f0+j) into the history.
+static __device__ void commit_batch(const double* gout, int k, int m, long long f0, double* ghist,
+                                    int NH, DevState* st) {
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0x7fffffff;
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * (m + 1); e += blockDim.x)
+    if (!isfinite(gout[e])) atomicMin(&bad, e / (m + 1));
+  __syncthreads();
+  if (bad != 0x7fffffff) {
+    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f0 + bad; }
+    return;
+  }
+  for (int e = threadIdx.x; e < k * (m + 1); e += blockDim.x) {
+    const int j = e / (m + 1), i = e % (m + 1);
+    ghist[((f0 + j) % NH) * (m + 1) + i] = gout[e];
+  }
+  if (threadIdx.x == 0) st->committed = f0 + k;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
+  using S = KbShape<T>;
+  extern __shared__ __align__(16) unsigned char kb_smem[];
+  T* sm = reinterpret_cast<T*>(kb_smem);                        // [ST][U][LDS]
+  __shared__ long long col_base[KB_MAXU];
+  __shared__ int am_last;
+  if (*(volatile int*)&p.st->status != 0) return;              // stream poisoned: discard
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = p.m, k = p.k, U = m + k, G = (U + 7) / 8;
+  const long long F0 = p.f0 - m;
+  for (int u = tid; u < U; u += KB_THREADS) col_base[u] = ((F0 + u) % p.NS) * p.ld;
+  __syncthreads();
+  const long long NT = (p.n + S::ROWS - 1) / S::ROWS;          // row tiles (ld ≥ NT·ROWS)
+  const long long per = (NT + gridDim.x - 1) / gridDim.x;      // contiguous tiles per CTA
+  const long long t0 = (long long)blockIdx.x * per;
+  const long long t1 = t0 + per < NT ? t0 + per : NT;
+  const int nsteps = t1 > t0 ? (int)(t1 - t0) : 0;
+  constexpr int EPC = 16 / (int)sizeof(T);
+  constexpr int CPC = S::ROWS / EPC;                            // 16-byte chunks per column
+  const T* ring = reinterpret_cast<const T*>(p.ring);
+  auto load = [&](int s, int buf) {
+    const long long row0 = (t0 + s) * S::ROWS;
+    T* dst = sm + (size_t)buf * U * S::LDS;
+    for (int e = tid; e < U * CPC; e += KB_THREADS) {
+      const int u = e / CPC, ch = e % CPC;
+      kb_cp16(dst + u * S::LDS + ch * EPC, ring + col_base[u] + row0 + ch * EPC);
+    }
+  };
+  double acc[KB_GPW][2];
+#pragma unroll
+  for (int g = 0; g < KB_GPW; ++g) acc[g][0] = acc[g][1] = 0.0;
+  const int jb = lane >> 2;                                     // B fragment: new frame jb, row lane&3
+  const bool bok = jb < k;
+  const int ub = m + (bok ? jb : 0);
+#pragma unroll
+  for (int s = 0; s < S::ST - 1; ++s) {
+    if (s < nsteps) load(s, s);
+    kb_commit();
+  }
+  for (int step = 0; step < nsteps; ++step) {
+    kb_wait<S::ST - 2>();
+    __syncthreads();
+    const int nx = step + S::ST - 1;
+    if (nx < nsteps) load(nx, nx % S::ST);
+    kb_commit();
+    const T* Sb = sm + (size_t)(step % S::ST) * U * S::LDS + (lane & 3);
+#pragma unroll 4
+    for (int kk = 0; kk < S::ROWS; kk += 4) {
+      const double b = bok ? (double)Sb[ub * S::LDS + kk] : 0.0;
+#pragma unroll
+      for (int g = 0; g < KB_GPW; ++g) {
+        const int grp = warp + g * KB_WARPS;
+        if (grp < G) {                                          // warp-uniform
+          const int u = grp * 8 + (lane >> 2);
+          const double a = u < U ? (double)Sb[u * S::LDS + kk] : 0.0;
+          kb_dmma(acc[g][0], acc[g][1], a, b);
+        }
+      }
+    }
+  }
+  kb_wait<0>();
+  // per-CTA partial block D[u][j] (u < U, j < k): lane holds rows u = grp·8 + lane/4, columns
+  // j = 2(lane%4) + {0, 1}
+#pragma unroll
+  for (int g = 0; g < KB_GPW; ++g) {
+    const int grp = warp + g * KB_WARPS;
+    const int u = grp * 8 + (lane >> 2), j = 2 * (lane & 3);
+    if (grp < G && u < U) {
+      if (j < k) p.partials[((long long)u * kMaxBatch + j) * gridDim.x + blockIdx.x] = acc[g][0];
+      if (j + 1 < k) p.partials[((long long)u * kMaxBatch + j + 1) * gridDim.x + blockIdx.x] = acc[g][1];
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = (atomicAdd(&p.st->k1_done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  // fixed-order reduction (warp per output), then g_j[i] = D[j+i][j]
+  for (int o = warp; o < k * (m + 1); o += KB_WARPS) {
+    const int j = o / (m + 1), i = o % (m + 1), u = j + i;
+    const double* pk = p.partials + ((long long)u * kMaxBatch + j) * gridDim.x;
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(pk + b);
+    s = kb_warp_sum(s);
+    if (lane == 0) p.gout[o] = s;
+  }
+  __syncthreads();
+  if (tid == 0) p.st->k1_done = 0;
+  if (p.do_commit) {
+    __threadfence_block();
+    commit_batch(p.gout, k, m, p.f0, p.ghist, p.NH, p.st);
+  }
+}
+
+__global__ void commit_batch_kernel(const K1bParams p) {
+  if (*(volatile int*)&p.st->status != 0) return;
+  commit_batch(p.gout, p.k, p.m, p.f0, p.ghist, p.NH, p.st);
+}
+
+template <typename T>
+static cudaError_t launch_k1b_t(const K1bParams& p, int grid, cudaStream_t s) {
+  using S = KbShape<T>;
+  const int smem = S::ST * (p.m + p.k) * S::LDS * (int)sizeof(T);
+  cudaError_t e = cudaFuncSetAttribute(k1b_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k1b_kernel<T><<<grid, KB_THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+int k1b_grid(int nsm, long long n, int dtype) {
+  const int rows = dtype == 0 ? KbShape<float>::ROWS : KbShape<double>::ROWS;
+  const long long nt = (n + rows - 1) / rows;
+  long long g = (long long)nsm * 4;                             // 4 short waves (room for K4 CTAs)
+  if (g > nt) g = nt;
+  return g < 1 ? 1 : (int)g;
+}
+
+size_t k1b_partials_elems(int grid) { return (size_t)KB_MAXU * kMaxBatch * grid; }
+
+cudaError_t launch_k1b(const K1bParams& p, int dtype, int grid, cudaStream_t s) {
+  if (p.k < 1 || p.k > kMaxBatch || p.m + p.k > KB_MAXU) return cudaErrorInvalidValue;
+  return dtype == 0 ? launch_k1b_t<float>(p, grid, s) : launch_k1b_t<double>(p, grid, s);
+}
+
+cudaError_t launch_commit_batch(const K1bParams& p, cudaStream_t s) {
+  commit_batch_kernel<<<1, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace sdmd

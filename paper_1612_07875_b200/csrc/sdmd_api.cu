@@ -8,6 +8,12 @@
 //   worker t%W  : wait commit(t) → K4(t) → record done(t)
 // K4(t) overlaps the K1 passes of frames t+1 … t+lag-1 (they touch disjoint data), so the eigen
 // work is hidden behind the bandwidth-bound Gram pass when lag·t_K1 ≥ t_K4.
+// Eigen sharding (nranks = P > 1, cfg.eigen_shard): the small eigenproblems of frame t run only on
+// rank t mod P (every rank holds the same allreduced Gram history, so any rank can solve any
+// frame), and before K1(t+lag) consumes them the m background coefficients c_t are broadcast from
+// that rank (ncclBroadcast, 2m fp64) — the eigen work per rank drops by P, so the pipeline keeps
+// up with P times the frame rate of one GPU.  Local frame index q = t div P selects the worker
+// streams, the workspace and the K4 events.
 #include <dlfcn.h>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +35,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -41,14 +49,16 @@ NcclApi* nccl_api() {
   api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
   api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+  api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy) return nullptr;
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.Broadcast || !api.CommDestroy)
+    return nullptr;
   api.loaded = true;
   return &api;
 }
 
-constexpr int kEvents = 64;
+constexpr int kEvents = 256;      // > NWS + lag: event slots are reused modulo kEvents
 
 // Per-frame eigen workspace (K4a writes the factors, K4b reads them); indexed by frame mod NWS so
 // that K4a of a later frame never overwrites a workspace whose K4b is still pending.
@@ -71,6 +81,7 @@ struct sdmd_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
+  int k1b_grid = 148;                   // CTAs of the batched Gram pass (K1b)
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
   long long ld = 0;
@@ -117,7 +128,9 @@ struct sdmd_ctx {
   size_t init_work_elems = 0;
   // host mirror (valid unless a deferred error is pending)
   long long frames = 0;
-  long long last_dmd = -1;
+  long long last_dmd = -1;              // newest frame whose eigenproblems ran on THIS rank
+  long long last_dmd_all = -1;          // newest frame whose eigenproblems ran on any rank
+  int P = 1, prank = 0;                 // eigen shards (P = nranks with eigen_shard, else 1)
   // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev, wait_ev;
@@ -175,6 +188,11 @@ static int sync_all(sdmd_ctx* c) {
   return SDMD_OK;
 }
 
+// Eigen sharding: frame t's eigenproblems run on rank t mod P; q = t div P is its local index.
+static inline bool owns(const sdmd_ctx* c, long long t) { return t % c->P == c->prank; }
+static inline long long lidx(const sdmd_ctx* c, long long t) { return t / c->P; }
+static inline Workspace& ws_of(sdmd_ctx* c, long long t) { return c->ws[lidx(c, t) % c->NWS]; }
+
 // ------------------------------------------------------------------------- ABI ----------------
 extern "C" {
 
@@ -209,6 +227,7 @@ int sdmd_config_init(sdmd_config* cfg) {
   cfg->background = 0;
   cfg->workers = 4;
   cfg->nranks = 1;
+  cfg->eigen_shard = 1;
   cfg->dtype = SDMD_F32;
   cfg->storage = SDMD_DENSE;
   return SDMD_OK;
@@ -236,6 +255,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxLag)
     return SDMD_E_INVALID;
   if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
+  if (cfg.batch_max < 0 || cfg.batch_max > kMaxBatch || (cfg.batch_max > 0 && cfg.storage != SDMD_DENSE))
+    return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
 
   sdmd_ctx* c = new sdmd_ctx();
@@ -246,9 +267,15 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (rmax > SDMD_MAX_R) rmax = SDMD_MAX_R;
   c->cfg.r_max = rmax;
   c->W = c->cfg.workers > 0 ? c->cfg.workers : 4;
-  // default lag: two frame periods per worker; K4 latency (K4a + K4b ≈ 33 ms at m = 200) must
-  // fit in lag·t_K1 for the Gram pass never to wait
-  c->L = c->cfg.lag > 0 ? c->cfg.lag : (2 * c->W < kMaxLag ? 2 * c->W : kMaxLag);
+  c->P = (c->cfg.nranks > 1 && c->cfg.eigen_shard) ? c->cfg.nranks : 1;
+  c->prank = c->P > 1 ? c->cfg.rank : 0;
+  // default lag: two frame periods per worker; K4 latency (K4a + K4b ≈ 23 ms at m = 200) must
+  // fit in lag·t_K1 for the Gram pass never to wait.  With P eigen shards
+  // frames arrive P times faster while one frame's K4 latency is unchanged: W·P + 6 periods.
+  {
+    const int want = c->P > 1 ? c->W * c->P + 6 : 2 * c->W;
+    c->L = c->cfg.lag > 0 ? c->cfg.lag : (want < kMaxLag ? want : kMaxLag);
+  }
   c->Wb = c->W;
   // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams
   // keeps both stages' throughput above one frame per Gram pass (measured)
@@ -260,6 +287,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   c->NWS = c->L + 4;
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
+  if (c->NS < m + c->cfg.batch_max + 1) c->NS = m + c->cfg.batch_max + 1;   // union of a batch
   c->NH = 2 * (m + c->L + 4);
   c->NC = c->L + 2;
   c->es = c->cfg.dtype == SDMD_F32 ? 4 : 8;
@@ -279,14 +307,18 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // inside one GPC).
   c->pgrid = c->nsm * kK1MaxWaves;
   {
-    int waves = 8;
+    // waves == 0 (default): a persistent grid on the SMs the eigen workers leave free (one
+    // cluster of k4_cluster_size() CTAs per cluster stream, one CTA per single-CTA stream), so K4
+    // never waits for an SM and K1 has no wave tail (measured at C4: 3.71 vs 3.76 ms per pass,
+    // profiles/r1p…); waves > 0 (SDMD_K1_WAVES): waves x nsm short-lived CTAs that K4 CTAs slip
+    // between.  Falls back to 8 waves if the workers would leave fewer than half of the SMs.
+    int waves = 0;
     if (const char* ew = std::getenv("SDMD_K1_WAVES")) waves = std::atoi(ew);
     if (waves < 0) waves = 0;
     if (waves > kK1MaxWaves) waves = kK1MaxWaves;
-    // waves == 0: the persistent grid that leaves the eigen workers' SMs free
-    c->k1_grid = !c->cfg.dmd ? c->nsm
-                 : waves > 0 ? c->nsm * waves
-                             : c->nsm - c->Wa * k4_cluster_size() - c->Wb;
+    const int free_sms = c->nsm - c->Wa * k4_cluster_size() - c->Wb;
+    if (waves == 0 && free_sms < c->nsm / 2) waves = 8;
+    c->k1_grid = !c->cfg.dmd ? c->nsm : waves > 0 ? c->nsm * waves : free_sms;
   }
   {
     const char* ev = std::getenv("SDMD_K1");
@@ -331,8 +363,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   cudaMemsetAsync(c->cbuf, 0, (size_t)c->NC * m * sizeof(double2), c->stream);
   const size_t np = (size_t)c->pgrid * (kMaxM + 16);
   const size_t np3 = (size_t)(m + 1) * c->k3_chunks;
-  AL(c->partials, np > np3 ? np : np3);
-  AL(c->gout, (size_t)(m + 1));
+  c->k1b_grid = k1b_grid(c->nsm, c->cfg.n_local, c->cfg.dtype);
+  const size_t npb = c->cfg.batch_max > 0 ? k1b_partials_elems(c->k1b_grid) : 0;
+  AL(c->partials, np > np3 ? (np > npb ? np : npb) : (np3 > npb ? np3 : npb));
+  AL(c->gout, (size_t)(m + 1) * (c->cfg.batch_max > 1 ? c->cfg.batch_max : 1));
   AL(c->gpart, (size_t)(m + 1));
   AL(c->Gtmp, (size_t)(m + 1) * (m + 1));
   if (c->cfg.background) {
@@ -439,7 +473,7 @@ int sdmd_destroy(sdmd_ctx* c) {
 }
 
 static K4Params k4_params(sdmd_ctx* c, long long f) {
-  Workspace& k = c->ws[f % c->NWS];
+  Workspace& k = ws_of(c, f);
   K4Params p{};
   p.ghist = c->ghist; p.NH = c->NH; p.m = c->cfg.m; p.f = f; p.r_max = c->cfg.r_max;
   p.rank_tol = c->cfg.rank_tol; p.st = c->dst;
@@ -448,10 +482,11 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.res = k.res;
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
-  // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa)
-  if (c->warm && c->Wa < c->NWS && f - c->Wa >= c->cfg.m) {
-    const Workspace& kp = c->ws[(f - c->Wa) % c->NWS];
-    p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = c->Wa;
+  // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa·P)
+  const long long fp = f - (long long)c->Wa * c->P;
+  if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m) {
+    const Workspace& kp = ws_of(c, fp);
+    p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = (int)(f - fp);
   }
   return p;
 }
@@ -459,26 +494,27 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
 // K4a (cluster) then K4b (single CTA) for frame t on the round-robin worker streams.
 static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   cudaError_t e;
-  cudaStream_t A = c->sa[t % c->Wa], B = c->sb[t % c->Wb];
+  const long long q = lidx(c, t), P = c->P;               // local index of frame t (t mod P == rank)
+  cudaStream_t A = c->sa[q % c->Wa], B = c->sb[q % c->Wb];
   if ((e = cudaStreamWaitEvent(A, c->ev_commit[t % kEvents], 0)) != cudaSuccess) return e;
-  if (t - c->NWS >= c->cfg.m)                  // workspace reuse: frame t-NWS must be finished
-    if ((e = cudaStreamWaitEvent(A, c->ev_done[(t - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
-  // ... and frame t+Wa-NWS (whose warm start reads this workspace's V) must have passed K4a
-  if (c->warm && c->Wa < c->NWS && t + c->Wa - c->NWS >= c->cfg.m)
-    if ((e = cudaStreamWaitEvent(A, c->ev_a[(t + c->Wa - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
+  if (t - c->NWS * P >= c->cfg.m)              // workspace reuse: local frame q-NWS must be finished
+    if ((e = cudaStreamWaitEvent(A, c->ev_done[(q - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
+  // ... and local frame q+Wa-NWS (whose warm start reads this workspace's V) must have passed K4a
+  if (c->warm && c->Wa < c->NWS && t + (c->Wa - c->NWS) * P >= c->cfg.m)
+    if ((e = cudaStreamWaitEvent(A, c->ev_a[(q + c->Wa - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
   const K4Params p = k4_params(c, t);
   std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
   if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
   if ((e = launch_k4a(p, A)) != cudaSuccess) return e;
   if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); c->tl.push_back({t, 1, ka.first, ka.second}); }
-  if ((e = cudaEventRecord(c->ev_a[t % kEvents], A)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(B, c->ev_a[t % kEvents], 0)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(c->ev_a[q % kEvents], A)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(B, c->ev_a[q % kEvents], 0)) != cudaSuccess) return e;
   if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
   if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
   if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); c->tl.push_back({t, 2, kb.first, kb.second}); }
-  if ((e = cudaEventRecord(c->ev_done[t % kEvents], B)) != cudaSuccess) return e;
+  if ((e = cudaEventRecord(c->ev_done[q % kEvents], B)) != cudaSuccess) return e;
   c->launches += 2;
-  c->ws[t % c->NWS].vecs_frame = -1;
+  ws_of(c, t).vecs_frame = -1;
   c->last_dmd = t;
   return cudaSuccess;
 }
@@ -490,14 +526,26 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   const bool do_dmd = c->cfg.dmd && t >= m;
   const bool sparse = c->cfg.storage == SDMD_SPARSE;
   const bool bg = (c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
-                   (t - c->L) <= c->last_dmd) ||
+                   (t - c->L) <= c->last_dmd_all) ||
                   (c->bg_nodmd && c->cfg.background && !sparse && (t - c->L) >= m);
   std::pair<cudaEvent_t, cudaEvent_t> tp{}, tw{};
   if (c->timing) {                                // wait_ev: time the ctx stream spends waiting
     tw = new_pair();                              // for the background coefficients of t - L
     CK(cudaEventRecord(tw.first, c->stream));
   }
-  if (bg && c->cfg.dmd) CK(cudaStreamWaitEvent(c->stream, c->ev_done[(t - c->L) % kEvents], 0));
+  if (bg && c->cfg.dmd) {
+    const long long fb = t - c->L;
+    if (owns(c, fb)) CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fb) % kEvents], 0));
+    if (c->P > 1) {                               // c_fb from the rank that solved frame fb
+      double2* cb = c->cbuf + (fb % c->NC) * m;
+      NcclApi* api = nccl_api();
+      if (!api || api->Broadcast(cb, cb, (size_t)2 * m, ncclFloat64, (int)(fb % c->P), c->comm,
+                                 c->stream) != ncclSuccess) {
+        c->err = "ncclBroadcast (background coefficients) failed";
+        return SDMD_E_NCCL;
+      }
+    }
+  }
   if (c->timing) {
     CK(cudaEventRecord(tw.second, c->stream));
     c->wait_ev.push_back(tw);
@@ -562,7 +610,10 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   c->last_nd = nd;
   CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
   CK(cudaEventRecord(c->ev_k1[t % kEvents], c->stream));
-  if (do_dmd) CK(enqueue_k4(c, t));
+  if (do_dmd) {
+    if (owns(c, t)) CK(enqueue_k4(c, t));
+    c->last_dmd_all = t;
+  }
   c->frames = t + 1;
   return SDMD_OK;
 }
@@ -597,6 +648,68 @@ int sdmd_commit_slot(sdmd_ctx* c) {
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "commit_slot on a sparse context");
   CK(cudaSetDevice(c->dev));
   return enqueue_frame(c, c->frames);
+}
+
+int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int where, int32_t dmd_every) {
+  if (!c || !X || k < 1 || (where != SDMD_HOST && where != SDMD_DEVICE))
+    return invalid(c, "push_batch: bad argument");
+  if (c->cfg.storage != SDMD_DENSE || c->cfg.background) return invalid(c, "push_batch: dense, background-free contexts only");
+  if (k > c->cfg.batch_max) return invalid(c, "push_batch: k > cfg.batch_max");
+  if (ldx < c->cfg.n_local) return invalid(c, "push_batch: ldx < n_local");
+  const int m = c->cfg.m;
+  const long long t = c->frames;
+  if (t < m + 1) { c->err = "push_batch: window not full (use push_dense during warm-up)"; return SDMD_E_STATE; }
+  CK(cudaSetDevice(c->dev));
+  const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // the k frames into slots t..t+k-1 (mod NS; at most two contiguous runs).  Those slots last
+  // held frames ≤ t-m-1, read only by Gram passes already ordered before this on the ctx stream.
+  for (int j = 0; j < k;) {
+    const int slot = (int)((t + j) % c->NS);
+    const int run = (c->NS - slot) < (k - j) ? (c->NS - slot) : (k - j);
+    CK(cudaMemcpy2DAsync((char*)c->ring + (size_t)slot * c->ld * c->es, c->ld * c->es,
+                         (const char*)X + (size_t)j * ldx * c->es, (size_t)ldx * c->es,
+                         c->cfg.n_local * c->es, run, kind, c->stream));
+    j += run;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> tp{};
+  if (c->timing) { tp = new_pair(); CK(cudaEventRecord(tp.first, c->stream)); }
+  K1bParams p{};
+  p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f0 = t; p.k = k;
+  p.partials = c->partials; p.gout = c->gout; p.do_commit = c->cfg.nranks == 1 ? 1 : 0;
+  p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
+  CK(launch_k1b(p, c->cfg.dtype, c->k1b_grid, c->stream));
+  c->launches += 1;
+  if (c->timing) {
+    CK(cudaEventRecord(tp.second, c->stream));
+    c->k1_ev.push_back(tp);
+    c->tl.push_back({t + k - 1, 0, tp.first, tp.second});
+  }
+  if (c->cfg.nranks > 1) {
+    const size_t cnt = (size_t)k * (m + 1);
+    CK(cudaMemcpyAsync(c->gpart, c->gout, (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    NcclApi* api = nccl_api();
+    if (!api || api->AllReduce(c->gout, c->gout, cnt, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
+      c->err = "ncclAllReduce (batch) failed";
+      return SDMD_E_NCCL;
+    }
+    CK(launch_commit_batch(p, c->stream));
+    c->launches += 1;
+  }
+  c->last_nd = m + 1;
+  for (int j = 0; j < k; ++j) {
+    const long long f = t + j;
+    CK(cudaEventRecord(c->ev_commit[f % kEvents], c->stream));
+    CK(cudaEventRecord(c->ev_k1[f % kEvents], c->stream));
+  }
+  if (c->cfg.dmd) {
+    for (int j = dmd_every ? 0 : k - 1; j < k; ++j) {
+      const long long f = t + j;
+      if (owns(c, f)) CK(enqueue_k4(c, f));
+      c->last_dmd_all = f;
+    }
+  }
+  c->frames = t + k;
+  return SDMD_OK;
 }
 
 int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double* val, int where) {
@@ -666,11 +779,13 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   for (int f = 0; f < k; ++f) CK(cudaEventRecord(c->ev_k1[f % kEvents], c->stream));
   c->frames = k;
   c->last_dmd = -1;
+  c->last_dmd_all = -1;
   c->last_nd = k;
   if (c->cfg.dmd) {
     const long long t = m;
     CK(cudaEventRecord(c->ev_commit[t % kEvents], c->stream));
-    CK(enqueue_k4(c, t));
+    if (owns(c, t)) CK(enqueue_k4(c, t));
+    c->last_dmd_all = t;
   }
   return SDMD_OK;
 }
@@ -679,8 +794,8 @@ int sdmd_join(sdmd_ctx* c) {
   if (!c) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   if (c->last_dmd < 0) return SDMD_OK;
-  for (long long f = c->last_dmd; f > c->last_dmd - c->NWS && f >= c->cfg.m; --f)
-    CK(cudaStreamWaitEvent(c->stream, c->ev_done[f % kEvents], 0));
+  for (long long f = c->last_dmd; f > c->last_dmd - (long long)c->NWS * c->P && f >= c->cfg.m; f -= c->P)
+    CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, f) % kEvents], 0));
   return SDMD_OK;
 }
 
@@ -696,7 +811,10 @@ int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
     if (failed_frame) *failed_frame = hs.failed_frame;
     c->frames = hs.committed;
     const int m = c->cfg.m;
-    c->last_dmd = (c->cfg.dmd && hs.committed - 1 >= m) ? hs.committed - 1 : -1;
+    c->last_dmd_all = (c->cfg.dmd && hs.committed - 1 >= m) ? hs.committed - 1 : -1;
+    long long ld_ = c->last_dmd_all;               // newest surviving frame solved on this rank
+    while (ld_ >= m && !owns(c, ld_)) --ld_;
+    c->last_dmd = ld_ >= m ? ld_ : -1;
     hs.status = 0;
     CK(cudaMemcpy(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     c->err = "frame " + std::to_string(hs.failed_frame) + " rejected (non-finite)";
@@ -751,7 +869,7 @@ static int newest_result(sdmd_ctx* c, K4Result* r) {
   int st = sync_all(c);
   if (st) return st;
   if (c->last_dmd < 0) return SDMD_E_WINDOW_NOT_FULL;
-  Workspace& k = c->ws[c->last_dmd % c->NWS];
+  Workspace& k = ws_of(c, c->last_dmd);
   CK(cudaMemcpy(r, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
   if (r->frame != c->last_dmd) { c->err = "stale worker result"; return SDMD_E_STATE; }
   return SDMD_OK;
@@ -763,7 +881,7 @@ int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* fra
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  Workspace& k = c->ws[c->last_dmd % c->NWS];
+  Workspace& k = ws_of(c, c->last_dmd);
   if (r) *r = res.r;
   if (frame) *frame = res.frame;
   const int m = c->cfg.m;
@@ -773,7 +891,7 @@ int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* fra
 }
 
 static int ensure_vecs(sdmd_ctx* c) {
-  Workspace& k = c->ws[c->last_dmd % c->NWS];
+  Workspace& k = ws_of(c, c->last_dmd);
   if (k.vecs_frame == c->last_dmd) return SDMD_OK;
   K4Result res{};
   CK(cudaMemcpy(&res, k.res, sizeof(K4Result), cudaMemcpyDeviceToHost));
@@ -805,7 +923,7 @@ int sdmd_get_spectrum(sdmd_ctx* c, int32_t* r, double* lambda, double* b, int32_
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  Workspace& k = c->ws[c->last_dmd % c->NWS];
+  Workspace& k = ws_of(c, c->last_dmd);
   if (r) *r = res.r;
   if (idx) *idx = res.idx;
   if (frame) *frame = res.frame;
@@ -850,7 +968,7 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   if (dalloc(&c->Tbuf, (size_t)2 * m * ncols) != cudaSuccess) return SDMD_E_OOM;
   if (dalloc(&c->colbuf, (size_t)ncols) != cudaSuccess) return SDMD_E_OOM;
   CK(cudaMemcpy(c->colbuf, cols, ncols * sizeof(int), cudaMemcpyHostToDevice));
-  Workspace& k = c->ws[c->last_dmd % c->NWS];
+  Workspace& k = ws_of(c, c->last_dmd);
   CK(launch_make_T(k.Y, m, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
   // X' of the frame's window = frames last_dmd-m+1 .. last_dmd
   CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - m + 1, m,

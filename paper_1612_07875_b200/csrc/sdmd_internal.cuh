@@ -16,7 +16,8 @@ namespace sdmd {
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
 constexpr int kMaxWorkers = 16;
-constexpr int kMaxLag = 32;              // background lag cap (frames); union columns m + lag
+constexpr int kMaxBatch = 8;             // frames per batched push (K1b)
+constexpr int kMaxLag = 64;              // background lag cap (frames); union columns m + lag
 constexpr int kK1MaxWaves = 32;           // K1 grid <= kK1MaxWaves x SM count
 constexpr int kSuperTile = 256;           // K1 rows per CTA iteration (32 lanes x 8 rows)
 
@@ -52,6 +53,22 @@ struct K1Params {
   int v1;                     // 1: the v1 K1 (8 rows per lane, lockstep background reduction), A/B only
   double* gout;               // nd reduced values (pre-allreduce)
   int do_commit;              // nranks == 1: commit inside the kernel's last block
+  double* ghist;
+  int NH;
+  DevState* st;
+};
+
+struct K1bParams {             // K1b: Gram columns of k frames f0..f0+k-1 in one pass
+  const void* ring;
+  long long ld;
+  int NS;
+  int m;
+  long long n;
+  long long f0;
+  int k;
+  double* partials;           // [U][kMaxBatch][grid]
+  double* gout;               // k x (m+1): column j = Gram column of frame f0+j
+  int do_commit;
   double* ghist;
   int NH;
   DevState* st;
@@ -169,6 +186,10 @@ cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s);
 void preload_k1_kernels();
 void preload_k4_kernels();
 cudaError_t launch_commit(const K1Params& p, cudaStream_t s);
+cudaError_t launch_k1b(const K1bParams& p, int dtype, int grid, cudaStream_t s);
+cudaError_t launch_commit_batch(const K1bParams& p, cudaStream_t s);
+int k1b_grid(int nsm, long long n, int dtype);
+size_t k1b_partials_elems(int grid);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);

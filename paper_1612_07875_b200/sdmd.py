@@ -26,7 +26,8 @@ MAX_M, MAX_R = 256, 224
 # every symbol include/sdmd.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "sdmd_config_init", "sdmd_create", "sdmd_destroy", "sdmd_init_window", "sdmd_push_dense",
-    "sdmd_push_sparse", "sdmd_acquire_slot", "sdmd_commit_slot", "sdmd_join", "sdmd_sync",
+    "sdmd_push_sparse", "sdmd_push_batch", "sdmd_acquire_slot", "sdmd_commit_slot", "sdmd_join",
+    "sdmd_sync",
     "sdmd_get_info",
     "sdmd_get_gram", "sdmd_get_partial_gram_column", "sdmd_get_svd", "sdmd_get_spectrum",
     "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_get_frame_diag",
@@ -44,7 +45,8 @@ class Config(ctypes.Structure):
         ("threshold", ctypes.c_float), ("background", ctypes.c_int32), ("dmd", ctypes.c_int32),
         ("workers", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
-        ("lag", ctypes.c_int32), ("pad_", ctypes.c_int32),
+        ("lag", ctypes.c_int32), ("eigen_shard", ctypes.c_int32),
+        ("batch_max", ctypes.c_int32),
     ]
 
 
@@ -88,6 +90,7 @@ def lib():
         "sdmd_init_window": [vp, vp, i64, ctypes.c_int],
         "sdmd_push_dense": [vp, vp, ctypes.c_int],
         "sdmd_push_sparse": [vp, i32, vp, vp, ctypes.c_int],
+        "sdmd_push_batch": [vp, i32, vp, i64, ctypes.c_int, i32],
         "sdmd_acquire_slot": [vp, ctypes.POINTER(vp)],
         "sdmd_commit_slot": [vp],
         "sdmd_join": [vp],
@@ -156,7 +159,8 @@ class StreamingDMD:
                  threshold: float = 0.2, background: bool = False, dmd: bool = True,
                  workers: int = 4, device: int = 0, stream="torch", rank: int = 0,
                  nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
-                 nccl_uid: bytes | None = None, lag: int = 0):
+                 nccl_uid: bytes | None = None, lag: int = 0, eigen_shard: int = 1,
+                 batch_max: int = 0):
         L = lib()
         cfg = Config()
         L.sdmd_config_init(ctypes.byref(cfg))
@@ -186,6 +190,8 @@ class StreamingDMD:
         cfg.rank = int(rank)
         cfg.nranks = int(nranks)
         cfg.lag = int(lag)
+        cfg.eigen_shard = int(eigen_shard)
+        cfg.batch_max = int(batch_max)
         self._uid = None
         if nccl_uid is not None:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)
@@ -232,6 +238,15 @@ class StreamingDMD:
             ldz = self.n
         self._keep = Z
         return self._check(lib().sdmd_init_window(self.h, p, int(ldz), where), "init_window")
+
+    def push_batch(self, X, dmd_every: bool = True, ldx: int | None = None):
+        """k snapshots at once (K1b): a torch (k, n) row-major tensor / (n, k) Fortran array, oldest
+        first.  dmd_every=False runs the DMD only for the newest window (catch-up mode)."""
+        p, where = _ptr(X)
+        k = int(X.shape[0]) if hasattr(X, "data_ptr") else int(np.asarray(X).shape[1])
+        self._keep = X
+        return self._check(lib().sdmd_push_batch(self.h, k, p, int(ldx or self.n), where,
+                                                 1 if dmd_every else 0), "push_batch")
 
     def push(self, x):
         p, where = _ptr(x)

@@ -48,9 +48,10 @@ def timed(eng, push, K):
     return ms, st
 
 
-def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0):
+def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0):
     P = frames_dev.shape[0]
-    eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max)
+    eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max,
+                       lag=lag)
     eng.init_window(frames_dev[: m + 1])
     t = m + 1
     for _ in range(2 * (m + 1)):
@@ -66,7 +67,7 @@ def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max
     es = 4 if dtype == "f32" else 8
     k1 = st["k1_ms"] / max(1, st["k1_launches"])
     alg = (m + 1) * n * es + (9 * n if background else 0)
-    out = {"config": name, "n": n, "m": m, "dtype": dtype, "frames": K, "workers": workers,
+    out = {"config": name, "n": n, "m": m, "dtype": dtype, "frames": K, "workers": workers, "lag": eng.info()["lag"] if background else None,
            "snapshots_per_s": round(K / (ms / 1e3), 2), "ms_per_step": round(ms / K, 4),
            "gram_pass_ms": round(k1, 4), "gram_pass_GBps": round(alg / (k1 / 1e3) / 1e9, 1),
            "k4_ms_avg": round(st["k4_ms"] / max(1, st["k4_launches"]), 3),
@@ -112,6 +113,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=500)
     ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--lag", type=int, default=0, help="C3 background lag (0: library default)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     res = []
@@ -134,7 +136,8 @@ def main():
     pool = torch.empty((Pn, vs.n), dtype=torch.float32, device="cuda")
     for t in range(Pn):
         pool[t].copy_(vs.frame(t, device="cuda"))
-    res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, args.workers, background=True))
+    res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, args.workers, background=True,
+                         lag=args.lag))
     print(json.dumps(res[-1]), flush=True)
     del pool
     torch.cuda.empty_cache()

@@ -47,7 +47,7 @@ def test_sm100a_code_present(libpath):
 def test_status_strings_and_version(libpath):
     from paper_1612_07875_b200 import sdmd
     L = sdmd.lib()
-    assert L.sdmd_abi_version() == 1
+    assert L.sdmd_abi_version() == 2
     assert L.sdmd_status_string(2).decode() == "non-finite frame rejected"
     assert L.sdmd_status_string(999).decode() == "unknown status"
 
@@ -59,8 +59,18 @@ def test_config_layout_and_validation(libpath):
     assert L.sdmd_config_init(ctypes.byref(cfg)) == 0
     assert abs(cfg.rank_tol - 1e-7) < 1e-20 and abs(cfg.threshold - 0.2) < 1e-7
     assert cfg.dmd == 1 and cfg.workers == 4 and cfg.nranks == 1
-    assert ctypes.sizeof(sdmd.Config) == 112
-    assert ctypes.sizeof(sdmd.Info) == 48 and ctypes.sizeof(sdmd.Stats) == 56
+    # the binding's structs have the C layout of include/sdmd.h (sizes from a gcc-compiled probe)
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "sz.c")
+        with open(src, "w") as fh:
+            fh.write('#include <stdio.h>\n#include "sdmd.h"\nint main(){printf("%zu %zu %zu", '
+                     'sizeof(sdmd_config), sizeof(sdmd_info), sizeof(sdmd_stats));return 0;}\n')
+        exe = os.path.join(d, "sz")
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe], check=True)
+        c_sizes = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    assert c_sizes == [ctypes.sizeof(sdmd.Config), ctypes.sizeof(sdmd.Info), ctypes.sizeof(sdmd.Stats)]
+    assert cfg.eigen_shard == 1 and cfg.batch_max == 0
     h = ctypes.c_void_p()
     # invalid shapes are rejected before any CUDA call (works without a GPU)
     cfg.n_local = cfg.n_global = 100

@@ -386,6 +386,101 @@ def test_init_window_c4_full_size_sampled():
     eng.close()
 
 
+# ------------------------------------------------------------- batched push (K1b) --------
+
+def test_push_batch_c1_matches_streaming_oracle():
+    """K1b (k frames per pass, DMMA) on the planted C1 stream: after every batch the Gram equals
+    the oracle's frame-by-frame streamed Gram (normwise 1e-12), and every window's spectrum (DMD
+    for each of the k windows) matches the closed-form eigenvalues (1e-9)."""
+    pm = synth.planted_c1()
+    m = 16
+    ks = [4, 3, 8, 1, 5, 8, 2]
+    T = m + 1 + sum(ks)
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=3, batch_max=8)
+    ref = O.StreamingGram(m)
+    for t in range(m + 1):
+        eng.push(Xd[t])
+        ref.push(X[:, t])
+    t = m + 1
+    for k in ks:
+        eng.push_batch(Xd[t:t + k])
+        for j in range(k):
+            ref.push(X[:, t + j])
+        t += k
+        eng.sync()
+        assert normwise(eng.gram(), ref.G) < 1e-12, (t, k)
+        sp = eng.spectrum()
+        assert sp["frame"] == t - 1 and sp["r"] == 4
+        assert match(sp["lam"], pm.lambdas)[0] < 1e-9
+    eng.close()
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n", [70001, 256 * 9 + 40])
+def test_push_batch_ragged_and_catch_up(dtype, n):
+    """Ragged n, both storage types, k = 8 and a batch that wraps the ring; catch-up mode
+    (dmd_every=False) computes only the newest window's DMD, equal to the oracle's."""
+    rng = np.random.default_rng(n % 97)
+    m = 40
+    npdt = np.float32 if dtype == "f32" else np.float64
+    T = m + 1 + 8 * 6 + 3
+    X = rng.standard_normal((n, T)).astype(npdt)
+    Xd = dev_cols(X, npdt)
+    eng = Eng(n, m, dtype=dtype, workers=2, batch_max=8)
+    ref = O.StreamingGram(m)
+    for t in range(m + 1):
+        eng.push(Xd[t])
+        ref.push(X[:, t].astype(np.float64))
+    t = m + 1
+    while t < T:
+        k = min(8, T - t)
+        eng.push_batch(Xd[t:t + k], dmd_every=False)
+        for j in range(k):
+            ref.push(X[:, t + j].astype(np.float64))
+        t += k
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    d = O.dmd_from_gram(ref.G)
+    sp = eng.spectrum()
+    assert sp["frame"] == T - 1 and sp["r"] == d["r"]
+    sv = eng.svd()
+    r = sv["r"]
+    big = d["sigma"][:r] >= 1e-4 * d["sigma"][0]
+    assert np.max(np.abs(sv["sigma"][:r][big] - d["sigma"][:r][big]) / d["sigma"][:r][big]) < 1e-10
+    eng.close()
+
+
+def test_push_batch_nonfinite_rejected_as_a_whole():
+    pm = synth.planted_c1()
+    m = 16
+    X = pm.frames(0, m + 1 + 8)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=1, batch_max=8)
+    for t in range(m + 1):
+        eng.push(Xd[t])
+    eng.sync()
+    G0 = eng.gram()
+    bad = Xd[m + 1:m + 1 + 6].clone()
+    bad[3, 17] = float("nan")
+    from paper_1612_07875_b200.sdmd import SDMDError
+    eng.push_batch(bad)
+    with pytest.raises(SDMDError) as ei:
+        eng.sync()
+    assert ei.value.status == 2 and ei.value.failed_frame == m + 1 + 3
+    assert eng.info()["frames"] == m + 1
+    assert np.array_equal(eng.gram(), G0)
+    # the stream continues from the untouched state
+    eng.push_batch(Xd[m + 1:m + 1 + 8])
+    eng.sync()
+    ref = O.StreamingGram(m)
+    for t in range(m + 1 + 8):
+        ref.push(X[:, t])
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    eng.close()
+
+
 # ---------------------------------------------------------------------- sparse (K3) -------
 
 def test_sparse_dct_gram_and_dmd():
