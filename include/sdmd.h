@@ -89,7 +89,7 @@ typedef struct sdmd_config {
   int32_t background; /* 1: compute the newest background column every push (fused into the Gram
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
-  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..16 (0 → 4); the cluster
+  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..20 (0 → 4); the cluster
                        * stage uses max(1, workers / 2) streams.  The context uses about
                        * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that
                        * (e.g. 32) before CUDA initialises, else streams share hardware queues

@@ -17,10 +17,12 @@
 
 namespace sdmd {
 
-constexpr int KB_WARPS = 8;
+constexpr int KB_WARPS = 16;
 constexpr int KB_THREADS = KB_WARPS * 32;
+constexpr int KB_CSETS = 8;                                     // column sets (warp & 7)
+constexpr int KB_RHALF = KB_WARPS / KB_CSETS;                   // row parts of a stage (warp >> 3)
 constexpr int KB_MAXU = kMaxM + kMaxBatch;                      // union columns
-constexpr int KB_GPW = ((KB_MAXU + 7) / 8 + KB_WARPS - 1) / KB_WARPS;   // 8-column groups per warp
+constexpr int KB_GPW = ((KB_MAXU + 7) / 8 + KB_CSETS - 1) / KB_CSETS;   // 8-column groups per warp
 
 template <typename T> struct KbShape {
   static constexpr int ROWS = sizeof(T) == 4 ? 64 : 32;         // rows per stage
@@ -100,6 +102,10 @@ __global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
   const int jb = lane >> 2;                                     // B fragment: new frame jb, row lane&3
   const bool bok = jb < k;
   const int ub = m + (bok ? jb : 0);
+  // warp = (row part wr, column set wc): groups wc, wc+8, … over rows [wr·R/2, (wr+1)·R/2) of
+  // each stage; the two row parts' partial sums are reduced with the CTA partials
+  const int wr = warp / KB_CSETS, wc = warp % KB_CSETS;
+  constexpr int RP = S::ROWS / KB_RHALF;                        // rows of a stage per warp
 #pragma unroll
   for (int s = 0; s < S::ST - 1; ++s) {
     if (s < nsteps) load(s, s);
@@ -111,31 +117,39 @@ __global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
     const int nx = step + S::ST - 1;
     if (nx < nsteps) load(nx, nx % S::ST);
     kb_commit();
-    const T* Sb = sm + (size_t)(step % S::ST) * U * S::LDS + (lane & 3);
-#pragma unroll 4
-    for (int kk = 0; kk < S::ROWS; kk += 4) {
-      const double b = bok ? (double)Sb[ub * S::LDS + kk] : 0.0;
+    const T* Sb = sm + (size_t)(step % S::ST) * U * S::LDS + wr * RP + (lane & 3);
+    // all fragments of the warp's RP rows first (independent shared-memory loads in flight),
+    // then the conversions and DMMAs
+    T bf[RP / 4], af[RP / 4][KB_GPW];
+#pragma unroll
+    for (int q = 0; q < RP / 4; ++q) {
+      bf[q] = bok ? Sb[ub * S::LDS + 4 * q] : (T)0;
 #pragma unroll
       for (int g = 0; g < KB_GPW; ++g) {
-        const int grp = warp + g * KB_WARPS;
-        if (grp < G) {                                          // warp-uniform
-          const int u = grp * 8 + (lane >> 2);
-          const double a = u < U ? (double)Sb[u * S::LDS + kk] : 0.0;
-          kb_dmma(acc[g][0], acc[g][1], a, b);
-        }
+        const int u = (wc + g * KB_CSETS) * 8 + (lane >> 2);
+        af[q][g] = u < U ? Sb[u * S::LDS + 4 * q] : (T)0;
       }
+    }
+#pragma unroll
+    for (int q = 0; q < RP / 4; ++q) {
+      const double b = (double)bf[q];
+#pragma unroll
+      for (int g = 0; g < KB_GPW; ++g)
+        if (wc + g * KB_CSETS < G) kb_dmma(acc[g][0], acc[g][1], (double)af[q][g], b);   // warp-uniform
     }
   }
   kb_wait<0>();
   // per-CTA partial block D[u][j] (u < U, j < k): lane holds rows u = grp·8 + lane/4, columns
   // j = 2(lane%4) + {0, 1}
+  const int np = gridDim.x * KB_RHALF;                          // partial sums per output
+  const int pc = blockIdx.x * KB_RHALF + wr;
 #pragma unroll
   for (int g = 0; g < KB_GPW; ++g) {
-    const int grp = warp + g * KB_WARPS;
+    const int grp = wc + g * KB_CSETS;
     const int u = grp * 8 + (lane >> 2), j = 2 * (lane & 3);
     if (grp < G && u < U) {
-      if (j < k) p.partials[((long long)u * kMaxBatch + j) * gridDim.x + blockIdx.x] = acc[g][0];
-      if (j + 1 < k) p.partials[((long long)u * kMaxBatch + j + 1) * gridDim.x + blockIdx.x] = acc[g][1];
+      if (j < k) p.partials[((long long)u * kMaxBatch + j) * np + pc] = acc[g][0];
+      if (j + 1 < k) p.partials[((long long)u * kMaxBatch + j + 1) * np + pc] = acc[g][1];
     }
   }
   __threadfence();
@@ -147,9 +161,9 @@ __global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
   // fixed-order reduction (warp per output), then g_j[i] = D[j+i][j]
   for (int o = warp; o < k * (m + 1); o += KB_WARPS) {
     const int j = o / (m + 1), i = o % (m + 1), u = j + i;
-    const double* pk = p.partials + ((long long)u * kMaxBatch + j) * gridDim.x;
+    const double* pk = p.partials + ((long long)u * kMaxBatch + j) * np;
     double s = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(pk + b);
+    for (int b = lane; b < np; b += 32) s += __ldcg(pk + b);
     s = kb_warp_sum(s);
     if (lane == 0) p.gout[o] = s;
   }
@@ -180,11 +194,12 @@ int k1b_grid(int nsm, long long n, int dtype) {
   const int rows = dtype == 0 ? KbShape<float>::ROWS : KbShape<double>::ROWS;
   const long long nt = (n + rows - 1) / rows;
   long long g = (long long)nsm * 4;                             // 4 short waves (room for K4 CTAs)
+  if (g > nt / 8) g = nt / 8 > nsm ? nt / 8 : nsm;              // small n: >= 8 tiles per CTA
   if (g > nt) g = nt;
   return g < 1 ? 1 : (int)g;
 }
 
-size_t k1b_partials_elems(int grid) { return (size_t)KB_MAXU * kMaxBatch * grid; }
+size_t k1b_partials_elems(int grid) { return (size_t)KB_MAXU * kMaxBatch * grid * KB_RHALF; }
 
 cudaError_t launch_k1b(const K1bParams& p, int dtype, int grid, cudaStream_t s) {
   if (p.k < 1 || p.k > kMaxBatch || p.m + p.k > KB_MAXU) return cudaErrorInvalidValue;

@@ -581,20 +581,42 @@ static __device__ void iv_normalise(double2* z, int r, int lane) {
   __syncwarp();
 }
 
+// The Householder vectors, the U factor and τ live in global memory (L2); every loop below loads
+// the NEXT row/vector into registers before it reduces the current one, so the L2 latency
+// overlaps the warp reductions instead of serialising with them.
 static __device__ void iv_apply_q(const double* Qv, const double* tau, int r, double2* v, int lane) {
-  for (int k = r - 3; k >= 0; --k) {                 // v <- P_k v, k = r-3 .. 0  (Q = P_0 … P_{r-3})
-    const double tk = tau[k];
-    if (tk == 0.0) continue;
-    const double* q = Qv + (long long)k * r;
-    double2 s = make_double2(0.0, 0.0);
-    for (int i = k + 1 + lane; i < r; i += 32) { const double qi = __ldcg(q + i); s.x = fma(qi, v[i].x, s.x); s.y = fma(qi, v[i].y, s.y); }
-    s = wsum2(s);
-    __syncwarp();
-    for (int i = k + 1 + lane; i < r; i += 32) {
-      const double qi = __ldcg(q + i);
-      v[i] = make_double2(v[i].x - tk * s.x * qi, v[i].y - tk * s.y * qi);
+  double qc[IV_S], qn[IV_S];                         // v <- P_k v, k = r-3 .. 0  (Q = P_0 … P_{r-3})
+  double tc = 0.0, tn = 0.0;
+  auto load = [&](int k, double (&q)[IV_S], double& t) {
+#pragma unroll
+    for (int s = 0; s < IV_S; ++s) {
+      const int i = lane + 32 * s;
+      q[s] = (k >= 0 && i > k && i < r) ? __ldcg(Qv + (long long)k * r + i) : 0.0;
     }
-    __syncwarp();
+    t = k >= 0 ? __ldcg(tau + k) : 0.0;
+  };
+  load(r - 3, qc, tc);
+  for (int k = r - 3; k >= 0; --k) {
+    load(k - 1, qn, tn);
+    if (tc != 0.0) {
+      double2 sm = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < IV_S; ++s) {
+        const int i = lane + 32 * s;
+        if (i > k && i < r) { sm.x = fma(qc[s], v[i].x, sm.x); sm.y = fma(qc[s], v[i].y, sm.y); }
+      }
+      sm = wsum2(sm);
+      __syncwarp();
+#pragma unroll
+      for (int s = 0; s < IV_S; ++s) {
+        const int i = lane + 32 * s;
+        if (i > k && i < r) v[i] = make_double2(v[i].x - tc * sm.x * qc[s], v[i].y - tc * sm.y * qc[s]);
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int s = 0; s < IV_S; ++s) qc[s] = qn[s];
+    tc = tn;
   }
 }
 
@@ -657,12 +679,32 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
       }
     }
     __syncwarp();
-    for (int i = r - 1; i >= 0; --i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = i + 1 + lane; j < r; j += 32) s = cadd(s, cmul(__ldcg(M + (long long)i * r + j), z[j]));
-      s = wsum2(s);
-      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), __ldcg(M + (long long)i * r + i));
-      __syncwarp();
+    {                                                // U z = rhs, row i of U prefetched one row ahead
+      double2 mc[IV_S], mn[IV_S], dc, dn;
+      auto load = [&](int i, double2 (&mr)[IV_S], double2& d) {
+#pragma unroll
+        for (int s = 0; s < IV_S; ++s) {
+          const int j = lane + 32 * s;
+          mr[s] = (i >= 0 && j > i && j < r) ? __ldcg(M + (long long)i * r + j) : make_double2(0.0, 0.0);
+        }
+        d = i >= 0 ? __ldcg(M + (long long)i * r + i) : make_double2(1.0, 0.0);
+      };
+      load(r - 1, mc, dc);
+      for (int i = r - 1; i >= 0; --i) {
+        load(i - 1, mn, dn);
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < IV_S; ++q) {
+          const int j = lane + 32 * q;
+          if (j > i && j < r) s = cadd(s, cmul(mc[q], z[j]));
+        }
+        s = wsum2(s);
+        if (lane == 0) z[i] = cdiv(csub(rhs[i], s), dc);
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < IV_S; ++q) mc[q] = mn[q];
+        dc = dn;
+      }
     }
     iv_normalise(z, r, lane);
     for (int i = lane; i < r; i += 32) rhs[i] = z[i];
@@ -705,12 +747,32 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
   for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
   __syncwarp();
   for (int it = 0; it < 2; ++it) {
-    for (int i = 0; i < r; ++i) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = lane; j < i; j += 32) s = cadd(s, cmul(cconj(__ldcg(M + (long long)j * r + i)), z[j]));
-      s = wsum2(s);
-      if (lane == 0) z[i] = cdiv(csub(rhs[i], s), cconj(__ldcg(M + (long long)i * r + i)));
-      __syncwarp();
+    {                                                // Uᴴ a = rhs, column i of U prefetched ahead
+      double2 mc[IV_S], mn[IV_S], dc, dn;
+      auto load = [&](int i, double2 (&mr)[IV_S], double2& d) {
+#pragma unroll
+        for (int s = 0; s < IV_S; ++s) {
+          const int j = lane + 32 * s;
+          mr[s] = (i < r && j < i) ? __ldcg(M + (long long)j * r + i) : make_double2(0.0, 0.0);
+        }
+        d = i < r ? __ldcg(M + (long long)i * r + i) : make_double2(1.0, 0.0);
+      };
+      load(0, mc, dc);
+      for (int i = 0; i < r; ++i) {
+        load(i + 1, mn, dn);
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < IV_S; ++q) {
+          const int j = lane + 32 * q;
+          if (j < i) s = cadd(s, cmul(cconj(mc[q]), z[j]));
+        }
+        s = wsum2(s);
+        if (lane == 0) z[i] = cdiv(csub(rhs[i], s), cconj(dc));
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < IV_S; ++q) mc[q] = mn[q];
+        dc = dn;
+      }
     }
     if (lane == 0) {
       for (int k = r - 2; k >= 0; --k) {

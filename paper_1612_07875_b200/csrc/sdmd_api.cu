@@ -280,6 +280,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams
   // keeps both stages' throughput above one frame per Gram pass (measured)
   c->Wa = c->W / 2 > 0 ? c->W / 2 : 1;
+  if (c->Wa + c->W + 2 > 32) c->Wa = 30 - c->W > 1 ? 30 - c->W : 1;   // 32 hardware queues
   if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
     const int v = std::atoi(ea);
     if (v >= 1 && v <= kMaxWorkers) c->Wa = v;

@@ -15,7 +15,7 @@ namespace sdmd {
 
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
-constexpr int kMaxWorkers = 16;
+constexpr int kMaxWorkers = 20;
 constexpr int kMaxBatch = 8;             // frames per batched push (K1b)
 constexpr int kMaxLag = 64;              // background lag cap (frames); union columns m + lag
 constexpr int kK1MaxWaves = 32;           // K1 grid <= kK1MaxWaves x SM count

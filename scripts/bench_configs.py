@@ -112,7 +112,7 @@ def sparse_run(K, workers, pool=160):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=500)
-    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--workers", type=int, default=20)
     ap.add_argument("--lag", type=int, default=0, help="C3 background lag (0: library default)")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
