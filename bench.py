@@ -205,7 +205,7 @@ def run_ours(args):
         free, _ = torch.cuda.mem_get_info(dev)
         frame_bytes = n_loc * 4
         if args.lag < 0:
-            args.lag = 9 if N == 1 else 0
+            args.lag = 8 if N == 1 else 0
         lag = args.lag if args.lag > 0 else min(2 * args.workers if N == 1 else args.workers * N + 6, 64)   # library default (eigen-sharded for N > 1)
         ring_bytes = (M + lag + 1) * ((n_loc + 255) // 256 * 256) * 4
         budget = free - ring_bytes - 12 * 2**30
@@ -365,8 +365,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workers", type=int, default=6)
     ap.add_argument("--lag", type=int, default=-1,
-                    help="background lag (frames); -1: 9 at N=1 (tuned for C4 with 6 workers, "
-                         "profiles/r1p), the library default W·N+6 at N>1; 0: library default")
+                    help="background lag (frames); -1: 8 at N=1 (tuned for C4 with 6 workers, "
+                         "profiles/r1u), the library default W·N+6 at N>1; 0: library default")
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", default="", help="save the timed region's device timeline (.npy)")

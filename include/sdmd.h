@@ -222,8 +222,10 @@ int sdmd_get_modes(sdmd_ctx* ctx, const int32_t* cols, int32_t ncols, double* ph
 /* Newest background column produced (frame index in *frame, -1 if none yet): lowrank = |l|,
  * sparse = x − |l| (cfg.dtype, n_local values each; either may be NULL) and mask (uint8, 1 where
  * sparse > threshold; may be NULL).  where = SDMD_HOST (synchronises) or SDMD_DEVICE (copies on
- * the ctx stream) or SDMD_HOST_ASYNC (pinned host buffers, copied in stream order without
- * synchronising; valid once the ctx stream has passed the call, e.g. after sdmd_sync). */
+ * the ctx stream) or SDMD_HOST_ASYNC (pinned host buffers; no host wait: the outputs of the
+ * newest enqueued background pass — its frame in *frame — are read back on the context's D2H
+ * stream, overlapping the next Gram pass (the outputs are double-buffered by frame parity); the
+ * host buffers are valid after sdmd_sync, or on the ctx stream after sdmd_join). */
 int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
                         int where);
 

@@ -48,6 +48,11 @@ namespace sdmd {
 #ifndef K1V2_SLACK
 #define K1V2_SLACK 1      // v2: extra reduction slots beyond the lag
 #endif
+#ifndef K1V2_SKIP
+#define K1V2_SKIP 0       // v2 A/B: 1 = warps skip (warp-uniform branch) the dummy slots past their
+                          // column count.  Measured slower (C4 pipeline pass 3.69 -> 4.78 ms at lag 9:
+                          // the predicated loads defeat the register double-buffering), so off.
+#endif
 #ifndef K1V2_DBG
 #define K1V2_DBG 0        // v2 experiments: 1 = skip the background reduction, 2 = skip its FMAs
 #endif
@@ -600,6 +605,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
   const VT* __restrict__ ringv = (const VT*)p.ring;
   const long long NT = p.ld / TILE;
   const unsigned* my_off = col_off[warp];
+  // real columns of this warp (j = warp + 16q < U); slots q >= cnt are dummies, which by default
+  // stream the L1-resident x_t tile with a zero coefficient (branch-free; K1V2_SKIP=1 skips them).
+  const int cnt = K1V2_SKIP ? (U > warp ? (U - warp + K1_WARPS - 1) / K1_WARPS : 0) : NQ;
   double acc[NQ];
 #pragma unroll
   for (int q = 0; q < NQ; ++q) acc[q] = 0.0;
@@ -659,7 +667,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
 #pragma unroll
     for (int c = 0; c < CB; ++c) {
       const int q = b * CB + c;
-      if (q < NQ) z[c] = __ldcs(base + my_off[q]);
+      if (q < NQ && q < cnt) z[c] = __ldcs(base + my_off[q]);
     }
   };
   VT za[CB], zb[CB];
@@ -685,7 +693,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
 #pragma unroll
       for (int c = 0; c < CB; ++c) {
         const int q = b * CB + c;
-        if (q < NQ) {
+        if (q < NQ && q < cnt) {
           double zd[EPV];
           to_double(cur[c], zd);
 #pragma unroll

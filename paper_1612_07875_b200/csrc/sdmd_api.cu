@@ -101,9 +101,16 @@ struct sdmd_ctx {
   double* scratch = nullptr;
   int k3_chunks = 1;
   // background outputs
-  void* bg_low = nullptr;
-  void* bg_sparse = nullptr;
-  unsigned char* bg_mask = nullptr;
+  // background outputs, double-buffered by frame parity: the D2H of frame f's outputs (on
+  // d2h_stream) overlaps the Gram pass that writes frame f+1's; the pass that writes f+2 into the
+  // same buffer waits for that D2H
+  void* bg_low[2] = {nullptr, nullptr};
+  void* bg_sparse[2] = {nullptr, nullptr};
+  unsigned char* bg_mask[2] = {nullptr, nullptr};
+  cudaStream_t d2h_stream = nullptr;
+  cudaEvent_t ev_bgw[2]{}, ev_d2h[2]{};
+  bool d2h_pending[2] = {false, false};
+  long long bg_last = -1;               // frame of the newest background pass enqueued
   // workers
   Workspace ws[kMaxWS];
   int NWS = 0, Wa = 1, Wb = 4;
@@ -182,6 +189,7 @@ static std::pair<cudaEvent_t, cudaEvent_t> new_pair() {
 
 static int sync_all(sdmd_ctx* c) {
   CK(cudaStreamSynchronize(c->copy_stream));
+  if (c->d2h_stream) CK(cudaStreamSynchronize(c->d2h_stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int w = 0; w < c->Wa; ++w) CK(cudaStreamSynchronize(c->sa[w]));
   for (int w = 0; w < c->Wb; ++w) CK(cudaStreamSynchronize(c->sb[w]));
@@ -339,6 +347,13 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->own_stream = true;
   }
   if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+  if (c->cfg.background) {
+    if (cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(SDMD_E_CUDA);
+    for (int b = 0; b < 2; ++b)
+      if (cudaEventCreateWithFlags(&c->ev_bgw[b], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_d2h[b], cudaEventDisableTiming) != cudaSuccess)
+        return bail(SDMD_E_CUDA);
+  }
 #define AL(ptr, n)                                                   \
   do {                                                               \
     if (dalloc(&(ptr), (n)) != cudaSuccess) return bail(SDMD_E_OOM); \
@@ -372,9 +387,11 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   AL(c->Gtmp, (size_t)(m + 1) * (m + 1));
   if (c->cfg.background) {
     // ld rows (padding included): K1 writes whole 16-byte vectors of its tiles without row guards
-    if (cudaMalloc(&c->bg_low, c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
-    if (cudaMalloc(&c->bg_sparse, c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
-    AL(c->bg_mask, (size_t)c->ld);
+    for (int b = 0; b < 2; ++b) {
+      if (cudaMalloc(&c->bg_low[b], c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+      if (cudaMalloc(&c->bg_sparse[b], c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
+      AL(c->bg_mask[b], (size_t)c->ld);
+    }
   }
   const int R = kMaxR;
   int prio_lo = 0, prio_hi = 0;                     // eigen workers: highest stream priority
@@ -451,9 +468,16 @@ int sdmd_destroy(sdmd_ctx* c) {
     if (c->ev_a[i]) cudaEventDestroy(c->ev_a[i]);
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->d2h_stream) { cudaStreamSynchronize(c->d2h_stream); cudaStreamDestroy(c->d2h_stream); }
+  for (int b = 0; b < 2; ++b) {
+    if (c->ev_bgw[b]) cudaEventDestroy(c->ev_bgw[b]);
+    if (c->ev_d2h[b]) cudaEventDestroy(c->ev_d2h[b]);
+    if (c->bg_low[b]) cudaFree(c->bg_low[b]);
+    if (c->bg_sparse[b]) cudaFree(c->bg_sparse[b]);
+    if (c->bg_mask[b]) cudaFree(c->bg_mask[b]);
+  }
   void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
-                  c->sp_val, c->sp_nnz, c->scratch, c->bg_low,
-                  c->bg_sparse, c->bg_mask, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
+                  c->sp_val, c->sp_nnz, c->scratch, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
                   c->Gtmp, c->init_work};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -560,13 +584,23 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f_new = t;
     p.nd = nd; p.bg = bg ? 1 : 0; p.f_bg = bg ? t - c->L : 0;
     p.cbg = bg ? c->cbuf + ((t - c->L) % c->NC) * m : nullptr;
-    p.lowrank = c->bg_low; p.sparse = c->bg_sparse; p.mask = c->bg_mask; p.thr = c->cfg.threshold;
+    const int bslot = bg ? (int)((t - c->L) & 1) : 0;
+    if (bg && c->d2h_pending[bslot]) {           // frame t-L-2's outputs still being read back
+      CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[bslot], 0));
+      c->d2h_pending[bslot] = false;
+    }
+    p.lowrank = c->bg_low[bslot]; p.sparse = c->bg_sparse[bslot]; p.mask = c->bg_mask[bslot];
+    p.thr = c->cfg.threshold;
     p.dbg = c->k1_dbg;
     p.partials = c->partials; p.pgrid = c->pgrid; p.gout = c->gout; p.do_commit = do_commit;
     p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
     p.v1 = c->k1_v1;
     CK(launch_k1(p, c->cfg.dtype, c->k1_grid, c->stream));
     c->launches += 1;
+    if (bg) {
+      CK(cudaEventRecord(c->ev_bgw[bslot], c->stream));
+      c->bg_last = t - c->L;
+    }
     if (c->timing) {
       CK(cudaEventRecord(tp.second, c->stream));
       c->k1_ev.push_back(tp);
@@ -794,6 +828,8 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
 int sdmd_join(sdmd_ctx* c) {
   if (!c) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
+  for (int b = 0; b < 2; ++b)                       // background read-backs still in flight
+    if (c->d2h_pending[b]) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[b], 0));
   if (c->last_dmd < 0) return SDMD_OK;
   for (long long f = c->last_dmd; f > c->last_dmd - (long long)c->NWS * c->P && f >= c->cfg.m; f -= c->P)
     CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, f) % kEvents], 0));
@@ -986,11 +1022,19 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   if (!c->cfg.background) return invalid(c, "background disabled in config");
   CK(cudaSetDevice(c->dev));
   const size_t n = c->cfg.n_local;
-  if (where == SDMD_HOST_ASYNC) {           // stream-ordered, no host wait; frame index unknown
-    if (frame) *frame = -1;
-    if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low, n * c->es, cudaMemcpyDeviceToHost, c->stream));
-    if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse, n * c->es, cudaMemcpyDeviceToHost, c->stream));
-    if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask, n, cudaMemcpyDeviceToHost, c->stream));
+  if (where == SDMD_HOST_ASYNC) {
+    // no host wait: the newest enqueued background pass's outputs are read back on the D2H
+    // stream (overlapping the next Gram pass, which writes the other buffer); complete after
+    // sdmd_sync, or on the ctx stream after sdmd_join
+    if (frame) *frame = c->bg_last;
+    if (c->bg_last < 0) return SDMD_E_STATE;
+    const int b = (int)(c->bg_last & 1);
+    CK(cudaStreamWaitEvent(c->d2h_stream, c->ev_bgw[b], 0));
+    if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low[b], n * c->es, cudaMemcpyDeviceToHost, c->d2h_stream));
+    if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse[b], n * c->es, cudaMemcpyDeviceToHost, c->d2h_stream));
+    if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask[b], n, cudaMemcpyDeviceToHost, c->d2h_stream));
+    CK(cudaEventRecord(c->ev_d2h[b], c->d2h_stream));
+    c->d2h_pending[b] = true;
     return SDMD_OK;
   }
   int st = sync_all(c);
@@ -1001,10 +1045,11 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   if (hs.committed == 0 || bf <= 0) bf = -1;
   if (frame) *frame = bf;
   if (bf < 0) return SDMD_E_STATE;
+  const int b = (int)(bf & 1);
   const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-  if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low, n * c->es, kind, c->stream));
-  if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse, n * c->es, kind, c->stream));
-  if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask, n, kind, c->stream));
+  if (lowrank) CK(cudaMemcpyAsync(lowrank, c->bg_low[b], n * c->es, kind, c->stream));
+  if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse[b], n * c->es, kind, c->stream));
+  if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask[b], n, kind, c->stream));
   if (where == SDMD_HOST) CK(cudaStreamSynchronize(c->stream));
   return SDMD_OK;
 }

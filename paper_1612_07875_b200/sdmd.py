@@ -273,12 +273,13 @@ class StreamingDMD:
         return self._check(lib().sdmd_join(self.h), "join")
 
     def background_async(self, mask=None, lowrank=None, sparse=None):
-        """Stream-ordered D2H of the newest background outputs into pinned host tensors."""
+        """Asynchronous D2H of the newest enqueued background outputs into pinned host tensors
+        (valid after sync(), or after join() on the ctx stream); returns their frame index."""
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
         fr = ctypes.c_int64(-1)
-        return self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
-                                                      ctypes.byref(fr), HOST_ASYNC),
-                           "get_background")
+        self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
+                                               ctypes.byref(fr), HOST_ASYNC), "get_background")
+        return int(fr.value)
 
     def sync(self) -> int:
         """Wait for all work; returns -1, or raises SDMDError(E_NONFINITE) with .failed_frame."""

@@ -212,6 +212,41 @@ def test_video_background_parity(workers):
     eng.close()
 
 
+def test_background_async_readback_every_frame():
+    """SDMD_HOST_ASYNC read-back after every push (the e2e path): the double-buffered outputs of
+    each background pass, copied on the D2H stream while the next Gram pass runs, equal the
+    oracle's background of the frame the call reports."""
+    vs = synth.video_config("C3s")
+    m, T = 30, 52
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+    ref = O.StreamingDMD(m, background=True)
+    outs, bufs = {}, {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(frames[:, t])
+        if o is not None:
+            outs[t] = o
+        low = torch.empty(vs.n, dtype=torch.float32, pin_memory=True)
+        mask = torch.empty(vs.n, dtype=torch.uint8, pin_memory=True)
+        try:
+            fb = eng.background_async(mask=mask, lowrank=low)
+        except Exception:
+            continue                                    # no background pass enqueued yet
+        bufs[fb] = (low, mask)
+    eng.sync()
+    lag = eng.info()["lag"]
+    assert sorted(bufs) == list(range(m, T - lag))
+    for fb, (low, mask) in bufs.items():
+        o = outs[fb]
+        rel = np.max(np.abs(low.numpy() - o["lowrank"])) / np.max(np.abs(o["lowrank"]))
+        assert rel < 1e-4, (fb, rel)
+        near = np.abs(o["sparse"] - 0.2) < 1e-4
+        assert np.all(mask.numpy()[~near] == o["mask"][~near]), fb
+    eng.close()
+
+
 # ------------------------------------------------------------------- robustness ----------
 
 def test_nonfinite_frame_rejected_atomically():
