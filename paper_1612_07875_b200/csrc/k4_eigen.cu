@@ -810,6 +810,53 @@ static __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// One Hestenes rotation of the column pair (cp, cq) of length m by a half-warp (lane hl holds rows
+// hl + 16e, e < EH; EH = ceil(m/16) rounded to an instantiated size, so the unrolled loops carry
+// no dead predicated rows).  Returns true if the pair was rotated.
+template <int EH>
+static __device__ __forceinline__ bool jacobi_pair(double* cp, double* cq, int m, int hl, bool act,
+                                                   double tol) {
+  double ap[EH], aq[EH];
+  double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll
+  for (int e = 0; e < EH; ++e) {
+    const int i = hl + 16 * e;
+    const bool ok = act && i < m;
+    ap[e] = ok ? cp[i] : 0.0;
+    aq[e] = ok ? cq[i] : 0.0;
+  }
+#pragma unroll
+  for (int e = 0; e < EH; ++e) {
+    al = fma(ap[e], ap[e], al);
+    be = fma(aq[e], aq[e], be);
+    ga = fma(ap[e], aq[e], ga);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {                 // reduce within the half-warp
+    al += __shfl_xor_sync(0xffffffffu, al, o);
+    be += __shfl_xor_sync(0xffffffffu, be, o);
+    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+  }
+  if (act && ga != 0.0 && ga * ga > tol * tol * (al * be)) {
+    // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
+    // one division: t = sign(β-α)·2γ / (|β-α| + sqrt((β-α)² + 4γ²))
+    const double d = be - al;
+    const double sq = sqrt(fma(d, d, 4.0 * ga * ga));
+    const double t = (d >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(d) + sq);
+    const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+#pragma unroll
+    for (int e = 0; e < EH; ++e) {
+      const int i = hl + 16 * e;
+      if (i < m) {
+        cp[i] = c * ap[e] - sn * aq[e];
+        cq[i] = sn * ap[e] + c * aq[e];
+      }
+    }
+    return true;
+  }
+  return false;
+}
+
 __global__ void __cluster_dims__(K4_CLUSTER, 1, 1) __launch_bounds__(K4_THREADS, 1)
 k4a_kernel(const K4Params p) {
   extern __shared__ __align__(16) unsigned char k4_smem[];
@@ -882,6 +929,7 @@ k4a_kernel(const K4Params p) {
   // blocks (round 0 also the pairs inside each block), so every pair of columns meets once per
   // block sweep.  Only the round boundaries need cluster barriers.
   const int bs = (m + 7) / 8;                     // block size (columns)
+  const int ehs = m <= 64 ? 4 : m <= 112 ? 7 : m <= 160 ? 10 : m <= 208 ? 13 : kMaxM / 16;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
   constexpr int EL = kMaxM / 32;
   double* sA = reinterpret_cast<double*>(k4_smem); // 2*bs columns x m, column-major
@@ -902,7 +950,6 @@ k4a_kernel(const K4Params p) {
       for (int st = 0; st < nsteps; ++st) {
         {
           // one column pair per half-warp (bs <= 32 pairs, 32 half-warps): 16 lanes x <=16 rows
-          constexpr int EH = kMaxM / 16;
           const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
           int P = 0, Q = 0;
           bool act = false;
@@ -911,48 +958,15 @@ k4a_kernel(const K4Params p) {
             else { P = hw; Q = bs + (hw + st) % bs; }
             act = gcol(P) < m && gcol(Q) < m;
           }
-          double ap[EH], aq[EH];
-          const double* cp = sA + P * m;
-          const double* cq = sA + Q * m;
-          double al = 0.0, be = 0.0, ga = 0.0;
-#pragma unroll
-          for (int e = 0; e < EH; ++e) {
-            const int i = hl + 16 * e;
-            const bool ok = act && i < m;
-            ap[e] = ok ? cp[i] : 0.0;
-            aq[e] = ok ? cq[i] : 0.0;
+          bool r_;
+          switch (ehs) {                                    // per-lane rows: ceil(m / 16)
+            case 4: r_ = jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+            case 7: r_ = jacobi_pair<7>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+            case 10: r_ = jacobi_pair<10>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+            case 13: r_ = jacobi_pair<13>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+            default: r_ = jacobi_pair<kMaxM / 16>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
           }
-#pragma unroll
-          for (int e = 0; e < EH; ++e) {
-            al = fma(ap[e], ap[e], al);
-            be = fma(aq[e], aq[e], be);
-            ga = fma(ap[e], aq[e], ga);
-          }
-#pragma unroll
-          for (int o = 8; o > 0; o >>= 1) {                 // reduce within the half-warp
-            al += __shfl_xor_sync(0xffffffffu, al, o);
-            be += __shfl_xor_sync(0xffffffffu, be, o);
-            ga += __shfl_xor_sync(0xffffffffu, ga, o);
-          }
-          if (act && ga != 0.0 && ga * ga > tol * tol * (al * be)) {
-            // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
-            // one division: t = sign(β-α)·2γ / (|β-α| + sqrt((β-α)² + 4γ²))
-            const double d = be - al;
-            const double sq = sqrt(fma(d, d, 4.0 * ga * ga));
-            const double t = (d >= 0.0 ? 2.0 * ga : -2.0 * ga) / (fabs(d) + sq);
-            const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
-            double* wp = sA + P * m;
-            double* wq = sA + Q * m;
-#pragma unroll
-            for (int e = 0; e < EH; ++e) {
-              const int i = hl + 16 * e;
-              if (i < m) {
-                wp[i] = c * ap[e] - sn * aq[e];
-                wq[i] = sn * ap[e] + c * aq[e];
-              }
-            }
-            rot = 1;
-          }
+          if (r_) rot = 1;
         }
         __syncthreads();
       }
