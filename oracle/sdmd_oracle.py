@@ -268,6 +268,41 @@ def background_newest(Xp_cols, x_newest, d: dict, b, idx: int, threshold: float 
     return low, s, s > threshold
 
 
+def background_set(lam, nb: int) -> list:
+    """Reading Q25 ("use some small subset of background DMD modes
+    rather than just the single slowest changing mode"): the nb modes with the smallest |log λ|,
+    ranked by Q5's key (|log λ|, |Im log λ|, Im λ >= 0 first, index), λ = 0 excluded, closed
+    under conjugation — if the nb-th mode's conjugate partner is the next in rank it is added
+    (at most nb + 1 modes).  nb = 1 gives [background_index(lam)]."""
+    ranked = []
+    for i, l in enumerate(np.asarray(lam, dtype=np.complex128)):
+        if l == 0:
+            continue
+        lg = np.log(l)
+        ranked.append(((abs(lg), abs(lg.imag), 0 if l.imag >= 0 else 1, i), i))
+    if not ranked:
+        raise OracleError(E_NO_VIABLE_MODE, "all eigenvalues zero")
+    order = [i for _, i in sorted(ranked)]
+    B = order[:nb]
+    lam = np.asarray(lam, dtype=np.complex128)
+    if nb < len(order) and lam[B[-1]].imag != 0 and lam[order[nb]] == np.conj(lam[B[-1]]):
+        B.append(order[nb])
+    return B
+
+
+def background_newest_multi(Xp_cols, x_newest, d: dict, b, B, threshold: float = 0.2):
+    """Streaming branch of Alg 3 with the mode set B (Q25) instead of the single
+    idx: l = Σ_{p∈B} b_p φ_p λ_p^m (e = m, Q4), s = x − |l|, mask = s > threshold (Q8)."""
+    m = d["m"]
+    phi = modes(Xp_cols, d, list(B))
+    l = np.zeros(phi.shape[0], dtype=np.complex128)
+    for q, p in enumerate(B):
+        l += b[p] * phi[:, q] * d["lam"][p] ** m
+    low = np.abs(l)
+    s = np.asarray(x_newest, dtype=np.float64) - low
+    return low, s, s > threshold
+
+
 def background_first_window(Z_cols, d: dict, b, idx: int, threshold: float = 0.2):
     """First-window branch of Alg 3: exponents 0..m over all m+1 window columns
     (Q24).  Returns (|L|, S, mask) as (n, m+1) arrays."""
@@ -291,9 +326,10 @@ class StreamingDMD:
     streaming branch of SBackSub (Alg 3) for the newest column."""
 
     def __init__(self, m: int, rank_tol: float = 1e-7, r_max: int | None = None,
-                 threshold: float = 0.2, background: bool = True):
+                 threshold: float = 0.2, background: bool = True, bg_modes: int = 1):
         self.m, self.rank_tol, self.r_max = m, rank_tol, r_max
         self.threshold, self.background = threshold, background
+        self.bg_modes = bg_modes
         self.gram = StreamingGram(m)
         self.frames = 0
         self.last = None
@@ -329,7 +365,12 @@ class StreamingDMD:
         out = dict(d, b=b, amp_status=st, idx=idx, G=G.copy(), frame=self.frames - 1)
         if self.background:
             cols = self.gram.cols
-            low, s, mask = background_newest(cols[1:], cols[-1], d, b, idx, self.threshold)
+            if self.bg_modes <= 1:
+                low, s, mask = background_newest(cols[1:], cols[-1], d, b, idx, self.threshold)
+            else:
+                B = background_set(d["lam"], self.bg_modes)
+                low, s, mask = background_newest_multi(cols[1:], cols[-1], d, b, B, self.threshold)
+                out.update(bg_set=B)
             out.update(lowrank=low, sparse=s, mask=mask)
         self.last = out
         return out

@@ -389,3 +389,44 @@ def test_oracle_init_window_equals_streamed():
     assert match_eigs(out_a["lam"], out_b["lam"]) < 1e-12
     x = pm.frames(m + 1, m + 2)[:, 0]
     assert match_eigs(a.push(x)["lam"], b.push(x)["lam"]) < 1e-12
+
+
+# ------------------------------------------- NEXT-2: multi-mode background (reading Q25) -----
+
+def test_background_set_rule_Q25():
+    """B = the nb smallest |log λ| in Q5's order, closed under conjugation; nb = 1 is idx."""
+    lam = np.array([0.5, np.exp(0.3j), np.exp(-0.3j), 1.0, 0.0, 0.9 * np.exp(1j), 0.9 * np.exp(-1j)])
+    assert O.background_set(lam, 1) == [O.background_index(lam)] == [3]
+    assert O.background_set(lam, 2) == [3, 1, 2]          # the cut pair is completed
+    assert O.background_set(lam, 3) == [3, 1, 2]
+    assert O.background_set(lam, 4) == [3, 1, 2, 0]        # |log 0.5| = 0.693 < |log 0.9e^{±i}| = 1.0055
+    assert O.background_set(lam, 5) == [3, 1, 2, 0, 5, 6]
+    assert O.background_set(lam, 7) == [3, 1, 2, 0, 5, 6]  # λ = 0 is never used
+    with pytest.raises(O.OracleError):
+        O.background_set(np.zeros(3), 2)
+
+
+def test_multi_mode_background_closed_form():
+    """Planted C1b (λ = 1 plus two conjugate pairs): with B = {1, e^{±iπ/8}} the streamed
+    background l = Σ_{p∈B} b_p φ_p λ_p^m equals the planted contributions of exactly those modes
+    to the newest frame (closed form), and nb = 1 reproduces the single-mode branch."""
+    pm = synth.planted_c1(with_unit_mode=True)
+    m, t0 = 16, 5
+    Z = pm.frames(t0, t0 + m + 1)
+    out = O.dmd_window(Z)
+    cols = [Z[:, k] for k in range(m + 1)]
+    B = O.background_set(out["lam"], 2)
+    lamB = sorted(out["lam"][B], key=lambda z: (z.imag, z.real))
+    want = sorted([1.0, np.exp(1j * np.pi / 8), np.exp(-1j * np.pi / 8)], key=lambda z: (z.imag, z.real))
+    assert np.max(np.abs(np.array(lamB) - np.array(want))) < 1e-10
+    low, s, mask = O.background_newest_multi(cols[1:], cols[-1], out, out["b"], B)
+    prods = pm.mode_products(t0 + m)
+    l_cf = sum(v for lam, v in prods.items() if abs(lam - 1.0) < 1e-12 or abs(abs(np.angle(lam)) - np.pi / 8) < 1e-12)
+    assert np.max(np.abs(low - np.abs(l_cf))) < 1e-10 * np.max(np.abs(l_cf))
+    # nb = 1: the single-mode branch (Alg 3 as written)
+    l1, s1, m1 = O.background_newest(cols[1:], cols[-1], out, out["b"], out["idx"])
+    l1m, s1m, m1m = O.background_newest_multi(cols[1:], cols[-1], out, out["b"], O.background_set(out["lam"], 1))
+    assert np.array_equal(l1, l1m) and np.array_equal(m1, m1m)
+    # all modes: the newest column itself (Q4 with every mode)
+    lall, _, _ = O.background_newest_multi(cols[1:], cols[-1], out, out["b"], list(range(out["r"])))
+    assert np.max(np.abs(lall - np.abs(Z[:, m]))) < 1e-10 * np.max(np.abs(Z[:, m]))
