@@ -50,6 +50,7 @@ extern "C" {
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
 #define SDMD_MAX_LAG 64  /* largest background lag (frames)                                     */
 #define SDMD_MAX_BATCH 8 /* largest k of sdmd_push_batch                                          */
+#define SDMD_MAX_BG_MODES 8 /* largest background mode set (plus a conjugate partner)             */
 #define SDMD_MAX_R 224   /* largest rank r (shared-memory Hessenberg QR)    */
 
 enum sdmd_status {
@@ -109,6 +110,10 @@ typedef struct sdmd_config {
                        * report the newest frame it solved.  0 → replicated on every rank      */
   int32_t batch_max;  /* largest k accepted by sdmd_push_batch, 0..SDMD_MAX_BATCH (0: batching
                        * off); the ring holds m + batch_max + 1 slots                          */
+  int32_t bg_modes;   /* background modes: 0 or 1 → the single
+                       * slowest mode of Alg 3; nb = 2..SDMD_MAX_BG_MODES → l = Σ_{p∈B} b_p φ_p λ_p^m
+                       * over B = the nb smallest |log λ| (Q5's order), closed under conjugation
+                       * (reading Q25); one inverse iteration per mode in K4     */
 } sdmd_config;
 
 typedef struct sdmd_info {

@@ -1284,6 +1284,114 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   __syncthreads();
   const int idx = sh_idx;
 
+  // ---- NEXT-2 (reading Q25): background from the mode set B = the nb smallest |log λ| in Q5's
+  // order, closed under conjugation; one warp per mode runs the inverse iteration (its own
+  // scratch and LU workspace), and c = Σ_{p∈B} b_p λ_p^m Y w_p is summed in B order
+  if (idx >= 0 && p.bg_modes > 1) {
+    __shared__ int bset[kMaxBgModes + 1];
+    __shared__ int nB;
+    __shared__ double2 bq_sh[kMaxBgModes + 1];
+    __shared__ unsigned char chosen[kMaxR];
+    for (int i = tid; i < r; i += K4_THREADS) chosen[i] = 0;
+    __syncthreads();
+    if (tid == 0) {
+      auto key_less = [&](int i, int j) {     // Q5 key of λ_i < key of λ_j
+        const double2 a = p.lam[i], b2 = p.lam[j];
+        const double ar = log(hypot(a.x, a.y)), ai = atan2(a.y, a.x);
+        const double br = log(hypot(b2.x, b2.y)), bi = atan2(b2.y, b2.x);
+        const double a1 = hypot(ar, ai), b1 = hypot(br, bi);
+        if (a1 != b1) return a1 < b1;
+        if (fabs(ai) != fabs(bi)) return fabs(ai) < fabs(bi);
+        const int a3 = a.y >= 0.0 ? 0 : 1, b3 = b2.y >= 0.0 ? 0 : 1;
+        if (a3 != b3) return a3 < b3;
+        return i < j;
+      };
+      auto next_best = [&]() {
+        int best = -1;
+        for (int i = 0; i < r; ++i) {
+          const double2 l = p.lam[i];
+          if ((l.x == 0.0 && l.y == 0.0) || chosen[i]) continue;
+          if (best < 0 || key_less(i, best)) best = i;
+        }
+        return best;
+      };
+      int cnt = 0;
+      const int nb = p.bg_modes < kMaxBgModes ? p.bg_modes : kMaxBgModes;
+      while (cnt < nb) {
+        const int bi = next_best();
+        if (bi < 0) break;
+        bset[cnt++] = bi;
+        chosen[bi] = 1;
+      }
+      if (cnt == nb) {                          // conjugate closure of the last mode
+        const double2 l = p.lam[bset[cnt - 1]];
+        const int nx = next_best();
+        if (l.y != 0.0 && nx >= 0 && p.lam[nx].x == l.x && p.lam[nx].y == -l.y) bset[cnt++] = nx;
+      }
+      nB = cnt;
+    }
+    __syncthreads();
+    const int nb_eff = nB;
+    constexpr size_t SCR = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);
+    double2* cpart = reinterpret_cast<double2*>(k4_smem + (size_t)nb_eff * SCR);   // [nB][m]
+    if (warp < nb_eff) {
+      unsigned char* base = k4_smem + (size_t)warp * SCR;
+      double2* zq = reinterpret_cast<double2*>(base);
+      double2* rq = zq + kMaxR;
+      double2* lq = rq + kMaxR;
+      int* sq = reinterpret_cast<int*>(lq + kMaxR);
+      double2* wq = p.w + (size_t)warp * kMaxR;
+      double2* yq = p.y + (size_t)warp * kMaxR;
+      const double2 lam = p.lam[bset[warp]];
+      inverse_iteration(H, p.Qv, p.tau, r, lam, p.M + (size_t)warp * kMaxR * kMaxR, zq, rq, lq, sq, wq, yq, lane);
+      double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
+      for (int i = lane; i < r; i += 32) {
+        const double2 yc = cconj(yq[i]);
+        ya = cadd(ya, make_double2(yc.x * p.alpha1[i], yc.y * p.alpha1[i]));
+        yw = cadd(yw, cmul(yc, wq[i]));
+      }
+      ya = wsum2(ya);
+      yw = wsum2(yw);
+      const double2 den = cmul(lam, yw);
+      const double2 b = cabs2(den) > 1e-300 ? cdiv(ya, den) : make_double2(0.0, 0.0);
+      double2 pw = make_double2(1.0, 0.0), bs_ = lam;        // λ^m by binary powering
+      for (int e = m; e > 0; e >>= 1) {
+        if (e & 1) pw = cmul(pw, bs_);
+        bs_ = cmul(bs_, bs_);
+      }
+      const double2 coef = cmul(b, pw);
+      for (int i = lane; i < m; i += 32) {
+        double2 s = make_double2(0.0, 0.0);
+        for (int j = 0; j < r; ++j) {
+          const double yv = p.Y[(long long)j * m + i];
+          s = cadd(s, make_double2(yv * wq[j].x, yv * wq[j].y));
+        }
+        cpart[(size_t)warp * m + i] = cmul(coef, s);
+      }
+      if (lane == 0) bq_sh[warp] = (cabs2(den) > 1e-300) ? b : make_double2(NAN, 0.0);
+    }
+    __syncthreads();
+    for (int i = tid; i < m; i += K4_THREADS) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int q = 0; q < nb_eff; ++q) s = cadd(s, cpart[(size_t)q * m + i]);
+      p.cout[i] = s;
+    }
+    if (tid == 0) {
+      int st = sh_status;
+      for (int q = 0; q < nb_eff; ++q)
+        if (isnan(bq_sh[q].x) && st == 0) st = 6;
+      const double2 lam = p.lam[idx];
+      const double2 b0 = isnan(bq_sh[0].x) ? make_double2(0.0, 0.0) : bq_sh[0];
+      ph[7] = clock64();
+      res->phase[5] = ph[6] - ph[5];
+      res->phase[6] = ph[7] - ph[6];
+      res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
+      res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
+      res->b_idx[0] = b0.x; res->b_idx[1] = b0.y; res->sigma1 = sigma1;
+    }
+    return;
+  }
+
   // ---- a8/a9: eigenvectors of the background mode, b_idx, and c (warp 0); scratch aliases the
   // (now free) packed Hessenberg area
   double2* z = reinterpret_cast<double2*>(k4_smem);
@@ -1337,14 +1445,17 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   }
 }
 
-size_t k4_smem_bytes(int r_max, int m) {
+size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const long long hs = hs_elems(r_max);
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);
   const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
   const size_t d = ((size_t)((r_max + 3) / 4) * r_max + 2 * kMaxR) * sizeof(double);  // Hessenberg rows
+  // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
+  const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b + (size_t)m * sizeof(double2)) : 0;
   size_t s = a > b ? a : b;
   s = s > c ? s : c;
+  s = s > e ? s : e;
   return s > d ? s : d;
 }
 
@@ -1355,7 +1466,7 @@ void preload_k4_kernels() {
 }
 
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
-  const size_t smem = k4_smem_bytes(p.r_max, p.m);
+  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
   cudaError_t e = cudaFuncSetAttribute(k4a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k4a_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
@@ -1363,7 +1474,7 @@ cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
 }
 
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s) {
-  const size_t smem = k4_smem_bytes(p.r_max, p.m);
+  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
   cudaError_t e = cudaFuncSetAttribute(k4b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k4b_kernel<<<1, K4_THREADS, smem, s>>>(p);

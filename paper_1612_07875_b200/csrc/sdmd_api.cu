@@ -265,6 +265,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
   if (cfg.batch_max < 0 || cfg.batch_max > kMaxBatch || (cfg.batch_max > 0 && cfg.storage != SDMD_DENSE))
     return SDMD_E_INVALID;
+  if (cfg.bg_modes < 0 || cfg.bg_modes > kMaxBgModes) return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
 
   sdmd_ctx* c = new sdmd_ctx();
@@ -412,10 +413,11 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(k.Qv, (size_t)R * R);
     AL(k.tau, (size_t)R);
     AL(k.alpha1, (size_t)R);
-    AL(k.M, (size_t)R * R);
+    const size_t nbs = c->cfg.bg_modes > 1 ? (size_t)c->cfg.bg_modes + 1 : 1;   // per-mode slots
+    AL(k.M, nbs * R * R);
     AL(k.lam, (size_t)R);
-    AL(k.w, (size_t)R);
-    AL(k.y, (size_t)R);
+    AL(k.w, nbs * R);
+    AL(k.y, nbs * R);
     AL(k.res, 1);
     AL(k.flags, 64);
     AL(k.mu, (size_t)kMaxM);
@@ -507,6 +509,7 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.res = k.res;
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
+  p.bg_modes = c->cfg.bg_modes;
   // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa·P)
   const long long fp = f - (long long)c->Wa * c->P;
   if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m) {

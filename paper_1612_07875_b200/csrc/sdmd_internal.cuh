@@ -16,7 +16,8 @@ namespace sdmd {
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
 constexpr int kMaxWorkers = 20;
-constexpr int kMaxBatch = 8;             // frames per batched push (K1b)
+constexpr int kMaxBatch = 8;
+constexpr int kMaxBgModes = 8;           // background modes (NEXT-2); +1 for the conjugate partner             // frames per batched push (K1b)
 constexpr int kMaxLag = 64;              // background lag cap (frames); union columns m + lag
 constexpr int kK1MaxWaves = 32;           // K1 grid <= kK1MaxWaves x SM count
 constexpr int kSuperTile = 256;           // K1 rows per CTA iteration (32 lanes x 8 rows)
@@ -118,6 +119,8 @@ struct K4Params {
   double2* cout;              // m background coefficients (cbuf slot), zero on failure
   int* flags;                 // per-sweep "rotated" flags (cluster-wide OR)
   double* mu;                 // m column norms
+  int bg_modes;               // nb > 1: background from the mode set B (reading Q25), M/w/y hold
+                              // nb+1 slots (strides kMaxR*kMaxR and kMaxR)
   double* wv;                 // kMaxR Householder scratch
   double* uv;                 // kMaxR Householder scratch
   // Jacobi warm start: eigenvectors of frame f - warm_k (same cluster stream, so complete), used
@@ -193,7 +196,7 @@ size_t k1b_partials_elems(int grid);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
-size_t k4_smem_bytes(int r_max, int m);
+size_t k4_smem_bytes(int r_max, int m, int bg_modes);
 int k4_cluster_size();
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
 cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,

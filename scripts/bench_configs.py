@@ -48,10 +48,10 @@ def timed(eng, push, K):
     return ms, st
 
 
-def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0):
+def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0, bg_modes=0):
     P = frames_dev.shape[0]
     eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max,
-                       lag=lag)
+                       lag=lag, bg_modes=bg_modes)
     eng.init_window(frames_dev[: m + 1])
     t = m + 1
     for _ in range(2 * (m + 1)):
@@ -138,6 +138,10 @@ def main():
         pool[t].copy_(vs.frame(t, device="cuda"))
     res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, args.workers, background=True,
                          lag=args.lag))
+    print(json.dumps(res[-1]), flush=True)
+    # NEXT-2: background from the 4 slowest modes (+ conjugate partner) instead of one
+    res.append(dense_run("C3 (4-mode background)", pool, vs.n, 100, "f32", args.frames, args.workers,
+                         background=True, lag=args.lag, bg_modes=4))
     print(json.dumps(res[-1]), flush=True)
     del pool
     torch.cuda.empty_cache()

@@ -247,6 +247,64 @@ def test_background_async_readback_every_frame():
     eng.close()
 
 
+@pytest.mark.parametrize("nb", [2, 3])
+def test_multi_mode_background_planted_closed_form(nb):
+    """NEXT-2 (reading Q25) on planted C1b (λ = 1 plus two conjugate pairs, fp64): the
+    background column built from the mode set B (nb = 2 → {1, e^{±iπ/8}} after conjugate
+    closure, nb = 3 → the same) equals the planted contributions of those modes to the frame
+    (closed form) and the oracle's multi-mode background."""
+    pm = synth.planted_c1(with_unit_mode=True)
+    m, T = 16, 40
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", background=True, workers=2, bg_modes=nb)
+    ref = O.StreamingDMD(m, background=True, bg_modes=nb)
+    outs = {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(X[:, t])
+        if o is not None:
+            outs[t] = o
+    eng.sync()
+    low, sp, mask, fb = eng.background()
+    o = outs[fb]
+    assert len(o["bg_set"]) == 3
+    prods = pm.mode_products(fb)
+    l_cf = sum(v for lam, v in prods.items()
+               if abs(lam - 1.0) < 1e-12 or abs(abs(np.angle(lam)) - np.pi / 8) < 1e-12)
+    scale = np.max(np.abs(l_cf))
+    assert np.max(np.abs(low - np.abs(l_cf))) < 1e-9 * scale
+    assert np.max(np.abs(low - o["lowrank"])) < 1e-9 * scale
+    eng.close()
+
+
+def test_multi_mode_background_video():
+    """NEXT-2 on the C3-shaped video (fp32, r ≈ m): background from the 4 slowest modes (plus a
+    conjugate partner) against the oracle, same tolerances as the single-mode video test."""
+    vs = synth.video_config("C3s")
+    m, T = 30, 48
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2, bg_modes=4)
+    ref = O.StreamingDMD(m, background=True, bg_modes=4)
+    outs = {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(frames[:, t])
+        if o is not None:
+            outs[t] = o
+    eng.sync()
+    low, sp, mask, fb = eng.background()
+    o = outs[fb]
+    x = frames[:, fb].astype(np.float64)
+    rel = np.max(np.abs(low - o["lowrank"])) / np.max(np.abs(o["lowrank"]))
+    assert rel < 1e-4, rel
+    near = np.abs(o["sparse"] - 0.2) < 1e-4
+    assert np.all(mask[~near] == o["mask"][~near])
+    assert np.max(np.abs(low.astype(np.float64) + sp - x)) < 1e-6
+    eng.close()
+
+
 # ------------------------------------------------------------------- robustness ----------
 
 def test_nonfinite_frame_rejected_atomically():
