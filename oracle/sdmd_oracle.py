@@ -326,10 +326,15 @@ class StreamingDMD:
     streaming branch of SBackSub (Alg 3) for the newest column."""
 
     def __init__(self, m: int, rank_tol: float = 1e-7, r_max: int | None = None,
-                 threshold: float = 0.2, background: bool = True, bg_modes: int = 1):
+                 threshold: float = 0.2, background: bool = True, bg_modes: int = 1,
+                 buildup: bool = False):
         self.m, self.rank_tol, self.r_max = m, rank_tol, r_max
         self.threshold, self.background = threshold, background
         self.bg_modes = bg_modes
+        # NEXT-4 (P:496-498 "start the algorithm with only 2 columns. Until the matrix is filled,
+        # the new columns would be appended without erasing the oldest"): with buildup the DMD
+        # also runs on the growing window of 2..m columns (no background before it is full)
+        self.buildup = buildup
         self.gram = StreamingGram(m)
         self.frames = 0
         self.last = None
@@ -353,17 +358,19 @@ class StreamingDMD:
         self.gram.push(x)
         self.frames += 1
         if not self.gram.full:
+            if self.buildup and len(self.gram.cols) >= 2:
+                return self._dmd(background=False)
             self.last = None
             return None
         return self._dmd()
 
-    def _dmd(self) -> dict:
+    def _dmd(self, background: bool = True) -> dict:
         G = self.gram.G
         d = dmd_from_gram(G, self.rank_tol, self.r_max)
         b, st = amplitudes(d)
         idx = background_index(d["lam"])
         out = dict(d, b=b, amp_status=st, idx=idx, G=G.copy(), frame=self.frames - 1)
-        if self.background:
+        if self.background and background:
             cols = self.gram.cols
             if self.bg_modes <= 1:
                 low, s, mask = background_newest(cols[1:], cols[-1], d, b, idx, self.threshold)

@@ -430,3 +430,27 @@ def test_multi_mode_background_closed_form():
     # all modes: the newest column itself (Q4 with every mode)
     lall, _, _ = O.background_newest_multi(cols[1:], cols[-1], out, out["b"], list(range(out["r"])))
     assert np.max(np.abs(lall - np.abs(Z[:, m]))) < 1e-10 * np.max(np.abs(Z[:, m]))
+
+
+# ------------------------------------------------ NEXT-4: DMD during build-up -----
+
+def test_buildup_dmd_closed_form_and_operator():
+    """With buildup the oracle decomposes the growing window from 2 columns on.  Planted C1
+    (rank 4): from 4 X-columns (frame 4) the spectrum is the planted one (closed form); before
+    that eig(Ã) equals the nonzero eigenvalues of the full operator X' pinv(X)."""
+    pm = synth.planted_c1()
+    m = 16
+    X = pm.frames(0, m + 1)
+    ref = O.StreamingDMD(m, background=False, buildup=True)
+    assert ref.push(X[:, 0]) is None
+    for t in range(1, m + 1):
+        out = ref.push(X[:, t])
+        assert out is not None and out["frame"] == t and out["m"] == t
+        if t >= 4:
+            assert out["r"] == 4 and match_eigs(out["lam"], pm.lambdas) < 1e-10
+        else:
+            Xa, Xb = X[:, :t], X[:, 1:t + 1]
+            # nonzero eig(X' pinv(X)) = eig(pinv(X) X') (AB and BA share nonzero eigenvalues)
+            ev = np.linalg.eigvals(np.linalg.pinv(Xa) @ Xb)
+            ev = ev[np.argsort(-np.abs(ev))][:out["r"]]
+            assert match_eigs(out["lam"], ev) < 1e-8
