@@ -114,6 +114,11 @@ typedef struct sdmd_config {
                        * slowest mode of Alg 3; nb = 2..SDMD_MAX_BG_MODES → l = Σ_{p∈B} b_p φ_p λ_p^m
                        * over B = the nb smallest |log λ| (Q5's order), closed under conjugation
                        * (reading Q25); one inverse iteration per mode in K4     */
+  int32_t buildup;    /* 1: DMD during the build-up ("start the
+                       * algorithm with only 2 columns"): every push from the 2nd frame on runs
+                       * the DMD of the growing window (X = the t columns x_0..x_{t-1}); the
+                       * getters then report windows narrower than m (sigma zero-padded, V
+                       * with leading dimension m).  No background before the window is full */
 } sdmd_config;
 
 typedef struct sdmd_info {

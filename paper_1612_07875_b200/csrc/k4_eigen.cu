@@ -55,11 +55,13 @@ static __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 static __device__ __forceinline__ double2 wsum2(double2 v) { return make_double2(wsum(v.x), wsum(v.y)); }
 
 // G_f(i, j), 0 <= i, j <= m, for the window ending at frame f (see sdmd_internal.cuh)
-static __device__ __forceinline__ double gram_at(const double* gh, int NH, int m, long long f, int i,
-                                                  int j) {
+static __device__ __forceinline__ double gram_at(const double* gh, int NH, int mh, int w, long long f,
+                                                int i, int j) {
+  // window of width w ending at frame f (frames f-w .. f); history rows of stride mh+1
+  // (row of frame g: <x_{g-mh+k}, x_g> at k)
   const int a = i < j ? i : j, b = i < j ? j : i;
-  const long long fb = f - m + b;
-  return gh[(fb % NH) * (m + 1) + (a - b + m)];
+  const long long fb = f - w + b;
+  return gh[(fb % NH) * (mh + 1) + (a - b + mh)];
 }
 
 static __device__ __forceinline__ int rr_player(int pos, int step, int mp) {
@@ -881,8 +883,8 @@ k4a_kernel(const K4Params p) {
   // ---- a5: S = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1] from the Gram history
   for (int idx = gtid; idx < m * m; idx += K4_GT) {
     const int i = idx % m, j = idx / m;
-    p.A[idx] = gram_at(p.ghist, p.NH, m, f, i, j);
-    p.Gxy[idx] = gram_at(p.ghist, p.NH, m, f, i, j + 1);
+    p.A[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j);
+    p.Gxy[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j + 1);
   }
   if (gtid < JACOBI_MAX_SWEEPS) p.flags[gtid] = 0;
   cl_sync();

@@ -200,6 +200,10 @@ static int sync_all(sdmd_ctx* c) {
 static inline bool owns(const sdmd_ctx* c, long long t) { return t % c->P == c->prank; }
 static inline long long lidx(const sdmd_ctx* c, long long t) { return t / c->P; }
 static inline Workspace& ws_of(sdmd_ctx* c, long long t) { return c->ws[lidx(c, t) % c->NWS]; }
+// first frame with a DMD: m (full window), or 1 with cfg.buildup (NEXT-4: from 2 columns)
+static inline long long first_dmd(const sdmd_ctx* c) { return c->cfg.buildup ? 1 : c->cfg.m; }
+// window width of frame f's DMD (X has w columns)
+static inline int win_of(const sdmd_ctx* c, long long f) { return f < c->cfg.m ? (int)f : c->cfg.m; }
 
 // ------------------------------------------------------------------------- ABI ----------------
 extern "C" {
@@ -502,7 +506,8 @@ int sdmd_destroy(sdmd_ctx* c) {
 static K4Params k4_params(sdmd_ctx* c, long long f) {
   Workspace& k = ws_of(c, f);
   K4Params p{};
-  p.ghist = c->ghist; p.NH = c->NH; p.m = c->cfg.m; p.f = f; p.r_max = c->cfg.r_max;
+  p.ghist = c->ghist; p.NH = c->NH; p.m = win_of(c, f); p.mh = c->cfg.m; p.f = f;
+  p.r_max = c->cfg.r_max < p.m ? c->cfg.r_max : p.m;
   p.rank_tol = c->cfg.rank_tol; p.st = c->dst;
   p.A = k.A; p.Gxy = k.Gxy; p.V = k.V; p.sigma = k.sigma; p.Y = k.Y; p.B = k.B; p.H = k.H;
   p.Qv = k.Qv; p.tau = k.tau; p.M = k.M; p.lam = k.lam; p.w = k.w; p.y = k.y; p.alpha1 = k.alpha1;
@@ -525,7 +530,7 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   const long long q = lidx(c, t), P = c->P;               // local index of frame t (t mod P == rank)
   cudaStream_t A = c->sa[q % c->Wa], B = c->sb[q % c->Wb];
   if ((e = cudaStreamWaitEvent(A, c->ev_commit[t % kEvents], 0)) != cudaSuccess) return e;
-  if (t - c->NWS * P >= c->cfg.m)              // workspace reuse: local frame q-NWS must be finished
+  if (t - c->NWS * P >= first_dmd(c))          // workspace reuse: local frame q-NWS must be finished
     if ((e = cudaStreamWaitEvent(A, c->ev_done[(q - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
   // ... and local frame q+Wa-NWS (whose warm start reads this workspace's V) must have passed K4a
   if (c->warm && c->Wa < c->NWS && t + (c->Wa - c->NWS) * P >= c->cfg.m)
@@ -551,7 +556,7 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
 static int enqueue_frame(sdmd_ctx* c, long long t) {
   const int m = c->cfg.m;
   const int nd = (int)(t + 1 < m + 1 ? t + 1 : m + 1);
-  const bool do_dmd = c->cfg.dmd && t >= m;
+  const bool do_dmd = c->cfg.dmd && t >= first_dmd(c);
   const bool sparse = c->cfg.storage == SDMD_SPARSE;
   const bool bg = (c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
                    (t - c->L) <= c->last_dmd_all) ||
@@ -834,7 +839,7 @@ int sdmd_join(sdmd_ctx* c) {
   for (int b = 0; b < 2; ++b)                       // background read-backs still in flight
     if (c->d2h_pending[b]) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[b], 0));
   if (c->last_dmd < 0) return SDMD_OK;
-  for (long long f = c->last_dmd; f > c->last_dmd - (long long)c->NWS * c->P && f >= c->cfg.m; f -= c->P)
+  for (long long f = c->last_dmd; f > c->last_dmd - (long long)c->NWS * c->P && f >= first_dmd(c); f -= c->P)
     CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, f) % kEvents], 0));
   return SDMD_OK;
 }
@@ -851,10 +856,12 @@ int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
     if (failed_frame) *failed_frame = hs.failed_frame;
     c->frames = hs.committed;
     const int m = c->cfg.m;
-    c->last_dmd_all = (c->cfg.dmd && hs.committed - 1 >= m) ? hs.committed - 1 : -1;
+    const long long f0 = first_dmd(c);
+    c->last_dmd_all = (c->cfg.dmd && hs.committed - 1 >= f0) ? hs.committed - 1 : -1;
     long long ld_ = c->last_dmd_all;               // newest surviving frame solved on this rank
-    while (ld_ >= m && !owns(c, ld_)) --ld_;
-    c->last_dmd = ld_ >= m ? ld_ : -1;
+    while (ld_ >= f0 && !owns(c, ld_)) --ld_;
+    c->last_dmd = ld_ >= f0 ? ld_ : -1;
+    (void)m;
     hs.status = 0;
     CK(cudaMemcpy(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     c->err = "frame " + std::to_string(hs.failed_frame) + " rejected (non-finite)";
@@ -924,9 +931,16 @@ int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* fra
   Workspace& k = ws_of(c, c->last_dmd);
   if (r) *r = res.r;
   if (frame) *frame = res.frame;
-  const int m = c->cfg.m;
-  if (sigma) CK(cudaMemcpy(sigma, k.sigma, m * sizeof(double), cudaMemcpyDeviceToHost));
-  if (V && res.r > 0) CK(cudaMemcpy(V, k.V, (size_t)m * res.r * sizeof(double), cudaMemcpyDeviceToHost));
+  const int m = c->cfg.m, w = win_of(c, c->last_dmd);   // w < m: a build-up window (NEXT-4)
+  if (sigma) {
+    for (int i = w; i < m; ++i) sigma[i] = 0.0;
+    CK(cudaMemcpy(sigma, k.sigma, w * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  if (V && res.r > 0) {
+    if (w < m) std::memset(V, 0, (size_t)m * res.r * sizeof(double));
+    CK(cudaMemcpy2D(V, m * sizeof(double), k.V, w * sizeof(double), w * sizeof(double), res.r,
+                    cudaMemcpyDeviceToHost));
+  }
   return res.status == 6 ? SDMD_OK : (res.status > 0 ? res.status : SDMD_OK);
 }
 
@@ -1009,9 +1023,10 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   if (dalloc(&c->colbuf, (size_t)ncols) != cudaSuccess) return SDMD_E_OOM;
   CK(cudaMemcpy(c->colbuf, cols, ncols * sizeof(int), cudaMemcpyHostToDevice));
   Workspace& k = ws_of(c, c->last_dmd);
-  CK(launch_make_T(k.Y, m, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
-  // X' of the frame's window = frames last_dmd-m+1 .. last_dmd
-  CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - m + 1, m,
+  const int w = win_of(c, c->last_dmd);
+  CK(launch_make_T(k.Y, w, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
+  // X' of the frame's window = frames last_dmd-w+1 .. last_dmd
+  CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - w + 1, w,
                   c->Tbuf, ncols, phi_dev, ld, c->stream));
   c->launches += 1 + (ncols + 31) / 32;
   CK(cudaStreamSynchronize(c->stream));

@@ -95,7 +95,8 @@ struct K4Result {
 struct K4Params {
   const double* ghist;
   int NH;
-  int m;
+  int m;                      // window width w of this frame's DMD (= cfg.m, or t during build-up)
+  int mh;                     // history row stride - 1 (= cfg.m)
   long long f;                // frame whose window is decomposed
   int r_max;
   double rank_tol;

@@ -46,7 +46,7 @@ class Config(ctypes.Structure):
         ("workers", ctypes.c_int32), ("device", ctypes.c_int32), ("stream", ctypes.c_void_p),
         ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
         ("lag", ctypes.c_int32), ("eigen_shard", ctypes.c_int32),
-        ("batch_max", ctypes.c_int32), ("bg_modes", ctypes.c_int32),
+        ("batch_max", ctypes.c_int32), ("bg_modes", ctypes.c_int32), ("buildup", ctypes.c_int32),
     ]
 
 
@@ -160,7 +160,7 @@ class StreamingDMD:
                  workers: int = 4, device: int = 0, stream="torch", rank: int = 0,
                  nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
                  nccl_uid: bytes | None = None, lag: int = 0, eigen_shard: int = 1,
-                 batch_max: int = 0, bg_modes: int = 0):
+                 batch_max: int = 0, bg_modes: int = 0, buildup: bool = False):
         L = lib()
         cfg = Config()
         L.sdmd_config_init(ctypes.byref(cfg))
@@ -193,6 +193,7 @@ class StreamingDMD:
         cfg.eigen_shard = int(eigen_shard)
         cfg.batch_max = int(batch_max)
         cfg.bg_modes = int(bg_modes)
+        cfg.buildup = 1 if buildup else 0
         self._uid = None
         if nccl_uid is not None:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)

@@ -305,6 +305,43 @@ def test_multi_mode_background_video():
     eng.close()
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_buildup_dmd_every_window(dtype):
+    """NEXT-4: with buildup the DMD runs from the 2nd frame on the growing window.
+    Planted C1: from 4 X-columns the spectrum is the planted one (closed form, 1e-9); every
+    build-up window's σ and λ match the oracle's; after the window fills, the stream continues
+    as without buildup."""
+    pm = synth.planted_c1()
+    m, T = 16, 24
+    npdt = np.float64 if dtype == "f64" else np.float32
+    X = pm.frames(0, T).astype(npdt)
+    Xd = dev_cols(X, npdt)
+    eng = Eng(pm.n, m, dtype=dtype, workers=2, buildup=True)
+    ref = O.StreamingDMD(m, background=False, buildup=True)
+    for t in range(T):
+        eng.push(Xd[t])
+        out = ref.push(X[:, t].astype(np.float64))
+        if t == 0:
+            assert out is None
+            continue
+        eng.sync()
+        sp = eng.spectrum()
+        assert sp["frame"] == t and sp["r"] == out["r"], (t, sp["r"], out["r"])
+        tol = 1e-9 * max(1.0, np.abs(out["lam"]).max())
+        if t >= 4 and dtype == "f64":
+            assert match(sp["lam"], pm.lambdas)[0] < 1e-9, t
+        assert match(sp["lam"], out["lam"])[0] < tol, t
+        sv = eng.svd()
+        w = min(t, m)
+        r = sv["r"]
+        assert np.all(sv["sigma"][w:] == 0.0)
+        assert np.max(np.abs(sv["sigma"][:r] - out["sigma"][:r]) / out["sigma"][:r]) < 1e-10, t
+        P = sv["V"][:w] @ sv["V"][:w].T
+        Pr = out["V"][:, :r] @ out["V"][:, :r].T
+        assert np.max(np.abs(P - Pr)) < 1e-9, t
+    eng.close()
+
+
 # ------------------------------------------------------------------- robustness ----------
 
 def test_nonfinite_frame_rejected_atomically():
