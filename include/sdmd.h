@@ -226,7 +226,9 @@ int sdmd_get_eigvecs(sdmd_ctx* ctx, double* W, int32_t* r);
 
 /* DMD modes of the newest DMD frame, this rank's rows: Φ[:, cols] = X' V Σ⁻¹ W[:, cols]
  * (Eq. Phi), computed on demand on the fp64 tensor pipe (K2).  phi_dev: device buffer,
- * n_local x ncols complex (interleaved), column-major with leading dimension ld >= n_local. */
+ * n_local x ncols complex (interleaved), column-major with leading dimension ld >= n_local.
+ * Sparse contexts return the modes in the coefficient space of the pushed snapshots (NEXT-3:
+ * Φ̂ = X̂'(YW), accumulated over the sparse window columns in fixed order). */
 int sdmd_get_modes(sdmd_ctx* ctx, const int32_t* cols, int32_t ncols, double* phi_dev, int64_t ld);
 
 /* Newest background column produced (frame index in *frame, -1 if none yet): lowrank = |l|,

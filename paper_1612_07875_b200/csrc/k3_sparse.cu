@@ -89,4 +89,47 @@ cudaError_t launch_set_int(int* p, int v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---- NEXT-3: DMD modes in coefficient space, Φ̂ = X̂'(Y W) over the sparse window (P:355-361:
+// the modes of the transformed data are the transformed modes, by unitary invariance).  Block q
+// owns mode column q; it zeroes Φ̂[:, q] and then walks the m window columns IN ORDER, its threads
+// scattering val_e · T[k][q] into the column's nonzero rows (indices are unique within a column,
+// and a block barrier separates columns): every element is accumulated in fixed k order.
+__global__ void __launch_bounds__(256) modes_sparse_kernel(const int* __restrict__ idx,
+                                                          const double* __restrict__ val,
+                                                          const int* __restrict__ nnz, int nnz_cap,
+                                                          int NS, long long row_begin, long long n,
+                                                          long long first_frame, int m,
+                                                          const double2* __restrict__ T, int nc,
+                                                          double2* __restrict__ phi, long long ldphi) {
+  const int q = blockIdx.x;
+  if (q >= nc) return;
+  double2* col = phi + (long long)q * ldphi;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) col[i] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int k = 0; k < m; ++k) {
+    const int slot = (int)((first_frame + k) % NS);
+    const int nz = nnz[slot];
+    const int* ik = idx + (long long)slot * nnz_cap;
+    const double* vk = val + (long long)slot * nnz_cap;
+    const double2 t = T[(long long)q * m + k];
+    for (int e = threadIdx.x; e < nz; e += blockDim.x) {
+      const long long row = ik[e] - row_begin;
+      const double v = vk[e];
+      double2 c = col[row];
+      c.x = fma(v, t.x, c.x);
+      c.y = fma(v, t.y, c.y);
+      col[row] = c;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_modes_sparse(const int* idx, const double* val, const int* nnz, int nnz_cap, int NS,
+                                long long row_begin, long long n, long long first_frame, int m,
+                                const double* T, int nc, double* phi, long long ldphi, cudaStream_t s) {
+  modes_sparse_kernel<<<nc, 256, 0, s>>>(idx, val, nnz, nnz_cap, NS, row_begin, n, first_frame, m,
+                                         (const double2*)T, nc, (double2*)phi, ldphi);
+  return cudaGetLastError();
+}
+
 }  // namespace sdmd

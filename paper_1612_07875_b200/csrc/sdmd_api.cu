@@ -772,12 +772,25 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
   const int slot = (int)(t % c->NS);
   int* sidx = c->sp_idx + (size_t)slot * c->cfg.nnz_cap;
   double* sval = c->sp_val + (size_t)slot * c->cfg.nnz_cap;
-  const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  if (nnz > 0) {
-    CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), kind, c->stream));
-    CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), kind, c->stream));
+  if (where == SDMD_HOST) {
+    // compressed ingest: only the nnz (index, value) pairs
+    // cross PCIe (12 B per nonzero), on the copy stream so that they overlap the previous sparse
+    // Gram pass; slot t mod NS was last read by the pass of frame t-2
+    if (t >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_k1[(t - 2) % kEvents], 0));
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), cudaMemcpyHostToDevice, c->copy_stream));
+      CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), cudaMemcpyHostToDevice, c->copy_stream));
+    }
+    CK(launch_set_int(c->sp_nnz + slot, nnz, c->copy_stream));
+    CK(cudaEventRecord(c->ev_copy[t % kEvents], c->copy_stream));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_copy[t % kEvents], 0));
+  } else {
+    if (nnz > 0) {
+      CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    CK(launch_set_int(c->sp_nnz + slot, nnz, c->stream));
   }
-  CK(launch_set_int(c->sp_nnz + slot, nnz, c->stream));
   c->launches += 1;
   return enqueue_frame(c, t);
 }
@@ -1005,7 +1018,7 @@ int sdmd_get_eigvecs(sdmd_ctx* c, double* W, int32_t* r) {
 
 int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_dev, int64_t ld) {
   if (!c || !cols || ncols < 1 || !phi_dev || ld < c->cfg.n_local) return invalid(c, "get_modes: bad argument");
-  if (c->cfg.storage != SDMD_DENSE) return invalid(c, "get_modes: dense storage only");
+
   CK(cudaSetDevice(c->dev));
   K4Result res{};
   int st = newest_result(c, &res);
@@ -1026,8 +1039,14 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   const int w = win_of(c, c->last_dmd);
   CK(launch_make_T(k.Y, w, res.r, c->Wall, c->colbuf, ncols, c->Tbuf, c->stream));
   // X' of the frame's window = frames last_dmd-w+1 .. last_dmd
-  CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - w + 1, w,
-                  c->Tbuf, ncols, phi_dev, ld, c->stream));
+  if (c->cfg.storage == SDMD_DENSE) {
+    CK(launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, c->last_dmd - w + 1, w,
+                    c->Tbuf, ncols, phi_dev, ld, c->stream));
+  } else {                                      // coefficient-space modes (NEXT-3), K3 scatter
+    CK(launch_modes_sparse(c->sp_idx, c->sp_val, c->sp_nnz, c->cfg.nnz_cap, c->NS, c->cfg.row_begin,
+                           c->cfg.n_local, c->last_dmd - w + 1, w, c->Tbuf, ncols, phi_dev, ld,
+                           c->stream));
+  }
   c->launches += 1 + (ncols + 31) / 32;
   CK(cudaStreamSynchronize(c->stream));
   return SDMD_OK;

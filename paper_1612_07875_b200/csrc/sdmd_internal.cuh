@@ -206,6 +206,10 @@ size_t init_gram_work_elems(long long n, int k);
 cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long long n,
                          long long first_frame, int m, const double* T /*m x nc complex*/,
                          int nc, double* phi, long long ldphi, cudaStream_t s);
+cudaError_t launch_modes_sparse(const int* idx, const double* val, const int* nnz, int nnz_cap, int NS,
+                                long long row_begin, long long n, long long first_frame, int m,
+                                const double* T /*m x nc complex*/, int nc, double* phi, long long ldphi,
+                                cudaStream_t s);
 cudaError_t launch_ghist_from_gram(const double* G, int k, double* ghist, int NH, int m,
                                    long long first_frame, cudaStream_t s);
 cudaError_t launch_gather_gram(const double* ghist, int NH, int m, long long f_last, int k,
