@@ -53,6 +53,9 @@ namespace sdmd {
                           // column count.  Measured slower (C4 pipeline pass 3.69 -> 4.78 ms at lag 9:
                           // the predicated loads defeat the register double-buffering), so off.
 #endif
+#ifndef K1V2_NORC
+#define K1V2_NORC 0       // v2 A/B: 1 = always accumulate the complex background (no real fast path)
+#endif
 #ifndef K1V2_DBG
 #define K1V2_DBG 0        // v2 experiments: 1 = skip the background reduction, 2 = skip its FMAs
 #endif
@@ -519,8 +522,10 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
 // every warp walks exactly NQ columns, the ones past the union U pointing at the (L1-resident)
 // x_t tile with a zero background coefficient and a discarded dot.  Column offsets are 32-bit, in
 // 16-byte units.
-template <typename T> struct BgAcc2;
-template <> struct BgAcc2<float> {              // rows (0,1) and (2,3) of the lane, packed FFMA2
+// RC: the background coefficients are real (c.y == 0 for every column: a real λ_idx, the usual
+// case for the slowest mode) — only the real part of l = X'c is accumulated.
+template <typename T, bool RC = false> struct BgAcc2;
+template <bool RC> struct BgAcc2<float, RC> {   // rows (0,1) and (2,3) of the lane, packed FFMA2
   using C2 = float2;
   using CW = float4;                           // (c.x, c.x, c.y, c.y)
   float2 re[2], im[2];
@@ -533,22 +538,25 @@ template <> struct BgAcc2<float> {              // rows (0,1) and (2,3) of the l
     const float2 z01 = make_float2(z.x, z.y), z23 = make_float2(z.z, z.w);
     re[0] = __ffma2_rn(cr, z01, re[0]);
     re[1] = __ffma2_rn(cr, z23, re[1]);
-    im[0] = __ffma2_rn(ci, z01, im[0]);
-    im[1] = __ffma2_rn(ci, z23, im[1]);
+    if (!RC) {
+      im[0] = __ffma2_rn(ci, z01, im[0]);
+      im[1] = __ffma2_rn(ci, z23, im[1]);
+    }
   }
   __device__ __forceinline__ C2 get(int e) const {
     return (e & 1) ? make_float2(re[e >> 1].y, im[e >> 1].y) : make_float2(re[e >> 1].x, im[e >> 1].x);
   }
 };
-template <> struct BgAcc2<double> {
+template <bool RC> struct BgAcc2<double, RC> {
   using C2 = double2;
   using CW = double2;
   double2 v[2];
   static __device__ __forceinline__ CW make(double2 c) { return c; }
   __device__ __forceinline__ void zero() { v[0] = v[1] = make_double2(0.0, 0.0); }
   __device__ __forceinline__ void add(const CW c, const double2 z) {
-    v[0].x = fma(c.x, z.x, v[0].x); v[0].y = fma(c.y, z.x, v[0].y);
-    v[1].x = fma(c.x, z.y, v[1].x); v[1].y = fma(c.y, z.y, v[1].y);
+    v[0].x = fma(c.x, z.x, v[0].x);
+    v[1].x = fma(c.x, z.y, v[1].x);
+    if (!RC) { v[0].y = fma(c.y, z.x, v[0].y); v[1].y = fma(c.y, z.y, v[1].y); }
   }
   __device__ __forceinline__ C2 get(int e) const { return v[e]; }
 };
@@ -600,7 +608,14 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
     for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], 1); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncthreads();
+  // real coefficients (every c.y == 0) select the real-only background accumulation
+  bool creal = true;
+  if (BG)
+    for (int k = tid; k < p.m; k += K1_THREADS) creal = creal && (p.cbg[k].y == 0.0);
+  const bool realc = __syncthreads_and(creal ? 1 : 0) != 0 && BG && !K1V2_NORC;
+  auto body = [&](auto rc_tag) {
+  constexpr bool RC = decltype(rc_tag)::value;
+  using AccR = BgAcc2<T, RC>;
 
   const VT* __restrict__ ringv = (const VT*)p.ring;
   const long long NT = p.ld / TILE;
@@ -681,7 +696,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
       to_double(xv, xd);
     }
     if (BG && !(K1V2_DBG & 1) && it >= LAGR && (((it - LAGR) & (K1_WARPS - 1)) == warp)) bg_load_x(it - LAGR);
-    Acc bacc;
+    AccR bacc;
     if (BG) bacc.zero();
     const long long next = tile + gridDim.x;
 #pragma unroll
@@ -754,6 +769,9 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
     __syncthreads();
     commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
   }
+  };  // body
+  if (realc) body(std::true_type{});
+  else body(std::false_type{});
 }
 
 __global__ void commit_kernel(const K1Params p) {
