@@ -64,7 +64,9 @@ static __device__ void commit_batch(const double* gout, int k, int m, long long 
     const int j = e / (m + 1), i = e % (m + 1);
     ghist[((f0 + j) % NH) * (m + 1) + i] = gout[e];
   }
-  if (threadIdx.x == 0) st->committed = f0 + k;
+  __syncthreads();
+  __threadfence();
+  if (threadIdx.x == 0) *(volatile long long*)&st->committed = f0 + k;
 }
 
 template <typename T>

@@ -61,7 +61,7 @@ static __device__ __forceinline__ double gram_at(const double* gh, int NH, int m
   // (row of frame g: <x_{g-mh+k}, x_g> at k)
   const int a = i < j ? i : j, b = i < j ? j : i;
   const long long fb = f - w + b;
-  return gh[(fb % NH) * (mh + 1) + (a - b + mh)];
+  return __ldcg(gh + (fb % NH) * (mh + 1) + (a - b + mh));   // L2: rows are published by commits
 }
 
 static __device__ __forceinline__ int rr_player(int pos, int step, int mp) {
@@ -876,15 +876,16 @@ k4a_kernel(const K4Params p) {
   K4Result* res = p.res;
   {
     volatile DevState* st = p.st;
-    // frame discarded by the poison contract (uniform across the cluster: st is read-only here)
-    if (st->status != 0 && st->failed_frame <= f) return;
+    // frame discarded by the poison contract.  K4a is released by the commit of frame f-1, so only
+    // poison from frames < f is settled (uniform across the cluster) here; frame f's own outcome
+    // is decided uniformly before the Ã stage
+    if (st->status != 0 && st->failed_frame < f) return;
   }
   if (tid == 0) ph[0] = clock64();
   // ---- a5: S = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1] from the Gram history
   for (int idx = gtid; idx < m * m; idx += K4_GT) {
     const int i = idx % m, j = idx / m;
     p.A[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j);
-    p.Gxy[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j + 1);
   }
   if (gtid < JACOBI_MAX_SWEEPS) p.flags[gtid] = 0;
   cl_sync();
@@ -1062,6 +1063,39 @@ k4a_kernel(const K4Params p) {
   }
   cl_sync();
   if (tid == 0) ph[3] = clock64();
+
+  // ---- XᵀX' = G[0:m,1:m+1] needs the Gram column of frame f itself.  S = G[0:m,0:m] only needs
+  // frames up to f-1, so K4a is released by the commit of frame f-1 and the Jacobi above overlaps
+  // the Gram pass of frame f; here it waits for that pass's commit (device counter, published
+  // after the history row) — or for the stream to be poisoned.
+  // Frame f either gets committed, or the stream is poisoned before it is (a rejected frame <= f,
+  // or a rejected batch containing f — whose failed_frame may be > f).  The poison flag is read
+  // BEFORE the counter: a poison raised after f's commit (a later frame) is causally after the
+  // commit, so seeing it and then an uncommitted f proves f will never commit.  Either outcome
+  // is permanent, so every CTA of the cluster reaches the same decision independently.
+  {
+    __shared__ int sh_go;
+    if (tid == 0) {
+      volatile DevState* vs = p.st;
+      int go = -1;
+      while (go < 0) {
+        const int poisoned = vs->status;
+        __threadfence();
+        if (vs->committed >= f + 1) go = 1;
+        else if (poisoned != 0) go = 0;
+        else __nanosleep(256);
+      }
+      sh_go = go;
+    }
+    __syncthreads();
+    if (!sh_go) return;                                      // frame f rejected: discard
+  }
+  __threadfence();
+  for (int idx = gtid; idx < m * m; idx += K4_GT) {
+    const int i = idx % m, j = idx / m;
+    p.Gxy[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j + 1);
+  }
+  cl_sync();
 
   // ---- a7: B = (XᵀX') Y (m x r), Ã = Yᵀ B (r x r, row-major into H) — zero n-length dots
   for (int idx = gtid; idx < m * r; idx += K4_GT) {

@@ -529,7 +529,9 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   cudaError_t e;
   const long long q = lidx(c, t), P = c->P;               // local index of frame t (t mod P == rank)
   cudaStream_t A = c->sa[q % c->Wa], B = c->sb[q % c->Wb];
-  if ((e = cudaStreamWaitEvent(A, c->ev_commit[t % kEvents], 0)) != cudaSuccess) return e;
+  // released by the commit of frame t-1 (S_t is complete then); K4a itself waits on the device
+  // for the commit of frame t before its Ã stage, so its Jacobi overlaps the Gram pass of frame t
+  if ((e = cudaStreamWaitEvent(A, c->ev_commit[(t - 1) % kEvents], 0)) != cudaSuccess) return e;
   if (t - c->NWS * P >= first_dmd(c))          // workspace reuse: local frame q-NWS must be finished
     if ((e = cudaStreamWaitEvent(A, c->ev_done[(q - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
   // ... and local frame q+Wa-NWS (whose warm start reads this workspace's V) must have passed K4a

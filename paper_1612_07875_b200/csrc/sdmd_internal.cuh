@@ -181,7 +181,11 @@ static __device__ __forceinline__ void commit_block(const double* gout, int nd, 
   double* row = ghist + (long long)(f_new % NH) * (m + 1);
   const int off = m + 1 - nd;
   for (int k = threadIdx.x; k < m + 1; k += blockDim.x) row[k] = (k >= off) ? gout[k - off] : 0.0;
-  if (threadIdx.x == 0) st->committed = f_new + 1;
+  // publish: the history row must be visible GPU-wide before the counter (K4a of frame f_new
+  // polls it to start its Ã stage, see k4_eigen.cu)
+  __syncthreads();
+  __threadfence();
+  if (threadIdx.x == 0) *(volatile long long*)&st->committed = f_new + 1;
 }
 
 

@@ -1,0 +1,9 @@
+mkdir -p gpurun_out
+export CUDA_DEVICE_MAX_CONNECTIONS=32
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider 2>&1 | tail -3
+B="python bench.py --steps 400 --warmup 5 --no-cpu-baseline --e2e-steps 2"
+run() { tag=$1; shift; echo "== $tag"; timeout 300 env "$@" 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); r=d['roofline']; print(d['value'], r['k1_ms_avg'], r['frac'], r['k4_ms_avg'], r['k1_wait_ms_avg'], d['clocks']['sm_mhz'])"; }
+run l8 $B
+run l7 $B --lag 7
+run l8b $B
+timeout 900 python scripts/bench_configs.py --out gpurun_out/configs_r2c.md 2>&1 | tail -7
