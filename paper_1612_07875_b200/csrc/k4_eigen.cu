@@ -1071,24 +1071,34 @@ k4a_kernel(const K4Params p) {
   // Frame f either gets committed, or the stream is poisoned before it is (a rejected frame <= f,
   // or a rejected batch containing f — whose failed_frame may be > f).  The poison flag is read
   // BEFORE the counter: a poison raised after f's commit (a later frame) is causally after the
-  // commit, so seeing it and then an uncommitted f proves f will never commit.  Either outcome
-  // is permanent, so every CTA of the cluster reaches the same decision independently.
+  // commit, so seeing it and then an uncommitted f proves f will never commit.  CTA 0 of the
+  // cluster decides (with a ~35 s bound so that a broken invariant can never hang the device) and
+  // the other CTAs read its decision through distributed shared memory: uniform by construction.
   {
     __shared__ int sh_go;
-    if (tid == 0) {
+    if (crank == 0 && tid == 0) {
       volatile DevState* vs = p.st;
       int go = -1;
+      const long long t_start = clock64();
       while (go < 0) {
         const int poisoned = vs->status;
         __threadfence();
         if (vs->committed >= f + 1) go = 1;
         else if (poisoned != 0) go = 0;
+        else if (clock64() - t_start > (1LL << 36)) go = 0;
         else __nanosleep(256);
       }
       sh_go = go;
     }
-    __syncthreads();
-    if (!sh_go) return;                                      // frame f rejected: discard
+    cl_sync();
+    int go;
+    {
+      unsigned a = (unsigned)__cvta_generic_to_shared(&sh_go), ra;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(a));
+      asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(go) : "r"(ra) : "memory");
+    }
+    cl_sync();                                               // rank 0's flag read by everyone
+    if (!go) return;                                         // frame f rejected: discard
   }
   __threadfence();
   for (int idx = gtid; idx < m * m; idx += K4_GT) {

@@ -764,6 +764,69 @@ def test_noisy_video_full_rank_spectrum(m):
     eng.close()
 
 
+def test_maximum_sizes_m256_r224_with_background():
+    """Edge case at the ABI maxima: m = SDMD_MAX_M = 256 (K1 union m + lag > 256 columns, the
+    widest K1 instance), r capped at SDMD_MAX_R = 224 on a full-rank noisy window (largest QR,
+    K4 shared memory), background on: Gram, σ, λ and the background against the oracle."""
+    vs = synth.video_config("C3s")
+    m = 256
+    T = m + 1 + 12
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+    lag = eng.info()["lag"]
+    ref = O.StreamingDMD(m, background=True, r_max=224)
+    outs = {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(frames[:, t])
+        if o is not None:
+            outs[t] = o
+    eng.sync()
+    out = ref.last
+    assert normwise(eng.gram(), ref.gram.G) < 1e-12
+    sp = eng.spectrum()
+    assert sp["r"] == out["r"] == 224
+    err, _ = match(sp["lam"], out["lam"])
+    assert err < 1e-7, err
+    assert abs(sp["lam"][sp["idx"]] - out["lam"][out["idx"]]) < 1e-9
+    sv = eng.svd(with_V=False)
+    keep = out["sigma"] / out["sigma"][0] >= 1e-4
+    assert np.max(np.abs(sv["sigma"][keep] - out["sigma"][keep]) / out["sigma"][keep]) < 1e-10
+    low, spv, mask, fb = eng.background()
+    assert fb == T - 1 - lag
+    o = outs[fb]
+    rel = np.max(np.abs(low - o["lowrank"])) / np.max(np.abs(o["lowrank"]))
+    assert rel < 1e-4, rel
+    eng.close()
+
+
+def test_empty_sparse_frames():
+    """Edge case: sparse snapshots with no nonzeros (nnz = 0) give zero Gram rows/columns and a
+    rank-deficient window; the Gram matches the oracle and the DMD still runs."""
+    st = synth.SparseDCTStream(N=64, k_low=8.0, n_shell=20, seed=5)
+    m, T = 10, 24
+    eng = Eng(st.n, m, storage="sparse", nnz_cap=st.nnz_cap, workers=1)
+    ref = O.StreamingGram(m)
+    for t in range(T):
+        if t in (3, 15, 16):
+            idx, val = np.zeros(0, dtype=np.int32), np.zeros(0, dtype=np.float64)
+            dense = np.zeros(st.n)
+        else:
+            idx, val = st.frame(t)
+            dense = st.dense(t)
+        eng.push_sparse(idx, val)
+        ref.push(dense)
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    G = eng.gram()
+    assert np.all(G[5, :] == 0.0) and np.all(G[:, 6] == 0.0)    # frames 15, 16 in window 13..23
+    d = O.dmd_from_gram(ref.G)
+    sp = eng.spectrum()
+    assert sp["r"] == d["r"]
+    eng.close()
+
+
 def test_constant_stream_fixed_point():
     """S:346, S:353, S:377 on the device: a constant video has σ₁ = √m‖x‖, r = 1, λ_idx = 1 and
     an all-background foreground (sparse ≈ 0, empty mask)."""
