@@ -119,6 +119,11 @@ typedef struct sdmd_config {
                        * the DMD of the growing window (X = the t columns x_0..x_{t-1}); the
                        * getters then report windows narrower than m (sigma zero-padded, V
                        * with leading dimension m).  No background before the window is full */
+  int32_t modes_every_frame; /* 1 (dense, one rank): the DMD modes Φ = X'(YW) of every frame are
+                       * computed on its eigen-worker stream (all r eigenvectors, then K2 on
+                       * DMMA; SURVEY §8(f) NEXT-2 "full Φ every frame") and sdmd_get_modes
+                       * returns the newest frame's columns without recomputing.  Meant for
+                       * small r (C2: r = 21); at C4 (r = 200) it would cost ~0.1 s per frame */
 } sdmd_config;
 
 typedef struct sdmd_info {

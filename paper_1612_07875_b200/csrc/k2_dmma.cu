@@ -560,6 +560,32 @@ __global__ void make_T_kernel(const double* Y, int m, int r, const double2* W, c
   T[idx] = s;
 }
 
+// T = Y W for every mode (per-frame modes, NEXT-2): r read on the device; columns r..r_max-1 = 0.
+__global__ void make_T_all_kernel(const double* Y, int m, const K4Result* res, int r_max,
+                                  const double2* W, double2* T) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * r_max) return;
+  const int r = ((volatile const K4Result*)res)->r;
+  const int k = idx % m, q = idx / m;
+  double2 s = make_double2(0.0, 0.0);
+  if (q < r) {
+    for (int i = 0; i < r; ++i) {
+      const double y = Y[(long long)i * m + k];
+      const double2 w = W[(long long)q * r + i];
+      s.x = fma(y, w.x, s.x);
+      s.y = fma(y, w.y, s.y);
+    }
+  }
+  T[idx] = s;
+}
+
+cudaError_t launch_make_T_all(const double* Y, int m, const K4Result* res, int r_max,
+                              const double2* W, double* T, cudaStream_t s) {
+  const int n = m * r_max;
+  make_T_all_kernel<<<(n + 255) / 256, 256, 0, s>>>(Y, m, res, r_max, W, (double2*)T);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_make_T(const double* Y, int m, int r, const double2* W, const int* cols, int nc,
                           double* T, cudaStream_t s) {
   const int n = m * nc;

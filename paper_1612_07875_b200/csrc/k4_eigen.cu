@@ -1532,7 +1532,7 @@ int k4_cluster_size() { return K4_CLUSTER; }
 // ------------------------------------------------------- on-demand eigenvectors and b --------
 __global__ void __launch_bounds__(32) k4_vecs_kernel(const K4VecParams p) {
   extern __shared__ __align__(16) unsigned char vs_smem[];
-  const int r = p.r;
+  const int r = p.res ? ((volatile const K4Result*)p.res)->r : p.r;   // p.r: r_max when p.res
   double2* z = reinterpret_cast<double2*>(vs_smem);
   double2* rhs = z + r;
   double2* lk = rhs + r;

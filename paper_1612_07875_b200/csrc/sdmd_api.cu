@@ -111,10 +111,18 @@ struct sdmd_ctx {
   cudaEvent_t ev_bgw[2]{}, ev_d2h[2]{};
   bool d2h_pending[2] = {false, false};
   long long bg_last = -1;               // frame of the newest background pass enqueued
+  // per-frame modes (cfg.modes_every_frame, NEXT-2): per single-CTA worker stream, the LU
+  // workspaces of all r inverse iterations, W, b, T = YW and Φ (ld x r_max complex)
+  double2* pm_M[kMaxWorkers]{};
+  double2* pm_W[kMaxWorkers]{};
+  double2* pm_b[kMaxWorkers]{};
+  double* pm_T[kMaxWorkers]{};
+  double2* pm_phi[kMaxWorkers]{};
   // workers
   Workspace ws[kMaxWS];
   int NWS = 0, Wa = 1, Wb = 4;
   bool warm = true;                     // Jacobi warm start (SDMD_WARM=0 disables, A/B)
+  bool throttle = true;                 // eigen-work flow control (SDMD_THROTTLE=0 disables, A/B)
   cudaStream_t sa[kMaxWorkers]{};      // cluster eigen workers (K4a: Jacobi .. Hessenberg)
   cudaStream_t sb[kMaxWorkers]{};      // single-CTA eigen workers (K4b: QR .. background coeffs)
   cudaEvent_t ev_a[kEvents]{};
@@ -270,6 +278,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (cfg.batch_max < 0 || cfg.batch_max > kMaxBatch || (cfg.batch_max > 0 && cfg.storage != SDMD_DENSE))
     return SDMD_E_INVALID;
   if (cfg.bg_modes < 0 || cfg.bg_modes > kMaxBgModes) return SDMD_E_INVALID;
+  if (cfg.modes_every_frame && (cfg.storage != SDMD_DENSE || cfg.nranks > 1 || !cfg.dmd))
+    return SDMD_E_INVALID;
   if (cfg.nranks > 1 && !cfg.nccl_uid) return SDMD_E_INVALID;
 
   sdmd_ctx* c = new sdmd_ctx();
@@ -302,6 +312,9 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
   if (c->NS < m + c->cfg.batch_max + 1) c->NS = m + c->cfg.batch_max + 1;   // union of a batch
+  // per-frame modes read X'_f on the worker stream up to ~lag frames after f was pushed: the ring
+  // keeps lag + 2 more slots, and push t waits for frame t-lag-2's worker (see enqueue_frame)
+  if (c->cfg.modes_every_frame && c->NS < m + c->L + 3) c->NS = m + c->L + 3;
   c->NH = 2 * (m + c->L + 4);
   c->NC = c->L + 2;
   c->es = c->cfg.dtype == SDMD_F32 ? 4 : 8;
@@ -341,6 +354,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* ew = std::getenv("SDMD_WARM");
     c->warm = !(ew && ew[0] == '0');
+    const char* et = std::getenv("SDMD_THROTTLE");
+    c->throttle = !(et && et[0] == '0');
     const char* eb = std::getenv("SDMD_BG_NODMD");
     c->bg_nodmd = eb && eb[0] == '1';
   }
@@ -429,6 +444,16 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(k.uv, (size_t)R);
     cudaMemsetAsync(k.res, 0, sizeof(K4Result), c->stream);
   }
+  if (c->cfg.modes_every_frame) {
+    const size_t rm = (size_t)c->cfg.r_max;
+    for (int w = 0; w < c->Wb; ++w) {
+      AL(c->pm_M[w], rm * rm * rm);
+      AL(c->pm_W[w], rm * rm);
+      AL(c->pm_b[w], rm);
+      AL(c->pm_T[w], 2 * (size_t)m * rm);
+      AL(c->pm_phi[w], (size_t)c->ld * rm);
+    }
+  }
   for (int i = 0; i < kEvents; ++i) {
     if (cudaEventCreateWithFlags(&c->ev_commit[i], cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -497,6 +522,9 @@ int sdmd_destroy(sdmd_ctx* c) {
   for (int w = 0; w < kMaxWorkers; ++w) {
     if (c->sa[w]) cudaStreamDestroy(c->sa[w]);
     if (c->sb[w]) cudaStreamDestroy(c->sb[w]);
+    void* pm[] = {c->pm_M[w], c->pm_W[w], c->pm_b[w], c->pm_T[w], c->pm_phi[w]};
+    for (void* q : pm)
+      if (q) cudaFree(q);
   }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -547,6 +575,18 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
   if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
   if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); c->tl.push_back({t, 2, kb.first, kb.second}); }
+  if (c->cfg.modes_every_frame) {               // NEXT-2: Φ_t = X'_t (Y W) for all r modes
+    const int sw = (int)(q % c->Wb), rm = c->cfg.r_max, w = win_of(c, t);
+    Workspace& k = ws_of(c, t);
+    K4VecParams v{};
+    v.r = rm; v.H = k.H; v.Qv = k.Qv; v.tau = k.tau; v.lam = k.lam; v.alpha1 = k.alpha1;
+    v.Mws = c->pm_M[sw]; v.W = c->pm_W[sw]; v.b = c->pm_b[sw]; v.j0 = 0; v.res = k.res;
+    if ((e = launch_k4_vecs(v, rm, B)) != cudaSuccess) return e;
+    if ((e = launch_make_T_all(k.Y, w, k.res, rm, c->pm_W[sw], c->pm_T[sw], B)) != cudaSuccess) return e;
+    if ((e = launch_modes(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, t - w + 1, w,
+                          c->pm_T[sw], rm, (double*)c->pm_phi[sw], c->ld, B)) != cudaSuccess) return e;
+    c->launches += 3;
+  }
   if ((e = cudaEventRecord(c->ev_done[q % kEvents], B)) != cudaSuccess) return e;
   c->launches += 2;
   ws_of(c, t).vecs_frame = -1;
@@ -567,6 +607,14 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   if (c->timing) {                                // wait_ev: time the ctx stream spends waiting
     tw = new_pair();                              // for the background coefficients of t - L
     CK(cudaEventRecord(tw.first, c->stream));
+  }
+  if (c->cfg.dmd && (c->cfg.modes_every_frame || c->throttle) && t - c->L - 2 >= first_dmd(c) &&
+      owns(c, t - c->L - 2)) {
+    // modes_every_frame: frame t-L-2's modes read ring slots that push t+2 may overwrite (see
+    // sdmd_create).  Otherwise flow control: at most ~lag frames of eigen work in flight (measured
+    // on the K4-bound configs: an unthrottled stream floods the worker queues, profiles/r2h…)
+    const long long fw = t - c->L - 2;
+    CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fw) % kEvents], 0));
   }
   if (bg && c->cfg.dmd) {
     const long long fb = t - c->L;
@@ -1027,6 +1075,14 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   if (st) return st;
   for (int q = 0; q < ncols; ++q)
     if (cols[q] < 0 || cols[q] >= res.r) return invalid(c, "get_modes: column out of range");
+  if (c->cfg.modes_every_frame) {                 // computed per frame on the worker stream
+    const int sw = (int)(lidx(c, c->last_dmd) % c->Wb);
+    for (int q = 0; q < ncols; ++q)
+      CK(cudaMemcpyAsync((double2*)phi_dev + (size_t)q * ld, c->pm_phi[sw] + (size_t)cols[q] * c->ld,
+                         c->cfg.n_local * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SDMD_OK;
+  }
   st = ensure_vecs(c);
   if (st) return st;
   const int m = c->cfg.m;

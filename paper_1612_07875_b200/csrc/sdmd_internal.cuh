@@ -143,6 +143,7 @@ struct K4VecParams {
   double2* W;                 // r*r column-major (output)
   double2* b;                 // r (output)
   int j0;                     // first eigenvalue of this launch
+  const K4Result* res;        // non-null: r (and the W stride) read on the device (per-frame modes)
 };
 
 struct K3Params {             // sparse Gram column
@@ -219,6 +220,8 @@ cudaError_t launch_ghist_from_gram(const double* G, int k, double* ghist, int NH
 cudaError_t launch_gather_gram(const double* ghist, int NH, int m, long long f_last, int k,
                                double* Gout, cudaStream_t s);
 cudaError_t launch_set_int(int* p, int v, cudaStream_t s);
+cudaError_t launch_make_T_all(const double* Y, int m, const K4Result* res, int r_max,
+                              const double2* W, double* T, cudaStream_t s);
 cudaError_t launch_make_T(const double* Y, int m, int r, const double2* W, const int* cols,
                           int nc, double* T, cudaStream_t s);
 

@@ -47,6 +47,7 @@ class Config(ctypes.Structure):
         ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
         ("lag", ctypes.c_int32), ("eigen_shard", ctypes.c_int32),
         ("batch_max", ctypes.c_int32), ("bg_modes", ctypes.c_int32), ("buildup", ctypes.c_int32),
+        ("modes_every_frame", ctypes.c_int32),
     ]
 
 
@@ -160,7 +161,8 @@ class StreamingDMD:
                  workers: int = 4, device: int = 0, stream="torch", rank: int = 0,
                  nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
                  nccl_uid: bytes | None = None, lag: int = 0, eigen_shard: int = 1,
-                 batch_max: int = 0, bg_modes: int = 0, buildup: bool = False):
+                 batch_max: int = 0, bg_modes: int = 0, buildup: bool = False,
+                 modes_every_frame: bool = False):
         L = lib()
         cfg = Config()
         L.sdmd_config_init(ctypes.byref(cfg))
@@ -194,6 +196,7 @@ class StreamingDMD:
         cfg.batch_max = int(batch_max)
         cfg.bg_modes = int(bg_modes)
         cfg.buildup = 1 if buildup else 0
+        cfg.modes_every_frame = 1 if modes_every_frame else 0
         self._uid = None
         if nccl_uid is not None:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)

@@ -48,10 +48,11 @@ def timed(eng, push, K):
     return ms, st
 
 
-def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0, bg_modes=0):
+def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0, bg_modes=0,
+              modes_every_frame=False):
     P = frames_dev.shape[0]
     eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max,
-                       lag=lag, bg_modes=bg_modes)
+                       lag=lag, bg_modes=bg_modes, modes_every_frame=modes_every_frame)
     eng.init_window(frames_dev[: m + 1])
     t = m + 1
     for _ in range(2 * (m + 1)):
@@ -134,6 +135,10 @@ def main():
     Xc = cw.frames(0, 300)
     Xcd = torch.from_numpy(np.ascontiguousarray(Xc.T)).cuda()
     res.append(dense_run("C2", Xcd, cw.n, 150, "f64", args.frames, args.workers, r_max=21))
+    print(json.dumps(res[-1]), flush=True)
+    # NEXT-2: the full Φ (n x 21 complex) of every frame on the worker streams
+    res.append(dense_run("C2 (modes every frame)", Xcd, cw.n, 150, "f64", args.frames, args.workers,
+                         r_max=21, modes_every_frame=True))
     print(json.dumps(res[-1]), flush=True)
     del Xcd
     # C3: 1920x1080 grey fp32 video, m = 100, background subtraction

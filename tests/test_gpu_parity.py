@@ -764,6 +764,38 @@ def test_noisy_video_full_rank_spectrum(m):
     eng.close()
 
 
+def test_modes_every_frame_matches_on_demand_and_oracle():
+    """NEXT-2 "full Φ every frame": with modes_every_frame the worker stream computes every
+    frame's modes (all eigenvectors, then K2); get_modes of the newest frame must equal the
+    on-demand path bitwise and b_j φ_j must match the oracle (planted C1, 1e-8)."""
+    pm = synth.planted_c1()
+    m, T = 16, 60
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    a = Eng(pm.n, m, dtype="f64", workers=3, modes_every_frame=True)
+    b = Eng(pm.n, m, dtype="f64", workers=3)
+    ref = O.StreamingDMD(m, background=False)
+    for t in range(T):
+        a.push(Xd[t])
+        b.push(Xd[t])
+        out = ref.push(X[:, t])
+    a.sync()
+    b.sync()
+    r = a.spectrum()["r"]
+    Pa = a.modes(list(range(r))).cpu().numpy()
+    Pb = b.modes(list(range(r))).cpu().numpy()
+    assert np.array_equal(Pa, Pb)
+    sp = a.spectrum(with_b=True)
+    err, perm = match(sp["lam"], out["lam"])
+    Phi_ref = O.modes(ref.gram.cols[1:], out)
+    for j in range(r):
+        u = sp["b"][j] * Pa[:, j]
+        v = out["b"][perm[j]] * Phi_ref[:, perm[j]]
+        assert np.linalg.norm(u - v) < 1e-8 * np.linalg.norm(v), j
+    a.close()
+    b.close()
+
+
 def test_maximum_sizes_m256_r224_with_background():
     """Edge case at the ABI maxima: m = SDMD_MAX_M = 256 (K1 union m + lag > 256 columns, the
     widest K1 instance), r capped at SDMD_MAX_R = 224 on a full-rank noisy window (largest QR,
