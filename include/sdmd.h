@@ -91,7 +91,8 @@ typedef struct sdmd_config {
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
   int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..20 (0 → 4); the cluster
-                       * stage uses max(1, workers / 2) streams.  The context uses about
+                       * stage uses max(1, workers / 2) streams (min(2·workers, 30 − workers, 20)
+                       * when r_max <= m/4: then the Jacobi stage bounds the rate).  The context uses about
                        * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that
                        * (e.g. 32) before CUDA initialises, else streams share hardware queues
                        * and the eigen stages serialise behind unrelated waits                  */

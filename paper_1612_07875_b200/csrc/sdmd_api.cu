@@ -303,7 +303,18 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams
   // keeps both stages' throughput above one frame per Gram pass (measured)
   c->Wa = c->W / 2 > 0 ? c->W / 2 : 1;
-  if (c->Wa + c->W + 2 > 32) c->Wa = 30 - c->W > 1 ? 30 - c->W : 1;   // 32 hardware queues
+  // r <= m/4 (e.g. C2: m = 150, r = 21): the single-CTA stage (QR of Ã) is light and the cluster
+  // stage (Jacobi of the m x m S) bounds the throughput: give it every remaining hardware queue
+  // (measured C2: W = 14 with 16 cluster streams 5455 vs W = 20 with 10 cluster streams 3486
+  // snapshots/s, profiles/r2j…)
+  if (4 * rmax <= c->cfg.m) {
+    int wa = 30 - c->W;
+    if (wa > 2 * c->W) wa = 2 * c->W;
+    if (wa > kMaxWorkers) wa = kMaxWorkers;
+    if (wa > c->Wa) c->Wa = wa;
+  }
+  if (c->Wa + c->W + 2 > 32) c->Wa = 30 - c->W;   // 32 hardware queues
+  if (c->Wa < 1) c->Wa = 1;
   if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
     const int v = std::atoi(ea);
     if (v >= 1 && v <= kMaxWorkers) c->Wa = v;
