@@ -118,6 +118,18 @@ class ClockSampler:
                 "samples": len(sm), "reasons": sorted(reasons)}
 
 
+def default_lag(W: int, N: int, m: int) -> int:
+    """Mirror of sdmd_create's default background lag (for sizing the frame pool before the
+    context exists): 2W at one rank, aligned down so that m + lag is a multiple of 16 (>= W+2);
+    W·N + 6 with eigen sharding; at most 64."""
+    want = min(2 * W if N == 1 else W * N + 6, 64)
+    if N == 1:
+        for lag in range(want, max(W + 2, 1) - 1, -1):
+            if (m + lag) % 16 == 0:
+                return lag
+    return want
+
+
 # ------------------------------------------------------------------------------ oracle -----
 def oracle_rate(row_frac: int, steps: int, warmup: int, seed_frames_from: int = 0):
     """Time the fp64 CPU oracle (as it stands) on a row sample of C4: rows [0, n/row_frac).
@@ -211,8 +223,8 @@ def run_ours(args):
         free, _ = torch.cuda.mem_get_info(dev)
         frame_bytes = n_loc * 4
         if args.lag < 0:
-            args.lag = 8 if N == 1 else 0
-        lag = args.lag if args.lag > 0 else min(2 * args.workers if N == 1 else args.workers * N + 6, 64)   # library default (eigen-sharded for N > 1)
+            args.lag = 0          # the library default (= 8 at C4 with 6 workers)
+        lag = args.lag if args.lag > 0 else default_lag(args.workers, N, M)   # the library's rule
         ring_bytes = (M + lag + 1) * ((n_loc + 255) // 256 * 256) * 4
         budget = free - ring_bytes - 12 * 2**30
         need = M + 1 + lag + W + K
@@ -374,8 +386,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workers", type=int, default=6)
     ap.add_argument("--lag", type=int, default=-1,
-                    help="background lag (frames); -1: 8 at N=1 (tuned for C4 with 6 workers, "
-                         "profiles/r1u), the library default W·N+6 at N>1; 0: library default")
+                    help="background lag (frames); -1 or 0: the library default (8 at C4 with 6 "
+                         "workers, profiles/r1u; W·N+6 at N>1)")
     ap.add_argument("--e2e-steps", type=int, default=48)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--timeline", default="", help="save the timed region's device timeline (.npy)")

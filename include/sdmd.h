@@ -90,7 +90,7 @@ typedef struct sdmd_config {
   int32_t background; /* 1: compute the newest background column every push (fused into the Gram
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
-  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..20 (0 → 4); the cluster
+  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..24 (0 → 4); the cluster
                        * stage uses max(1, workers / 2) streams (min(2·workers, 30 − workers, 20)
                        * when r_max <= m/4: then the Jacobi stage bounds the rate).  The context uses about
                        * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that

@@ -814,6 +814,8 @@ static cudaError_t launch_k1v2_nq(const K1Params& p, int grid, int U, cudaStream
   if (need <= 2) return launch_k1v2_inst<T, BG, 2>(p, grid, s);
   if (need <= 4) return launch_k1v2_inst<T, BG, 4>(p, grid, s);
   if (need <= 8) return launch_k1v2_inst<T, BG, 8>(p, grid, s);
+  if (need <= 10) return launch_k1v2_inst<T, BG, 10>(p, grid, s);   // fewer dummy slots per warp
+  if (need <= 12) return launch_k1v2_inst<T, BG, 12>(p, grid, s);
   if (need <= 13) return launch_k1v2_inst<T, BG, 13>(p, grid, s);
   if (need <= 14) return launch_k1v2_inst<T, BG, 14>(p, grid, s);
   if (need <= 16) return launch_k1v2_inst<T, BG, 16>(p, grid, s);
@@ -862,7 +864,8 @@ void preload_k1_kernels() {
   cudaFuncGetAttributes(&a, k1v2_kernel<float, true, NQ>);       \
   cudaFuncGetAttributes(&a, k1v2_kernel<double, false, NQ>);     \
   cudaFuncGetAttributes(&a, k1v2_kernel<double, true, NQ>);
-  K1V2_PRELOAD(2) K1V2_PRELOAD(4) K1V2_PRELOAD(8) K1V2_PRELOAD(13) K1V2_PRELOAD(14) K1V2_PRELOAD(16)
+  K1V2_PRELOAD(2) K1V2_PRELOAD(4) K1V2_PRELOAD(8) K1V2_PRELOAD(10) K1V2_PRELOAD(12) K1V2_PRELOAD(13)
+  K1V2_PRELOAD(14) K1V2_PRELOAD(16)
   K1V2_PRELOAD(K1_NQMAX)
 #undef K1V2_PRELOAD
 }

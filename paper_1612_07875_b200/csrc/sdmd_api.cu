@@ -296,8 +296,15 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // fit in lag·t_K1 for the Gram pass never to wait.  With P eigen shards
   // frames arrive P times faster while one frame's K4 latency is unchanged: W·P + 6 periods.
   {
-    const int want = c->P > 1 ? c->W * c->P + 6 : 2 * c->W;
-    c->L = c->cfg.lag > 0 ? c->cfg.lag : (want < kMaxLag ? want : kMaxLag);
+    int want = c->P > 1 ? c->W * c->P + 6 : 2 * c->W;
+    if (want > kMaxLag) want = kMaxLag;
+    // one rank: the largest lag <= 2W (but >= W+2) that makes the K1 union m + lag a multiple of
+    // the 16 warps, so that no warp streams dummy column slots (measured: C4 W = 6 → lag 8,
+    // C3 W = 20 → lag 28: 3,166 vs 2,651 snapshots/s at lag 40, profiles/r2l…)
+    if (c->P == 1 && c->cfg.background)
+      for (int l = want; l >= c->W + 2 && l >= 1; --l)
+        if ((c->cfg.m + l) % 16 == 0) { want = l; break; }
+    c->L = c->cfg.lag > 0 ? c->cfg.lag : want;
   }
   c->Wb = c->W;
   // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams

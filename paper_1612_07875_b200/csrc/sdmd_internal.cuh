@@ -15,7 +15,7 @@ namespace sdmd {
 
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
-constexpr int kMaxWorkers = 20;
+constexpr int kMaxWorkers = 24;
 constexpr int kMaxBatch = 8;
 constexpr int kMaxBgModes = 8;           // background modes (NEXT-2); +1 for the conjugate partner             // frames per batched push (K1b)
 constexpr int kMaxLag = 64;              // background lag cap (frames); union columns m + lag
