@@ -15,7 +15,10 @@
 // up with P times the frame rate of one GPU.  Local frame index q = t div P selects the worker
 // streams, the workspace and the K4 events.
 #include <dlfcn.h>
+#include <condition_variable>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -57,6 +60,34 @@ NcclApi* nccl_api() {
   api.loaded = true;
   return &api;
 }
+
+// In-process collective group (TEST backend, SDMD_LOCAL_GROUP=1): the ranks are contexts on the
+// SAME device driven by different host threads of one process.  Collectives stage each rank's
+// buffer in device memory, rendezvous on the host (so every rank's event is recorded before any
+// rank waits on it), and reduce in rank order — bit-identical on every rank, like NCCL's
+// single-reduction algorithms.  It exists only so that the multi-rank data path (row sharding,
+// the allreduce of g, eigen sharding and the broadcast of c_t) can be tested on one GPU: NCCL
+// refuses two ranks on one device.  Production runs use NCCL.
+struct LocalGroup {
+  int n = 0, arrived = 0;
+  long long gen = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  double* stage[8]{};
+  double** d_stage = nullptr;              // device copy of stage[] for the sum kernel
+  size_t cap = 0;
+  int refs = 0;
+  cudaEvent_t ev_in[8]{}, ev_out[8]{};
+  bool out_pending[8]{};
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == n) { arrived = 0; ++gen; cv.notify_all(); }
+    else cv.wait(lk, [&] { return gen != g; });
+  }
+};
+static std::mutex g_groups_mu;
+static std::map<std::string, LocalGroup*> g_groups;
 
 constexpr int kEvents = 256;      // > NWS + lag: event slots are reused modulo kEvents
 
@@ -154,6 +185,7 @@ struct sdmd_ctx {
   long long launches = 0;
   // nccl
   ncclComm_t comm = nullptr;
+  LocalGroup* lgroup = nullptr;           // SDMD_LOCAL_GROUP test backend
   std::string err;
 };
 
@@ -201,6 +233,72 @@ static int sync_all(sdmd_ctx* c) {
   CK(cudaStreamSynchronize(c->stream));
   for (int w = 0; w < c->Wa; ++w) CK(cudaStreamSynchronize(c->sa[w]));
   for (int w = 0; w < c->Wb; ++w) CK(cudaStreamSynchronize(c->sb[w]));
+  return SDMD_OK;
+}
+
+__global__ void lg_sum_kernel(double* const* stage, int n, size_t count, double* out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += stage[r][i];          // rank order: bitwise identical
+    out[i] = s;
+  }
+}
+
+// Collectives of the path (all on the ctx stream, in the same order on every rank): the sum of a
+// fp64 vector (partial Gram column / init Gram) and the broadcast of a fp64 vector (background
+// coefficients of an eigen-sharded frame).
+static int lg_begin(sdmd_ctx* c, const double* src, size_t count) {
+  LocalGroup* g = c->lgroup;
+  const int r = c->cfg.rank;
+  if (count > g->cap) { c->err = "local group: collective larger than its staging"; return SDMD_E_INVALID; }
+  for (int q = 0; q < g->n; ++q)          // previous collective's readers of my staging are done
+    if (g->out_pending[q]) CK(cudaStreamWaitEvent(c->stream, g->ev_out[q], 0));
+  if (src) CK(cudaMemcpyAsync(g->stage[r], src, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaEventRecord(g->ev_in[r], c->stream));
+  g->barrier();                            // every rank's ev_in is recorded
+  return SDMD_OK;
+}
+static int lg_end(sdmd_ctx* c) {
+  LocalGroup* g = c->lgroup;
+  CK(cudaEventRecord(g->ev_out[c->cfg.rank], c->stream));
+  g->barrier();                            // every rank's ev_out is recorded
+  for (int q = 0; q < g->n; ++q) g->out_pending[q] = true;
+  return SDMD_OK;
+}
+static int coll_allreduce(sdmd_ctx* c, double* buf, size_t count) {
+  if (c->lgroup) {
+    LocalGroup* g = c->lgroup;
+    int st = lg_begin(c, buf, count);
+    if (st) return st;
+    for (int q = 0; q < g->n; ++q) CK(cudaStreamWaitEvent(c->stream, g->ev_in[q], 0));
+    lg_sum_kernel<<<64, 256, 0, c->stream>>>(g->d_stage, g->n, count, buf);
+    CK(cudaGetLastError());
+    c->launches += 1;
+    return lg_end(c);
+  }
+  NcclApi* api = nccl_api();
+  if (!api || api->AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
+    c->err = "ncclAllReduce failed";
+    return SDMD_E_NCCL;
+  }
+  return SDMD_OK;
+}
+static int coll_broadcast(sdmd_ctx* c, double* buf, size_t count, int root) {
+  if (c->lgroup) {
+    LocalGroup* g = c->lgroup;
+    int st = lg_begin(c, c->cfg.rank == root ? buf : nullptr, count);
+    if (st) return st;
+    if (c->cfg.rank != root) {
+      CK(cudaStreamWaitEvent(c->stream, g->ev_in[root], 0));
+      CK(cudaMemcpyAsync(buf, g->stage[root], count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return lg_end(c);
+  }
+  NcclApi* api = nccl_api();
+  if (!api || api->Broadcast(buf, buf, count, ncclFloat64, root, c->comm, c->stream) != ncclSuccess) {
+    c->err = "ncclBroadcast failed";
+    return SDMD_E_NCCL;
+  }
   return SDMD_OK;
 }
 
@@ -480,7 +578,27 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
         cudaEventCreateWithFlags(&c->ev_a[i], cudaEventDisableTiming) != cudaSuccess)
       return bail(SDMD_E_CUDA);
   }
-  if (c->cfg.nranks > 1) {
+  const char* elg = std::getenv("SDMD_LOCAL_GROUP");
+  if (c->cfg.nranks > 1 && elg && elg[0] == '1') {       // TEST backend (see LocalGroup)
+    if (c->cfg.nranks > 8) return bail(SDMD_E_INVALID);
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    const std::string key((const char*)c->cfg.nccl_uid, 128);
+    LocalGroup*& g = g_groups[key];
+    if (!g) {
+      g = new LocalGroup();
+      g->n = c->cfg.nranks;
+      g->cap = (size_t)(m + 1) * (m + 1) + (size_t)kMaxBatch * (m + 1) + 2 * (size_t)m;
+      for (int q = 0; q < g->n; ++q) {
+        if (cudaMalloc(&g->stage[q], g->cap * sizeof(double)) != cudaSuccess) return bail(SDMD_E_OOM);
+        cudaEventCreateWithFlags(&g->ev_in[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&g->ev_out[q], cudaEventDisableTiming);
+      }
+      if (cudaMalloc(&g->d_stage, 8 * sizeof(double*)) != cudaSuccess) return bail(SDMD_E_OOM);
+      cudaMemcpy(g->d_stage, g->stage, 8 * sizeof(double*), cudaMemcpyHostToDevice);
+    }
+    ++g->refs;
+    c->lgroup = g;
+  } else if (c->cfg.nranks > 1) {
     NcclApi* api = nccl_api();
     if (!api) { c->err = "libnccl.so.2 not loadable"; return bail(SDMD_E_NCCL); }
     ncclUniqueId id;
@@ -507,6 +625,21 @@ int sdmd_destroy(sdmd_ctx* c) {
   if (c->comm) {
     NcclApi* api = nccl_api();
     if (api) api->CommDestroy(c->comm);
+  }
+  if (c->lgroup) {
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    LocalGroup* g = c->lgroup;
+    if (--g->refs == 0) {
+      for (auto it = g_groups.begin(); it != g_groups.end(); ++it)
+        if (it->second == g) { g_groups.erase(it); break; }
+      for (int q = 0; q < g->n; ++q) {
+        cudaFree(g->stage[q]);
+        cudaEventDestroy(g->ev_in[q]);
+        cudaEventDestroy(g->ev_out[q]);
+      }
+      cudaFree(g->d_stage);
+      delete g;
+    }
   }
   destroy_timing(c);
   for (int i = 0; i < kEvents; ++i) {
@@ -639,12 +772,8 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     if (owns(c, fb)) CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fb) % kEvents], 0));
     if (c->P > 1) {                               // c_fb from the rank that solved frame fb
       double2* cb = c->cbuf + (fb % c->NC) * m;
-      NcclApi* api = nccl_api();
-      if (!api || api->Broadcast(cb, cb, (size_t)2 * m, ncclFloat64, (int)(fb % c->P), c->comm,
-                                 c->stream) != ncclSuccess) {
-        c->err = "ncclBroadcast (background coefficients) failed";
-        return SDMD_E_NCCL;
-      }
+      const int st_ = coll_broadcast(c, (double*)cb, (size_t)2 * m, (int)(fb % c->P));
+      if (st_) return st_;
     }
   }
   if (c->timing) {
@@ -684,11 +813,8 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     }
     if (c->cfg.nranks > 1) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      NcclApi* api = nccl_api();
-      if (!api || api->AllReduce(c->gout, c->gout, nd, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
-        c->err = "ncclAllReduce failed";
-        return SDMD_E_NCCL;
-      }
+      const int st_ = coll_allreduce(c, c->gout, nd);
+      if (st_) return st_;
       CK(launch_commit(p, c->stream));
       c->launches += 1;
     }
@@ -707,11 +833,8 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     }
     if (c->cfg.nranks > 1) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      NcclApi* api = nccl_api();
-      if (!api || api->AllReduce(c->gout, c->gout, nd, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
-        c->err = "ncclAllReduce failed";
-        return SDMD_E_NCCL;
-      }
+      const int st_ = coll_allreduce(c, c->gout, nd);
+      if (st_) return st_;
       K1Params q{};
       q.gout = c->gout; q.nd = nd; q.m = m; q.f_new = t; q.ghist = c->ghist; q.NH = c->NH; q.st = c->dst;
       CK(launch_commit(q, c->stream));
@@ -798,11 +921,8 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
   if (c->cfg.nranks > 1) {
     const size_t cnt = (size_t)k * (m + 1);
     CK(cudaMemcpyAsync(c->gpart, c->gout, (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    NcclApi* api = nccl_api();
-    if (!api || api->AllReduce(c->gout, c->gout, cnt, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
-      c->err = "ncclAllReduce (batch) failed";
-      return SDMD_E_NCCL;
-    }
+    const int st_ = coll_allreduce(c, c->gout, cnt);
+    if (st_) return st_;
     CK(launch_commit_batch(p, c->stream));
     c->launches += 1;
   }
@@ -887,11 +1007,8 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   CK(launch_init_gram(c->ring, c->ld, c->cfg.dtype, c->cfg.n_local, k, c->Gtmp, c->init_work, c->stream));
   c->launches += 2;
   if (c->cfg.nranks > 1) {
-    NcclApi* api = nccl_api();
-    if (!api || api->AllReduce(c->Gtmp, c->Gtmp, (size_t)k * k, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
-      c->err = "ncclAllReduce (init) failed";
-      return SDMD_E_NCCL;
-    }
+    const int st_ = coll_allreduce(c, c->Gtmp, (size_t)k * k);
+    if (st_) return st_;
   }
   CK(launch_ghist_from_gram(c->Gtmp, k, c->ghist, c->NH, m, 0, c->stream));
   c->launches += 1;

@@ -904,3 +904,63 @@ def test_c3_full_size_sampled():
     gt = vs.truth_mask(fb)
     assert 2 * np.sum(mask & gt) / (mask.sum() + gt.sum()) > 0.85
     eng.close()
+
+
+# ------------------------------------------- two ranks on one GPU (SDMD_LOCAL_GROUP) ---------
+
+@pytest.mark.parametrize("eigen_shard", [1, 0])
+def test_two_ranks_one_gpu_local_group(monkeypatch, eigen_shard):
+    """The multi-rank data path on one GPU: two contexts (ranks 0 and 1, half of the rows each)
+    driven by two host threads, collectives through the in-process test group (NCCL refuses two
+    ranks on one device).  Row sharding + allreduce of g: both ranks hold the same Gram, bitwise,
+    equal to one rank's within 1e-12 (summation split only).  Eigen sharding + broadcast of c_t:
+    the background rows of the two ranks form the one-rank background; each rank's spectrum is
+    the newest frame it solved."""
+    import threading
+    from paper_1612_07875_b200 import row_partition
+    monkeypatch.setenv("SDMD_LOCAL_GROUP", "1")
+    vs = synth.VideoStream(108, 192, 1, seed=31, side=24)
+    m, T = 24, 61
+    uid = bytes((7 * i + eigen_shard) % 256 for i in range(128))
+    res, errs = {}, []
+
+    def run(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                b, e = row_partition(vs.n, 2, rank)
+                eng = Eng(e - b, m, dtype="f32", background=True, workers=2, rank=rank, nranks=2,
+                          row_begin=b, n_global=vs.n, nccl_uid=uid, eigen_shard=eigen_shard)
+                for t in range(T):
+                    eng.push(vs.frame(t, "cuda:0", (b, e)))
+                eng.sync()
+                res[rank] = (eng.gram(), eng.background(), eng.spectrum(), eng.info())
+                eng.close()
+        except Exception as ex:                        # surfaced below
+            errs.append(repr(ex))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=300)
+    assert not errs, errs
+    one = Eng(vs.n, m, dtype="f32", background=True, workers=2, lag=res[0][3]["lag"])
+    for t in range(T):
+        one.push(vs.frame(t, "cuda:0"))
+    one.sync()
+    G1 = one.gram()
+    low1, sp1, mask1, fb1 = one.background()
+    spec1 = one.spectrum()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert normwise(res[0][0], G1) < 1e-12
+    low = np.concatenate([res[0][1][0], res[1][1][0]])
+    assert res[0][1][3] == res[1][1][3] == fb1
+    assert np.max(np.abs(low - low1)) < 1e-4 * np.max(np.abs(low1))
+    if eigen_shard:
+        assert res[0][2]["frame"] == T - 1 and res[1][2]["frame"] == T - 2   # T-1 = 60 is even
+    else:
+        assert res[0][2]["frame"] == res[1][2]["frame"] == T - 1
+        assert np.array_equal(res[0][2]["lam"], res[1][2]["lam"])
+    r0 = res[0][2] if res[0][2]["frame"] == T - 1 else res[1][2]
+    assert match(r0["lam"], spec1["lam"])[0] < 1e-8 * max(1.0, np.abs(spec1["lam"]).max())
+    one.close()
