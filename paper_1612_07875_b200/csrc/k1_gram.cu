@@ -56,6 +56,9 @@ namespace sdmd {
 #ifndef K1V2_NORC
 #define K1V2_NORC 0       // v2 A/B: 1 = always accumulate the complex background (no real fast path)
 #endif
+#ifndef K1V2_PF
+#define K1V2_PF 0         // v2: L2 bulk-prefetch distance in tiles (0 = off)
+#endif
 #ifndef K1V2_DBG
 #define K1V2_DBG 0        // v2 experiments: 1 = skip the background reduction, 2 = skip its FMAs
 #endif
@@ -690,6 +693,16 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
   long long it = 0;
   if (tile < NT) load_batch(za, 0, tile);
   for (; tile < NT; tile += gridDim.x, ++it) {
+    if (K1V2_PF > 0) {
+      // L2 prefetch of this warp's column chunks K1V2_PF tiles ahead (one bulk prefetch of the
+      // 16 x 32 B chunk per column, issued by lane q for column q): the loads of that tile then
+      // hit L2, so fewer registers' worth of bytes in flight sustain the same bandwidth
+      const long long pt = tile + (long long)K1V2_PF * gridDim.x;
+      if (pt < NT && lane < NQ) {
+        const VT* a = ringv + pt * 32 + my_off[lane];
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "n"(32 * (int)sizeof(VT)) : "memory");
+      }
+    }
     double xd[EPV];
     {
       const VT xv = __ldg(ringv + xoff + tile * 32 + lane);
