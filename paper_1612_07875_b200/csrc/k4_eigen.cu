@@ -344,12 +344,53 @@ static __device__ __forceinline__ MsRefl ms_reflector(double P, double Q, double
   return f;
 }
 
+#ifndef K4_MS_PIPE
+#define K4_MS_PIPE 160     // r >= this: shifts computed one sweep ahead by warp 0 while warps 2..15
+                           // chase (0 = never).  Measured QR cycles pipelined vs in place:
+                           // r = 100 10.8 M vs 9.4 M, r = 128 12.9 M vs 12.9 M, r = 200 19.9 M vs
+                           // 22.3 M (more, staler sweeps; the shift work leaves the critical path)
+#endif
 struct MsShared {
   double dense[MS_SMALL * MS_DLD]; // dense copy of the shift block (ns x ns) or of a tail block
   double st[MS_NB], sd[MS_NB];
+  double stn[MS_NB], sdn[MS_NB];   // pipelined shifts for the next sweep
   double2 sw[MS_SMALL];
-  int l, nbe, fail;
+  int l, nbe, fail, nbn;
 };
+
+// eigenvalues of the dense ns x ns copy (one warp) paired into double shifts (trace, det)
+static __device__ int ms_pair_shifts(MsShared* sh, int ns, double* st, double* sd, int lane) {
+  int its_s = 0;
+  const int rc = qr_block(DenseAcc{sh->dense, MS_DLD}, 0, ns - 1, sh->sw, lane, &its_s, nullptr);
+  __syncwarp();
+  int nb = 0;
+  if (rc == 0) {
+    double rl = 0.0;
+    bool have_real = false;
+    for (int i = 0; i < ns && nb < MS_NB; ++i) {
+      const double2 e = sh->sw[i];
+      if (e.y != 0.0) {                            // conjugate pair (i, i+1)
+        if (lane == 0) { st[nb] = 2.0 * e.x; sd[nb] = e.x * e.x + e.y * e.y; }
+        ++nb;
+        ++i;
+      } else if (have_real) {
+        if (lane == 0) { st[nb] = rl + e.x; sd[nb] = rl * e.x; }
+        ++nb;
+        have_real = false;
+      } else {
+        rl = e.x;
+        have_real = true;
+      }
+    }
+  }
+  __syncwarp();
+  return nb;
+}
+
+static __device__ __forceinline__ void ms_chase_sync(bool pipe) {
+  if (pipe) asm volatile("bar.sync 1, %0;" ::"n"(K4_THREADS - 64) : "memory");   // warps 2..15
+  else __syncthreads();
+}
 
 template <class Acc>
 static __device__ void ms_two_roots(Acc a, int nn, double2* wv) {
@@ -393,6 +434,7 @@ static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, 
     an = wsum(an);
   }
   int nn = n - 1, stall = 0, status = 0;
+  bool pend = false;                                 // pipelined shifts available (sh->stn/sdn)
   while (nn >= 0) {
     // ---- deflation at the bottom of the active block (warp 0)
     if (warp == 0) {
@@ -444,53 +486,53 @@ static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, 
       if (status) return status;
       continue;
     }
-    // ---- shifts: eigenvalues of the trailing ns x ns block (dense copy, warp 0)
+    // ---- shifts: eigenvalues of the trailing ns x ns block (dense copy, warp 0).  Pipelined
+    // (K4_MS_PIPE): after the first sweep, the shifts of sweep s come from the trailing block at
+    // the START of sweep s-1, computed by warp 0 while warps 2..15 chase sweep s-1 (one sweep
+    // stale: more sweeps, but the shift computation leaves the critical path; the numpy model
+    // scripts/proto/qr_aed.py counts +25-38 % sweeps).  The first sweep computes them in place.
     int ns = 2 * MS_NB;
     if (ns > ((nact - 2) & ~1)) ns = (nact - 2) & ~1;
     const long long t_sh0 = clock64();
-    ms_copy_block(a, nn - ns + 1, ns, sh->dense, tid);
-    __syncthreads();
-    if (warp == 0) {
-      int its_s = 0;
-      const int rc = qr_block(DenseAcc{sh->dense, MS_DLD}, 0, ns - 1, sh->sw, lane, &its_s, nullptr);
-      __syncwarp();
-      if (lane == 0) {
-        int nb = 0;
-        if (rc == 0) {
-          double rl = 0.0;
-          bool have_real = false;
-          for (int i = 0; i < ns && nb < MS_NB; ++i) {
-            const double2 e = sh->sw[i];
-            if (e.y != 0.0) {                            // conjugate pair (i, i+1)
-              sh->st[nb] = 2.0 * e.x;
-              sh->sd[nb] = e.x * e.x + e.y * e.y;
-              ++nb;
-              ++i;
-            } else if (have_real) {
-              sh->st[nb] = rl + e.x;
-              sh->sd[nb] = rl * e.x;
-              ++nb;
-              have_real = false;
-            } else {
-              rl = e.x;
-              have_real = true;
-            }
-          }
+    const bool pipe = K4_MS_PIPE > 0 && n >= K4_MS_PIPE && pend;   // uniform
+    if (!pipe) {
+      ms_copy_block(a, nn - ns + 1, ns, sh->dense, tid);
+      __syncthreads();
+      if (warp == 0) {
+        const int nb = ms_pair_shifts(sh, ns, sh->st, sh->sd, lane);
+        if (lane == 0) {
+          sh->nbe = nb;
+          for (int q = 0; q < nb; ++q) { sh->stn[q] = sh->st[q]; sh->sdn[q] = sh->sd[q]; }
+          sh->nbn = nb;                                   // sweep s+1 reuses them (same state)
         }
+      }
+    } else {
+      if (tid == 0) {
+        const int nb = sh->nbn < MS_NB - 1 ? sh->nbn : MS_NB - 1;   // 7 bulges on warps 2..15
+        for (int q = 0; q < nb; ++q) { sh->st[q] = sh->stn[q]; sh->sd[q] = sh->sdn[q]; }
         sh->nbe = nb;
       }
+      ms_copy_block(a, nn - ns + 1, ns, sh->dense, tid);   // snapshot for sweep s+1's shifts
     }
     __syncthreads();
     if (tid == 0 && shift_cycles) *shift_cycles += clock64() - t_sh0;
     const int nbe = sh->nbe;
-    if (nbe == 0) { stall = MS_STALL; continue; }
-    // ---- chase nbe bulges in lockstep, bulge b on warps 2b (half 0) and 2b+1 (half 1)
-    const int b = warp >> 1, half = warp & 1;
+    if (nbe == 0) { stall = MS_STALL; pend = false; continue; }
+    if (K4_MS_PIPE > 0 && n >= K4_MS_PIPE) pend = true;
+    if (pipe && warp == 0) {                                 // next sweep's shifts, concurrently
+      const int nb = ms_pair_shifts(sh, ns, sh->stn, sh->sdn, lane);
+      if (lane == 0) sh->nbn = nb;
+    }
+    // ---- chase nbe bulges in lockstep, bulge b on warps 2b (half 0) and 2b+1 (half 1); when
+    // pipelined, on warps 2b+2 and 2b+3 with a named barrier over those 14 warps
+    const int bw = pipe ? warp - 2 : warp;
+    const int b = bw >= 0 ? bw >> 1 : MS_NB, half = warp & 1;
     const double st_b = (b < nbe) ? sh->st[b] : 0.0, sd_b = (b < nbe) ? sh->sd[b] : 0.0;
     const int G = (nn - 1 - l) + MS_SPACING * (nbe - 1);
+    const bool chaser = !pipe || warp >= 2;
     MsRefl rf{};                       // reflector of the current step (both halves)
     long long t_ab = 0, t_c = 0;
-    for (int g = 0; g <= G; ++g) {
+    for (int g = 0; chaser && g <= G; ++g) {
       const long long t0 = clock64();
       const int k = l + g - MS_SPACING * b;
       const bool act = (b < nbe) && (k >= l && k <= nn - 1);
@@ -518,7 +560,7 @@ static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, 
           }
         }
       }
-      __syncthreads();
+      ms_chase_sync(pipe);
       const long long t1 = clock64();
       if (act && rf.on) {
         // (C) columns k..k+2, rows l..min(nn, k+3); bulge column k-1
@@ -537,11 +579,12 @@ static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, 
           ri[k] = c0 - pc;
         }
       }
-      __syncthreads();
+      ms_chase_sync(pipe);
       t_ab += t1 - t0;
       t_c += clock64() - t1;
     }
-    if (tid == 0 && chase_cycles) { chase_cycles[0] += t_ab; chase_cycles[1] += t_c; }
+    __syncthreads();                                           // chase and shift warps join
+    if (tid == (pipe ? 64 : 0) && chase_cycles) { chase_cycles[0] += t_ab; chase_cycles[1] += t_c; }
     if (tid == 0) { *total_its += 1; if (cnt) { cnt[1] += G + 1; cnt[3] += 1; } }
     ++stall;
   }
