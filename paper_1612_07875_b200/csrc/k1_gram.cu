@@ -33,9 +33,6 @@ namespace sdmd {
 #ifndef K1_LAGR
 #define K1_LAGR 1         // tiles between publishing and reducing
 #endif
-#ifndef K1_BG_LDG
-#define K1_BG_LDG 1       // background path: 1 = register (LDG) streaming, 0 = bulk-copy rings
-#endif
 #ifndef K1_CB32
 #define K1_CB32 4         // fp32 background LDG path: columns (2 LDG.128 each) in flight per lane
 #endif
@@ -62,9 +59,6 @@ namespace sdmd {
 #ifndef K1V2_DBG
 #define K1V2_DBG 0        // v2 experiments: 1 = skip the background reduction, 2 = skip its FMAs
 #endif
-#ifndef K1_DEPTH32
-#define K1_DEPTH32 8      // per-warp bulk-copy ring depth (fp32 chunks of 1 KB)
-#endif
 constexpr int K1_THREADS = 512;
 constexpr int K1_WARPS = K1_THREADS / 32;
 constexpr int K1_MAXU = kMaxM + kMaxLag;          // union columns: m + lag
@@ -88,7 +82,23 @@ static __device__ __forceinline__ void k1_mbar_init(unsigned long long* bar, uns
 static __device__ __forceinline__ void k1_mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(k1_smem_u32(bar)) : "memory");
 }
+#ifndef K1_MBAR_HINT
+#define K1_MBAR_HINT 0    // ns: suspend-time hint of the mbarrier waits (0 = the default policy)
+#endif
 static __device__ __forceinline__ void k1_mbar_wait(unsigned long long* bar, unsigned parity) {
+#if K1_MBAR_HINT > 0
+  // the waiting warp is suspended (not spinning on issue slots) until the phase completes or the
+  // hint expires
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "K1_WAIT:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra K1_DONE;\n\t"
+      "bra K1_WAIT;\n"
+      "K1_DONE:\n\t}" ::"r"(k1_smem_u32(bar)),
+      "r"(parity), "n"(K1_MBAR_HINT)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "K1_WAIT:\n\t"
@@ -98,6 +108,7 @@ static __device__ __forceinline__ void k1_mbar_wait(unsigned long long* bar, uns
       "K1_DONE:\n\t}" ::"r"(k1_smem_u32(bar)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 
@@ -164,37 +175,11 @@ template <> struct BgAcc<double> {
   __device__ __forceinline__ C2 get(int e) const { return v[e]; }
 };
 
-static __device__ __forceinline__ void k1_mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(k1_smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-// try_wait spin without the release/acquire sem of k1_mbar_wait (the bulk copy's complete_tx
-// makes the bytes visible to the waiting threads)
-static __device__ __forceinline__ void k1_mbar_wait_tx(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "K1_WAIT_TX:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra K1_DONE_TX;\n\t"
-      "bra K1_WAIT_TX;\n"
-      "K1_DONE_TX:\n\t}" ::"r"(k1_smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-static __device__ __forceinline__ void k1_bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                                   unsigned long long* bar, unsigned long long pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;" ::"r"(k1_smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(k1_smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-
 template <typename T, bool BG, int NQ>
 // One 512-thread CTA per SM (<= 128 registers).  Without the background: register streaming,
-// 16 warps x CB columns x 2 LDG.128 per lane in flight.  With the background: per-warp rings of
-// DEPTH column chunks filled by one-instruction bulk copies (cp.async.bulk, mbarrier complete_tx)
-// so that address generation costs one lane per 1 KB instead of every lane per 16 bytes.
+// 16 warps x CB columns x 2 LDG.128 per lane in flight, with or without the background.  (A
+// bulk-copy ring variant of the background path measured slower: its 210 KB of shared memory
+// starves L1 and couples the warps — removed.)
 __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p) {
   using VT = typename VecOf<T>::type;
   using BT2 = typename BgAcc<T>::C2;
@@ -208,18 +193,13 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   constexpr int NSLOT = K1_NSLOT;
   constexpr int LAGR = K1_LAGR;
   static_assert(LAGR >= 1 && LAGR < NSLOT, "reduction lag must leave a free slot");
-  // BG: per-warp ring of DEPTH chunks (one chunk = the warp's 256 rows of one column, 1 KB fp32 /
-  // 2 KB fp64), in flight across tile boundaries
-  constexpr int CHUNK = kSuperTile * (int)sizeof(T);
-  constexpr int DEPTH = (BG && !K1_BG_LDG) ? (sizeof(T) == 4 ? K1_DEPTH32 : 2) : 0;
+
   __shared__ __align__(16) CW cw_s[BG ? K1_WARPS : 1][BG ? MAXQ : 1];   // coefficient per warp column
   __shared__ long long col_off[K1_WARPS][MAXQ];   // ring offset (slot * ld) of each warp column
   __shared__ int col_kd[K1_WARPS][MAXQ];          // Gram-column index, or -1
   extern __shared__ __align__(128) unsigned char red_raw[];
-  unsigned char* zring = red_raw;                                       // [K1_WARPS][DEPTH][CHUNK]
-  BT2* red = reinterpret_cast<BT2*>(red_raw + K1_WARPS * DEPTH * CHUNK);
+  BT2* red = reinterpret_cast<BT2*>(red_raw);
   __shared__ unsigned long long fullb[NSLOT], emptyb[NSLOT];
-  __shared__ unsigned long long zbar[DEPTH > 0 ? K1_WARPS * DEPTH : 1];
   __shared__ int am_last;
 
   if (*(volatile int*)&p.st->status != 0) return;   // stream poisoned: discard (header contract)
@@ -241,7 +221,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
   if (BG) {
     if (tid == 0)
       for (int s = 0; s < NSLOT; ++s) { k1_mbar_init(&fullb[s], K1_WARPS); k1_mbar_init(&emptyb[s], K1_WARPS); }
-    if (tid < K1_WARPS * DEPTH) k1_mbar_init(&zbar[tid], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -353,7 +332,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       for (int q = LAGR; q > 0; --q) xq[q] = xq[q - 1];
       xq[0] = (lane < 16) ? __ldcs(bg_col + row0 + rt_red) : (T)0;
     };
-#if K1_BG_LDG
     // ---- background, register streaming: CB columns (VPL LDG.128 each) in flight per lane
     for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
       const long long row0 = tile * kSuperTile;
@@ -398,82 +376,6 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1_gram_kernel(const K1Params p
       }
       tile_end(bacc);
     }
-#else
-    // ---- background, per-warp bulk-copy rings: s = (local tile) * cnt + q
-    const long long ntl = (NT > blockIdx.x) ? (NT - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    const long long S = ntl * cnt;
-    unsigned char* wring = zring + warp * (DEPTH * CHUNK);
-    unsigned long long* wbar = zbar + warp * DEPTH;
-    unsigned long long pol = 0;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const long long tstride = (long long)gridDim.x * kSuperTile;
-    long long s_iss = 0;                    // next chunk to issue
-    int q_iss = 0;                          // its column
-    int i_slot = 0;                         // its ring slot
-    const T* tile_iss = ring + (long long)blockIdx.x * kSuperTile;   // its tile's row 0
-    auto issue = [&]() {
-      if (s_iss < S) {
-        if (lane == 0) {
-          k1_mbar_expect_tx(wbar + i_slot, CHUNK);
-          k1_bulk_g2s(wring + i_slot * CHUNK, tile_iss + col_off[warp][q_iss], CHUNK, wbar + i_slot, pol);
-        }
-        if (++q_iss == cnt) { q_iss = 0; tile_iss += tstride; }
-        if (++i_slot == DEPTH) i_slot = 0;
-      }
-      ++s_iss;
-    };
-#pragma unroll 1
-    for (int d = 0; d < DEPTH; ++d) issue();
-    VT xn[VPL];                             // x_t of the next tile (prefetched one tile ahead)
-    if (ntl > 0) {
-#pragma unroll
-      for (int v = 0; v < VPL; ++v)
-        xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + (long long)blockIdx.x * kSuperTile + v * 32 * EPV) + lane);
-    }
-    int c_slot = 0;                         // ring slot / phase of the next chunk to consume
-    unsigned c_par = 0;
-    for (long long tile = blockIdx.x; tile < NT; tile += gridDim.x, ++it) {
-      const long long row0 = tile * kSuperTile;
-      double xd[8];
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) to_double(xn[v], xd + v * EPV);
-      if (tile + gridDim.x < NT) {
-#pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          xn[v] = __ldg(reinterpret_cast<const VT*>(xslot + row0 + (long long)gridDim.x * kSuperTile + v * 32 * EPV) + lane);
-      }
-      tile_begin(row0);
-      BgAcc<T> bacc;
-      bacc.zero();
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        if (q < cnt) {
-          k1_mbar_wait_tx(wbar + c_slot, c_par);          // the chunk has landed
-          const unsigned char* src = wring + c_slot * CHUNK;
-          if (++c_slot == DEPTH) { c_slot = 0; c_par ^= 1u; }
-          VT zv[VPL];
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) zv[v] = *reinterpret_cast<const VT*>(src + v * 512 + lane * 16);
-          const CW c = cw_s[warp][q];
-          double zd[8];
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) to_double(zv[v], zd + v * EPV);
-          double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) { a0 = fma(xd[e], zd[e], a0); a1 = fma(xd[e + 1], zd[e + 1], a1); }
-          accv[q] += a0 + a1;                     // non-Gram columns are discarded at the end
-          if (!(p.dbg & 2)) bacc.add(c, reinterpret_cast<const T*>(&zv[0]));   // c = 0 outside X'_{f_bg}
-          __syncwarp();                           // every lane has read the slot: refill it
-          issue();
-        }
-      }
-      if (p.dbg & 1) {
-        if (bacc.get(0).x == 12345.f) p.mask[0] = 7;      // keep the accumulators live
-        continue;
-      }
-      tile_end(bacc);
-    }
-#endif
     // drain the last LAGR tiles
     if (!(p.dbg & 1)) {
 #pragma unroll
@@ -846,8 +748,7 @@ cudaError_t launch_k1(const K1Params& p, int dtype, int grid, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
   }
-  const int depth = (p.bg && !K1_BG_LDG) ? (dtype == 0 ? K1_DEPTH32 : 2) : 0;
-  int smem = K1_WARPS * depth * kSuperTile * es;                  // bulk-copy rings (background path)
+  int smem = 0;
   if (p.bg) smem += K1_NSLOT * K1_WARPS * 8 * (dtype == 0 ? 40 : 36) * (dtype == 0 ? (int)sizeof(float2) : (int)sizeof(double2));
   // union of the Gram window and X' of the background frame
   const int U = p.bg ? (p.nd > (int)(p.f_new - p.f_bg) + p.m ? p.nd : (int)(p.f_new - p.f_bg) + p.m) : p.nd;

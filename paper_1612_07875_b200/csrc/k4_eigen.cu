@@ -908,7 +908,7 @@ k4a_kernel(const K4Params p) {
   __shared__ double mu[kMaxM];
   __shared__ double sig[kMaxM];
   __shared__ int perm[kMaxM];
-  __shared__ int sh_r, sh_status, sh_idx, sh_its;
+  __shared__ int sh_r, sh_status;
   __shared__ long long ph[8];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -1,6 +1,6 @@
 """K2 (DMMA) timing: a0 init Gram and a12 modes on the C4 and C2 shapes, one GPU.
 
-    python scripts/k2_bench.py [--skip-c4]      (SDMD_K2=v1 selects the previous kernels)
+    python scripts/k2_bench.py [--skip-c4]
 
 Wall time of sdmd_init_window (D2D copy of the window into the ring + Gram) and of
 sdmd_get_modes (T = Y W, Φ = X'T), synchronised on both sides; kernel-only times come from the
@@ -47,7 +47,7 @@ def run(name, Zd, n, m, dtype, nc, r_max=0):
            "init_gram_flops": n * k * (k + 1),
            "modes_ms_wall": round(t_modes * 1e3, 3),
            "modes_flops": 4 * n * m * nc,
-           "k2": os.environ.get("SDMD_K2", "v2")}
+           }
     eng.close()
     print(json.dumps(res), flush=True)
 
