@@ -36,6 +36,15 @@
  *    discarded until the next sdmd_sync(), which returns the error and the rejected frame index.
  *  - One writer per ctx.  With nranks > 1, sdmd_init_window and sdmd_push_* are collective:
  *    every rank calls them in the same order (NCCL semantics).
+ *
+ * Environment (read at sdmd_create; experiment and test knobs, defaults are the measured best):
+ *    SDMD_K1_WAVES=w     Gram pass as w x SMs short CTAs instead of the persistent grid
+ *    SDMD_K1=v1          the earlier 8-rows-per-lane Gram kernel (A/B; checked by the tests)
+ *    SDMD_WARM=0         no Jacobi warm start;   SDMD_THROTTLE=0  no eigen-work flow control
+ *    SDMD_WA=n           n cluster eigen streams; SDMD_BG_NODMD=1 background pass with c = 0
+ *    SDMD_LOCAL_GROUP=1  TEST ONLY: nranks > 1 contexts of one process on one device exchange
+ *                        through an in-process group instead of NCCL (keyed by nccl_uid bytes;
+ *                        each rank driven by its own host thread)
  */
 #ifndef SDMD_H
 #define SDMD_H
