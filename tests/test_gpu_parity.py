@@ -278,6 +278,33 @@ def test_multi_mode_background_planted_closed_form(nb):
     eng.close()
 
 
+def test_single_mode_background_fp64_real_coefficients_closed_form():
+    """Alg 3 as written on planted C1b in fp64 (λ_idx = 1 is real, so K1 takes its real-coefficient
+    background path with fp64 storage): the background column equals the planted contribution
+    of the unit mode to the frame (closed form) and the oracle's background."""
+    pm = synth.planted_c1(with_unit_mode=True)
+    m, T = 16, 40
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", background=True, workers=2)
+    ref = O.StreamingDMD(m, background=True)
+    outs = {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(X[:, t])
+        if o is not None:
+            outs[t] = o
+    eng.sync()
+    low, sp, mask, fb = eng.background()
+    prods = pm.mode_products(fb)
+    l_cf = sum(v for lam, v in prods.items() if abs(lam - 1.0) < 1e-12)
+    scale = np.max(np.abs(l_cf))
+    assert np.max(np.abs(low - np.abs(l_cf))) < 1e-9 * scale
+    assert np.max(np.abs(low - outs[fb]["lowrank"])) < 1e-9 * scale
+    assert np.max(np.abs(low + sp - X[:, fb])) < 1e-12 * np.max(np.abs(X[:, fb]))
+    eng.close()
+
+
 def test_multi_mode_background_video():
     """NEXT-2 on the C3-shaped video (fp32, r ≈ m): background from the 4 slowest modes (plus a
     conjugate partner) against the oracle, same tolerances as the single-mode video test."""
