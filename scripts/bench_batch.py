@@ -100,6 +100,13 @@ def main():
         for mode in ("single", "batch", "catchup"):
             res.append(measure("C3 (no background)", pool, vs.n, 100, "f32", a.frames, a.k, mode, 16))
         del pool
+    if not a.only or a.only == "C1":
+        pm = synth.planted_c1()
+        X = pm.frames(0, 17 + 400)
+        pool = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+        for mode in ("single", "batch", "catchup"):
+            res.append(measure("C1", pool, pm.n, 16, "f64", a.frames, a.k, mode, 4))
+        del pool
     if not a.only or a.only == "C2":
         cw = synth.cylinder_wake()
         Xc = cw.frames(0, 300)
