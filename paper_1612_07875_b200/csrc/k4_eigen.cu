@@ -987,9 +987,15 @@ k4a_kernel(const K4Params p) {
       const int PB = rr_player(crank, rd, 8), QB = rr_player(7 - crank, rd, 8);
       // local column lc in [0, 2bs): global column gc(lc)
       auto gcol = [&](int lc) { return lc < bs ? PB * bs + lc : QB * bs + (lc - bs); };
-      for (int e = tid; e < 2 * bs * m; e += K4_THREADS) {
-        const int lc = e / m, i = e % m, gc = gcol(lc);
-        sA[e] = gc < m ? __ldcg(p.A + (long long)gc * m + i) : 0.0;
+      for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {     // warp per column: no divisions
+        const int gc = gcol(lc);
+        double* dst = sA + lc * m;
+        if (gc < m) {
+          const double* src = p.A + (long long)gc * m;
+          for (int i = lane; i < m; i += 32) dst[i] = __ldcg(src + i);
+        } else {
+          for (int i = lane; i < m; i += 32) dst[i] = 0.0;
+        }
       }
       __syncthreads();
       const int nsteps = (rd == 0) ? 2 * bs - 1 : bs;
@@ -1001,7 +1007,7 @@ k4a_kernel(const K4Params p) {
           bool act = false;
           if (hw < bs) {
             if (rd == 0) { P = rr_player(hw, st, 2 * bs); Q = rr_player(2 * bs - 1 - hw, st, 2 * bs); }
-            else { P = hw; Q = bs + (hw + st) % bs; }
+            else { const int hs = hw + st; P = hw; Q = bs + (hs >= bs ? hs - bs : hs); }   // hw, st < bs
             act = gcol(P) < m && gcol(Q) < m;
           }
           bool r_;
@@ -1016,9 +1022,13 @@ k4a_kernel(const K4Params p) {
         }
         __syncthreads();
       }
-      for (int e = tid; e < 2 * bs * m; e += K4_THREADS) {
-        const int lc = e / m, i = e % m, gc = gcol(lc);
-        if (gc < m) p.A[(long long)gc * m + i] = sA[e];
+      for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
+        const int gc = gcol(lc);
+        if (gc < m) {
+          const double* src = sA + lc * m;
+          double* dst = p.A + (long long)gc * m;
+          for (int i = lane; i < m; i += 32) dst[i] = src[i];
+        }
       }
       cl_sync();
     }
