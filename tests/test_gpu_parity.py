@@ -991,3 +991,50 @@ def test_two_ranks_one_gpu_local_group(monkeypatch, eigen_shard):
     r0 = res[0][2] if res[0][2]["frame"] == T - 1 else res[1][2]
     assert match(r0["lam"], spec1["lam"])[0] < 1e-8 * max(1.0, np.abs(spec1["lam"]).max())
     one.close()
+
+
+def test_two_ranks_one_gpu_init_window_and_batches(monkeypatch):
+    """The other collectives of the multi-rank path on one GPU (test group): the (m+1)² init
+    Gram allreduce of sdmd_init_window and the k(m+1) allreduce of sdmd_push_batch, with eigen
+    sharding; both ranks end with the one-rank Gram (1e-12, bitwise equal across ranks)."""
+    import threading
+    from paper_1612_07875_b200 import row_partition
+    monkeypatch.setenv("SDMD_LOCAL_GROUP", "1")
+    rng = np.random.default_rng(23)
+    n, m, k = 20011, 30, 4
+    T = m + 1 + 5 * k
+    X = rng.standard_normal((n, T)).astype(np.float32)
+    uid = bytes((11 * i + 3) % 256 for i in range(128))
+    res, errs = {}, []
+
+    def run(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                b, e = row_partition(n, 2, rank)
+                Xd = torch.from_numpy(np.ascontiguousarray(X[b:e].T)).cuda()
+                eng = Eng(e - b, m, dtype="f32", workers=2, rank=rank, nranks=2, row_begin=b,
+                          n_global=n, nccl_uid=uid, batch_max=k)
+                eng.init_window(Xd[: m + 1])
+                for t in range(m + 1, T, k):
+                    eng.push_batch(Xd[t:t + k])
+                eng.sync()
+                res[rank] = (eng.gram(), eng.spectrum())
+                eng.close()
+        except Exception as ex:
+            errs.append(repr(ex))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=300)
+    assert not errs, errs
+    ref = O.StreamingGram(m)
+    for t in range(T):
+        ref.push(X[:, t].astype(np.float64))
+    assert np.array_equal(res[0][0], res[1][0])
+    assert normwise(res[0][0], ref.G) < 1e-12
+    d = O.dmd_from_gram(ref.G)
+    last = res[0][1] if res[0][1]["frame"] == T - 1 else res[1][1]
+    assert last["frame"] == T - 1
+    assert match(last["lam"], d["lam"])[0] < 1e-7 * max(1.0, np.abs(d["lam"]).max())
