@@ -1038,3 +1038,43 @@ def test_two_ranks_one_gpu_init_window_and_batches(monkeypatch):
     last = res[0][1] if res[0][1]["frame"] == T - 1 else res[1][1]
     assert last["frame"] == T - 1
     assert match(last["lam"], d["lam"])[0] < 1e-7 * max(1.0, np.abs(d["lam"]).max())
+
+
+def test_two_ranks_one_gpu_sparse(monkeypatch):
+    """Sparse (K3) pushes on two ranks (test group): each rank holds the coefficient indices of
+    its row range; the allreduced Gram equals the one-rank sparse Gram (1e-12)."""
+    import threading
+    from paper_1612_07875_b200 import row_partition
+    monkeypatch.setenv("SDMD_LOCAL_GROUP", "1")
+    st = synth.SparseDCTStream(N=96, k_low=10.0, n_shell=40, seed=29)
+    m, T = 16, 30
+    frames = [st.frame(t) for t in range(T)]
+    uid = bytes((13 * i + 5) % 256 for i in range(128))
+    res, errs = {}, []
+
+    def run(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                b, e = row_partition(st.n, 2, rank)
+                eng = Eng(e - b, m, storage="sparse", nnz_cap=st.nnz_cap, workers=1, rank=rank,
+                          nranks=2, row_begin=b, n_global=st.n, nccl_uid=uid)
+                for idx, val in frames:
+                    sel = (idx >= b) & (idx < e)
+                    eng.push_sparse(np.ascontiguousarray(idx[sel]), np.ascontiguousarray(val[sel]))
+                eng.sync()
+                res[rank] = eng.gram()
+                eng.close()
+        except Exception as ex:
+            errs.append(repr(ex))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=300)
+    assert not errs, errs
+    ref = O.StreamingGram(m)
+    for t in range(T):
+        ref.push(st.dense(t))
+    assert np.array_equal(res[0], res[1])
+    assert normwise(res[0], ref.G) < 1e-12
