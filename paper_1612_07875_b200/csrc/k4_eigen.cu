@@ -344,6 +344,9 @@ static __device__ __forceinline__ MsRefl ms_reflector(double P, double Q, double
   return f;
 }
 
+#ifndef K4_JAC_FLAGS
+#define K4_JAC_FLAGS 1     // Jacobi rounds 1..6 synchronised by neighbour step counters, not barriers
+#endif
 #ifndef K4_MS_PIPE
 #define K4_MS_PIPE 160     // r >= this: shifts computed one sweep ahead by warp 0 while warps 2..15
                            // chase (0 = never).  Measured QR cycles pipelined vs in place:
@@ -860,7 +863,7 @@ static __device__ __forceinline__ void cl_sync() {
 // no dead predicated rows).  Returns true if the pair was rotated.
 template <int EH>
 static __device__ __forceinline__ bool jacobi_pair(double* cp, double* cq, int m, int hl, bool act,
-                                                   double tol) {
+                                                   double tol, unsigned mask = 0xffffffffu) {
   double ap[EH], aq[EH];
   double al = 0.0, be = 0.0, ga = 0.0;
 #pragma unroll
@@ -878,9 +881,9 @@ static __device__ __forceinline__ bool jacobi_pair(double* cp, double* cq, int m
   }
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) {                 // reduce within the half-warp
-    al += __shfl_xor_sync(0xffffffffu, al, o);
-    be += __shfl_xor_sync(0xffffffffu, be, o);
-    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+    al += __shfl_xor_sync(mask, al, o);
+    be += __shfl_xor_sync(mask, be, o);
+    ga += __shfl_xor_sync(mask, ga, o);
   }
   if (act && ga != 0.0 && ga * ga > tol * tol * (al * be)) {
     // t = tan θ = sign(ζ)/(|ζ| + sqrt(1+ζ²)), ζ = (β-α)/(2γ), written with one sqrt and
@@ -975,6 +978,7 @@ k4a_kernel(const K4Params p) {
   // blocks (round 0 also the pairs inside each block), so every pair of columns meets once per
   // block sweep.  Only the round boundaries need cluster barriers.
   const int bs = (m + 7) / 8;                     // block size (columns)
+  __shared__ volatile int jdone[32];
   const int ehs = m <= 64 ? 4 : m <= 112 ? 7 : m <= 160 ? 10 : m <= 208 ? 13 : kMaxM / 16;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
   constexpr int EL = kMaxM / 32;
@@ -985,6 +989,7 @@ k4a_kernel(const K4Params p) {
     int rot = 0;
     for (int rd = 0; rd < 7; ++rd) {
       const int PB = rr_player(crank, rd, 8), QB = rr_player(7 - crank, rd, 8);
+      if (tid < 32) jdone[tid] = -1;                   // per-half-warp step counters (flags mode)
       // local column lc in [0, 2bs): global column gc(lc)
       auto gcol = [&](int lc) { return lc < bs ? PB * bs + lc : QB * bs + (lc - bs); };
       for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {     // warp per column: no divisions
@@ -999,6 +1004,36 @@ k4a_kernel(const K4Params p) {
       }
       __syncthreads();
       const int nsteps = (rd == 0) ? 2 * bs - 1 : bs;
+      if (K4_JAC_FLAGS && rd > 0) {
+        // Rounds 1..6: half-warp hw keeps column P = hw and takes over column Q from half-warp
+        // hw+1 (mod bs) each step, so it only has to wait for that neighbour's previous step
+        // (a per-half-warp step counter in shared memory) instead of a CTA barrier per step.
+        const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
+        const unsigned hmask = (lane >> 4) ? 0xffff0000u : 0x0000ffffu;
+        if (hw < bs) {
+          const int nb = hw + 1 == bs ? 0 : hw + 1;
+          for (int st = 0; st < bs; ++st) {
+            if (st > 0) {
+              while (jdone[nb] < st - 1) { }
+              __threadfence_block();
+            }
+            const int hs = hw + st, P = hw, Q = bs + (hs >= bs ? hs - bs : hs);
+            const bool act = gcol(P) < m && gcol(Q) < m;
+            bool r_;
+            switch (ehs) {
+              case 4: r_ = jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
+              case 7: r_ = jacobi_pair<7>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
+              case 10: r_ = jacobi_pair<10>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
+              case 13: r_ = jacobi_pair<13>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
+              default: r_ = jacobi_pair<kMaxM / 16>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
+            }
+            if (r_) rot = 1;
+            __syncwarp(hmask);
+            if (hl == 0) { __threadfence_block(); jdone[hw] = st; }
+          }
+        }
+        __syncthreads();
+      } else
       for (int st = 0; st < nsteps; ++st) {
         {
           // one column pair per half-warp (bs <= 32 pairs, 32 half-warps): 16 lanes x <=16 rows
@@ -1033,7 +1068,9 @@ k4a_kernel(const K4Params p) {
       cl_sync();
     }
     ++sweeps;
-    if (rot && lane == 0) atomicOr(p.flags + sweep, 1);
+    // rotations happen per half-warp: vote over the whole warp (lane 0 alone would miss a sweep
+    // whose only rotations were on the upper half-warp)
+    if (__any_sync(0xffffffffu, rot) && lane == 0) atomicOr(p.flags + sweep, 1);
     cl_sync();
     if (*(volatile int*)(p.flags + sweep) == 0) { converged = true; break; }
   }
