@@ -307,7 +307,10 @@ static __device__ int qr_block(Acc a, int lo, int hi, double2* wv, int lane, int
 // back to the single-bulge qr_block.  (Golub–Van Loan §7.5; small-bulge multishift idea of
 // Braman–Byers–Mathias; no aggressive early deflation.)
 constexpr int MS_NB = 8;           // bulges per sweep (2 warps each)
-constexpr int MS_SMALL = 32;       // blocks up to this size use the single-bulge iteration
+#ifndef K4_MS_SMALL
+#define K4_MS_SMALL 32
+#endif
+constexpr int MS_SMALL = K4_MS_SMALL;   // blocks up to this size use the single-bulge iteration
 constexpr int MS_STALL = 30;       // sweeps without deflation before falling back
 constexpr int MS_SPACING = 4;
 constexpr int MS_DLD = MS_SMALL + 1;   // leading dimension of the dense small-block copy
