@@ -125,6 +125,47 @@ def test_gram_stream_ragged(dtype, n):
     eng.close()
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n", [1, 5, 31, 33, 129])
+def test_gram_stream_tiny_n(dtype, n):
+    """Fewer rows than one warp / one tile; n = 1 makes every Gram entry a plain product."""
+    rng = np.random.default_rng(1000 + n)
+    m, T = 12, 20
+    npdt = np.float32 if dtype == "f32" else np.float64
+    X = rng.standard_normal((n, T)).astype(npdt)
+    Xd = dev_cols(X, npdt)
+    eng = Eng(n, m, dtype=dtype, dmd=False, workers=1)
+    sg = O.StreamingGram(m)
+    for t in range(T):
+        eng.push(Xd[t])
+        sg.push(X[:, t])
+    eng.sync()
+    assert normwise(eng.gram(), sg.G) < 1e-12
+    eng.close()
+
+
+def test_dmd_fewer_rows_than_window():
+    """n = 6 < m = 16: the window Gram has rank 4 (two planted complex pairs); the truncation must
+    find r = 4 and the eigenvalues must be the planted ones (closed form) and the oracle's."""
+    pairs = [(np.exp(1j * np.pi / 8), np.exp(0.3j)), (0.99 * np.exp(1j * np.pi / 5), 0.5 * np.exp(1.1j))]
+    pm = synth.PlantedModes(n=6, pairs=pairs, reals=[], seed=3)
+    m, T = 16, 40
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=2)
+    ref = O.StreamingDMD(m, background=False)
+    for t in range(T):
+        eng.push(Xd[t])
+        out = ref.push(X[:, t])
+    eng.sync()
+    sp = eng.spectrum()
+    assert sp["r"] == out["r"] == 4 and sp["frame"] == T - 1
+    e_cf, _ = match(sp["lam"], pm.lambdas)
+    e_or, _ = match(sp["lam"], out["lam"])
+    assert e_cf < 1e-9 and e_or < 1e-9, (e_cf, e_or)
+    eng.close()
+
+
 def test_host_input_and_zero_copy_slot():
     rng = np.random.default_rng(1)
     n, m, T = 5000, 6, 12
