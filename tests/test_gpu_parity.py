@@ -166,6 +166,31 @@ def test_dmd_fewer_rows_than_window():
     eng.close()
 
 
+@pytest.mark.parametrize("which", [0, 1, 2])
+@pytest.mark.parametrize("m", [2, 3])
+def test_minimum_window_planted_spectra(which, m):
+    """The smallest windows the ABI accepts (m = 2, 3) on SPEC.md's planted spectra: the
+    eigenvalues are the planted ones wherever the window holds the full rank."""
+    pm = synth.planted_spec(which)
+    T = 12
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=1)
+    ref = O.StreamingDMD(m, background=False)
+    for t in range(T):
+        eng.push(Xd[t])
+        out = ref.push(X[:, t])
+    eng.sync()
+    sp = eng.spectrum()
+    assert sp["r"] == out["r"] and sp["frame"] == T - 1
+    e_or, _ = match(sp["lam"], out["lam"])
+    assert e_or < 1e-9, e_or
+    if out["r"] == len(pm.lambdas):
+        e_cf, _ = match(sp["lam"], pm.lambdas)
+        assert e_cf < 1e-9, e_cf
+    eng.close()
+
+
 def test_host_input_and_zero_copy_slot():
     rng = np.random.default_rng(1)
     n, m, T = 5000, 6, 12
