@@ -952,6 +952,38 @@ def test_empty_sparse_frames():
     eng.close()
 
 
+def test_sparse_fully_dense_frames_and_rejected_pushes():
+    """Edge cases of the sparse ingest: frames with nnz = n = nnz_cap (every coefficient nonzero,
+    the maximum size) match the dense oracle; pushes that break the contract (nnz > nnz_cap,
+    indices not strictly ascending, out of range) raise and leave the stream unchanged."""
+    from paper_1612_07875_b200 import SDMDError
+    rng = np.random.default_rng(77)
+    n, m, T = 300, 8, 20
+    X = rng.standard_normal((n, T))
+    eng = Eng(n, m, storage="sparse", nnz_cap=n, workers=1)
+    ref = O.StreamingGram(m)
+    all_idx = np.arange(n, dtype=np.int32)
+    bad = [(np.arange(n + 1, dtype=np.int32) % n, np.ones(n + 1)),            # nnz > nnz_cap
+           (np.array([5, 3], dtype=np.int32), np.ones(2)),                     # descending
+           (np.array([4, 4], dtype=np.int32), np.ones(2)),                     # duplicate
+           (np.array([0, n], dtype=np.int32), np.ones(2))]                     # out of range
+    for t in range(T):
+        if t in (4, 13):
+            for idx, val in bad:
+                with pytest.raises(SDMDError):
+                    eng.push_sparse(idx, val)
+        eng.push_sparse(all_idx, np.ascontiguousarray(X[:, t]))
+        ref.push(X[:, t])
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    d = O.dmd_from_gram(ref.G)
+    sp = eng.spectrum()
+    assert sp["r"] == d["r"] and sp["frame"] == T - 1
+    e_or, _ = match(sp["lam"], d["lam"])
+    assert e_or < 1e-9, e_or
+    eng.close()
+
+
 def test_constant_stream_fixed_point():
     """S:346, S:353, S:377 on the device: a constant video has σ₁ = √m‖x‖, r = 1, λ_idx = 1 and
     an all-background foreground (sparse ≈ 0, empty mask)."""
