@@ -181,7 +181,11 @@ int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
 
 /* Push one sparse snapshot in an orthonormal coefficient basis (§3.5): nnz pairs,
  * idx strictly ascending in [row_begin, row_begin + n_local) (int32), val fp64.  nnz <= nnz_cap.
- * The Gram column uses sparse–sparse inner products; nothing is densified in HBM. */
+ * The Gram column uses sparse–sparse inner products; nothing is densified in HBM.
+ * Errors: nnz > nnz_cap, or (where = SDMD_HOST) indices not strictly ascending / out of range ->
+ * SDMD_E_INVALID, nothing queued.  Device-resident indices are checked on the device: a violation
+ * rejects the frame like a non-finite one (nothing scattered; the next sdmd_sync returns
+ * SDMD_E_NONFINITE with failed_frame = this frame, consistently on every rank). */
 int sdmd_push_sparse(sdmd_ctx* ctx, int32_t nnz, const int32_t* idx, const double* val,
                      int where);
 

@@ -65,6 +65,10 @@ __global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
   const int* ix = p.idx + (long long)sl * p.nnz_cap;
   __syncthreads();
   for (int e = threadIdx.x; e < nn; e += K3_THREADS) p.scratch[ix[e] - p.row_begin] = 0.0;
+  // a device-pushed frame whose indices failed the check (nnz recorded as -1, nothing scattered):
+  // a NaN self inner product, so that the commit rejects the frame — after the allreduce when
+  // rows are sharded, i.e. on every rank alike
+  if (nn < 0 && threadIdx.x == 0) p.gout[p.nd - 1] = __longlong_as_double(0x7ff8000000000000LL);
   if (threadIdx.x == 0) p.st->k3_done = 0;
   if (p.do_commit) {
     __syncthreads();
@@ -78,6 +82,28 @@ cudaError_t launch_k3(const K3Params& p, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   dim3 grid(p.chunks, p.nd);
   k3_dot_kernel<<<grid, K3_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+// Record the nonzero count of a device-pushed sparse frame after checking its indices on the
+// device (the host cannot see them): strictly ascending and inside [lo, hi).  A violation records
+// nnz = -1, which makes the scatter, gather and clear loops empty (no out-of-range access) and the
+// Gram pass reject the frame (see k3_dot_kernel).
+__global__ void __launch_bounds__(256) sparse_nnz_checked_kernel(const int* __restrict__ idx, int nnz,
+                                                                 long long lo, long long hi,
+                                                                 int* __restrict__ nnz_slot) {
+  int bad = 0;
+  for (int e = threadIdx.x; e < nnz; e += blockDim.x) {
+    const int i = idx[e];
+    bad |= (i < lo) | (i >= hi) | (e > 0 && i <= idx[e - 1]);
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) *nnz_slot = bad ? -1 : nnz;
+}
+
+cudaError_t launch_sparse_nnz_checked(const int* idx, int nnz, long long lo, long long hi,
+                                      int* nnz_slot, cudaStream_t s) {
+  sparse_nnz_checked_kernel<<<1, 256, 0, s>>>(idx, nnz, lo, hi, nnz_slot);
   return cudaGetLastError();
 }
 

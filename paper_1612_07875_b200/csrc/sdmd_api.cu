@@ -977,7 +977,7 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
       CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
       CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     }
-    CK(launch_set_int(c->sp_nnz + slot, nnz, c->stream));
+    CK(launch_sparse_nnz_checked(sidx, nnz, lo, hi, c->sp_nnz + slot, c->stream));
   }
   c->launches += 1;
   return enqueue_frame(c, t);
@@ -1062,7 +1062,8 @@ int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
     (void)m;
     hs.status = 0;
     CK(cudaMemcpy(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice));
-    c->err = "frame " + std::to_string(hs.failed_frame) + " rejected (non-finite)";
+    c->err = "frame " + std::to_string(hs.failed_frame) +
+             " rejected (non-finite Gram column, or invalid device-side sparse indices)";
     return SDMD_E_NONFINITE;
   }
   return SDMD_OK;

@@ -200,6 +200,8 @@ cudaError_t launch_commit_batch(const K1bParams& p, cudaStream_t s);
 int k1b_grid(int nsm, long long n, int dtype);
 size_t k1b_partials_elems(int grid);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
+cudaError_t launch_sparse_nnz_checked(const int* idx, int nnz, long long lo, long long hi,
+                                      int* nnz_slot, cudaStream_t s);
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
 size_t k4_smem_bytes(int r_max, int m, int bg_modes);

@@ -1176,3 +1176,100 @@ def test_two_ranks_one_gpu_sparse(monkeypatch):
         ref.push(st.dense(t))
     assert np.array_equal(res[0], res[1])
     assert normwise(res[0], ref.G) < 1e-12
+
+
+def _sparse_dev(idx, val):
+    return (torch.from_numpy(np.ascontiguousarray(idx, dtype=np.int32)).to("cuda:0"),
+            torch.from_numpy(np.ascontiguousarray(val, dtype=np.float64)).to("cuda:0"))
+
+
+def test_sparse_device_indices_checked_on_device():
+    """Device-resident sparse frames are validated on the device (the host cannot see them): a
+    frame with descending or out-of-range indices is rejected like a non-finite one — nothing is
+    scattered, sync reports it and the stream resumes from the last committed frame."""
+    from paper_1612_07875_b200 import SDMDError
+    st = synth.SparseDCTStream(N=64, k_low=8.0, n_shell=20, seed=41)
+    m, T = 10, 30
+    bad = {12: lambda i: i[::-1].copy(), 20: lambda i: i + st.n}     # descending, out of range
+    eng = Eng(st.n, m, storage="sparse", nnz_cap=st.nnz_cap, workers=1)
+    ref = O.StreamingGram(m)
+    committed, skip = 0, set()
+    for t in range(T):
+        if t in skip:
+            continue
+        if t in bad:
+            eng.sync()
+            G0 = eng.gram()
+            idx, val = st.frame(t)
+            eng.push_sparse(*_sparse_dev(bad[t](idx), val))
+            eng.push_sparse(*_sparse_dev(*st.frame(t + 1)))         # discarded by the poison contract
+            skip.add(t + 1)
+            with pytest.raises(SDMDError) as e:
+                eng.sync()
+            assert e.value.status == 2 and e.value.failed_frame == committed
+            assert np.array_equal(eng.gram(), G0)
+            assert eng.info()["frames"] == committed
+            continue
+        eng.push_sparse(*_sparse_dev(*st.frame(t)))
+        ref.push(st.dense(t))
+        committed += 1
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    d = O.dmd_from_gram(ref.G)
+    assert eng.spectrum()["r"] == d["r"]
+    eng.close()
+
+
+def test_two_ranks_one_gpu_sparse_bad_indices_rejected_on_every_rank(monkeypatch):
+    """Rank 0 pushes a device frame with an index outside its row range: the NaN self product goes through
+    the allreduce, so BOTH ranks reject the same frame and resume in step."""
+    import threading
+    from paper_1612_07875_b200 import SDMDError, row_partition
+    monkeypatch.setenv("SDMD_LOCAL_GROUP", "1")
+    st = synth.SparseDCTStream(N=64, k_low=8.0, n_shell=20, seed=43)
+    m, T, bad_at = 8, 24, 11
+    uid = bytes((7 * i + 3) % 256 for i in range(128))
+    res, errs, fails = {}, [], {}
+
+    def run(rank):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                b, e = row_partition(st.n, 2, rank)
+                eng = Eng(e - b, m, storage="sparse", nnz_cap=st.nnz_cap, workers=1, rank=rank,
+                          nranks=2, row_begin=b, n_global=st.n, nccl_uid=uid)
+
+                def push(t, corrupt=False):
+                    idx, val = st.frame(t)
+                    sel = (idx >= b) & (idx < e)
+                    ii = idx[sel].copy()
+                    if corrupt and ii.size:
+                        ii[-1] = e + 5 if rank == 0 else ii[-1]   # a valid index, but rank 1's
+                    eng.push_sparse(*_sparse_dev(ii, val[sel]))
+                for t in range(bad_at):
+                    push(t)
+                push(bad_at, corrupt=True)
+                try:
+                    eng.sync()
+                    fails[rank] = None
+                except SDMDError as ex:
+                    fails[rank] = (ex.status, ex.failed_frame)
+                for t in range(bad_at + 1, T):
+                    push(t)
+                eng.sync()
+                res[rank] = eng.gram()
+                eng.close()
+        except Exception as ex:
+            errs.append(repr(ex))
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=300)
+    assert not errs, errs
+    assert fails[0] == fails[1] == (2, bad_at), fails
+    ref = O.StreamingGram(m)
+    for t in list(range(bad_at)) + list(range(bad_at + 1, T)):
+        ref.push(st.dense(t))
+    assert np.array_equal(res[0], res[1])
+    assert normwise(res[0], ref.G) < 1e-12
