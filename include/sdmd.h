@@ -171,7 +171,8 @@ int sdmd_destroy(sdmd_ctx* ctx);
 /* First window in one call (Alg 1 first branch "xtx = X.T * X"): Z is n_local x (m+1),
  * column-major with leading dimension ldz >= n_local, oldest column first, dtype = cfg.dtype.
  * The batch Gram runs on the fp64 tensor pipe (DMMA, kernel K2); the DMD of the window is then
- * computed if cfg.dmd.  Replaces any previous state.  Dense storage only. */
+ * computed if cfg.dmd.  Replaces any previous state.  Dense storage only.  A window whose Gram
+ * has a non-finite entry is rejected whole: SDMD_E_NONFINITE, the stream is left empty (0 frames). */
 int sdmd_init_window(sdmd_ctx* ctx, const void* Z, int64_t ldz, int where);
 
 /* Push one dense snapshot (n_local values of cfg.dtype).  While fewer than m+1 frames are held

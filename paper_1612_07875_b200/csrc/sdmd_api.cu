@@ -20,6 +20,7 @@
 #include <map>
 #include <mutex>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -1009,6 +1010,21 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   if (c->cfg.nranks > 1) {
     const int st_ = coll_allreduce(c, c->Gtmp, (size_t)k * k);
     if (st_) return st_;
+  }
+  {
+    // one-off: a non-finite window is rejected whole, leaving an empty stream; after the
+    // allreduce every rank sees the same Gram and takes the same decision
+    std::vector<double> hg((size_t)k * k);
+    CK(cudaMemcpyAsync(hg.data(), c->Gtmp, hg.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (double v : hg)
+      if (!std::isfinite(v)) {
+        c->frames = 0;
+        c->last_dmd = c->last_dmd_all = -1;
+        c->err = "init_window rejected (non-finite Gram)";
+        return SDMD_E_NONFINITE;
+      }
   }
   CK(launch_ghist_from_gram(c->Gtmp, k, c->ghist, c->NH, m, 0, c->stream));
   c->launches += 1;

@@ -535,6 +535,29 @@ def test_init_window_dmma_gram(dtype):
     eng.close()
 
 
+def test_init_window_nonfinite_rejected_whole():
+    """A first window with a NaN (or Inf) is rejected: SDMD_E_NONFINITE, 0 frames; the
+    stream then starts cleanly from a good window."""
+    from paper_1612_07875_b200 import SDMDError
+    rng = np.random.default_rng(8)
+    n, m = 5000, 12
+    Z = rng.standard_normal((n, m + 1))
+    eng = Eng(n, m, dtype="f64", workers=1)
+    for bad in (float("nan"), float("inf")):
+        Zb = Z.copy()
+        Zb[777, 5] = bad
+        with pytest.raises(SDMDError) as e:
+            eng.init_window(dev_cols(Zb, np.float64))
+        assert e.value.status == 2
+        assert eng.info()["frames"] == 0
+    eng.init_window(dev_cols(Z, np.float64))
+    eng.sync()
+    assert eng.info()["frames"] == m + 1
+    assert normwise(eng.gram(), O.gram(Z)) < 1e-12
+    assert match(eng.spectrum()["lam"], O.dmd_window(Z)["lam"])[0] < 1e-9
+    eng.close()
+
+
 def _planted_window(n, m, npairs, seed):
     """n x (m+1) window of 2·npairs planted DMD modes x_t = Σ 2 Re(b_j φ_j λ_j^t) (fp64)."""
     rng = np.random.default_rng(seed)
