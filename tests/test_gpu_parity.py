@@ -558,6 +558,35 @@ def test_init_window_nonfinite_rejected_whole():
     eng.close()
 
 
+def test_maximum_workers_every_window_and_limits():
+    """The largest worker-stream count the ABI accepts (24): every window's spectrum, read after
+    each push, still equals the closed form; 25 workers and batches above batch_max are refused."""
+    from paper_1612_07875_b200 import SDMDError
+    pm = synth.planted_c1()
+    m, T = 16, 60
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    with pytest.raises(SDMDError) as e:
+        Eng(pm.n, m, dtype="f64", workers=25)
+    assert e.value.status == 1
+    eng = Eng(pm.n, m, dtype="f64", workers=24, batch_max=4)
+    for t in range(T):
+        eng.push(Xd[t])
+        if t >= m + 1 and t % 3 == 0:
+            eng.sync()
+            sp = eng.spectrum()
+            assert sp["frame"] == t and sp["r"] == 4
+            assert match(sp["lam"], pm.lambdas)[0] < 1e-9, t
+    with pytest.raises(SDMDError) as e:
+        eng.push_batch(dev_cols(pm.frames(T, T + 5), np.float64))
+    assert e.value.status == 1
+    eng.push_batch(dev_cols(pm.frames(T, T + 4), np.float64))
+    eng.sync()
+    sp = eng.spectrum()
+    assert sp["frame"] == T + 3 and match(sp["lam"], pm.lambdas)[0] < 1e-9
+    eng.close()
+
+
 def _planted_window(n, m, npairs, seed):
     """n x (m+1) window of 2·npairs planted DMD modes x_t = Σ 2 Re(b_j φ_j λ_j^t) (fp64)."""
     rng = np.random.default_rng(seed)
