@@ -504,6 +504,41 @@ def test_determinism_bitwise():
         assert np.array_equal(a, b)
 
 
+def test_determinism_bitwise_sparse_batch_background():
+    """Every reduction is fixed-order: the sparse Gram (K3 partials), batched pushes (K1b) and the
+    fused background pass (K1, 4-mode set) repeat bit for bit across contexts."""
+    st = synth.SparseDCTStream(N=96, k_low=10.0, n_shell=40, seed=31)
+    frames = [st.frame(t) for t in range(28)]
+    rng = np.random.default_rng(6)
+    n, m = 40000, 12
+    X = rng.random((n, 36)).astype(np.float32)
+    Xd = dev_cols(X, np.float32)
+    runs = []
+    workers = 3
+    for _ in range(2):
+        sp = Eng(st.n, 10, storage="sparse", nnz_cap=st.nnz_cap, workers=workers)
+        for idx, val in frames:
+            sp.push_sparse(idx, val)
+        sp.sync()
+        bt = Eng(n, m, dtype="f32", dmd=False, workers=workers, batch_max=8)
+        for t in range(m + 1):                                # batches need a full window
+            bt.push(Xd[t])
+        for t0 in range(m + 1, 36, 8):
+            bt.push_batch(Xd[t0:min(t0 + 8, 36)])
+        bt.sync()
+        bg = Eng(n, m, dtype="f32", workers=workers, background=True, bg_modes=4, lag=4)
+        for t in range(36):
+            bg.push(Xd[t])
+        bg.sync()
+        low, sparse, mask, fr = bg.background()
+        runs.append((sp.gram(), sp.spectrum()["lam"], bt.gram(), bg.gram(), low, sparse, mask,
+                     np.array([fr])))
+        for e in (sp, bt, bg):
+            e.close()
+    for a, b in zip(runs[0], runs[1]):
+        assert np.array_equal(a, b)
+
+
 # --------------------------------------------------------------- init window (K2) --------
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
