@@ -1,40 +1,97 @@
 """ORACLE — test infrastructure, NOT part of the product.
 
-Plain, slow, obviously-correct fp64 CPU implementation of the streaming method-of-snapshots
-SVD / DMD / background-subtraction path of arXiv 1612.07875 (reference: /root/reference/
-PAPER.md, cited as P:<line>).  Only ``tests/``, ``__graft_entry__.smoke()`` and the
-``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this module.  It shares
-no code with the CUDA path (``paper_1612_07875_b200/``) and never imports it.
+Plain, slow, fp64 CPU implementation of the streaming method-of-snapshots SVD / DMD /
+background-subtraction path of arXiv 1612.07875 (reference: /root/reference/PAPER.md, cited as
+P:<line>; SPEC.md as S:<line>).  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this module.  It shares no
+code with the CUDA path (``paper_1612_07875_b200/``) and never imports it.
 
-Each function follows the paper's algorithm in the paper's order and notation; library
-primitives serve as single steps exactly where the paper itself calls a library routine
-(``X.T * X`` → numpy matmul/dot, ``eig`` → LAPACK via numpy.linalg, ``lstsq``).  Readings
-where the paper is ambiguous or garbled are the ones listed in DESIGN.md §"Readings"
-(SURVEY.md §8(c) Q1–Q24); each is cited as Qk where used.
+The arithmetic lives in ``oracle/csrc/sdmd_oracle.c`` (C99, explicit loops, no BLAS/LAPACK),
+called here through ctypes; this module holds the step order of the paper's Algorithms 1-3 and the
+conventions (sorting, normalisation, index rules).  Steps follow SURVEY.md §8(c) O1-O13:
+  O1  Gram: Neumaier-compensated fp64 row-order sums of exact products      (C: orc_gram/orc_dots)
+  O3  symmetric eig of S: cyclic-by-row Jacobi, stable rotation            (C: orc_jacobi)
+  O6  eig(Ã): Householder-Hessenberg + Francis double-shift QR + back-substitution
+                                                                           (C: orc_eig_real)
+  O7  modes Φ = X'(Y W): compensated complex accumulation                  (C: orc_modes)
+  O9  b = (WΛ)⁻¹α₁: complex Gaussian elimination with partial pivoting;
+      singular fallback: complex column-pivoted Householder least squares  (C: orc_csolve/clstsq)
+Small dense products (Ã = Yᵀ G_xy Y, T = Y W, the O(r) sums) use numpy matmul as a library
+primitive, as the paper's own pseudo-code does ("*" products, Alg 2).  Readings where
+the paper is ambiguous or garbled are DESIGN.md §3; each is cited
+as Qk/Rk where used.
 
-Pins (tests/test_oracle_*.py, ``-m "not gpu"``): closed-form planted spectra, worked examples
-from SPEC.md (cited), exact-rational brute force on tiny inputs, streamed == batch, Gram
-slice identities, invariance under orthonormal transforms, Eckart–Young, eigenvalue
-equivalence with the full operator X' pinv(X), LAPACK SVD of X on tiny inputs.
+Pins (tests/test_oracle.py, ``-m "not gpu"``): closed-form planted spectra, worked examples from
+SPEC.md (cited), exact-rational brute force on tiny inputs, streamed == batch, Gram slice
+identities, invariance under orthonormal transforms, Eckart-Young, eigenvalue equivalence with
+the full operator X' pinv(X), LAPACK (numpy.linalg, test side only — independent of this
+module now) on tiny inputs, the singular-amplitude branch on a planted zero eigenvalue, the
+first-window background on a constant video, and the Q12 order on hand-built spectra.
 
 Parity unpinned: eigenvalues of Ã for noisy video windows with r ≈ m have no closed form;
 they are checked only GPU-vs-oracle within κ(λ)·‖ΔÃ‖ (DESIGN.md §"Parity").
 """
 from __future__ import annotations
 
+import ctypes
+import os
+
 import numpy as np
 
 # ----------------------------------------------------------------------------------------
-# status codes (mirror of include/sdmd.h values, redefined here: no shared code)
+# status codes (values of include/sdmd.h redefined here: no shared code)
 # ----------------------------------------------------------------------------------------
 OK, E_INVALID, E_NONFINITE, E_WINDOW_NOT_FULL, E_ZERO_MATRIX = 0, 1, 2, 3, 4
 E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE = 5, 6, 7
+
+THREADS = int(os.environ.get("ORACLE_THREADS", "0"))   # 0: all host cores (row-chunk sums)
 
 
 class OracleError(Exception):
     def __init__(self, code: int, msg: str = ""):
         super().__init__(f"status {code}: {msg}")
         self.code = code
+
+
+_clib = None
+
+
+def clib():
+    """The oracle's C library (built on first use with gcc; see oracle/build.py)."""
+    global _clib
+    if _clib is None:
+        from oracle.build import build
+        L = ctypes.CDLL(build())
+        vp, i32, i64, dp = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+        L.orc_dots.argtypes = [vp, i64, i32, vp, i64, i32, i32, dp]
+        L.orc_dots.restype = None
+        L.orc_gram.argtypes = [vp, i64, i32, i64, i32, i32, dp]
+        L.orc_gram.restype = None
+        L.orc_jacobi.argtypes = [i32, dp, dp, dp, i32, ctypes.POINTER(ctypes.c_int)]
+        L.orc_jacobi.restype = ctypes.c_int
+        L.orc_eig_real.argtypes = [i32, dp, dp, dp, dp, dp, ctypes.POINTER(ctypes.c_int)]
+        L.orc_eig_real.restype = ctypes.c_int
+        L.orc_csolve.argtypes = [i32, dp, dp, dp]
+        L.orc_csolve.restype = ctypes.c_int
+        L.orc_clstsq.argtypes = [i32, i32, dp, dp, dp]
+        L.orc_clstsq.restype = ctypes.c_int
+        L.orc_modes.argtypes = [vp, i64, i32, i64, i32, dp, i32, dp, i64, i32]
+        L.orc_modes.restype = None
+        _clib = L
+    return _clib
+
+
+def _p(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _real_cols(cols) -> tuple[np.ndarray, int]:
+    """Columns as one Fortran-ordered (n, k) array of float32 (dtype 0) or float64 (dtype 1); fp32
+    inputs stay fp32 (promoted exactly inside the C sums, Q9)."""
+    arrs = [np.asarray(c) for c in cols]
+    if all(a.dtype == np.float32 for a in arrs):
+        return np.asfortranarray(np.stack(arrs, axis=1)), 0
+    return np.asfortranarray(np.stack([a.astype(np.float64) for a in arrs], axis=1)), 1
 
 
 # ----------------------------------------------------------------------------------------
@@ -44,41 +101,53 @@ class OracleError(Exception):
 def gram(Z) -> np.ndarray:
     """G = Zᵀ Z of the full window Z = [z_0 .. z_m] (n x (m+1)), fp64.
 
-    Alg 1 P:291 ("xtx = X.T * X") applied to the full window (reading Q2: the full-window
-    Gram holds both XᵀX = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1]).  fp32 inputs are promoted
-    exactly to fp64 before the products (Q9)."""
-    Zd = np.asarray(Z, dtype=np.float64)
-    return Zd.T @ Zd
+    Alg 1 P:291 ("xtx = X.T * X") applied to the full window (reading Q2: the full-window Gram
+    holds both XᵀX = G[0:m,0:m] and XᵀX' = G[0:m,1:m+1]).  Every entry is the Neumaier-
+    compensated sum over the rows in increasing order of the exact products (fp32 inputs are
+    promoted exactly, Q9; fp64 products carry their fma rounding error)."""
+    Z = np.asarray(Z)
+    if Z.ndim == 1:
+        Z = Z[:, None]
+    Zf, dt = _real_cols([Z[:, j] for j in range(Z.shape[1])]) if Z.shape[1] else (Z, 1)
+    n, k = Zf.shape
+    G = np.zeros((k, k), dtype=np.float64)
+    if k:
+        clib().orc_gram(_p(Zf), n, k, n, dt, THREADS, _p(G))
+    return G
 
 
 def gram_column(cols, x_new) -> np.ndarray:
-    """g_k = <z_k, x_new> for each window column z_k (x_new itself last gives the self-dot).
+    """g_k = <z_k, x_new> for each window column z_k (pass x_new itself last for the self-dot).
 
-    Alg 1 else-branch P:294 ("xtx[:, -1] = X.T * X[:, -1]"); §3.1 P:236 ("only the last row
-    or column will need to be recalculated").  One library dot per column."""
-    x = np.asarray(x_new, dtype=np.float64)
-    return np.array([float(np.dot(np.asarray(c, dtype=np.float64), x)) for c in cols])
+    Alg 1 else-branch P:294 ("xtx[:, -1] = X.T * X[:, -1]"); §3.1 P:236 ("only the last row or
+    column will need to be recalculated").  Compensated row-order dots (O1)."""
+    A, dt = _real_cols(list(cols) + [x_new])
+    n, k = A.shape[0], A.shape[1] - 1
+    x = np.ascontiguousarray(A[:, -1])
+    out = np.zeros(max(k, 1), dtype=np.float64)
+    if k:
+        clib().orc_dots(_p(A), n, k, _p(x), n, dt, THREADS, _p(out))
+    return out[:k]
 
 
 def sparse_gram_column(slots, x_new, n: int) -> np.ndarray:
-    """Sparse variant (§3.5): each snapshot is (idx, val) in an orthonormal
-    coefficient basis; g_k is the dot of the *scattered* dense vectors (definition)."""
+    """Sparse variant (§3.5): each snapshot is (idx, val) in an orthonormal coefficient
+    basis; g_k is the dot of the *scattered* dense vectors (definition)."""
     def dense(sv):
         idx, val = sv
         d = np.zeros(n, dtype=np.float64)
         d[np.asarray(idx, dtype=np.int64)] = np.asarray(val, dtype=np.float64)
         return d
-    xd = dense(x_new)
-    return np.array([float(np.dot(dense(s), xd)) for s in slots])
+    return gram_column([dense(s) for s in slots], dense(x_new))
 
 
 class StreamingGram:
     """Sliding-window Gram state (Alg 1 else-branch P:293-295, on the full window, Q2).
 
-    Warm-up: while fewer than m+1 columns are held, push appends a column and extends G
-    (Q14).  Full: push drops the oldest column, keeps G[1:,1:] (copied,
-    not recomputed) and computes the new last row/column.  A frame whose
-    self-dot is not finite is rejected and the state is left unchanged."""
+    Warm-up: while fewer than m+1 columns are held, push appends a column and extends G (Q14,
+    P:496-498).  Full: push drops the oldest column, keeps G[1:,1:] (copied, not
+    recomputed) and computes the new last row/column.  A frame whose Gram column is
+    not finite is rejected and the state is left unchanged."""
 
     def __init__(self, m: int):
         self.m = m
@@ -91,7 +160,8 @@ class StreamingGram:
         return len(self.cols) == self.m + 1
 
     def push(self, x) -> None:
-        x = np.asarray(x, dtype=np.float64).copy()
+        x = np.asarray(x)
+        x = (x.astype(np.float32) if x.dtype == np.float32 else x.astype(np.float64)).copy()
         if self.full:
             keep = self.cols[1:]
             Gk = self.G[1:, 1:]                       # "xtx[:-1, :-1] = xtx[1:, 1:]"
@@ -99,7 +169,7 @@ class StreamingGram:
             keep = self.cols
             Gk = self.G
         g = gram_column(keep + [x], x)                 # "xtx[:, -1] = X.T * X[:, -1]"
-        if not np.isfinite(g[-1]) or not np.all(np.isfinite(g)):
+        if not np.all(np.isfinite(g)):
             raise OracleError(E_NONFINITE, "non-finite frame rejected; state unchanged")
         self.fresh_dots += len(g)
         k = len(keep)
@@ -115,6 +185,21 @@ class StreamingGram:
 # O3–O4  Method-of-snapshots SVD from the Gram  (§2.1; Alg 1)
 # ----------------------------------------------------------------------------------------
 
+def jacobi_eigh(S, max_sweeps: int = 60):
+    """(μ, V, sweeps) of the symmetric S by cyclic-by-row Jacobi (O3; C orc_jacobi): "s, v =
+    eig(xtx)" (Alg 1).  μ unsorted, V[:, j] the eigenvector of μ_j.  Raises
+    E_NO_CONVERGENCE after max_sweeps sweeps."""
+    S = np.ascontiguousarray(np.asarray(S, dtype=np.float64))
+    m = S.shape[0]
+    mu = np.zeros(m)
+    V = np.zeros((m, m), order="F")
+    sw = ctypes.c_int(0)
+    st = clib().orc_jacobi(m, _p(S), _p(mu), _p(V), int(max_sweeps), ctypes.byref(sw))
+    if st:
+        raise OracleError(E_NO_CONVERGENCE, f"Jacobi: no convergence in {max_sweeps} sweeps")
+    return mu, V, sw.value
+
+
 def _sign_normalize_real(V: np.ndarray) -> np.ndarray:
     """Q6: make each column's largest-|.| entry positive (first such entry on ties)."""
     V = V.copy()
@@ -128,14 +213,12 @@ def _sign_normalize_real(V: np.ndarray) -> np.ndarray:
 def svd_from_gram(S, rank_tol: float = 1e-7, r_max: int | None = None):
     """σ, V, r of X from S = XᵀX.
 
-    "s, v = eig(xtx)" (Alg 1; eig of the symmetric Gram, LAPACK via numpy),
-    "sigma = sort(sqrt(abs(s)), 'desc')" with V permuted alike (Q6),
-    r = min(r_max, #{σ_i > rank_tol·σ_1}) (Q7).  Raises E_ZERO_MATRIX if σ_1 == 0."""
-    S = np.asarray(S, dtype=np.float64)
-    S = 0.5 * (S + S.T)
-    mu, V = np.linalg.eigh(S)
+    "s, v = eig(xtx)" (Alg 1; cyclic Jacobi, O3), "sigma = sort(sqrt(abs(s)), 'desc')"
+     with V permuted alike (Q6), r = min(r_max, #{σ_i > rank_tol·σ_1}) (Q7).  Raises
+    E_ZERO_MATRIX if σ_1 == 0."""
+    mu, V, _ = jacobi_eigh(S)
     sigma = np.sqrt(np.abs(mu))
-    order = np.argsort(-sigma, kind="stable")
+    order = sorted(range(len(sigma)), key=lambda i: (-sigma[i], i))   # stable descending
     sigma = sigma[order]
     V = _sign_normalize_real(V[:, order])
     if sigma.size == 0 or sigma[0] == 0.0:
@@ -155,6 +238,21 @@ def left_singular(X, sigma, V, r: int) -> np.ndarray:
 # O5–O6  Projected operator and its eigendecomposition  (Eq. Atilde; Alg 2)
 # ----------------------------------------------------------------------------------------
 
+def eig_real(A):
+    """(λ, W) of the real square A (O6; C orc_eig_real): Householder-Hessenberg, Francis double-
+    shift QR to real Schur form, eigenvectors by back-substitution ("lambda, w = eig(atilde)",
+    Alg 2).  Unordered, unnormalised.  Raises E_NO_CONVERGENCE past 100 r iterations."""
+    A = np.ascontiguousarray(np.asarray(A, dtype=np.float64))
+    r = A.shape[0]
+    wr, wi = np.zeros(r), np.zeros(r)
+    Wr, Wi = np.zeros((r, r), order="F"), np.zeros((r, r), order="F")
+    its = ctypes.c_int(0)
+    st = clib().orc_eig_real(r, _p(A), _p(wr), _p(wi), _p(Wr), _p(Wi), ctypes.byref(its))
+    if st:
+        raise OracleError(E_NO_CONVERGENCE, "Francis QR: no convergence")
+    return wr + 1j * wi, Wr + 1j * Wi
+
+
 def order_eigs(lam: np.ndarray) -> np.ndarray:
     """Q12: |λ| descending, then Re descending, then Im descending (stable)."""
     keys = [(-abs(l), -l.real, -l.imag, i) for i, l in enumerate(lam)]
@@ -166,7 +264,7 @@ def normalize_eigvecs(W: np.ndarray) -> np.ndarray:
     W = np.asarray(W, dtype=np.complex128).copy()
     for j in range(W.shape[1]):
         w = W[:, j]
-        w = w / np.linalg.norm(w)
+        w = w / np.sqrt(np.sum(np.abs(w) ** 2))
         i = int(np.argmax(np.abs(w)))
         w = w * (np.conj(w[i]) / abs(w[i]))
         W[:, j] = w
@@ -187,7 +285,7 @@ def dmd_from_gram(G, rank_tol: float = 1e-7, r_max: int | None = None) -> dict:
     sigma, V, r = svd_from_gram(S, rank_tol, r_max)
     vsi = V[:, :r] / sigma[:r]
     atilde = vsi.T @ xty @ vsi
-    lam, W = np.linalg.eig(atilde)
+    lam, W = eig_real(atilde)
     o = order_eigs(lam)
     lam = lam[o]
     W = normalize_eigvecs(W[:, o])
@@ -199,23 +297,47 @@ def dmd_from_gram(G, rank_tol: float = 1e-7, r_max: int | None = None) -> dict:
 # O8–O10  Amplitudes and background mode  (§3.3; Alg 3)
 # ----------------------------------------------------------------------------------------
 
-def amplitudes(d: dict) -> tuple[np.ndarray, int]:
+def csolve(A, b):
+    """x = A⁻¹b (complex, Gaussian elimination with partial pivoting, C orc_csolve); None if a
+    pivot is numerically zero."""
+    A = np.asfortranarray(np.asarray(A, dtype=np.complex128))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.complex128))
+    x = np.zeros(A.shape[0], dtype=np.complex128)
+    st = clib().orc_csolve(A.shape[0], _p(A), _p(b), _p(x))
+    return None if st else x
+
+
+def clstsq(A, b):
+    """(x, rank): least squares min‖Ax − b‖ by complex Householder QR with column pivoting (C
+    orc_clstsq); columns beyond the numerical rank get x = 0."""
+    A = np.asfortranarray(np.asarray(A, dtype=np.complex128))
+    b = np.ascontiguousarray(np.asarray(b, dtype=np.complex128))
+    x = np.zeros(A.shape[1], dtype=np.complex128)
+    rk = clib().orc_clstsq(A.shape[0], A.shape[1], _p(A), _p(b), _p(x))
+    return x, rk
+
+
+def amplitudes(d: dict, rank_tol: float = 1e-7) -> tuple[np.ndarray, int]:
     """b = (WΛ)⁻¹ α₁ with α₁ = POD coefficients of x₁ = σ ⊙ V[0, :r] (Q3).
 
-    "alpha1 = sigma * v[:, 0].T; wl = w * lambda; b = lstsq(wl, alpha1)" (Alg 3),
-    §3.3 P:268.  Returns (b, status): W_SINGULAR when WΛ is numerically singular, in which
-    case modes with |λ| < rank_tol·max|λ| get b = 0 and the rest are solved (Q15)."""
+    "alpha1 = sigma * v[:, 0].T; wl = w * lambda; b = lstsq(wl, alpha1)" (Alg 3), §3.3
+    P:268.  Reading Q15 (SPEC S:272, S:296 design decision): WΛ is singular when some
+    |λ_j| < rank_tol·max|λ| (or elimination meets a zero pivot); those modes are excluded and get
+    b = 0, the others are the least-squares solution of the kept columns (min-norm for full column
+    rank), and the status is W_SINGULAR.  Otherwise b is the square solve, status OK."""
     r = d["r"]
-    alpha1 = d["sigma"][:r] * d["V"][0, :r]
+    alpha1 = (d["sigma"][:r] * d["V"][0, :r]).astype(np.complex128)
     lam, W = d["lam"], d["W"]
     wl = W * lam[None, :]
-    s = np.linalg.svd(wl, compute_uv=False)
-    if s[-1] > 1e-13 * s[0]:
-        return np.linalg.solve(wl, alpha1.astype(np.complex128)), OK
-    keep = np.abs(lam) >= 1e-7 * max(np.abs(lam).max(), 1e-300)
+    amax = float(np.max(np.abs(lam))) if len(lam) else 0.0
+    keep = np.abs(lam) >= rank_tol * amax if amax > 0 else np.zeros(len(lam), dtype=bool)
+    if keep.all():
+        b = csolve(wl, alpha1)
+        if b is not None:
+            return b, OK
     b = np.zeros(len(lam), dtype=np.complex128)
     if keep.any():
-        b[keep] = np.linalg.lstsq(wl[:, keep], alpha1.astype(np.complex128), rcond=None)[0]
+        b[keep] = clstsq(wl[:, keep], alpha1)[0]
     return b, W_SINGULAR
 
 
@@ -244,15 +366,18 @@ def background_index(lam) -> int:
 def modes(Xp_cols, d: dict, which=None) -> np.ndarray:
     """Φ = X' V Σ⁻¹ W = X' (vsi w)  ("vsiw = vsi * w; phi = X[:, 1:] * vsiw").
 
-    ``Xp_cols``: the m columns of X' (list of n-vectors); ``which``: mode indices (default
-    all).  Explicit accumulation over the m columns."""
+    ``Xp_cols``: the m columns of X' (list of n-vectors, or an (n, m) array); ``which``: mode
+    indices (default all).  Each entry is a compensated sum over the m columns (O7, C
+    orc_modes)."""
     vsiw = d["vsi"] @ d["W"]                            # P:315
-    cols = range(vsiw.shape[1]) if which is None else list(which)
-    n = len(Xp_cols[0])
-    Phi = np.zeros((n, len(cols)), dtype=np.complex128)
-    for k, xk in enumerate(Xp_cols):
-        xk = np.asarray(xk, dtype=np.float64)
-        Phi += np.outer(xk, vsiw[k, cols])
+    cols = list(range(vsiw.shape[1])) if which is None else list(which)
+    if isinstance(Xp_cols, np.ndarray) and Xp_cols.ndim == 2:
+        Xp_cols = [Xp_cols[:, k] for k in range(Xp_cols.shape[1])]
+    X, dt = _real_cols(Xp_cols)
+    n, m = X.shape
+    T = np.asfortranarray(vsiw[:, cols].astype(np.complex128))
+    Phi = np.zeros((n, len(cols)), dtype=np.complex128, order="F")
+    clib().orc_modes(_p(X), n, m, n, dt, _p(T), len(cols), _p(Phi), n, THREADS)
     return Phi
 
 
@@ -342,8 +467,8 @@ class StreamingDMD:
     def init_window(self, Z) -> dict | None:
         """First step (Alg 1 first branch "xtx = X.T * X"): the whole window at once.
         Z: n x (m+1) array (or a list of m+1 columns), oldest first."""
-        cols = [np.asarray(c, dtype=np.float64) for c in
-                (Z if isinstance(Z, (list, tuple)) else np.asarray(Z).T)]
+        cols = [np.asarray(c) for c in (Z if isinstance(Z, (list, tuple)) else np.asarray(Z).T)]
+        cols = [c.astype(np.float32) if c.dtype == np.float32 else c.astype(np.float64) for c in cols]
         if len(cols) != self.m + 1:
             raise OracleError(E_INVALID, "init_window needs m+1 columns")
         G = gram(np.stack(cols, axis=1))
@@ -367,7 +492,7 @@ class StreamingDMD:
     def _dmd(self, background: bool = True) -> dict:
         G = self.gram.G
         d = dmd_from_gram(G, self.rank_tol, self.r_max)
-        b, st = amplitudes(d)
+        b, st = amplitudes(d, self.rank_tol)
         idx = background_index(d["lam"])
         out = dict(d, b=b, amp_status=st, idx=idx, G=G.copy(), frame=self.frames - 1)
         if self.background and background:
@@ -388,6 +513,6 @@ def dmd_window(Z, rank_tol: float = 1e-7, r_max: int | None = None) -> dict:
     (the paper's non-streaming CPU/GPU variants)."""
     G = gram(Z)
     d = dmd_from_gram(G, rank_tol, r_max)
-    b, st = amplitudes(d)
+    b, st = amplitudes(d, rank_tol)
     idx = background_index(d["lam"])
     return dict(d, b=b, amp_status=st, idx=idx, G=G)

@@ -1,6 +1,7 @@
-"""Pins of the oracle (oracle/sdmd_oracle.py) against things other than itself:
-closed forms, SPEC worked examples (tests/golden), exact rational arithmetic, invariants and
-independent library routines (LAPACK SVD of X, pinv) on tiny inputs.  CPU only."""
+"""Pins of the oracle (oracle/sdmd_oracle.py + oracle/csrc/sdmd_oracle.c) against things other
+than itself: closed forms, SPEC worked examples (tests/golden), exact rational arithmetic,
+correctly rounded sums (math.fsum), invariants and independent library routines (LAPACK via
+numpy.linalg / scipy, which the oracle itself no longer uses) on small inputs.  CPU only."""
 import json
 import math
 import os
@@ -191,9 +192,14 @@ def test_zero_window():
 
 @pytest.mark.parametrize("ex", GOLD["eig"], ids=lambda e: e["cite"][:20])
 def test_eig_worked(ex):
-    A = np.array(ex["A"])
-    lam = np.linalg.eig(A)[0]
+    """SPEC worked 2x2 examples through the oracle's own O6 (Hessenberg + Francis QR +
+    back-substitution), not LAPACK."""
+    A = np.array(ex["A"], dtype=np.float64)
+    lam, W = O.eig_real(A)
     assert match_eigs(lam, np.array(ex["lam_re"]) + 1j * np.array(ex["lam_im"])) < 1e-14
+    for j in range(len(lam)):                    # eigen-pairs where the matrix is diagonalisable
+        if np.linalg.norm(W[:, j]) > 0 and not np.allclose(A, np.triu(A, 1)):
+            assert np.linalg.norm(A @ W[:, j] - lam[j] * W[:, j]) <= 1e-14 * np.linalg.norm(W[:, j]) * max(1.0, np.abs(A).max())
 
 
 def test_c1_closed_form_lambda_every_window():
@@ -454,3 +460,274 @@ def test_buildup_dmd_closed_form_and_operator():
             ev = np.linalg.eigvals(np.linalg.pinv(Xa) @ Xb)
             ev = ev[np.argsort(-np.abs(ev))][:out["r"]]
             assert match_eigs(out["lam"], ev) < 1e-8
+
+
+# ------------------------------------------- pins of the C arithmetic (round 2) ------------
+
+def test_gram_compensated_vs_correctly_rounded_cancellation():
+    """O1 against math.fsum (the correctly rounded sum of the exact products) on fp32 columns with
+    heavy cancellation (naive fp64 summation loses ~8 digits here): every entry within 2 ulp."""
+    rng = np.random.default_rng(21)
+    n = 20000
+    base = rng.standard_normal(n).astype(np.float32) * np.float32(1e4)
+    Z = np.stack([base, -base + rng.standard_normal(n).astype(np.float32),
+                  rng.standard_normal(n).astype(np.float32), base * np.float32(0.5)], axis=1)
+    Z = Z.astype(np.float32)
+    G = O.gram(Z)
+    Zd = Z.astype(np.float64)
+    for i in range(4):
+        for j in range(4):
+            ref = math.fsum(Zd[:, i] * Zd[:, j])          # products exact (fp32 x fp32 in fp64)
+            assert abs(G[i, j] - ref) <= 2 * np.spacing(abs(ref)), (i, j)
+    naive = float(np.sum(Zd[:, 0] * Zd[:, 1]))
+    assert abs(G[0, 1] - math.fsum(Zd[:, 0] * Zd[:, 1])) <= abs(naive - math.fsum(Zd[:, 0] * Zd[:, 1]))
+
+
+def test_gram_fp64_products_compensated_vs_exact_rational():
+    """fp64 inputs whose products round: O1 carries the product error (fma), so each entry matches
+    the exact rational dot to ~1 ulp even with cancellation."""
+    rng = np.random.default_rng(22)
+    a = rng.standard_normal(300)
+    b = -a + 1e-9 * rng.standard_normal(300)
+    Z = np.stack([a, b, rng.standard_normal(300)], axis=1)
+    G = O.gram(Z)
+    for i in range(3):
+        for j in range(3):
+            ex = float(sum(Fraction(Z[k, i]) * Fraction(Z[k, j]) for k in range(300)))
+            assert abs(G[i, j] - ex) <= 2 * np.spacing(abs(ex)), (i, j)
+
+
+def test_gram_threads_agree():
+    """Row-chunk threads (timing mode) and the single row-order sum agree to rounding."""
+    rng = np.random.default_rng(23)
+    Z = rng.random((100000, 5)).astype(np.float32)
+    old = O.THREADS
+    try:
+        O.THREADS = 1
+        G1 = O.gram(Z)
+        O.THREADS = 7
+        G7 = O.gram(Z)
+    finally:
+        O.THREADS = old
+    assert normwise(G1, G7) < 1e-15
+
+
+def test_gram_column_equals_gram_last_column():
+    rng = np.random.default_rng(24)
+    Z = rng.standard_normal((777, 6))
+    g = O.gram_column([Z[:, k] for k in range(6)], Z[:, 5])
+    assert np.array_equal(g, O.gram(Z)[:, 5])
+
+
+@pytest.mark.parametrize("m", [1, 2, 7, 50, 200])
+def test_jacobi_vs_lapack_eigh(m):
+    """O3 (cyclic Jacobi) vs LAPACK dsyevd on random symmetric matrices: eigenvalues within
+    1e-13·‖S‖, V orthogonal, S V = V diag(μ)."""
+    rng = np.random.default_rng(30 + m)
+    B = rng.standard_normal((m, m))
+    S = B + B.T
+    mu, V, sweeps = O.jacobi_eigh(S)
+    ref = np.linalg.eigvalsh(S)
+    nrm = np.linalg.norm(S, 2)
+    assert np.max(np.abs(np.sort(mu) - ref)) < 1e-13 * nrm
+    assert np.max(np.abs(V.T @ V - np.eye(m))) < 1e-13
+    assert np.linalg.norm(S @ V - V * mu[None, :]) < 1e-13 * nrm * m
+    assert sweeps <= 15
+
+
+def test_jacobi_graded_psd_relative_accuracy():
+    """S = XᵀX with σ spread over 1e0..1e-6 (MoS squares it to 1e-12): every eigenvalue meets the
+    method-of-snapshots floor of reading Q7, |Δμ_i|/μ_i <= 4u (σ_1/σ_i)^2, against the squared
+    LAPACK SVD of X itself (forming XᵀX costs u‖X‖² absolute; Jacobi adds no more)."""
+    rng = np.random.default_rng(31)
+    Q1, _ = np.linalg.qr(rng.standard_normal((400, 12)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((12, 12)))
+    sv = np.logspace(0, -6, 12)
+    X = (Q1 * sv) @ Q2.T
+    mu, V, _ = O.jacobi_eigh(X.T @ X)
+    ref = np.linalg.svd(X, compute_uv=False) ** 2
+    u = 2.0 ** -53
+    rel = np.abs(np.sort(mu)[::-1] - ref) / ref
+    assert np.all(rel <= 4 * u * ref[0] / ref + 1e-15)
+
+
+def test_jacobi_no_convergence_reported():
+    rng = np.random.default_rng(32)
+    B = rng.standard_normal((20, 20))
+    with pytest.raises(O.OracleError) as e:
+        O.jacobi_eigh(B + B.T, max_sweeps=1)
+    assert e.value.code == O.E_NO_CONVERGENCE
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 5, 16, 64, 150, 224])
+def test_eig_real_vs_lapack_and_residual(r):
+    """O6 on random nonsymmetric matrices: eigenvalues vs LAPACK dgeev (test side) after optimal
+    matching, and the eigen-pair residual ‖A w − λ w‖ / (‖A‖‖w‖) ≤ 1e-12."""
+    rng = np.random.default_rng(40 + r)
+    A = rng.standard_normal((r, r)) / math.sqrt(r)
+    lam, W = O.eig_real(A)
+    assert match_eigs(lam, np.linalg.eigvals(A)) < 1e-11
+    nA = np.linalg.norm(A, 2)
+    for j in range(r):
+        w = W[:, j]
+        assert np.linalg.norm(A @ w - lam[j] * w) <= 1e-12 * nA * np.linalg.norm(w)
+    # conjugate pairs come with conjugate vectors
+    for j in range(r):
+        if lam[j].imag > 0:
+            k = int(np.argmin(np.abs(lam - np.conj(lam[j]))))
+            assert abs(lam[k] - np.conj(lam[j])) < 1e-12
+
+
+def test_eig_real_closed_forms():
+    """Closed forms: a triangular matrix (λ = its diagonal), a companion matrix with known roots,
+    a block-diagonal rotation/scaling (λ = ρ e^{±iθ}), a permutation cycle (roots of unity)."""
+    T = np.triu(np.arange(1.0, 26.0).reshape(5, 5))
+    assert match_eigs(O.eig_real(T)[0], np.diag(T)) < 1e-12
+    roots = np.array([0.9, -0.5, 0.3 + 0.4j, 0.3 - 0.4j, 1.1])
+    c = np.poly(roots).real                      # monic coefficients
+    C = np.zeros((5, 5))
+    C[0, :] = -c[1:]
+    C[1:, :-1] = np.eye(4)
+    assert match_eigs(O.eig_real(C)[0], roots) < 1e-12
+    blocks = [(0.95, 0.3), (0.5, 1.2), (0.99, 0.01)]
+    A = np.zeros((6, 6))
+    for q, (rho, th) in enumerate(blocks):
+        A[2 * q:2 * q + 2, 2 * q:2 * q + 2] = rho * np.array([[math.cos(th), -math.sin(th)],
+                                                             [math.sin(th), math.cos(th)]])
+    rng = np.random.default_rng(45)
+    Qo, _ = np.linalg.qr(rng.standard_normal((6, 6)))
+    ref = [rho * np.exp(s * 1j * th) for rho, th in blocks for s in (1, -1)]
+    assert match_eigs(O.eig_real(Qo @ A @ Qo.T)[0], ref) < 1e-13
+    P = np.roll(np.eye(7), 1, axis=0)
+    assert match_eigs(O.eig_real(P)[0], np.exp(2j * np.pi * np.arange(7) / 7)) < 1e-13
+
+
+def test_eig_real_degenerate():
+    """Zero matrix, nilpotent Jordan block, identity: eigenvalues exact, no failure."""
+    assert np.all(O.eig_real(np.zeros((4, 4)))[0] == 0)
+    J = np.diag(np.ones(4), 1)
+    lam, _ = O.eig_real(J)
+    assert np.all(lam == 0)
+    lam, W = O.eig_real(np.eye(3))
+    assert np.all(lam == 1) and np.linalg.matrix_rank(W) == 3
+
+
+def test_csolve_and_singular_detection():
+    rng = np.random.default_rng(50)
+    A = rng.standard_normal((30, 30)) + 1j * rng.standard_normal((30, 30))
+    b = rng.standard_normal(30) + 1j * rng.standard_normal(30)
+    x = O.csolve(A, b)
+    assert np.linalg.norm(x - np.linalg.solve(A, b)) < 1e-12 * np.linalg.norm(x)
+    A[:, 7] = 0.0
+    assert O.csolve(A, b) is None
+
+
+def test_clstsq_vs_lapack_and_rank():
+    rng = np.random.default_rng(51)
+    A = rng.standard_normal((40, 12)) + 1j * rng.standard_normal((40, 12))
+    b = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    x, rk = O.clstsq(A, b)
+    ref = np.linalg.lstsq(A, b, rcond=None)[0]
+    assert rk == 12 and np.linalg.norm(x - ref) < 1e-12 * np.linalg.norm(ref)
+    A[:, 3] = A[:, 5] * (2 - 1j)                    # rank 11: a basic solution with one zero
+    x, rk = O.clstsq(A, b)
+    ref = np.linalg.lstsq(A, b, rcond=None)[0]
+    assert rk == 11
+    assert abs(np.linalg.norm(A @ x - b) - np.linalg.norm(A @ ref - b)) < 1e-10 * np.linalg.norm(b)
+
+
+def _planted_zero_mode(n=300, m=6, orth=True, seed=60):
+    """Real modes, λ = {0, 0.9, -0.7, 0.5}: x_t = Σ b_j φ_j λ_j^t (so φ_0 appears in x_0 only)."""
+    rng = np.random.default_rng(seed)
+    lam = np.array([0.0, 0.9, -0.7, 0.5])
+    b = np.array([1.3, 0.8, -0.6, 1.1])
+    Phi = rng.standard_normal((n, 4))
+    if orth:
+        Phi, _ = np.linalg.qr(Phi)
+    X = np.stack([Phi @ (b * lam ** t) for t in range(m + 1)], axis=1)   # 0^0 = 1
+    return X, lam, b, Phi
+
+
+def test_amplitudes_singular_branch_planted_zero_eigenvalue():
+    """O9 singular branch (Q15): the window starting at t = 0 of planted
+    dynamics with λ_0 = 0 gives Ã an exact zero eigenvalue; the oracle flags W_SINGULAR, gives the
+    zero mode b = 0 and, with orthonormal modes (so that α₁'s zero-mode part is orthogonal to the
+    kept eigenvectors), recovers the planted b_j of the others as b_j φ_j."""
+    X, lam_p, b_p, Phi_p = _planted_zero_mode()
+    d = O.dmd_window(X)
+    assert d["r"] == 4 and d["amp_status"] == O.W_SINGULAR
+    lam = d["lam"]
+    assert match_eigs(lam, lam_p) < 1e-10
+    j0 = int(np.argmin(np.abs(lam)))
+    assert d["b"][j0] == 0
+    Phi = O.modes(X[:, 1:], d)
+    for j in range(4):
+        if j == j0:
+            continue
+        k = int(np.argmin(np.abs(lam_p - lam[j])))
+        assert np.linalg.norm(d["b"][j] * Phi[:, j] - b_p[k] * Phi_p[:, k]) < 1e-9 * abs(b_p[k])
+
+
+def test_amplitudes_singular_branch_is_least_squares_on_kept_modes():
+    """Non-orthogonal modes: the kept b are the least-squares solution of the kept columns of WΛ
+    (LAPACK lstsq on the test side), not the oblique (left-eigenvector) solution."""
+    X, lam_p, _, _ = _planted_zero_mode(orth=False, seed=61)
+    d = O.dmd_window(X)
+    assert d["amp_status"] == O.W_SINGULAR
+    keep = np.abs(d["lam"]) >= 1e-7 * np.abs(d["lam"]).max()
+    alpha1 = d["sigma"][:d["r"]] * d["V"][0, :d["r"]]
+    wl = d["W"] * d["lam"][None, :]
+    ref = np.linalg.lstsq(wl[:, keep], alpha1.astype(complex), rcond=None)[0]
+    assert np.linalg.norm(d["b"][keep] - ref) < 1e-10 * np.linalg.norm(ref)
+    assert np.all(d["b"][~keep] == 0)
+
+
+def test_amplitudes_all_zero_spectrum():
+    """Nilpotent window (x_t = 0 for t >= 1): every λ is 0 -> b = 0, W_SINGULAR, and the
+    background index reports E_NO_VIABLE_MODE."""
+    rng = np.random.default_rng(62)
+    X = np.zeros((50, 5))
+    X[:, 0] = rng.standard_normal(50)
+    with pytest.raises(O.OracleError):
+        O.dmd_window(X)                                # σ_1 > 0 but Ã = 0: no viable mode
+    G = O.gram(X)
+    d = O.dmd_from_gram(G)
+    b, st = O.amplitudes(d)
+    assert st == O.W_SINGULAR and np.all(b == 0) and np.all(d["lam"] == 0)
+
+
+def test_order_eigs_rule_Q12():
+    lam = np.array([0.5, -0.9, 0.9j, -0.9j, 0.9, 0.3 + 0.4j, 0.3 - 0.4j, 0.5])
+    o = O.order_eigs(lam)
+    # |λ| = 0.9 group: Re desc (0.9, then 0±0.9i, then -0.9), Im desc within equal Re
+    assert list(lam[o]) == [0.9, 0.9j, -0.9j, -0.9, 0.5, 0.5, 0.3 + 0.4j, 0.3 - 0.4j]
+    assert list(o[4:6]) == [0, 7]                      # equal keys keep input order
+
+
+def test_background_first_window_constant_video():
+    """Alg 3 first branch (Q24) on a constant video: λ_idx = 1, |L| = x in every column
+    e = 0..m, S ≈ 0, empty mask."""
+    rng = np.random.default_rng(63)
+    x = 0.1 + 0.8 * rng.random(400)
+    m = 8
+    Z = np.tile(x[:, None], (1, m + 1))
+    d = O.dmd_window(Z)
+    assert d["r"] == 1 and abs(d["lam"][d["idx"]] - 1) < 1e-13
+    L, S, mask = O.background_first_window([Z[:, k] for k in range(m + 1)], d, d["b"], d["idx"])
+    assert L.shape == (400, m + 1)
+    assert np.max(np.abs(S)) < 1e-12 and not mask.any()
+
+
+def test_background_first_window_planted_exponents():
+    """First branch uses exponents 0..m (Q24): on a planted rank-2 real decaying+constant video the
+    background mode's reconstruction reproduces that mode's part of every column."""
+    rng = np.random.default_rng(64)
+    n, m = 300, 6
+    bg = 0.5 + 0.1 * rng.random(n)
+    dec = rng.random(n) * 0.2
+    Z = np.stack([bg + dec * 0.6 ** t for t in range(m + 1)], axis=1)
+    d = O.dmd_window(Z)
+    L, S, _ = O.background_first_window([Z[:, k] for k in range(m + 1)], d, d["b"], d["idx"])
+    assert abs(d["lam"][d["idx"]] - 1) < 1e-10
+    assert np.max(np.abs(L - bg[:, None])) < 1e-9
+    assert np.max(np.abs(S - np.stack([dec * 0.6 ** t for t in range(m + 1)], axis=1))) < 1e-9
