@@ -688,10 +688,10 @@ def test_init_window_c4_full_size_sampled():
 
     def fr(t):
         if t not in cache:
-            cache[t] = vs.frame(t).numpy().astype(np.float64)
+            cache[t] = vs.frame(t).numpy()
         return cache[t]
     for i, j in ((0, 0), (0, 200), (57, 123), (199, 200), (200, 200), (123, 123)):
-        ref = float(np.dot(fr(i), fr(j)))
+        ref = float(O.gram_column([fr(i)], fr(j))[0])         # compensated oracle dot (O1)
         assert abs(G[i, j] - ref) <= 1e-12 * math.sqrt(G[i, i] * G[j, j]), (i, j)
     eng.close()
 
@@ -872,10 +872,10 @@ def test_c4_full_size_sampled():
     G = eng.gram()
     assert np.allclose(G, G.T, rtol=0, atol=0)
     t = T - 1
-    x_t = vs.frame(t).numpy().astype(np.float64)
+    x_t = vs.frame(t).numpy()
     for k in (0, 57, 199, 200):
-        z = vs.frame(t - m + k).numpy().astype(np.float64)
-        ref = float(np.dot(z, x_t))
+        z = vs.frame(t - m + k).numpy()
+        ref = float(O.gram_column([z], x_t)[0])                # compensated oracle dot (O1)
         assert abs(G[k, m] - ref) <= 1e-12 * math.sqrt(G[k, k] * G[m, m]), k
     low, sp, mask, fb = eng.background()
     assert fb == T - 1 - lag
@@ -1106,10 +1106,11 @@ def test_c3_full_size_sampled():
     eng.sync()
     G = eng.gram()
     t = T - 1
-    x_t = vs.frame(t).numpy().astype(np.float64)
+    x_t = vs.frame(t).numpy()
     for k in (0, 33, 99, 100):
-        z = vs.frame(t - m + k).numpy().astype(np.float64)
-        assert abs(G[k, m] - float(np.dot(z, x_t))) <= 1e-12 * math.sqrt(G[k, k] * G[m, m]), k
+        z = vs.frame(t - m + k).numpy()
+        ref = float(O.gram_column([z], x_t)[0])                # compensated oracle dot (O1)
+        assert abs(G[k, m] - ref) <= 1e-12 * math.sqrt(G[k, k] * G[m, m]), k
     low, sp, mask, fb = eng.background()
     x = vs.frame(fb).numpy().astype(np.float64)
     assert np.max(np.abs(low.astype(np.float64) + sp - x)) < 1e-6
