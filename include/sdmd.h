@@ -34,6 +34,12 @@
  *  - Device-detected errors (non-finite frame) are recorded in a device status word; the frame
  *    is rejected ON THE DEVICE (state bit-identical) and every frame pushed after it is
  *    discarded until the next sdmd_sync(), which returns the error and the rejected frame index.
+ *    The device also sets a host-visible mirror of the status; a push (or sdmd_acquire_slot)
+ *    whose ring slot could hold data the rolled-back state still needs first waits for the
+ *    commit of the frame `D` pushes earlier (D = ring slots − frames the state reads, >= 8 thanks
+ *    to spare slots) and, if the stream is poisoned, returns SDMD_E_NONFINITE WITHOUT writing or
+ *    enqueuing anything; call sdmd_sync to learn the rejected frame and resume.  The host thus
+ *    never runs more than D frames ahead of the device's commits.
  *  - One writer per ctx.  With nranks > 1, sdmd_init_window and sdmd_push_* are collective:
  *    every rank calls them in the same order (NCCL semantics).
  *

@@ -6,11 +6,16 @@ call does, and fails loudly if it was not built (there is no CPU fallback).
 """
 import os as _os
 
-# The engine runs the Gram pass, the copy stream and up to 2·workers eigen streams concurrently;
-# CUDA's default of 8 hardware work queues makes some of them share a queue, so an eigen stage
-# waits behind an unrelated stream-wait (measured +5.5 ms per frame of K4 latency).  Only
-# effective if set before CUDA initialises in this process; an explicit user setting wins.
-_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+def recommended_env() -> None:
+    """Opt-in helper: set CUDA_DEVICE_MAX_CONNECTIONS=32 unless the user set it.  The engine runs
+    the Gram pass, the copy stream and up to 2·workers eigen streams concurrently; CUDA's default of
+    8 hardware work queues makes some of them share a queue, so an eigen stage waits behind an
+    unrelated stream-wait (measured +5.5 ms per frame of K4 latency).  Only effective if called
+    before CUDA initialises in this process; importing the package does NOT change the environment
+    (other libraries in the process may rely on their own setting)."""
+    _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 
 from .sdmd import (StreamingDMD, SDMDError, lib, nccl_unique_id, row_partition,  # noqa: F401
                    LIB_PATH, EXPORTS)

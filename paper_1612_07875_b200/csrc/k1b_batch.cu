@@ -57,7 +57,7 @@ static __device__ void commit_batch(const double* gout, int k, int m, long long 
     if (!isfinite(gout[e])) atomicMin(&bad, e / (m + 1));
   __syncthreads();
   if (bad != 0x7fffffff) {
-    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f0 + bad; }
+    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f0 + bad; poison_mirror(st); }
     return;
   }
   for (int e = threadIdx.x; e < k * (m + 1); e += blockDim.x) {

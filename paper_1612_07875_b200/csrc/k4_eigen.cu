@@ -1117,6 +1117,7 @@ k4a_kernel(const K4Params p) {
       for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
       if (tid == 0) {
         res->frame = f; res->status = 4; res->r = 0; res->idx = -1; res->sweeps = sweeps; res->vframe = -1;
+        res->nkeep = 0; res->nB = 0;
         res->qr_its = 0; res->sigma1 = sig[0];
       }
     }
@@ -1310,7 +1311,7 @@ k4a_kernel(const K4Params p) {
     p.tau[r > 0 ? r - 1 : 0] = 0.0;
     ph[5] = clock64();
     res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
-    res->qr_its = 0; res->sigma1 = sig[0];
+    res->qr_its = 0; res->sigma1 = sig[0]; res->nkeep = r; res->nB = 0;
     res->vframe = converged ? f : -1;            // V usable as the next warm start
     for (int q = 0; q < 5; ++q) res->phase[q] = ph[q + 1] - ph[q];
     res->phase[5] = res->phase[6] = 0;
@@ -1322,7 +1323,7 @@ k4a_kernel(const K4Params p) {
 // background index, inverse iteration for w_idx / y_idx, b_idx and the background coefficients.
 __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   extern __shared__ __align__(16) unsigned char k4_smem[];
-  __shared__ int sh_status, sh_idx, sh_its, sh_go;
+  __shared__ int sh_status, sh_idx, sh_its, sh_go, sh_nkeep;
   __shared__ long long ph[8];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = p.m;
@@ -1419,6 +1420,17 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     }
     sh_idx = best;
     if (best < 0 && sh_status == 0) sh_status = 7;
+    // reading Q15: WΛ is singular when some |λ_j| < rank_tol·max|λ|; those
+    // modes form a suffix of the sorted λ.  Flag W_SINGULAR; the kept-mode least squares of b
+    // (and c) is redone by k4s_kernel right after this kernel on the same stream.
+    const double a0 = r > 0 ? cabs2(p.lam[0]) : 0.0;
+    int nk = 0;
+    if (a0 > 0.0) {
+      nk = r;
+      while (nk > 0 && !(cabs2(p.lam[nk - 1]) >= p.rank_tol * a0)) --nk;
+    }
+    sh_nkeep = nk;
+    if (nk < r && sh_status == 0) sh_status = 6;
   }
   __syncthreads();
   const int idx = sh_idx;
@@ -1527,6 +1539,8 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
       res->b_idx[0] = b0.x; res->b_idx[1] = b0.y; res->sigma1 = sigma1;
+      res->nkeep = sh_nkeep; res->nB = nb_eff;
+      for (int q = 0; q < nb_eff; ++q) res->bset[q] = bset[q];
     }
     return;
   }
@@ -1574,12 +1588,13 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
       res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sigma1;
+      res->nkeep = sh_nkeep; res->nB = 1; res->bset[0] = idx;
     }
   } else if (idx < 0) {
     for (int i = tid; i < m; i += K4_THREADS) p.cout[i] = make_double2(0.0, 0.0);
     if (tid == 0) {
       res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
-      res->qr_its = sh_its; res->sigma1 = sigma1;
+      res->qr_its = sh_its; res->sigma1 = sigma1; res->nkeep = sh_nkeep; res->nB = 0;
     }
   }
 }
@@ -1656,6 +1671,129 @@ __global__ void __launch_bounds__(32) k4_vecs_kernel(const K4VecParams p) {
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s) {
   const size_t smem = 5 * (size_t)p.r * sizeof(double2) + (size_t)p.r * sizeof(int) + 16;
   k4_vecs_kernel<<<count, 32, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------ W_SINGULAR amplitudes (reading Q15) --------
+// One warp per CTA.  (1) The CTAs compute the right eigenvectors of the kept modes j < nkeep by
+// inverse iteration on the Hessenberg form (CTA c: j = c, c + grid, …; its own LU workspace).
+// (2) The last CTA to finish solves min ‖A b − α₁‖, A = W_K diag(λ_K) (r x nkeep), by complex
+// Householder QR (reflector H = I − 2 v vᴴ / vᴴv, v = x + e^{i arg x₀}‖x‖e₁) and back-
+// substitution; b_j = 0 for j >= nkeep.  (3) Per frame it rewrites the background coefficients
+// c = Σ_{q∈B} b_q λ_q^m Y w_q and b_idx.  Per frame the kernel returns at once unless this frame's
+// K4b flagged W_SINGULAR with nkeep < r.
+__global__ void __launch_bounds__(32) k4s_kernel(const K4SingParams p, int vecs) {
+  extern __shared__ __align__(16) unsigned char ss_smem[];
+  __shared__ int am_last;
+  const int lane = threadIdx.x;
+  int r, nk, m = p.m;
+  if (p.res) {
+    const volatile K4Result* vr = p.res;
+    if (vr->frame != p.f || vr->status != 6) return;
+    r = vr->r;
+    nk = vr->nkeep;
+    if (nk >= r) return;
+  } else {
+    r = p.r;
+    nk = p.nkeep;
+  }
+  const int R = p.r;                                  // workspace stride (r_max per frame)
+  double2* z = reinterpret_cast<double2*>(ss_smem);
+  double2* rhs = z + R;
+  double2* lk = rhs + R;
+  double2* bsh = lk + R;
+  int* swk = reinterpret_cast<int*>(bsh + R);
+  if (vecs) {
+    double2* M = p.Mws + (long long)blockIdx.x * R * R;
+    for (int j = blockIdx.x; j < nk; j += gridDim.x)
+      inverse_iteration(p.H, p.Qv, p.tau, r, p.lam[j], M, z, rhs, lk, swk, p.W + (long long)j * r,
+                        nullptr, lane);
+    __threadfence();
+    if (lane == 0) am_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
+    __syncwarp();
+    if (!am_last) return;
+    __threadfence();
+    if (lane == 0) *p.counter = 0u;
+  }
+  // (2) least squares on A = W_K Λ_K
+  double2* A = p.A;
+  for (int e = lane; e < r * nk; e += 32) {
+    const int i = e % r, j = e / r;
+    A[(long long)j * r + i] = cmul(__ldcg(p.W + (long long)j * r + i), p.lam[j]);
+  }
+  for (int i = lane; i < r; i += 32) rhs[i] = make_double2(p.alpha1[i], 0.0);
+  __syncwarp();
+  for (int k = 0; k < nk; ++k) {
+    double s2 = 0.0;
+    for (int i = k + lane; i < r; i += 32) { const double2 a = A[(long long)k * r + i]; s2 += a.x * a.x + a.y * a.y; }
+    s2 = wsum(s2);
+    const double nrm = sqrt(s2);
+    if (nrm == 0.0) continue;                          // R_kk = 0: b_k = 0 below
+    const double2 x0 = A[(long long)k * r + k];
+    const double ax0 = cabs2(x0);
+    const double2 ph = ax0 > 0.0 ? make_double2(x0.x / ax0, x0.y / ax0) : make_double2(1.0, 0.0);
+    const double vv = 2.0 * nrm * (nrm + ax0);
+    for (int i = k + lane; i < r; i += 32)           // v in z[k..r)
+      z[i] = (i == k) ? cadd(x0, make_double2(ph.x * nrm, ph.y * nrm)) : A[(long long)k * r + i];
+    __syncwarp();
+    for (int j = k; j <= nk; ++j) {                    // columns k..nk-1, then the right-hand side
+      double2* col = (j < nk) ? A + (long long)j * r : rhs;
+      double2 d = make_double2(0.0, 0.0);
+      for (int i = k + lane; i < r; i += 32) d = cadd(d, cmul(cconj(z[i]), col[i]));
+      d = wsum2(d);
+      d = make_double2(2.0 * d.x / vv, 2.0 * d.y / vv);
+      __syncwarp();
+      for (int i = k + lane; i < r; i += 32) col[i] = csub(col[i], cmul(z[i], d));
+      __syncwarp();
+    }
+  }
+  for (int i = nk - 1; i >= 0; --i) {                  // R b = (Qᴴα₁)[0:nk]
+    double2 sacc = make_double2(0.0, 0.0);
+    for (int j = i + 1 + lane; j < nk; j += 32) sacc = cadd(sacc, cmul(A[(long long)j * r + i], bsh[j]));
+    sacc = wsum2(sacc);
+    if (lane == 0) {
+      const double2 d = A[(long long)i * r + i];
+      bsh[i] = cabs2(d) > 0.0 ? cdiv(csub(rhs[i], sacc), d) : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+  }
+  for (int j = lane; j < r; j += 32) p.b[j] = j < nk ? bsh[j] : make_double2(0.0, 0.0);
+  __syncwarp();
+  if (p.cout && p.res) {                              // (3) background coefficients of the set B
+    const int nB = p.res->nB;
+    for (int i = lane; i < m; i += 32) {
+      double2 cc = make_double2(0.0, 0.0);
+      for (int q = 0; q < nB; ++q) {
+        const int jq = p.res->bset[q];
+        if (jq < 0 || jq >= nk) continue;
+        double2 pw = make_double2(1.0, 0.0), base = p.lam[jq];
+        for (int e = m; e > 0; e >>= 1) {
+          if (e & 1) pw = cmul(pw, base);
+          base = cmul(base, base);
+        }
+        const double2 coef = cmul(bsh[jq], pw);
+        double2 sacc = make_double2(0.0, 0.0);
+        for (int j = 0; j < r; ++j) {
+          const double yv = p.Y[(long long)j * m + i];
+          const double2 wv = __ldcg(p.W + (long long)jq * r + j);
+          sacc = cadd(sacc, make_double2(yv * wv.x, yv * wv.y));
+        }
+        cc = cadd(cc, cmul(coef, sacc));
+      }
+      p.cout[i] = cc;
+    }
+    if (lane == 0) {
+      const int idx = p.res->idx;
+      const double2 bi = (idx >= 0 && idx < nk) ? bsh[idx] : make_double2(0.0, 0.0);
+      p.res_out->b_idx[0] = bi.x;
+      p.res_out->b_idx[1] = bi.y;
+    }
+  }
+}
+
+cudaError_t launch_k4_singular(const K4SingParams& p, bool vecs, cudaStream_t s) {
+  const size_t smem = 4 * (size_t)p.r * sizeof(double2) + (size_t)p.r * sizeof(int) + 16;
+  k4s_kernel<<<vecs ? kSingVecGrid : 1, 32, smem, s>>>(p, vecs ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -22,7 +22,9 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <deque>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sdmd.h"
@@ -91,6 +93,13 @@ static std::mutex g_groups_mu;
 static std::map<std::string, LocalGroup*> g_groups;
 
 constexpr int kEvents = 256;      // > NWS + lag: event slots are reused modulo kEvents
+// Ring slots beyond what the window (and the background lag) needs.  After a rejected frame p the
+// state rolls back to "p frames committed"; the pushes that follow p before the host learns of
+// the rejection still write ring slots.  Writes of frames p+1 .. p+D-1 land in slots of frames
+// older than anything the rolled-back state reads (D = NS - frames needed, see ring_guard), so the
+// host only has to check the poison mirror once frame t-D has committed before writing frame t.
+// The spare slots raise D, so the host may run D frames ahead of the device without waiting.
+constexpr int kRingSpare = 6;
 
 // Per-frame eigen workspace (K4a writes the factors, K4b reads them); indexed by frame mod NWS so
 // that K4a of a later frame never overwrites a workspace whose K4b is still pending.
@@ -150,6 +159,14 @@ struct sdmd_ctx {
   double2* pm_b[kMaxWorkers]{};
   double* pm_T[kMaxWorkers]{};
   double2* pm_phi[kMaxWorkers]{};
+  // W_SINGULAR amplitudes (k4s_kernel), per single-CTA worker stream: LU workspaces, kept
+  // eigenvectors, least-squares matrix, b, last-block counters; and the on-demand LS matrix
+  double2* sg_M[kMaxWorkers]{};
+  double2* sg_W[kMaxWorkers]{};
+  double2* sg_A[kMaxWorkers]{};
+  double2* sg_b[kMaxWorkers]{};
+  unsigned int* sg_cnt = nullptr;
+  double2* od_A = nullptr;
   // workers
   Workspace ws[kMaxWS];
   int NWS = 0, Wa = 1, Wb = 4;
@@ -184,6 +201,16 @@ struct sdmd_ctx {
   struct TL { long long f; int kind; cudaEvent_t a, b; };   // timeline view of the events above
   std::vector<TL> tl;
   long long launches = 0;
+  // rejection mirror (mapped pinned host word, written by the device on every rejection) and the
+  // ring-write guard: frames < known_clean are known to be committed without a rejection
+  int* h_poison = nullptr;
+  int* d_poison = nullptr;
+  long long known_clean = 0;
+  int guard_d = 2;
+  long long fenced = -1;                // eigen tasks of frames <= fenced are fenced before commits
+  // frames whose eigenproblems were enqueued on this rank, with their single-CTA worker stream
+  // (flow control of push_batch and the Gram-history / ring reuse fences)
+  std::deque<std::pair<long long, int>> solved;
   // nccl
   ncclComm_t comm = nullptr;
   LocalGroup* lgroup = nullptr;           // SDMD_LOCAL_GROUP test backend
@@ -312,6 +339,42 @@ static inline long long first_dmd(const sdmd_ctx* c) { return c->cfg.buildup ? 1
 // window width of frame f's DMD (X has w columns)
 static inline int win_of(const sdmd_ctx* c, long long f) { return f < c->cfg.m ? (int)f : c->cfg.m; }
 
+// Ring-write guard (header contract: a rejected frame leaves the state bit-identical).  Writing
+// ring slots for frames up to t_last is safe unless a frame <= t_last - guard_d was rejected (the
+// slots the rolled-back state reads would be overwritten, see kRingSpare).  The device records
+// every rejection in the mapped host word h_poison; once the commit of frame t_last - guard_d is
+// known complete and the mirror is clear, the writes cannot harm.  Returns SDMD_E_NONFINITE
+// (nothing written, nothing enqueued) if the stream is poisoned; sdmd_sync reports and clears it.
+static int ring_guard(sdmd_ctx* c, long long t_last) {
+  if (*(volatile int*)c->h_poison) {
+    c->err = "stream poisoned by a rejected frame: call sdmd_sync";
+    return SDMD_E_NONFINITE;
+  }
+  const long long fchk = t_last - c->guard_d;
+  if (fchk >= c->known_clean) {
+    CK(cudaEventSynchronize(c->ev_commit[fchk % kEvents]));
+    if (*(volatile int*)c->h_poison) {
+      c->err = "stream poisoned by a rejected frame: call sdmd_sync";
+      return SDMD_E_NONFINITE;
+    }
+    c->known_clean = fchk + 1;
+  }
+  return SDMD_OK;
+}
+
+// Make the ctx stream wait until every eigen task of a frame <= thr has finished (per single-CTA
+// worker stream: its newest such frame; stream order covers the older ones).  Used before a
+// commit overwrites Gram-history rows (or a ring slot) that those tasks read.
+static int wait_solved_upto(sdmd_ctx* c, long long thr) {
+  long long best[kMaxWorkers];
+  for (int w = 0; w < kMaxWorkers; ++w) best[w] = -1;
+  for (auto it = c->solved.rbegin(); it != c->solved.rend(); ++it)
+    if (it->first <= thr && it->first > best[it->second]) best[it->second] = it->first;
+  for (int w = 0; w < c->Wb; ++w)
+    if (best[w] >= 0) CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, best[w]) % kEvents], 0));
+  return SDMD_OK;
+}
+
 // ------------------------------------------------------------------------- ABI ----------------
 extern "C" {
 
@@ -432,6 +495,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // per-frame modes read X'_f on the worker stream up to ~lag frames after f was pushed: the ring
   // keeps lag + 2 more slots, and push t waits for frame t-lag-2's worker (see enqueue_frame)
   if (c->cfg.modes_every_frame && c->NS < m + c->L + 3) c->NS = m + c->L + 3;
+  c->NS += kRingSpare;
+  // frames the rolled-back state may still read: the window (m), or with the fused background
+  // the window of the oldest pending background frame (m + L - 1)
+  c->guard_d = c->NS - (c->cfg.background ? m + c->L - 1 : m);
   c->NH = 2 * (m + c->L + 4);
   c->NC = c->L + 2;
   c->es = c->cfg.dtype == SDMD_F32 ? 4 : 8;
@@ -509,7 +576,14 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->k3_chunks = (c->cfg.nnz_cap + 2047) / 2048;
   }
   AL(c->dst, 1);
-  cudaMemsetAsync(c->dst, 0, sizeof(DevState), c->stream);
+  if (cudaHostAlloc((void**)&c->h_poison, sizeof(int), cudaHostAllocMapped) != cudaSuccess) return bail(SDMD_E_OOM);
+  *(volatile int*)c->h_poison = 0;
+  if (cudaHostGetDevicePointer((void**)&c->d_poison, c->h_poison, 0) != cudaSuccess) return bail(SDMD_E_CUDA);
+  {
+    DevState hs0{};
+    hs0.hpoison = c->d_poison;
+    if (cudaMemcpy(c->dst, &hs0, sizeof(hs0), cudaMemcpyHostToDevice) != cudaSuccess) return bail(SDMD_E_CUDA);
+  }
   AL(c->ghist, (size_t)c->NH * (m + 1));
   cudaMemsetAsync(c->ghist, 0, (size_t)c->NH * (m + 1) * sizeof(double), c->stream);
   AL(c->cbuf, (size_t)c->NC * m);
@@ -570,6 +644,17 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       AL(c->pm_T[w], 2 * (size_t)m * rm);
       AL(c->pm_phi[w], (size_t)c->ld * rm);
     }
+  }
+  if (c->cfg.dmd) {
+    const size_t rm = (size_t)c->cfg.r_max;
+    for (int w = 0; w < c->Wb; ++w) {
+      AL(c->sg_M[w], (size_t)kSingVecGrid * rm * rm);
+      AL(c->sg_W[w], rm * rm);
+      AL(c->sg_A[w], rm * rm);
+      AL(c->sg_b[w], rm);
+    }
+    AL(c->sg_cnt, (size_t)kMaxWorkers);
+    cudaMemsetAsync(c->sg_cnt, 0, kMaxWorkers * sizeof(unsigned int), c->stream);
   }
   for (int i = 0; i < kEvents; ++i) {
     if (cudaEventCreateWithFlags(&c->ev_commit[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -661,7 +746,7 @@ int sdmd_destroy(sdmd_ctx* c) {
   }
   void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
                   c->sp_val, c->sp_nnz, c->scratch, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
-                  c->Gtmp, c->init_work};
+                  c->Gtmp, c->init_work, c->sg_cnt, c->od_A};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int w = 0; w < kMaxWS; ++w) {
@@ -674,11 +759,13 @@ int sdmd_destroy(sdmd_ctx* c) {
   for (int w = 0; w < kMaxWorkers; ++w) {
     if (c->sa[w]) cudaStreamDestroy(c->sa[w]);
     if (c->sb[w]) cudaStreamDestroy(c->sb[w]);
-    void* pm[] = {c->pm_M[w], c->pm_W[w], c->pm_b[w], c->pm_T[w], c->pm_phi[w]};
+    void* pm[] = {c->pm_M[w], c->pm_W[w], c->pm_b[w], c->pm_T[w], c->pm_phi[w], c->sg_M[w], c->sg_W[w],
+                  c->sg_A[w], c->sg_b[w]};
     for (void* q : pm)
       if (q) cudaFree(q);
   }
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  if (c->h_poison) cudaFreeHost(c->h_poison);
   delete c;
   return SDMD_OK;
 }
@@ -726,6 +813,16 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   if ((e = cudaStreamWaitEvent(B, c->ev_a[q % kEvents], 0)) != cudaSuccess) return e;
   if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
   if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
+  {                                             // W_SINGULAR frames only (device-side decision)
+    const int sw = (int)(q % c->Wb);
+    K4SingParams sp{};
+    sp.r = c->cfg.r_max; sp.m = p.m; sp.f = t; sp.res = p.res; sp.res_out = p.res;
+    sp.H = p.H; sp.Qv = p.Qv; sp.tau = p.tau; sp.lam = p.lam; sp.alpha1 = p.alpha1; sp.Y = p.Y;
+    sp.Mws = c->sg_M[sw]; sp.W = c->sg_W[sw]; sp.A = c->sg_A[sw]; sp.b = c->sg_b[sw];
+    sp.cout = p.cout; sp.counter = c->sg_cnt + sw;
+    if ((e = launch_k4_singular(sp, true, B)) != cudaSuccess) return e;
+    c->launches += 1;
+  }
   if (c->timing) { cudaEventRecord(kb.second, B); c->k4_ev.push_back(kb); c->tl.push_back({t, 2, kb.first, kb.second}); }
   if (c->cfg.modes_every_frame) {               // NEXT-2: Φ_t = X'_t (Y W) for all r modes
     const int sw = (int)(q % c->Wb), rm = c->cfg.r_max, w = win_of(c, t);
@@ -740,6 +837,8 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
     c->launches += 3;
   }
   if ((e = cudaEventRecord(c->ev_done[q % kEvents], B)) != cudaSuccess) return e;
+  c->solved.emplace_back(t, (int)(q % c->Wb));
+  while (c->solved.size() > 1024) c->solved.pop_front();
   c->launches += 2;
   ws_of(c, t).vecs_frame = -1;
   c->last_dmd = t;
@@ -767,6 +866,14 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     // on the K4-bound configs: an unthrottled stream floods the worker queues, profiles/r2h…)
     const long long fw = t - c->L - 2;
     CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fw) % kEvents], 0));
+  }
+  if (c->cfg.dmd && t - c->NH + m > c->fenced) {
+    // Gram-history reuse fence: the commit of t overwrites the row of frame t - NH, read by the
+    // eigen tasks of frames up to t - NH + m; fence every worker up to t - L - 2 (covers the next
+    // NH - m - L - 2 commits at the cost of one wait per worker)
+    const int st_ = wait_solved_upto(c, t - c->L - 2);
+    if (st_) return st_;
+    c->fenced = t - c->L - 2;
   }
   if (bg && c->cfg.dmd) {
     const long long fb = t - c->L;
@@ -858,6 +965,7 @@ int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "push_dense on a sparse context");
   CK(cudaSetDevice(c->dev));
   const long long t = c->frames;
+  if (int g = ring_guard(c, t)) return g;
   char* dst = (char*)c->ring + (size_t)(t % c->NS) * c->ld * c->es;
   if (where == SDMD_HOST) {
     // H2D on the copy stream so it overlaps K1(t-1): slot t mod NS was last read by K1(t-2)
@@ -874,6 +982,8 @@ int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
 int sdmd_acquire_slot(sdmd_ctx* c, void** dev_ptr) {
   if (!c || !dev_ptr) return invalid(c, "acquire_slot: bad argument");
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "acquire_slot on a sparse context");
+  CK(cudaSetDevice(c->dev));
+  if (int g = ring_guard(c, c->frames)) return g;
   *dev_ptr = (char*)c->ring + (size_t)(c->frames % c->NS) * c->ld * c->es;
   return SDMD_OK;
 }
@@ -895,6 +1005,14 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
   const long long t = c->frames;
   if (t < m + 1) { c->err = "push_batch: window not full (use push_dense during warm-up)"; return SDMD_E_STATE; }
   CK(cudaSetDevice(c->dev));
+  if (int g = ring_guard(c, t + k - 1)) return g;
+  // flow control and reuse fences: the commits of frames t..t+k-1 overwrite Gram-
+  // history rows (and, with per-frame modes, ring slots) that eigen tasks of frames up to
+  // t+k-1-L-2 may read; wait for them on the device, like enqueue_frame's throttle
+  if (c->cfg.dmd) {
+    if (int w = wait_solved_upto(c, t + k - 1 - c->L - 2)) return w;
+    c->fenced = t + k - 1 - c->L - 2;
+  }
   const cudaMemcpyKind kind = where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   // the k frames into slots t..t+k-1 (mod NS; at most two contiguous runs).  Those slots last
   // held frames ≤ t-m-1, read only by Gram passes already ordered before this on the ctx stream.
@@ -958,6 +1076,7 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
     }
   }
   const long long t = c->frames;
+  if (int g = ring_guard(c, t)) return g;
   const int slot = (int)(t % c->NS);
   int* sidx = c->sp_idx + (size_t)slot * c->cfg.nnz_cap;
   double* sval = c->sp_val + (size_t)slot * c->cfg.nnz_cap;
@@ -993,7 +1112,11 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   if (st) return st;
   const int m = c->cfg.m, k = m + 1;
   // fresh state: frames 0..m occupy slots 0..m
-  CK(cudaMemsetAsync(c->dst, 0, sizeof(DevState), c->stream));
+  {
+    DevState z{};
+    z.hpoison = c->d_poison;                 // the rejection mirror survives the reset
+    CK(cudaMemcpyAsync(c->dst, &z, sizeof(z), cudaMemcpyHostToDevice, c->stream));
+  }
   CK(cudaMemsetAsync(c->ghist, 0, (size_t)c->NH * (m + 1) * sizeof(double), c->stream));
   CK(cudaMemcpy2DAsync(c->ring, c->ld * c->es, Z, (size_t)ldz * c->es, c->cfg.n_local * c->es, k,
                        where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
@@ -1031,6 +1154,11 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   DevState hs{};
   hs.committed = k;
   hs.bg_frame = -1;
+  hs.hpoison = c->d_poison;
+  *(volatile int*)c->h_poison = 0;
+  c->known_clean = k;
+  c->fenced = -1;
+  c->solved.clear();
   CK(cudaMemcpyAsync(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int f = 0; f < k; ++f) CK(cudaEventRecord(c->ev_k1[f % kEvents], c->stream));
@@ -1078,6 +1206,10 @@ int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
     (void)m;
     hs.status = 0;
     CK(cudaMemcpy(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    *(volatile int*)c->h_poison = 0;
+    if (c->known_clean > hs.committed) c->known_clean = hs.committed;
+    if (c->fenced > hs.committed - 1) c->fenced = hs.committed - 1;
+    while (!c->solved.empty() && c->solved.back().first >= hs.committed) c->solved.pop_back();
     c->err = "frame " + std::to_string(hs.failed_frame) +
              " rejected (non-finite Gram column, or invalid device-side sparse indices)";
     return SDMD_E_NONFINITE;
@@ -1179,6 +1311,14 @@ static int ensure_vecs(sdmd_ctx* c) {
     p.j0 = j0;
     const int cnt = r - j0 < c->mws_chunk ? r - j0 : c->mws_chunk;
     CK(launch_k4_vecs(p, cnt, c->stream));
+    c->launches += 1;
+  }
+  if (res.status == SDMD_W_SINGULAR && res.nkeep < r) {   // kept-mode least squares (Q15)
+    if (!c->od_A && dalloc(&c->od_A, (size_t)R * R) != cudaSuccess) return SDMD_E_OOM;
+    K4SingParams sp{};
+    sp.r = r; sp.nkeep = res.nkeep; sp.H = k.H; sp.Qv = k.Qv; sp.tau = k.tau; sp.lam = k.lam;
+    sp.alpha1 = k.alpha1; sp.W = c->Wall; sp.A = c->od_A; sp.b = c->ball;
+    CK(launch_k4_singular(sp, false, c->stream));
     c->launches += 1;
   }
   CK(cudaStreamSynchronize(c->stream));

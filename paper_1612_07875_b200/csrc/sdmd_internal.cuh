@@ -31,7 +31,17 @@ struct DevState {
   unsigned int k1_done;       // last-block counter of K1
   unsigned int k3_done;       // last-block counter of K3
   unsigned int pad1[2];
+  int* hpoison;               // device alias of a mapped pinned host word, set to 1 by every rejection
+                              // (the host reads it to refuse ring-slot writes while poisoned)
 };
+
+// Record a rejection (the caller already set status / failed_frame) in the host-visible mirror.
+static __device__ __forceinline__ void poison_mirror(DevState* st) {
+  if (st->hpoison) {
+    *(volatile int*)st->hpoison = 1;
+    __threadfence_system();
+  }
+}
 
 struct K1Params {
   const void* ring;
@@ -90,6 +100,34 @@ struct K4Result {
   int qr_cnt[4];              // QR: single-bulge steps, multishift steps, single-bulge its, multishift sweeps
   long long qr_dbg[2];        // SM cycles of the multishift chase: (AB) phase + barrier, (C) phase + barrier (warp 0)
   long long vframe;           // frame whose converged eigenvectors V this workspace holds (K4a), or -1
+  int nkeep;                  // modes with |λ_j| >= rank_tol·max|λ| (a prefix of the sorted λ); < r → W_SINGULAR
+  int nB;                     // background mode set of this frame (B[0] = idx)
+  int bset[kMaxBgModes + 1];
+};
+
+// W_SINGULAR amplitudes (reading Q15): the modes j >= nkeep get b_j = 0, the
+// kept ones the least-squares solution of min ‖W_K Λ_K b − α₁‖ (K = 0..nkeep-1).  Per frame
+// (res != null) both kernels return at once unless the frame's K4b flagged it singular; then
+// they recompute b over the kept modes and the background coefficients c.
+struct K4SingParams {
+  int r;                      // r (on-demand) or r_max (per frame: r, nkeep read from res)
+  int m;                      // window width (per frame)
+  long long f;                // frame (per frame)
+  const K4Result* res;        // per frame: the frame's summary (else null)
+  K4Result* res_out;          // per frame: b_idx updated here
+  int nkeep;                  // on demand
+  const double* H;
+  const double* Qv;
+  const double* tau;
+  const double2* lam;
+  const double* alpha1;
+  const double* Y;            // m x r (per frame: for c)
+  double2* Mws;               // [grid][r_max^2] inverse-iteration LU workspaces
+  double2* W;                 // r x r column-major: kept right eigenvectors (ld r)
+  double2* A;                 // r x r workspace of the least squares
+  double2* b;                 // r amplitudes (output)
+  double2* cout;              // m background coefficients (per frame) or null
+  unsigned int* counter;      // last-block counter (zero between launches)
 };
 
 struct K4Params {
@@ -176,7 +214,7 @@ static __device__ __forceinline__ void commit_block(const double* gout, int nd, 
     if (!isfinite(gout[k])) bad = 1;
   __syncthreads();
   if (bad) {
-    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f_new; }
+    if (threadIdx.x == 0) { st->status = 2 /*SDMD_E_NONFINITE*/; st->failed_frame = f_new; poison_mirror(st); }
     return;
   }
   double* row = ghist + (long long)(f_new % NH) * (m + 1);
@@ -207,6 +245,8 @@ cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
 size_t k4_smem_bytes(int r_max, int m, int bg_modes);
 int k4_cluster_size();
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
+cudaError_t launch_k4_singular(const K4SingParams& p, bool vecs, cudaStream_t s);
+constexpr int kSingVecGrid = 16;          // CTAs (one warp each) of the singular-path eigenvectors
 cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long n, int k,
                              double* Gout, double* work, cudaStream_t s);
 size_t init_gram_work_elems(long long n, int k);

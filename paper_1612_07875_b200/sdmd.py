@@ -147,6 +147,39 @@ def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data), HOST
 
 
+_TORCH_NP = {"torch.float32": np.float32, "torch.float64": np.float64, "torch.int32": np.int32}
+
+
+def _checked(a, np_dtype, count: int, what: str, n: int | None = None):
+    """(obj, pointer, where) of an input buffer after checking that it holds at least ``count``
+    elements of ``np_dtype`` contiguously (the library reads raw memory).  Torch tensors must be
+    contiguous with the exact dtype; numpy arrays (or lists) of another dtype or layout are
+    converted here, and the converted object is returned so that the caller keeps it alive until
+    the (possibly asynchronous) copy has run."""
+    if hasattr(a, "data_ptr"):
+        dt = _TORCH_NP.get(str(a.dtype))
+        if dt is not np_dtype:
+            raise TypeError(f"{what}: tensor dtype {a.dtype} does not match the engine dtype "
+                            f"{np.dtype(np_dtype).name}")
+        if not a.is_contiguous():
+            raise ValueError(f"{what}: tensor must be contiguous (pass .contiguous())")
+        if a.numel() < count:
+            raise ValueError(f"{what}: {a.numel()} elements, need {count}")
+        return a, ctypes.c_void_p(a.data_ptr()), (DEVICE if a.is_cuda else HOST)
+    arr = np.asarray(a)
+    if arr.ndim <= 1:
+        if arr.dtype != np_dtype or not arr.flags.c_contiguous:
+            arr = np.ascontiguousarray(arr, dtype=np_dtype)
+    elif n is not None and arr.ndim == 2 and arr.shape[0] == n and arr.shape[1] != n:
+        if arr.dtype != np_dtype or not arr.flags.f_contiguous:
+            arr = np.asfortranarray(arr, dtype=np_dtype)        # (n, k): columns contiguous
+    elif arr.dtype != np_dtype or not arr.flags.c_contiguous:
+        arr = np.ascontiguousarray(arr, dtype=np_dtype)         # (k, n): rows contiguous
+    if arr.size < count:
+        raise ValueError(f"{what}: {arr.size} elements, need {count}")
+    return arr, ctypes.c_void_p(arr.ctypes.data), HOST
+
+
 def _dp(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data)
 
@@ -204,6 +237,11 @@ class StreamingDMD:
         self.cfg = cfg
         self.n, self.m = int(n), int(m)
         self.np_dtype = np.float32 if cfg.dtype == F32 else np.float64
+        # inputs of recent pushes stay referenced until the library no longer reads them (pinned
+        # host buffers are copied asynchronously; the ring guard bounds how far the host runs
+        # ahead, so 64 pushes is ample); sync() drops them
+        import collections
+        self._pending = collections.deque(maxlen=64)
         h = ctypes.c_void_p()
         st = L.sdmd_create(ctypes.byref(cfg), ctypes.byref(h))
         if st:
@@ -238,31 +276,34 @@ class StreamingDMD:
     def init_window(self, Z, ldz: int | None = None):
         """Z: (m+1) columns of n values, column-major (a torch (m+1, n) row-major tensor or an
         (n, m+1) Fortran array both work; pass ldz for padded layouts)."""
-        p, where = _ptr(Z)
         if ldz is None:
             ldz = self.n
-        self._keep = Z
+        Z, p, where = _checked(Z, self.np_dtype, int(ldz) * self.m + self.n, "init_window", self.n)
+        self._pending.append(Z)
         return self._check(lib().sdmd_init_window(self.h, p, int(ldz), where), "init_window")
 
     def push_batch(self, X, dmd_every: bool = True, ldx: int | None = None):
         """k snapshots at once (K1b): a torch (k, n) row-major tensor / (n, k) Fortran array, oldest
         first.  dmd_every=False runs the DMD only for the newest window (catch-up mode)."""
-        p, where = _ptr(X)
         k = int(X.shape[0]) if hasattr(X, "data_ptr") else int(np.asarray(X).shape[1])
-        self._keep = X
-        return self._check(lib().sdmd_push_batch(self.h, k, p, int(ldx or self.n), where,
+        ld = int(ldx or self.n)
+        X, p, where = _checked(X, self.np_dtype, ld * (k - 1) + self.n, "push_batch", self.n)
+        self._pending.append(X)
+        return self._check(lib().sdmd_push_batch(self.h, k, p, ld, where,
                                                  1 if dmd_every else 0), "push_batch")
 
     def push(self, x):
-        p, where = _ptr(x)
-        self._keep = x
+        x, p, where = _checked(x, self.np_dtype, self.n, "push")
+        self._pending.append(x)
         return self._check(lib().sdmd_push_dense(self.h, p, where), "push_dense")
 
     def push_sparse(self, idx, val):
-        pi, wi = _ptr(idx)
-        pv, wv = _ptr(val)
-        self._keep = (idx, val)
         nnz = int(idx.shape[0]) if hasattr(idx, "shape") else len(idx)
+        idx, pi, wi = _checked(idx, np.int32, nnz, "push_sparse idx")
+        val, pv, wv = _checked(val, np.float64, nnz, "push_sparse val")
+        if wi != wv:
+            raise ValueError("push_sparse: idx and val must both be host or both be device buffers")
+        self._pending.append((idx, val))
         return self._check(lib().sdmd_push_sparse(self.h, nnz, pi, pv, wi), "push_sparse")
 
     def acquire_slot(self) -> int:
@@ -290,6 +331,7 @@ class StreamingDMD:
         """Wait for all work; returns -1, or raises SDMDError(E_NONFINITE) with .failed_frame."""
         f = ctypes.c_int64(-1)
         st = lib().sdmd_sync(self.h, ctypes.byref(f))
+        self._pending.clear()
         if st:
             e = SDMDError(st, lib().sdmd_last_error(self.h).decode())
             e.failed_frame = int(f.value)

@@ -6,6 +6,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -96,3 +97,43 @@ def test_row_partition_covers_rows():
                 assert b == c and a < b
             if P > 1 and n >= 32 * P:
                 assert all(a % 32 == 0 for a, _ in spans)
+
+
+def test_binding_input_checks():
+    """the binding checks dtype, length and contiguity of every input buffer
+    before passing a raw pointer, converts numpy inputs it can, and returns the converted object so
+    the caller keeps it alive."""
+    import torch
+    from paper_1612_07875_b200.sdmd import _checked
+    with pytest.raises(TypeError):
+        _checked(torch.zeros(10, dtype=torch.float64), np.float32, 10, "push")
+    with pytest.raises(ValueError):
+        _checked(torch.zeros(10, dtype=torch.float32), np.float32, 11, "push")
+    with pytest.raises(ValueError):
+        _checked(torch.zeros((10, 4), dtype=torch.float32)[:, 1], np.float32, 10, "push")
+    a, p, where = _checked([1.0, 2.0, 3.0], np.float32, 3, "push")
+    assert a.dtype == np.float32 and p.value == a.ctypes.data and where == 0
+    x64 = np.arange(6.0)
+    a, p, _ = _checked(x64, np.float32, 6, "push")
+    assert a.dtype == np.float32 and np.array_equal(a, x64.astype(np.float32))
+    # (n, k) C-ordered numpy -> Fortran copy (columns contiguous); (k, n) C-ordered kept as is
+    Z = np.arange(12.0).reshape(4, 3)
+    a, p, _ = _checked(Z, np.float64, 12, "init_window", n=4)
+    assert a.flags.f_contiguous and np.array_equal(a, Z)
+    Zt = np.ascontiguousarray(Z.T)
+    a, p, _ = _checked(Zt, np.float64, 12, "init_window", n=4)
+    assert a is Zt
+    with pytest.raises(ValueError):
+        _checked(np.zeros(5), np.float64, 6, "push")
+
+
+def test_import_does_not_change_environment(monkeypatch):
+    """importing the package leaves CUDA_DEVICE_MAX_CONNECTIONS alone."""
+    import importlib
+    import sys
+    monkeypatch.delenv("CUDA_DEVICE_MAX_CONNECTIONS", raising=False)
+    for k in [k for k in sys.modules if k.startswith("paper_1612_07875_b200")]:
+        monkeypatch.delitem(sys.modules, k)
+    importlib.import_module("paper_1612_07875_b200")
+    import os
+    assert "CUDA_DEVICE_MAX_CONNECTIONS" not in os.environ

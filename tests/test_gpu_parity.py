@@ -453,7 +453,7 @@ def test_nonfinite_frame_rejected_atomically():
     bad = Xd[15].clone()
     bad[123] = float("nan")
     eng.push(bad)
-    eng.push(Xd[16])                                 # discarded by the poison contract
+    _push_through_poison(eng, Xd, 16, 1)             # discarded by the poison contract (or refused)
     with pytest.raises(SDMDError) as e:
         eng.sync()
     assert e.value.status == 2 and e.value.failed_frame == 15
@@ -465,6 +465,133 @@ def test_nonfinite_frame_rejected_atomically():
     eng.sync()
     assert normwise(eng.gram(), ref.gram.G) < 1e-12
     assert match(eng.spectrum()["lam"], ref.last["lam"])[0] < 1e-9
+    eng.close()
+
+
+def _push_through_poison(eng, frames_dev, t0, count):
+    """Push frames t0 .. t0+count-1 after a rejected frame, before any sync: the first few are
+    accepted (their ring slots cannot hold anything the rolled-back state reads), then the ring
+    guard refuses further pushes with E_NONFINITE.  Returns how many were accepted."""
+    from paper_1612_07875_b200 import SDMDError
+    accepted = 0
+    for t in range(t0, t0 + count):
+        try:
+            eng.push(frames_dev[t])
+            accepted += 1
+        except SDMDError as e:
+            assert e.status == 2
+    return accepted
+
+
+def test_nonfinite_then_many_pushes_before_sync_leaves_state_intact():
+    """a rejected frame followed by many pushes before sync (more than the ring's
+    spare slots) must leave the rolled-back state bit-identical; the resumed stream matches the
+    oracle (Gram 1e-12, λ 1e-9)."""
+    from paper_1612_07875_b200 import SDMDError
+    rng = np.random.default_rng(12)
+    n, m = 3000, 8
+    X = rng.standard_normal((n, 80))
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(n, m, dtype="f64", workers=2)
+    ref = O.StreamingDMD(m, background=False)
+    for t in range(15):
+        eng.push(Xd[t])
+        ref.push(X[:, t])
+    eng.sync()
+    G0 = eng.gram()
+    bad = Xd[15].clone()
+    bad[123] = float("nan")
+    eng.push(bad)
+    acc = _push_through_poison(eng, Xd, 16, 2 * (m + eng.info()["ring_slots"]))
+    assert acc < eng.info()["ring_slots"] - m          # the guard stopped the writes
+    with pytest.raises(SDMDError) as e:
+        eng.sync()
+    assert e.value.status == 2 and e.value.failed_frame == 15
+    assert np.array_equal(eng.gram(), G0)
+    assert eng.info()["frames"] == 15
+    for t in range(16, 80):
+        eng.push(Xd[t])
+        ref.push(X[:, t])
+    eng.sync()
+    assert normwise(eng.gram(), ref.gram.G) < 1e-12
+    assert match(eng.spectrum()["lam"], ref.last["lam"])[0] < 1e-9
+    eng.close()
+
+
+def test_nonfinite_then_many_pushes_with_background():
+    """The same with the fused background (its lag keeps older ring slots live): after the
+    rollback and lag + 6 valid frames, the newest background column equals the oracle's."""
+    from paper_1612_07875_b200 import SDMDError
+    vs = synth.video_config("C3s")
+    m = 30
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+    lag = eng.info()["lag"]
+    T = m + 2 * lag + 40
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    ref = O.StreamingDMD(m, background=True)
+    p = m + lag + 3
+    for t in range(p):
+        eng.push(Xd[t])
+        ref.push(frames[:, t])
+    eng.sync()
+    bad = Xd[p].clone()
+    bad[7] = float("inf")
+    eng.push(bad)
+    _push_through_poison(eng, Xd, p + 1, T - p - 1)
+    with pytest.raises(SDMDError) as e:
+        eng.sync()
+    assert e.value.failed_frame == p and eng.info()["frames"] == p
+    outs = {}
+    for t in range(p + 1, T):                         # frame p's data is skipped: the valid
+        eng.push(Xd[t])                               # stream continues with frame p+1
+        o = ref.push(frames[:, t])
+        outs[ref.frames - 1] = o
+    eng.sync()
+    low, sp, mask, fb = eng.background()
+    o = outs[fb]
+    rel = np.max(np.abs(low - o["lowrank"])) / np.max(np.abs(o["lowrank"]))
+    assert rel < 1e-4, rel
+    assert normwise(eng.gram(), ref.gram.G) < 1e-12
+    eng.close()
+
+
+def test_push_batch_flow_control_many_batches_without_sync():
+    """hundreds of dmd_every batches with one slow eigen worker and no sync.  The
+    batched Gram pass may not run ahead of the eigen work it would overwrite: every K1b pass that
+    commits frames up to t_last starts after the eigen tasks of all frames <= t_last - lag - 2
+    have finished (device timeline), and the final Gram / spectrum match the closed form."""
+    pm = synth.planted_c1()
+    m, k, nb = 16, 8, 50                             # t <= 416: 0.99^t stays well resolved
+    T = m + 1 + k * nb
+    X = pm.frames(0, T)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=1, batch_max=k)
+    L = eng.info()["lag"]
+    for t in range(m + 1):
+        eng.push(Xd[t])
+    eng.sync()
+    eng.set_timing(True)
+    eng.stats(reset=True)
+    t = m + 1
+    for _ in range(nb):
+        eng.push_batch(Xd[t:t + k], dmd_every=True)
+        t += k
+    eng.sync()
+    tl = eng.timeline()
+    k4b_end = {int(f): e for f, kind, s, e in tl if kind == 2}
+    passes = [(int(f), s) for f, kind, s, e in tl if kind == 0]
+    assert len(passes) == nb and len(k4b_end) == nb * k
+    for f_last, start in passes:                      # eigen tasks enqueued before this batch
+        done_before = [e for f, e in k4b_end.items() if f <= min(f_last - L - 2, f_last - k)]
+        if done_before:
+            assert max(done_before) <= start + 1e-3, (f_last, max(done_before), start)
+    ref = O.StreamingGram(m)
+    for tt in range(T - m - 1, T):
+        ref.push(X[:, tt])
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    sp = eng.spectrum()
+    assert sp["frame"] == T - 1 and match(sp["lam"], pm.lambdas)[0] < 1e-9
     eng.close()
 
 
@@ -1290,7 +1417,10 @@ def test_sparse_device_indices_checked_on_device():
             G0 = eng.gram()
             idx, val = st.frame(t)
             eng.push_sparse(*_sparse_dev(bad[t](idx), val))
-            eng.push_sparse(*_sparse_dev(*st.frame(t + 1)))         # discarded by the poison contract
+            try:                                                   # discarded by the poison contract
+                eng.push_sparse(*_sparse_dev(*st.frame(t + 1)))    # (or refused if the host
+            except SDMDError as e:                                 #  already saw the rejection)
+                assert e.status == 2
             skip.add(t + 1)
             with pytest.raises(SDMDError) as e:
                 eng.sync()
@@ -1361,3 +1491,70 @@ def test_two_ranks_one_gpu_sparse_bad_indices_rejected_on_every_rank(monkeypatch
         ref.push(st.dense(t))
     assert np.array_equal(res[0], res[1])
     assert normwise(res[0], ref.G) < 1e-12
+
+
+# ------------------------------------------------ W_SINGULAR amplitudes (reading Q15) --------
+
+def _planted_zero_mode(n=300, m=6, orth=True, seed=60, T=None):
+    """Real modes, λ = {0, 0.9, -0.7, 0.5}: x_t = Σ b_j φ_j λ_j^t (φ_0 appears in x_0 only), so the
+    window that starts at t = 0 has an exact zero DMD eigenvalue (WΛ singular)."""
+    rng = np.random.default_rng(seed)
+    lam = np.array([0.0, 0.9, -0.7, 0.5])
+    b = np.array([1.3, 0.8, -0.6, 1.1])
+    Phi = rng.standard_normal((n, 4))
+    if orth:
+        Phi, _ = np.linalg.qr(Phi)
+    T = m + 1 if T is None else T
+    X = np.stack([Phi @ (b * lam ** t) for t in range(T)], axis=1)
+    return X, lam, b, Phi
+
+
+@pytest.mark.parametrize("orth", [True, False])
+def test_singular_amplitudes_least_squares_on_kept_modes(orth):
+    """GPU W_SINGULAR semantics = the oracle's (O9): status W_SINGULAR, b = 0 for the zero mode,
+    least squares of WΛ's kept columns for the others (compared as b_j φ_j, 1e-9 relative)."""
+    m = 6
+    X, lam_p, _, _ = _planted_zero_mode(m=m, orth=orth, seed=70 + int(orth))
+    ref = O.dmd_window(X)
+    assert ref["amp_status"] == O.W_SINGULAR
+    eng = Eng(X.shape[0], m, dtype="f64", workers=1)
+    eng.init_window(dev_cols(X, np.float64))
+    sp = eng.spectrum(with_b=True)
+    assert sp["status"] == 6 and sp["r"] == ref["r"] == 4
+    err, perm = match(sp["lam"], ref["lam"])
+    assert err < 1e-9
+    Phi = eng.modes(list(range(4))).cpu().numpy()
+    Phi_ref = O.modes(X[:, 1:], ref)
+    for j in range(4):
+        k = perm[j]
+        got, want = sp["b"][j] * Phi[:, j], ref["b"][k] * Phi_ref[:, k]
+        scale = max(np.linalg.norm(want), 1e-300)
+        if np.all(want == 0):
+            assert np.linalg.norm(got) == 0
+        else:
+            assert np.linalg.norm(got - want) < 1e-9 * scale, (j, np.linalg.norm(got - want) / scale)
+    eng.close()
+
+
+def test_singular_frame_background_uses_least_squares():
+    """The per-frame path: the streamed background column of a W_SINGULAR window (built from the
+    kept-mode least-squares b_idx on the device) equals the oracle's, 1e-9 relative (fp64)."""
+    m = 6
+    eng = Eng(300, m, dtype="f64", background=True, workers=1)
+    L = eng.info()["lag"]
+    X, _, _, _ = _planted_zero_mode(m=m, orth=False, seed=72, T=m + 1 + L)
+    X = X + 0.5                                        # an exact constant mode: λ = 1 is idx
+    ref = O.StreamingDMD(m, background=True)
+    out_m = ref.init_window(X[:, :m + 1])
+    assert out_m["amp_status"] == O.W_SINGULAR
+    eng.init_window(dev_cols(X[:, :m + 1], np.float64))
+    assert eng.spectrum()["status"] == 6
+    Xd = dev_cols(X, np.float64)
+    for t in range(m + 1, m + 1 + L):
+        eng.push(Xd[t])
+    eng.sync()
+    low, sp_, mask, fb = eng.background()
+    assert fb == m
+    rel = np.max(np.abs(low - out_m["lowrank"])) / np.max(np.abs(out_m["lowrank"]))
+    assert rel < 1e-9, rel
+    eng.close()
