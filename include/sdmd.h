@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define SDMD_ABI_VERSION 2
+#define SDMD_ABI_VERSION 3
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
 #define SDMD_MAX_LAG 64  /* largest background lag (frames)                                     */
 #define SDMD_MAX_BATCH 8 /* largest k of sdmd_push_batch                                          */
@@ -162,6 +162,9 @@ typedef struct sdmd_stats {
   int64_t gpu_launches; /* all kernels this ctx launched since the last reset                   */
   double k1_gap_ms;     /* summed ctx-stream time between consecutive Gram passes (ingest, waits) */
   double k1_wait_ms;    /* part of k1_gap_ms spent waiting for background coefficients (K4)     */
+  int64_t collectives;  /* collectives (allreduce/broadcast) issued since the last reset: one per
+                         * push at nranks > 1 (the Gram column and, under eigen sharding, the
+                         * background coefficients of a later frame share it)                  */
 } sdmd_stats;
 
 /* Fill *cfg with defaults (rank_tol 1e-7, threshold 0.2, dmd 1, background 0, workers 4, …).

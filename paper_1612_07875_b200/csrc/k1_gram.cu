@@ -691,6 +691,7 @@ __global__ void __launch_bounds__(K1_THREADS, 1) k1v2_kernel(const K1Params p) {
 
 __global__ void commit_kernel(const K1Params p) {
   if (*(volatile int*)&p.st->status != 0) return;
+  for (int i = threadIdx.x; i < p.cfold_n; i += blockDim.x) p.cfold_dst[i] = p.cfold_src[i];
   commit_block(p.gout, p.nd, p.m, p.f_new, p.ghist, p.NH, p.st);
 }
 

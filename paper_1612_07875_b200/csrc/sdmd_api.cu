@@ -10,10 +10,11 @@
 // work is hidden behind the bandwidth-bound Gram pass when lag·t_K1 ≥ t_K4.
 // Eigen sharding (nranks = P > 1, cfg.eigen_shard): the small eigenproblems of frame t run only on
 // rank t mod P (every rank holds the same allreduced Gram history, so any rank can solve any
-// frame), and before K1(t+lag) consumes them the m background coefficients c_t are broadcast from
-// that rank (ncclBroadcast, 2m fp64) — the eigen work per rank drops by P, so the pipeline keeps
-// up with P times the frame rate of one GPU.  Local frame index q = t div P selects the worker
-// streams, the workspace and the K4 events.
+// frame).  The m background coefficients c_t that K1(t+lag) consumes ride in the allreduce of the
+// Gram column of frame t+lag-1 (2m fp64 appended: the owner's values, zeros on every other rank,
+// so the sum is the owner's value exactly) — ONE collective per frame, as SURVEY §8(e) states.
+// The eigen work per rank drops by P, so the pipeline keeps up with P times the frame rate of one
+// GPU.  Local frame index q = t div P selects the worker streams, the workspace and the K4 events.
 #include <dlfcn.h>
 #include <condition_variable>
 #include <cstdio>
@@ -41,8 +42,6 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
-  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
-                            cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
@@ -55,10 +54,9 @@ NcclApi* nccl_api() {
   api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
   api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
-  api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.Broadcast || !api.CommDestroy)
+  if (!api.GetUniqueId || !api.CommInitRank || !api.AllReduce || !api.CommDestroy)
     return nullptr;
   api.loaded = true;
   return &api;
@@ -195,6 +193,10 @@ struct sdmd_ctx {
   long long last_dmd = -1;              // newest frame whose eigenproblems ran on THIS rank
   long long last_dmd_all = -1;          // newest frame whose eigenproblems ran on any rank
   int P = 1, prank = 0;                 // eigen shards (P = nranks with eigen_shard, else 1)
+  bool coll = false;                    // collectives on: nranks > 1, or SDMD_FORCE_NCCL=1 (test knob:
+                                        // a 1-rank NCCL communicator runs the multi-rank code path)
+  long long c_folded = -1;              // newest frame whose background coefficients rode an allreduce
+  long long collectives = 0;
   // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev, wait_ev;
@@ -272,9 +274,9 @@ __global__ void lg_sum_kernel(double* const* stage, int n, size_t count, double*
   }
 }
 
-// Collectives of the path (all on the ctx stream, in the same order on every rank): the sum of a
-// fp64 vector (partial Gram column / init Gram) and the broadcast of a fp64 vector (background
-// coefficients of an eigen-sharded frame).
+// The one collective of the path (on the ctx stream, in the same order on every rank): the sum of
+// a fp64 vector — the partial Gram column of a frame (with, under eigen sharding, the background
+// coefficients of a later frame appended), or the partial init Gram.
 static int lg_begin(sdmd_ctx* c, const double* src, size_t count) {
   LocalGroup* g = c->lgroup;
   const int r = c->cfg.rank;
@@ -294,6 +296,7 @@ static int lg_end(sdmd_ctx* c) {
   return SDMD_OK;
 }
 static int coll_allreduce(sdmd_ctx* c, double* buf, size_t count) {
+  c->collectives += 1;
   if (c->lgroup) {
     LocalGroup* g = c->lgroup;
     int st = lg_begin(c, buf, count);
@@ -307,24 +310,6 @@ static int coll_allreduce(sdmd_ctx* c, double* buf, size_t count) {
   NcclApi* api = nccl_api();
   if (!api || api->AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream) != ncclSuccess) {
     c->err = "ncclAllReduce failed";
-    return SDMD_E_NCCL;
-  }
-  return SDMD_OK;
-}
-static int coll_broadcast(sdmd_ctx* c, double* buf, size_t count, int root) {
-  if (c->lgroup) {
-    LocalGroup* g = c->lgroup;
-    int st = lg_begin(c, c->cfg.rank == root ? buf : nullptr, count);
-    if (st) return st;
-    if (c->cfg.rank != root) {
-      CK(cudaStreamWaitEvent(c->stream, g->ev_in[root], 0));
-      CK(cudaMemcpyAsync(buf, g->stage[root], count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    }
-    return lg_end(c);
-  }
-  NcclApi* api = nccl_api();
-  if (!api || api->Broadcast(buf, buf, count, ncclFloat64, root, c->comm, c->stream) != ncclSuccess) {
-    c->err = "ncclBroadcast failed";
     return SDMD_E_NCCL;
   }
   return SDMD_OK;
@@ -593,7 +578,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   c->k1b_grid = k1b_grid(c->nsm, c->cfg.n_local, c->cfg.dtype);
   const size_t npb = c->cfg.batch_max > 0 ? k1b_partials_elems(c->k1b_grid) : 0;
   AL(c->partials, np > np3 ? (np > npb ? np : npb) : (np3 > npb ? np3 : npb));
-  AL(c->gout, (size_t)(m + 1) * (c->cfg.batch_max > 1 ? c->cfg.batch_max : 1));
+  AL(c->gout, (size_t)(m + 1) * (c->cfg.batch_max > 1 ? c->cfg.batch_max : 1) + 2 * (size_t)m);
   AL(c->gpart, (size_t)(m + 1));
   AL(c->Gtmp, (size_t)(m + 1) * (m + 1));
   if (c->cfg.background) {
@@ -684,14 +669,24 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     }
     ++g->refs;
     c->lgroup = g;
-  } else if (c->cfg.nranks > 1) {
-    NcclApi* api = nccl_api();
-    if (!api) { c->err = "libnccl.so.2 not loadable"; return bail(SDMD_E_NCCL); }
-    ncclUniqueId id;
-    std::memcpy(id.internal, c->cfg.nccl_uid, 128);
-    if (api->CommInitRank(&c->comm, c->cfg.nranks, id, c->cfg.rank) != ncclSuccess) {
-      c->err = "ncclCommInitRank failed";
-      return bail(SDMD_E_NCCL);
+    c->coll = true;
+  } else {
+    const char* ef = std::getenv("SDMD_FORCE_NCCL");
+    const bool force = c->cfg.nranks == 1 && ef && ef[0] == '1';
+    if (c->cfg.nranks > 1 || force) {
+      NcclApi* api = nccl_api();
+      if (!api) { c->err = "libnccl.so.2 not loadable"; return bail(SDMD_E_NCCL); }
+      ncclUniqueId id;
+      if (force) {
+        if (api->GetUniqueId(&id) != ncclSuccess) { c->err = "ncclGetUniqueId failed"; return bail(SDMD_E_NCCL); }
+      } else {
+        std::memcpy(id.internal, c->cfg.nccl_uid, 128);
+      }
+      if (api->CommInitRank(&c->comm, c->cfg.nranks, id, c->cfg.rank) != ncclSuccess) {
+        c->err = "ncclCommInitRank failed";
+        return bail(SDMD_E_NCCL);
+      }
+      c->coll = true;
     }
   }
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return bail(SDMD_E_CUDA);
@@ -845,6 +840,41 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   return cudaSuccess;
 }
 
+// Under eigen sharding (or the forced 1-rank NCCL test path) the background coefficients of frame
+// fb come from the rank that solved fb; they travel inside the per-frame allreduce of g.
+static inline bool fold_c(const sdmd_ctx* c) {
+  return c->coll && c->cfg.background && c->cfg.dmd && c->cfg.storage == SDMD_DENSE &&
+         (c->P > 1 || c->cfg.nranks == 1);
+}
+
+// Stage c_fb at gout + off for the allreduce: the owner copies its coefficients (after its eigen
+// worker finished fb), every other rank contributes zeros.
+static int stage_c(sdmd_ctx* c, long long fb, int off) {
+  const int m = c->cfg.m;
+  double* dst = c->gout + off;
+  if (owns(c, fb)) {
+    CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fb) % kEvents], 0));
+    CK(cudaMemcpyAsync(dst, c->cbuf + (fb % c->NC) * m, 2 * (size_t)m * sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(cudaMemsetAsync(dst, 0, 2 * (size_t)m * sizeof(double), c->stream));
+  }
+  return SDMD_OK;
+}
+
+// Fallback: an allreduce of c_fb alone, then copied into its cbuf slot.
+static int allreduce_c(sdmd_ctx* c, long long fb, int off) {
+  const int m = c->cfg.m;
+  int st = stage_c(c, fb, off);
+  if (st) return st;
+  st = coll_allreduce(c, c->gout + off, 2 * (size_t)m);
+  if (st) return st;
+  CK(cudaMemcpyAsync(c->cbuf + (fb % c->NC) * m, c->gout + off, 2 * (size_t)m * sizeof(double),
+                     cudaMemcpyDeviceToDevice, c->stream));
+  c->c_folded = fb;
+  return SDMD_OK;
+}
+
 // Everything after the frame data sits in its slot: Gram column, reduction, DMD, events.
 static int enqueue_frame(sdmd_ctx* c, long long t) {
   const int m = c->cfg.m;
@@ -878,9 +908,10 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   if (bg && c->cfg.dmd) {
     const long long fb = t - c->L;
     if (owns(c, fb)) CK(cudaStreamWaitEvent(c->stream, c->ev_done[lidx(c, fb) % kEvents], 0));
-    if (c->P > 1) {                               // c_fb from the rank that solved frame fb
-      double2* cb = c->cbuf + (fb % c->NC) * m;
-      const int st_ = coll_broadcast(c, (double*)cb, (size_t)2 * m, (int)(fb % c->P));
+    if (fold_c(c) && c->c_folded != fb) {
+      // c_fb did not ride the allreduce of frame t-1 (lag 1, or the first frame after an
+      // init_window / a rollback): an allreduce of c alone (owner's values, zeros elsewhere)
+      const int st_ = allreduce_c(c, fb, 0);
       if (st_) return st_;
     }
   }
@@ -891,7 +922,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     tp = new_pair();
     CK(cudaEventRecord(tp.first, c->stream));
   }
-  const int do_commit = c->cfg.nranks == 1 ? 1 : 0;
+  const int do_commit = c->coll ? 0 : 1;
   if (!sparse) {
     K1Params p{};
     p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f_new = t;
@@ -919,12 +950,27 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
       c->k1_ev.push_back(tp);
       c->tl.push_back({t, 0, tp.first, tp.second});
     }
-    if (c->cfg.nranks > 1) {
+    if (c->coll) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      const int st_ = coll_allreduce(c, c->gout, nd);
+      // the next push's background coefficients c_{t+1-L} ride this allreduce (computed by frame
+      // t+1-L's owner; L >= 2 so that its eigen task was enqueued before this commit)
+      const long long fb1 = t + 1 - c->L;
+      const long long newest = do_dmd ? t : c->last_dmd_all;
+      const bool fold = fold_c(c) && c->L >= 2 && fb1 >= m && fb1 <= newest && fb1 <= t - 1;
+      size_t cnt = nd;
+      if (fold) {
+        const int st_ = stage_c(c, fb1, nd);
+        if (st_) return st_;
+        cnt += 2 * (size_t)m;
+        p.cfold_src = c->gout + nd;
+        p.cfold_dst = (double*)(c->cbuf + (fb1 % c->NC) * m);
+        p.cfold_n = 2 * m;
+      }
+      const int st_ = coll_allreduce(c, c->gout, cnt);
       if (st_) return st_;
       CK(launch_commit(p, c->stream));
       c->launches += 1;
+      if (fold) c->c_folded = fb1;
     }
   } else {
     K3Params p{};
@@ -939,7 +985,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
       c->k1_ev.push_back(tp);
       c->tl.push_back({t, 0, tp.first, tp.second});
     }
-    if (c->cfg.nranks > 1) {
+    if (c->coll) {
       CK(cudaMemcpyAsync(c->gpart, c->gout, nd * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
       const int st_ = coll_allreduce(c, c->gout, nd);
       if (st_) return st_;
@@ -1028,7 +1074,7 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
   if (c->timing) { tp = new_pair(); CK(cudaEventRecord(tp.first, c->stream)); }
   K1bParams p{};
   p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f0 = t; p.k = k;
-  p.partials = c->partials; p.gout = c->gout; p.do_commit = c->cfg.nranks == 1 ? 1 : 0;
+  p.partials = c->partials; p.gout = c->gout; p.do_commit = c->coll ? 0 : 1;
   p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
   CK(launch_k1b(p, c->cfg.dtype, c->k1b_grid, c->stream));
   c->launches += 1;
@@ -1037,7 +1083,7 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
     c->k1_ev.push_back(tp);
     c->tl.push_back({t + k - 1, 0, tp.first, tp.second});
   }
-  if (c->cfg.nranks > 1) {
+  if (c->coll) {
     const size_t cnt = (size_t)k * (m + 1);
     CK(cudaMemcpyAsync(c->gpart, c->gout, (m + 1) * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     const int st_ = coll_allreduce(c, c->gout, cnt);
@@ -1130,7 +1176,7 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   }
   CK(launch_init_gram(c->ring, c->ld, c->cfg.dtype, c->cfg.n_local, k, c->Gtmp, c->init_work, c->stream));
   c->launches += 2;
-  if (c->cfg.nranks > 1) {
+  if (c->coll) {
     const int st_ = coll_allreduce(c, c->Gtmp, (size_t)k * k);
     if (st_) return st_;
   }
@@ -1159,6 +1205,7 @@ int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
   c->known_clean = k;
   c->fenced = -1;
   c->solved.clear();
+  c->c_folded = -1;
   CK(cudaMemcpyAsync(c->dst, &hs, sizeof(hs), cudaMemcpyHostToDevice, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   for (int f = 0; f < k; ++f) CK(cudaEventRecord(c->ev_k1[f % kEvents], c->stream));
@@ -1210,6 +1257,7 @@ int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
     if (c->known_clean > hs.committed) c->known_clean = hs.committed;
     if (c->fenced > hs.committed - 1) c->fenced = hs.committed - 1;
     while (!c->solved.empty() && c->solved.back().first >= hs.committed) c->solved.pop_back();
+    c->c_folded = -1;
     c->err = "frame " + std::to_string(hs.failed_frame) +
              " rejected (non-finite Gram column, or invalid device-side sparse indices)";
     return SDMD_E_NONFINITE;
@@ -1254,7 +1302,7 @@ int sdmd_get_partial_gram_column(sdmd_ctx* c, double* g, int32_t* k_out) {
   if (st) return st;
   if (k_out) *k_out = c->last_nd;
   if (c->last_nd == 0) return SDMD_E_STATE;
-  CK(cudaMemcpy(g, c->cfg.nranks > 1 ? c->gpart : c->gout, c->last_nd * sizeof(double),
+  CK(cudaMemcpy(g, c->coll ? c->gpart : c->gout, c->last_nd * sizeof(double),
                 cudaMemcpyDeviceToHost));
   return SDMD_OK;
 }
@@ -1482,7 +1530,8 @@ int sdmd_get_stats(sdmd_ctx* c, sdmd_stats* s, int reset) {
   s->k1_wait_ms = 0.0;
   for (auto& pr : c->wait_ev) { float ms = 0; cudaEventElapsedTime(&ms, pr.first, pr.second); s->k1_wait_ms += ms; }
   s->gpu_launches = c->launches;
-  if (reset) { destroy_timing(c); c->launches = 0; }
+  s->collectives = c->collectives;
+  if (reset) { destroy_timing(c); c->launches = 0; c->collectives = 0; }
   return SDMD_OK;
 }
 

@@ -67,6 +67,11 @@ struct K1Params {
   double* ghist;
   int NH;
   DevState* st;
+  // commit kernel (multi-rank): background coefficients carried by the same allreduce (one
+  // collective per frame): copy cfold_n doubles from cfold_src (after the g part) to cfold_dst
+  const double* cfold_src;
+  double* cfold_dst;
+  int cfold_n;
 };
 
 struct K1bParams {             // K1b: Gram columns of k frames f0..f0+k-1 in one pass

@@ -62,7 +62,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("k1_launches", ctypes.c_int64), ("k1_ms", ctypes.c_double),
                 ("k4_launches", ctypes.c_int64), ("k4_ms", ctypes.c_double),
                 ("gpu_launches", ctypes.c_int64), ("k1_gap_ms", ctypes.c_double),
-                ("k1_wait_ms", ctypes.c_double)]
+                ("k1_wait_ms", ctypes.c_double), ("collectives", ctypes.c_int64)]
 
 
 class SDMDError(RuntimeError):

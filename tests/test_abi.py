@@ -48,7 +48,7 @@ def test_sm100a_code_present(libpath):
 def test_status_strings_and_version(libpath):
     from paper_1612_07875_b200 import sdmd
     L = sdmd.lib()
-    assert L.sdmd_abi_version() == 2
+    assert L.sdmd_abi_version() == 3
     assert L.sdmd_status_string(2).decode() == "non-finite frame rejected"
     assert L.sdmd_status_string(999).decode() == "unknown status"
 

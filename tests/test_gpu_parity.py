@@ -1253,9 +1253,10 @@ def test_two_ranks_one_gpu_local_group(monkeypatch, eigen_shard):
     """The multi-rank data path on one GPU: two contexts (ranks 0 and 1, half of the rows each)
     driven by two host threads, collectives through the in-process test group (NCCL refuses two
     ranks on one device).  Row sharding + allreduce of g: both ranks hold the same Gram, bitwise,
-    equal to one rank's within 1e-12 (summation split only).  Eigen sharding + broadcast of c_t:
-    the background rows of the two ranks form the one-rank background; each rank's spectrum is
-    the newest frame it solved."""
+    equal to one rank's within 1e-12 (summation split only).  Eigen sharding, c_t carried by the
+    allreduce of a later frame's Gram column: the background rows of the two ranks form the
+    one-rank background; each rank's spectrum is the newest frame it solved.  Exactly ONE
+    collective per push (the allreduce of the (m+1)-vector is the only one)."""
     import threading
     from paper_1612_07875_b200 import row_partition
     monkeypatch.setenv("SDMD_LOCAL_GROUP", "1")
@@ -1274,7 +1275,7 @@ def test_two_ranks_one_gpu_local_group(monkeypatch, eigen_shard):
                 for t in range(T):
                     eng.push(vs.frame(t, "cuda:0", (b, e)))
                 eng.sync()
-                res[rank] = (eng.gram(), eng.background(), eng.spectrum(), eng.info())
+                res[rank] = (eng.gram(), eng.background(), eng.spectrum(), eng.info(), eng.stats())
                 eng.close()
         except Exception as ex:                        # surfaced below
             errs.append(repr(ex))
@@ -1293,6 +1294,7 @@ def test_two_ranks_one_gpu_local_group(monkeypatch, eigen_shard):
     spec1 = one.spectrum()
     assert np.array_equal(res[0][0], res[1][0])
     assert normwise(res[0][0], G1) < 1e-12
+    assert res[0][4]["collectives"] == res[1][4]["collectives"] == T
     low = np.concatenate([res[0][1][0], res[1][1][0]])
     assert res[0][1][3] == res[1][1][3] == fb1
     assert np.max(np.abs(low - low1)) < 1e-4 * np.max(np.abs(low1))
@@ -1557,4 +1559,134 @@ def test_singular_frame_background_uses_least_squares():
     assert fb == m
     rel = np.max(np.abs(low - out_m["lowrank"])) / np.max(np.abs(out_m["lowrank"]))
     assert rel < 1e-9, rel
+    eng.close()
+
+
+# ------------------------------------------- the real NCCL data plane on a 1-rank communicator --
+
+def test_nccl_one_rank_communicator_matches_single_rank(monkeypatch):
+    """SDMD_FORCE_NCCL=1 runs the multi-rank code path of a 1-rank context through a real NCCL
+    communicator (ncclCommInitRank with nranks = 1): the init-Gram allreduce, the per-frame
+    allreduce of g with the background coefficients folded in, and the separate commit kernel.
+    A 1-rank sum is the identity, so Gram, spectrum and background equal the plain single-rank
+    run bitwise, with exactly one NCCL call per push."""
+    vs = synth.VideoStream(108, 192, 1, seed=33, side=24)
+    m, T = 24, 70
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+
+    def run(force):
+        if force:
+            monkeypatch.setenv("SDMD_FORCE_NCCL", "1")
+        else:
+            monkeypatch.delenv("SDMD_FORCE_NCCL", raising=False)
+        eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+        eng.init_window(Xd[:m + 1])
+        eng.sync()
+        eng.stats(reset=True)
+        for t in range(m + 1, T):
+            eng.push(Xd[t])
+        eng.sync()
+        out = (eng.gram(), eng.background(), eng.spectrum(), eng.stats(), eng.partial_gram_column())
+        eng.close()
+        return out
+    plain, nccl = run(False), run(True)
+    assert plain[3]["collectives"] == 0
+    assert nccl[3]["collectives"] == T - m - 1
+    assert np.array_equal(plain[0], nccl[0])
+    for a, b in zip(plain[1][:3], nccl[1][:3]):
+        assert np.array_equal(a, b)
+    assert plain[1][3] == nccl[1][3]
+    assert np.array_equal(plain[2]["lam"], nccl[2]["lam"]) and plain[2]["idx"] == nccl[2]["idx"]
+    assert np.array_equal(plain[4], nccl[4])
+
+
+def test_nccl_one_rank_batches_and_sparse(monkeypatch):
+    """The batched (k-frame allreduce) and sparse (K3 + allreduce + commit kernel) multi-rank paths
+    through a real 1-rank NCCL communicator equal the oracle's streamed Gram (1e-12)."""
+    monkeypatch.setenv("SDMD_FORCE_NCCL", "1")
+    pm = synth.planted_c1()
+    m = 16
+    X = pm.frames(0, m + 1 + 24)
+    Xd = dev_cols(X, np.float64)
+    eng = Eng(pm.n, m, dtype="f64", workers=2, batch_max=8)
+    ref = O.StreamingGram(m)
+    for t in range(m + 1):
+        eng.push(Xd[t])
+        ref.push(X[:, t])
+    for t0 in (m + 1, m + 9, m + 17):
+        eng.push_batch(Xd[t0:t0 + 8])
+        for j in range(8):
+            ref.push(X[:, t0 + j])
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    assert match(eng.spectrum()["lam"], pm.lambdas)[0] < 1e-9
+    eng.close()
+    st = synth.SparseDCTStream(N=128, k_low=14.0, n_shell=60, seed=5)
+    m, T = 12, 30
+    eng = Eng(st.n, m, storage="sparse", nnz_cap=st.nnz_cap, workers=1)
+    ref = O.StreamingGram(m)
+    for t in range(T):
+        eng.push_sparse(*st.frame(t))
+        ref.push(st.dense(t))
+    eng.sync()
+    assert normwise(eng.gram(), ref.G) < 1e-12
+    assert eng.stats()["collectives"] == T
+    eng.close()
+
+
+# ------------------------------------------------ parity at the benchmarked instances --------
+
+def test_c5_scale_sparse_multi_chunk_gram_and_lambda_idx():
+    """BASELINE config 5 at full size (1024² DCT coefficients, ~1% nonzeros, m = 128): nnz_cap
+    ≈ 10.6k takes K3's 6-chunk reduction.  Gram vs the oracle's compensated definition (on the
+    window's union support, bitwise equal to the dense definition) normwise 1e-12; r equal; λ_idx
+    within 1e-9 (§3.5)."""
+    st = synth.SparseDCTStream()                      # C5: N=1024, k_low=110, n_shell=1000
+    m, T = 128, 128 + 1 + 12
+    assert (st.nnz_cap + 2047) // 2048 >= 5
+    eng = Eng(st.n, m, storage="sparse", nnz_cap=st.nnz_cap, workers=4)
+    slots = []
+    for t in range(T):
+        fr = st.frame(t)
+        eng.push_sparse(*fr)
+        slots = (slots + [fr])[-(m + 1):]
+    eng.sync()
+    G = eng.gram()
+    Gr = O.gram(O.sparse_window_on_support(slots))
+    assert normwise(G, Gr) < 1e-12
+    d = O.dmd_from_gram(Gr)
+    idx_ref = O.background_index(d["lam"])
+    sp = eng.spectrum()
+    assert sp["r"] == d["r"] and sp["frame"] == T - 1
+    assert abs(sp["lam"][sp["idx"]] - d["lam"][idx_ref]) < 1e-9
+    eng.close()
+
+
+def test_c4s_bench_kernel_instance_background_elementwise():
+    """The bench's background instance (k1v2_kernel<float, bg, 13>: m = 200, 6 workers, lag 8 →
+    208 union columns) on a reduced-n C4-shaped video (384x216x3): low-rank, sparse and mask of the
+    streamed background column vs the oracle element by element (fp32 path: 1e-4 relative;
+    mask equal away from |s − 0.2| < 1e-4)."""
+    vs = synth.video_config("C4s")
+    m = 200
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=6)
+    info = eng.info()
+    assert info["lag"] == 8 and (m + info["lag"]) == 16 * 13
+    T = m + info["lag"] + 6
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    for t in range(T):
+        eng.push(Xd[t])
+    eng.sync()
+    low, sp, mask, fb = eng.background()
+    assert fb == T - 1 - info["lag"]
+    ref = O.StreamingDMD(m, background=True)
+    o = ref.init_window([frames[:, k] for k in range(fb - m, fb + 1)])
+    x = frames[:, fb].astype(np.float64)
+    rel = np.max(np.abs(low - o["lowrank"])) / np.max(np.abs(o["lowrank"]))
+    assert rel < 1e-4, rel
+    assert np.max(np.abs(sp - o["sparse"])) < 1e-4 * np.max(np.abs(x))
+    near = np.abs(o["sparse"] - 0.2) < 1e-4
+    assert np.all(mask[~near] == o["mask"][~near])
     eng.close()

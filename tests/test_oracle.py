@@ -731,3 +731,11 @@ def test_background_first_window_planted_exponents():
     assert abs(d["lam"][d["idx"]] - 1) < 1e-10
     assert np.max(np.abs(L - bg[:, None])) < 1e-9
     assert np.max(np.abs(S - np.stack([dec * 0.6 ** t for t in range(m + 1)], axis=1))) < 1e-9
+
+
+def test_sparse_window_on_support_equals_dense_definition_bitwise():
+    """The support-compressed sparse window has exactly the Gram of the scattered dense vectors."""
+    st = synth.SparseDCTStream(N=64, k_low=8.0, n_shell=30, seed=12)
+    slots = [st.frame(t) for t in range(6)]
+    D = np.stack([st.dense(t) for t in range(6)], axis=1)
+    assert np.array_equal(O.gram(O.sparse_window_on_support(slots)), O.gram(D))
