@@ -274,8 +274,10 @@ int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mas
  * sweeps, [5]=QR iterations, [6..12]=SM cycles spent in the K4 phases (build S, Jacobi, sort/V,
  * Ã, Hessenberg, QR, eigenvectors+c), [13]=single-bulge chase steps, [14]=multishift global
  * steps, [15]=multishift sweeps, [16]=SM cycles spent computing multishift shifts, [17]=single-
- * bulge iterations, [18..19]=SM cycles of the multishift chase phases.  Synchronises. */
-int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[20]);
+ * bulge iterations, [18..19]=SM cycles of the multishift chase phases, [20]=Ehrlich–Aberth
+ * iterations of eig(Ã) (0: QR used, −1: Aberth did not certify → QR), [21]=Hyman evaluations.
+ * Synchronises. */
+int sdmd_get_frame_diag(sdmd_ctx* ctx, int64_t out[24]);
 
 /* Kernel timing (CUDA events around every K1/K3 and K4 launch) and launch counts. */
 int sdmd_set_timing(sdmd_ctx* ctx, int enable);

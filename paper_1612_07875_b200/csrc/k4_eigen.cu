@@ -597,6 +597,219 @@ static __device__ int multishift_qr(RowAcc a, int n, double2* wv, MsShared* sh, 
   return status;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Eigenvalues of the unreduced upper Hessenberg H (r x r) by the Ehrlich–Aberth simultaneous
+// iteration (Aberth 1973; Bini–Gemignani–Tisseur's Hessenberg variant), warm-started from an
+// earlier frame's spectrum.  For each root z_k the Newton ratio N = p(z)/p'(z), p = det(H − zI),
+// comes from Hyman's method: the back-recurrence of (H − zI) x = α e₁ with x_{r-1} = 1,
+//     x_{j-1} = −[(h_jj − z) x_j + Σ_{i>j} h_ji x_i] / h_{j,j-1},   α = (h_00 − z) x_0 + Σ h_0i x_i,
+// so p(z) ∝ α(z) and p'/p = α'/α (the constant Π h_{j,j-1} cancels; x and its z-derivative x' are
+// rescaled together whenever they leave [1e-100, 1e100]).  One warp per root: lanes own rows,
+// accumulate the partial sums Σ_{i>j} h_ji x_i column by column (column-packed H in shared memory,
+// 1/h_{j,j-1} stored in place of h_{j,j-1}), and the owner lane of row j forms x_{j-1}.  The update
+// z_k ← z_k − N_k / (1 − N_k Σ_{j≠k} 1/(z_k − z_j)) is Jacobi-style (every root from the previous
+// iterate), so the result is deterministic.  A root is frozen once its correction is below
+// 4u|z_k|.  Returns 0 with the spectrum (conjugate pairs made exact, near-real roots snapped to
+// the real axis) in lam_out, or −1 (not converged in the budget, a non-finite step, a trace
+// mismatch, a reducible H) — the caller then runs the Francis QR.
+constexpr int AB_MAXIT = 40;
+constexpr int AB_RQ = (kMaxR + 31) / 32;
+__host__ __device__ __forceinline__ int ab_cofs(int j) { return j * (j + 5) / 2; }  // column j start
+
+static __device__ double2 hyman_ratio(const double* hc, int r, double2 z, int lane) {
+  double2 s[AB_RQ], sd[AB_RQ];
+#pragma unroll
+  for (int q = 0; q < AB_RQ; ++q) { s[q] = make_double2(0.0, 0.0); sd[q] = make_double2(0.0, 0.0); }
+  double2 x = make_double2(1.0, 0.0), xd = make_double2(0.0, 0.0);
+  // rows in blocks of 32 (block qb: rows 32qb .. 32qb+31, lane = row mod 32), unrolled over qb so
+  // that the owner's partial sums s[qb] and the axpy extents are static: at step j (block qb,
+  // jj = j - 32qb) the owner is lane jj; column j updates the full blocks q < qb and lanes < jj
+  // of block qb (rows i < j)
+#pragma unroll
+  for (int qb = AB_RQ - 1; qb >= 0; --qb) {
+    if (32 * qb >= r) continue;
+    const int jhi = (r - 1 - 32 * qb) < 31 ? (r - 1 - 32 * qb) : 31;
+    const int jlo = qb == 0 ? 1 : 0;
+    for (int jj = jhi; jj >= jlo; --jj) {
+      const int j = 32 * qb + jj;
+      const double* cj = hc + ab_cofs(j);
+      const double2 dz = make_double2(cj[j] - z.x, -z.y);             // h_jj − z
+      const double inv = hc[ab_cofs(j - 1) + j];                        // 1/h_{j,j-1} (in place)
+      // owner (lane jj): x_{j-1} = −[(h_jj − z) x_j + s_j] / h_{j,j-1}, and its z-derivative
+      const double2 rr = cadd(cmul(dz, x), s[qb]);
+      const double2 rd = csub(cadd(cmul(dz, xd), sd[qb]), x);
+      const double2 xn = make_double2(-rr.x * inv, -rr.y * inv);
+      const double2 xdn = make_double2(-rd.x * inv, -rd.y * inv);
+      // column j into the rows above it
+#pragma unroll
+      for (int q = 0; q < qb; ++q) {
+        const double h = cj[lane + 32 * q];
+        s[q] = make_double2(fma(h, x.x, s[q].x), fma(h, x.y, s[q].y));
+        sd[q] = make_double2(fma(h, xd.x, sd[q].x), fma(h, xd.y, sd[q].y));
+      }
+      if (lane < jj) {
+        const double h = cj[lane + 32 * qb];
+        s[qb] = make_double2(fma(h, x.x, s[qb].x), fma(h, x.y, s[qb].y));
+        sd[qb] = make_double2(fma(h, xd.x, sd[qb].x), fma(h, xd.y, sd[qb].y));
+      }
+      x = make_double2(__shfl_sync(0xffffffffu, xn.x, jj), __shfl_sync(0xffffffffu, xn.y, jj));
+      xd = make_double2(__shfl_sync(0xffffffffu, xdn.x, jj), __shfl_sync(0xffffffffu, xdn.y, jj));
+      if ((jj & 3) == 0) {                                             // warp-uniform rescale
+        const double mx = fabs(x.x) + fabs(x.y) + fabs(xd.x) + fabs(xd.y);
+        if (mx > 1e100 || (mx < 1e-100 && mx > 0.0)) {
+          const double f = 1.0 / mx;
+          x = make_double2(x.x * f, x.y * f);
+          xd = make_double2(xd.x * f, xd.y * f);
+#pragma unroll
+          for (int q = 0; q < AB_RQ; ++q) {
+            s[q] = make_double2(s[q].x * f, s[q].y * f);
+            sd[q] = make_double2(sd[q].x * f, sd[q].y * f);
+          }
+        }
+      }
+    }
+  }
+  // row 0 (owner: lane 0, block 0): α = (h_00 − z) x_0 + s_0, α' = (h_00 − z) x'_0 − x_0 + s'_0
+  double2 N = make_double2(0.0, 0.0);
+  if (lane == 0) {
+    const double2 dz = make_double2(hc[0] - z.x, -z.y);
+    const double2 a = cadd(cmul(dz, x), s[0]);
+    const double2 ad = csub(cadd(cmul(dz, xd), sd[0]), x);
+    N = cdiv(a, ad);
+  }
+  return make_double2(__shfl_sync(0xffffffffu, N.x, 0), __shfl_sync(0xffffffffu, N.y, 0));
+}
+
+// z, zn: r complex each; act: r ints (all in shared memory, aliasing free space of the caller)
+static __device__ int aberth_eigs(const double* Hg, int r, double* hc, const double2* z0, int n0,
+                                  double2* z, double2* zn, int* act, double2* lam_out, int tid,
+                                  int warp, int lane, int* its_out, int* evals_out) {
+  __shared__ int sh_na, sh_bad;
+  __shared__ double sh_tr[2];
+  if (n0 != r || z0 == nullptr || r < 2) return -1;
+  // column-packed H: column j holds rows 0..min(j+1, r-1); 1/h_{j+1,j} replaces h_{j+1,j}
+  for (int j = warp; j < r; j += K4_WARPS) {
+    const int len = j + 2 < r ? j + 2 : r;
+    for (int i = lane; i < len; i += 32) hc[ab_cofs(j) + i] = __ldcg(Hg + (long long)i * r + j);
+  }
+  if (tid == 0) { sh_bad = 0; sh_tr[0] = 0.0; sh_tr[1] = 0.0; }
+  __syncthreads();
+  for (int j = tid + 1; j < r; j += K4_THREADS) {
+    const double sub = hc[ab_cofs(j - 1) + j];
+    const double sc = fabs(hc[ab_cofs(j - 1) + j - 1]) + fabs(hc[ab_cofs(j) + j]);
+    if (!(fabs(sub) > DBL_EPSILON * sc) || !isfinite(sub)) atomicOr(&sh_bad, 1);   // reducible
+  }
+  __syncthreads();
+  if (sh_bad) return -1;
+  for (int j = tid + 1; j < r; j += K4_THREADS) hc[ab_cofs(j - 1) + j] = 1.0 / hc[ab_cofs(j - 1) + j];
+  // initial guesses: the warm spectrum, real roots nudged off the axis (alternating sides), every
+  // root perturbed by a distinct relative 1e-9 k so that repeated values separate
+  for (int k = tid; k < r; k += K4_THREADS) {
+    double2 g = z0[k];
+    const double a = hypot(g.x, g.y);
+    const double sc = a > 0.0 ? a : 1.0;
+    if (g.y == 0.0) g.y = ((k & 1) ? 1e-3 : -1e-3) * sc;
+    g.x *= 1.0 + 1e-9 * (k + 1);
+    z[k] = g;
+    act[k] = k;
+  }
+  if (tid == 0) sh_na = r;
+  __syncthreads();
+  int its = 0, evals = 0;
+  const double tol = 4.0 * DBL_EPSILON;
+  while (sh_na > 0) {
+    if (its == AB_MAXIT) return -1;
+    ++its;
+    const int na = sh_na;
+    evals += na;
+    for (int q = warp; q < na; q += K4_WARPS) {             // one warp per active root
+      const int k = act[q];
+      const double2 zk = z[k];
+      const double2 N = hyman_ratio(hc, r, zk, lane);
+      double2 S = make_double2(0.0, 0.0);                  // Σ_{j≠k} 1/(z_k − z_j)
+      for (int jj = lane; jj < r; jj += 32)
+        if (jj != k) {                                     // 1/d = conj(d)/|d|^2
+          const double2 d = csub(zk, z[jj]);
+          const double id = 1.0 / fma(d.x, d.x, d.y * d.y);
+          S = make_double2(fma(d.x, id, S.x), fma(-d.y, id, S.y));
+        }
+      S = wsum2(S);
+      if (lane == 0) {
+        const double2 den = csub(make_double2(1.0, 0.0), cmul(N, S));
+        const double2 step = cdiv(N, den);
+        double2 nz = csub(zk, step);
+        if (!isfinite(nz.x) || !isfinite(nz.y)) { sh_bad = 1; nz = zk; }
+        zn[k] = nz;
+        // frozen when the correction is at rounding level (encoded in act by the compaction)
+        if (hypot(step.x, step.y) <= tol * hypot(nz.x, nz.y)) act[q] = -1 - k;
+      }
+    }
+    __syncthreads();
+    if (sh_bad) return -1;
+    for (int q = tid; q < na; q += K4_THREADS) {            // publish the new iterate
+      const int a = act[q];
+      const int k = a >= 0 ? a : -1 - a;
+      z[k] = zn[k];
+    }
+    __syncthreads();
+    if (tid == 0) {                                           // compact the active list in order
+      int c = 0;
+      for (int q = 0; q < na; ++q)
+        if (act[q] >= 0) act[c++] = act[q];
+      sh_na = c;
+    }
+    __syncthreads();
+  }
+  // trace check: Σ z_k = Σ h_kk (a lost/duplicated root shows here)
+  if (warp == 0) {
+    double2 sz = make_double2(0.0, 0.0);
+    double tr = 0.0, ta = 0.0;
+    for (int k = lane; k < r; k += 32) {
+      sz = cadd(sz, z[k]);
+      tr += hc[ab_cofs(k) + k];
+      ta += fabs(hc[ab_cofs(k) + k]) + hypot(z[k].x, z[k].y);
+    }
+    sz = wsum2(sz);
+    tr = wsum(tr);
+    ta = wsum(ta);
+    if (lane == 0 && (fabs(sz.x - tr) > 1e-10 * ta || fabs(sz.y) > 1e-10 * ta)) sh_bad = 1;
+  }
+  __syncthreads();
+  if (sh_bad) return -1;
+  // exact conjugate symmetry: snap near-real roots, pair each Im > 0 root with the Im < 0 root
+  // nearest to its conjugate (thread 0, O(r^2); r <= 224)
+  if (tid == 0) {
+    for (int k = 0; k < r; ++k) {
+      act[k] = 0;                                            // 0 unpaired, 1 done
+      if (fabs(z[k].y) <= 1e-10 * hypot(z[k].x, z[k].y)) { z[k].y = 0.0; act[k] = 1; }
+    }
+    for (int k = 0; k < r && !sh_bad; ++k) {
+      if (act[k] || z[k].y < 0.0) continue;
+      int best = -1;
+      double bd = 0.0;
+      for (int j = 0; j < r; ++j) {
+        if (act[j] || z[j].y >= 0.0) continue;
+        const double d = hypot(z[j].x - z[k].x, z[j].y + z[k].y);
+        if (best < 0 || d < bd) { best = j; bd = d; }
+      }
+      if (best < 0 || bd > 1e-8 * hypot(z[k].x, z[k].y)) { sh_bad = 1; break; }
+      const double re = 0.5 * (z[k].x + z[best].x), im = 0.5 * (z[k].y - z[best].y);
+      z[k] = make_double2(re, im);
+      z[best] = make_double2(re, -im);
+      act[k] = act[best] = 1;
+    }
+    for (int k = 0; k < r && !sh_bad; ++k)
+      if (!act[k]) sh_bad = 1;
+  }
+  __syncthreads();
+  if (sh_bad) return -1;
+  for (int k = tid; k < r; k += K4_THREADS) lam_out[k] = z[k];
+  if (its_out) *its_out = its;
+  if (evals_out) *evals_out = evals;
+  __syncthreads();
+  return 0;
+}
+
 // Inverse iteration on the Hessenberg form H (row-major r x r, global) for eigenvalue lam, one
 // warp.  Returns the right eigenvector w = Q z and (if yout) the left eigenvector y = Q u of the
 // ORIGINAL matrix Ã = Q H Qᵀ, both unit 2-norm; w additionally has its largest entry real > 0.
@@ -671,14 +884,16 @@ static __device__ void iv_apply_q(const double* Qv, const double* tau, int r, do
   }
 }
 
-static __device__ void inverse_iteration(const double* H, const double* Qv, const double* tau, int r,
-                                         double2 lam, double2* M, double2* z, double2* rhs,
-                                         double2* lk, int* sw, double2* wout, double2* yout,
-                                         int lane) {
-  double hn = 0.0;
-  for (int i = 0; i < r; ++i)
-    for (int j = (i > 0 ? i - 1 : 0) + lane; j < r; j += 32) hn = fmax(hn, fabs(__ldcg(H + (long long)i * r + j)));
-  hn = wmax(hn);
+// (H − λI) = P L U (see inverse_iteration); hn_in >= 0: max |h_ij| precomputed by the caller
+static __device__ void iv_lu(const double* H, int r, double2 lam, double2* M, double2* lk, int* sw,
+                             int lane, double hn_in) {
+  double hn = hn_in;
+  if (hn < 0.0) {
+    hn = 0.0;
+    for (int i = 0; i < r; ++i)
+      for (int j = (i > 0 ? i - 1 : 0) + lane; j < r; j += 32) hn = fmax(hn, fabs(__ldcg(H + (long long)i * r + j)));
+    hn = wmax(hn);
+  }
   const double small = (hn > 0.0 ? hn : 1.0) * DBL_EPSILON;
   // ---- streaming LU of (H - λI); U rows -> M (row-major, entries j >= k of row k)
   double2 cur[IV_S], nxt[IV_S];
@@ -719,6 +934,12 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
     if (lane == ((r - 1) & 31)) M[(long long)(r - 1) * r + r - 1] = (cabs2(d) == 0.0) ? make_double2(small, 0.0) : d;
   }
   __syncwarp();
+}
+
+// right eigenvector from the LU of iv_lu: two solves U z = (L⁻¹P) rhs, w = Q z, Q12 normalisation
+static __device__ void iv_right(const double* Qv, const double* tau, int r, const double2* M,
+                                const double2* lk, const int* sw, double2* z, double2* rhs,
+                                double2* wout, int lane) {
   // ---- right vector: two solves U z = (L⁻¹P) rhs, rhs = e then the normalised z
   for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
   __syncwarp();
@@ -793,7 +1014,12 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
     if (lane == 0) wout[bi] = make_double2(wout[bi].x, 0.0);
     __syncwarp();
   }
-  if (yout == nullptr) return;
+}
+
+// left eigenvector from the LU of iv_lu: Mᴴ u = e (two solves), y = Q u, unit norm
+static __device__ void iv_left(const double* Qv, const double* tau, int r, const double2* M,
+                               const double2* lk, const int* sw, double2* z, double2* rhs,
+                               double2* yout, int lane) {
   // ---- left vector: Mᴴ u = e  →  Uᴴ a = rhs (forward), then a ← S_k E_kᴴ a for k = r-2 … 0
   for (int i = lane; i < r; i += 32) rhs[i] = make_double2(1.0, 0.0);
   __syncwarp();
@@ -839,6 +1065,16 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
   for (int i = lane; i < r; i += 32) yout[i] = z[i];
   __syncwarp();
   iv_apply_q(Qv, tau, r, yout, lane);
+}
+
+static __device__ void inverse_iteration(const double* H, const double* Qv, const double* tau, int r,
+                                         double2 lam, double2* M, double2* z, double2* rhs,
+                                         double2* lk, int* sw, double2* wout, double2* yout,
+                                         int lane, double hn = -1.0) {
+  iv_lu(H, r, lam, M, lk, sw, lane, hn);
+  __syncwarp();
+  iv_right(Qv, tau, r, M, lk, sw, z, rhs, wout, lane);
+  if (yout != nullptr) iv_left(Qv, tau, r, M, lk, sw, z, rhs, yout, lane);
 }
 
 // ------------------------------------------------------------------ the per-frame kernel ------
@@ -1346,10 +1582,26 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   const double sigma1 = res->sigma1;
   double* H = p.H;
 
-  // ---- a8: eigenvalues by Francis double-shift QR in shared memory (warp 0)
+  // ---- a8: eigenvalues.  Ehrlich–Aberth (Hyman's method) warm-started from the previous frame of
+  // this worker stream; the Francis multishift QR in shared memory when there is no warm spectrum
+  // of the same size, H is reducible, or the iteration does not certify (see aberth_eigs)
   double* hs = reinterpret_cast<double*>(k4_smem);
   const long long hsz = hs_elems(r);
   double2* lam_raw = reinterpret_cast<double2*>(hs + ((hsz + 1) & ~1LL));
+  __shared__ MsShared ms_sh;
+  int ab_rc = -1, ab_its = 0, ab_ev = 0;
+  bool ab_tried = false;
+  if (r > K4_MS_SMALL && p.r_warm != nullptr) {
+    const int n0 = *(volatile const int*)p.r_warm;
+    if (n0 == r) {
+      ab_tried = true;
+      double2* zz = reinterpret_cast<double2*>(ms_sh.dense);      // MsShared is free until the QR
+      double2* zn = zz + kMaxR;
+      int* act = reinterpret_cast<int*>(zn + kMaxR);
+      ab_rc = aberth_eigs(H, r, hs, p.lam_warm, n0, zz, zn, act, lam_raw, tid, warp, lane, &ab_its, &ab_ev);
+    }
+  }
+  if (ab_rc != 0) {
   for (int i = warp; i < r; i += K4_WARPS) {
     const int lo = i > 3 ? i - 3 : 0;
     const long long o = hs_off(i, r);
@@ -1359,7 +1611,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   for (int i = tid; i < r; i += K4_THREADS) lam_raw[i] = make_double2(0.0, 0.0);
   __syncthreads();
   {
-    __shared__ MsShared ms_sh;
     __shared__ int qc_sh[4];
     if (tid < 4) qc_sh[tid] = 0;
     __shared__ int its_sh;
@@ -1384,6 +1635,16 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       res->qr_dbg[1] = chase_cyc[1];
     }
   }
+  } else if (tid == 0) {
+    sh_its = 0;
+    res->qr_cnt[0] = res->qr_cnt[1] = res->qr_cnt[2] = res->qr_cnt[3] = 0;
+    res->phase[7] = 0;
+    res->qr_dbg[0] = res->qr_dbg[1] = 0;
+  }
+  if (tid == 0) {
+    res->aberth_its = ab_rc == 0 ? ab_its : (ab_tried ? -1 : 0);
+    res->aberth_evals = ab_ev;
+  }
   __syncthreads();
   if (tid == 0) ph[6] = clock64();
 
@@ -1402,6 +1663,10 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     p.lam[rk] = lj;
   }
   __syncthreads();
+  if (p.r_warm != nullptr) {                      // the next frame of this stream starts from here
+    for (int k = tid; k < r; k += K4_THREADS) p.lam_warm[k] = p.lam[k];
+    if (tid == 0) *p.r_warm = (sh_status == 5) ? 0 : r;
+  }
 
   // ---- a10: idx = argmin |log λ| (principal branch), λ = 0 excluded; ties (Q5)
   if (tid == 0) {
@@ -1545,49 +1810,81 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     return;
   }
 
-  // ---- a8/a9: eigenvectors of the background mode, b_idx, and c (warp 0); scratch aliases the
+  // ---- a8/a9: eigenvectors of the background mode (LU on warp 0, then the right solve on warp 0
+  // and the left solve on warp 1 concurrently), b_idx, and c (all threads); scratch aliases the
   // (now free) packed Hessenberg area
   double2* z = reinterpret_cast<double2*>(k4_smem);
   double2* rhs = z + kMaxR;
   double2* lk = rhs + kMaxR;
-  int* swk = reinterpret_cast<int*>(lk + kMaxR);
-  if (idx >= 0 && warp == 0) {
-    const double2 lam = p.lam[idx];
-    inverse_iteration(H, p.Qv, p.tau, r, lam, p.M, z, rhs, lk, swk, p.w, p.y, lane);
-    double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
-    for (int i = lane; i < r; i += 32) {
-      const double2 yc = cconj(p.y[i]);
-      ya = cadd(ya, make_double2(yc.x * p.alpha1[i], yc.y * p.alpha1[i]));
-      yw = cadd(yw, cmul(yc, p.w[i]));
-    }
-    ya = wsum2(ya);
-    yw = wsum2(yw);
-    const double2 den = cmul(lam, yw);
-    double2 b = make_double2(0.0, 0.0);
-    int st = sh_status;
-    if (cabs2(den) > 1e-300) b = cdiv(ya, den);
-    else if (st == 0) st = 6;
-    double2 pw = make_double2(1.0, 0.0), base = lam;       // λ^m by binary powering
-    for (int e = m; e > 0; e >>= 1) {
-      if (e & 1) pw = cmul(pw, base);
-      base = cmul(base, base);
-    }
-    const double2 coef = cmul(b, pw);
-    for (int i = lane; i < m; i += 32) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int j = 0; j < r; ++j) {
-        const double yv = p.Y[(long long)j * m + i];
-        s = cadd(s, make_double2(yv * p.w[j].x, yv * p.w[j].y));
+  double2* z2 = lk + kMaxR;
+  double2* rhs2 = z2 + kMaxR;
+  double2* wsm = rhs2 + kMaxR;
+  int* swk = reinterpret_cast<int*>(wsm + kMaxR);
+  __shared__ double hn_sh;
+  __shared__ double2 coef_sh;
+  __shared__ int st_sh;
+  if (idx >= 0) {
+    {                                                    // max |h_ij| of the Hessenberg form
+      double hn = 0.0;
+      for (int e = tid; e < r * r; e += K4_THREADS) {
+        const int i = e / r, j = e % r;
+        if (j >= i - 1) hn = fmax(hn, fabs(__ldcg(H + e)));
       }
-      p.cout[i] = cmul(coef, s);
+      hn = wmax(hn);
+      if (tid == 0) hn_sh = 0.0;
+      __syncthreads();
+      if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&hn_sh), __double_as_longlong(hn));
+      __syncthreads();
     }
-    if (lane == 0) {
+    const double2 lam = p.lam[idx];
+    if (warp == 0) iv_lu(H, r, lam, p.M, lk, swk, lane, hn_sh);
+    __syncthreads();
+    if (warp == 0) iv_right(p.Qv, p.tau, r, p.M, lk, swk, z, rhs, p.w, lane);
+    else if (warp == 1) iv_left(p.Qv, p.tau, r, p.M, lk, swk, z2, rhs2, p.y, lane);
+    __syncthreads();
+    if (warp == 0) {
+      double2 ya = make_double2(0, 0), yw = make_double2(0, 0);
+      for (int i = lane; i < r; i += 32) {
+        const double2 yc = cconj(p.y[i]);
+        ya = cadd(ya, make_double2(yc.x * p.alpha1[i], yc.y * p.alpha1[i]));
+        yw = cadd(yw, cmul(yc, p.w[i]));
+      }
+      ya = wsum2(ya);
+      yw = wsum2(yw);
+      if (lane == 0) {
+        const double2 den = cmul(lam, yw);
+        double2 b = make_double2(0.0, 0.0);
+        int st = sh_status;
+        if (cabs2(den) > 1e-300) b = cdiv(ya, den);
+        else if (st == 0) st = 6;
+        double2 pw = make_double2(1.0, 0.0), base = lam;   // λ^m by binary powering
+        for (int e = m; e > 0; e >>= 1) {
+          if (e & 1) pw = cmul(pw, base);
+          base = cmul(base, base);
+        }
+        coef_sh = cmul(b, pw);
+        st_sh = st;
+        res->b_idx[0] = b.x; res->b_idx[1] = b.y;
+      }
+    }
+    for (int j = tid; j < r; j += K4_THREADS) wsm[j] = p.w[j];
+    __syncthreads();
+    const double2 coef = coef_sh;
+    for (int i = tid; i < m; i += K4_THREADS) {          // c = b_idx λ^m Y w_idx, one row per thread
+      double2 sacc = make_double2(0.0, 0.0);
+      for (int j = 0; j < r; ++j) {
+        const double yv = __ldcg(p.Y + (long long)j * m + i);
+        sacc = make_double2(fma(yv, wsm[j].x, sacc.x), fma(yv, wsm[j].y, sacc.y));
+      }
+      p.cout[i] = cmul(coef, sacc);
+    }
+    if (tid == 0) {
       ph[7] = clock64();
       res->phase[5] = ph[6] - ph[5];
       res->phase[6] = ph[7] - ph[6];
-      res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
+      res->frame = f; res->status = st_sh; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
-      res->b_idx[0] = b.x; res->b_idx[1] = b.y; res->sigma1 = sigma1;
+      res->sigma1 = sigma1;
       res->nkeep = sh_nkeep; res->nB = 1; res->bset[0] = idx;
     }
   } else if (idx < 0) {
@@ -1602,11 +1899,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
 size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const long long hs = hs_elems(r_max);
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
-  const size_t b = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);
+  const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
   const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
   const size_t d = ((size_t)((r_max + 3) / 4) * r_max + 2 * kMaxR) * sizeof(double);  // Hessenberg rows
   // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
-  const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b + (size_t)m * sizeof(double2)) : 0;
+  const size_t b3 = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // per mode
+  const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b3 + (size_t)m * sizeof(double2)) : 0;
   size_t s = a > b ? a : b;
   s = s > c ? s : c;
   s = s > e ? s : e;

@@ -165,6 +165,9 @@ struct sdmd_ctx {
   double2* sg_b[kMaxWorkers]{};
   unsigned int* sg_cnt = nullptr;
   double2* od_A = nullptr;
+  // eig(Ã) warm start per single-CTA worker stream (sorted spectrum and r of its previous frame)
+  double2* lam_warm[kMaxWorkers]{};
+  int* r_warm = nullptr;
   // workers
   Workspace ws[kMaxWS];
   int NWS = 0, Wa = 1, Wb = 4;
@@ -640,6 +643,9 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     }
     AL(c->sg_cnt, (size_t)kMaxWorkers);
     cudaMemsetAsync(c->sg_cnt, 0, kMaxWorkers * sizeof(unsigned int), c->stream);
+    for (int w = 0; w < c->Wb; ++w) AL(c->lam_warm[w], (size_t)kMaxR);
+    AL(c->r_warm, (size_t)kMaxWorkers);
+    cudaMemsetAsync(c->r_warm, 0, kMaxWorkers * sizeof(int), c->stream);
   }
   for (int i = 0; i < kEvents; ++i) {
     if (cudaEventCreateWithFlags(&c->ev_commit[i], cudaEventDisableTiming) != cudaSuccess ||
@@ -741,7 +747,7 @@ int sdmd_destroy(sdmd_ctx* c) {
   }
   void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
                   c->sp_val, c->sp_nnz, c->scratch, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
-                  c->Gtmp, c->init_work, c->sg_cnt, c->od_A};
+                  c->Gtmp, c->init_work, c->sg_cnt, c->od_A, c->r_warm};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int w = 0; w < kMaxWS; ++w) {
@@ -755,7 +761,7 @@ int sdmd_destroy(sdmd_ctx* c) {
     if (c->sa[w]) cudaStreamDestroy(c->sa[w]);
     if (c->sb[w]) cudaStreamDestroy(c->sb[w]);
     void* pm[] = {c->pm_M[w], c->pm_W[w], c->pm_b[w], c->pm_T[w], c->pm_phi[w], c->sg_M[w], c->sg_W[w],
-                  c->sg_A[w], c->sg_b[w]};
+                  c->sg_A[w], c->sg_b[w], c->lam_warm[w]};
     for (void* q : pm)
       if (q) cudaFree(q);
   }
@@ -782,6 +788,11 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m) {
     const Workspace& kp = ws_of(c, fp);
     p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = (int)(f - fp);
+  }
+  if (c->r_warm) {
+    const int sw = (int)(lidx(c, f) % c->Wb);
+    p.lam_warm = c->lam_warm[sw];
+    p.r_warm = c->r_warm + sw;
   }
   return p;
 }
@@ -1489,18 +1500,19 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   return SDMD_OK;
 }
 
-int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[20]) {
+int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[24]) {
   if (!c || !out) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   K4Result res{};
   int st = newest_result(c, &res);
   if (st) return st;
-  for (int i = 0; i < 20; ++i) out[i] = 0;
+  for (int i = 0; i < 24; ++i) out[i] = 0;
   out[0] = res.frame; out[1] = res.status; out[2] = res.r; out[3] = res.idx;
   out[4] = res.sweeps; out[5] = res.qr_its;
   for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q];
   out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[3];
   out[16] = res.phase[7]; out[17] = res.qr_cnt[2]; out[18] = res.qr_dbg[0]; out[19] = res.qr_dbg[1];
+  out[20] = res.aberth_its; out[21] = res.aberth_evals;
   return SDMD_OK;
 }
 

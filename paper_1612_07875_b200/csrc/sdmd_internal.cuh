@@ -103,6 +103,8 @@ struct K4Result {
   double sigma1;
   long long phase[8];         // SM cycles per K4 phase: build S, Jacobi, sort/V, Ã, Hessenberg (K4a), QR, eigvec+c (K4b)
   int qr_cnt[4];              // QR: single-bulge steps, multishift steps, single-bulge its, multishift sweeps
+  int aberth_its;             // Ehrlich–Aberth iterations (0: not used), < 0: failed → QR fallback
+  int aberth_evals;           // Hyman evaluations
   long long qr_dbg[2];        // SM cycles of the multishift chase: (AB) phase + barrier, (C) phase + barrier (warp 0)
   long long vframe;           // frame whose converged eigenvectors V this workspace holds (K4a), or -1
   int nkeep;                  // modes with |λ_j| >= rank_tol·max|λ| (a prefix of the sorted λ); < r → W_SINGULAR
@@ -172,6 +174,10 @@ struct K4Params {
   const double* Vprev;
   const K4Result* res_prev;
   int warm_k;
+  // eig(Ã) warm start: the sorted spectrum of the previous frame solved on the same single-CTA
+  // worker stream (stream-ordered: read at the start of K4b, rewritten at its end)
+  double2* lam_warm;          // kMaxR
+  int* r_warm;                // its r (0: none yet)
 };
 
 // per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)

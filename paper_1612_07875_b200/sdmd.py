@@ -427,7 +427,7 @@ class StreamingDMD:
         return fr.value
 
     def frame_diag(self) -> dict:
-        o = np.zeros(20, dtype=np.int64)
+        o = np.zeros(24, dtype=np.int64)
         self._check(lib().sdmd_get_frame_diag(self.h, _dp(o)), "get_frame_diag")
         names = ["build_S", "jacobi", "sort_V", "atilde", "hessenberg", "qr", "eigvec_c"]
         return dict(frame=int(o[0]), status=int(o[1]), r=int(o[2]), idx=int(o[3]),
@@ -435,7 +435,8 @@ class StreamingDMD:
                     cycles={k: int(v) for k, v in zip(names, o[6:13])},
                     qr_steps=int(o[13]), ms_steps=int(o[14]), ms_sweeps=int(o[15]),
                     ms_shift_cycles=int(o[16]), qr_block_its=int(o[17]),
-                    ms_chase_ab_cycles=int(o[18]), ms_chase_c_cycles=int(o[19]))
+                    ms_chase_ab_cycles=int(o[18]), ms_chase_c_cycles=int(o[19]),
+                    aberth_its=int(o[20]), aberth_evals=int(o[21]))
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")
