@@ -34,6 +34,7 @@ they are checked only GPU-vs-oracle within κ(λ)·‖ΔÃ‖ (DESIGN.md §"Pari
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 
 import numpy as np
@@ -451,6 +452,132 @@ def background_first_window(Z_cols, d: dict, b, idx: int, threshold: float = 0.2
     Z = np.stack([np.asarray(c, dtype=np.float64) for c in Z_cols], axis=1)
     S = Z - L
     return L, S, S > threshold
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-3  Compressed ingestion beyond the real DCT  (§3.5; reading Q10/Q11, Q27)
+# ----------------------------------------------------------------------------------------
+
+def rfft_weights(rows: int, cols: int) -> np.ndarray:
+    """Weights of the stored half spectrum of a real rows x cols field (numpy.fft.rfft2 layout:
+    bin (ky, kx), ky in [0, rows), kx in [0, cols//2], flat index ky*(cols//2+1) + kx).
+
+    Reading Q10's trap: the omitted bins are the complex conjugates of the stored
+    bins (kx, ky) -> (-kx, -ky), so Parseval over the full spectrum counts every stored bin twice,
+    except the columns kx = 0 and, for even cols, kx = cols/2, whose partners are stored themselves.
+    Weight 2 off those columns, 1 on them."""
+    h = cols // 2 + 1
+    w = np.full((rows, h), 2.0)
+    w[:, 0] = 1.0
+    if cols % 2 == 0:
+        w[:, cols // 2] = 1.0
+    return w.ravel()
+
+
+def fourier_gram_column(slots, x_new, n: int, weights=None) -> np.ndarray:
+    """Gram column over complex Fourier-coefficient snapshots (reading Q27): each snapshot is
+    (idx, val) with complex val; g_k = Σ_i w_i Re(conj(ẑ_k[i]) x̂[i]) over the scattered dense
+    vectors (definition; w = 1 for full-spectrum storage, rfft_weights for the half spectrum).
+    With the unitary ("ortho") transform this is the pixel-space inner product (Parseval, P:359
+    "unitary transforms"); the real part is exact for Hermitian data, where the imaginary parts
+    cancel.  Evaluated as compensated row-order dots (O1) of the real vectors [w·Re ẑ, w·Im ẑ] and
+    [Re x̂, Im x̂]: w ∈ {1, 2} scales exactly."""
+    wt = np.ones(n) if weights is None else np.asarray(weights, dtype=np.float64)
+
+    def dense(sv, weighted):
+        idx, val = sv
+        idx = np.asarray(idx, dtype=np.int64)
+        d = np.zeros(n, dtype=np.complex128)
+        d[idx] = np.asarray(val, dtype=np.complex128)
+        if weighted:
+            d = d * wt
+        return np.concatenate([d.real, d.imag])
+    return gram_column([dense(s, True) for s in slots], dense(x_new, False))
+
+
+def modes_complex(Xp_cols, d: dict, which=None) -> np.ndarray:
+    """Φ̂ = X̂'(vsi W) for complex coefficient-space columns (Eq. Phi P:158-160 in the Fourier
+    basis, NEXT-3): (A + iB) T = A T + i B T with A = Re X̂', B = Im X̂', each a compensated O7
+    sum (C orc_modes)."""
+    if isinstance(Xp_cols, np.ndarray) and Xp_cols.ndim == 2:
+        Xp_cols = [Xp_cols[:, k] for k in range(Xp_cols.shape[1])]
+    cols = [np.asarray(c, dtype=np.complex128) for c in Xp_cols]
+    return modes([c.real for c in cols], d, which) + 1j * modes([c.imag for c in cols], d, which)
+
+
+def dct_matrix(N: int) -> np.ndarray:
+    """Orthonormal DCT-II matrix (reading Q11): C[k, p] = w_k cos(π k (2p+1) / (2N)), w_0 = √(1/N),
+    w_k = √(2/N).  X̂ = C x;  x = Cᵀ X̂ (DCT-III, the inverse, since C is orthogonal)."""
+    k = np.arange(N)[:, None]
+    p = np.arange(N)[None, :]
+    C = np.cos(np.pi * k * (2 * p + 1) / (2.0 * N))
+    C[0, :] *= np.sqrt(1.0 / N)
+    C[1:, :] *= np.sqrt(2.0 / N)
+    return C
+
+
+def idct2(coef, rows: int, cols: int) -> np.ndarray:
+    """Pixel field (row-major rows x cols, flattened) of orthonormal 2-D DCT-II coefficients
+    (flat index ky*cols + kx): x = C_rowsᵀ X̂ C_cols, two matrix products (library primitive)."""
+    Xh = np.asarray(coef).reshape(rows, cols)
+    if np.iscomplexobj(Xh):
+        return idct2(Xh.real, rows, cols) + 1j * idct2(Xh.imag, rows, cols)
+    return (dct_matrix(rows).T @ Xh @ dct_matrix(cols)).ravel()
+
+
+def background_newest_pixel(Xp_slots, x_slot, n: int, rows: int, cols: int, d: dict, b, idx: int,
+                            threshold: float = 0.2):
+    """Streaming branch of Alg 3 for a sparse-DCT context, returned in pixel space
+    (NEXT-3 "an inverse-DCT kernel for pixel-space background", "transfer the compressed
+    DMD from the GPU back"): φ̂_idx = X̂'(vsi w_idx) over the scattered coefficient columns (O7),
+    l̂ = b_idx φ̂_idx λ_idx^m (e = m, Q4), l = IDCT2(l̂) (the transform is linear and real, so it
+    maps the complex coefficient vector part by part), x = IDCT2(x̂_newest), s = x − |l|,
+    mask = s > threshold (Q8)."""
+    def dense(sv):
+        i, v = sv
+        z = np.zeros(n)
+        z[np.asarray(i, dtype=np.int64)] = np.asarray(v, dtype=np.float64)
+        return z
+    m = d["m"]
+    phi = modes([dense(s) for s in Xp_slots], d, [idx])[:, 0]
+    lhat = b[idx] * phi * d["lam"][idx] ** m
+    low = np.abs(idct2(lhat, rows, cols))
+    x = idct2(dense(x_slot), rows, cols)
+    s = x - low
+    return low, s, s > threshold
+
+
+# ----------------------------------------------------------------------------------------
+# NEXT-4  BMC-style scoring  (Table 2 P:433-443; SPEC S:366-373; reading Q26)
+# ----------------------------------------------------------------------------------------
+
+def evaluate(masks, gts) -> dict:
+    """Recall, precision, F-measure and PSNR of foreground masks against ground-truth masks
+    (Table 2, "BMC Evaluation Wizard"; recall = TP/(TP+FN), precision =
+    TP/(TP+FP), F = 2PR/(P+R)).  Reading Q26: counts are pooled over all frames scored (one number
+    per sequence, as Table 2 reports); PSNR is that of the binary mask sequence against the
+    ground truth at the pixel range's peak (0/1 masks, i.e. 0/255 images): 10·log10(N / (FP+FN))
+    over the N pixels scored, +inf when no pixel differs.  Undefined ratios are reported as 0
+    with a flag."""
+    tp = fp = fn = tn = 0
+    for mk, gt in zip(masks, gts):
+        mk = np.asarray(mk).astype(bool).ravel()
+        gt = np.asarray(gt).astype(bool).ravel()
+        if mk.shape != gt.shape:
+            raise OracleError(E_INVALID, "mask and ground truth shapes differ")
+        tp += int(np.count_nonzero(mk & gt))
+        fp += int(np.count_nonzero(mk & ~gt))
+        fn += int(np.count_nonzero(~mk & gt))
+        tn += int(np.count_nonzero(~mk & ~gt))
+    npx = tp + fp + fn + tn
+    empty_gt = (tp + fn) == 0
+    empty_mask = (tp + fp) == 0
+    recall = 0.0 if empty_gt else tp / (tp + fn)
+    precision = 0.0 if empty_mask else tp / (tp + fp)
+    f = 0.0 if recall + precision == 0 else 2.0 * precision * recall / (precision + recall)
+    psnr = math.inf if fp + fn == 0 else 10.0 * math.log10(npx / (fp + fn))
+    return dict(tp=tp, fp=fp, fn=fn, tn=tn, recall=recall, precision=precision, f_measure=f,
+                psnr=psnr, empty_gt=empty_gt, empty_mask=empty_mask)
 
 
 # ----------------------------------------------------------------------------------------

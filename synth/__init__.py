@@ -347,6 +347,105 @@ class SparseDCTStream:
         return x
 
 
+class SparseFourierStream:
+    """Sparse snapshots of a real rows x cols field in the unitary 2-D Fourier basis (SURVEY Q10's
+    "complex FFT" variant of C5).  Values complex128, indices int32 ascending.
+
+    half=True: the stored half spectrum of numpy.fft.rfft2 (bin (ky, kx), kx <= cols//2, flat
+    index ky*(cols//2+1) + kx); half=False: the full spectrum (flat index ky*cols + kx), every
+    bin's conjugate partner stored as well.  A fixed low band |k| <= k_low (signed wavenumbers)
+    carries A(k) e^{i(ω(k) t + θ_k)}, A = (1+|k|)^-2, ω = 0.05|k|^(2/3); each frame adds n_shell
+    fresh bins from the shell k_low < |k| <= min(rows, cols)/2, off the self-conjugate columns
+    (kx = 0, cols/2), with values A (N(0,1) + i N(0,1))/√2.  Hermitian consistency (a real field)
+    is built in: on the self-conjugate columns X[-ky] = conj(X[ky]) and the self-paired bins are
+    real; in the full spectrum every bin's partner (-ky, -kx) holds the conjugate."""
+
+    def __init__(self, rows: int = 1024, cols: int = 1024, k_low: float = 110.0,
+                 n_shell: int = 1000, seed: int = 1617, half: bool = True):
+        self.rows, self.cols, self.half = rows, cols, half
+        self.h = cols // 2 + 1
+        self.n = rows * self.h if half else rows * cols
+        self.seed, self.n_shell = seed, n_shell
+        ky = np.arange(rows)
+        kys = np.where(ky <= rows // 2, ky, ky - rows).astype(np.float64)
+        kx = np.arange(self.h).astype(np.float64)
+        KY, KX = np.meshgrid(kys, kx, indexing="ij")
+        kk = np.sqrt(KY ** 2 + KX ** 2)                   # (rows, h)
+        self.kmag = kk.ravel()
+        self_conj_col = np.zeros(self.h, dtype=bool)
+        self_conj_col[0] = True
+        if cols % 2 == 0:
+            self_conj_col[cols // 2] = True
+        flat = np.arange(rows * self.h).reshape(rows, self.h)
+        low = kk <= k_low
+        # on a self-conjugate column keep only one bin of each conjugate pair (ky <= partner) as
+        # the generated one; the partner is filled by conjugation
+        partner = (-ky) % rows
+        gen = low.copy()
+        for c in np.nonzero(self_conj_col)[0]:
+            gen[:, c] &= ky <= partner
+        self.gen_idx = flat[gen].astype(np.int64)          # half-spectrum bins carrying values
+        self.low_idx = flat[low].astype(np.int64)          # all stored low-band bins
+        rng = np.random.default_rng(seed)
+        self.theta = rng.uniform(0, 2 * np.pi, size=self.gen_idx.size)
+        kg = self.kmag[self.gen_idx]
+        self.A = (1.0 + kg) ** -2.0
+        self.w = 0.05 * kg ** (2.0 / 3.0)
+        # bins that must be real (their own partner) and the partner map on self-conjugate columns
+        gy, gx = np.divmod(self.gen_idx, self.h)
+        self.gen_real = self_conj_col[gx] & (gy == partner[gy])
+        shell = (kk > k_low) & (kk <= min(rows, cols) / 2) & ~self_conj_col[None, :]
+        self.shell_idx = flat[shell].astype(np.int64)
+        self._partner_col = self_conj_col
+
+    @property
+    def nnz_cap(self) -> int:
+        n_half = int(self.low_idx.size + self.n_shell)
+        return n_half if self.half else 2 * n_half
+
+    def _half_frame(self, t: int):
+        """dict {half-spectrum flat index: complex value} of frame t."""
+        ph = self.w * t + self.theta
+        v = self.A * np.exp(1j * ph)
+        v = np.where(self.gen_real, v.real + 0j, v)
+        vals = dict(zip(self.gen_idx.tolist(), v.tolist()))
+        gy, gx = np.divmod(self.gen_idx, self.h)
+        for i, y, x, val in zip(self.gen_idx.tolist(), gy.tolist(), gx.tolist(), v.tolist()):
+            if self._partner_col[x]:
+                p = ((-y) % self.rows) * self.h + x
+                if p != i:
+                    vals[p] = complex(val).conjugate()
+        rng = np.random.default_rng((self.seed, t))
+        sh = rng.choice(self.shell_idx, size=self.n_shell, replace=False)
+        a = (1.0 + self.kmag[sh]) ** -2.0
+        sv = a * (rng.standard_normal(self.n_shell) + 1j * rng.standard_normal(self.n_shell)) / np.sqrt(2.0)
+        for i, val in zip(sh.tolist(), sv.tolist()):
+            vals[i] = val
+        return vals
+
+    def frame(self, t: int):
+        """(idx int32 ascending, val complex128) of frame t in this stream's storage."""
+        hv = self._half_frame(t)
+        if self.half:
+            idx = np.array(sorted(hv), dtype=np.int64)
+            return idx.astype(np.int32), np.array([hv[i] for i in idx.tolist()], dtype=np.complex128)
+        full = {}
+        for i, val in hv.items():
+            y, x = divmod(i, self.h)
+            full[y * self.cols + x] = val
+            px = (-x) % self.cols
+            if px != x:                                    # the omitted conjugate half
+                full[((-y) % self.rows) * self.cols + px] = complex(val).conjugate()
+        idx = np.array(sorted(full), dtype=np.int64)
+        return idx.astype(np.int32), np.array([full[i] for i in idx.tolist()], dtype=np.complex128)
+
+    def dense(self, t: int) -> np.ndarray:
+        idx, val = self.frame(t)
+        x = np.zeros(self.n, dtype=np.complex128)
+        x[idx] = val
+        return x
+
+
 CONFIGS = {
     # name: (description, n, m, dtype)
     "C1": ("synthetic n=4096, m=16, rank 4 closed-form modes, fp64", 4096, 16, "f64"),
