@@ -61,7 +61,7 @@
 extern "C" {
 #endif
 
-#define SDMD_ABI_VERSION 3
+#define SDMD_ABI_VERSION 4
 #define SDMD_MAX_M 256   /* largest window width m supported                              */
 #define SDMD_MAX_LAG 64  /* largest background lag (frames)                                     */
 #define SDMD_MAX_BATCH 8 /* largest k of sdmd_push_batch                                          */
@@ -85,6 +85,15 @@ enum sdmd_status {
 
 enum sdmd_dtype { SDMD_F32 = 0, SDMD_F64 = 1 };
 enum sdmd_storage { SDMD_DENSE = 0, SDMD_SPARSE = 1 };
+/* Basis of sparse snapshots (§3.5 P:355-363 "Fourier" compression; readings Q10, Q11, Q27):
+ *  SDMD_BASIS_DCT   real orthonormal 2-D DCT-II coefficients; val = nnz doubles
+ *  SDMD_BASIS_FFT   unitary 2-D DFT of a real field, FULL spectrum stored (every bin's conjugate
+ *                   partner present); val = nnz interleaved complex (re, im); g = Σ Re(conj(ẑ) x̂)
+ *  SDMD_BASIS_RFFT  the stored HALF spectrum of a real grid_rows x grid_cols field (rfft2 layout:
+ *                   index ky*(grid_cols/2+1) + kx); val = nnz interleaved complex; every bin off
+ *                   the self-conjugate columns kx = 0 and kx = grid_cols/2 (even grid_cols)
+ *                   counts twice (its omitted conjugate partner), g = Σ w Re(conj(ẑ) x̂)        */
+enum sdmd_basis { SDMD_BASIS_DCT = 0, SDMD_BASIS_FFT = 1, SDMD_BASIS_RFFT = 2 };
 enum sdmd_where { SDMD_HOST = 0, SDMD_DEVICE = 1, SDMD_HOST_ASYNC = 2 /* pinned host, stream-ordered */ };
 
 typedef struct sdmd_ctx sdmd_ctx; /* opaque; owns ALL device state (ring, G history, factors) */
@@ -121,9 +130,10 @@ typedef struct sdmd_config {
                        * consumes the background coefficients of frame t, so K4 may take up to
                        * lag frame periods before the Gram pass waits                          */
   int32_t eigen_shard; /* nranks > 1: 1 → the eigenproblems of frame t run only on rank t mod
-                       * nranks and its m background coefficients are broadcast (ncclBroadcast)
-                       * before the Gram pass that consumes them; the getters of a rank then
-                       * report the newest frame it solved.  0 → replicated on every rank      */
+                       * nranks; its m background coefficients ride the allreduce of a later
+                       * frame's Gram column (owner's values, zeros elsewhere: one collective per
+                       * push) before the Gram pass that consumes them; the getters of a rank
+                       * then report the newest frame it solved.  0 → replicated on every rank */
   int32_t batch_max;  /* largest k accepted by sdmd_push_batch, 0..SDMD_MAX_BATCH (0: batching
                        * off); the ring holds m + batch_max + 1 slots                          */
   int32_t bg_modes;   /* background modes: 0 or 1 → the single
@@ -140,6 +150,13 @@ typedef struct sdmd_config {
                        * DMMA; SURVEY §8(f) NEXT-2 "full Φ every frame") and sdmd_get_modes
                        * returns the newest frame's columns without recomputing.  Meant for
                        * small r (C2: r = 21); at C4 (r = 200) it would cost ~0.1 s per frame */
+  int32_t basis;      /* sparse storage: enum sdmd_basis (0 = DCT)                              */
+  int32_t grid_rows;  /* 2-D grid of the sparse transform (0: unknown).  DCT / FFT: n_global =   */
+  int32_t grid_cols;  /* grid_rows*grid_cols; RFFT: n_global = grid_rows*(grid_cols/2+1) and the
+                       * grid is required (the weights depend on grid_cols).  A sparse DCT context
+                       * with background = 1 returns its background in PIXEL space (SURVEY §8(f)
+                       * NEXT-3 "inverse-DCT kernel for pixel-space background"): one rank, grid
+                       * sides powers of two in [2, 4096], pixels row-major, fp64 outputs        */
 } sdmd_config;
 
 typedef struct sdmd_info {
@@ -167,6 +184,21 @@ typedef struct sdmd_stats {
                          * background coefficients of a later frame share it)                  */
 } sdmd_stats;
 
+/* BMC-style scores of the background masks (Table 2 P:437-443 "Recall,
+ * Precision, F-measure, Psnr"; reading Q26): counts pooled over every mask scored
+ * since the last reset, this rank's rows. */
+typedef struct sdmd_scores {
+  int64_t frames;       /* masks scored                                                          */
+  int64_t tp, fp, fn, tn; /* pixel counts: mask & gt, mask & !gt, !mask & gt, !mask & !gt         */
+  double recall;        /* tp / (tp + fn); 0 with empty_gt                                        */
+  double precision;     /* tp / (tp + fp); 0 with empty_mask                                      */
+  double f_measure;     /* 2PR / (P + R); 0 when P + R = 0                                        */
+  double psnr;          /* binary mask images at the range's peak: 10 log10(N / (fp + fn)) dB over
+                         * the N pixels scored; +inf when no pixel differs                         */
+  int32_t empty_gt;     /* tp + fn == 0 (recall undefined)                                 */
+  int32_t empty_mask;   /* tp + fp == 0 (precision undefined)                              */
+} sdmd_scores;
+
 /* Fill *cfg with defaults (rank_tol 1e-7, threshold 0.2, dmd 1, background 0, workers 4, …).
  * n_global/n_local/m must still be set by the caller. */
 int sdmd_config_init(sdmd_config* cfg);
@@ -190,8 +222,10 @@ int sdmd_init_window(sdmd_ctx* ctx, const void* Z, int64_t ldz, int where);
 int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
 
 /* Push one sparse snapshot in an orthonormal coefficient basis (§3.5): nnz pairs,
- * idx strictly ascending in [row_begin, row_begin + n_local) (int32), val fp64.  nnz <= nnz_cap.
- * The Gram column uses sparse–sparse inner products; nothing is densified in HBM.
+ * idx strictly ascending in [row_begin, row_begin + n_local) (int32), val fp64 — nnz doubles for
+ * cfg.basis = SDMD_BASIS_DCT, nnz interleaved complex (2·nnz doubles) for the Fourier bases.
+ * nnz <= nnz_cap.  The Gram column uses sparse–sparse inner products (weighted real parts for the
+ * Fourier bases, see enum sdmd_basis); nothing is densified in HBM.
  * Errors: nnz > nnz_cap, or (where = SDMD_HOST) indices not strictly ascending / out of range ->
  * SDMD_E_INVALID, nothing queued.  Device-resident indices are checked on the device: a violation
  * rejects the frame like a non-finite one (nothing scattered; the next sdmd_sync returns
@@ -262,13 +296,34 @@ int sdmd_get_modes(sdmd_ctx* ctx, const int32_t* cols, int32_t ncols, double* ph
 
 /* Newest background column produced (frame index in *frame, -1 if none yet): lowrank = |l|,
  * sparse = x − |l| (cfg.dtype, n_local values each; either may be NULL) and mask (uint8, 1 where
- * sparse > threshold; may be NULL).  where = SDMD_HOST (synchronises) or SDMD_DEVICE (copies on
+ * sparse > threshold; may be NULL).  A sparse DCT context returns them in pixel space: n_local =
+ * grid_rows·grid_cols fp64 values, row-major (l = IDCT2(X̂'c), x = IDCT2(x̂), NEXT-3).  where = SDMD_HOST (synchronises) or SDMD_DEVICE (copies on
  * the ctx stream) or SDMD_HOST_ASYNC (pinned host buffers; no host wait: the outputs of the
  * newest enqueued background pass — its frame in *frame — are read back on the context's D2H
  * stream, overlapping the next Gram pass (the outputs are double-buffered by frame parity); the
  * host buffers are valid after sdmd_sync, or on the ctx stream after sdmd_join). */
 int sdmd_get_background(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
                         int where);
+
+/* Alg 3's first-window branch (reading Q24) on the window of the newest DMD frame f:
+ * for every window column e = 0..m (frames f-m..f), l_e = b_idx φ_idx λ_idx^e, lowrank = |l_e|,
+ * sparse = z_e − |l_e|, mask = sparse > threshold.  Outputs are DEVICE buffers (any may be NULL),
+ * n_local x (m+1) column-major with leading dimension ld >= n_local (cfg.dtype; mask uint8);
+ * *frame = f.  Dense single-mode contexts with dmd = 1 and a full window.  Synchronises.
+ * Returns the frame's status (OK or W_SINGULAR), E_STATE / E_NO_VIABLE_MODE when there is no
+ * full-window DMD with a background mode. */
+int sdmd_get_background_window(sdmd_ctx* ctx, void* lowrank, void* sparse, uint8_t* mask,
+                               int64_t ld, int64_t* frame);
+
+/* Score the newest background mask produced (frame `frame`, which must be the frame
+ * sdmd_get_background reports, else SDMD_E_INVALID) against the ground-truth foreground mask gt
+ * (n_local bytes, nonzero = foreground; SDMD_HOST: copied before the call returns, SDMD_DEVICE:
+ * stream-ordered).  Counts accumulate on the device (kernel on the ctx stream, no host wait).
+ * Errors: E_INVALID (background off, bad where, frame mismatch), E_STATE (no mask yet). */
+int sdmd_score_background(sdmd_ctx* ctx, int64_t frame, const uint8_t* gt, int where);
+
+/* Read (synchronises) and optionally reset the accumulated scores. */
+int sdmd_get_scores(sdmd_ctx* ctx, sdmd_scores* out, int reset);
 
 /* Diagnostics of the newest DMD frame: out[0]=frame, [1]=status, [2]=r, [3]=idx, [4]=Jacobi
  * sweeps, [5]=QR iterations, [6..12]=SM cycles spent in the K4 phases (build S, Jacobi, sort/V,

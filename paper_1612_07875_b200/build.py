@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsdmd.so")
-SOURCES = ["sdmd_api.cu", "k1_gram.cu", "k1b_batch.cu", "k2_dmma.cu", "k3_sparse.cu", "k4_eigen.cu"]
+SOURCES = ["sdmd_api.cu", "k1_gram.cu", "k1b_batch.cu", "k2_dmma.cu", "k3_sparse.cu", "k4_eigen.cu", "k6_background.cu"]
 HEADERS = ["sdmd_internal.cuh", os.path.join("..", "..", "include", "sdmd.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1,4 +1,5 @@
-// k3_sparse.cu — K3: Gram column over natively compressed (sparse orthonormal-DCT) snapshots.
+// k3_sparse.cu — K3: Gram column over natively compressed snapshots (sparse orthonormal-DCT
+// coefficients, or complex Fourier coefficients of a real field: full or half spectrum, NEXT-3).
 //
 // §3.5: SVD and DMD are invariant under unitary transforms, so the window may be kept
 // in a sparse transform basis and "many of the core steps … performed on sparse data matrices"
@@ -14,17 +15,44 @@ namespace sdmd {
 constexpr int K3_THREADS = 256;
 constexpr int K3_CHUNK = 2048;     // nonzeros per block
 
+// Value access of the two storage kinds: DCT (real, one double per nonzero) and the Fourier bases
+// (interleaved complex, one double2; reading Q27: the Gram entry is Σ w Re(conj(ẑ) x̂), which is the
+// pixel-space inner product of the real fields by Parseval — P:359 "unitary transforms").
+struct RealVal {
+  using T = double;
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  static __device__ __forceinline__ double dot(T a, T b) { return a * b; }
+};
+struct CplxVal {
+  using T = double2;
+  static __device__ __forceinline__ T zero() { return make_double2(0.0, 0.0); }
+  static __device__ __forceinline__ double dot(T a, T b) { return fma(a.x, b.x, a.y * b.y); }
+};
+
+// RFFT half spectrum: weight 2 on every stored bin whose conjugate partner is omitted (columns
+// kx = 1 .. cols/2 - 1, plus kx = cols/2 for odd cols); 1 on the self-conjugate columns
+static __device__ __forceinline__ double half_weight(long long gi, long long h, int even) {
+  if (h == 0) return 1.0;
+  const long long kx = gi % h;
+  return (kx == 0 || (even && kx == h - 1)) ? 1.0 : 2.0;
+}
+
+template <class V>
 __global__ void k3_scatter_kernel(const K3Params p) {
+  using T = typename V::T;
   if (*(volatile int*)&p.st->status != 0) return;
   const int slot = (int)(p.f_new % p.NS);
   const int nnz = p.nnz[slot];
   const int* idx = p.idx + (long long)slot * p.nnz_cap;
-  const double* val = p.val + (long long)slot * p.nnz_cap;
+  const T* val = reinterpret_cast<const T*>(p.val) + (long long)slot * p.nnz_cap;
+  T* scratch = reinterpret_cast<T*>(p.scratch);
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += gridDim.x * blockDim.x)
-    p.scratch[idx[e] - p.row_begin] = val[e];
+    scratch[idx[e] - p.row_begin] = val[e];
 }
 
+template <class V>
 __global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
+  using T = typename V::T;
   __shared__ double red[K3_THREADS / 32];
   __shared__ int am_last;
   if (*(volatile int*)&p.st->status != 0) return;
@@ -34,11 +62,15 @@ __global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
   const int slot = (int)(f % p.NS);
   const int nnz = p.nnz[slot];
   const int* idx = p.idx + (long long)slot * p.nnz_cap;
-  const double* val = p.val + (long long)slot * p.nnz_cap;
+  const T* val = reinterpret_cast<const T*>(p.val) + (long long)slot * p.nnz_cap;
+  T* scratch = reinterpret_cast<T*>(p.scratch);
   double s = 0.0;
   const int e0 = c * K3_CHUNK, e1 = min(nnz, e0 + K3_CHUNK);
-  for (int e = e0 + threadIdx.x; e < e1; e += K3_THREADS)
-    s = fma(val[e], __ldcg(&p.scratch[idx[e] - p.row_begin]), s);
+  for (int e = e0 + threadIdx.x; e < e1; e += K3_THREADS) {
+    const int gi = idx[e];
+    const double d = V::dot(val[e], __ldcg(&scratch[gi - p.row_begin]));
+    s = fma(half_weight(gi, p.half_h, p.half_even), d, s);   // w in {1, 2}: exact scaling
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -64,7 +96,7 @@ __global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
   const int nn = p.nnz[sl];
   const int* ix = p.idx + (long long)sl * p.nnz_cap;
   __syncthreads();
-  for (int e = threadIdx.x; e < nn; e += K3_THREADS) p.scratch[ix[e] - p.row_begin] = 0.0;
+  for (int e = threadIdx.x; e < nn; e += K3_THREADS) scratch[ix[e] - p.row_begin] = V::zero();
   // a device-pushed frame whose indices failed the check (nnz recorded as -1, nothing scattered):
   // a NaN self inner product, so that the commit rejects the frame — after the allreduce when
   // rows are sharded, i.e. on every rank alike
@@ -77,11 +109,18 @@ __global__ void __launch_bounds__(K3_THREADS) k3_dot_kernel(const K3Params p) {
 }
 
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s) {
-  k3_scatter_kernel<<<64, 256, 0, s>>>(p);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
   dim3 grid(p.chunks, p.nd);
-  k3_dot_kernel<<<grid, K3_THREADS, 0, s>>>(p);
+  if (p.cplx) {
+    k3_scatter_kernel<CplxVal><<<64, 256, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k3_dot_kernel<CplxVal><<<grid, K3_THREADS, 0, s>>>(p);
+  } else {
+    k3_scatter_kernel<RealVal><<<64, 256, 0, s>>>(p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k3_dot_kernel<RealVal><<<grid, K3_THREADS, 0, s>>>(p);
+  }
   return cudaGetLastError();
 }
 
@@ -119,13 +158,24 @@ cudaError_t launch_set_int(int* p, int v, cudaStream_t s) {
 // the modes of the transformed data are the transformed modes, by unitary invariance).  Block q
 // owns mode column q; it zeroes Φ̂[:, q] and then walks the m window columns IN ORDER, its threads
 // scattering val_e · T[k][q] into the column's nonzero rows (indices are unique within a column,
-// and a block barrier separates columns): every element is accumulated in fixed k order.
+// and a block barrier separates columns): every element is accumulated in fixed k order.  For the
+// Fourier bases val_e is complex (complex x complex product).
+static __device__ __forceinline__ void cacc(double2& c, double v, double2 t) {
+  c.x = fma(v, t.x, c.x);
+  c.y = fma(v, t.y, c.y);
+}
+static __device__ __forceinline__ void cacc(double2& c, double2 v, double2 t) {
+  c.x = fma(v.x, t.x, fma(-v.y, t.y, c.x));
+  c.y = fma(v.x, t.y, fma(v.y, t.x, c.y));
+}
+
+template <class T>
 __global__ void __launch_bounds__(256) modes_sparse_kernel(const int* __restrict__ idx,
-                                                          const double* __restrict__ val,
+                                                          const T* __restrict__ val,
                                                           const int* __restrict__ nnz, int nnz_cap,
                                                           int NS, long long row_begin, long long n,
                                                           long long first_frame, int m,
-                                                          const double2* __restrict__ T, int nc,
+                                                          const double2* __restrict__ Tm, int nc,
                                                           double2* __restrict__ phi, long long ldphi) {
   const int q = blockIdx.x;
   if (q >= nc) return;
@@ -136,14 +186,12 @@ __global__ void __launch_bounds__(256) modes_sparse_kernel(const int* __restrict
     const int slot = (int)((first_frame + k) % NS);
     const int nz = nnz[slot];
     const int* ik = idx + (long long)slot * nnz_cap;
-    const double* vk = val + (long long)slot * nnz_cap;
-    const double2 t = T[(long long)q * m + k];
+    const T* vk = val + (long long)slot * nnz_cap;
+    const double2 t = Tm[(long long)q * m + k];
     for (int e = threadIdx.x; e < nz; e += blockDim.x) {
       const long long row = ik[e] - row_begin;
-      const double v = vk[e];
       double2 c = col[row];
-      c.x = fma(v, t.x, c.x);
-      c.y = fma(v, t.y, c.y);
+      cacc(c, vk[e], t);
       col[row] = c;
     }
     __syncthreads();
@@ -152,9 +200,16 @@ __global__ void __launch_bounds__(256) modes_sparse_kernel(const int* __restrict
 
 cudaError_t launch_modes_sparse(const int* idx, const double* val, const int* nnz, int nnz_cap, int NS,
                                 long long row_begin, long long n, long long first_frame, int m,
-                                const double* T, int nc, double* phi, long long ldphi, cudaStream_t s) {
-  modes_sparse_kernel<<<nc, 256, 0, s>>>(idx, val, nnz, nnz_cap, NS, row_begin, n, first_frame, m,
-                                         (const double2*)T, nc, (double2*)phi, ldphi);
+                                const double* T, int nc, double* phi, long long ldphi, int cplx,
+                                cudaStream_t s) {
+  if (cplx)
+    modes_sparse_kernel<double2><<<nc, 256, 0, s>>>(idx, (const double2*)val, nnz, nnz_cap, NS, row_begin,
+                                                    n, first_frame, m, (const double2*)T, nc,
+                                                    (double2*)phi, ldphi);
+  else
+    modes_sparse_kernel<double><<<nc, 256, 0, s>>>(idx, val, nnz, nnz_cap, NS, row_begin, n,
+                                                   first_frame, m, (const double2*)T, nc,
+                                                   (double2*)phi, ldphi);
   return cudaGetLastError();
 }
 

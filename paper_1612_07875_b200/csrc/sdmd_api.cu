@@ -150,6 +150,13 @@ struct sdmd_ctx {
   cudaEvent_t ev_bgw[2]{}, ev_d2h[2]{};
   bool d2h_pending[2] = {false, false};
   long long bg_last = -1;               // frame of the newest background pass enqueued
+  // sparse DCT contexts with background: pixel-space background work planes (NEXT-3)
+  double* pix_planes = nullptr;         // 3 x n: Re l̂, Im l̂, x̂ (then their inverse transforms)
+  double* pix_tmp = nullptr;            // 3 x n
+  bool cplx = false;                    // Fourier bases: complex sparse values
+  // NEXT-4 scoring: device counters {tp, fp, fn, frames} and the host-gt staging buffer
+  unsigned long long* score_cnt = nullptr;
+  unsigned char* gt_stage = nullptr;
   // per-frame modes (cfg.modes_every_frame, NEXT-2): per single-CTA worker stream, the LU
   // workspaces of all r inverse iterations, W, b, T = YW and Φ (ld x r_max complex)
   double2* pm_M[kMaxWorkers]{};
@@ -424,7 +431,24 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       cfg.rank < 0 || cfg.rank >= cfg.nranks || cfg.r_max < 0 || cfg.workers < 0 ||
       cfg.workers > kMaxWorkers || !(cfg.rank_tol >= 0.0) || cfg.lag < 0 || cfg.lag > kMaxLag)
     return SDMD_E_INVALID;
-  if (cfg.storage == SDMD_SPARSE && (cfg.nnz_cap < 1 || cfg.background)) return SDMD_E_INVALID;
+  if (cfg.storage == SDMD_SPARSE && cfg.nnz_cap < 1) return SDMD_E_INVALID;
+  if (cfg.basis < SDMD_BASIS_DCT || cfg.basis > SDMD_BASIS_RFFT || cfg.grid_rows < 0 || cfg.grid_cols < 0 ||
+      (cfg.basis != SDMD_BASIS_DCT && cfg.storage != SDMD_SPARSE))
+    return SDMD_E_INVALID;
+  {
+    const long long gr = cfg.grid_rows, gc = cfg.grid_cols;
+    const bool grid = gr > 0 && gc > 0;
+    if ((gr > 0) != (gc > 0)) return SDMD_E_INVALID;
+    if (cfg.basis == SDMD_BASIS_RFFT && (!grid || gr * (gc / 2 + 1) != cfg.n_global)) return SDMD_E_INVALID;
+    if (grid && cfg.basis != SDMD_BASIS_RFFT && gr * gc != cfg.n_global) return SDMD_E_INVALID;
+    if (cfg.storage == SDMD_SPARSE && cfg.background) {
+      // pixel-space background (NEXT-3): DCT basis, one rank, power-of-two grid sides in [2, 4096]
+      auto pow2 = [](long long v) { return v >= 2 && v <= 4096 && (v & (v - 1)) == 0; };
+      if (cfg.basis != SDMD_BASIS_DCT || cfg.nranks != 1 || !grid || !pow2(gr) || !pow2(gc) ||
+          cfg.n_local != cfg.n_global)
+        return SDMD_E_INVALID;
+    }
+  }
   if (cfg.batch_max < 0 || cfg.batch_max > kMaxBatch || (cfg.batch_max > 0 && cfg.storage != SDMD_DENSE))
     return SDMD_E_INVALID;
   if (cfg.bg_modes < 0 || cfg.bg_modes > kMaxBgModes) return SDMD_E_INVALID;
@@ -489,7 +513,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   c->guard_d = c->NS - (c->cfg.background ? m + c->L - 1 : m);
   c->NH = 2 * (m + c->L + 4);
   c->NC = c->L + 2;
-  c->es = c->cfg.dtype == SDMD_F32 ? 4 : 8;
+  c->es = (c->cfg.dtype == SDMD_F32 && c->cfg.storage == SDMD_DENSE) ? 4 : 8;   // sparse: fp64 values
+  c->cplx = c->cfg.storage == SDMD_SPARSE && c->cfg.basis != SDMD_BASIS_DCT;
   c->ld = (c->cfg.n_local + kSuperTile - 1) / kSuperTile * kSuperTile;
   c->dev = c->cfg.device;
   auto bail = [&](int st) { sdmd_destroy(c); return st; };
@@ -556,10 +581,15 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     if (cudaMemsetAsync(c->ring, 0, bytes, c->stream) != cudaSuccess) return bail(SDMD_E_CUDA);
   } else {
     AL(c->sp_idx, (size_t)c->NS * c->cfg.nnz_cap);
-    AL(c->sp_val, (size_t)c->NS * c->cfg.nnz_cap);
+    const size_t vs = c->cplx ? 2 : 1;            // doubles per value (complex: interleaved)
+    AL(c->sp_val, (size_t)c->NS * c->cfg.nnz_cap * vs);
     AL(c->sp_nnz, (size_t)c->NS);
-    AL(c->scratch, (size_t)c->cfg.n_local);
-    cudaMemsetAsync(c->scratch, 0, c->cfg.n_local * sizeof(double), c->stream);
+    AL(c->scratch, (size_t)c->cfg.n_local * vs);
+    cudaMemsetAsync(c->scratch, 0, c->cfg.n_local * vs * sizeof(double), c->stream);
+    if (c->cfg.background) {
+      AL(c->pix_planes, 3 * (size_t)c->cfg.n_local);
+      AL(c->pix_tmp, 3 * (size_t)c->cfg.n_local);
+    }
     cudaMemsetAsync(c->sp_nnz, 0, c->NS * sizeof(int), c->stream);
     c->k3_chunks = (c->cfg.nnz_cap + 2047) / 2048;
   }
@@ -591,6 +621,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
       if (cudaMalloc(&c->bg_sparse[b], c->ld * c->es) != cudaSuccess) return bail(SDMD_E_OOM);
       AL(c->bg_mask[b], (size_t)c->ld);
     }
+    AL(c->score_cnt, 4);
+    cudaMemsetAsync(c->score_cnt, 0, 4 * sizeof(unsigned long long), c->stream);
   }
   const int R = kMaxR;
   int prio_lo = 0, prio_hi = 0;                     // eigen workers: highest stream priority
@@ -747,7 +779,8 @@ int sdmd_destroy(sdmd_ctx* c) {
   }
   void* ptrs[] = {c->ring, c->dst, c->ghist, c->cbuf, c->partials, c->gout, c->gpart, c->sp_idx,
                   c->sp_val, c->sp_nnz, c->scratch, c->Wall, c->ball, c->Mws, c->Tbuf, c->colbuf,
-                  c->Gtmp, c->init_work, c->sg_cnt, c->od_A, c->r_warm};
+                  c->Gtmp, c->init_work, c->sg_cnt, c->od_A, c->r_warm, c->pix_planes, c->pix_tmp,
+                  c->score_cnt, c->gt_stage};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int w = 0; w < kMaxWS; ++w) {
@@ -892,7 +925,9 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
   const int nd = (int)(t + 1 < m + 1 ? t + 1 : m + 1);
   const bool do_dmd = c->cfg.dmd && t >= first_dmd(c);
   const bool sparse = c->cfg.storage == SDMD_SPARSE;
-  const bool bg = (c->cfg.background && c->cfg.dmd && !sparse && (t - c->L) >= m &&
+  // the background of frame t - L: fused into the Gram pass K1(t) (dense), or the pixel-space
+  // pipeline of k6_background.cu before the sparse Gram pass (sparse DCT)
+  const bool bg = (c->cfg.background && c->cfg.dmd && (t - c->L) >= m &&
                    (t - c->L) <= c->last_dmd_all) ||
                   (c->bg_nodmd && c->cfg.background && !sparse && (t - c->L) >= m);
   std::pair<cudaEvent_t, cudaEvent_t> tp{}, tw{};
@@ -984,8 +1019,32 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
       if (fold) c->c_folded = fb1;
     }
   } else {
+    if (bg) {                                    // pixel-space background of frame t - L (NEXT-3)
+      const long long fb = t - c->L;
+      const int bslot = (int)(fb & 1);
+      if (c->d2h_pending[bslot]) {
+        CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[bslot], 0));
+        c->d2h_pending[bslot] = false;
+      }
+      PixBgParams q{};
+      q.idx = c->sp_idx; q.val = c->sp_val; q.nnz = c->sp_nnz; q.nnz_cap = c->cfg.nnz_cap;
+      q.NS = c->NS; q.m = m; q.f_bg = fb; q.c = c->cbuf + (fb % c->NC) * m;
+      q.rows = c->cfg.grid_rows; q.cols = c->cfg.grid_cols;
+      q.planes = c->pix_planes; q.tmp = c->pix_tmp;
+      q.lowrank = (double*)c->bg_low[bslot]; q.sparse = (double*)c->bg_sparse[bslot];
+      q.mask = c->bg_mask[bslot]; q.thr = c->cfg.threshold; q.st = c->dst;
+      CK(launch_pixel_background(q, c->stream));
+      c->launches += 4;
+      CK(cudaEventRecord(c->ev_bgw[bslot], c->stream));
+      c->bg_last = fb;
+    }
     K3Params p{};
     p.idx = c->sp_idx; p.val = c->sp_val; p.nnz = c->sp_nnz; p.nnz_cap = c->cfg.nnz_cap;
+    p.cplx = c->cplx ? 1 : 0;
+    if (c->cfg.basis == SDMD_BASIS_RFFT) {
+      p.half_h = c->cfg.grid_cols / 2 + 1;
+      p.half_even = (c->cfg.grid_cols % 2) == 0;
+    }
     p.NS = c->NS; p.m = m; p.f_new = t; p.nd = nd; p.scratch = c->scratch;
     p.row_begin = c->cfg.row_begin; p.partials = c->partials; p.chunks = c->k3_chunks;
     p.gout = c->gout; p.do_commit = do_commit; p.ghist = c->ghist; p.NH = c->NH; p.st = c->dst;
@@ -1135,8 +1194,9 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
   const long long t = c->frames;
   if (int g = ring_guard(c, t)) return g;
   const int slot = (int)(t % c->NS);
+  const size_t vs = c->cplx ? 2 : 1;              // doubles per value
   int* sidx = c->sp_idx + (size_t)slot * c->cfg.nnz_cap;
-  double* sval = c->sp_val + (size_t)slot * c->cfg.nnz_cap;
+  double* sval = c->sp_val + (size_t)slot * c->cfg.nnz_cap * vs;
   if (where == SDMD_HOST) {
     // compressed ingest: only the nnz (index, value) pairs
     // cross PCIe (12 B per nonzero), on the copy stream so that they overlap the previous sparse
@@ -1144,7 +1204,7 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
     if (t >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_k1[(t - 2) % kEvents], 0));
     if (nnz > 0) {
       CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), cudaMemcpyHostToDevice, c->copy_stream));
-      CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), cudaMemcpyHostToDevice, c->copy_stream));
+      CK(cudaMemcpyAsync(sval, val, nnz * vs * sizeof(double), cudaMemcpyHostToDevice, c->copy_stream));
     }
     CK(launch_set_int(c->sp_nnz + slot, nnz, c->copy_stream));
     CK(cudaEventRecord(c->ev_copy[t % kEvents], c->copy_stream));
@@ -1152,7 +1212,7 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
   } else {
     if (nnz > 0) {
       CK(cudaMemcpyAsync(sidx, idx, nnz * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
-      CK(cudaMemcpyAsync(sval, val, nnz * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(sval, val, nnz * vs * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     }
     CK(launch_sparse_nnz_checked(sidx, nnz, lo, hi, c->sp_nnz + slot, c->stream));
   }
@@ -1454,7 +1514,7 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
   } else {                                      // coefficient-space modes (NEXT-3), K3 scatter
     CK(launch_modes_sparse(c->sp_idx, c->sp_val, c->sp_nnz, c->cfg.nnz_cap, c->NS, c->cfg.row_begin,
                            c->cfg.n_local, c->last_dmd - w + 1, w, c->Tbuf, ncols, phi_dev, ld,
-                           c->stream));
+                           c->cplx ? 1 : 0, c->stream));
   }
   c->launches += 1 + (ncols + 31) / 32;
   CK(cudaStreamSynchronize(c->stream));
@@ -1497,6 +1557,75 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
   if (sparse) CK(cudaMemcpyAsync(sparse, c->bg_sparse[b], n * c->es, kind, c->stream));
   if (mask) CK(cudaMemcpyAsync(mask, c->bg_mask[b], n, kind, c->stream));
   if (where == SDMD_HOST) CK(cudaStreamSynchronize(c->stream));
+  return SDMD_OK;
+}
+
+int sdmd_get_background_window(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask, int64_t ld,
+                               int64_t* frame) {
+  if (!c || ld < c->cfg.n_local) return invalid(c, "get_background_window: bad argument");
+  if (c->cfg.storage != SDMD_DENSE || !c->cfg.dmd || c->cfg.bg_modes > 1)
+    return invalid(c, "get_background_window: dense single-mode DMD contexts only");
+  CK(cudaSetDevice(c->dev));
+  K4Result res{};
+  int st = newest_result(c, &res);              // synchronises
+  if (st) return st;
+  if (frame) *frame = res.frame;
+  if (res.status && res.status != SDMD_W_SINGULAR) return res.status;
+  const long long f = c->last_dmd;
+  if (win_of(c, f) < c->cfg.m) { c->err = "get_background_window: newest DMD window not full"; return SDMD_E_STATE; }
+  if (res.idx < 0) { c->err = "get_background_window: no background mode"; return SDMD_E_NO_VIABLE_MODE; }
+  Workspace& k = ws_of(c, f);
+  CK(launch_window_background(c->ring, c->ld, c->NS, c->cfg.dtype, c->cfg.n_local, f, c->cfg.m,
+                              c->cbuf + (f % c->NC) * c->cfg.m, k.res, lowrank, sparse, mask, ld,
+                              c->cfg.threshold, c->stream));
+  c->launches += 1;
+  CK(cudaStreamSynchronize(c->stream));
+  return res.status;
+}
+
+int sdmd_score_background(sdmd_ctx* c, int64_t frame, const uint8_t* gt, int where) {
+  if (!c || !gt || (where != SDMD_HOST && where != SDMD_DEVICE)) return invalid(c, "score_background: bad argument");
+  if (!c->cfg.background) return invalid(c, "score_background: background disabled in config");
+  CK(cudaSetDevice(c->dev));
+  if (c->bg_last < 0) { c->err = "score_background: no background mask produced yet"; return SDMD_E_STATE; }
+  if (frame != c->bg_last) return invalid(c, "score_background: frame is not the newest background frame");
+  const size_t n = c->cfg.n_local;
+  const uint8_t* g = gt;
+  if (where == SDMD_HOST) {                     // stage: the host buffer is free when we return
+    if (!c->gt_stage && dalloc(&c->gt_stage, n) != cudaSuccess) return SDMD_E_OOM;
+    CK(cudaMemcpyAsync(c->gt_stage, gt, n, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    g = c->gt_stage;
+  }
+  const int b = (int)(c->bg_last & 1);
+  CK(cudaStreamWaitEvent(c->stream, c->ev_bgw[b], 0));
+  CK(launch_score(c->bg_mask[b], g, (long long)n, c->score_cnt, c->stream));
+  c->launches += 1;
+  return SDMD_OK;
+}
+
+int sdmd_get_scores(sdmd_ctx* c, sdmd_scores* o, int reset) {
+  if (!c || !o) return SDMD_E_INVALID;
+  if (!c->cfg.background) return invalid(c, "get_scores: background disabled in config");
+  CK(cudaSetDevice(c->dev));
+  unsigned long long h[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(h, c->score_cnt, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (reset) {
+    CK(cudaMemsetAsync(c->score_cnt, 0, sizeof(h), c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  // Table 2 P:437-443 / SPEC S:368; reading Q26 (pooled counts, binary-mask PSNR at the peak)
+  const long long tp = (long long)h[0], fp = (long long)h[1], fn = (long long)h[2], fr = (long long)h[3];
+  const long long npx = fr * (long long)c->cfg.n_local;
+  o->frames = fr; o->tp = tp; o->fp = fp; o->fn = fn; o->tn = npx - tp - fp - fn;
+  o->empty_gt = (tp + fn) == 0;
+  o->empty_mask = (tp + fp) == 0;
+  o->recall = o->empty_gt ? 0.0 : (double)tp / (double)(tp + fn);
+  o->precision = o->empty_mask ? 0.0 : (double)tp / (double)(tp + fp);
+  o->f_measure = (o->recall + o->precision) == 0.0 ? 0.0
+                 : 2.0 * o->precision * o->recall / (o->precision + o->recall);
+  o->psnr = (fp + fn) == 0 ? HUGE_VAL : 10.0 * std::log10((double)npx / (double)(fp + fn));
   return SDMD_OK;
 }
 

@@ -204,8 +204,12 @@ struct K3Params {             // sparse Gram column
   int m;
   long long f_new;
   int nd;
-  double* scratch;            // dense n_local fp64 scatter target (kept zero between pushes)
+  double* scratch;            // dense n_local fp64 (double2 for the Fourier bases) scatter target,
+                              // kept zero between pushes
   long long row_begin;
+  int cplx;                   // 1: Fourier bases, val holds interleaved complex (double2) values
+  long long half_h;           // RFFT: grid_cols/2 + 1 (weights 2 off the self-conjugate columns), else 0
+  int half_even;              // RFFT: grid_cols even (column half_h - 1 is self-conjugate too)
   double* partials;           // [nd][chunks]
   int chunks;
   double* gout;
@@ -267,7 +271,35 @@ cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long
 cudaError_t launch_modes_sparse(const int* idx, const double* val, const int* nnz, int nnz_cap, int NS,
                                 long long row_begin, long long n, long long first_frame, int m,
                                 const double* T /*m x nc complex*/, int nc, double* phi, long long ldphi,
-                                cudaStream_t s);
+                                int cplx, cudaStream_t s);
+// NEXT-3 pixel-space background of a sparse DCT context (k6_background.cu)
+struct PixBgParams {
+  const int* idx;             // sparse ring (NS x nnz_cap), DCT values
+  const double* val;
+  const int* nnz;
+  int nnz_cap;
+  int NS;
+  int m;
+  long long f_bg;             // background frame: X' = frames f_bg-m+1 .. f_bg, x = frame f_bg
+  const double2* c;           // m coefficients (column k <-> frame f_bg-m+1+k)
+  int rows, cols;             // coefficient / pixel grid (powers of two)
+  double* planes;             // 3 x rows x cols: Re l̂, Im l̂, x̂ (then the transforms, in place)
+  double* tmp;                // 3 x rows x cols
+  double* lowrank;            // rows x cols fp64 outputs
+  double* sparse;
+  unsigned char* mask;
+  float thr;
+  DevState* st;
+};
+cudaError_t launch_pixel_background(const PixBgParams& p, cudaStream_t s);
+// Alg 3 first-window branch over the newest DMD window (reading Q24)
+cudaError_t launch_window_background(const void* ring, long long ld, int NS, int dtype, long long n,
+                                     long long f, int m, const double2* cf, const K4Result* res,
+                                     void* low, void* sparse, unsigned char* mask, long long ldo,
+                                     float thr, cudaStream_t s);
+// NEXT-4 scoring: TP/FP/FN counts of mask vs gt accumulated into cnt[0..2], cnt[3] += 1 (frames)
+cudaError_t launch_score(const unsigned char* mask, const unsigned char* gt, long long n,
+                         unsigned long long* cnt, cudaStream_t s);
 cudaError_t launch_ghist_from_gram(const double* G, int k, double* ghist, int NH, int m,
                                    long long first_frame, cudaStream_t s);
 cudaError_t launch_gather_gram(const double* ghist, int NH, int m, long long f_last, int k,

@@ -20,6 +20,7 @@ E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE, E_CUDA, E_NCCL, E_OOM, E_STATE =
     5, 6, 7, 8, 9, 10, 11)
 F32, F64 = 0, 1
 DENSE, SPARSE = 0, 1
+BASIS_DCT, BASIS_FFT, BASIS_RFFT = 0, 1, 2
 HOST, DEVICE, HOST_ASYNC = 0, 1, 2
 MAX_M, MAX_R = 256, 224
 
@@ -31,6 +32,7 @@ EXPORTS = [
     "sdmd_get_info",
     "sdmd_get_gram", "sdmd_get_partial_gram_column", "sdmd_get_svd", "sdmd_get_spectrum",
     "sdmd_get_eigvecs", "sdmd_get_modes", "sdmd_get_background", "sdmd_get_frame_diag",
+    "sdmd_score_background", "sdmd_get_scores", "sdmd_get_background_window",
     "sdmd_set_timing",
     "sdmd_get_stats", "sdmd_get_timeline", "sdmd_nccl_unique_id", "sdmd_status_string", "sdmd_last_error",
     "sdmd_abi_version",
@@ -47,7 +49,8 @@ class Config(ctypes.Structure):
         ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("nccl_uid", ctypes.c_void_p),
         ("lag", ctypes.c_int32), ("eigen_shard", ctypes.c_int32),
         ("batch_max", ctypes.c_int32), ("bg_modes", ctypes.c_int32), ("buildup", ctypes.c_int32),
-        ("modes_every_frame", ctypes.c_int32),
+        ("modes_every_frame", ctypes.c_int32), ("basis", ctypes.c_int32),
+        ("grid_rows", ctypes.c_int32), ("grid_cols", ctypes.c_int32),
     ]
 
 
@@ -63,6 +66,14 @@ class Stats(ctypes.Structure):
                 ("k4_launches", ctypes.c_int64), ("k4_ms", ctypes.c_double),
                 ("gpu_launches", ctypes.c_int64), ("k1_gap_ms", ctypes.c_double),
                 ("k1_wait_ms", ctypes.c_double), ("collectives", ctypes.c_int64)]
+
+
+class Scores(ctypes.Structure):
+    _fields_ = [("frames", ctypes.c_int64), ("tp", ctypes.c_int64), ("fp", ctypes.c_int64),
+                ("fn", ctypes.c_int64), ("tn", ctypes.c_int64), ("recall", ctypes.c_double),
+                ("precision", ctypes.c_double), ("f_measure", ctypes.c_double),
+                ("psnr", ctypes.c_double), ("empty_gt", ctypes.c_int32),
+                ("empty_mask", ctypes.c_int32)]
 
 
 class SDMDError(RuntimeError):
@@ -106,6 +117,9 @@ def lib():
         "sdmd_get_modes": [vp, vp, i32, vp, i64],
         "sdmd_get_background": [vp, vp, vp, vp, ctypes.POINTER(i64), ctypes.c_int],
         "sdmd_get_frame_diag": [vp, dp],
+        "sdmd_score_background": [vp, i64, vp, ctypes.c_int],
+        "sdmd_get_scores": [vp, ctypes.POINTER(Scores), ctypes.c_int],
+        "sdmd_get_background_window": [vp, vp, vp, vp, i64, ctypes.POINTER(i64)],
         "sdmd_set_timing": [vp, ctypes.c_int],
         "sdmd_get_stats": [vp, ctypes.POINTER(Stats), ctypes.c_int],
         "sdmd_get_timeline": [vp, ctypes.POINTER(ctypes.c_double), ctypes.c_int,
@@ -195,7 +209,7 @@ class StreamingDMD:
                  nranks: int = 1, row_begin: int = 0, n_global: int | None = None,
                  nccl_uid: bytes | None = None, lag: int = 0, eigen_shard: int = 1,
                  batch_max: int = 0, bg_modes: int = 0, buildup: bool = False,
-                 modes_every_frame: bool = False):
+                 modes_every_frame: bool = False, basis: str = "dct", grid=None):
         L = lib()
         cfg = Config()
         L.sdmd_config_init(ctypes.byref(cfg))
@@ -230,6 +244,9 @@ class StreamingDMD:
         cfg.bg_modes = int(bg_modes)
         cfg.buildup = 1 if buildup else 0
         cfg.modes_every_frame = 1 if modes_every_frame else 0
+        cfg.basis = {"dct": BASIS_DCT, "fft": BASIS_FFT, "rfft": BASIS_RFFT}[basis]
+        if grid is not None:
+            cfg.grid_rows, cfg.grid_cols = int(grid[0]), int(grid[1])
         self._uid = None
         if nccl_uid is not None:
             self._uid = (ctypes.c_uint8 * 128).from_buffer_copy(nccl_uid)
@@ -237,6 +254,8 @@ class StreamingDMD:
         self.cfg = cfg
         self.n, self.m = int(n), int(m)
         self.np_dtype = np.float32 if cfg.dtype == F32 else np.float64
+        # background outputs: the dense storage dtype; fp64 pixels for a sparse (DCT) context
+        self.out_dtype = np.float64 if cfg.storage == SPARSE else self.np_dtype
         # inputs of recent pushes stay referenced until the library no longer reads them (pinned
         # host buffers are copied asynchronously; the ring guard bounds how far the host runs
         # ahead, so 64 pushes is ample); sync() drops them
@@ -298,9 +317,14 @@ class StreamingDMD:
         return self._check(lib().sdmd_push_dense(self.h, p, where), "push_dense")
 
     def push_sparse(self, idx, val):
+        """nnz (index, value) pairs; values fp64 (DCT basis) or complex128 (Fourier bases: numpy
+        complex128 arrays, or torch float64 tensors holding 2·nnz interleaved doubles)."""
         nnz = int(idx.shape[0]) if hasattr(idx, "shape") else len(idx)
         idx, pi, wi = _checked(idx, np.int32, nnz, "push_sparse idx")
-        val, pv, wv = _checked(val, np.float64, nnz, "push_sparse val")
+        vs = 2 if self.cfg.basis != BASIS_DCT else 1
+        if vs == 2 and not hasattr(val, "data_ptr"):
+            val = np.ascontiguousarray(np.asarray(val, dtype=np.complex128)).view(np.float64)
+        val, pv, wv = _checked(val, np.float64, vs * nnz, "push_sparse val")
         if wi != wv:
             raise ValueError("push_sparse: idx and val must both be host or both be device buffers")
         self._pending.append((idx, val))
@@ -411,8 +435,8 @@ class StreamingDMD:
 
     def background(self):
         """(lowrank, sparse, mask, frame) as numpy arrays (host copy)."""
-        low = np.zeros(self.n, dtype=self.np_dtype)
-        sp = np.zeros(self.n, dtype=self.np_dtype)
+        low = np.zeros(self.n, dtype=self.out_dtype)
+        sp = np.zeros(self.n, dtype=self.out_dtype)
         mask = np.zeros(self.n, dtype=np.uint8)
         fr = ctypes.c_int64(-1)
         self._check(lib().sdmd_get_background(self.h, _dp(low), _dp(sp), _dp(mask),
@@ -425,6 +449,46 @@ class StreamingDMD:
         self._check(lib().sdmd_get_background(self.h, p(lowrank), p(sparse), p(mask),
                                                ctypes.byref(fr), DEVICE), "get_background")
         return fr.value
+
+    def background_window(self):
+        """Alg 3 first-window branch on the newest DMD window: (lowrank, sparse, mask, frame) as
+        torch CUDA tensors of shape (m+1, n) — row e is window column e (exponent e)."""
+        import torch
+        dt = torch.float32 if self.cfg.dtype == F32 else torch.float64
+        dev = f"cuda:{self.cfg.device}"
+        low = torch.empty((self.m + 1, self.n), dtype=dt, device=dev)
+        sp = torch.empty_like(low)
+        mask = torch.empty((self.m + 1, self.n), dtype=torch.uint8, device=dev)
+        fr = ctypes.c_int64(-1)
+        self._check(lib().sdmd_get_background_window(self.h, ctypes.c_void_p(low.data_ptr()),
+                                                     ctypes.c_void_p(sp.data_ptr()),
+                                                     ctypes.c_void_p(mask.data_ptr()), self.n,
+                                                     ctypes.byref(fr)),
+                    "get_background_window", ok=(OK, W_SINGULAR))
+        return low, sp, mask.bool(), int(fr.value)
+
+    def score(self, frame: int, gt):
+        """Accumulate TP/FP/FN of the newest background mask (frame ``frame``) against the ground
+        truth ``gt`` (n bytes, nonzero = foreground; numpy host array or torch CUDA uint8)."""
+        if hasattr(gt, "data_ptr"):
+            if gt.numel() < self.n or str(gt.dtype) not in ("torch.uint8", "torch.bool") \
+                    or not gt.is_contiguous():
+                raise ValueError("score: gt must be a contiguous tensor of n uint8/bool values")
+            g, p, where = gt, ctypes.c_void_p(gt.data_ptr()), (DEVICE if gt.is_cuda else HOST)
+        else:
+            g = np.ascontiguousarray(np.asarray(gt).astype(np.uint8).ravel())
+            if g.size < self.n:
+                raise ValueError("score: gt must hold n values")
+            p, where = ctypes.c_void_p(g.ctypes.data), HOST
+        self._pending.append(g)
+        return self._check(lib().sdmd_score_background(self.h, int(frame), p, where), "score_background")
+
+    def scores(self, reset: bool = False) -> dict:
+        o = Scores()
+        self._check(lib().sdmd_get_scores(self.h, ctypes.byref(o), 1 if reset else 0), "get_scores")
+        d = {k: getattr(o, k) for k, _ in Scores._fields_}
+        d["empty_gt"], d["empty_mask"] = bool(d["empty_gt"]), bool(d["empty_mask"])
+        return d
 
     def frame_diag(self) -> dict:
         o = np.zeros(24, dtype=np.int64)

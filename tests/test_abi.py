@@ -48,7 +48,7 @@ def test_sm100a_code_present(libpath):
 def test_status_strings_and_version(libpath):
     from paper_1612_07875_b200 import sdmd
     L = sdmd.lib()
-    assert L.sdmd_abi_version() == 3
+    assert L.sdmd_abi_version() == 4
     assert L.sdmd_status_string(2).decode() == "non-finite frame rejected"
     assert L.sdmd_status_string(999).decode() == "unknown status"
 
@@ -65,12 +65,13 @@ def test_config_layout_and_validation(libpath):
     with tempfile.TemporaryDirectory() as d:
         src = os.path.join(d, "sz.c")
         with open(src, "w") as fh:
-            fh.write('#include <stdio.h>\n#include "sdmd.h"\nint main(){printf("%zu %zu %zu", '
-                     'sizeof(sdmd_config), sizeof(sdmd_info), sizeof(sdmd_stats));return 0;}\n')
+            fh.write('#include <stdio.h>\n#include "sdmd.h"\nint main(){printf("%zu %zu %zu %zu", '
+                     'sizeof(sdmd_config), sizeof(sdmd_info), sizeof(sdmd_stats), sizeof(sdmd_scores));return 0;}\n')
         exe = os.path.join(d, "sz")
         subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe], check=True)
         c_sizes = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
-    assert c_sizes == [ctypes.sizeof(sdmd.Config), ctypes.sizeof(sdmd.Info), ctypes.sizeof(sdmd.Stats)]
+    assert c_sizes == [ctypes.sizeof(sdmd.Config), ctypes.sizeof(sdmd.Info), ctypes.sizeof(sdmd.Stats),
+                       ctypes.sizeof(sdmd.Scores)]
     assert cfg.eigen_shard == 1 and cfg.batch_max == 0
     h = ctypes.c_void_p()
     # invalid shapes are rejected before any CUDA call (works without a GPU)
@@ -137,3 +138,34 @@ def test_import_does_not_change_environment(monkeypatch):
     importlib.import_module("paper_1612_07875_b200")
     import os
     assert "CUDA_DEVICE_MAX_CONNECTIONS" not in os.environ
+
+
+def test_sparse_basis_and_grid_validation(libpath):
+    """NEXT-3 config rules are enforced before any device work: the RFFT basis needs its grid
+    (n_global = rows·(cols/2+1)); a sparse background needs the DCT basis, one rank and a
+    power-of-two grid covering n; Fourier bases need sparse storage."""
+    from paper_1612_07875_b200 import sdmd
+    L = sdmd.lib()
+    h = ctypes.c_void_p()
+
+    def cfg(**kw):
+        c = sdmd.Config()
+        L.sdmd_config_init(ctypes.byref(c))
+        c.m, c.storage, c.nnz_cap = 8, sdmd.SPARSE, 100
+        c.n_local = c.n_global = 64 * 64
+        for k, v in kw.items():
+            setattr(c, k, v)
+        return c
+    bad = [
+        cfg(basis=sdmd.BASIS_RFFT),                                  # no grid
+        cfg(basis=sdmd.BASIS_RFFT, grid_rows=64, grid_cols=64),      # 64*33 != n
+        cfg(basis=3),
+        cfg(storage=sdmd.DENSE, basis=sdmd.BASIS_FFT),
+        cfg(background=1),                                           # no grid
+        cfg(background=1, grid_rows=64, grid_cols=64, basis=sdmd.BASIS_FFT),
+        cfg(background=1, grid_rows=32, grid_cols=128, n_local=4096, n_global=4096, nranks=2),
+        cfg(background=1, grid_rows=48, grid_cols=48, n_local=48 * 48, n_global=48 * 48),  # not 2^k
+        cfg(grid_rows=64, grid_cols=0),
+    ]
+    for c in bad:
+        assert L.sdmd_create(ctypes.byref(c), ctypes.byref(h)) == sdmd.E_INVALID
