@@ -777,32 +777,45 @@ static __device__ int aberth_eigs(const double* Hg, int r, double* hc, const dou
   __syncthreads();
   if (sh_bad) return -1;
   // exact conjugate symmetry: snap near-real roots, pair each Im > 0 root with the Im < 0 root
-  // nearest to its conjugate (thread 0, O(r^2); r <= 224)
-  if (tid == 0) {
-    for (int k = 0; k < r; ++k) {
-      act[k] = 0;                                            // 0 unpaired, 1 done
-      if (fabs(z[k].y) <= 1e-10 * hypot(z[k].x, z[k].y)) { z[k].y = 0.0; act[k] = 1; }
-    }
-    for (int k = 0; k < r && !sh_bad; ++k) {
-      if (act[k] || z[k].y < 0.0) continue;
-      int best = -1;
-      double bd = 0.0;
-      for (int j = 0; j < r; ++j) {
-        if (act[j] || z[j].y >= 0.0) continue;
-        const double d = hypot(z[j].x - z[k].x, z[j].y + z[k].y);
-        if (best < 0 || d < bd) { best = j; bd = d; }
-      }
-      if (best < 0 || bd > 1e-8 * hypot(z[k].x, z[k].y)) { sh_bad = 1; break; }
-      const double re = 0.5 * (z[k].x + z[best].x), im = 0.5 * (z[k].y - z[best].y);
-      z[k] = make_double2(re, im);
-      z[best] = make_double2(re, -im);
-      act[k] = act[best] = 1;
-    }
-    for (int k = 0; k < r && !sh_bad; ++k)
-      if (!act[k]) sh_bad = 1;
+  // nearest to its conjugate.  In parallel (one thread per root): every Im > 0 root picks its
+  // nearest Im < 0 candidate; the pairing must come out a bijection (each Im < 0 root chosen
+  // exactly once, within 1e-8 relative) — then it is the same pairing a sequential greedy pass in
+  // root order would make — else the Francis QR decides.
+  int* partner = reinterpret_cast<int*>(zn);                 // zn is free after the iteration
+  int* chosen = partner + kMaxR;
+  for (int k = tid; k < r; k += K4_THREADS) {
+    act[k] = 0;                                              // 1: real (snapped)
+    chosen[k] = 0;
+    partner[k] = -1;
+    if (fabs(z[k].y) <= 1e-10 * hypot(z[k].x, z[k].y)) { z[k].y = 0.0; act[k] = 1; }
   }
   __syncthreads();
+  for (int k = tid; k < r; k += K4_THREADS) {
+    if (act[k] || z[k].y < 0.0) continue;
+    int best = -1;
+    double bd = 0.0;
+    for (int j = 0; j < r; ++j) {
+      if (act[j] || z[j].y >= 0.0) continue;
+      const double d = hypot(z[j].x - z[k].x, z[j].y + z[k].y);
+      if (best < 0 || d < bd) { best = j; bd = d; }
+    }
+    if (best < 0 || bd > 1e-8 * hypot(z[k].x, z[k].y)) { atomicOr(&sh_bad, 1); continue; }
+    partner[k] = best;
+    atomicAdd(&chosen[best], 1);
+  }
+  __syncthreads();
+  for (int j = tid; j < r; j += K4_THREADS)
+    if (!act[j] && z[j].y < 0.0 && chosen[j] != 1) atomicOr(&sh_bad, 1);
+  __syncthreads();
   if (sh_bad) return -1;
+  for (int k = tid; k < r; k += K4_THREADS) {
+    const int b = partner[k];
+    if (b < 0) continue;
+    const double re = 0.5 * (z[k].x + z[b].x), im = 0.5 * (z[k].y - z[b].y);
+    z[k] = make_double2(re, im);
+    z[b] = make_double2(re, -im);
+  }
+  __syncthreads();
   for (int k = tid; k < r; k += K4_THREADS) lam_out[k] = z[k];
   if (its_out) *its_out = its;
   if (evals_out) *evals_out = evals;
@@ -1144,6 +1157,69 @@ static __device__ __forceinline__ bool jacobi_pair(double* cp, double* cq, int m
   return false;
 }
 
+// ---- a7 tiles: out[i0+ii][j] (rows [i0, i0+ni), columns j < r) = Σ_k A[i0+ii][k] Bm[k][j] over
+// k < m, with A read by `ga(i, k)` and Bm by `gb(k, j)`, staged through shared memory in k-chunks of
+// 32 (A chunk [32][mb], B chunk [32][r]); thread (ti, tj) of the 16 x 32 grid accumulates rows
+// ti + 16a, columns tj + 32b (a < 4, b < 7) as fixed-order fma chains over k.  Kept out of line so
+// that its register tile does not raise the pressure of the Jacobi phase.
+// mode 0: A = XᵀX' (gathered from the Gram history of the window ending at f), Bm = Y, out = B
+//         (column-major, ld m);  mode 1: A = Yᵀ, Bm = B, out = Ã (row-major, ld r, into H)
+static __device__ __noinline__ void k4_tiled_product(int mode, int m, int r, int i0, int ni, int mb,
+                                                     int tid, double* t0, const double* gh, int NH,
+                                                     int mh, long long f, const double* Y, double* B,
+                                                     double* H) {
+  auto ga = [&](int i, int k) -> double {
+    return mode == 0 ? gram_at(gh, NH, mh, m, f, i, k + 1) : __ldcg(Y + (long long)i * m + k);
+  };
+  auto gb = [&](int k, int j) -> double {
+    return __ldcg((mode == 0 ? Y : B) + (long long)j * m + k);
+  };
+  auto st = [&](int i, int j, double v) {
+    if (mode == 0) B[(long long)j * m + i] = v;
+    else H[(long long)i * r + j] = v;
+  };
+  constexpr int KC = 32, RA = 4, RB = (kMaxR + 31) / 32;
+  const int ti = tid >> 5, tj = tid & 31;
+  double* As = t0;                                           // [KC][mb]
+  double* Bs = t0 + KC * mb;                                 // [KC][r]
+  double acc[RA][RB];
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < m; k0 += KC) {
+    const int nk = min(KC, m - k0);
+    for (int e = tid; e < KC * mb; e += K4_THREADS) {
+      const int ii = e / KC, kk = e % KC;
+      As[kk * mb + ii] = (kk < nk && ii < ni) ? ga(i0 + ii, k0 + kk) : 0.0;
+    }
+    for (int e = tid; e < KC * r; e += K4_THREADS) {
+      const int j = e / KC, kk = e % KC;
+      Bs[kk * r + j] = kk < nk ? gb(k0 + kk, j) : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < nk; ++kk) {
+      double g[RA], y[RB];
+#pragma unroll
+      for (int a = 0; a < RA; ++a) g[a] = (ti + 16 * a < mb) ? As[kk * mb + ti + 16 * a] : 0.0;
+#pragma unroll
+      for (int b = 0; b < RB; ++b) y[b] = (tj + 32 * b < r) ? Bs[kk * r + tj + 32 * b] : 0.0;
+#pragma unroll
+      for (int a = 0; a < RA; ++a)
+#pragma unroll
+        for (int b = 0; b < RB; ++b) acc[a][b] = fma(g[a], y[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int ii = ti + 16 * a, j = tj + 32 * b;
+      if (ii < ni && j < r) st(i0 + ii, j, acc[a][b]);
+    }
+}
+
 __global__ void __cluster_dims__(K4_CLUSTER, 1, 1) __launch_bounds__(K4_THREADS, 1)
 k4a_kernel(const K4Params p) {
   extern __shared__ __align__(16) unsigned char k4_smem[];
@@ -1393,6 +1469,7 @@ k4a_kernel(const K4Params p) {
   }
   cl_sync();
   if (tid == 0) ph[3] = clock64();
+  long long t_wait0 = 0;
 
   // ---- XᵀX' = G[0:m,1:m+1] needs the Gram column of frame f itself.  S = G[0:m,0:m] only needs
   // frames up to f-1, so K4a is released by the commit of frame f-1 and the Jacobi above overlaps
@@ -1430,32 +1507,49 @@ k4a_kernel(const K4Params p) {
     cl_sync();                                               // rank 0's flag read by everyone
     if (!go) return;                                         // frame f rejected: discard
   }
+  if (tid == 0) t_wait0 = clock64() - ph[3];                 // commit wait (diagnostics)
   __threadfence();
-  for (int idx = gtid; idx < m * m; idx += K4_GT) {
-    const int i = idx % m, j = idx / m;
-    p.Gxy[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j + 1);
+  if (p.atilde_v1) {                                        // A/B: the untiled L2 version
+    for (int idx = gtid; idx < m * m; idx += K4_GT) {
+      const int i = idx % m, j = idx / m;
+      p.Gxy[idx] = gram_at(p.ghist, p.NH, p.mh, m, f, i, j + 1);
+    }
+    cl_sync();
+    for (int idx = gtid; idx < m * r; idx += K4_GT) {
+      const int i = idx % m, j = idx / m;
+      const double* yj = p.Y + (long long)j * m;
+      double s = 0.0;
+      for (int k = 0; k < m; ++k) s = fma(__ldcg(p.Gxy + (long long)k * m + i), __ldcg(yj + k), s);
+      p.B[idx] = s;
+    }
+    cl_sync();
+    for (int idx = gwarp; idx < r * r; idx += K4_GW) {
+      const int i = idx / r, j = idx % r;
+      const double* yi = p.Y + (long long)i * m;
+      const double* bj = p.B + (long long)j * m;
+      double s = 0.0;
+      for (int k = lane; k < m; k += 32) s = fma(__ldcg(yi + k), __ldcg(bj + k), s);
+      s = wsum(s);
+      if (lane == 0) p.H[(long long)i * r + j] = s;
+    }
+    cl_sync();
+  } else {
+  // ---- a7: B = (XᵀX') Y (m x r), then Ã = Yᵀ B (r x r, row-major into H) — zero n-length dots.
+  // Two fp64 products tiled through shared memory (k4_tiled_product), split over the cluster by
+  // output rows (CTA c: rows [c·mb, (c+1)·mb) of B, then rows [c·rb, (c+1)·rb) of Ã); XᵀX' =
+  // G[0:m,1:m+1] is gathered from the Gram history straight into the tiles.
+  {
+    double* t0 = reinterpret_cast<double*>(k4_smem);
+    const int mb = (m + K4_CLUSTER - 1) / K4_CLUSTER;
+    const int i0 = crank * mb, ni = max(0, min(m, i0 + mb) - i0);
+    k4_tiled_product(0, m, r, i0, ni, mb, tid, t0, p.ghist, p.NH, p.mh, f, p.Y, p.B, p.H);
+    cl_sync();                                               // all of B visible cluster-wide
+    const int rb = (r + K4_CLUSTER - 1) / K4_CLUSTER;
+    const int i1 = crank * rb, n1 = max(0, min(r, i1 + rb) - i1);
+    k4_tiled_product(1, m, r, i1, n1, rb, tid, t0, p.ghist, p.NH, p.mh, f, p.Y, p.B, p.H);
   }
   cl_sync();
-
-  // ---- a7: B = (XᵀX') Y (m x r), Ã = Yᵀ B (r x r, row-major into H) — zero n-length dots
-  for (int idx = gtid; idx < m * r; idx += K4_GT) {
-    const int i = idx % m, j = idx / m;
-    const double* yj = p.Y + (long long)j * m;
-    double s = 0.0;
-    for (int k = 0; k < m; ++k) s = fma(__ldcg(p.Gxy + (long long)k * m + i), __ldcg(yj + k), s);
-    p.B[idx] = s;
   }
-  cl_sync();
-  for (int idx = gwarp; idx < r * r; idx += K4_GW) {         // warp per entry: coalesced dots
-    const int i = idx / r, j = idx % r;
-    const double* yi = p.Y + (long long)i * m;
-    const double* bj = p.B + (long long)j * m;
-    double s = 0.0;
-    for (int k = lane; k < m; k += 32) s = fma(__ldcg(yi + k), __ldcg(bj + k), s);
-    s = wsum(s);
-    if (lane == 0) p.H[(long long)i * r + j] = s;
-  }
-  cl_sync();
   if (tid == 0) ph[4] = clock64();
 
   // ---- a8: Householder reduction to upper Hessenberg form.  The rows of Ã are distributed over
@@ -1550,6 +1644,7 @@ k4a_kernel(const K4Params p) {
     res->qr_its = 0; res->sigma1 = sig[0]; res->nkeep = r; res->nB = 0;
     res->vframe = converged ? f : -1;            // V usable as the next warm start
     for (int q = 0; q < 5; ++q) res->phase[q] = ph[q + 1] - ph[q];
+    res->commit_wait = t_wait0;
     res->phase[5] = res->phase[6] = 0;
   }
 }
@@ -1902,12 +1997,15 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
   const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
   const size_t d = ((size_t)((r_max + 3) / 4) * r_max + 2 * kMaxR) * sizeof(double);  // Hessenberg rows
+  // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
+  const size_t d2 = (size_t)32 * ((((m > r_max ? m : r_max) + 3) / 4) + r_max) * sizeof(double);
   // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
   const size_t b3 = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // per mode
   const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b3 + (size_t)m * sizeof(double2)) : 0;
   size_t s = a > b ? a : b;
   s = s > c ? s : c;
   s = s > e ? s : e;
+  s = s > d2 ? s : d2;
   return s > d ? s : d;
 }
 

@@ -123,6 +123,7 @@ struct sdmd_ctx {
   int k1b_grid = 148;                   // CTAs of the batched Gram pass (K1b)
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
+  int atilde_v1 = 0;                    // SDMD_ATILDE=v1 selects the untiled Ã stage of K4a (A/B)
   long long ld = 0;
   size_t es = 4;
   void* ring = nullptr;
@@ -547,6 +548,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   {
     const char* ev = std::getenv("SDMD_K1");
     c->k1_v1 = (ev && std::strcmp(ev, "v1") == 0) ? 1 : 0;
+    const char* ea1 = std::getenv("SDMD_ATILDE");
+    c->atilde_v1 = (ea1 && std::strcmp(ea1, "v1") == 0) ? 1 : 0;
     const char* ed = std::getenv("SDMD_K1_DBG");
     c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* ew = std::getenv("SDMD_WARM");
@@ -816,6 +819,7 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
   p.bg_modes = c->cfg.bg_modes;
+  p.atilde_v1 = c->atilde_v1;
   // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa·P)
   const long long fp = f - (long long)c->Wa * c->P;
   if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m) {
@@ -1641,7 +1645,7 @@ int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[24]) {
   for (int q = 0; q < 7; ++q) out[6 + q] = res.phase[q];
   out[13] = res.qr_cnt[0]; out[14] = res.qr_cnt[1]; out[15] = res.qr_cnt[3];
   out[16] = res.phase[7]; out[17] = res.qr_cnt[2]; out[18] = res.qr_dbg[0]; out[19] = res.qr_dbg[1];
-  out[20] = res.aberth_its; out[21] = res.aberth_evals;
+  out[20] = res.aberth_its; out[21] = res.aberth_evals; out[22] = res.commit_wait;
   return SDMD_OK;
 }
 

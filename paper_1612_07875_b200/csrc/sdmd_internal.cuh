@@ -109,6 +109,7 @@ struct K4Result {
   long long vframe;           // frame whose converged eigenvectors V this workspace holds (K4a), or -1
   int nkeep;                  // modes with |λ_j| >= rank_tol·max|λ| (a prefix of the sorted λ); < r → W_SINGULAR
   int nB;                     // background mode set of this frame (B[0] = idx)
+  long long commit_wait;      // K4a SM cycles spent waiting for frame f's commit (inside phase[3])
   int bset[kMaxBgModes + 1];
 };
 
@@ -178,6 +179,7 @@ struct K4Params {
   // worker stream (stream-ordered: read at the start of K4b, rewritten at its end)
   double2* lam_warm;          // kMaxR
   int* r_warm;                // its r (0: none yet)
+  int atilde_v1;              // SDMD_ATILDE=v1: the untiled Ã stage (A/B only)
 };
 
 // per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)

@@ -500,7 +500,7 @@ class StreamingDMD:
                     qr_steps=int(o[13]), ms_steps=int(o[14]), ms_sweeps=int(o[15]),
                     ms_shift_cycles=int(o[16]), qr_block_its=int(o[17]),
                     ms_chase_ab_cycles=int(o[18]), ms_chase_c_cycles=int(o[19]),
-                    aberth_its=int(o[20]), aberth_evals=int(o[21]))
+                    aberth_its=int(o[20]), aberth_evals=int(o[21]), commit_wait=int(o[22]))
 
     def set_timing(self, on: bool = True):
         return self._check(lib().sdmd_set_timing(self.h, 1 if on else 0), "set_timing")
