@@ -680,149 +680,6 @@ static __device__ double2 hyman_ratio(const double* hc, int r, double2 z, int la
   return make_double2(__shfl_sync(0xffffffffu, N.x, 0), __shfl_sync(0xffffffffu, N.y, 0));
 }
 
-// z, zn: r complex each; act: r ints (all in shared memory, aliasing free space of the caller)
-static __device__ int aberth_eigs(const double* Hg, int r, double* hc, const double2* z0, int n0,
-                                  double2* z, double2* zn, int* act, double2* lam_out, int tid,
-                                  int warp, int lane, int* its_out, int* evals_out) {
-  __shared__ int sh_na, sh_bad;
-  __shared__ double sh_tr[2];
-  if (n0 != r || z0 == nullptr || r < 2) return -1;
-  // column-packed H: column j holds rows 0..min(j+1, r-1); 1/h_{j+1,j} replaces h_{j+1,j}
-  for (int j = warp; j < r; j += K4_WARPS) {
-    const int len = j + 2 < r ? j + 2 : r;
-    for (int i = lane; i < len; i += 32) hc[ab_cofs(j) + i] = __ldcg(Hg + (long long)i * r + j);
-  }
-  if (tid == 0) { sh_bad = 0; sh_tr[0] = 0.0; sh_tr[1] = 0.0; }
-  __syncthreads();
-  for (int j = tid + 1; j < r; j += K4_THREADS) {
-    const double sub = hc[ab_cofs(j - 1) + j];
-    const double sc = fabs(hc[ab_cofs(j - 1) + j - 1]) + fabs(hc[ab_cofs(j) + j]);
-    if (!(fabs(sub) > DBL_EPSILON * sc) || !isfinite(sub)) atomicOr(&sh_bad, 1);   // reducible
-  }
-  __syncthreads();
-  if (sh_bad) return -1;
-  for (int j = tid + 1; j < r; j += K4_THREADS) hc[ab_cofs(j - 1) + j] = 1.0 / hc[ab_cofs(j - 1) + j];
-  // initial guesses: the warm spectrum, real roots nudged off the axis (alternating sides), every
-  // root perturbed by a distinct relative 1e-9 k so that repeated values separate
-  for (int k = tid; k < r; k += K4_THREADS) {
-    double2 g = z0[k];
-    const double a = hypot(g.x, g.y);
-    const double sc = a > 0.0 ? a : 1.0;
-    if (g.y == 0.0) g.y = ((k & 1) ? 1e-3 : -1e-3) * sc;
-    g.x *= 1.0 + 1e-9 * (k + 1);
-    z[k] = g;
-    act[k] = k;
-  }
-  if (tid == 0) sh_na = r;
-  __syncthreads();
-  int its = 0, evals = 0;
-  const double tol = 4.0 * DBL_EPSILON;
-  while (sh_na > 0) {
-    if (its == AB_MAXIT) return -1;
-    ++its;
-    const int na = sh_na;
-    evals += na;
-    for (int q = warp; q < na; q += K4_WARPS) {             // one warp per active root
-      const int k = act[q];
-      const double2 zk = z[k];
-      const double2 N = hyman_ratio(hc, r, zk, lane);
-      double2 S = make_double2(0.0, 0.0);                  // Σ_{j≠k} 1/(z_k − z_j)
-      for (int jj = lane; jj < r; jj += 32)
-        if (jj != k) {                                     // 1/d = conj(d)/|d|^2
-          const double2 d = csub(zk, z[jj]);
-          const double id = 1.0 / fma(d.x, d.x, d.y * d.y);
-          S = make_double2(fma(d.x, id, S.x), fma(-d.y, id, S.y));
-        }
-      S = wsum2(S);
-      if (lane == 0) {
-        const double2 den = csub(make_double2(1.0, 0.0), cmul(N, S));
-        const double2 step = cdiv(N, den);
-        double2 nz = csub(zk, step);
-        if (!isfinite(nz.x) || !isfinite(nz.y)) { sh_bad = 1; nz = zk; }
-        zn[k] = nz;
-        // frozen when the correction is at rounding level (encoded in act by the compaction)
-        if (hypot(step.x, step.y) <= tol * hypot(nz.x, nz.y)) act[q] = -1 - k;
-      }
-    }
-    __syncthreads();
-    if (sh_bad) return -1;
-    for (int q = tid; q < na; q += K4_THREADS) {            // publish the new iterate
-      const int a = act[q];
-      const int k = a >= 0 ? a : -1 - a;
-      z[k] = zn[k];
-    }
-    __syncthreads();
-    if (tid == 0) {                                           // compact the active list in order
-      int c = 0;
-      for (int q = 0; q < na; ++q)
-        if (act[q] >= 0) act[c++] = act[q];
-      sh_na = c;
-    }
-    __syncthreads();
-  }
-  // trace check: Σ z_k = Σ h_kk (a lost/duplicated root shows here)
-  if (warp == 0) {
-    double2 sz = make_double2(0.0, 0.0);
-    double tr = 0.0, ta = 0.0;
-    for (int k = lane; k < r; k += 32) {
-      sz = cadd(sz, z[k]);
-      tr += hc[ab_cofs(k) + k];
-      ta += fabs(hc[ab_cofs(k) + k]) + hypot(z[k].x, z[k].y);
-    }
-    sz = wsum2(sz);
-    tr = wsum(tr);
-    ta = wsum(ta);
-    if (lane == 0 && (fabs(sz.x - tr) > 1e-10 * ta || fabs(sz.y) > 1e-10 * ta)) sh_bad = 1;
-  }
-  __syncthreads();
-  if (sh_bad) return -1;
-  // exact conjugate symmetry: snap near-real roots, pair each Im > 0 root with the Im < 0 root
-  // nearest to its conjugate.  In parallel (one thread per root): every Im > 0 root picks its
-  // nearest Im < 0 candidate; the pairing must come out a bijection (each Im < 0 root chosen
-  // exactly once, within 1e-8 relative) — then it is the same pairing a sequential greedy pass in
-  // root order would make — else the Francis QR decides.
-  int* partner = reinterpret_cast<int*>(zn);                 // zn is free after the iteration
-  int* chosen = partner + kMaxR;
-  for (int k = tid; k < r; k += K4_THREADS) {
-    act[k] = 0;                                              // 1: real (snapped)
-    chosen[k] = 0;
-    partner[k] = -1;
-    if (fabs(z[k].y) <= 1e-10 * hypot(z[k].x, z[k].y)) { z[k].y = 0.0; act[k] = 1; }
-  }
-  __syncthreads();
-  for (int k = tid; k < r; k += K4_THREADS) {
-    if (act[k] || z[k].y < 0.0) continue;
-    int best = -1;
-    double bd = 0.0;
-    for (int j = 0; j < r; ++j) {
-      if (act[j] || z[j].y >= 0.0) continue;
-      const double d = hypot(z[j].x - z[k].x, z[j].y + z[k].y);
-      if (best < 0 || d < bd) { best = j; bd = d; }
-    }
-    if (best < 0 || bd > 1e-8 * hypot(z[k].x, z[k].y)) { atomicOr(&sh_bad, 1); continue; }
-    partner[k] = best;
-    atomicAdd(&chosen[best], 1);
-  }
-  __syncthreads();
-  for (int j = tid; j < r; j += K4_THREADS)
-    if (!act[j] && z[j].y < 0.0 && chosen[j] != 1) atomicOr(&sh_bad, 1);
-  __syncthreads();
-  if (sh_bad) return -1;
-  for (int k = tid; k < r; k += K4_THREADS) {
-    const int b = partner[k];
-    if (b < 0) continue;
-    const double re = 0.5 * (z[k].x + z[b].x), im = 0.5 * (z[k].y - z[b].y);
-    z[k] = make_double2(re, im);
-    z[b] = make_double2(re, -im);
-  }
-  __syncthreads();
-  for (int k = tid; k < r; k += K4_THREADS) lam_out[k] = z[k];
-  if (its_out) *its_out = its;
-  if (evals_out) *evals_out = evals;
-  __syncthreads();
-  return 0;
-}
-
 // Inverse iteration on the Hessenberg form H (row-major r x r, global) for eigenvalue lam, one
 // warp.  Returns the right eigenvector w = Q z and (if yout) the left eigenvector y = Q u of the
 // ORIGINAL matrix Ã = Q H Qᵀ, both unit 2-norm; w additionally has its largest entry real > 0.
@@ -1155,6 +1012,174 @@ static __device__ __forceinline__ bool jacobi_pair(double* cp, double* cq, int m
     return true;
   }
   return false;
+}
+
+// ---- a8 on the K4a cluster: the Ehrlich–Aberth iteration of aberth_eigs with the active roots
+// spread over all K4_CLUSTER CTAs (root q of the active list on CTA q mod 4, warp (q / 4) mod 16),
+// so four SMs' shared-memory bandwidth and fp64 pipes share the Hyman evaluations.  Every CTA
+// holds the column-packed H and the full iterate; each writes the new iterate of its roots (and
+// its freeze / failure marks) into every CTA's shared memory (DSMEM), then one cluster barrier
+// publishes them and a second one keeps the next iteration's remote writes behind every CTA's
+// publish.  All CTAs therefore hold identical state and leave the loop together; CTA 0 then runs
+// the trace check and the conjugate pairing (as aberth_eigs) and returns 0 with lam_out filled, or
+// −1 (the caller falls back to the Francis QR).  CTAs other than 0 return 1 after the loop.
+static __device__ __forceinline__ unsigned dsm_addr(const void* p, unsigned cta) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(p), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(cta));
+  return ra;
+}
+static __device__ __forceinline__ void dsm_st(double2* p, unsigned cta, double2 v) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(dsm_addr(p, cta)), "d"(v.x), "d"(v.y) : "memory");
+}
+static __device__ __forceinline__ void dsm_st(float* p, unsigned cta, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dsm_addr(p, cta)), "f"(v) : "memory");
+}
+static __device__ __forceinline__ void dsm_st(int* p, unsigned cta, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, cta)), "r"(v) : "memory");
+}
+
+static __device__ int aberth_eigs_cluster(const double* Hg, int r, double* hc, const double2* z0,
+                                          int n0, double2* z, double2* zn, int* act, double2* lam_out,
+                                          int crank, int tid, int warp, int lane, int* its_out,
+                                          int* evals_out) {
+  __shared__ int sh_na, sh_bad;
+  __shared__ float prv[kMaxR];                               // |correction| of each root's last step
+  if (n0 != r || z0 == nullptr || r < 2) return crank == 0 ? -1 : 1;
+  for (int j = warp; j < r; j += K4_WARPS) {
+    const int len = j + 2 < r ? j + 2 : r;
+    for (int i = lane; i < len; i += 32) hc[ab_cofs(j) + i] = __ldcg(Hg + (long long)i * r + j);
+  }
+  if (tid == 0) sh_bad = 0;
+  __syncthreads();
+  for (int j = tid + 1; j < r; j += K4_THREADS) {
+    const double sub = hc[ab_cofs(j - 1) + j];
+    const double sc = fabs(hc[ab_cofs(j - 1) + j - 1]) + fabs(hc[ab_cofs(j) + j]);
+    if (!(fabs(sub) > DBL_EPSILON * sc) || !isfinite(sub)) atomicOr(&sh_bad, 1);   // reducible
+  }
+  __syncthreads();
+  if (sh_bad) return crank == 0 ? -2 : 1;                    // reducible (same data everywhere)
+  for (int j = tid + 1; j < r; j += K4_THREADS) hc[ab_cofs(j - 1) + j] = 1.0 / hc[ab_cofs(j - 1) + j];
+  for (int k = tid; k < r; k += K4_THREADS) {
+    double2 g = z0[k];
+    const double a = hypot(g.x, g.y);
+    const double sc = a > 0.0 ? a : 1.0;
+    if (g.y == 0.0) g.y = ((k & 1) ? 1e-3 : -1e-3) * sc;
+    g.x *= 1.0 + 1e-9 * (k + 1);
+    z[k] = g;
+    act[k] = k;
+    prv[k] = INFINITY;
+  }
+  if (tid == 0) sh_na = r;
+  cl_sync();                                                 // every CTA initialised before remote writes
+  int its = 0, evals = 0;
+  const double tol = 4.0 * DBL_EPSILON;
+  while (sh_na > 0) {
+    if (its == AB_MAXIT) return crank == 0 ? -3 : 1;
+    ++its;
+    const int na = sh_na;
+    evals += na;
+    for (int q = crank + K4_CLUSTER * warp; q < na; q += K4_CLUSTER * K4_WARPS) {
+      const int k = act[q];
+      const double2 zk = z[k];
+      const double2 N = hyman_ratio(hc, r, zk, lane);
+      double2 S = make_double2(0.0, 0.0);                    // Σ_{j≠k} 1/(z_k − z_j)
+      for (int jj = lane; jj < r; jj += 32)
+        if (jj != k) {
+          const double2 d = csub(zk, z[jj]);
+          const double id = 1.0 / fma(d.x, d.x, d.y * d.y);
+          S = make_double2(fma(d.x, id, S.x), fma(-d.y, id, S.y));
+        }
+      S = wsum2(S);
+      if (lane < K4_CLUSTER) {                               // lane c writes CTA c's copy
+        const double2 den = csub(make_double2(1.0, 0.0), cmul(N, S));
+        const double2 step = cdiv(N, den);
+        double2 nz = csub(zk, step);
+        const bool bad = !isfinite(nz.x) || !isfinite(nz.y);
+        if (bad) nz = zk;
+        dsm_st(zn + k, (unsigned)lane, nz);
+        if (bad) dsm_st(&sh_bad, (unsigned)lane, 1);
+        // frozen at rounding level, or stagnating at the evaluation's noise floor: a correction
+        // below 1e-11|z| that no longer shrinks by half (cubic convergence shrinks it far more;
+        // an ill-conditioned or clustered root hovers there instead, as accurate as QR would be)
+        const double as = hypot(step.x, step.y), az = hypot(nz.x, nz.y);
+        if (as <= tol * az || (as <= 1e-11 * az && as > 0.5 * (double)prv[k]))
+          dsm_st(act + q, (unsigned)lane, -1 - k);
+        dsm_st(prv + k, (unsigned)lane, (float)as);
+      }
+    }
+    cl_sync();                                               // the new iterate everywhere
+    if (sh_bad) return crank == 0 ? -4 : 1;
+    for (int q = tid; q < na; q += K4_THREADS) {
+      const int a = act[q];
+      const int k = a >= 0 ? a : -1 - a;
+      z[k] = zn[k];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int c = 0;
+      for (int q = 0; q < na; ++q)
+        if (act[q] >= 0) act[c++] = act[q];
+      sh_na = c;
+    }
+    cl_sync();                                               // publish done before new remote writes
+  }
+  if (its_out) *its_out = its;
+  if (evals_out) *evals_out = evals;
+  if (crank != 0) return 1;
+  // CTA 0: trace check and exact conjugate symmetry, as in aberth_eigs
+  if (warp == 0) {
+    double2 sz = make_double2(0.0, 0.0);
+    double tr = 0.0, ta = 0.0;
+    for (int k = lane; k < r; k += 32) {
+      sz = cadd(sz, z[k]);
+      tr += hc[ab_cofs(k) + k];
+      ta += fabs(hc[ab_cofs(k) + k]) + hypot(z[k].x, z[k].y);
+    }
+    sz = wsum2(sz);
+    tr = wsum(tr);
+    ta = wsum(ta);
+    if (lane == 0 && (fabs(sz.x - tr) > 1e-10 * ta || fabs(sz.y) > 1e-10 * ta)) sh_bad = 1;
+  }
+  __syncthreads();
+  if (sh_bad) return -5;                                     // trace mismatch
+  int* partner = reinterpret_cast<int*>(zn);
+  int* chosen = partner + kMaxR;
+  for (int k = tid; k < r; k += K4_THREADS) {
+    act[k] = 0;
+    chosen[k] = 0;
+    partner[k] = -1;
+    if (fabs(z[k].y) <= 1e-10 * hypot(z[k].x, z[k].y)) { z[k].y = 0.0; act[k] = 1; }
+  }
+  __syncthreads();
+  for (int k = tid; k < r; k += K4_THREADS) {
+    if (act[k] || z[k].y < 0.0) continue;
+    int best = -1;
+    double bd = 0.0;
+    for (int j = 0; j < r; ++j) {
+      if (act[j] || z[j].y >= 0.0) continue;
+      const double d = hypot(z[j].x - z[k].x, z[j].y + z[k].y);
+      if (best < 0 || d < bd) { best = j; bd = d; }
+    }
+    if (best < 0 || bd > 1e-8 * hypot(z[k].x, z[k].y)) { atomicOr(&sh_bad, 1); continue; }
+    partner[k] = best;
+    atomicAdd(&chosen[best], 1);
+  }
+  __syncthreads();
+  for (int j = tid; j < r; j += K4_THREADS)
+    if (!act[j] && z[j].y < 0.0 && chosen[j] != 1) atomicOr(&sh_bad, 1);
+  __syncthreads();
+  if (sh_bad) return -6;                                     // conjugate pairing failed
+  for (int k = tid; k < r; k += K4_THREADS) {
+    const int b = partner[k];
+    if (b < 0) continue;
+    const double re = 0.5 * (z[k].x + z[b].x), im = 0.5 * (z[k].y - z[b].y);
+    z[k] = make_double2(re, im);
+    z[b] = make_double2(re, -im);
+  }
+  __syncthreads();
+  for (int k = tid; k < r; k += K4_THREADS) lam_out[k] = z[k];
+  __syncthreads();
+  return 0;
 }
 
 // ---- a7 tiles: out[i0+ii][j] (rows [i0, i0+ni), columns j < r) = Σ_k A[i0+ii][k] Bm[k][j] over
@@ -1635,17 +1660,93 @@ k4a_kernel(const K4Params p) {
     for (int e = tid; e < nr * r; e += K4_THREADS) p.H[(long long)r0 * r + e] = sH[e];
     cl_sync();
   }
+  if (tid == 0) ph[5] = clock64();
+
+  // ---- a8: eigenvalues of Ã (unsorted, into p.lam; K4b orders them).  Ehrlich–Aberth with Hyman's
+  // method on all CTAs of the cluster (aberth_eigs_cluster), warm-started from the previous frame
+  // of this cluster stream; the Francis multishift QR on CTA 0 when there is no warm spectrum of
+  // the same size, H is reducible, or the iteration does not certify.
+  __shared__ MsShared ms_sh;
+  __shared__ int qr_st;
+  {
+    double* hs = reinterpret_cast<double*>(k4_smem);
+    double2* lam_raw = reinterpret_cast<double2*>(hs + ((hs_elems(r) + 1) & ~1LL));
+    int ab_rc = -1, ab_its = 0, ab_ev = 0;
+    bool ab_tried = false;
+    if (r > K4_MS_SMALL && p.r_warm != nullptr) {
+      const int n0 = *(volatile const int*)p.r_warm;       // written by this stream's previous K4a
+      if (n0 == r) {
+        ab_tried = true;
+        double2* zz = reinterpret_cast<double2*>(ms_sh.dense);
+        double2* zn = zz + kMaxR;
+        int* act = reinterpret_cast<int*>(zn + kMaxR);
+        ab_rc = aberth_eigs_cluster(p.H, r, hs, p.lam_warm, n0, zz, zn, act, lam_raw, crank, tid, warp,
+                                    lane, &ab_its, &ab_ev);
+      }
+    }
+    if (crank != 0) return;                                  // the rest is CTA 0's
+    if (tid == 0) qr_st = 0;
+    if (ab_rc != 0) {
+      for (int i = warp; i < r; i += K4_WARPS) {
+        const int lo = i > 3 ? i - 3 : 0;
+        const long long o = hs_off(i, r);
+        for (int j = lo + lane; j < r; j += 32)
+          hs[o + j - lo] = (j >= i - 1) ? __ldcg(p.H + (long long)i * r + j) : 0.0;
+      }
+      for (int i = tid; i < r; i += K4_THREADS) lam_raw[i] = make_double2(0.0, 0.0);
+      __syncthreads();
+      __shared__ int qc_sh[4];
+      __shared__ int its_sh;
+      __shared__ int roff_sh[kMaxR];
+      if (tid < 4) qc_sh[tid] = 0;
+      if (tid == 0) its_sh = 0;
+      for (int i = tid; i < r; i += K4_THREADS) roff_sh[i] = (int)(hs_off(i, r) - (i > 3 ? i - 3 : 0));
+      __syncthreads();
+      int its_local = 0;
+      long long shift_cyc = 0, chase_cyc[2] = {0, 0};
+      const int rc = multishift_qr(RowAcc{hs, roff_sh}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
+                                   warp == 0 ? qc_sh : nullptr, &shift_cyc, chase_cyc);
+      if (warp == 0 && lane == 0) atomicAdd(&its_sh, its_local);
+      __syncthreads();
+      if (tid == 0) {
+        if (rc != 0) qr_st = 5;
+        res->qr_its = its_sh;
+        res->qr_cnt[0] = qc_sh[0]; res->qr_cnt[1] = qc_sh[1]; res->qr_cnt[2] = qc_sh[2];
+        res->qr_cnt[3] = qc_sh[3];
+        res->phase[7] = shift_cyc;
+        res->qr_dbg[0] = chase_cyc[0];
+        res->qr_dbg[1] = chase_cyc[1];
+      }
+    } else if (tid == 0) {
+      res->qr_its = 0;
+      res->qr_cnt[0] = res->qr_cnt[1] = res->qr_cnt[2] = res->qr_cnt[3] = 0;
+      res->phase[7] = 0;
+      res->qr_dbg[0] = res->qr_dbg[1] = 0;
+    }
+    __syncthreads();
+    for (int k = tid; k < r; k += K4_THREADS) {
+      p.lam[k] = lam_raw[k];
+      if (p.r_warm != nullptr) p.lam_warm[k] = lam_raw[k];  // the next frame of this stream starts here
+    }
+    if (tid == 0) {
+      if (p.r_warm != nullptr) *p.r_warm = qr_st ? 0 : r;
+      // its, or the failure: −1 no warm start tried... −2 reducible, −3 no convergence in AB_MAXIT,
+      // −4 non-finite step, −5 trace mismatch, −6 conjugate pairing
+      res->aberth_its = ab_rc == 0 ? ab_its : (ab_tried ? ab_rc : 0);
+      res->aberth_evals = ab_ev;
+    }
+  }
   // K4a done: publish the factors' summary for K4b (same stream order via events)
-  if (crank == 0 && tid == 0) {
+  if (tid == 0) {
     if (r >= 2) p.tau[r - 2] = 0.0;
     p.tau[r > 0 ? r - 1 : 0] = 0.0;
-    ph[5] = clock64();
-    res->frame = f; res->status = sh_status; res->r = r; res->idx = -1; res->sweeps = sweeps;
-    res->qr_its = 0; res->sigma1 = sig[0]; res->nkeep = r; res->nB = 0;
+    ph[6] = clock64();
+    res->frame = f; res->status = (sh_status == 0 && qr_st) ? 5 : sh_status; res->r = r; res->idx = -1;
+    res->sweeps = sweeps; res->sigma1 = sig[0]; res->nkeep = r; res->nB = 0;
     res->vframe = converged ? f : -1;            // V usable as the next warm start
-    for (int q = 0; q < 5; ++q) res->phase[q] = ph[q + 1] - ph[q];
+    for (int q = 0; q < 6; ++q) res->phase[q] = ph[q + 1] - ph[q];
     res->commit_wait = t_wait0;
-    res->phase[5] = res->phase[6] = 0;
+    res->phase[6] = 0;
   }
 }
 
@@ -1677,69 +1778,12 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   const double sigma1 = res->sigma1;
   double* H = p.H;
 
-  // ---- a8: eigenvalues.  Ehrlich–Aberth (Hyman's method) warm-started from the previous frame of
-  // this worker stream; the Francis multishift QR in shared memory when there is no warm spectrum
-  // of the same size, H is reducible, or the iteration does not certify (see aberth_eigs)
+  // ---- a8: the eigenvalues of Ã were computed by K4a's cluster (unsorted in p.lam, see k4a_kernel)
   double* hs = reinterpret_cast<double*>(k4_smem);
   const long long hsz = hs_elems(r);
   double2* lam_raw = reinterpret_cast<double2*>(hs + ((hsz + 1) & ~1LL));
-  __shared__ MsShared ms_sh;
-  int ab_rc = -1, ab_its = 0, ab_ev = 0;
-  bool ab_tried = false;
-  if (r > K4_MS_SMALL && p.r_warm != nullptr) {
-    const int n0 = *(volatile const int*)p.r_warm;
-    if (n0 == r) {
-      ab_tried = true;
-      double2* zz = reinterpret_cast<double2*>(ms_sh.dense);      // MsShared is free until the QR
-      double2* zn = zz + kMaxR;
-      int* act = reinterpret_cast<int*>(zn + kMaxR);
-      ab_rc = aberth_eigs(H, r, hs, p.lam_warm, n0, zz, zn, act, lam_raw, tid, warp, lane, &ab_its, &ab_ev);
-    }
-  }
-  if (ab_rc != 0) {
-  for (int i = warp; i < r; i += K4_WARPS) {
-    const int lo = i > 3 ? i - 3 : 0;
-    const long long o = hs_off(i, r);
-    for (int j = lo + lane; j < r; j += 32)
-      hs[o + j - lo] = (j >= i - 1) ? __ldcg(H + (long long)i * r + j) : 0.0;
-  }
-  for (int i = tid; i < r; i += K4_THREADS) lam_raw[i] = make_double2(0.0, 0.0);
-  __syncthreads();
-  {
-    __shared__ int qc_sh[4];
-    if (tid < 4) qc_sh[tid] = 0;
-    __shared__ int its_sh;
-    if (tid == 0) its_sh = 0;
-    __syncthreads();
-    int its_local = 0;
-    __shared__ int roff_sh[kMaxR];
-    for (int i = tid; i < r; i += K4_THREADS) roff_sh[i] = (int)(hs_off(i, r) - (i > 3 ? i - 3 : 0));
-    __syncthreads();
-    long long shift_cyc = 0, chase_cyc[2] = {0, 0};
-    const int rc = multishift_qr(RowAcc{hs, roff_sh}, r, lam_raw, &ms_sh, tid, warp, lane, &its_local,
-                                 warp == 0 ? qc_sh : nullptr, &shift_cyc, chase_cyc);
-    if (warp == 0 && lane == 0) atomicAdd(&its_sh, its_local);
-    __syncthreads();
-    if (tid == 0) {
-      sh_its = its_sh;
-      if (rc != 0) sh_status = 5;
-      res->qr_cnt[0] = qc_sh[0]; res->qr_cnt[1] = qc_sh[1]; res->qr_cnt[2] = qc_sh[2];
-      res->qr_cnt[3] = qc_sh[3];
-      res->phase[7] = shift_cyc;
-      res->qr_dbg[0] = chase_cyc[0];
-      res->qr_dbg[1] = chase_cyc[1];
-    }
-  }
-  } else if (tid == 0) {
-    sh_its = 0;
-    res->qr_cnt[0] = res->qr_cnt[1] = res->qr_cnt[2] = res->qr_cnt[3] = 0;
-    res->phase[7] = 0;
-    res->qr_dbg[0] = res->qr_dbg[1] = 0;
-  }
-  if (tid == 0) {
-    res->aberth_its = ab_rc == 0 ? ab_its : (ab_tried ? -1 : 0);
-    res->aberth_evals = ab_ev;
-  }
+  for (int k = tid; k < r; k += K4_THREADS) lam_raw[k] = __ldcg(p.lam + k);
+  if (tid == 0) sh_its = res->qr_its;
   __syncthreads();
   if (tid == 0) ph[6] = clock64();
 
@@ -1758,10 +1802,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     p.lam[rk] = lj;
   }
   __syncthreads();
-  if (p.r_warm != nullptr) {                      // the next frame of this stream starts from here
-    for (int k = tid; k < r; k += K4_THREADS) p.lam_warm[k] = p.lam[k];
-    if (tid == 0) *p.r_warm = (sh_status == 5) ? 0 : r;
-  }
 
   // ---- a10: idx = argmin |log λ| (principal branch), λ = 0 excluded; ties (Q5)
   if (tid == 0) {
@@ -1894,7 +1934,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       const double2 lam = p.lam[idx];
       const double2 b0 = isnan(bq_sh[0].x) ? make_double2(0.0, 0.0) : bq_sh[0];
       ph[7] = clock64();
-      res->phase[5] = ph[6] - ph[5];
       res->phase[6] = ph[7] - ph[6];
       res->frame = f; res->status = st; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;
@@ -1975,7 +2014,6 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
     }
     if (tid == 0) {
       ph[7] = clock64();
-      res->phase[5] = ph[6] - ph[5];
       res->phase[6] = ph[7] - ph[6];
       res->frame = f; res->status = st_sh; res->r = r; res->idx = idx; res->sweeps = sweeps;
       res->qr_its = sh_its; res->lam_idx[0] = lam.x; res->lam_idx[1] = lam.y;

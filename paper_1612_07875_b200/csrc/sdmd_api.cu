@@ -678,7 +678,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     }
     AL(c->sg_cnt, (size_t)kMaxWorkers);
     cudaMemsetAsync(c->sg_cnt, 0, kMaxWorkers * sizeof(unsigned int), c->stream);
-    for (int w = 0; w < c->Wb; ++w) AL(c->lam_warm[w], (size_t)kMaxR);
+    for (int w = 0; w < c->Wa; ++w) AL(c->lam_warm[w], (size_t)kMaxR);
     AL(c->r_warm, (size_t)kMaxWorkers);
     cudaMemsetAsync(c->r_warm, 0, kMaxWorkers * sizeof(int), c->stream);
   }
@@ -826,8 +826,8 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
     const Workspace& kp = ws_of(c, fp);
     p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = (int)(f - fp);
   }
-  if (c->r_warm) {
-    const int sw = (int)(lidx(c, f) % c->Wb);
+  if (c->r_warm) {                              // per cluster stream (K4a computes eig(Ã))
+    const int sw = (int)(lidx(c, f) % c->Wa);
     p.lam_warm = c->lam_warm[sw];
     p.r_warm = c->r_warm + sw;
   }

@@ -175,8 +175,8 @@ struct K4Params {
   const double* Vprev;
   const K4Result* res_prev;
   int warm_k;
-  // eig(Ã) warm start: the sorted spectrum of the previous frame solved on the same single-CTA
-  // worker stream (stream-ordered: read at the start of K4b, rewritten at its end)
+  // eig(Ã) warm start: the spectrum of the previous frame solved on the same cluster stream
+  // (stream-ordered: read at the start of K4a's eigenvalue stage, rewritten at its end)
   double2* lam_warm;          // kMaxR
   int* r_warm;                // its r (0: none yet)
   int atilde_v1;              // SDMD_ATILDE=v1: the untiled Ã stage (A/B only)
