@@ -77,19 +77,22 @@ def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max
     return out
 
 
-def sparse_run(K, workers, pool=160, host=False):
-    ss = synth.SparseDCTStream()
+def sparse_run(K, workers, pool=160, host=False, bg=False, basis="dct"):
+    ss = synth.SparseDCTStream() if basis == "dct" else synth.SparseFourierStream(half=basis == "rfft")
     m = 128
     hostmem = host
     host = [ss.frame(t) for t in range(pool)]
     cap = ss.nnz_cap
+    vv = (lambda v: v) if basis == "dct" else (lambda v: v.view(np.float64))   # noqa: E731
     if hostmem:     # NEXT-3: compressed ingest from pinned host memory (only the nonzeros cross PCIe)
         idx_d = [torch.from_numpy(np.ascontiguousarray(i)).pin_memory() for i, _ in host]
-        val_d = [torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for _, v in host]
+        val_d = [torch.from_numpy(np.ascontiguousarray(vv(v))).pin_memory() for _, v in host]
     else:
         idx_d = [torch.from_numpy(np.ascontiguousarray(i)).cuda() for i, _ in host]
-        val_d = [torch.from_numpy(np.ascontiguousarray(v)).cuda() for _, v in host]
-    eng = StreamingDMD(ss.n, m, dtype="f64", storage="sparse", nnz_cap=cap, workers=workers)
+        val_d = [torch.from_numpy(np.ascontiguousarray(vv(v))).cuda() for _, v in host]
+    grid = (ss.N, ss.N) if basis == "dct" else (ss.rows, ss.cols)
+    eng = StreamingDMD(ss.n, m, dtype="f64", storage="sparse", nnz_cap=cap, workers=workers,
+                       background=bg, basis=basis, grid=grid, threshold=1e-4)
     t = 0
     for _ in range(3 * (m + 1)):
         eng.push_sparse(idx_d[t % pool], val_d[t % pool])
@@ -104,7 +107,10 @@ def sparse_run(K, workers, pool=160, host=False):
     sp = eng.spectrum()
     k3 = st["k1_ms"] / max(1, st["k1_launches"])
     nnz = float(np.mean([i.size for i, _ in host]))
-    out = {"config": "C5" + (" (host-pinned sparse ingest, 12 B/nonzero H2D)" if hostmem else ""),
+    name = "C5" if basis == "dct" else f"C5-{basis.upper()} ({'half' if basis == 'rfft' else 'full'} spectrum, complex)"
+    if bg:
+        name += " (pixel-space background: IDCT2)"
+    out = {"config": name + (" (host-pinned sparse ingest, 12 B/nonzero H2D)" if hostmem else ""),
            "n": ss.n, "m": m, "dtype": "f64 sparse", "nnz_avg": round(nnz, 1),
            "frames": K, "workers": workers, "snapshots_per_s": round(K / (ms / 1e3), 2),
            "ms_per_step": round(ms / K, 4), "gram_pass_ms": round(k3, 4),
@@ -163,6 +169,11 @@ def main():
     res.append(sparse_run(args.frames, args.workers))
     print(json.dumps(res[-1]), flush=True)
     res.append(sparse_run(args.frames, args.workers, host=True))
+    print(json.dumps(res[-1]), flush=True)
+    # NEXT-3: pixel-space background of the sparse DCT stream; the complex rfft half-spectrum basis
+    res.append(sparse_run(args.frames, args.workers, bg=True))
+    print(json.dumps(res[-1]), flush=True)
+    res.append(sparse_run(args.frames, args.workers, basis="rfft"))
     print(json.dumps(res[-1]), flush=True)
     if args.out:
         with open(args.out, "w") as fh:
