@@ -1031,6 +1031,9 @@ static __device__ __forceinline__ unsigned dsm_addr(const void* p, unsigned cta)
 static __device__ __forceinline__ void dsm_st(double2* p, unsigned cta, double2 v) {
   asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(dsm_addr(p, cta)), "d"(v.x), "d"(v.y) : "memory");
 }
+static __device__ __forceinline__ void dsm_st(double* p, unsigned cta, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(dsm_addr(p, cta)), "d"(v) : "memory");
+}
 static __device__ __forceinline__ void dsm_st(float* p, unsigned cta, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dsm_addr(p, cta)), "f"(v) : "memory");
 }
@@ -1579,7 +1582,9 @@ k4a_kernel(const K4Params p) {
 
   // ---- a8: Householder reduction to upper Hessenberg form.  The rows of Ã are distributed over
   // the cluster's shared memory (CTA c owns rows [c·rb, (c+1)·rb)); per reflector only the pivot
-  // column and the partial row-sums wᵀ = vᵀH cross CTAs (two cluster barriers per step).
+  // column and the partial row-sums wᵀ = vᵀH cross CTAs, written straight into every CTA's shared
+  // memory (DSMEM; two cluster barriers per step, no global round trips).  The partial sums are
+  // added in CTA order on every CTA, so all hold the same reflector and the same τw.
   {
     const int rb = (r + K4_CLUSTER - 1) / K4_CLUSTER;
     const int r0 = crank * rb, r1 = min(r, r0 + rb);
@@ -1587,21 +1592,24 @@ k4a_kernel(const K4Params p) {
     double* sH = reinterpret_cast<double*>(k4_smem);        // nr x r, row-major
     double* sv = sH + (size_t)rb * r;                        // v  (kMaxR)
     double* sw = sv + kMaxR;                                 // τw (kMaxR)
-    double* colk = p.B;                                      // published pivot column
-    double* wpart = p.B + kMaxR;                             // [K4_CLUSTER][kMaxR] partial wᵀ
+    double* colk = sw + kMaxR;                               // pivot column (kMaxR, every CTA's rows)
+    double* wpart = colk + kMaxR;                            // [K4_CLUSTER][kMaxR] partial wᵀ
     __shared__ double sh_tk, sh_beta;
     for (int e = tid; e < nr * r; e += K4_THREADS) sH[e] = __ldcg(p.H + (long long)r0 * r + e);
     __syncthreads();
     for (int k = 0; k < r - 2; ++k) {
       const int L = r - k - 1;
       const int i0 = r0 > k + 1 ? r0 : k + 1;                // my rows taking part in the reflector
-      for (int i = i0 + tid; i < r1; i += K4_THREADS) colk[i] = sH[(size_t)(i - r0) * r + k];
+      for (int e = tid; e < (r1 - i0) * K4_CLUSTER; e += K4_THREADS) {
+        const int i = i0 + e / K4_CLUSTER;
+        dsm_st(colk + i, (unsigned)(e % K4_CLUSTER), sH[(size_t)(i - r0) * r + k]);
+      }
       cl_sync();
       if (warp == 0) {                                       // identical on every CTA
         double s2 = 0.0;
-        for (int i = 1 + lane; i < L; i += 32) { const double x = __ldcg(colk + k + 1 + i); s2 = fma(x, x, s2); }
+        for (int i = 1 + lane; i < L; i += 32) { const double x = colk[k + 1 + i]; s2 = fma(x, x, s2); }
         s2 = wsum(s2);
-        const double x0 = __ldcg(colk + k + 1);
+        const double x0 = colk[k + 1];
         double tauk = 0.0, beta = x0, v0 = 1.0;
         if (s2 != 0.0) {
           const double mu_ = sqrt(x0 * x0 + s2);
@@ -1610,7 +1618,7 @@ k4a_kernel(const K4Params p) {
           beta = mu_;
         }
         for (int i = lane; i < L; i += 32) {
-          const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? __ldcg(colk + k + 1 + i) / v0 : 0.0);
+          const double v = (i == 0) ? 1.0 : (tauk != 0.0 ? colk[k + 1 + i] / v0 : 0.0);
           sv[i] = v;
           if (crank == 0) p.Qv[(long long)k * r + k + 1 + i] = v;
         }
@@ -1628,12 +1636,13 @@ k4a_kernel(const K4Params p) {
         for (int j = k + 1 + tid; j < r; j += K4_THREADS) {  // partial wᵀ = vᵀ H over my rows
           double s = 0.0;
           for (int i = i0; i < r1; ++i) s = fma(sv[i - k - 1], sH[(size_t)(i - r0) * r + j], s);
-          wpart[crank * kMaxR + j] = s;
+#pragma unroll
+          for (int c = 0; c < K4_CLUSTER; ++c) dsm_st(wpart + crank * kMaxR + j, (unsigned)c, s);
         }
         cl_sync();
         for (int j = k + 1 + tid; j < r; j += K4_THREADS) {
           double s = 0.0;
-          for (int c = 0; c < K4_CLUSTER; ++c) s += __ldcg(wpart + c * kMaxR + j);
+          for (int c = 0; c < K4_CLUSTER; ++c) s += wpart[c * kMaxR + j];
           sw[j] = s * tk;
         }
         __syncthreads();
@@ -2034,7 +2043,7 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
   const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
-  const size_t d = ((size_t)((r_max + 3) / 4) * r_max + 2 * kMaxR) * sizeof(double);  // Hessenberg rows
+  const size_t d = ((size_t)((r_max + 3) / 4) * r_max + (3 + K4_CLUSTER) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
   // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
   const size_t d2 = (size_t)32 * ((((m > r_max ? m : r_max) + 3) / 4) + r_max) * sizeof(double);
   // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
