@@ -756,7 +756,7 @@ static __device__ void iv_apply_q(const double* Qv, const double* tau, int r, do
 
 // (H − λI) = P L U (see inverse_iteration); hn_in >= 0: max |h_ij| precomputed by the caller
 static __device__ void iv_lu(const double* H, int r, double2 lam, double2* M, double2* lk, int* sw,
-                             int lane, double hn_in) {
+                             int lane, double hn_in, double2* Mc = nullptr) {
   double hn = hn_in;
   if (hn < 0.0) {
     hn = 0.0;
@@ -794,16 +794,61 @@ static __device__ void iv_lu(const double* H, int r, double2 lam, double2* M, do
       const int j = lane + 32 * s;
       const double2 urow = swp ? nxt[s] : cur[s];
       const double2 crow = swp ? cur[s] : nxt[s];
-      if (j >= k && j < r) M[(long long)k * r + j] = (j == k) ? piv : urow;
+      if (j >= k && j < r) {
+        const double2 u = (j == k) ? piv : urow;
+        M[(long long)k * r + j] = u;
+        if (Mc) Mc[(long long)j * r + k] = u;            // column-major copy (CTA-group right solve)
+      }
       cur[s] = (j > k) ? csub(crow, cmul(l, urow)) : make_double2(0.0, 0.0);
     }
     if (lane == 0) { lk[k] = l; sw[k] = swp ? 1 : 0; }
   }
   {
     const double2 d = shfl2(iv_pick(cur, (r - 1) >> 5), (r - 1) & 31);
-    if (lane == ((r - 1) & 31)) M[(long long)(r - 1) * r + r - 1] = (cabs2(d) == 0.0) ? make_double2(small, 0.0) : d;
+    if (lane == ((r - 1) & 31)) {
+      const double2 u = (cabs2(d) == 0.0) ? make_double2(small, 0.0) : d;
+      M[(long long)(r - 1) * r + r - 1] = u;
+      if (Mc) Mc[(long long)(r - 1) * r + r - 1] = u;
+    }
   }
   __syncwarp();
+}
+
+// w = Q z with the Q12 normalisation (unit norm, largest-|.| entry real > 0), one warp
+static __device__ void iv_finish_right(const double* Qv, const double* tau, int r, const double2* z,
+                                      double2* wout, int lane) {
+  for (int i = lane; i < r; i += 32) wout[i] = z[i];
+  __syncwarp();
+  iv_apply_q(Qv, tau, r, wout, lane);
+  {                                                  // unit norm, largest-|.| entry real > 0 (Q12)
+    double best = -1.0;
+    int bi = 0;
+    double ss = 0.0;
+    for (int i = lane; i < r; i += 32) {
+      const double av = cabs2(wout[i]);
+      ss += av * av;
+      if (av > best) { best = av; bi = i; }
+    }
+    ss = wsum(ss);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const double2 pv = wout[bi];
+    const double ap = cabs2(pv);
+    const double2 ph = make_double2(pv.x / ap, -pv.y / ap);
+    const double inv = 1.0 / sqrt(ss);
+    __syncwarp();
+    for (int i = lane; i < r; i += 32) {
+      const double2 v = cmul(wout[i], ph);
+      wout[i] = make_double2(v.x * inv, v.y * inv);
+    }
+    __syncwarp();
+    if (lane == 0) wout[bi] = make_double2(wout[bi].x, 0.0);
+    __syncwarp();
+  }
 }
 
 // right eigenvector from the LU of iv_lu: two solves U z = (L⁻¹P) rhs, w = Q z, Q12 normalisation
@@ -852,38 +897,7 @@ static __device__ void iv_right(const double* Qv, const double* tau, int r, cons
     for (int i = lane; i < r; i += 32) rhs[i] = z[i];
     __syncwarp();
   }
-  for (int i = lane; i < r; i += 32) wout[i] = z[i];
-  __syncwarp();
-  iv_apply_q(Qv, tau, r, wout, lane);
-  {                                                  // unit norm, largest-|.| entry real > 0 (Q12)
-    double best = -1.0;
-    int bi = 0;
-    double ss = 0.0;
-    for (int i = lane; i < r; i += 32) {
-      const double av = cabs2(wout[i]);
-      ss += av * av;
-      if (av > best) { best = av; bi = i; }
-    }
-    ss = wsum(ss);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-    }
-    const double2 pv = wout[bi];
-    const double ap = cabs2(pv);
-    const double2 ph = make_double2(pv.x / ap, -pv.y / ap);
-    const double inv = 1.0 / sqrt(ss);
-    __syncwarp();
-    for (int i = lane; i < r; i += 32) {
-      const double2 v = cmul(wout[i], ph);
-      wout[i] = make_double2(v.x * inv, v.y * inv);
-    }
-    __syncwarp();
-    if (lane == 0) wout[bi] = make_double2(wout[bi].x, 0.0);
-    __syncwarp();
-  }
+  iv_finish_right(Qv, tau, r, z, wout, lane);
 }
 
 // left eigenvector from the LU of iv_lu: Mᴴ u = e (two solves), y = Q u, unit norm
@@ -935,6 +949,120 @@ static __device__ void iv_left(const double* Qv, const double* tau, int r, const
   for (int i = lane; i < r; i += 32) yout[i] = z[i];
   __syncwarp();
   iv_apply_q(Qv, tau, r, yout, lane);
+}
+
+// ---- CTA-group triangular solves of the per-frame inverse iteration (K4b, single background
+// mode).  A group of IV_GT threads (8 warps) owns one row each (thread j <-> row j, r <= 224 <
+// IV_GT): after the owner of row i forms its unknown and publishes it in shared memory, one named
+// barrier, and every other thread updates its own right-hand side in a register — one barrier
+// per row instead of a warp reduction.  The U entries a thread needs do not depend on the solve,
+// so each thread streams them IV_PD rows/columns ahead through a register shift queue (the L2
+// latency hides behind the solve).  Same arithmetic as the row-oriented warp solves up to the
+// summation order of each row.
+constexpr int IV_GT = 256;                           // threads per group
+constexpr int IV_PD = 8;                             // prefetch depth
+static __device__ __forceinline__ void grp_bar(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(IV_GT) : "memory");
+}
+
+// U z = rhs (backward), U column-major: column i at Uc[i*r + (0..i)]; rhs[j] in, z[] out (smem)
+static __device__ __noinline__ void grp_solve_upper(const double2* Uc, int r, const double2* rhs, double2* z, int j,
+                                       int bar) {
+  double2 b = j < r ? rhs[j] : make_double2(0.0, 0.0);
+  double2 q[IV_PD];
+#pragma unroll
+  for (int d = 0; d < IV_PD; ++d) {
+    const int i = r - 1 - d;
+    q[d] = (j < r && i >= j) ? __ldcg(Uc + (long long)i * r + j) : make_double2(0.0, 0.0);
+  }
+  for (int i = r - 1; i >= 0; --i) {
+    const double2 u = q[0];
+#pragma unroll
+    for (int d = 0; d < IV_PD - 1; ++d) q[d] = q[d + 1];
+    {
+      const int in = i - IV_PD;
+      q[IV_PD - 1] = (j < r && in >= j) ? __ldcg(Uc + (long long)in * r + j) : make_double2(0.0, 0.0);
+    }
+    if (j == i) z[i] = cdiv(b, u);
+    grp_bar(bar);
+    if (j < i) b = csub(b, cmul(u, z[i]));
+  }
+  grp_bar(bar);
+}
+
+// Uᴴ a = rhs (forward), U row-major: row i at Ur[i*r + (i..r-1)]
+static __device__ __noinline__ void grp_solve_upper_h(const double2* Ur, int r, const double2* rhs, double2* a, int k,
+                                         int bar) {
+  double2 b = k < r ? rhs[k] : make_double2(0.0, 0.0);
+  double2 q[IV_PD];
+#pragma unroll
+  for (int d = 0; d < IV_PD; ++d)
+    q[d] = (k < r && d <= k) ? __ldcg(Ur + (long long)d * r + k) : make_double2(0.0, 0.0);
+  for (int i = 0; i < r; ++i) {
+    const double2 u = q[0];
+#pragma unroll
+    for (int d = 0; d < IV_PD - 1; ++d) q[d] = q[d + 1];
+    {
+      const int in = i + IV_PD;
+      q[IV_PD - 1] = (k < r && in <= k) ? __ldcg(Ur + (long long)in * r + k) : make_double2(0.0, 0.0);
+    }
+    if (k == i) a[i] = cdiv(b, cconj(u));
+    grp_bar(bar);
+    if (k > i) b = csub(b, cmul(cconj(u), a[i]));
+  }
+  grp_bar(bar);
+}
+
+// right eigenvector by the group (gt = thread in the group, gw = warp in the group): two inverse
+// iterations U z = L⁻¹P rhs, then w = Q z with the Q12 normalisation (as iv_right)
+static __device__ void iv_right_grp(const double* Qv, const double* tau, int r, const double2* Uc,
+                                    const double2* lk, const int* sw, double2* z, double2* rhs,
+                                    double2* wout, int gt, int gw, int lane, int bar) {
+  for (int i = gt; i < r; i += IV_GT) rhs[i] = make_double2(1.0, 0.0);
+  grp_bar(bar);
+  for (int it = 0; it < 2; ++it) {
+    if (gt == 0) {
+      for (int k = 0; k < r - 1; ++k) {
+        if (sw[k]) { const double2 t = rhs[k]; rhs[k] = rhs[k + 1]; rhs[k + 1] = t; }
+        rhs[k + 1] = csub(rhs[k + 1], cmul(lk[k], rhs[k]));
+      }
+    }
+    grp_bar(bar);
+    grp_solve_upper(Uc, r, rhs, z, gt, bar);
+    if (gw == 0) {
+      iv_normalise(z, r, lane);
+      for (int i = lane; i < r; i += 32) rhs[i] = z[i];
+    }
+    grp_bar(bar);
+  }
+  if (gw == 0) iv_finish_right(Qv, tau, r, z, wout, lane);
+}
+
+static __device__ void iv_left_grp(const double* Qv, const double* tau, int r, const double2* Ur,
+                                   const double2* lk, const int* sw, double2* z, double2* rhs,
+                                   double2* yout, int gt, int gw, int lane, int bar) {
+  for (int i = gt; i < r; i += IV_GT) rhs[i] = make_double2(1.0, 0.0);
+  grp_bar(bar);
+  for (int it = 0; it < 2; ++it) {
+    grp_solve_upper_h(Ur, r, rhs, z, gt, bar);
+    if (gt == 0) {
+      for (int k = r - 2; k >= 0; --k) {
+        z[k] = csub(z[k], cmul(cconj(lk[k]), z[k + 1]));
+        if (sw[k]) { const double2 t = z[k]; z[k] = z[k + 1]; z[k + 1] = t; }
+      }
+    }
+    grp_bar(bar);
+    if (gw == 0) {
+      iv_normalise(z, r, lane);
+      for (int i = lane; i < r; i += 32) rhs[i] = z[i];
+    }
+    grp_bar(bar);
+  }
+  if (gw == 0) {
+    for (int i = lane; i < r; i += 32) yout[i] = z[i];
+    __syncwarp();
+    iv_apply_q(Qv, tau, r, yout, lane);
+  }
 }
 
 static __device__ void inverse_iteration(const double* H, const double* Qv, const double* tau, int r,
@@ -1980,10 +2108,11 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
       __syncthreads();
     }
     const double2 lam = p.lam[idx];
-    if (warp == 0) iv_lu(H, r, lam, p.M, lk, swk, lane, hn_sh);
+    if (warp == 0) iv_lu(H, r, lam, p.M, lk, swk, lane, hn_sh, p.Mc);
     __syncthreads();
-    if (warp == 0) iv_right(p.Qv, p.tau, r, p.M, lk, swk, z, rhs, p.w, lane);
-    else if (warp == 1) iv_left(p.Qv, p.tau, r, p.M, lk, swk, z2, rhs2, p.y, lane);
+    // right vector on threads 0..255, left vector on 256..511 (named barriers 1 and 2)
+    if (tid < IV_GT) iv_right_grp(p.Qv, p.tau, r, p.Mc, lk, swk, z, rhs, p.w, tid, warp, lane, 1);
+    else iv_left_grp(p.Qv, p.tau, r, p.M, lk, swk, z2, rhs2, p.y, tid - IV_GT, warp - IV_GT / 32, lane, 2);
     __syncthreads();
     if (warp == 0) {
       double2 ya = make_double2(0, 0), yw = make_double2(0, 0);

@@ -105,7 +105,7 @@ constexpr int kMaxWS = kMaxLag + 4;      // per-frame eigen workspaces (NWS = la
 struct Workspace {
   double *A = nullptr, *Gxy = nullptr, *V = nullptr, *sigma = nullptr, *Y = nullptr, *B = nullptr;
   double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
-  double2 *M = nullptr, *lam = nullptr, *w = nullptr, *y = nullptr;
+  double2 *M = nullptr, *Mc = nullptr, *lam = nullptr, *w = nullptr, *y = nullptr;
   K4Result* res = nullptr;
   int* flags = nullptr;
   double *mu = nullptr, *wv = nullptr, *uv = nullptr;
@@ -648,6 +648,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     AL(k.alpha1, (size_t)R);
     const size_t nbs = c->cfg.bg_modes > 1 ? (size_t)c->cfg.bg_modes + 1 : 1;   // per-mode slots
     AL(k.M, nbs * R * R);
+    AL(k.Mc, (size_t)R * R);
     AL(k.lam, (size_t)R);
     AL(k.w, nbs * R);
     AL(k.y, nbs * R);
@@ -788,7 +789,7 @@ int sdmd_destroy(sdmd_ctx* c) {
     if (p) cudaFree(p);
   for (int w = 0; w < kMaxWS; ++w) {
     Workspace& k = c->ws[w];
-    void* wp[] = {k.A, k.Gxy, k.V, k.sigma, k.Y, k.B, k.H, k.Qv, k.tau, k.alpha1, k.M, k.lam, k.w,
+    void* wp[] = {k.A, k.Gxy, k.V, k.sigma, k.Y, k.B, k.H, k.Qv, k.tau, k.alpha1, k.M, k.Mc, k.lam, k.w,
                   k.y, k.res, k.flags, k.mu, k.wv, k.uv};
     for (void* p : wp)
       if (p) cudaFree(p);
@@ -814,7 +815,7 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.r_max = c->cfg.r_max < p.m ? c->cfg.r_max : p.m;
   p.rank_tol = c->cfg.rank_tol; p.st = c->dst;
   p.A = k.A; p.Gxy = k.Gxy; p.V = k.V; p.sigma = k.sigma; p.Y = k.Y; p.B = k.B; p.H = k.H;
-  p.Qv = k.Qv; p.tau = k.tau; p.M = k.M; p.lam = k.lam; p.w = k.w; p.y = k.y; p.alpha1 = k.alpha1;
+  p.Qv = k.Qv; p.tau = k.tau; p.M = k.M; p.Mc = k.Mc; p.lam = k.lam; p.w = k.w; p.y = k.y; p.alpha1 = k.alpha1;
   p.res = k.res;
   p.cout = c->cbuf + (f % c->NC) * c->cfg.m;
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;

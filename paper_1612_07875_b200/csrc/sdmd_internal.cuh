@@ -158,6 +158,7 @@ struct K4Params {
   double* Qv;                 // kMaxR*kMaxR row-major: Householder vector k in row k
   double* tau;                // kMaxR
   double2* M;                 // kMaxR*kMaxR complex row-major (inverse-iteration LU)
+  double2* Mc;                // kMaxR*kMaxR complex: the same U factor column-major (K4b group solve)
   double2* lam;               // kMaxR sorted eigenvalues of Ã
   double2* w;                 // kMaxR right eigenvector (background mode)
   double2* y;                 // kMaxR left eigenvector
