@@ -697,7 +697,7 @@ __global__ void commit_kernel(const K1Params p) {
 
 template <typename T, bool BG, int NQ>
 static cudaError_t launch_k1_inst(const K1Params& p, int grid, int smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k1_gram_kernel<T, BG, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_max_dyn_smem((const void*)k1_gram_kernel<T, BG, NQ>, smem);
   static const int carve = [] { const char* c = std::getenv("SDMD_K1_CARVEOUT"); return c ? std::atoi(c) : -1; }();
   if (e == cudaSuccess && carve >= 0)      // experiment knob: shared-memory carveout (percent)
     e = cudaFuncSetAttribute(k1_gram_kernel<T, BG, NQ>, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
@@ -717,7 +717,7 @@ static cudaError_t launch_k1v2_inst(const K1Params& p, int grid, cudaStream_t s)
   constexpr int EPV = VecOf<T>::E;
   const int smem = BG ? (K1V2_LAGR + K1V2_SLACK) * K1_WARPS * EPV * 33 * (int)(2 * sizeof(T)) : 0;
   if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k1v2_kernel<T, BG, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const cudaError_t e = set_max_dyn_smem((const void*)k1v2_kernel<T, BG, NQ>, smem);
     if (e != cudaSuccess) return e;
   }
   k1v2_kernel<T, BG, NQ><<<grid, K1_THREADS, smem, s>>>(p);

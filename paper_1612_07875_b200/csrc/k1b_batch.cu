@@ -186,7 +186,7 @@ template <typename T>
 static cudaError_t launch_k1b_t(const K1bParams& p, int grid, cudaStream_t s) {
   using S = KbShape<T>;
   const int smem = S::ST * (p.m + p.k) * S::LDS * (int)sizeof(T);
-  cudaError_t e = cudaFuncSetAttribute(k1b_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = set_max_dyn_smem((const void*)k1b_kernel<T>, smem);
   if (e != cudaSuccess) return e;
   k1b_kernel<T><<<grid, KB_THREADS, smem, s>>>(p);
   return cudaGetLastError();

@@ -217,10 +217,10 @@ cudaError_t launch_init_gram(const void* Z, long long ldz, int dtype, long long 
   cudaError_t e;
   const size_t smem = dtype == 0 ? g2_smem<float>() : g2_smem<double>();
   if (dtype == 0) {
-    if ((e = cudaFuncSetAttribute(gram_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem((const void*)gram_tc_kernel<float>, (int)smem)) != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tc_kernel<float>, G2_THREADS, smem);
   } else {
-    if ((e = cudaFuncSetAttribute(gram_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem((const void*)gram_tc_kernel<double>, (int)smem)) != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gram_tc_kernel<double>, G2_THREADS, smem);
   }
   if (occ < 1) occ = 1;
@@ -342,12 +342,12 @@ cudaError_t launch_modes(const void* ring, long long ld, int NS, int dtype, long
   cudaError_t e;
   if (dtype == 0) {
     const size_t sm = m2_smem<float>();
-    if ((e = cudaFuncSetAttribute(modes_tc_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem((const void*)modes_tc_kernel<float>, (int)sm)) != cudaSuccess) return e;
     modes_tc_kernel<float><<<(unsigned)grid, M2_THREADS, sm, s>>>((const float*)ring, ld, NS, n, first_frame, m,
                                                                   (const double2*)T, nc, (double2*)phi, ldphi, nchunks);
   } else {
     const size_t sm = m2_smem<double>();
-    if ((e = cudaFuncSetAttribute(modes_tc_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)) != cudaSuccess) return e;
+    if ((e = set_max_dyn_smem((const void*)modes_tc_kernel<double>, (int)sm)) != cudaSuccess) return e;
     modes_tc_kernel<double><<<(unsigned)grid, M2_THREADS, sm, s>>>((const double*)ring, ld, NS, n, first_frame, m,
                                                                    (const double2*)T, nc, (double2*)phi, ldphi, nchunks);
   }

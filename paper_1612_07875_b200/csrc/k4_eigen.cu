@@ -1083,6 +1083,7 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
 // L1 lines).  The inherently sequential Francis QR, the eigenvector solves and the background
 // coefficients then run on CTA 0.
 constexpr int K4_CLUSTER = 4;
+constexpr int K4_SMALL_M = 64;                         // single-CTA Jacobi up to this window width
 constexpr int K4_GW = K4_WARPS * K4_CLUSTER;           // warps in the cluster
 constexpr int K4_GT = K4_THREADS * K4_CLUSTER;         // threads in the cluster
 
@@ -1443,6 +1444,44 @@ k4a_kernel(const K4Params p) {
   }
   if (tid == 0) ph[1] = clock64();
 
+  // ---- a5 (small windows, m <= K4_SMALL_M): the whole S fits one CTA's shared memory, so CTA 0
+  // runs the cyclic one-sided Jacobi alone (round-robin tournament of the m columns, one column
+  // pair per half-warp, a CTA barrier per round) instead of the cluster's block tournament, whose
+  // per-round cluster barriers and L2 staging dominate at small m (C1: m = 16).
+  constexpr int EL = kMaxM / 32;
+  int sweeps = 0;
+  bool converged = false;
+  if (m <= K4_SMALL_M) {
+    if (crank == 0) {
+      const int mp = (m + 1) & ~1;
+      double* sA = reinterpret_cast<double*>(k4_smem);       // mp columns x m, column-major
+      for (int e = tid; e < mp * m; e += K4_THREADS) sA[e] = e < m * m ? __ldcg(p.A + e) : 0.0;
+      __syncthreads();
+      const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
+      const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
+      for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
+        int rot = 0;
+        for (int st = 0; st < mp - 1; ++st) {
+          int P = 0, Q = 0;
+          bool act = false;
+          if (hw < mp / 2) {
+            P = rr_player(hw, st, mp);
+            Q = rr_player(mp - 1 - hw, st, mp);
+            act = P < m && Q < m;
+          }
+          if (jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol)) rot = 1;
+          __syncthreads();
+        }
+        ++sweeps;
+        if (!__syncthreads_or(rot)) { converged = true; break; }
+      }
+      for (int e = tid; e < m * m; e += K4_THREADS) p.A[e] = sA[e];
+      if (tid == 0) { p.flags[0] = converged ? 1 : 0; p.flags[1] = sweeps; }
+    }
+    cl_sync();
+    converged = *(volatile int*)(p.flags) != 0;
+    sweeps = *(volatile int*)(p.flags + 1);
+  } else {
   // ---- a5: one-sided (Hestenes) block Jacobi on S.  The m columns form 8 blocks; a block sweep
   // is the round-robin tournament of the 8 blocks (7 rounds).  In each round CTA c of the cluster
   // holds block pair c in shared memory and rotates every column pair that crosses the two
@@ -1452,10 +1491,7 @@ k4a_kernel(const K4Params p) {
   __shared__ volatile int jdone[32];
   const int ehs = m <= 64 ? 4 : m <= 112 ? 7 : m <= 160 ? 10 : m <= 208 ? 13 : kMaxM / 16;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
-  constexpr int EL = kMaxM / 32;
   double* sA = reinterpret_cast<double*>(k4_smem); // 2*bs columns x m, column-major
-  int sweeps = 0;
-  bool converged = false;
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
     int rot = 0;
     for (int rd = 0; rd < 7; ++rd) {
@@ -1544,6 +1580,7 @@ k4a_kernel(const K4Params p) {
     if (__any_sync(0xffffffffu, rot) && lane == 0) atomicOr(p.flags + sweep, 1);
     cl_sync();
     if (*(volatile int*)(p.flags + sweep) == 0) { converged = true; break; }
+  }
   }
   if (tid == 0) ph[2] = clock64();
 
@@ -2171,7 +2208,8 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const long long hs = hs_elems(r_max);
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
-  const size_t c = 2 * (size_t)((m + 7) / 8) * m * sizeof(double);   // Jacobi block pair
+  const size_t c = m <= K4_SMALL_M ? (size_t)((m + 1) & ~1) * m * sizeof(double)   // whole S (small m)
+                                   : 2 * (size_t)((m + 7) / 8) * m * sizeof(double);  // Jacobi block pair
   const size_t d = ((size_t)((r_max + 3) / 4) * r_max + (3 + K4_CLUSTER) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
   // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
   const size_t d2 = (size_t)32 * ((((m > r_max ? m : r_max) + 3) / 4) + r_max) * sizeof(double);
@@ -2193,7 +2231,7 @@ void preload_k4_kernels() {
 
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
   const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
-  cudaError_t e = cudaFuncSetAttribute(k4a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)k4a_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   k4a_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
@@ -2201,13 +2239,14 @@ cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
 
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s) {
   const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
-  cudaError_t e = cudaFuncSetAttribute(k4b_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_max_dyn_smem((const void*)k4b_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   k4b_kernel<<<1, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 int k4_cluster_size() { return K4_CLUSTER; }
+int k4_small_m() { return K4_SMALL_M; }
 
 // ------------------------------------------------------- on-demand eigenvectors and b --------
 __global__ void __launch_bounds__(32) k4_vecs_kernel(const K4VecParams p) {

@@ -195,7 +195,7 @@ cudaError_t launch_pixel_background(const PixBgParams& p, cudaStream_t s) {
   size_t sm_c = (size_t)(p.rows + p.rows / 2) * sizeof(double2);
   const size_t smax = sm_r > sm_c ? sm_r : sm_c;
   if (smax > 48 * 1024) {
-    e = cudaFuncSetAttribute(idct_lines_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax);
+    e = set_max_dyn_smem((const void*)idct_lines_kernel, (int)smax);
     if (e != cudaSuccess) return e;
   }
   idct_lines_kernel<<<3 * p.rows / 2, 256, sm_r, s>>>(p.planes, p.tmp, lr, p.rows, n, p.cols, 1, p.st);

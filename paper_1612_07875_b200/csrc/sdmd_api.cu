@@ -16,6 +16,7 @@
 // The eigen work per rank drops by P, so the pipeline keeps up with P times the frame rate of one
 // GPU.  Local frame index q = t div P selects the worker streams, the workspace and the K4 events.
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 #include <condition_variable>
 #include <cstdio>
 #include <map>
@@ -241,6 +242,15 @@ static int fail_cuda(sdmd_ctx* c, cudaError_t e, const char* what) {
     if (e_ != cudaSuccess) return fail_cuda(c, e_, #call);  \
   } while (0)
 
+// NVTX range over an ABI call (header-only nvtx3: a no-op unless a tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+#define SDMD_NVTX() NvtxRange nvtx_range_(__func__)
+
+static inline bool m_small(int m) { return m <= k4_small_m(); }
+
 static int invalid(sdmd_ctx* c, const char* msg) {
   if (c) c->err = msg;
   return SDMD_E_INVALID;
@@ -422,6 +432,7 @@ int sdmd_nccl_unique_id(uint8_t out[128]) {
 }
 
 int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
+  SDMD_NVTX();
   if (!cfg_in || !out) return SDMD_E_INVALID;
   *out = nullptr;
   const sdmd_config& cfg = *cfg_in;
@@ -495,6 +506,9 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     if (wa > kMaxWorkers) wa = kMaxWorkers;
     if (wa > c->Wa) c->Wa = wa;
   }
+  // small windows (m <= 64: single-CTA Jacobi inside K4a) make K4a short and latency-bound (its
+  // commit wait is a sizeable part): as many cluster streams as single-CTA ones (C1, profiles/r2…)
+  if (m_small(c->cfg.m) && c->Wa < c->W) c->Wa = c->W;
   if (c->Wa + c->W + 2 > 32) c->Wa = 30 - c->W;   // 32 hardware queues
   if (c->Wa < 1) c->Wa = 1;
   if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
@@ -1082,6 +1096,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
 }
 
 int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
+  SDMD_NVTX();
   if (!c || !x || (where != SDMD_HOST && where != SDMD_DEVICE)) return invalid(c, "push_dense: bad argument");
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "push_dense on a sparse context");
   CK(cudaSetDevice(c->dev));
@@ -1110,6 +1125,7 @@ int sdmd_acquire_slot(sdmd_ctx* c, void** dev_ptr) {
 }
 
 int sdmd_commit_slot(sdmd_ctx* c) {
+  SDMD_NVTX();
   if (!c) return SDMD_E_INVALID;
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "commit_slot on a sparse context");
   CK(cudaSetDevice(c->dev));
@@ -1117,6 +1133,7 @@ int sdmd_commit_slot(sdmd_ctx* c) {
 }
 
 int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int where, int32_t dmd_every) {
+  SDMD_NVTX();
   if (!c || !X || k < 1 || (where != SDMD_HOST && where != SDMD_DEVICE))
     return invalid(c, "push_batch: bad argument");
   if (c->cfg.storage != SDMD_DENSE || c->cfg.background) return invalid(c, "push_batch: dense, background-free contexts only");
@@ -1184,6 +1201,7 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
 }
 
 int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double* val, int where) {
+  SDMD_NVTX();
   if (!c || nnz < 0 || (nnz > 0 && (!idx || !val)) || (where != SDMD_HOST && where != SDMD_DEVICE))
     return invalid(c, "push_sparse: bad argument");
   if (c->cfg.storage != SDMD_SPARSE) return invalid(c, "push_sparse on a dense context");
@@ -1226,6 +1244,7 @@ int sdmd_push_sparse(sdmd_ctx* c, int32_t nnz, const int32_t* idx, const double*
 }
 
 int sdmd_init_window(sdmd_ctx* c, const void* Z, int64_t ldz, int where) {
+  SDMD_NVTX();
   if (!c || !Z || ldz < c->cfg.n_local || (where != SDMD_HOST && where != SDMD_DEVICE))
     return invalid(c, "init_window: bad argument");
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "init_window needs dense storage");
@@ -1310,6 +1329,7 @@ int sdmd_join(sdmd_ctx* c) {
 }
 
 int sdmd_sync(sdmd_ctx* c, int64_t* failed_frame) {
+  SDMD_NVTX();
   if (!c) return SDMD_E_INVALID;
   if (failed_frame) *failed_frame = -1;
   CK(cudaSetDevice(c->dev));
@@ -1394,6 +1414,7 @@ static int newest_result(sdmd_ctx* c, K4Result* r) {
 }
 
 int sdmd_get_svd(sdmd_ctx* c, int32_t* r, double* sigma, double* V, int64_t* frame) {
+  SDMD_NVTX();
   if (!c) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   K4Result res{};
@@ -1451,6 +1472,7 @@ static int ensure_vecs(sdmd_ctx* c) {
 }
 
 int sdmd_get_spectrum(sdmd_ctx* c, int32_t* r, double* lambda, double* b, int32_t* idx, int64_t* frame) {
+  SDMD_NVTX();
   if (!c) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   K4Result res{};
@@ -1470,6 +1492,7 @@ int sdmd_get_spectrum(sdmd_ctx* c, int32_t* r, double* lambda, double* b, int32_
 }
 
 int sdmd_get_eigvecs(sdmd_ctx* c, double* W, int32_t* r) {
+  SDMD_NVTX();
   if (!c || !W) return SDMD_E_INVALID;
   CK(cudaSetDevice(c->dev));
   K4Result res{};
@@ -1483,6 +1506,7 @@ int sdmd_get_eigvecs(sdmd_ctx* c, double* W, int32_t* r) {
 }
 
 int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_dev, int64_t ld) {
+  SDMD_NVTX();
   if (!c || !cols || ncols < 1 || !phi_dev || ld < c->cfg.n_local) return invalid(c, "get_modes: bad argument");
 
   CK(cudaSetDevice(c->dev));
@@ -1528,6 +1552,7 @@ int sdmd_get_modes(sdmd_ctx* c, const int32_t* cols, int32_t ncols, double* phi_
 
 int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask, int64_t* frame,
                         int where) {
+  SDMD_NVTX();
   if (!c || (where != SDMD_HOST && where != SDMD_DEVICE && where != SDMD_HOST_ASYNC))
     return SDMD_E_INVALID;
   if (!c->cfg.background) return invalid(c, "background disabled in config");
@@ -1567,6 +1592,7 @@ int sdmd_get_background(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask,
 
 int sdmd_get_background_window(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t* mask, int64_t ld,
                                int64_t* frame) {
+  SDMD_NVTX();
   if (!c || ld < c->cfg.n_local) return invalid(c, "get_background_window: bad argument");
   if (c->cfg.storage != SDMD_DENSE || !c->cfg.dmd || c->cfg.bg_modes > 1)
     return invalid(c, "get_background_window: dense single-mode DMD contexts only");
@@ -1589,6 +1615,7 @@ int sdmd_get_background_window(sdmd_ctx* c, void* lowrank, void* sparse, uint8_t
 }
 
 int sdmd_score_background(sdmd_ctx* c, int64_t frame, const uint8_t* gt, int where) {
+  SDMD_NVTX();
   if (!c || !gt || (where != SDMD_HOST && where != SDMD_DEVICE)) return invalid(c, "score_background: bad argument");
   if (!c->cfg.background) return invalid(c, "score_background: background disabled in config");
   CK(cudaSetDevice(c->dev));

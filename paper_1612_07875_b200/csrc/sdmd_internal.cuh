@@ -10,8 +10,27 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <map>
+#include <mutex>
+#include <utility>
 
 namespace sdmd {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, size increase): the
+// per-push launch paths call this on every launch, and the runtime call is not free on the host
+// (C1's push is host-bound).
+inline cudaError_t set_max_dyn_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> set;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = set[{func, dev}];
+  if (bytes <= have) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 
 constexpr int kMaxM = 256;
 constexpr int kMaxR = 224;
@@ -262,6 +281,7 @@ cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
 size_t k4_smem_bytes(int r_max, int m, int bg_modes);
 int k4_cluster_size();
+int k4_small_m();                  // K4a runs its Jacobi on one CTA up to this window width
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
 cudaError_t launch_k4_singular(const K4SingParams& p, bool vecs, cudaStream_t s);
 constexpr int kSingVecGrid = 16;          // CTAs (one warp each) of the singular-path eigenvectors
