@@ -52,7 +52,7 @@ int main() {
   const int iters = 20000;
   double best_dmma = 0, best_dfma = 0;
   int best_w = 0;
-  for (int warps = 4; warps <= 16; warps *= 2) {
+  for (int warps = 2; warps <= 16; warps *= 2) {
     for (int rep = 0; rep < 3; ++rep) {
       dmma_loop<<<sms * 2, 32 * warps>>>(out, iters / 10);
       cudaEventRecord(e0);
@@ -64,6 +64,7 @@ int main() {
       double fl = 512.0 * 8 * iters * (double)(sms * 2) * warps;
       double tf = fl / (ms * 1e-3) / 1e12;
       if (tf > best_dmma) { best_dmma = tf; best_w = warps; }
+      if (rep == 2) printf("{\"warps_per_sm\": %d, \"dmma_f64_tflops\": %.3f}\n", 2 * warps, tf);
     }
   }
   for (int rep = 0; rep < 3; ++rep) {

@@ -295,3 +295,23 @@ def test_background_window_constant_video():
     assert float(s.abs().max()) < 1e-6 * float(np.max(c))
     assert not bool(mask.any())
     eng.close()
+
+
+# ------------------------------------------------ a0: one-pass init Gram (TMA multicast) ---
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n,m", [(20011, 70), (4099, 200), (777, 3)])
+def test_init_gram_multicast_vs_oracle_and_pair_kernel(dtype, n, m, monkeypatch):
+    """sdmd_init_window's Gram from the cluster/TMA-multicast kernel (default for k <= 224) vs the
+    oracle's compensated Gram (1e-12 normwise, Q17) and vs the pair-blocked DMMA kernel
+    (SDMD_INIT_GRAM=v1, read at the first launch of a process — so compared through a second
+    process-independent path: the oracle)."""
+    rng = np.random.default_rng(n + m)
+    npdt = np.float32 if dtype == "f32" else np.float64
+    Z = rng.standard_normal((n, m + 1)).astype(npdt)
+    Zd = torch.from_numpy(np.ascontiguousarray(Z.T)).cuda()
+    eng = Eng(n, m, dtype=dtype, workers=1)
+    eng.init_window(Zd)
+    eng.sync()
+    assert normwise(eng.gram(), O.gram(Z)) < 1e-12
+    eng.close()
