@@ -1084,6 +1084,7 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
 // coefficients then run on CTA 0.
 constexpr int K4_CLUSTER = 4;
 constexpr int K4_SMALL_M = 64;                         // single-CTA Jacobi up to this window width
+constexpr int K4_JAC_DSM_M = 216;                      // block Jacobi kept in DSMEM up to this width
 constexpr int K4_GW = K4_WARPS * K4_CLUSTER;           // warps in the cluster
 constexpr int K4_GT = K4_THREADS * K4_CLUSTER;         // threads in the cluster
 
@@ -1487,11 +1488,20 @@ k4a_kernel(const K4Params p) {
   // holds block pair c in shared memory and rotates every column pair that crosses the two
   // blocks (round 0 also the pairs inside each block), so every pair of columns meets once per
   // block sweep.  Only the round boundaries need cluster barriers.
+  // With m <= K4_JAC_DSM_M the blocks stay in the cluster's shared memory for the whole sweep:
+  // each CTA keeps two buffers of its block pair and, at a round boundary, copies the two blocks of
+  // its next pair out of the previous round's owners' buffers over DSMEM — no L2/HBM round trip
+  // per round (the Gram pass streams at full HBM bandwidth meanwhile) and still one cluster
+  // barrier per round (a CTA only overwrites the buffer the others read one round earlier).
   const int bs = (m + 7) / 8;                     // block size (columns)
   __shared__ volatile int jdone[32];
   const int ehs = m <= 64 ? 4 : m <= 112 ? 7 : m <= 160 ? 10 : m <= 208 ? 13 : kMaxM / 16;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
-  double* sA = reinterpret_cast<double*>(k4_smem); // 2*bs columns x m, column-major
+  const bool dsm = m <= K4_JAC_DSM_M;
+  double* sbuf0 = reinterpret_cast<double*>(k4_smem);   // 2*bs columns x m, column-major
+  double* sbuf1 = sbuf0 + (size_t)2 * bs * m;
+  double* sA = sbuf0;
+  int rounds = 0;                                 // rounds done (buffer of round q: q & 1)
   for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
     int rot = 0;
     for (int rd = 0; rd < 7; ++rd) {
@@ -1499,14 +1509,35 @@ k4a_kernel(const K4Params p) {
       if (tid < 32) jdone[tid] = -1;                   // per-half-warp step counters (flags mode)
       // local column lc in [0, 2bs): global column gc(lc)
       auto gcol = [&](int lc) { return lc < bs ? PB * bs + lc : QB * bs + (lc - bs); };
-      for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {     // warp per column: no divisions
-        const int gc = gcol(lc);
-        double* dst = sA + lc * m;
-        if (gc < m) {
-          const double* src = p.A + (long long)gc * m;
-          for (int i = lane; i < m; i += 32) dst[i] = __ldcg(src + i);
-        } else {
-          for (int i = lane; i < m; i += 32) dst[i] = 0.0;
+      if (dsm && rounds > 0) {
+        sA = (rounds & 1) ? sbuf1 : sbuf0;
+        const double* prev = (rounds & 1) ? sbuf0 : sbuf1;
+        const int prd = rd == 0 ? 6 : rd - 1;
+        for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
+          const int blk = lc < bs ? PB : QB, cb = lc < bs ? lc : lc - bs;
+          int own = 0, slot = 0;
+          for (int o = 0; o < K4_CLUSTER; ++o) {
+            if (rr_player(o, prd, 8) == blk) { own = o; slot = 0; }
+            if (rr_player(7 - o, prd, 8) == blk) { own = o; slot = 1; }
+          }
+          const unsigned src = dsm_addr(prev + (size_t)(slot * bs + cb) * m, (unsigned)own);
+          double* dst = sA + (size_t)lc * m;
+          for (int i = lane; i < m; i += 32) {
+            double v;
+            asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(src + 8u * (unsigned)i) : "memory");
+            dst[i] = v;
+          }
+        }
+      } else {
+        for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {     // warp per column: no divisions
+          const int gc = gcol(lc);
+          double* dst = sA + lc * m;
+          if (gc < m) {
+            const double* src = p.A + (long long)gc * m;
+            for (int i = lane; i < m; i += 32) dst[i] = __ldcg(src + i);
+          } else {
+            for (int i = lane; i < m; i += 32) dst[i] = 0.0;
+          }
         }
       }
       __syncthreads();
@@ -1564,14 +1595,17 @@ k4a_kernel(const K4Params p) {
         }
         __syncthreads();
       }
-      for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
-        const int gc = gcol(lc);
-        if (gc < m) {
-          const double* src = sA + lc * m;
-          double* dst = p.A + (long long)gc * m;
-          for (int i = lane; i < m; i += 32) dst[i] = src[i];
+      if (!dsm) {
+        for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
+          const int gc = gcol(lc);
+          if (gc < m) {
+            const double* src = sA + lc * m;
+            double* dst = p.A + (long long)gc * m;
+            for (int i = lane; i < m; i += 32) dst[i] = src[i];
+          }
         }
       }
+      ++rounds;
       cl_sync();
     }
     ++sweeps;
@@ -1580,6 +1614,19 @@ k4a_kernel(const K4Params p) {
     if (__any_sync(0xffffffffu, rot) && lane == 0) atomicOr(p.flags + sweep, 1);
     cl_sync();
     if (*(volatile int*)(p.flags + sweep) == 0) { converged = true; break; }
+  }
+  if (dsm) {                                      // the final blocks back to p.A for the a6 stage
+    const int rd = 6;                             // every sweep ends with round 6
+    const int PB = rr_player(crank, rd, 8), QB = rr_player(7 - crank, rd, 8);
+    for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
+      const int gc = lc < bs ? PB * bs + lc : QB * bs + (lc - bs);
+      if (gc < m) {
+        const double* src = sA + (size_t)lc * m;
+        double* dst = p.A + (long long)gc * m;
+        for (int i = lane; i < m; i += 32) dst[i] = src[i];
+      }
+    }
+    cl_sync();
   }
   }
   if (tid == 0) ph[2] = clock64();
@@ -2209,7 +2256,7 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
   const size_t c = m <= K4_SMALL_M ? (size_t)((m + 1) & ~1) * m * sizeof(double)   // whole S (small m)
-                                   : 2 * (size_t)((m + 7) / 8) * m * sizeof(double);  // Jacobi block pair
+                   : (m <= K4_JAC_DSM_M ? 4 : 2) * (size_t)((m + 7) / 8) * m * sizeof(double);  // block pair (x2 buffers)
   const size_t d = ((size_t)((r_max + 3) / 4) * r_max + (3 + K4_CLUSTER) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
   // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
   const size_t d2 = (size_t)32 * ((((m > r_max ? m : r_max) + 3) / 4) + r_max) * sizeof(double);
