@@ -114,12 +114,12 @@ typedef struct sdmd_config {
   int32_t background; /* 1: compute the newest background column every push (fused into the Gram
                        * pass, emitted with a lag of `lag` frames, see sdmd_info); 0: off       */
   int32_t dmd;        /* 1: run the DMD (a5..a10) on every push once the window is full       */
-  int32_t workers;    /* eigen-worker streams for the single-CTA stage, 1..24 (0 → 4); the cluster
-                       * stage uses max(1, workers / 2) streams (min(2·workers, 30 − workers, 20)
-                       * when r_max <= m/4: then the Jacobi stage bounds the rate).  The context uses about
-                       * 1.5·workers + 2 streams: set CUDA_DEVICE_MAX_CONNECTIONS >= that
-                       * (e.g. 32) before CUDA initialises, else streams share hardware queues
-                       * and the eigen stages serialise behind unrelated waits                  */
+  int32_t workers;    /* eigen-worker budget W, 1..24 (0 → 4): the context runs max(2, W/4) single-
+                       * CTA streams (K4b; W/2 with bg_modes > 1) and W/2 four-CTA cluster streams (K4a; W − W/4 for sparse
+                       * storage; min(2W, 30 − W, 20) when r_max <= m/4; W when m <= 64).  About
+                       * W + 2 streams in all: set CUDA_DEVICE_MAX_CONNECTIONS >= that (e.g. 32)
+                       * before CUDA initialises, else streams share hardware queues and the
+                       * eigen stages serialise behind unrelated waits                          */
   int32_t device;     /* CUDA device ordinal                                                   */
   void* stream;       /* cudaStream_t to order work on, or NULL (the ctx creates one)          */
   int32_t rank;       /* this rank, 0..nranks-1                                                 */

@@ -492,10 +492,16 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
         if ((c->cfg.m + l) % 16 == 0) { want = l; break; }
     c->L = c->cfg.lag > 0 ? c->cfg.lag : want;
   }
-  c->Wb = c->W;
-  // K4a (4-CTA cluster, ≈11 ms at m = 200) vs K4b (1 CTA, ≈22 ms): half as many cluster streams
-  // keeps both stages' throughput above one frame per Gram pass (measured)
-  c->Wa = c->W / 2 > 0 ? c->W / 2 : 1;
+  // Since eig(Ã) runs on the K4a cluster, K4b (ordering, inverse iteration, b, c: ≈ 1 ms at
+  // r = 200) needs few streams: Wb = W/4 (at least 2), and the SMs go to the clusters and the Gram
+  // pass (measured sweeps, profiles/r2/r6h…: C3 W = 16 → 8 + 4 streams 4,096 vs 3,383/s with
+  // 10 + 20; C4 W = 6 → 3 + 2, K1 on 134 SMs).  Dense contexts: W/2 cluster streams; sparse ones
+  // (the Gram pass needs few SMs): the rest of the W budget.
+  c->Wb = c->W >= 2 ? (c->W / 4 > 2 ? c->W / 4 : 2) : 1;
+  // a multi-mode background runs one inverse iteration per mode in K4b: keep W/2 streams there
+  if (c->cfg.bg_modes > 1 && c->Wb < c->W / 2) c->Wb = c->W / 2;
+  c->Wa = c->cfg.storage == SDMD_SPARSE ? c->W - c->Wb : c->W / 2;
+  if (c->Wa < 1) c->Wa = 1;
   // r <= m/4 (e.g. C2: m = 150, r = 21): the single-CTA stage (QR of Ã) is light and the cluster
   // stage (Jacobi of the m x m S) bounds the throughput: give it every remaining hardware queue
   // (measured C2: W = 14 with 16 cluster streams 5455 vs W = 20 with 10 cluster streams 3486
@@ -514,6 +520,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
     const int v = std::atoi(ea);
     if (v >= 1 && v <= kMaxWorkers) c->Wa = v;
+  }
+  if (const char* eb = std::getenv("SDMD_WB")) {      // experiment knob: single-CTA workers
+    const int v = std::atoi(eb);
+    if (v >= 1 && v <= kMaxWorkers) c->Wb = v;
   }
   c->NWS = c->L + 4;
   const int m = c->cfg.m;

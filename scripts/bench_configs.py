@@ -156,16 +156,20 @@ def main():
     pool = torch.empty((Pn, vs.n), dtype=torch.float32, device="cuda")
     for t in range(Pn):
         pool[t].copy_(vs.frame(t, device="cuda"))
-    res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, args.workers, background=True,
+    # C3: 16 workers = 8 cluster + 4 single-CTA eigen streams (profiles/r2/r6h…: the Gram pass keeps
+    # 103+ SMs; more clusters starve it, fewer starve K4a)
+    wc3 = min(args.workers, 16)
+    res.append(dense_run("C3", pool, vs.n, 100, "f32", args.frames, wc3, background=True,
                          lag=args.lag))
     print(json.dumps(res[-1]), flush=True)
     # NEXT-2: background from the 4 slowest modes (+ conjugate partner) instead of one
-    res.append(dense_run("C3 (4-mode background)", pool, vs.n, 100, "f32", args.frames, args.workers,
+    res.append(dense_run("C3 (4-mode background)", pool, vs.n, 100, "f32", args.frames, wc3,
                          background=True, lag=args.lag, bg_modes=4))
     print(json.dumps(res[-1]), flush=True)
     del pool
     torch.cuda.empty_cache()
-    # C5: sparse DCT, m = 128
+    # C5: sparse DCT, m = 128; 16 workers = 12 cluster + 4 single-CTA streams (profiles/r2/r6h…)
+    args.workers = min(args.workers, 16)
     res.append(sparse_run(args.frames, args.workers))
     print(json.dumps(res[-1]), flush=True)
     res.append(sparse_run(args.frames, args.workers, host=True))
