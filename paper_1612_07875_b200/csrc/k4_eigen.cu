@@ -2024,12 +2024,14 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   }
   __syncthreads();
 
-  // ---- a10: idx = argmin |log λ| (principal branch), λ = 0 excluded; ties (Q5)
-  if (tid == 0) {
+  // ---- a10: idx = argmin |log λ| (principal branch), λ = 0 excluded; ties (Q5).  Warp 0: each
+  // lane the lexicographic minimum (|log λ|, |arg λ|, Im λ < 0, index) of its strided subset, then
+  // a shuffle reduction with the same order — the result equals the sequential scan's.
+  if (warp == 0) {
     int best = -1;
     double k1 = 0, k2 = 0;
     int k3 = 0;
-    for (int i = 0; i < r; ++i) {
+    for (int i = lane; i < r; i += 32) {
       const double2 l = p.lam[i];
       if (l.x == 0.0 && l.y == 0.0) continue;
       const double lr = log(hypot(l.x, l.y)), li = atan2(l.y, l.x);
@@ -2039,7 +2041,19 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
         best = i; k1 = a1; k2 = a2; k3 = a3;
       }
     }
-    sh_idx = best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const double o1 = __shfl_xor_sync(0xffffffffu, k1, o), o2 = __shfl_xor_sync(0xffffffffu, k2, o);
+      const int o3 = __shfl_xor_sync(0xffffffffu, k3, o);
+      const bool take = ob >= 0 && (best < 0 || o1 < k1 ||
+                        (o1 == k1 && (o2 < k2 || (o2 == k2 && (o3 < k3 || (o3 == k3 && ob < best))))));
+      if (take) { best = ob; k1 = o1; k2 = o2; k3 = o3; }
+    }
+    if (lane == 0) sh_idx = best;
+  }
+  if (tid == 0) {
+    const int best = sh_idx;
     if (best < 0 && sh_status == 0) sh_status = 7;
     // reading Q15: WΛ is singular when some |λ_j| < rank_tol·max|λ|; those
     // modes form a suffix of the sorted λ.  Flag W_SINGULAR; the kept-mode least squares of b
