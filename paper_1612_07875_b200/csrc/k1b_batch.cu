@@ -13,6 +13,15 @@
 // i = 0..m (Alg 1 P:294 per frame, reading Q1/Q2).  Per-CTA partial blocks are reduced in fixed
 // order by the last CTA (bitwise reproducible), which then commits the k columns atomically: a
 // batch containing a non-finite value is rejected as a whole (S:285 extended to batches).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "sdmd_internal.cuh"
 
 namespace sdmd {
@@ -177,6 +186,206 @@ __global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
   }
 }
 
+// ---- K1b with TMA tiles (default): the v1 kernel above moves each stage with ~3.3k 16-byte
+// cp.async per CTA, and at 8 cycles per LDGSTS that issue work, not HBM, bounds it (~0.5 of the
+// HBM rate; 256-byte cp.async.bulk per column was slower still, profiles/r2/r6l…).  Here a producer
+// warp fetches a stage as 2-D TMA boxes of 16 ring slots x 128 bytes of rows (128-byte swizzle:
+// conflict-free DMMA fragment loads) — 2·ceil(U/16) boxes per stage, plus two into a scratch region
+// when a 16-slot group wraps past the ring's last slot (the out-of-range slots of the first box are
+// zero-filled) — completing on the stage's full barrier; the 16 compute warps wait, load fragments,
+// convert, issue DMMA and release the stage on its empty barrier.  Same partial layout, reduction
+// and commit as v1.
+__device__ __forceinline__ void kbt_mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void kbt_mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+               ::"r"((unsigned)__cvta_generic_to_shared(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void kbt_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"((unsigned)__cvta_generic_to_shared(b)) : "memory");
+}
+__device__ __forceinline__ void kbt_mbar_wait(unsigned long long* b, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(b);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "KBTW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra KBTW_%=;\n}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void kbt_tma2d(void* dst, const CUtensorMap* tm, int c0, int c1, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+               ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(tm), "r"(c0), "r"(c1),
+                 "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+
+constexpr int KBT_THREADS = KB_THREADS + 32;                   // + the producer warp
+constexpr int KBT_BOX = 2048;                                  // 16 slots x 128 bytes
+constexpr int KBT_MAXG = (KB_MAXU + 15) / 16;                  // 16-slot groups
+
+template <typename T>
+__global__ void __maxnreg__(96) k1b_tma_kernel(const __grid_constant__ CUtensorMap tm, const K1bParams p) {
+  constexpr int R = 128 / (int)sizeof(T);                       // rows per box (= rows per warp part)
+  constexpr int RS = 2 * R;                                     // rows per stage (two row parts)
+  constexpr int ST = 3;
+  extern __shared__ __align__(1024) unsigned char kbt_raw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)kbt_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ int g_s0[KBT_MAXG];
+  __shared__ __align__(8) unsigned long long full[ST], empty[ST];
+  __shared__ int am_last;
+  if (*(volatile int*)&p.st->status != 0) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = p.m, k = p.k, U = m + k, G = (U + 7) / 8, NG = (U + 15) / 16;
+  const long long F0 = p.f0 - m;
+  for (int g = tid; g < NG; g += KBT_THREADS) g_s0[g] = (int)((F0 + 16LL * g) % p.NS);
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) { kbt_mbar_init(&full[s], 1); kbt_mbar_init(&empty[s], KB_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int wg = -1;                                                  // the group that wraps (at most one)
+  for (int g = 0; g < NG; ++g)
+    if (g_s0[g] + 16 > p.NS) wg = g;
+  const unsigned stage_bytes = (unsigned)(NG + 1) * 2 * KBT_BOX;
+  const long long NT = (p.n + RS - 1) / RS;
+  const long long per = (NT + gridDim.x - 1) / gridDim.x;
+  const long long t0 = (long long)blockIdx.x * per;
+  const long long t1 = t0 + per < NT ? t0 + per : NT;
+  const int nsteps = t1 > t0 ? (int)(t1 - t0) : 0;
+  double acc[KB_GPW][2];
+#pragma unroll
+  for (int g = 0; g < KB_GPW; ++g) acc[g][0] = acc[g][1] = 0.0;
+  const int wr = warp / KB_CSETS, wc = warp % KB_CSETS;
+  if (warp == KB_WARPS) {                                       // producer
+    if (lane == 0) {
+      const unsigned bytes = (unsigned)(NG + (wg >= 0 ? 1 : 0)) * 2 * KBT_BOX;
+      for (int st = 0; st < nsteps; ++st) {
+        const int slot = st % ST;
+        if (st >= ST) kbt_mbar_wait(&empty[slot], (unsigned)(((st / ST) - 1) & 1));
+        kbt_mbar_expect_tx(&full[slot], bytes);
+        const int row0 = (int)((t0 + st) * RS);
+        unsigned char* base = sm + (size_t)slot * stage_bytes;
+        for (int g = 0; g < NG; ++g)
+          for (int rb = 0; rb < 2; ++rb)
+            kbt_tma2d(base + (size_t)(g * 2 + rb) * KBT_BOX, &tm, row0 + rb * R, g_s0[g], &full[slot]);
+        if (wg >= 0)
+          for (int rb = 0; rb < 2; ++rb)
+            kbt_tma2d(base + (size_t)(NG * 2 + rb) * KBT_BOX, &tm, row0 + rb * R, 0, &full[slot]);
+      }
+    }
+  } else {
+    // byte offset (within a stage) of column u's line in this warp's row box, and its swizzle key
+    auto col_off = [&](int u, int& key) -> int {
+      const int g = u >> 4, c = u & 15, s0 = g_s0[g];
+      int region = g, cc = c;
+      if (s0 + c >= p.NS) { region = NG; cc = s0 + c - p.NS; }
+      key = cc & 7;
+      return (region * 2 + wr) * KBT_BOX + cc * 128;
+    };
+    const int jb = lane >> 2, fr = lane & 3;
+    const bool bok = jb < k;
+    int bkey, akey[KB_GPW];
+    const int boff = col_off(m + (bok ? jb : 0), bkey);
+    int aoff[KB_GPW];
+    bool aok[KB_GPW];
+#pragma unroll
+    for (int g = 0; g < KB_GPW; ++g) {
+      const int u = (wc + g * KB_CSETS) * 8 + (lane >> 2);
+      aok[g] = u < U;
+      aoff[g] = col_off(aok[g] ? u : 0, akey[g]);
+    }
+    // element (row rl of the box, line with key) inside the 128-byte swizzled line
+    auto ld = [&](const unsigned char* st_base, int off, int key, int q) -> T {
+      const int rl = 4 * q + fr;
+      const int byte = rl * (int)sizeof(T);
+      return *reinterpret_cast<const T*>(st_base + off + ((((byte >> 4) ^ key)) << 4) + (byte & 15));
+    };
+    for (int st = 0; st < nsteps; ++st) {
+      const int slot = st % ST;
+      kbt_mbar_wait(&full[slot], (unsigned)((st / ST) & 1));
+      const unsigned char* sb = sm + (size_t)slot * stage_bytes;
+#pragma unroll
+      for (int q = 0; q < R / 4; ++q) {
+        const double b = bok ? (double)ld(sb, boff, bkey, q) : 0.0;
+#pragma unroll
+        for (int g = 0; g < KB_GPW; ++g)
+          if (wc + g * KB_CSETS < G) {
+            const double a = aok[g] ? (double)ld(sb, aoff[g], akey[g], q) : 0.0;
+            kb_dmma(acc[g][0], acc[g][1], a, b);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) kbt_mbar_arrive(&empty[slot]);
+    }
+  }
+  const int np = gridDim.x * KB_RHALF;
+  const int pc = blockIdx.x * KB_RHALF + wr;
+  if (warp < KB_WARPS) {
+#pragma unroll
+    for (int g = 0; g < KB_GPW; ++g) {
+      const int grp = wc + g * KB_CSETS;
+      const int u = grp * 8 + (lane >> 2), j = 2 * (lane & 3);
+      if (grp < G && u < U) {
+        if (j < k) p.partials[((long long)u * kMaxBatch + j) * np + pc] = acc[g][0];
+        if (j + 1 < k) p.partials[((long long)u * kMaxBatch + j + 1) * np + pc] = acc[g][1];
+      }
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) am_last = (atomicAdd(&p.st->k1_done, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  for (int o = warp; o < k * (m + 1); o += KB_WARPS + 1) {
+    const int j = o / (m + 1), i = o % (m + 1), u = j + i;
+    const double* pk = p.partials + ((long long)u * kMaxBatch + j) * np;
+    double s = 0.0;
+    for (int b = lane; b < np; b += 32) s += __ldcg(pk + b);
+    s = kb_warp_sum(s);
+    if (lane == 0) p.gout[o] = s;
+  }
+  __syncthreads();
+  if (tid == 0) p.st->k1_done = 0;
+  if (p.do_commit) {
+    __threadfence_block();
+    commit_batch(p.gout, k, m, p.f0, p.ghist, p.NH, p.st);
+  }
+}
+
+// tensor map over the ring (rows x slots), one per (ring, ld, NS, dtype)
+static bool kbt_tensor_map(const K1bParams& p, int dtype, CUtensorMap* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, long long, int, int>, CUtensorMap> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(p.ring, p.ld, p.NS, dtype);
+  auto it = cache.find(key);
+  if (it != cache.end()) { *out = it->second; return true; }
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!enc) return false;
+  const int es = dtype == 0 ? 4 : 8;
+  const cuuint64_t dims[2] = {(cuuint64_t)p.ld, (cuuint64_t)p.NS};
+  const cuuint64_t strides[1] = {(cuuint64_t)p.ld * es};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / es), 16u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  CUtensorMap tm;
+  if (enc(&tm, dtype == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+          const_cast<void*>(p.ring), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  cache[key] = tm;
+  *out = tm;
+  return true;
+}
+
 __global__ void commit_batch_kernel(const K1bParams p) {
   if (*(volatile int*)&p.st->status != 0) return;
   commit_batch(p.gout, p.k, p.m, p.f0, p.ghist, p.NH, p.st);
@@ -185,6 +394,24 @@ __global__ void commit_batch_kernel(const K1bParams p) {
 template <typename T>
 static cudaError_t launch_k1b_t(const K1bParams& p, int grid, cudaStream_t s) {
   using S = KbShape<T>;
+  // measured (profiles/r2/r6m…): the TMA kernel wins while the ring is small (C3 ring 0.85 GB: 0.87
+  // vs 1.26 ms per 8-frame batch; C2: 0.21 vs 0.32 ms) and loses on the 21 GB C4 ring (10.8 vs
+  // 8.1 ms: every 16-slot box touches 16 far-apart 2 MB pages); SDMD_K1B=v1|tma forces one
+  static const int force = [] {
+    const char* e = std::getenv("SDMD_K1B");
+    return !e ? 0 : std::strcmp(e, "v1") == 0 ? 1 : std::strcmp(e, "tma") == 0 ? 2 : 0;
+  }();
+  const double ring_bytes = (double)p.NS * (double)p.ld * (double)sizeof(T);
+  const bool use_tma = force == 2 || (force == 0 && ring_bytes <= 2.0 * (1 << 30));
+  CUtensorMap tm;
+  if (use_tma && kbt_tensor_map(p, sizeof(T) == 4 ? 0 : 1, &tm)) {
+    const int NG = (p.m + p.k + 15) / 16;
+    const int smem = 3 * (NG + 1) * 2 * KBT_BOX + 1024;
+    cudaError_t e = set_max_dyn_smem((const void*)k1b_tma_kernel<T>, smem);
+    if (e != cudaSuccess) return e;
+    k1b_tma_kernel<T><<<grid, KBT_THREADS, smem, s>>>(tm, p);
+    return cudaGetLastError();
+  }
   const int smem = S::ST * (p.m + p.k) * S::LDS * (int)sizeof(T);
   cudaError_t e = set_max_dyn_smem((const void*)k1b_kernel<T>, smem);
   if (e != cudaSuccess) return e;

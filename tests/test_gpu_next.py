@@ -315,3 +315,42 @@ def test_init_gram_multicast_vs_oracle_and_pair_kernel(dtype, n, m, monkeypatch)
     eng.sync()
     assert normwise(eng.gram(), O.gram(Z)) < 1e-12
     eng.close()
+
+
+# ------------------------------------------------ NEXT-1: both K1b kernels ----------------
+
+@pytest.mark.parametrize("kernel", ["tma", "v1"])
+def test_push_batch_kernels_agree_with_oracle(kernel, monkeypatch):
+    """The batched Gram pass through the TMA-tile kernel and through the cp.async kernel
+    (SDMD_K1B, read once per process — so each parametrisation runs in a subprocess) gives the
+    oracle's Gram (1e-12 normwise) on a window that wraps past the ring's last slot."""
+    import subprocess
+    import sys
+    import textwrap
+    code = textwrap.dedent('''
+        import numpy as np, torch, synth
+        from oracle import sdmd_oracle as O
+        from paper_1612_07875_b200 import StreamingDMD
+        rng = np.random.default_rng(7)
+        n, m, k = 5000, 20, 8
+        X = rng.standard_normal((n, 3 * (m + 1) + 5 * k)).astype(np.float32)
+        Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+        eng = StreamingDMD(n, m, dtype="f32", workers=2, batch_max=k)
+        sg = O.StreamingGram(m)
+        t = 0
+        for _ in range(m + 1):
+            eng.push(Xd[t]); sg.push(X[:, t]); t += 1
+        while t + k <= X.shape[1]:
+            eng.push_batch(Xd[t:t + k]); [sg.push(X[:, t + j]) for j in range(k)]; t += k
+        eng.sync()
+        G = eng.gram(); Gr = sg.G
+        d = np.sqrt(np.diag(Gr)); err = float(np.max(np.abs(G - Gr) / np.outer(d, d)))
+        print(err)
+        assert err < 1e-12, err
+    ''')
+    import os
+    env = dict(os.environ, SDMD_K1B=kernel)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
