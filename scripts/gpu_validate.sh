@@ -13,7 +13,7 @@ timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_tests.log 2
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/${TAG}_bench20.json 2> gpurun_out/${TAG}_bench20.err
 timeout 900 python bench.py > gpurun_out/${TAG}_bench_default.json 2> gpurun_out/${TAG}_bench_default.err
-/usr/bin/time -v timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${TAG}_reference.json 2> gpurun_out/${TAG}_reference.err
+{ time timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${TAG}_reference.json ; } 2> gpurun_out/${TAG}_reference.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-name-base demangled \
   -k regex:sdmd -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 20 --warmup 3 --repeats 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_bench.log 2>&1
