@@ -245,6 +245,7 @@ def run_ours(args):
         pool = torch.empty((P, n_loc), dtype=torch.float32, device=dev)
         for t in range(P):
             pool[t].copy_(vs.frame(t, device=dev, row_slice=(b, e)))
+        torch.cuda.synchronize(dev)           # the pool is complete before any READY push
         eng = StreamingDMD(n_loc, M, dtype="f32", background=True, workers=args.workers,
                            device=local, stream=stream, rank=rank, nranks=N, row_begin=b,
                            n_global=n, nccl_uid=uid, lag=args.lag)
@@ -252,13 +253,15 @@ def run_ours(args):
         eng.init_window(pool[: M + 1])
         assert info["lag"] == lag
         t = M + 1
+        # the pool is complete (synchronised above), so its frames are pushed as SDMD_DEVICE_READY:
+        # the ring copy of frame t runs on the copy stream during the Gram pass of frame t-1.
         # pipeline fill (setup, not warm-up): the background of frame t is emitted by the push of
         # frame t + lag, so the first lag pushes after the initial window carry no background pass
         for _ in range(lag):
-            eng.push(pool[t % P])
+            eng.push(pool[t % P], ready=True)
             t += 1
         for _ in range(W):
-            eng.push(pool[t % P])
+            eng.push(pool[t % P], ready=True)
             t += 1
         eng.sync()
         eng.stats(reset=True)
@@ -277,7 +280,7 @@ def run_ours(args):
             ev1 = torch.cuda.Event(enable_timing=True)
             ev0.record(stream)
             for _ in range(K):
-                eng.push(pool[t % P])
+                eng.push(pool[t % P], ready=True)
                 t += 1
             eng.join()
             ev1.record(stream)

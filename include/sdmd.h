@@ -94,7 +94,8 @@ enum sdmd_storage { SDMD_DENSE = 0, SDMD_SPARSE = 1 };
  *                   the self-conjugate columns kx = 0 and kx = grid_cols/2 (even grid_cols)
  *                   counts twice (its omitted conjugate partner), g = Σ w Re(conj(ẑ) x̂)        */
 enum sdmd_basis { SDMD_BASIS_DCT = 0, SDMD_BASIS_FFT = 1, SDMD_BASIS_RFFT = 2 };
-enum sdmd_where { SDMD_HOST = 0, SDMD_DEVICE = 1, SDMD_HOST_ASYNC = 2 /* pinned host, stream-ordered */ };
+enum sdmd_where { SDMD_HOST = 0, SDMD_DEVICE = 1, SDMD_HOST_ASYNC = 2 /* pinned host, stream-ordered */,
+                  SDMD_DEVICE_READY = 3 /* device buffer already complete: sdmd_push_dense only */ };
 
 typedef struct sdmd_ctx sdmd_ctx; /* opaque; owns ALL device state (ring, G history, factors) */
 
@@ -218,7 +219,14 @@ int sdmd_init_window(sdmd_ctx* ctx, const void* Z, int64_t ldz, int where);
 
 /* Push one dense snapshot (n_local values of cfg.dtype).  While fewer than m+1 frames are held
  * the column is appended (warm-up, Q14); afterwards the oldest column is dropped (§3.1).  Work is
- * enqueued asynchronously; see the header notes for the NONFINITE contract. */
+ * enqueued asynchronously; see the header notes for the NONFINITE contract.
+ * where = SDMD_HOST (copied on the context's copy stream, overlapping the previous Gram pass),
+ * SDMD_DEVICE (copied into the ring in ctx-stream order, after the work already queued there —
+ * including the previous Gram pass), or SDMD_DEVICE_READY: a device buffer whose contents are
+ * complete when the call is made (a host-synchronised producer, a static pool); it is copied on
+ * the copy stream like a host frame, so the copy overlaps the previous Gram pass instead of
+ * sitting between two passes.  In every case x must stay unmodified until the ctx stream passes
+ * the push. */
 int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
 
 /* Push one sparse snapshot in an orthonormal coefficient basis (§3.5): nnz pairs,

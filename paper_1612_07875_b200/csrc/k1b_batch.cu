@@ -396,7 +396,9 @@ static cudaError_t launch_k1b_t(const K1bParams& p, int grid, cudaStream_t s) {
   using S = KbShape<T>;
   // measured (profiles/r2/r6m…): the TMA kernel wins while the ring is small (C3 ring 0.85 GB: 0.87
   // vs 1.26 ms per 8-frame batch; C2: 0.21 vs 0.32 ms) and loses on the 21 GB C4 ring (10.8 vs
-  // 8.1 ms: every 16-slot box touches 16 far-apart 2 MB pages); SDMD_K1B=v1|tma forces one
+  // 8.1 ms: every 16-slot box touches 16 far-apart 2 MB pages); SDMD_K1B=v1|tma forces one.
+  // (DMMA fragments loaded straight from the ring — one 16-byte load per lane, 64 contiguous bytes
+  // per column and warp — measured 16.5 ms at C4: profiles/r2/r8k…, rejected)
   static const int force = [] {
     const char* e = std::getenv("SDMD_K1B");
     return !e ? 0 : std::strcmp(e, "v1") == 0 ? 1 : std::strcmp(e, "tma") == 0 ? 2 : 0;

@@ -16,6 +16,7 @@
 // The result c is consumed by a later K1 pass (fused background).  Everything is deterministic
 // (fixed reduction orders, no atomics), so replicated ranks compute bit-identical factors.
 #include <cfloat>
+#include <cstdlib>
 #include "sdmd_internal.cuh"
 
 namespace sdmd {
@@ -1084,6 +1085,7 @@ static __device__ void inverse_iteration(const double* H, const double* Qv, cons
 // coefficients then run on CTA 0.
 constexpr int K4_CLUSTER = 4;
 constexpr int K4_SMALL_M = 64;                         // single-CTA Jacobi up to this window width
+constexpr int K4_SOLO_M = 128;                         // K4a on one CTA (CL = 1) up to this width
 constexpr int K4_JAC_DSM_M = 216;                      // block Jacobi kept in DSMEM up to this width
 constexpr int K4_GW = K4_WARPS * K4_CLUSTER;           // warps in the cluster
 constexpr int K4_GT = K4_THREADS * K4_CLUSTER;         // threads in the cluster
@@ -1171,10 +1173,12 @@ static __device__ __forceinline__ void dsm_st(int* p, unsigned cta, int v) {
   asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(dsm_addr(p, cta)), "r"(v) : "memory");
 }
 
+template <int CL>
 static __device__ int aberth_eigs_cluster(const double* Hg, int r, double* hc, const double2* z0,
                                           int n0, double2* z, double2* zn, int* act, double2* lam_out,
                                           int crank, int tid, int warp, int lane, int* its_out,
                                           int* evals_out) {
+  constexpr int K4_CLUSTER = CL;                             // CTAs sharing the roots
   __shared__ int sh_na, sh_bad;
   __shared__ float prv[kMaxR];                               // |correction| of each root's last step
   if (n0 != r || z0 == nullptr || r < 2) return crank == 0 ? -1 : 1;
@@ -1378,8 +1382,16 @@ static __device__ __noinline__ void k4_tiled_product(int mode, int m, int r, int
     }
 }
 
-__global__ void __cluster_dims__(K4_CLUSTER, 1, 1) __launch_bounds__(K4_THREADS, 1)
+// CL = CTAs per cluster: 4 (the cluster path above), or 1 for windows up to K4_SOLO_M: the whole
+// K4a on one SM (Jacobi with S in shared memory, Ã, Hessenberg and the Aberth iteration on one
+// CTA) — about half the SM-cycles of the 4-CTA cluster per frame at m = 100-128, at a longer
+// latency that the background lag absorbs; more worker streams then run concurrently.
+template <int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(K4_THREADS, 1)
 k4a_kernel(const K4Params p) {
+  constexpr int K4_CLUSTER = CL;
+  constexpr int K4_GW = K4_WARPS * CL;                      // warps in the cluster
+  constexpr int K4_GT = K4_THREADS * CL;                    // threads in the cluster
   extern __shared__ __align__(16) unsigned char k4_smem[];
   __shared__ double mu[kMaxM];
   __shared__ double sig[kMaxM];
@@ -1426,8 +1438,7 @@ k4a_kernel(const K4Params p) {
       double* q0 = reinterpret_cast<double*>(k4_smem);        // [nj][m]: Q0 columns j0..j1
       for (int e = tid; e < nj * m; e += K4_THREADS) {
         const int jj = e / m, i = e % m;
-        int src = i + p.warm_k;
-        src -= (src >= m) ? m : 0;
+        const int src = (i + p.warm_k) % m;                  // any orthogonal Q0 is valid
         q0[e] = __ldcg(p.Vprev + (long long)(j0 + jj) * m + src);
       }
       __syncthreads();
@@ -1452,7 +1463,7 @@ k4a_kernel(const K4Params p) {
   constexpr int EL = kMaxM / 32;
   int sweeps = 0;
   bool converged = false;
-  if (m <= K4_SMALL_M) {
+  if (CL == 1 || m <= K4_SMALL_M) {
     if (crank == 0) {
       const int mp = (m + 1) & ~1;
       double* sA = reinterpret_cast<double*>(k4_smem);       // mp columns x m, column-major
@@ -1460,17 +1471,30 @@ k4a_kernel(const K4Params p) {
       __syncthreads();
       const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
       const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
+      const int np = mp / 2;                                 // column pairs per step (<= 64)
+      const int eh = m <= 64 ? 4 : m <= 112 ? 7 : 8;         // rows per lane: ceil(m / 16)
       for (int sweep = 0; sweep < JACOBI_MAX_SWEEPS; ++sweep) {
         int rot = 0;
         for (int st = 0; st < mp - 1; ++st) {
-          int P = 0, Q = 0;
-          bool act = false;
-          if (hw < mp / 2) {
-            P = rr_player(hw, st, mp);
-            Q = rr_player(mp - 1 - hw, st, mp);
-            act = P < m && Q < m;
+          // pairs hw, hw + 32 (m > 64): every half-warp runs the same number of passes, so the
+          // half-warp shuffles of both halves of a warp stay converged
+          for (int pb = 0; pb < np; pb += 2 * K4_WARPS) {
+            const int pp = pb + hw;
+            int P = 0, Q = 0;
+            bool act = false;
+            if (pp < np) {
+              P = rr_player(pp, st, mp);
+              Q = rr_player(mp - 1 - pp, st, mp);
+              act = P < m && Q < m;
+            }
+            bool r_;
+            switch (eh) {
+              case 4: r_ = jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+              case 7: r_ = jacobi_pair<7>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+              default: r_ = jacobi_pair<8>(sA + P * m, sA + Q * m, m, hl, act, tol); break;
+            }
+            if (r_) rot = 1;
           }
-          if (jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol)) rot = 1;
           __syncthreads();
         }
         ++sweeps;
@@ -1780,13 +1804,18 @@ k4a_kernel(const K4Params p) {
   // G[0:m,1:m+1] is gathered from the Gram history straight into the tiles.
   {
     double* t0 = reinterpret_cast<double*>(k4_smem);
+    // (one call covers at most 64 output rows: 16 warps x 4 rows per thread)
     const int mb = (m + K4_CLUSTER - 1) / K4_CLUSTER;
     const int i0 = crank * mb, ni = max(0, min(m, i0 + mb) - i0);
-    k4_tiled_product(0, m, r, i0, ni, mb, tid, t0, p.ghist, p.NH, p.mh, f, p.Y, p.B, p.H);
+    for (int s0 = 0; s0 < ni; s0 += 64)
+      k4_tiled_product(0, m, r, i0 + s0, min(64, ni - s0), min(64, mb), tid, t0, p.ghist, p.NH, p.mh, f,
+                       p.Y, p.B, p.H);
     cl_sync();                                               // all of B visible cluster-wide
     const int rb = (r + K4_CLUSTER - 1) / K4_CLUSTER;
     const int i1 = crank * rb, n1 = max(0, min(r, i1 + rb) - i1);
-    k4_tiled_product(1, m, r, i1, n1, rb, tid, t0, p.ghist, p.NH, p.mh, f, p.Y, p.B, p.H);
+    for (int s0 = 0; s0 < n1; s0 += 64)
+      k4_tiled_product(1, m, r, i1 + s0, min(64, n1 - s0), min(64, rb), tid, t0, p.ghist, p.NH, p.mh, f,
+                       p.Y, p.B, p.H);
   }
   cl_sync();
   }
@@ -1901,7 +1930,7 @@ k4a_kernel(const K4Params p) {
         double2* zz = reinterpret_cast<double2*>(ms_sh.dense);
         double2* zn = zz + kMaxR;
         int* act = reinterpret_cast<int*>(zn + kMaxR);
-        ab_rc = aberth_eigs_cluster(p.H, r, hs, p.lam_warm, n0, zz, zn, act, lam_raw, crank, tid, warp,
+        ab_rc = aberth_eigs_cluster<CL>(p.H, r, hs, p.lam_warm, n0, zz, zn, act, lam_raw, crank, tid, warp,
                                     lane, &ab_its, &ab_ev);
       }
     }
@@ -2265,15 +2294,16 @@ __global__ void __launch_bounds__(K4_THREADS, 1) k4b_kernel(const K4Params p) {
   }
 }
 
-size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
+size_t k4_smem_bytes(int r_max, int m, int bg_modes, int cl) {
   const long long hs = hs_elems(r_max);
   const size_t a = (size_t)((hs + 1) & ~1LL) * sizeof(double) + (size_t)kMaxR * sizeof(double2);
   const size_t b = 6 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // eigvec scratch (K4b)
-  const size_t c = m <= K4_SMALL_M ? (size_t)((m + 1) & ~1) * m * sizeof(double)   // whole S (small m)
+  const size_t c = (cl == 1 || m <= K4_SMALL_M) ? (size_t)((m + 1) & ~1) * m * sizeof(double)   // whole S
                    : (m <= K4_JAC_DSM_M ? 4 : 2) * (size_t)((m + 7) / 8) * m * sizeof(double);  // block pair (x2 buffers)
-  const size_t d = ((size_t)((r_max + 3) / 4) * r_max + (3 + K4_CLUSTER) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
+  const size_t d = ((size_t)((r_max + cl - 1) / cl) * r_max + (3 + cl) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
   // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
-  const size_t d2 = (size_t)32 * ((((m > r_max ? m : r_max) + 3) / 4) + r_max) * sizeof(double);
+  const int rows2 = ((m > r_max ? m : r_max) + cl - 1) / cl;
+  const size_t d2 = (size_t)32 * ((rows2 < 64 ? rows2 : 64) + r_max) * sizeof(double);
   // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
   const size_t b3 = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // per mode
   const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b3 + (size_t)m * sizeof(double2)) : 0;
@@ -2286,27 +2316,40 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes) {
 
 void preload_k4_kernels() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, k4a_kernel);
+  cudaFuncGetAttributes(&a, k4a_kernel<K4_CLUSTER>);
+  cudaFuncGetAttributes(&a, k4a_kernel<1>);
   cudaFuncGetAttributes(&a, k4b_kernel);
 }
 
-cudaError_t launch_k4a(const K4Params& p, cudaStream_t s) {
-  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
-  cudaError_t e = set_max_dyn_smem((const void*)k4a_kernel, (int)smem);
+cudaError_t launch_k4a(const K4Params& p, cudaStream_t s, int cl) {
+  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes, cl);
+  const void* fn = cl == 1 ? (const void*)k4a_kernel<1> : (const void*)k4a_kernel<K4_CLUSTER>;
+  cudaError_t e = set_max_dyn_smem(fn, (int)smem);
   if (e != cudaSuccess) return e;
-  k4a_kernel<<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
+  if (cl == 1) k4a_kernel<1><<<1, K4_THREADS, smem, s>>>(p);
+  else k4a_kernel<K4_CLUSTER><<<K4_CLUSTER, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s) {
-  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes);
+  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes, K4_CLUSTER);
   cudaError_t e = set_max_dyn_smem((const void*)k4b_kernel, (int)smem);
   if (e != cudaSuccess) return e;
   k4b_kernel<<<1, K4_THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
-int k4_cluster_size() { return K4_CLUSTER; }
+// CTAs per K4a launch: one for dense windows with K4_SMALL_M < m <= K4_SOLO_M (the Gram pass needs
+// the SMs: about half the K4a SM-cycles of the cluster, at a latency the background lag absorbs),
+// else the 4-CTA cluster (sparse contexts are eigen-bound and latency-bound by the stream count;
+// small windows are launch-bound).  SDMD_K4_CL=1|4 overrides (A/B).
+int k4_cluster_size(int m, bool sparse) {
+  const char* ev = std::getenv("SDMD_K4_CL");
+  const int env = ev ? std::atoi(ev) : 0;
+  if (env == 4 || m > K4_SOLO_M) return K4_CLUSTER;
+  if (env == 1) return 1;
+  return (!sparse && m > K4_SMALL_M) ? 1 : K4_CLUSTER;
+}
 int k4_small_m() { return K4_SMALL_M; }
 
 // ------------------------------------------------------- on-demand eigenvectors and b --------

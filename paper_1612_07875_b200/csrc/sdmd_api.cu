@@ -102,7 +102,7 @@ constexpr int kRingSpare = 6;
 
 // Per-frame eigen workspace (K4a writes the factors, K4b reads them); indexed by frame mod NWS so
 // that K4a of a later frame never overwrites a workspace whose K4b is still pending.
-constexpr int kMaxWS = kMaxLag + 4;      // per-frame eigen workspaces (NWS = lag + 4)
+constexpr int kMaxWS = kMaxLag + 4 + kMaxWorkers;   // per-frame eigen workspaces (NWS = lag + 4 + Wa)
 struct Workspace {
   double *A = nullptr, *Gxy = nullptr, *V = nullptr, *sigma = nullptr, *Y = nullptr, *B = nullptr;
   double *H = nullptr, *Qv = nullptr, *tau = nullptr, *alpha1 = nullptr;
@@ -122,6 +122,7 @@ struct sdmd_ctx {
   bool own_stream = false;
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
   int k1b_grid = 148;                   // CTAs of the batched Gram pass (K1b)
+  int k4cl = 4;                         // CTAs per K4a launch (k4_cluster_size(m))
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
   int atilde_v1 = 0;                    // SDMD_ATILDE=v1 selects the untiled Ã stage of K4a (A/B)
@@ -500,7 +501,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   c->Wb = c->W >= 2 ? (c->W / 4 > 2 ? c->W / 4 : 2) : 1;
   // a multi-mode background runs one inverse iteration per mode in K4b: keep W/2 streams there
   if (c->cfg.bg_modes > 1 && c->Wb < c->W / 2) c->Wb = c->W / 2;
-  c->Wa = c->cfg.storage == SDMD_SPARSE ? c->W - c->Wb : c->W / 2;
+  // sparse contexts: the Gram pass needs few SMs and the rate is the number of K4a clusters in
+  // flight over their latency, so every hardware queue left (C5 W = 16: 24 + 4 streams, 6,200 vs
+  // 4,270 snapshots/s with 16 + 4, profiles/r2/r8…)
+  c->Wa = c->cfg.storage == SDMD_SPARSE ? (c->W >= 8 ? 29 - c->Wb : c->W - c->Wb) : c->W / 2;
   if (c->Wa < 1) c->Wa = 1;
   // r <= m/4 (e.g. C2: m = 150, r = 21): the single-CTA stage (QR of Ã) is light and the cluster
   // stage (Jacobi of the m x m S) bounds the throughput: give it every remaining hardware queue
@@ -515,7 +519,13 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // small windows (m <= 64: single-CTA Jacobi inside K4a) make K4a short and latency-bound (its
   // commit wait is a sizeable part): as many cluster streams as single-CTA ones (C1, profiles/r2…)
   if (m_small(c->cfg.m) && c->Wa < c->W) c->Wa = c->W;
-  if (c->Wa + c->W + 2 > 32) c->Wa = 30 - c->W;   // 32 hardware queues
+  // K4a on one CTA (dense, 64 < m <= 128): about half the SM-cycles of the cluster per frame at
+  // about twice its latency, so more streams (the background lag covers the latency; C3 W = 16:
+  // 20 + 4 streams, profiles/r2/r8…)
+  c->k4cl = k4_cluster_size(c->cfg.m, c->cfg.storage == SDMD_SPARSE);
+  if (c->k4cl == 1 && !m_small(c->cfg.m) && c->Wa < c->W + c->W / 4) c->Wa = c->W + c->W / 4;
+  if (c->Wa > kMaxWorkers) c->Wa = kMaxWorkers;
+  if (c->Wa + c->Wb + 3 > 32) c->Wa = 29 - c->Wb;   // 32 hardware queues (+ ctx, copy, d2h)
   if (c->Wa < 1) c->Wa = 1;
   if (const char* ea = std::getenv("SDMD_WA")) {      // experiment knob: cluster workers
     const int v = std::atoi(ea);
@@ -525,7 +535,9 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     const int v = std::atoi(eb);
     if (v >= 1 && v <= kMaxWorkers) c->Wb = v;
   }
-  c->NWS = c->L + 4;
+  // workspaces: the frames in flight (lag + 4) plus the Wa frames whose V a later frame of the
+  // same cluster stream reads as its warm start (enqueue_k4 orders reuse after that read)
+  c->NWS = c->L + 4 + c->Wa;
   const int m = c->cfg.m;
   c->NS = c->cfg.background ? m + c->L + 1 : m + 2;
   if (c->NS < m + c->cfg.batch_max + 1) c->NS = m + c->cfg.batch_max + 1;   // union of a batch
@@ -565,7 +577,7 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     if (const char* ew = std::getenv("SDMD_K1_WAVES")) waves = std::atoi(ew);
     if (waves < 0) waves = 0;
     if (waves > kK1MaxWaves) waves = kK1MaxWaves;
-    const int free_sms = c->nsm - c->Wa * k4_cluster_size() - c->Wb;
+    const int free_sms = c->nsm - c->Wa * c->k4cl - c->Wb;
     if (waves == 0 && free_sms < c->nsm / 2) waves = 8;
     c->k1_grid = !c->cfg.dmd ? c->nsm : waves > 0 ? c->nsm * waves : free_sms;
   }
@@ -847,7 +859,8 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.atilde_v1 = c->atilde_v1;
   // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa·P)
   const long long fp = f - (long long)c->Wa * c->P;
-  if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m) {
+  // (only while the two windows overlap: Wa·P < m)
+  if (c->warm && c->Wa < c->NWS && fp >= c->cfg.m && f - fp < p.m) {
     const Workspace& kp = ws_of(c, fp);
     p.Vprev = kp.V; p.res_prev = kp.res; p.warm_k = (int)(f - fp);
   }
@@ -875,7 +888,7 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
   const K4Params p = k4_params(c, t);
   std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
   if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
-  if ((e = launch_k4a(p, A)) != cudaSuccess) return e;
+  if ((e = launch_k4a(p, A, c->k4cl)) != cudaSuccess) return e;
   if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); c->tl.push_back({t, 1, ka.first, ka.second}); }
   if ((e = cudaEventRecord(c->ev_a[q % kEvents], A)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(B, c->ev_a[q % kEvents], 0)) != cudaSuccess) return e;
@@ -1107,16 +1120,19 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
 
 int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
   SDMD_NVTX();
-  if (!c || !x || (where != SDMD_HOST && where != SDMD_DEVICE)) return invalid(c, "push_dense: bad argument");
+  if (!c || !x || (where != SDMD_HOST && where != SDMD_DEVICE && where != SDMD_DEVICE_READY))
+    return invalid(c, "push_dense: bad argument");
   if (c->cfg.storage != SDMD_DENSE) return invalid(c, "push_dense on a sparse context");
   CK(cudaSetDevice(c->dev));
   const long long t = c->frames;
   if (int g = ring_guard(c, t)) return g;
   char* dst = (char*)c->ring + (size_t)(t % c->NS) * c->ld * c->es;
-  if (where == SDMD_HOST) {
-    // H2D on the copy stream so it overlaps K1(t-1): slot t mod NS was last read by K1(t-2)
+  if (where != SDMD_DEVICE) {
+    // H2D (or a ready D2D) on the copy stream so it overlaps K1(t-1): slot t mod NS was last read
+    // by K1(t-2) at the latest (kRingSpare slots of margin)
     if (t >= 2) CK(cudaStreamWaitEvent(c->copy_stream, c->ev_k1[(t - 2) % kEvents], 0));
-    CK(cudaMemcpyAsync(dst, x, c->cfg.n_local * c->es, cudaMemcpyHostToDevice, c->copy_stream));
+    CK(cudaMemcpyAsync(dst, x, c->cfg.n_local * c->es,
+                       where == SDMD_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->copy_stream));
     CK(cudaEventRecord(c->ev_copy[t % kEvents], c->copy_stream));
     CK(cudaStreamWaitEvent(c->stream, c->ev_copy[t % kEvents], 0));
   } else {

@@ -277,10 +277,10 @@ size_t k1b_partials_elems(int grid);
 cudaError_t launch_k3(const K3Params& p, cudaStream_t s);
 cudaError_t launch_sparse_nnz_checked(const int* idx, int nnz, long long lo, long long hi,
                                       int* nnz_slot, cudaStream_t s);
-cudaError_t launch_k4a(const K4Params& p, cudaStream_t s);
+cudaError_t launch_k4a(const K4Params& p, cudaStream_t s, int cl);   // cl: k4_cluster_size(m)
 cudaError_t launch_k4b(const K4Params& p, cudaStream_t s);
-size_t k4_smem_bytes(int r_max, int m, int bg_modes);
-int k4_cluster_size();
+size_t k4_smem_bytes(int r_max, int m, int bg_modes, int cl);
+int k4_cluster_size(int m, bool sparse);   // CTAs per K4a launch (1 or 4)
 int k4_small_m();                  // K4a runs its Jacobi on one CTA up to this window width
 cudaError_t launch_k4_vecs(const K4VecParams& p, int count, cudaStream_t s);
 cudaError_t launch_k4_singular(const K4SingParams& p, bool vecs, cudaStream_t s);

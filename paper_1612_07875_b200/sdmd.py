@@ -21,7 +21,7 @@ E_NO_CONVERGENCE, W_SINGULAR, E_NO_VIABLE_MODE, E_CUDA, E_NCCL, E_OOM, E_STATE =
 F32, F64 = 0, 1
 DENSE, SPARSE = 0, 1
 BASIS_DCT, BASIS_FFT, BASIS_RFFT = 0, 1, 2
-HOST, DEVICE, HOST_ASYNC = 0, 1, 2
+HOST, DEVICE, HOST_ASYNC, DEVICE_READY = 0, 1, 2, 3
 MAX_M, MAX_R = 256, 224
 
 # every symbol include/sdmd.h declares (checked by tests/test_abi.py)
@@ -311,8 +311,12 @@ class StreamingDMD:
         return self._check(lib().sdmd_push_batch(self.h, k, p, ld, where,
                                                  1 if dmd_every else 0), "push_batch")
 
-    def push(self, x):
+    def push(self, x, ready: bool = False):
+        """One dense snapshot.  ready=True (CUDA tensors): the tensor's contents are complete now
+        (SDMD_DEVICE_READY: copied on the copy stream, overlapping the previous Gram pass)."""
         x, p, where = _checked(x, self.np_dtype, self.n, "push")
+        if ready and where == DEVICE:
+            where = DEVICE_READY
         self._pending.append(x)
         return self._check(lib().sdmd_push_dense(self.h, p, where), "push_dense")
 

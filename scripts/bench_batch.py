@@ -80,7 +80,9 @@ def main():
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--workers", type=int, default=8)
     ap.add_argument("--only", default="")
+    ap.add_argument("--modes", default="single,batch,catchup")
     a = ap.parse_args()
+    modes = tuple(a.modes.split(","))
     res = []
     if not a.only or a.only == "C4":
         vs = synth.video_config("C4")
@@ -88,7 +90,7 @@ def main():
         pool = torch.empty((Pn, vs.n), dtype=torch.float32, device="cuda")
         for t in range(Pn):
             pool[t].copy_(vs.frame(t, device="cuda"))
-        for mode in ("single", "batch", "catchup"):
+        for mode in modes:
             res.append(measure("C4", pool, vs.n, 200, "f32", a.frames, a.k, mode, a.workers))
         del pool
         torch.cuda.empty_cache()
@@ -97,21 +99,21 @@ def main():
         pool = torch.empty((300, vs.n), dtype=torch.float32, device="cuda")
         for t in range(300):
             pool[t].copy_(vs.frame(t, device="cuda"))
-        for mode in ("single", "batch", "catchup"):
+        for mode in modes:
             res.append(measure("C3 (no background)", pool, vs.n, 100, "f32", a.frames, a.k, mode, 16))
         del pool
     if not a.only or a.only == "C1":
         pm = synth.planted_c1()
         X = pm.frames(0, 17 + 400)
         pool = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
-        for mode in ("single", "batch", "catchup"):
+        for mode in modes:
             res.append(measure("C1", pool, pm.n, 16, "f64", a.frames, a.k, mode, 4))
         del pool
     if not a.only or a.only == "C2":
         cw = synth.cylinder_wake()
         Xc = cw.frames(0, 300)
         pool = torch.from_numpy(np.ascontiguousarray(Xc.T)).cuda()
-        for mode in ("single", "batch", "catchup"):
+        for mode in modes:
             res.append(measure("C2", pool, cw.n, 150, "f64", a.frames, a.k, mode, 16, r_max=21))
 
 

@@ -43,6 +43,11 @@ def timed(eng, push, K):
     e1.synchronize()
     eng.sync()
     ms = e0.elapsed_time(e1)
+    if os.environ.get("SDMD_TL_OUT"):        # device timeline of the timed region (scripts/tl_view.py)
+        np.save(os.environ["SDMD_TL_OUT"], eng.timeline())
+        d = eng.frame_diag()                  # K4 phase cycles of the newest frame, in the pipeline
+        print(json.dumps({"diag": {k: d[k] for k in ("frame", "sweeps", "aberth_its", "cycles",
+                                                     "commit_wait")}}), flush=True)
     st = eng.stats(reset=True)
     eng.set_timing(False)
     return ms, st

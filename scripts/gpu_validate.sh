@@ -20,3 +20,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --kernel-n
 timeout 600 python scripts/diag_k4.py 100 128 200 > gpurun_out/${TAG}_diag_k4.jsonl 2>&1
 timeout 1800 python scripts/bench_configs.py --frames 500 --workers 20 --out gpurun_out/${TAG}_configs.md \
   > gpurun_out/${TAG}_configs.jsonl 2>&1
+timeout 600 python scripts/score_stream.py --config C3 --frames 400 --out gpurun_out/${TAG}_score_c3.json \
+  > gpurun_out/${TAG}_score_c3.log 2>&1

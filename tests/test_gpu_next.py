@@ -319,11 +319,12 @@ def test_init_gram_multicast_vs_oracle_and_pair_kernel(dtype, n, m, monkeypatch)
 
 # ------------------------------------------------ NEXT-1: both K1b kernels ----------------
 
-@pytest.mark.parametrize("kernel", ["tma", "v1"])
-def test_push_batch_kernels_agree_with_oracle(kernel, monkeypatch):
+@pytest.mark.parametrize("kernel,dtype", [("tma", "f32"), ("v1", "f32"), ("tma", "f64"), ("v1", "f64")])
+def test_push_batch_kernels_agree_with_oracle(kernel, dtype, monkeypatch):
     """The batched Gram pass through the TMA-tile kernel and through the cp.async kernel
     (SDMD_K1B, read once per process — so each parametrisation runs in a subprocess) gives the
-    oracle's Gram (1e-12 normwise) on a window that wraps past the ring's last slot."""
+    oracle's Gram (1e-12 normwise) on a window that wraps past the ring's last slot, with a ragged
+    row tail (n = 5000), for fp32 and fp64 storage."""
     import subprocess
     import sys
     import textwrap
@@ -333,9 +334,10 @@ def test_push_batch_kernels_agree_with_oracle(kernel, monkeypatch):
         from paper_1612_07875_b200 import StreamingDMD
         rng = np.random.default_rng(7)
         n, m, k = 5000, 20, 8
-        X = rng.standard_normal((n, 3 * (m + 1) + 5 * k)).astype(np.float32)
+        dt = "DTYPE"
+        X = rng.standard_normal((n, 3 * (m + 1) + 5 * k)).astype(np.float32 if dt == "f32" else np.float64)
         Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
-        eng = StreamingDMD(n, m, dtype="f32", workers=2, batch_max=k)
+        eng = StreamingDMD(n, m, dtype=dt, workers=2, batch_max=k)
         sg = O.StreamingGram(m)
         t = 0
         for _ in range(m + 1):
@@ -349,6 +351,7 @@ def test_push_batch_kernels_agree_with_oracle(kernel, monkeypatch):
         assert err < 1e-12, err
     ''')
     import os
+    code = code.replace("DTYPE", dtype)
     env = dict(os.environ, SDMD_K1B=kernel)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,

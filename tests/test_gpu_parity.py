@@ -213,6 +213,38 @@ def test_host_input_and_zero_copy_slot():
     eng.close()
 
 
+def test_device_ready_pushes_with_background_vs_oracle():
+    """SDMD_DEVICE_READY pushes (ring copies on the copy stream, overlapping the previous Gram
+    pass) mixed with ordered DEVICE and HOST pushes: the Gram and the fused background equal the
+    oracle's, frame by frame, across several ring wraps."""
+    vs = synth.video_config("C3s")
+    m, T = 12, 60
+    frames = vs.frames(0, T).numpy()
+    pool = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    torch.cuda.synchronize()
+    eng = Eng(vs.n, m, dtype="f32", background=True, workers=2)
+    lag = eng.info()["lag"]
+    ref = O.StreamingDMD(m, background=True)
+    outs = {}
+    for t in range(T):
+        if t % 3 == 2:
+            eng.push(np.ascontiguousarray(frames[:, t]))
+        else:
+            eng.push(pool[t], ready=(t % 3 == 0))
+        o = ref.push(frames[:, t].astype(np.float64))
+        if o is not None:
+            outs[t] = o
+        fb = t - lag
+        if fb >= m + 1 and t % 4 == 0:
+            low, sp_, mask, f = eng.background()
+            assert f == fb
+            lr = outs[fb]["lowrank"]
+            assert np.max(np.abs(low - lr)) / np.max(np.abs(lr)) < 1e-4, t
+    eng.sync()
+    assert normwise(eng.gram(), ref.gram.G) < 1e-12
+    eng.close()
+
+
 # ------------------------------------------------------------------------------ C2 --------
 
 def test_c2_wake_fp64_rank21():
