@@ -54,22 +54,23 @@ def timed(eng, push, K):
 
 
 def dense_run(name, frames_dev, n, m, dtype, K, workers, background=False, r_max=0, lag=0, bg_modes=0,
-              modes_every_frame=False):
+              modes_every_frame=False, dmd=True):
     P = frames_dev.shape[0]
+    torch.cuda.synchronize()             # the pool is complete: its frames are pushed as READY
     eng = StreamingDMD(n, m, dtype=dtype, background=background, workers=workers, r_max=r_max,
-                       lag=lag, bg_modes=bg_modes, modes_every_frame=modes_every_frame)
+                       lag=lag, bg_modes=bg_modes, modes_every_frame=modes_every_frame, dmd=dmd)
     eng.init_window(frames_dev[: m + 1])
     t = m + 1
     for _ in range(2 * (m + 1)):
-        eng.push(frames_dev[t % P])
+        eng.push(frames_dev[t % P], ready=True)
         t += 1
     base = t
 
     def push(j):
-        eng.push(frames_dev[(base + j) % P])
+        eng.push(frames_dev[(base + j) % P], ready=True)
 
     ms, st = timed(eng, push, K)
-    sp = eng.spectrum()
+    sp = eng.spectrum() if dmd else {"r": None, "idx": None}
     es = 4 if dtype == "f32" else 8
     k1 = st["k1_ms"] / max(1, st["k1_launches"])
     alg = (m + 1) * n * es + (9 * n if background else 0)
