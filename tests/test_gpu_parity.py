@@ -1103,6 +1103,45 @@ def test_noisy_video_full_rank_spectrum(m):
     eng.close()
 
 
+@pytest.mark.parametrize("m", [65, 128])
+@pytest.mark.parametrize("cl", ["1", "4"])
+def test_k4a_one_cta_and_cluster_vs_oracle(m, cl, monkeypatch):
+    """K4a on one CTA (the default for dense 64 < m <= 128: whole S in shared memory, Ã in 64-row
+    chunks, one-CTA Hessenberg and Aberth) and on the 4-CTA cluster (SDMD_K4_CL=4, read at create)
+    give the oracle's SVD and spectrum on a noisy full-rank video window at both ends of the
+    one-CTA range, every window of the stream (warm starts included), and the same fused
+    background: σ 1e-10 relative (σ/σ1 >= 1e-4), λ_idx 1e-9, all λ 1e-7 (assignment), lowrank 1e-4."""
+    monkeypatch.setenv("SDMD_K4_CL", cl)
+    vs = synth.video_config("C3s")
+    T = m + 12
+    frames = vs.frames(0, T).numpy()
+    Xd = torch.from_numpy(np.ascontiguousarray(frames.T)).cuda()
+    eng = Eng(vs.n, m, dtype="f32", workers=3, background=True)
+    lag = eng.info()["lag"]
+    ref = O.StreamingDMD(m, background=True)
+    outs = {}
+    for t in range(T):
+        eng.push(Xd[t])
+        o = ref.push(frames[:, t])
+        if o is not None:
+            outs[t] = o
+        if t >= m + 2 and t % 3 == 0:
+            eng.sync()
+            out = ref.last
+            sp = eng.spectrum()
+            assert sp["frame"] == t and sp["r"] == out["r"]
+            assert abs(sp["lam"][sp["idx"]] - out["lam"][out["idx"]]) < 1e-9, t
+            assert match(sp["lam"], out["lam"])[0] < 1e-7, t
+            sv = eng.svd(with_V=False)
+            keep = out["sigma"] / out["sigma"][0] >= 1e-4
+            assert np.max(np.abs(sv["sigma"][keep] - out["sigma"][keep]) / out["sigma"][keep]) < 1e-10
+    eng.sync()
+    low, sp_, mask, fb = eng.background()
+    lr = outs[fb]["lowrank"]
+    assert np.max(np.abs(low - lr)) / np.max(np.abs(lr)) < 1e-4
+    eng.close()
+
+
 def test_modes_every_frame_matches_on_demand_and_oracle():
     """NEXT-2 "full Φ every frame": with modes_every_frame the worker stream computes every
     frame's modes (all eigenvectors, then K2); get_modes of the newest frame must equal the
