@@ -186,9 +186,10 @@ __global__ void __launch_bounds__(KB_THREADS, 1) k1b_kernel(const K1bParams p) {
   }
 }
 
-// ---- K1b with TMA tiles (default): the v1 kernel above moves each stage with ~3.3k 16-byte
-// cp.async per CTA, and at 8 cycles per LDGSTS that issue work, not HBM, bounds it (~0.5 of the
-// HBM rate; 256-byte cp.async.bulk per column was slower still, profiles/r2/r6l…).  Here a producer
+// ---- K1b with TMA tiles (default for rings <= 2 GB): the v1 kernel above moves each stage with
+// ~3.3k 16-byte cp.async per CTA and reaches ~0.5 of the HBM rate (ncu at C4: the DMMA sub-pipe is
+// the limiter, 54.5 % active under math-pipe throttle, profiles/r2/k1bn…; 256-byte cp.async.bulk
+// per column was slower still, profiles/r2/r6l…).  Here a producer
 // warp fetches a stage as 2-D TMA boxes of 16 ring slots x 128 bytes of rows (128-byte swizzle:
 // conflict-free DMMA fragment loads) — 2·ceil(U/16) boxes per stage, plus two into a scratch region
 // when a 16-slot group wraps past the ring's last slot (the out-of-range slots of the first box are
