@@ -1382,6 +1382,117 @@ static __device__ __noinline__ void k4_tiled_product(int mode, int m, int r, int
     }
 }
 
+// C[i][j] = Σ_{k<K} X(i,k)·Y(k,j) for rows i in [i0, i0+ni) (ni <= 64) and all N <= kMaxR columns,
+// tiled through shared memory t0 (32 x (64 + N) doubles); X, Y element accessors, st(i, j, v) the
+// store.  CTA-wide (K4_THREADS threads: 16 row groups x 32 column lanes, 4 x 7 outputs each).
+template <class FX, class FY, class FS>
+static __device__ __forceinline__ void k4_gemm_rows(int K, int N, int i0, int ni, int tid, double* t0,
+                                                    FX X, FY Y, FS st) {
+  constexpr int KC = 32, RA = 4, RB = (kMaxR + 31) / 32, MB = 64;
+  const int ti = tid >> 5, tj = tid & 31;
+  double* As = t0;                                           // [KC][MB]
+  double* Bs = t0 + KC * MB;                                 // [KC][N]
+  double acc[RA][RB];
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int nk = min(KC, K - k0);
+    for (int e = tid; e < KC * MB; e += K4_THREADS) {
+      const int ii = e / KC, kk = e % KC;
+      As[kk * MB + ii] = (kk < nk && ii < ni) ? X(i0 + ii, k0 + kk) : 0.0;
+    }
+    for (int e = tid; e < KC * N; e += K4_THREADS) {
+      const int j = e / KC, kk = e % KC;
+      Bs[kk * N + j] = kk < nk ? Y(k0 + kk, j) : 0.0;
+    }
+    __syncthreads();
+    for (int kk = 0; kk < nk; ++kk) {
+      double g[RA], y[RB];
+#pragma unroll
+      for (int a = 0; a < RA; ++a) g[a] = As[kk * MB + ti + 16 * a];
+#pragma unroll
+      for (int b = 0; b < RB; ++b) y[b] = (tj + 32 * b < N) ? Bs[kk * N + tj + 32 * b] : 0.0;
+#pragma unroll
+      for (int a = 0; a < RA; ++a)
+#pragma unroll
+        for (int b = 0; b < RB; ++b) acc[a][b] = fma(g[a], y[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < RA; ++a)
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+      const int ii = ti + 16 * a, j = tj + 32 * b;
+      if (ii < ni && j < N) st(i0 + ii, j, acc[a][b]);
+    }
+}
+
+// Pivoted Cholesky (largest remaining diagonal first, lowest index on ties) of the symmetric
+// positive semidefinite Sw (column-major m x m in Ag), left-looking, rows kept in the ORIGINAL
+// column order: step k writes R[k][j] to Rg[k*m + j], so that RᵀR = Sw without a permutation.
+// Stops at the first non-positive pivot (the numerical null space); the remaining rows are zero.
+// One CTA; returns the number of steps taken.
+static __device__ __noinline__ int k4_pchol(const double* Ag, double* Rg, int m, int tid, int warp, int lane) {
+  __shared__ double dg[kMaxM];
+  __shared__ double rp[kMaxM];                               // R[0..k-1][piv] of the current step
+  __shared__ unsigned char used[kMaxM];
+  __shared__ double wb[K4_WARPS];
+  __shared__ int wi[K4_WARPS];
+  __shared__ int sh_piv;
+  __shared__ double sh_d;
+  for (int j = tid; j < m; j += K4_THREADS) { dg[j] = __ldcg(Ag + (long long)j * m + j); used[j] = 0; }
+  __syncthreads();
+  int k = 0;
+  for (; k < m; ++k) {
+    double b = -INFINITY;
+    int bi = m;
+    for (int j = tid; j < m; j += K4_THREADS)
+      if (!used[j] && dg[j] > b) { b = dg[j]; bi = j; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > b || (ob == b && oi < bi)) { b = ob; bi = oi; }
+    }
+    if (lane == 0) { wb[warp] = b; wi[warp] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double bb = wb[0];
+      int ii = wi[0];
+      for (int w = 1; w < K4_WARPS; ++w)
+        if (wb[w] > bb || (wb[w] == bb && wi[w] < ii)) { bb = wb[w]; ii = wi[w]; }
+      sh_piv = ii;
+      sh_d = bb;
+    }
+    __syncthreads();
+    const int piv = sh_piv;
+    const double d = sh_d;
+    if (!(d > 0.0) || piv >= m) break;                       // uniform
+    for (int l = tid; l < k; l += K4_THREADS) rp[l] = __ldcg(Rg + (long long)l * m + piv);
+    __syncthreads();
+    const double rkk = sqrt(d), irk = 1.0 / rkk;
+    for (int j = tid; j < m; j += K4_THREADS) {
+      double v = 0.0;
+      if (j == piv) {
+        v = rkk;
+        used[j] = 1;                                         // only this thread reads used[piv] now
+      } else if (!used[j]) {
+        double sacc = __ldcg(Ag + (long long)piv * m + j);   // Sw[j][piv]
+        for (int l = 0; l < k; ++l) sacc = fma(-rp[l], __ldcg(Rg + (long long)l * m + j), sacc);
+        v = sacc * irk;
+        dg[j] -= v * v;
+      }
+      Rg[(long long)k * m + j] = v;
+    }
+    __syncthreads();
+  }
+  for (long long e = (long long)k * m + tid; e < (long long)m * m; e += K4_THREADS) Rg[e] = 0.0;
+  return k;
+}
+
 // CL = CTAs per cluster: 4 (the cluster path above), or 1 for windows up to K4_SOLO_M: the whole
 // K4a on one SM (Jacobi with S in shared memory, Ã, Hessenberg and the Aberth iteration on one
 // CTA) — about half the SM-cycles of the 4-CTA cluster per frame at m = 100-128, at a longer
@@ -1424,6 +1535,8 @@ k4a_kernel(const K4Params p) {
   // columns are still V·Λ).  Q0 = the previous frame's eigenvectors with rows shifted by the k
   // frames the window moved (Q0[i][j] = V_prev[(i + k) mod m][j]), which leaves far fewer
   // rotations to do than Q0 = I.
+  __shared__ int sh_chol_full;                // CTA 0: the Cholesky start ran all m steps
+  if (tid == 0) sh_chol_full = 1;
   {
     __shared__ int sh_warm;
     if (tid == 0) {
@@ -1431,7 +1544,51 @@ k4a_kernel(const K4Params p) {
       sh_warm = (p.Vprev != nullptr && rp != nullptr && p.warm_k > 0 && rp->vframe == f - p.warm_k) ? 1 : 0;
     }
     __syncthreads();
-    if (sh_warm) {                              // uniform across the cluster (same inputs)
+    if (p.chol) {
+      // ---- Cholesky-preconditioned start (Veselić–Hari): S = Q0 Sw Q0ᵀ with Sw = Q0ᵀ S Q0, and
+      // Sw = RᵀR by pivoted Cholesky, so S = A Aᵀ for A = Q0 Rᵀ; one-sided Jacobi on A then gives
+      // A J = U Σ with U the eigenvectors of S and Σ² its eigenvalues (σ = column norms).  The rows
+      // of a pivoted Cholesky factor are graded, and with the warm Q0 the Jacobi needs ~7 sweeps
+      // where S·Q0 needed 9–21 (C4, C5; profiles/r2 …).  Q0 = the previous frame's eigenvectors of
+      // this stream with rows shifted by the window move (as below), or I.
+      const int wk = sh_warm ? p.warm_k : 0;
+      const double* Vp = p.Vprev;
+      double* t0 = reinterpret_cast<double*>(k4_smem);
+      const int mb = (m + K4_CLUSTER - 1) / K4_CLUSTER;
+      const int i0 = crank * mb, ni = max(0, min(m, i0 + mb) - i0);
+      if (sh_warm) {
+        // B = S·Q0, then Sw = Q0ᵀ·B into A (rows of each split over the cluster, 64-row chunks)
+        for (int s0 = 0; s0 < ni; s0 += 64)
+          k4_gemm_rows(m, m, i0 + s0, min(64, ni - s0), tid, t0,
+                       [&](int i, int k) { return __ldcg(p.A + (long long)k * m + i); },
+                       [&](int k, int j) { return __ldcg(Vp + (long long)j * m + (k + wk) % m); },
+                       [&](int i, int j, double v) { p.B[(long long)j * m + i] = v; });
+        cl_sync();
+        for (int s0 = 0; s0 < ni; s0 += 64)
+          k4_gemm_rows(m, m, i0 + s0, min(64, ni - s0), tid, t0,
+                       [&](int i, int k) { return __ldcg(Vp + (long long)i * m + (k + wk) % m); },
+                       [&](int k, int j) { return __ldcg(p.B + (long long)j * m + k); },
+                       [&](int i, int j, double v) { p.A[(long long)j * m + i] = v; });
+        cl_sync();
+      }
+      // (a breakdown before step m leaves zero columns in A, hence zero columns of V beyond the
+      // numerical rank: such a V is not orthogonal, so it must not seed a later warm start)
+      if (crank == 0) {
+        const int ks = k4_pchol(p.A, p.B, m, tid, warp, lane);   // R rows -> columns of B
+        if (tid == 0) sh_chol_full = ks == m ? 1 : 0;
+      }
+      cl_sync();
+      if (sh_warm) {                                         // A = Q0·Rᵀ
+        for (int s0 = 0; s0 < ni; s0 += 64)
+          k4_gemm_rows(m, m, i0 + s0, min(64, ni - s0), tid, t0,
+                       [&](int i, int k) { return __ldcg(Vp + (long long)k * m + (i + wk) % m); },
+                       [&](int k, int j) { return __ldcg(p.B + (long long)j * m + k); },
+                       [&](int i, int j, double v) { p.A[(long long)j * m + i] = v; });
+      } else {
+        for (int e = crank * K4_THREADS + tid; e < m * m; e += K4_GT) p.A[e] = __ldcg(p.B + e);
+      }
+      cl_sync();
+    } else if (sh_warm) {                       // uniform across the cluster (same inputs)
       const int cb = (m + K4_CLUSTER - 1) / K4_CLUSTER;
       const int j0 = crank * cb, j1 = min(m, j0 + cb);
       const int nj = j1 > j0 ? j1 - j0 : 0;
@@ -1661,7 +1818,7 @@ k4a_kernel(const K4Params p) {
     double s = 0.0;
     for (int i = lane; i < m; i += 32) { const double v = __ldcg(cj + i); s = fma(v, v, s); }
     s = wsum(s);
-    if (lane == 0) p.mu[j] = sqrt(s);
+    if (lane == 0) p.mu[j] = p.chol ? s : sqrt(s);             // μ = σ² in both starts
   }
   cl_sync();
   for (int j = tid; j < m; j += K4_THREADS) mu[j] = __ldcg(p.mu + j);
@@ -1701,7 +1858,8 @@ k4a_kernel(const K4Params p) {
   }
   for (int i = gwarp; i < m; i += K4_GW) {
     const int src = perm[i];
-    const double inv = mu[src] > 0.0 ? 1.0 / mu[src] : 0.0;
+    // ‖a_j‖ = σ_j (Cholesky start) or |μ_j| = σ_j² (S·Q0 start)
+    const double inv = mu[src] > 0.0 ? (p.chol ? 1.0 / sqrt(mu[src]) : 1.0 / mu[src]) : 0.0;
     const double* cj = p.A + (long long)src * m;
     double v[EL];
     double best = -1.0;
@@ -1993,7 +2151,7 @@ k4a_kernel(const K4Params p) {
     ph[6] = clock64();
     res->frame = f; res->status = (sh_status == 0 && qr_st) ? 5 : sh_status; res->r = r; res->idx = -1;
     res->sweeps = sweeps; res->sigma1 = sig[0]; res->nkeep = r; res->nB = 0;
-    res->vframe = converged ? f : -1;            // V usable as the next warm start
+    res->vframe = (converged && sh_chol_full) ? f : -1;   // V usable as the next warm start
     for (int q = 0; q < 6; ++q) res->phase[q] = ph[q + 1] - ph[q];
     res->commit_wait = t_wait0;
     res->phase[6] = 0;
@@ -2303,7 +2461,8 @@ size_t k4_smem_bytes(int r_max, int m, int bg_modes, int cl) {
   const size_t d = ((size_t)((r_max + cl - 1) / cl) * r_max + (3 + cl) * kMaxR) * sizeof(double);  // Hessenberg rows + exchange
   // Ã tiles (K4a a7): 32 x (ceil(max(m, r)/4) + r) doubles
   const int rows2 = ((m > r_max ? m : r_max) + cl - 1) / cl;
-  const size_t d2 = (size_t)32 * ((rows2 < 64 ? rows2 : 64) + r_max) * sizeof(double);
+  const int cols2 = m <= kMaxR && m > r_max ? m : r_max;            // Cholesky-start GEMMs: N = m
+  const size_t d2 = (size_t)32 * (64 + cols2) * sizeof(double);
   // multi-mode background: per-mode inverse-iteration scratch (one warp each) + coefficient parts
   const size_t b3 = 3 * (size_t)kMaxR * sizeof(double2) + (size_t)kMaxR * sizeof(int);   // per mode
   const size_t e = bg_modes > 1 ? (size_t)(bg_modes + 1) * (b3 + (size_t)m * sizeof(double2)) : 0;

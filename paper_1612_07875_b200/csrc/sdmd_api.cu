@@ -123,6 +123,7 @@ struct sdmd_ctx {
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
   int k1b_grid = 148;                   // CTAs of the batched Gram pass (K1b)
   int k4cl = 4;                         // CTAs per K4a launch (k4_cluster_size(m))
+  int k4chol = 0;                       // Cholesky-preconditioned Jacobi start (SDMD_K4_CHOL=1)
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
   int atilde_v1 = 0;                    // SDMD_ATILDE=v1 selects the untiled Ã stage of K4a (A/B)
@@ -508,11 +509,10 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   if (c->Wa < 1) c->Wa = 1;
   // r <= m/4 (e.g. C2: m = 150, r = 21): the single-CTA stage (QR of Ã) is light and the cluster
   // stage (Jacobi of the m x m S) bounds the throughput: give it every remaining hardware queue
-  // (measured C2: W = 14 with 16 cluster streams 5455 vs W = 20 with 10 cluster streams 3486
-  // snapshots/s, profiles/r2j…)
+  // (measured C2, W = 14: 24 cluster streams 8,513 vs 16 streams 5,888 snapshots/s with the Gram
+  // pass persistent on the 49 SMs left, profiles/r2/c2…)
   if (4 * rmax <= c->cfg.m) {
-    int wa = 30 - c->W;
-    if (wa > 2 * c->W) wa = 2 * c->W;
+    int wa = 29 - c->Wb;
     if (wa > kMaxWorkers) wa = kMaxWorkers;
     if (wa > c->Wa) c->Wa = wa;
   }
@@ -571,14 +571,16 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     // waves == 0 (default): a persistent grid on the SMs the eigen workers leave free (one
     // cluster of k4_cluster_size() CTAs per cluster stream, one CTA per single-CTA stream), so K4
     // never waits for an SM and K1 has no wave tail (measured at C4: 3.71 vs 3.76 ms per pass,
-    // profiles/r1p…); waves > 0 (SDMD_K1_WAVES): waves x nsm short-lived CTAs that K4 CTAs slip
-    // between.  Falls back to 8 waves if the workers would leave fewer than half of the SMs.
+    // profiles/r1p…; C2 with 24 clusters: 0.044 ms on 49 SMs vs 0.111 ms in waves); waves > 0
+    // (SDMD_K1_WAVES): waves x nsm short-lived CTAs that K4 CTAs slip between.  Falls back to
+    // 8 waves only if the workers would leave fewer than 16 SMs.
     int waves = 0;
-    if (const char* ew = std::getenv("SDMD_K1_WAVES")) waves = std::atoi(ew);
+    if (const char* ew = std::getenv("SDMD_K1_WAVES")) waves = std::atoi(ew);   // < 0: persistent always
+    const bool force_persistent = waves < 0;
     if (waves < 0) waves = 0;
     if (waves > kK1MaxWaves) waves = kK1MaxWaves;
     const int free_sms = c->nsm - c->Wa * c->k4cl - c->Wb;
-    if (waves == 0 && free_sms < c->nsm / 2) waves = 8;
+    if (waves == 0 && !force_persistent && free_sms < 16) waves = 8;
     c->k1_grid = !c->cfg.dmd ? c->nsm : waves > 0 ? c->nsm * waves : free_sms;
   }
   {
@@ -586,6 +588,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->k1_v1 = (ev && std::strcmp(ev, "v1") == 0) ? 1 : 0;
     const char* ea1 = std::getenv("SDMD_ATILDE");
     c->atilde_v1 = (ea1 && std::strcmp(ea1, "v1") == 0) ? 1 : 0;
+    const char* ech = std::getenv("SDMD_K4_CHOL");
+    c->k4chol = (ech && ech[0] == '1') ? 1 : 0;
     const char* ed = std::getenv("SDMD_K1_DBG");
     c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* ew = std::getenv("SDMD_WARM");
@@ -857,6 +861,7 @@ static K4Params k4_params(sdmd_ctx* c, long long f) {
   p.flags = k.flags; p.mu = k.mu; p.wv = k.wv; p.uv = k.uv;
   p.bg_modes = c->cfg.bg_modes;
   p.atilde_v1 = c->atilde_v1;
+  p.chol = (c->k4chol && p.m <= kMaxR) ? 1 : 0;
   // Jacobi warm start from the previous frame of the same cluster stream (frame f - Wa·P)
   const long long fp = f - (long long)c->Wa * c->P;
   // (only while the two windows overlap: Wa·P < m)

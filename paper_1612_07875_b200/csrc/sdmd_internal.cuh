@@ -200,6 +200,7 @@ struct K4Params {
   double2* lam_warm;          // kMaxR
   int* r_warm;                // its r (0: none yet)
   int atilde_v1;              // SDMD_ATILDE=v1: the untiled Ã stage (A/B only)
+  int chol;                   // Jacobi on Q0·Rᵀ (pivoted Cholesky of Q0ᵀSQ0) instead of S·Q0 (m <= kMaxR)
 };
 
 // per-eigenvalue on-demand eigenvectors (right W[:, j], left, amplitude b_j)

@@ -14,7 +14,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 import bench_configs as B  # noqa: E402
 
-KNOBS = ("SDMD_WA", "SDMD_WB", "SDMD_K4_CL", "SDMD_JACQ")
+KNOBS = ("SDMD_WA", "SDMD_WB", "SDMD_K4_CL", "SDMD_K1_WAVES")
 
 
 def with_env(env, f):
@@ -42,12 +42,10 @@ which = args or ["C2", "C3", "C5"]
 K = 400
 # (W, SDMD_WA, SDMD_WB, extra env)
 RUNS = {   # (W, SDMD_WA, SDMD_WB, env, background lag (C3; 0 = library default))
-    "C5": [(16, 16, 4, {"SDMD_K4_CL": 4}, 0), (16, 20, 4, {"SDMD_K4_CL": 4}, 0),
-           (16, 24, 4, {"SDMD_K4_CL": 4}, 0), (20, 24, 5, {"SDMD_K4_CL": 4}, 0)],
-    "C3": [(16, 0, 0, {"SDMD_K4_CL": 4}, 12), (16, 0, 0, {"SDMD_K4_CL": 4}, 20),
-           (12, 0, 0, {"SDMD_K4_CL": 4}, 12), (20, 0, 0, {"SDMD_K4_CL": 4}, 12),
-           (16, 20, 4, {}, 12), (16, 20, 4, {}, 20)],
-    "C2": [(14, 0, 0, {}, 0)],
+    "C5": [(16, 0, 0, {}, 0)],
+    "C3": [(16, 0, 0, {}, 0)],
+    "C2": [(14, 0, 0, {}, 0), (14, 20, 3, {"SDMD_K1_WAVES": -1}, 0), (14, 24, 3, {"SDMD_K1_WAVES": -1}, 0),
+           (14, 24, 5, {"SDMD_K1_WAVES": -1}, 0), (14, 24, 3, {}, 0), (8, 16, 2, {}, 0)],
 }
 
 
