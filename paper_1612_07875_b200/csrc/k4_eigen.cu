@@ -1430,19 +1430,85 @@ static __device__ __forceinline__ void k4_gemm_rows(int K, int N, int i0, int ni
     }
 }
 
+constexpr int K4_CHOL_SMEM_M = 157;                    // R (m² fp64) in shared memory up to this m
+
 // Pivoted Cholesky (largest remaining diagonal first, lowest index on ties) of the symmetric
-// positive semidefinite Sw (column-major m x m in Ag), left-looking, rows kept in the ORIGINAL
-// column order: step k writes R[k][j] to Rg[k*m + j], so that RᵀR = Sw without a permutation.
-// Stops at the first non-positive pivot (the numerical null space); the remaining rows are zero.
-// One CTA; returns the number of steps taken.
-static __device__ __noinline__ int k4_pchol(const double* Ag, double* Rg, int m, int tid, int warp, int lane) {
+// positive semidefinite Sw (column-major m x m in Ag), rows kept in the ORIGINAL column order:
+// step k writes R[k][j] to Rg[k*m + j], so that RᵀR = Sw without a permutation.  Stops at the
+// first non-positive pivot (the numerical null space); the remaining rows are zero.  One CTA;
+// returns the number of steps taken.
+//  - Ts != nullptr (m <= K4_CHOL_SMEM_M): the rows of R (and Sw itself for m <= 110) in shared
+//    memory: per step one warp picks the pivot, then each unused column forms its entry of row k
+//    from the k previous rows — two barriers and no L2 round trip per step (a right-looking rank-1
+//    update of the Schur complement in shared memory measured slower: smem-bandwidth bound);
+//  - else the same from L2 (row k from Sw and the previous rows, four loads in flight).
+static __device__ __noinline__ int k4_pchol(const double* Ag, double* Rg, int m, int tid, int warp, int lane,
+                                            double* Ts) {
   __shared__ double dg[kMaxM];
-  __shared__ double rp[kMaxM];                               // R[0..k-1][piv] of the current step
+  __shared__ double rp[kMaxM];                               // R[0..k-1][piv] (left-looking) / row k (right-looking)
   __shared__ unsigned char used[kMaxM];
   __shared__ double wb[K4_WARPS];
   __shared__ int wi[K4_WARPS];
   __shared__ int sh_piv;
   __shared__ double sh_d;
+  if (Ts) {
+    // left-looking with R (and, for m <= 110, Sw) in shared memory: per step warp 0 picks the pivot
+    // from the running diagonal, then every unused column j forms R[k][j] from k shared-memory rows
+    // (four partial sums) — two barriers per step
+    const bool sw_s = m <= 110;
+    double* Ss = Ts + (size_t)m * m;                         // Sw copy (sw_s)
+    for (int j = tid; j < m; j += K4_THREADS) { dg[j] = __ldcg(Ag + (long long)j * m + j); used[j] = 0; }
+    if (sw_s)
+      for (int e = tid; e < m * m; e += K4_THREADS) Ss[e] = __ldcg(Ag + e);
+    __syncthreads();
+    int k = 0;
+    for (; k < m; ++k) {
+      if (warp == 0) {
+        double b = -INFINITY;
+        int bi = m;
+        for (int j = lane; j < m; j += 32)
+          if (!used[j] && dg[j] > b) { b = dg[j]; bi = j; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > b || (ob == b && oi < bi)) { b = ob; bi = oi; }
+        }
+        if (lane == 0) { sh_piv = bi; sh_d = b; }
+      }
+      __syncthreads();
+      const int piv = sh_piv;
+      const double d = sh_d;
+      if (!(d > 0.0) || piv >= m) break;                     // uniform
+      const double rkk = sqrt(d), irk = 1.0 / rkk;
+      for (int j = tid; j < m; j += K4_THREADS) {
+        double v = 0.0;
+        if (j == piv) {
+          v = rkk;
+          used[j] = 1;                                       // only this thread reads used[piv] now
+        } else if (!used[j]) {
+          double sacc = sw_s ? Ss[piv * m + j] : __ldcg(Ag + (long long)piv * m + j);   // Sw[j][piv]
+          double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          int l = 0;
+          for (; l + 4 <= k; l += 4) {
+            sacc = fma(-Ts[l * m + piv], Ts[l * m + j], sacc);
+            s1 = fma(-Ts[(l + 1) * m + piv], Ts[(l + 1) * m + j], s1);
+            s2 = fma(-Ts[(l + 2) * m + piv], Ts[(l + 2) * m + j], s2);
+            s3 = fma(-Ts[(l + 3) * m + piv], Ts[(l + 3) * m + j], s3);
+          }
+          for (; l < k; ++l) sacc = fma(-Ts[l * m + piv], Ts[l * m + j], sacc);
+          sacc += (s1 + s2) + s3;
+          v = sacc * irk;
+          dg[j] -= v * v;
+        }
+        Ts[k * m + j] = v;
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < k * m; e += K4_THREADS) Rg[e] = Ts[e];
+    for (long long e = (long long)k * m + tid; e < (long long)m * m; e += K4_THREADS) Rg[e] = 0.0;
+    return k;
+  }
   for (int j = tid; j < m; j += K4_THREADS) { dg[j] = __ldcg(Ag + (long long)j * m + j); used[j] = 0; }
   __syncthreads();
   int k = 0;
@@ -1481,7 +1547,18 @@ static __device__ __noinline__ int k4_pchol(const double* Ag, double* Rg, int m,
         used[j] = 1;                                         // only this thread reads used[piv] now
       } else if (!used[j]) {
         double sacc = __ldcg(Ag + (long long)piv * m + j);   // Sw[j][piv]
-        for (int l = 0; l < k; ++l) sacc = fma(-rp[l], __ldcg(Rg + (long long)l * m + j), sacc);
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;                 // four loads in flight per step
+        int l = 0;
+        for (; l + 4 <= k; l += 4) {
+          const double r0 = __ldcg(Rg + (long long)l * m + j), r1 = __ldcg(Rg + (long long)(l + 1) * m + j);
+          const double r2 = __ldcg(Rg + (long long)(l + 2) * m + j), r3 = __ldcg(Rg + (long long)(l + 3) * m + j);
+          sacc = fma(-rp[l], r0, sacc);
+          s1 = fma(-rp[l + 1], r1, s1);
+          s2 = fma(-rp[l + 2], r2, s2);
+          s3 = fma(-rp[l + 3], r3, s3);
+        }
+        for (; l < k; ++l) sacc = fma(-rp[l], __ldcg(Rg + (long long)l * m + j), sacc);
+        sacc += (s1 + s2) + s3;
         v = sacc * irk;
         dg[j] -= v * v;
       }
@@ -1536,7 +1613,8 @@ k4a_kernel(const K4Params p) {
   // frames the window moved (Q0[i][j] = V_prev[(i + k) mod m][j]), which leaves far fewer
   // rotations to do than Q0 = I.
   __shared__ int sh_chol_full;                // CTA 0: the Cholesky start ran all m steps
-  if (tid == 0) sh_chol_full = 1;
+  __shared__ long long ch_cyc[2];             // CTA 0: Cholesky start/end (diagnostics)
+  if (tid == 0) { sh_chol_full = 1; ch_cyc[0] = ch_cyc[1] = 0; }
   {
     __shared__ int sh_warm;
     if (tid == 0) {
@@ -1573,11 +1651,14 @@ k4a_kernel(const K4Params p) {
       }
       // (a breakdown before step m leaves zero columns in A, hence zero columns of V beyond the
       // numerical rank: such a V is not orthogonal, so it must not seed a later warm start)
+      if (tid == 0) ch_cyc[0] = clock64();
       if (crank == 0) {
-        const int ks = k4_pchol(p.A, p.B, m, tid, warp, lane);   // R rows -> columns of B
+        const int ks = k4_pchol(p.A, p.B, m, tid, warp, lane,   // R rows -> columns of B
+                                m <= K4_CHOL_SMEM_M ? reinterpret_cast<double*>(k4_smem) : nullptr);
         if (tid == 0) sh_chol_full = ks == m ? 1 : 0;
       }
       cl_sync();
+      if (tid == 0) ch_cyc[1] = clock64();
       if (sh_warm) {                                         // A = Q0·Rᵀ
         for (int s0 = 0; s0 < ni; s0 += 64)
           k4_gemm_rows(m, m, i0 + s0, min(64, ni - s0), tid, t0,
@@ -2129,7 +2210,8 @@ k4a_kernel(const K4Params p) {
       res->qr_its = 0;
       res->qr_cnt[0] = res->qr_cnt[1] = res->qr_cnt[2] = res->qr_cnt[3] = 0;
       res->phase[7] = 0;
-      res->qr_dbg[0] = res->qr_dbg[1] = 0;
+      res->qr_dbg[0] = ch_cyc[1] - ch_cyc[0];    // (Aberth path) diagnostics: pivoted-Cholesky cycles
+      res->qr_dbg[1] = 0;
     }
     __syncthreads();
     for (int k = tid; k < r; k += K4_THREADS) {
@@ -2481,7 +2563,11 @@ void preload_k4_kernels() {
 }
 
 cudaError_t launch_k4a(const K4Params& p, cudaStream_t s, int cl) {
-  const size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes, cl);
+  size_t smem = k4_smem_bytes(p.r_max, p.m, p.bg_modes, cl);
+  if (p.chol && p.m <= K4_CHOL_SMEM_M) {                     // the Cholesky factor (and Sw) in shared memory
+    const size_t need = (size_t)p.m * p.m * sizeof(double) * (p.m <= 110 ? 2 : 1);
+    if (smem < need) smem = need;
+  }
   const void* fn = cl == 1 ? (const void*)k4a_kernel<1> : (const void*)k4a_kernel<K4_CLUSTER>;
   cudaError_t e = set_max_dyn_smem(fn, (int)smem);
   if (e != cudaSuccess) return e;

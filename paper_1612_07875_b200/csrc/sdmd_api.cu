@@ -123,7 +123,7 @@ struct sdmd_ctx {
   int W = 4, L = 5, NS = 0, NH = 0, NC = 0, nsm = 148, k1_grid = 148, pgrid = 148, k1_dbg = 0;
   int k1b_grid = 148;                   // CTAs of the batched Gram pass (K1b)
   int k4cl = 4;                         // CTAs per K4a launch (k4_cluster_size(m))
-  int k4chol = 0;                       // Cholesky-preconditioned Jacobi start (SDMD_K4_CHOL=1)
+  int k4chol = 1;                       // Cholesky-preconditioned Jacobi start (SDMD_K4_CHOL=0: off)
   bool bg_nodmd = false;                // SDMD_BG_NODMD=1: background pass with c = 0 (benchmarks)
   int k1_v1 = 0;                        // SDMD_K1=v1 selects the v1 K1 (A/B)
   int atilde_v1 = 0;                    // SDMD_ATILDE=v1 selects the untiled Ã stage of K4a (A/B)
@@ -588,8 +588,8 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
     c->k1_v1 = (ev && std::strcmp(ev, "v1") == 0) ? 1 : 0;
     const char* ea1 = std::getenv("SDMD_ATILDE");
     c->atilde_v1 = (ea1 && std::strcmp(ea1, "v1") == 0) ? 1 : 0;
-    const char* ech = std::getenv("SDMD_K4_CHOL");
-    c->k4chol = (ech && ech[0] == '1') ? 1 : 0;
+    const char* ech = std::getenv("SDMD_K4_CHOL");          // 0: the S·Q0 Jacobi start (A/B)
+    c->k4chol = (ech && ech[0] == '0') ? 0 : 1;
     const char* ed = std::getenv("SDMD_K1_DBG");
     c->k1_dbg = ed ? std::atoi(ed) : 0;
     const char* ew = std::getenv("SDMD_WARM");

@@ -1103,15 +1103,17 @@ def test_noisy_video_full_rank_spectrum(m):
     eng.close()
 
 
-@pytest.mark.parametrize("m", [65, 128])
-@pytest.mark.parametrize("cl", ["1", "4"])
-def test_k4a_one_cta_and_cluster_vs_oracle(m, cl, monkeypatch):
+@pytest.mark.parametrize("m,cl,chol", [(65, "1", "1"), (128, "1", "1"), (65, "4", "1"), (128, "4", "1"),
+                                        (128, "1", "0"), (128, "4", "0")])
+def test_k4a_one_cta_and_cluster_vs_oracle(m, cl, chol, monkeypatch):
     """K4a on one CTA (the default for dense 64 < m <= 128: whole S in shared memory, Ã in 64-row
-    chunks, one-CTA Hessenberg and Aberth) and on the 4-CTA cluster (SDMD_K4_CL=4, read at create)
+    chunks, one-CTA Hessenberg and Aberth) and on the 4-CTA cluster (SDMD_K4_CL=4, read at create),
+    with the Cholesky-preconditioned Jacobi start (default) and the S·Q0 start (SDMD_K4_CHOL=0),
     give the oracle's SVD and spectrum on a noisy full-rank video window at both ends of the
     one-CTA range, every window of the stream (warm starts included), and the same fused
     background: σ 1e-10 relative (σ/σ1 >= 1e-4), λ_idx 1e-9, all λ 1e-7 (assignment), lowrank 1e-4."""
     monkeypatch.setenv("SDMD_K4_CL", cl)
+    monkeypatch.setenv("SDMD_K4_CHOL", chol)
     vs = synth.video_config("C3s")
     T = m + 12
     frames = vs.frames(0, T).numpy()
