@@ -1613,8 +1613,9 @@ k4a_kernel(const K4Params p) {
   // frames the window moved (Q0[i][j] = V_prev[(i + k) mod m][j]), which leaves far fewer
   // rotations to do than Q0 = I.
   __shared__ int sh_chol_full;                // CTA 0: the Cholesky start ran all m steps
+  __shared__ int sh_nc;                       // CTA 0: columns of A that can be nonzero (Cholesky steps)
   __shared__ long long ch_cyc[2];             // CTA 0: Cholesky start/end (diagnostics)
-  if (tid == 0) { sh_chol_full = 1; ch_cyc[0] = ch_cyc[1] = 0; }
+  if (tid == 0) { sh_chol_full = 1; sh_nc = m; ch_cyc[0] = ch_cyc[1] = 0; }
   {
     __shared__ int sh_warm;
     if (tid == 0) {
@@ -1655,7 +1656,7 @@ k4a_kernel(const K4Params p) {
       if (crank == 0) {
         const int ks = k4_pchol(p.A, p.B, m, tid, warp, lane,   // R rows -> columns of B
                                 m <= K4_CHOL_SMEM_M ? reinterpret_cast<double*>(k4_smem) : nullptr);
-        if (tid == 0) sh_chol_full = ks == m ? 1 : 0;
+        if (tid == 0) { sh_chol_full = ks == m ? 1 : 0; sh_nc = ks; }
       }
       cl_sync();
       if (tid == 0) ch_cyc[1] = clock64();
@@ -1693,6 +1694,18 @@ k4a_kernel(const K4Params p) {
     }
   }
   if (tid == 0) ph[1] = clock64();
+  // the columns of A past the Cholesky steps are zero and never rotate: the Jacobi tournament runs
+  // over the first nc columns only (rank-deficient windows: C2's rank-21 S breaks down after ~31
+  // steps, so 31 instead of 150 columns).  nc is CTA 0's (read over DSMEM: uniform).
+  int nc = m;
+  if (p.chol) {
+    cl_sync();
+    unsigned a = (unsigned)__cvta_generic_to_shared(&sh_nc), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(ra) : "r"(a));
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(nc) : "r"(ra) : "memory");
+    cl_sync();
+    nc = nc < 2 ? (m < 2 ? m : 2) : nc;
+  }
 
   // ---- a5 (small windows, m <= K4_SMALL_M): the whole S fits one CTA's shared memory, so CTA 0
   // runs the cyclic one-sided Jacobi alone (round-robin tournament of the m columns, one column
@@ -1703,9 +1716,9 @@ k4a_kernel(const K4Params p) {
   bool converged = false;
   if (CL == 1 || m <= K4_SMALL_M) {
     if (crank == 0) {
-      const int mp = (m + 1) & ~1;
+      const int mp = (nc + 1) & ~1;                         // tournament over the nc live columns
       double* sA = reinterpret_cast<double*>(k4_smem);       // mp columns x m, column-major
-      for (int e = tid; e < mp * m; e += K4_THREADS) sA[e] = e < m * m ? __ldcg(p.A + e) : 0.0;
+      for (int e = tid; e < mp * m; e += K4_THREADS) sA[e] = e < nc * m ? __ldcg(p.A + e) : 0.0;
       __syncthreads();
       const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
       const int hw = warp * 2 + (lane >> 4), hl = lane & 15;
@@ -1723,7 +1736,7 @@ k4a_kernel(const K4Params p) {
             if (pp < np) {
               P = rr_player(pp, st, mp);
               Q = rr_player(mp - 1 - pp, st, mp);
-              act = P < m && Q < m;
+              act = P < nc && Q < nc;
             }
             bool r_;
             switch (eh) {
@@ -1738,7 +1751,7 @@ k4a_kernel(const K4Params p) {
         ++sweeps;
         if (!__syncthreads_or(rot)) { converged = true; break; }
       }
-      for (int e = tid; e < m * m; e += K4_THREADS) p.A[e] = sA[e];
+      for (int e = tid; e < nc * m; e += K4_THREADS) p.A[e] = sA[e];   // (columns >= nc stay zero)
       if (tid == 0) { p.flags[0] = converged ? 1 : 0; p.flags[1] = sweeps; }
     }
     cl_sync();
@@ -1755,7 +1768,7 @@ k4a_kernel(const K4Params p) {
   // its next pair out of the previous round's owners' buffers over DSMEM — no L2/HBM round trip
   // per round (the Gram pass streams at full HBM bandwidth meanwhile) and still one cluster
   // barrier per round (a CTA only overwrites the buffer the others read one round earlier).
-  const int bs = (m + 7) / 8;                     // block size (columns)
+  const int bs = (nc + 7) / 8;                    // block size (columns; the nc live ones)
   __shared__ volatile int jdone[32];
   const int ehs = m <= 64 ? 4 : m <= 112 ? 7 : m <= 160 ? 10 : m <= 208 ? 13 : kMaxM / 16;
   const double tol = fmax(1e-15, (double)m * DBL_EPSILON);
@@ -1794,7 +1807,7 @@ k4a_kernel(const K4Params p) {
         for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {     // warp per column: no divisions
           const int gc = gcol(lc);
           double* dst = sA + lc * m;
-          if (gc < m) {
+          if (gc < nc) {
             const double* src = p.A + (long long)gc * m;
             for (int i = lane; i < m; i += 32) dst[i] = __ldcg(src + i);
           } else {
@@ -1818,7 +1831,7 @@ k4a_kernel(const K4Params p) {
               __threadfence_block();
             }
             const int hs = hw + st, P = hw, Q = bs + (hs >= bs ? hs - bs : hs);
-            const bool act = gcol(P) < m && gcol(Q) < m;
+            const bool act = gcol(P) < nc && gcol(Q) < nc;
             bool r_;
             switch (ehs) {
               case 4: r_ = jacobi_pair<4>(sA + P * m, sA + Q * m, m, hl, act, tol, hmask); break;
@@ -1843,7 +1856,7 @@ k4a_kernel(const K4Params p) {
           if (hw < bs) {
             if (rd == 0) { P = rr_player(hw, st, 2 * bs); Q = rr_player(2 * bs - 1 - hw, st, 2 * bs); }
             else { const int hs = hw + st; P = hw; Q = bs + (hs >= bs ? hs - bs : hs); }   // hw, st < bs
-            act = gcol(P) < m && gcol(Q) < m;
+            act = gcol(P) < nc && gcol(Q) < nc;
           }
           bool r_;
           switch (ehs) {                                    // per-lane rows: ceil(m / 16)
@@ -1860,7 +1873,7 @@ k4a_kernel(const K4Params p) {
       if (!dsm) {
         for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
           const int gc = gcol(lc);
-          if (gc < m) {
+          if (gc < nc) {
             const double* src = sA + lc * m;
             double* dst = p.A + (long long)gc * m;
             for (int i = lane; i < m; i += 32) dst[i] = src[i];
@@ -1882,7 +1895,7 @@ k4a_kernel(const K4Params p) {
     const int PB = rr_player(crank, rd, 8), QB = rr_player(7 - crank, rd, 8);
     for (int lc = warp; lc < 2 * bs; lc += K4_WARPS) {
       const int gc = lc < bs ? PB * bs + lc : QB * bs + (lc - bs);
-      if (gc < m) {
+      if (gc < nc) {
         const double* src = sA + (size_t)lc * m;
         double* dst = p.A + (long long)gc * m;
         for (int i = lane; i < m; i += 32) dst[i] = src[i];

@@ -42,10 +42,9 @@ which = args or ["C2", "C3", "C5"]
 K = 400
 # (W, SDMD_WA, SDMD_WB, extra env)
 RUNS = {   # (W, SDMD_WA, SDMD_WB, env, background lag (C3; 0 = library default))
-    "C5": [(16, 0, 0, {}, 0)],
+    "C5": [(16, 0, 0, {}, 0), (16, 24, 2, {}, 0)],
     "C3": [(16, 0, 0, {}, 0)],
-    "C2": [(14, 0, 0, {}, 0), (14, 20, 3, {"SDMD_K1_WAVES": -1}, 0), (14, 24, 3, {"SDMD_K1_WAVES": -1}, 0),
-           (14, 24, 5, {"SDMD_K1_WAVES": -1}, 0), (14, 24, 3, {}, 0), (8, 16, 2, {}, 0)],
+    "C2": [(14, 0, 0, {}, 0), (14, 24, 5, {}, 0), (14, 20, 3, {}, 0)],
 }
 
 
