@@ -505,14 +505,16 @@ int sdmd_create(const sdmd_config* cfg_in, sdmd_ctx** out) {
   // sparse contexts: the Gram pass needs few SMs and the rate is the number of K4a clusters in
   // flight over their latency, so every hardware queue left (C5 W = 16: 24 + 4 streams, 6,200 vs
   // 4,270 snapshots/s with 16 + 4, profiles/r2/r8…)
-  c->Wa = c->cfg.storage == SDMD_SPARSE ? (c->W >= 8 ? 29 - c->Wb : c->W - c->Wb) : c->W / 2;
+  // (measured at W = 16: 22 + 6 streams 7,693 vs 24 + 4 7,204 snapshots/s, profiles/r2/t2…)
+  if (c->cfg.storage == SDMD_SPARSE && c->W >= 16 && c->Wb < 6) c->Wb = 6;
+  c->Wa = c->cfg.storage == SDMD_SPARSE ? (c->W >= 8 ? 28 - c->Wb : c->W - c->Wb) : c->W / 2;
   if (c->Wa < 1) c->Wa = 1;
   // r <= m/4 (e.g. C2: m = 150, r = 21): the single-CTA stage (QR of Ã) is light and the cluster
-  // stage (Jacobi of the m x m S) bounds the throughput: give it every remaining hardware queue
-  // (measured C2, W = 14: 24 cluster streams 8,513 vs 16 streams 5,888 snapshots/s with the Gram
-  // pass persistent on the 49 SMs left, profiles/r2/c2…)
+  // stage (Jacobi of the m x m S) bounds the throughput: give it most of the remaining hardware
+  // queues (measured C2, W = 14, S·Q0 start: 24 cluster streams 8,513 vs 16 streams 5,888
+  // snapshots/s with the Gram pass persistent on the 49 SMs left, profiles/r2/c2…)
   if (4 * rmax <= c->cfg.m) {
-    int wa = 29 - c->Wb;
+    int wa = 23 - c->Wb;                               // (W = 14: 20 streams 20,118 vs 24 18,313/s)
     if (wa > kMaxWorkers) wa = kMaxWorkers;
     if (wa > c->Wa) c->Wa = wa;
   }
