@@ -214,6 +214,7 @@ struct sdmd_ctx {
   // timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> k1_ev, k4_ev, wait_ev;
+  std::vector<cudaEvent_t> ev_pool;     // recycled timing events
   struct TL { long long f; int kind; cudaEvent_t a, b; };   // timeline view of the events above
   std::vector<TL> tl;
   long long launches = 0;
@@ -263,21 +264,36 @@ static cudaError_t dalloc(T** p, size_t count) {
   return cudaMalloc((void**)p, count * sizeof(T) > 0 ? count * sizeof(T) : 16);
 }
 
-static void destroy_timing(sdmd_ctx* c) {
-  for (auto& pr : c->k1_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
-  for (auto& pr : c->k4_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
-  for (auto& pr : c->wait_ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+// Timing events are recycled through a per-context pool: cudaEventCreate costs microseconds of
+// host time, which a launch-bound config (C1: ≈ 50 µs per push) would otherwise pay ~8 times per
+// frame while it is being measured.  sdmd_set_timing(1) pre-fills the pool.
+static void destroy_timing(sdmd_ctx* c, bool release = false) {
+  for (auto* v : {&c->k1_ev, &c->k4_ev, &c->wait_ev})
+    for (auto& pr : *v) { c->ev_pool.push_back(pr.first); c->ev_pool.push_back(pr.second); }
   c->k1_ev.clear();
   c->k4_ev.clear();
   c->wait_ev.clear();
   c->tl.clear();
+  if (release) {
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    c->ev_pool.clear();
+  }
 }
 
-static std::pair<cudaEvent_t, cudaEvent_t> new_pair() {
-  cudaEvent_t a, b;
-  cudaEventCreate(&a);
-  cudaEventCreate(&b);
-  return {a, b};
+static cudaEvent_t pool_event(sdmd_ctx* c) {
+  if (c->ev_pool.empty()) {
+    cudaEvent_t a;
+    cudaEventCreate(&a);
+    return a;
+  }
+  cudaEvent_t a = c->ev_pool.back();
+  c->ev_pool.pop_back();
+  return a;
+}
+
+static std::pair<cudaEvent_t, cudaEvent_t> new_pair(sdmd_ctx* c) {
+  cudaEvent_t a = pool_event(c);
+  return {a, pool_event(c)};
 }
 
 static int sync_all(sdmd_ctx* c) {
@@ -806,7 +822,7 @@ int sdmd_destroy(sdmd_ctx* c) {
       delete g;
     }
   }
-  destroy_timing(c);
+  destroy_timing(c, true);
   for (int i = 0; i < kEvents; ++i) {
     if (c->ev_commit[i]) cudaEventDestroy(c->ev_commit[i]);
     if (c->ev_done[i]) cudaEventDestroy(c->ev_done[i]);
@@ -894,12 +910,12 @@ static cudaError_t enqueue_k4(sdmd_ctx* c, long long t) {
     if ((e = cudaStreamWaitEvent(A, c->ev_a[(q + c->Wa - c->NWS) % kEvents], 0)) != cudaSuccess) return e;
   const K4Params p = k4_params(c, t);
   std::pair<cudaEvent_t, cudaEvent_t> ka{}, kb{};
-  if (c->timing) { ka = new_pair(); cudaEventRecord(ka.first, A); }
+  if (c->timing) { ka = new_pair(c); cudaEventRecord(ka.first, A); }
   if ((e = launch_k4a(p, A, c->k4cl)) != cudaSuccess) return e;
   if (c->timing) { cudaEventRecord(ka.second, A); c->k4_ev.push_back(ka); c->tl.push_back({t, 1, ka.first, ka.second}); }
   if ((e = cudaEventRecord(c->ev_a[q % kEvents], A)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(B, c->ev_a[q % kEvents], 0)) != cudaSuccess) return e;
-  if (c->timing) { kb = new_pair(); cudaEventRecord(kb.first, B); }
+  if (c->timing) { kb = new_pair(c); cudaEventRecord(kb.first, B); }
   if ((e = launch_k4b(p, B)) != cudaSuccess) return e;
   {                                             // W_SINGULAR frames only (device-side decision)
     const int sw = (int)(q % c->Wb);
@@ -981,7 +997,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
                   (c->bg_nodmd && c->cfg.background && !sparse && (t - c->L) >= m);
   std::pair<cudaEvent_t, cudaEvent_t> tp{}, tw{};
   if (c->timing) {                                // wait_ev: time the ctx stream spends waiting
-    tw = new_pair();                              // for the background coefficients of t - L
+    tw = new_pair(c);                              // for the background coefficients of t - L
     CK(cudaEventRecord(tw.first, c->stream));
   }
   if (c->cfg.dmd && (c->cfg.modes_every_frame || c->throttle) && t - c->L - 2 >= first_dmd(c) &&
@@ -1014,7 +1030,7 @@ static int enqueue_frame(sdmd_ctx* c, long long t) {
     CK(cudaEventRecord(tw.second, c->stream));
     c->wait_ev.push_back(tw);
     c->tl.push_back({t, 3, tw.first, tw.second});
-    tp = new_pair();
+    tp = new_pair(c);
     CK(cudaEventRecord(tp.first, c->stream));
   }
   const int do_commit = c->coll ? 0 : 1;
@@ -1196,7 +1212,7 @@ int sdmd_push_batch(sdmd_ctx* c, int32_t k, const void* X, int64_t ldx, int wher
     j += run;
   }
   std::pair<cudaEvent_t, cudaEvent_t> tp{};
-  if (c->timing) { tp = new_pair(); CK(cudaEventRecord(tp.first, c->stream)); }
+  if (c->timing) { tp = new_pair(c); CK(cudaEventRecord(tp.first, c->stream)); }
   K1bParams p{};
   p.ring = c->ring; p.ld = c->ld; p.NS = c->NS; p.m = m; p.n = c->cfg.n_local; p.f0 = t; p.k = k;
   p.partials = c->partials; p.gout = c->gout; p.do_commit = c->coll ? 0 : 1;
@@ -1713,6 +1729,14 @@ int sdmd_get_frame_diag(sdmd_ctx* c, int64_t out[24]) {
 int sdmd_set_timing(sdmd_ctx* c, int enable) {
   if (!c) return SDMD_E_INVALID;
   c->timing = enable != 0;
+  if (c->timing) {
+    CK(cudaSetDevice(c->dev));
+    while (c->ev_pool.size() < 8192) {                 // ≈ 1000 frames of K1/wait/K4a/K4b pairs
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) break;
+      c->ev_pool.push_back(e);
+    }
+  }
   return SDMD_OK;
 }
 
