@@ -1150,6 +1150,9 @@ int sdmd_push_dense(sdmd_ctx* c, const void* x, int where) {
   const long long t = c->frames;
   if (int g = ring_guard(c, t)) return g;
   char* dst = (char*)c->ring + (size_t)(t % c->NS) * c->ld * c->es;
+  // a small ready frame (< 1 MB, e.g. C1's 32 KB) is copied in ctx-stream order: one call instead
+  // of the copy-stream handshake's four, and its copy time is negligible
+  if (where == SDMD_DEVICE_READY && (size_t)c->cfg.n_local * c->es < ((size_t)1 << 20)) where = SDMD_DEVICE;
   if (where != SDMD_DEVICE) {
     // H2D (or a ready D2D) on the copy stream so it overlaps K1(t-1): slot t mod NS was last read
     // by K1(t-2) at the latest (kRingSpare slots of margin)
