@@ -225,8 +225,9 @@ int sdmd_init_window(sdmd_ctx* ctx, const void* Z, int64_t ldz, int where);
  * including the previous Gram pass), or SDMD_DEVICE_READY: a device buffer whose contents are
  * complete when the call is made (a host-synchronised producer, a static pool); it is copied on
  * the copy stream like a host frame, so the copy overlaps the previous Gram pass instead of
- * sitting between two passes.  In every case x must stay unmodified until the ctx stream passes
- * the push. */
+ * sitting between two passes (frames under 1 MB are copied in ctx-stream order as for
+ * SDMD_DEVICE: one call, negligible copy time).  In every case x must stay unmodified until the
+ * ctx stream passes the push. */
 int sdmd_push_dense(sdmd_ctx* ctx, const void* x, int where);
 
 /* Push one sparse snapshot in an orthonormal coefficient basis (§3.5): nnz pairs,
