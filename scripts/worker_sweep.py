@@ -42,9 +42,9 @@ which = args or ["C2", "C3", "C5"]
 K = 400
 # (W, SDMD_WA, SDMD_WB, extra env)
 RUNS = {   # (W, SDMD_WA, SDMD_WB, env, background lag (C3; 0 = library default))
-    "C5": [(16, 0, 0, {}, 0), (16, 20, 5, {}, 0), (16, 22, 6, {}, 0)],
-    "C3": [(16, 0, 0, {}, 0), (16, 16, 4, {}, 0), (16, 18, 3, {}, 0)],
-    "C2": [(14, 0, 0, {}, 0), (14, 12, 3, {}, 0), (14, 16, 3, {}, 0), (14, 20, 3, {}, 0), (14, 16, 6, {}, 0)],
+    "C5": [(16, 0, 0, {}, 0)],
+    "C3": [(16, 0, 0, {}, 0), (16, 16, 3, {}, 0), (16, 18, 3, {}, 0), (16, 17, 2, {}, 0), (16, 14, 3, {}, 0)],
+    "C2": [(14, 0, 0, {}, 0), (14, 18, 3, {}, 0), (14, 22, 3, {}, 0)],
 }
 
 
